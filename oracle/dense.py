@@ -1,0 +1,104 @@
+"""Dense collocation matrices, assembled entry by entry (Sec. 2.2-2.3, 5.1-5.2, 6.2.1).
+
+Test infrastructure only (see oracle/__init__.py).
+
+Row order: interior collocation rows in natural row-major grid order (x outer),
+then boundary rows in the caller's order.  The paper orders rows like Pi X~
+(PAPER.md:142); the least-squares problem is invariant under a row permutation
+(reading R19 in DESIGN.md), and natural order is what the C ABI exposes.
+Column order: j = j_x n + j_y.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2308_14490_b200 import inputs as I
+from .kernel import periodized
+
+
+def _Phi(points: np.ndarray, centers: np.ndarray, eps: float, T: float, order: int) -> np.ndarray:
+    """Phi[i, j] = phi^per_order(points[i] - centers[j])."""
+    return periodized(points[:, None] - centers[None, :], eps, T, order)
+
+
+def assemble_rows(cfg: I.Config, pts: np.ndarray, kind: str) -> np.ndarray:
+    """Rows of A at `pts` (1-D: (m,), 2-D: (m, 2)).
+
+    kind "value":     phi_j(x)
+    kind "laplacian": alpha (phi_jx'' phi_jy + phi_jx phi_jy'')     (k0^2 = 0)
+    """
+    c = I.center_axis(cfg)
+    eps, T = cfg.eps, cfg.T
+    if cfg.dim == 1:
+        if kind == "value":
+            return _Phi(pts, c, eps, T, 0)
+        return cfg.row_scale * _Phi(pts, c, eps, T, 2)
+    X0 = _Phi(pts[:, 0], c, eps, T, 0)
+    Y0 = _Phi(pts[:, 1], c, eps, T, 0)
+    if kind == "value":
+        # entry (i, jx*n + jy) = phi(x_i - c_jx) phi(y_i - c_jy)
+        return (X0[:, :, None] * Y0[:, None, :]).reshape(pts.shape[0], -1)
+    X2 = _Phi(pts[:, 0], c, eps, T, 2)
+    Y2 = _Phi(pts[:, 1], c, eps, T, 2)
+    L = X2[:, :, None] * Y0[:, None, :] + X0[:, :, None] * Y2[:, None, :]
+    return cfg.row_scale * L.reshape(pts.shape[0], -1)
+
+
+def assemble_A(cfg: I.Config) -> np.ndarray:
+    """A = [A^i ; beta A^b], shape (M + M_b, N)."""
+    kind = "laplacian" if cfg.row_op == I.ROW_LAPLACIAN else "value"
+    Ai = assemble_rows(cfg, I.collocation_points(cfg), kind)
+    if cfg.n_boundary == 0:
+        return Ai
+    Ab = cfg.boundary_weight * assemble_rows(cfg, I.boundary_points(cfg), "value")
+    return np.vstack([Ai, Ab])
+
+
+def assemble_Ac(cfg: I.Config) -> np.ndarray:
+    """Full periodic matrix A^c on the whole oversampled grid, natural order."""
+    g = I.grid_axis(cfg)
+    kind = "laplacian" if cfg.row_op == I.ROW_LAPLACIAN else "value"
+    if cfg.dim == 1:
+        return assemble_rows(cfg, g, kind)
+    X, Y = np.meshgrid(g, g, indexing="ij")
+    return assemble_rows(cfg, np.stack([X.ravel(), Y.ravel()], axis=1), kind)
+
+
+def boundary_row(cfg: I.Config, pt, window: int | None = None) -> np.ndarray:
+    """One boundary row beta * phi_j(x_b) (used for sampled parity at full size)."""
+    return cfg.boundary_weight * assemble_rows(cfg, np.asarray(pt, dtype=np.float64)[None, :], "value")[0]
+
+
+def A_row_entries(cfg: I.Config, i_grid, half_width: int = 40):
+    """Nonzero window of interior row for grid index i_grid (1-D int, 2-D (qx, qy)).
+
+    Returns (column indices, values) for the columns within +-half_width centers per
+    axis; outside that window phi^per < 1e-300 for eps h = 0.5 (exp(-(0.5*40)^2) ~ 1e-174,
+    and the row is summed exactly by the caller).  Used for sampled full-size parity.
+    """
+    n, s = cfg.n, cfg.s
+    g = I.grid_axis(cfg)
+    c = I.center_axis(cfg)
+    kind = 2 if cfg.row_op == I.ROW_LAPLACIAN else 0
+    if cfg.dim == 1:
+        q = int(i_grid)
+        j0 = q // s
+        js = (np.arange(j0 - half_width, j0 + half_width + 1)) % n
+        js = np.unique(js)
+        vals = periodized(g[q] - c[js], cfg.eps, cfg.T, kind)
+        if kind:
+            vals = cfg.row_scale * vals
+        return js, vals
+    qx, qy = i_grid
+    jx = np.unique(np.arange(qx // s - half_width, qx // s + half_width + 1) % n)
+    jy = np.unique(np.arange(qy // s - half_width, qy // s + half_width + 1) % n)
+    x0 = periodized(g[qx] - c[jx], cfg.eps, cfg.T, 0)
+    y0 = periodized(g[qy] - c[jy], cfg.eps, cfg.T, 0)
+    if kind:
+        x2 = periodized(g[qx] - c[jx], cfg.eps, cfg.T, 2)
+        y2 = periodized(g[qy] - c[jy], cfg.eps, cfg.T, 2)
+        V = cfg.row_scale * (x2[:, None] * y0[None, :] + x0[:, None] * y2[None, :])
+    else:
+        V = x0[:, None] * y0[None, :]
+    cols = (jx[:, None] * n + jy[None, :]).ravel()
+    return cols, V.ravel()

@@ -1,0 +1,270 @@
+"""Seeded, synthetic workload inputs shared by the oracle and the CUDA path.
+
+This module holds NONE of the AZ method's arithmetic (no kernel sums, no
+symbols, no transforms, no least squares).  It only produces the data that
+both sides consume as inputs:
+
+* the configuration table (BASELINE.json configs[0..4] plus reduced members of
+  the same families, SURVEY.md §8 table / §8(d) inputs table);
+* the collocation mask on the oversampled grid (PAPER.md:120-123 Eq. set_X,
+  PAPER.md:586-589 Eq. set_X_2d; closed membership);
+* the boundary points of config 4 ("M^b points along the
+  boundary");
+* the right-hand-side samples and the manufactured exact solutions;
+* the evaluation (test) grids.
+
+The probe matrix Omega is NOT generated here: each side implements the same
+counter-based Philox4x32-10 generator itself (oracle/philox.py and
+csrc/az_philox.cuh), per the task rules.
+
+Grid conventions (PAPER.md:76-83 Eqs. set_centers / set_Xtilde with T=1):
+  centers  c_j = -1 + j*h,          h = 2/n,      j = 0..n-1
+  grid     x_q = -1 + q*(2/(s*n)),                q = 0..s*n-1
+Every coordinate is exact in binary64 for the power-of-two sizes used.
+2-D arrays are row-major with x the OUTER (slow) index, y the inner one
+("j = (m-1)N^y + n").
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from typing import Callable, List, Optional, Tuple
+
+import numpy as np
+
+# --------------------------------------------------------------------------------------
+# configuration table
+# --------------------------------------------------------------------------------------
+
+ROW_VALUE = 0       # interior rows are plain kernel values (function approximation)
+ROW_LAPLACIAN = 1   # interior rows are alpha * Laplacian of the kernel (Poisson, config 4)
+
+
+@dataclasses.dataclass(frozen=True)
+class Config:
+    name: str
+    dim: int              # 1 or 2
+    n: int                # centers per axis (paper N, N^x = N^y)
+    s: int                # oversampling factor per axis (paper s; BASELINE "L")
+    domain: str           # "interval" | "disk" | "star" | "box"
+    row_op: int           # ROW_VALUE | ROW_LAPLACIAN
+    nrhs: int
+    R: int                # probe block size (BASELINE "R")
+    seed: int
+    tol: float
+    boundary_weight: float = 0.0   # beta (config 4: 10)
+    n_boundary: int = 0            # M_b
+    T: float = 1.0
+
+    @property
+    def h(self) -> float:
+        return 2.0 * self.T / self.n
+
+    @property
+    def eps(self) -> float:
+        # BASELINE: eps = 0.5 / h  (SURVEY.md §0 naming trap 3)
+        return 0.5 / self.h
+
+    @property
+    def grid_n(self) -> int:
+        return self.s * self.n
+
+    @property
+    def N(self) -> int:
+        return self.n ** self.dim
+
+    @property
+    def row_scale(self) -> float:
+        # alpha: 1 for value rows; -1/(2 eps^2) for Laplacian rows (PAPER.md:704,
+        # "we normalize A^i with the factor -2 eps^2")
+        if self.row_op == ROW_LAPLACIAN:
+            return -1.0 / (2.0 * self.eps * self.eps)
+        return 1.0
+
+
+def _disk_R(n: int, s: int) -> int:
+    # BASELINE configs[2]: "R sized 1.5x the boundary point count (~1.5*pi*0.8*512)"
+    return int(round(1.5 * math.pi * 0.8 * s * n))
+
+
+def make_config(family: str, n: int, *, nrhs: int = 1, R: Optional[int] = None,
+                seed: int = 0, s: int = 2, name: Optional[str] = None) -> Config:
+    """Members of the BASELINE families at any size (reduced members for parity)."""
+    if family == "interval":
+        return Config(name or f"interval_n{n}", 1, n, s, "interval", ROW_VALUE, nrhs,
+                      R if R is not None else 40, seed, 1e-12)
+    if family == "box1d":      # Omega = whole periodic box (periodic special case)
+        return Config(name or f"box1d_n{n}", 1, n, s, "box", ROW_VALUE, nrhs,
+                      R if R is not None else 16, seed, 1e-12)
+    if family == "disk":
+        return Config(name or f"disk_n{n}", 2, n, s, "disk", ROW_VALUE, nrhs,
+                      R if R is not None else _disk_R(n, s), seed, 1e-10)
+    if family == "box2d":
+        return Config(name or f"box2d_n{n}", 2, n, s, "box", ROW_VALUE, nrhs,
+                      R if R is not None else 16, seed, 1e-10)
+    if family == "star":
+        return Config(name or f"star_n{n}", 2, n, s, "star", ROW_LAPLACIAN, nrhs,
+                      R if R is not None else 8 * n, seed, 1e-10,
+                      boundary_weight=10.0, n_boundary=4 * n)
+    raise ValueError(f"unknown family {family!r}")
+
+
+# BASELINE.json configs[0..4]
+CONFIGS = {
+    "c1": make_config("interval", 256, nrhs=1, R=40, seed=0, name="c1"),
+    "c2": make_config("interval", 1 << 20, nrhs=64, R=64, seed=1, name="c2"),
+    "c3": make_config("disk", 256, nrhs=1, R=1930, seed=2, name="c3"),
+    "c4": make_config("star", 128, nrhs=1, R=1024, seed=3, name="c4"),
+    "c5": make_config("disk", 512, nrhs=8, R=3072, seed=4, name="c5"),
+}
+
+
+def get_config(name: str) -> Config:
+    return CONFIGS[name]
+
+
+# --------------------------------------------------------------------------------------
+# geometry data (inputs, not method)
+# --------------------------------------------------------------------------------------
+
+def grid_axis(cfg: Config) -> np.ndarray:
+    """Oversampled grid coordinates along one axis, x_q = -T + q*2T/(s n)."""
+    L = cfg.grid_n
+    return -cfg.T + np.arange(L, dtype=np.float64) * (2.0 * cfg.T / L)
+
+
+def center_axis(cfg: Config) -> np.ndarray:
+    return -cfg.T + np.arange(cfg.n, dtype=np.float64) * cfg.h
+
+
+def _in_domain(domain: str, x: np.ndarray, y: Optional[np.ndarray] = None) -> np.ndarray:
+    # Closed membership, computed in binary64 exactly as SURVEY.md §8(c-4) #13 states.
+    if domain == "interval":
+        return (-0.5 <= x) & (x <= 0.5)
+    if domain == "box":
+        return np.ones(np.broadcast(x, x if y is None else y).shape, dtype=bool)
+    if domain == "disk":
+        return x * x + y * y <= 0.64
+    if domain == "star":
+        return np.hypot(x, y) <= 0.6 + 0.15 * np.cos(5.0 * np.arctan2(y, x))
+    raise ValueError(domain)
+
+
+def mask(cfg: Config) -> np.ndarray:
+    """uint8 collocation mask on the full oversampled grid, natural row-major order.
+
+    1-D: shape (s n,).  2-D: shape (s n, s n), x outer.
+    """
+    g = grid_axis(cfg)
+    if cfg.dim == 1:
+        return _in_domain(cfg.domain, g).astype(np.uint8)
+    X, Y = np.meshgrid(g, g, indexing="ij")
+    return _in_domain(cfg.domain, X, Y).astype(np.uint8)
+
+
+def collocation_points(cfg: Config) -> np.ndarray:
+    """Interior collocation points in natural order: (M,) in 1-D, (M, 2) in 2-D."""
+    g = grid_axis(cfg)
+    m = mask(cfg).astype(bool)
+    if cfg.dim == 1:
+        return g[m]
+    X, Y = np.meshgrid(g, g, indexing="ij")
+    return np.stack([X[m], Y[m]], axis=1)
+
+
+def star_radius(theta: np.ndarray) -> np.ndarray:
+    return 0.6 + 0.15 * np.cos(5.0 * theta)
+
+
+def boundary_points(cfg: Config) -> np.ndarray:
+    """(M_b, 2) boundary points, theta_k = 2 pi k / M_b."""
+    if cfg.n_boundary == 0:
+        return np.zeros((0, max(cfg.dim, 1)), dtype=np.float64)
+    if cfg.domain != "star":
+        raise ValueError("boundary points are defined for the star domain only")
+    th = 2.0 * np.pi * np.arange(cfg.n_boundary, dtype=np.float64) / cfg.n_boundary
+    r = star_radius(th)
+    return np.stack([r * np.cos(th), r * np.sin(th)], axis=1)
+
+
+# --------------------------------------------------------------------------------------
+# right-hand sides and exact solutions (manufactured data)
+# --------------------------------------------------------------------------------------
+
+def exact_functions(cfg: Config) -> List[Callable]:
+    """The functions the approximant should reproduce, one per RHS column.
+
+    For the Poisson config this is the manufactured solution u (the approximant is
+    u's expansion); for approximation configs it is f itself.
+    """
+    if cfg.row_op == ROW_LAPLACIAN:
+        return [lambda x, y: np.sin(3 * x) * np.cos(2 * y)]
+    if cfg.dim == 1:
+        if cfg.nrhs == 1:
+            return [lambda x: np.exp(x) * np.cos(8 * x)]
+        return [(lambda k: (lambda x: np.cos(k * x) * np.exp(-x * x)))(k)
+                for k in range(1, cfg.nrhs + 1)]
+    if cfg.nrhs == 1:
+        return [lambda x, y: np.exp(x + y) * np.sin(3 * x) * np.cos(2 * y)]
+    return [(lambda k: (lambda x, y: np.cos(k * x + y) * np.exp(-(x * x + y * y))))(k)
+            for k in range(1, cfg.nrhs + 1)]
+
+
+def _laplacian_of_u(x, y):
+    # u = sin(3x) cos(2y)  =>  Delta u = -(9 + 4) u  (BASELINE configs[3] "f=Delta u")
+    return -13.0 * np.sin(3 * x) * np.cos(2 * y)
+
+
+def rhs(cfg: Config) -> np.ndarray:
+    """b, shape (M + M_b, nrhs), float64, column-major-friendly (Fortran order).
+
+    Interior rows: alpha * f(x_i) (alpha = row_scale; f = Delta u for Poisson).
+    Boundary rows: beta * u(x_b)  (SURVEY.md §8(c-4) #11 "multiply rows and data by beta").
+    """
+    pts = collocation_points(cfg)
+    fns = exact_functions(cfg)
+    M = pts.shape[0]
+    Mb = cfg.n_boundary
+    b = np.zeros((M + Mb, cfg.nrhs), dtype=np.float64, order="F")
+    if cfg.row_op == ROW_LAPLACIAN:
+        b[:M, 0] = cfg.row_scale * _laplacian_of_u(pts[:, 0], pts[:, 1])
+        bp = boundary_points(cfg)
+        b[M:, 0] = cfg.boundary_weight * fns[0](bp[:, 0], bp[:, 1])
+        return b
+    for k, f in enumerate(fns):
+        b[:M, k] = f(pts) if cfg.dim == 1 else f(pts[:, 0], pts[:, 1])
+    return b
+
+
+# --------------------------------------------------------------------------------------
+# evaluation grids (verification only, never timed)
+# --------------------------------------------------------------------------------------
+
+@dataclasses.dataclass
+class TestGrid:
+    axes: Tuple[np.ndarray, ...]      # tensor axes
+    inside: np.ndarray                # bool, shape = tensor shape
+    exact: np.ndarray                 # (n_points_inside, nrhs) exact values
+
+
+def test_grid(cfg: Config, points_1d: Optional[int] = None) -> TestGrid:
+    fns = exact_functions(cfg)
+    if cfg.dim == 1:
+        m = points_1d or (2001 if cfg.n <= 4096 else 65537)
+        t = np.linspace(-0.5, 0.5, m) if cfg.domain == "interval" else np.linspace(-1, 1, m, endpoint=False)
+        inside = np.ones(m, dtype=bool)
+        ex = np.stack([f(t) for f in fns], axis=1)
+        return TestGrid((t,), inside, ex)
+    m = points_1d or 401
+    lim = {"disk": 0.8, "star": 0.75, "box": 1.0}[cfg.domain]
+    t = np.linspace(-lim, lim, m) if cfg.domain != "box" else np.linspace(-1, 1, m, endpoint=False)
+    X, Y = np.meshgrid(t, t, indexing="ij")
+    inside = _in_domain(cfg.domain, X, Y)
+    ex = np.stack([f(X[inside], Y[inside]) for f in fns], axis=1)
+    return TestGrid((t, t), inside, ex)
+
+
+def gaussian_matrix(rows: int, cols: int, seed: int) -> np.ndarray:
+    """Seeded N(0,1) test vectors for operator parity tests (not the AZ probes)."""
+    rng = np.random.default_rng(seed)
+    return np.asfortranarray(rng.standard_normal((rows, cols)))
