@@ -1,0 +1,182 @@
+/*
+ * az.h -- C ABI of libaz: the data-parallel hot path of the AZ algorithm for
+ * oversampled periodised-Gaussian RBF collocation (arXiv:2308.14490, PAPER.md),
+ * hand-written for NVIDIA B200 (sm_100a), FP64 / complex128 throughout.
+ *
+ * The path (Alg. 1, with Z* = F B^dag P E):
+ *   step 1   solve (I - A Z*) A x2 = (I - A Z*) b with the randomized low-rank solver
+ *            (PAPER.md:257, 269): S = (A - A Z* A) Omega, truncated SVD, x2 = Omega y
+ *   step 2   x1 = Z* (b - A x2)
+ *   step 3   x  = x1 + x2
+ *
+ * Conventions (all entry points):
+ *   - Every vector/matrix argument is a caller-owned DEVICE pointer to float64 data,
+ *     column-major, `nvec` columns with leading dimension ld >= rows, unless stated.
+ *   - Coefficient vectors (length N = n^dim) are in natural row-major order of the
+ *     centres, j = jx*n + jy.
+ *   - Row vectors (length M + Mb) hold the M interior collocation rows in natural
+ *     row-major order of the oversampled grid (x outer), then the Mb boundary rows
+ *     in the caller's order.  The paper orders the
+ *     interior rows like Pi X~; a row permutation does not change
+ *     the least-squares problem, and the polyphase order is internal only.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     All calls are asynchronous on `stream` unless stated; the library never
+ *     synchronises the device except where a host result is returned.
+ *   - Errors are status codes; no C++ exception crosses the ABI.  Arguments are
+ *     validated before any launch and outputs are untouched on argument errors.
+ *     az_last_error() returns a thread-local detail string for the last failure.
+ *   - There is no CPU fallback: every arithmetic step runs in libaz's kernels.
+ */
+#ifndef AZ_H_
+#define AZ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct az_plan_s* az_plan_t;
+
+typedef enum {
+  AZ_OK = 0,
+  AZ_ERR_INVALID_ARGUMENT = 1,
+  AZ_ERR_OVERSAMPLING = 2,      /* M + Mb <= N: "choose s large enough such that M > N" */
+  AZ_ERR_SINGULAR_SYMBOL = 3,   /* max_k sigma(k) == 0 (SPEC.md:188 singular-symbol)                */
+  AZ_ERR_OUT_OF_MEMORY = 4,
+  AZ_ERR_CUDA = 5,
+  AZ_ERR_NOT_SUPPORTED = 6,     /* size/oversampling outside the supported FFT lengths              */
+  AZ_ERR_WORKSPACE = 7,         /* workspace too small                                              */
+  AZ_WARN_SKETCH_SATURATED = 100 /* rank == probes - p after max_blocks probe blocks (x still written) */
+} az_status_t;
+
+typedef enum {
+  AZ_ROW_VALUE = 0,      /* interior rows phi_j(x_i) (function approximation) */
+  AZ_ROW_LAPLACIAN = 1   /* interior rows row_scale * (d2/dx2 + d2/dy2) phi_j(x_i), PAPER.md:741-752 with k0^2 = 0 */
+} az_row_op_t;
+
+/* Plan descriptor.  Box [-T, T)^dim, n centres per axis c_j = -T + j 2T/n,
+ * oversampled grid of L*n points per axis x_q = -T + q 2T/(L n).
+ * Supported: dim = 1 with n a power of two in [16, 2^21]; dim = 2 with n a power of two in
+ * [8, 1024]; L in {1, 2, 4} with L*n <= 2048 per 2-D axis. */
+typedef struct {
+  int32_t dim;                 /* 1 or 2 */
+  int64_t n;                   /* centres per axis (paper N, N^x = N^y) */
+  int32_t L;                   /* oversampling factor per axis (paper s; BASELINE "L") */
+  double T;                    /* half-period of the box (paper T) */
+  double eps;                  /* Gaussian shape parameter */
+  int32_t op;                  /* az_row_op_t */
+  double row_scale;            /* alpha: interior rows and data scaled by it (-1/(2 eps^2)) */
+  const uint8_t* mask;         /* HOST, (L n)^dim bytes, natural row-major (x outer); 1 = collocation point
+                                  (PAPER.md:121-123, 587-589).  Deep-copied. */
+  int64_t n_boundary;          /* Mb (0 if none) */
+  const double* boundary_xy;   /* HOST, Mb x dim row-major points; deep-copied */
+  double boundary_weight;      /* beta: boundary rows are beta * phi_j(x_b) */
+  double zstar_rcond;          /* Z* keeps modes with sigma(k) > rcond * max sigma (reading R3) */
+  uint64_t seed;               /* Philox key of the probe matrix Omega */
+} az_plan_desc_t;
+
+typedef struct {
+  int64_t N;          /* columns n^dim */
+  int64_t M;          /* interior rows */
+  int64_t Mb;         /* boundary rows */
+  double sigma_max;   /* largest singular value of the periodic A^c (unitary normalisation, Lemma 3) */
+  double sigma_min_kept;
+  int64_t n_dropped;  /* Z* modes below the threshold */
+  double zstar_norm;  /* ||Z*||_2 = 1 / sigma_min_kept */
+} az_plan_info_t;
+
+/* Build the plan (step 0): kernel samples and their DFTs (Lemma 3,
+ * PAPER.md:344-353) for the symbol of B, sigma(k)^2 = sum_i |d_i(k)|^2 and the thresholded
+ * pseudo-inverse diagonals, mask packing, device scratch.
+ * Synchronises `stream` once (reads back sigma_max).  *out receives the plan. */
+az_status_t az_plan_create(const az_plan_desc_t* desc, void* stream, az_plan_t* out);
+az_status_t az_plan_destroy(az_plan_t plan);
+az_status_t az_plan_query(az_plan_t plan, az_plan_info_t* info);
+
+/* y (M+Mb x nvec) = A x (N x nvec).  A = [R P* B F* ; beta A^b].  */
+az_status_t az_apply_A(az_plan_t plan, const double* x, int64_t ldx, double* y, int64_t ldy,
+                       int64_t nvec, void* stream);
+/* x (N x nvec) = A^T y (M+Mb x nvec).  The adjoint of az_apply_A.            */
+az_status_t az_apply_At(az_plan_t plan, const double* y, int64_t ldy, double* x, int64_t ldx,
+                        int64_t nvec, void* stream);
+/* x (N x nvec) = Z* y.  Z* = [F B^dag P E, 0_{N x Mb}]:
+ * the boundary rows of y are ignored.                                                        */
+az_status_t az_apply_Zstar(az_plan_t plan, const double* y, int64_t ldy, double* x, int64_t ldx,
+                           int64_t nvec, void* stream);
+/* y (M+Mb x nvec) = (A - A Z* A) v  -- the step-1 operator.                */
+az_status_t az_apply_step1(az_plan_t plan, const double* v, int64_t ldv, double* y, int64_t ldy,
+                           int64_t nvec, void* stream);
+/* y (M+Mb x nvec) = (I - A Z*) b  -- the step-1 right-hand side.              */
+az_status_t az_apply_resid(az_plan_t plan, const double* b, int64_t ldb, double* y, int64_t ldy,
+                           int64_t nvec, void* stream);
+
+/* S[:, 0:ncols] = (A - A Z* A) Omega[:, col0 : col0+ncols] with Omega generated on the fly
+ * (Philox4x32-10 keyed by plan seed and GLOBAL column index; probes never stored).
+ * PAPER.md:269 "r+p matrix vector products".  Used by az_solve and by multi-GPU drivers that
+ * shard probe columns.  S is (M+Mb) x ncols, leading dimension ldS.                          */
+az_status_t az_sketch(az_plan_t plan, int64_t col0, int64_t ncols, double* S, int64_t ldS,
+                      void* stream);
+/* x (N x nrhs) (+)= Omega[:, col0 : col0+ncols] y  (y: ncols x nrhs, DEVICE).  accumulate = 0
+ * overwrites x.  Regenerates Omega (a9 of SURVEY.md §8(a)).                                  */
+az_status_t az_omega_apply(az_plan_t plan, int64_t col0, int64_t ncols, const double* y, int64_t ldy,
+                           int64_t nrhs, double* x, int64_t ldx, int accumulate, void* stream);
+
+/* R factor of a tall matrix by Householder TSQR (no Q is formed; "SVD of an
+ * (r+p)-by-M matrix" done as QR + small SVD).  A: m x k DEVICE column-major (ld lda), k <= 256
+ * for the single-pass TSQR; larger k uses blocked Householder (A is overwritten).
+ * Rout: k x k upper-triangular DEVICE, leading dimension ldr (strict lower part zeroed).
+ * Rows may be in any order (QR is row-permutation equivariant).                              */
+az_status_t az_qr_r(az_plan_t plan, double* A, int64_t m, int64_t k, int64_t lda,
+                    double* Rout, int64_t ldr, void* workspace, size_t ws_bytes, void* stream);
+az_status_t az_qr_workspace_size(int64_t m, int64_t k, size_t* bytes);
+
+/* Truncated least squares on the QR-reduced sketch: with Rf = [R_S | c] (R_S: r x r upper
+ * triangular, c: r x nrhs = (Q^T b')[:r]), compute R_S = U Sigma V^T (one-sided Jacobi SVD),
+ * keep sigma_i > theta * sigma_1, y = V_k Sigma_k^-1 U_k^T c.  All DEVICE.  rank_out (HOST,
+ * may be NULL) receives k and sigma_out (DEVICE, may be NULL) the r singular values
+ * (descending).  Synchronises the stream when rank_out != NULL.                              */
+az_status_t az_tsvd_solve(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta,
+                          double* y, int64_t ldy, double* sigma_out, int64_t* rank_out,
+                          void* workspace, size_t ws_bytes, void* stream);
+az_status_t az_tsvd_workspace_size(int64_t r, int64_t nrhs, size_t* bytes);
+
+typedef struct {
+  int64_t rank_used;        /* k: kept singular values of the sketch */
+  int64_t probes_used;      /* number of probe columns drawn (multiple of R) */
+  int32_t saturated;        /* 1 if k > probes_used - p after max_blocks blocks */
+  double sigma_first, sigma_last_kept;
+  double ms_rhs, ms_sketch, ms_qr, ms_svd, ms_step2, ms_total;   /* CUDA-event stage times */
+} az_solve_report_t;
+
+/* Bytes of DEVICE workspace az_solve needs for nrhs right-hand sides, probe block R and at
+ * most max_blocks probe blocks. */
+az_status_t az_solve_workspace_size(az_plan_t plan, int64_t nrhs, int64_t R, int32_t max_blocks,
+                                    size_t* bytes);
+/* The whole AZ solve (Alg. 1).  b: (M+Mb) x nrhs, x: N x nrhs (DEVICE).
+ * theta: sketch truncation threshold relative to sigma_1 of the sketch (R4).
+ * R: probe block size; blocks are added until rank <= probes - p (p = 10) or
+ * max_blocks is reached (R5; max_blocks = 1 is the literal single-block sketch).
+ * report: HOST, may be NULL.  Synchronises the stream (block-adaptive decisions and the
+ * report need host values).  Returns AZ_WARN_SKETCH_SATURATED if the last block saturated.  */
+az_status_t az_solve(az_plan_t plan, const double* b, int64_t ldb, double* x, int64_t ldx,
+                     int64_t nrhs, double theta, int64_t R, int32_t max_blocks,
+                     void* workspace, size_t ws_bytes, az_solve_report_t* report, void* stream);
+
+/* Host-buffer convenience: b (HOST, (M+Mb) x nrhs) -> x (HOST, N x nrhs), including the
+ * host<->device copies (pinned staging owned by the plan).  Used for end-to-end timing.      */
+az_status_t az_solve_host(az_plan_t plan, const double* b_host, double* x_host, int64_t nrhs,
+                          double theta, int64_t R, int32_t max_blocks, az_solve_report_t* report,
+                          void* stream);
+
+const char* az_status_string(az_status_t s);
+const char* az_last_error(void);
+/* Number of libaz kernel launches issued by this thread since the last reset (instrumentation
+ * for the bench's gpu_launches field). */
+int64_t az_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AZ_H_ */

@@ -1,0 +1,88 @@
+// Internal plan structure and cross-file declarations of libaz.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "az_common.cuh"
+
+enum az_layout_t {
+  AZ_LAYOUT_1D_SMALL = 0,   // 1-D, L = s n <= 2048: whole chain per vector pair in one CTA
+  AZ_LAYOUT_1D_FOURSTEP = 1,// 1-D, n > 1024: four-step [N1][N2] / [N1][L2] layout, 5 HBM passes
+  AZ_LAYOUT_2D = 2          // 2-D, [x][y] row-major, y contiguous
+};
+
+// Operation selectors shared by the pass kernels.
+enum az_op_t { OP_A = 0, OP_AT = 1, OP_ZSTAR = 2, OP_STEP1 = 3, OP_RESID = 4 };
+
+// Input sources for coefficient-space entry.
+enum az_src_t { SRC_VEC = 0, SRC_PROBE = 1 };
+
+struct az_plan_s {
+  // geometry
+  int dim;
+  int64_t n, s, L;          // L = s n grid points per axis
+  int64_t N, G;             // n^dim, L^dim
+  int64_t M, Mb;
+  double T, eps, alpha, beta, rcond;
+  uint64_t seed;
+  int op;
+  int layout;
+  // four-step factorisation (1-D large): n = N1 N2, L = N1 L2
+  int64_t N1, N2, L2;
+  // device tables
+  uint8_t* d_mask = nullptr;    // G
+  int32_t* d_pos = nullptr;     // G: row index of an interior grid point, -1 outside
+  cplx* d_W0 = nullptr;         // fine symbol, order 0 (per axis length L; four-step: [N1][L2])
+  cplx* d_W2 = nullptr;         // fine symbol, order 2 (Laplacian)
+  double* d_zinv = nullptr;     // N: 1/sigma^2(k) if kept else 0 (coefficient spectrum order)
+  cplx* d_tw = nullptr;         // TWN-point twiddle table e^{-2 pi i t / TWN}
+  cplx* d_tw4hi = nullptr;      // four-step twiddles e^{-2 pi i (h 2^TW4B) / L}
+  cplx* d_tw4lo = nullptr;      // e^{-2 pi i l / L}
+  double* d_bxy = nullptr;      // Mb x 2 boundary points
+  // scratch for the pass kernels
+  int64_t Bmax = 0;             // max vector PAIRS per batch
+  cplx* d_C1 = nullptr;         // Bmax * N complex
+  cplx* d_G = nullptr;          // Bmax * G complex
+  // host-side info
+  double sigma_max2 = 0, sigma_min_kept2 = 0;
+  int64_t n_dropped = 0;
+  // pinned host staging for az_solve_host
+  double* h_stage = nullptr;
+  size_t h_stage_bytes = 0;
+  void* d_solve_ws = nullptr;
+  size_t d_solve_ws_bytes = 0;
+};
+
+constexpr int TWN = 2048;
+constexpr int TW4B = 11;
+
+// --- 1-D small layout (az_ops1d.cu)
+az_status_t az1s_apply(az_plan_s* p, int op, int src, const double* in, int64_t ldin, double* out,
+                       int64_t ldout, int64_t nvec, int64_t col0, cudaStream_t st);
+az_status_t az1s_fft_table(az_plan_s* p, cplx* data, int64_t len, cudaStream_t st);
+
+// --- 1-D four-step layout (az_ops1f.cu)
+az_status_t az1f_apply(az_plan_s* p, int op, int src, const double* in, int64_t ldin, double* out,
+                       int64_t ldout, int64_t nvec, int64_t col0, cudaStream_t st);
+az_status_t az1f_fft_fine_forward(az_plan_s* p, cplx* data, cudaStream_t st);
+
+// --- 2-D layout (az_ops2d.cu)
+az_status_t az2_apply(az_plan_s* p, int op, int src, const double* in, int64_t ldin, double* out,
+                      int64_t ldout, int64_t nvec, int64_t col0, cudaStream_t st);
+
+// generic FFT of `count` contiguous vectors of length len (len <= 2048) in place
+az_status_t az_fft_batch(const cplx* tw, cplx* data, int64_t len, int64_t count, int dir, cudaStream_t st);
+
+// --- QR / SVD / solve
+az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R, int64_t ldr,
+                         void* ws, size_t ws_bytes, cudaStream_t st);
+size_t az_qr_ws_bytes(int64_t m, int64_t k);
+az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta,
+                         double* y, int64_t ldy, double* sigma_out, int64_t* rank_out,
+                         void* ws, size_t ws_bytes, cudaStream_t st);
+size_t az_tsvd_ws_bytes(int64_t r, int64_t nrhs);
+
+
+inline unsigned az_div_up(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }

@@ -1,0 +1,198 @@
+// 1-D operators for L = s n <= 2048: the whole operator chain for one vector pair runs in one
+// CTA with the data resident in shared memory (only the compulsory bytes touch HBM).
+//
+// Fine-grid formulation (equivalent to PAPER.md Sec. 3.1):
+//   A^c a    = IFFT_L( W . FFT_L(a_up) ) / L,   a_up = a zero-stuffed onto the fine grid
+//              (FFT_L(a_up)(kf) = a^(kf mod n): the s aliases of the coefficient spectrum),
+//   W        = FFT_L( phi^per(q h_L) )  (Lemma 3 on the fine grid: W(k + m n) are the s
+//              diagonals d_i of B up to the polyphase phase factors),
+//   Z* y     = IFFT_n( zinv . sum_m conj(W(k+mn)) FFT_L(E y)(k+mn) ) / n   (B^dag P E, then F),
+//   A^T y    = IFFT_n( sum_m conj(W(k+mn)) FFT_L(y)(k+mn) ) / L.
+// IFFT_n of a spectrum f is read off the fine grid: IFFT_L(extend f)[s j] = s IFFT_n(f)[j].
+// Two real vectors are processed together as one complex vector (real part = column 2p,
+// imaginary part = column 2p+1): every operator here is real, so it acts on both at once.
+#include "az_fft.cuh"
+#include "az_internal.h"
+
+struct P1s {
+  const cplx* W0;
+  const cplx* W2;
+  const double* zinv;
+  const int32_t* pos;
+  const cplx* tw;
+  int lap;
+  double alpha;
+  int n, s;
+  uint64_t seed;
+  const double* in;
+  int64_t ldin;
+  double* out;
+  int64_t ldout;
+  int64_t nvec;
+  int64_t col0;
+};
+
+AZ_D cplx sym1(const P1s& a, int kf) { return a.lap ? cscale(a.W2[kf], a.alpha) : a.W0[kf]; }
+
+template <int L, int OP, int SRC>
+__global__ void __launch_bounds__(L / 8) k_chain1s(P1s a) {
+  extern __shared__ cplx sm[];
+  cplx* buf = sm;                       // spad_len(L)
+  cplx* aux = sm + spad_len(L);         // n
+  constexpr int NT = L / 8;
+  const int tid = threadIdx.x;
+  const int n = a.n, s = a.s;
+  const int64_t cre = 2 * (int64_t)blockIdx.x, cim = cre + 1;
+  const bool has_im = cim < a.nvec;
+  const double invL = 1.0 / (double)L;
+
+  if constexpr (OP == OP_A || OP == OP_STEP1) {
+    // ---- coefficient input, zero-stuffed onto the fine grid ----
+    for (int q = tid; q < L; q += NT) buf[spad(q)] = czero();
+    __syncthreads();
+    if constexpr (SRC == SRC_PROBE) {
+      for (int m = tid; m < n / 2; m += NT) {
+        const cpair pr = probe_cplx_pair((uint64_t)m, (uint64_t)(a.col0 + cre), (uint64_t)(a.col0 + cim),
+                                         has_im, a.seed);
+        buf[spad(2 * m * s)] = pr.a;
+        buf[spad((2 * m + 1) * s)] = pr.b;
+      }
+    } else {
+      for (int j = tid; j < n; j += NT) {
+        const double re = a.in[j + cre * a.ldin];
+        const double im = has_im ? a.in[j + cim * a.ldin] : 0.0;
+        buf[spad(j * s)] = make_double2(re, im);
+      }
+    }
+    __syncthreads();
+    fft_smem<L, -1>(buf, tid, a.tw, TWN);          // FFT_L(a_up)(kf) = a^(kf mod n)
+    if constexpr (OP == OP_STEP1) {
+      for (int k = tid; k < n; k += NT) aux[k] = buf[spad(k)];   // v^ kept for r^ = v^ - w^
+    }
+    for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = cscale(cmul(buf[spad(kf)], sym1(a, kf)), invL);
+    __syncthreads();
+    fft_smem<L, 1>(buf, tid, a.tw, TWN);           // A^c a on the full grid
+    if constexpr (OP == OP_STEP1) {
+      // E R: keep the collocation points only
+      for (int q = tid; q < L; q += NT)
+        if (a.pos[q] < 0) buf[spad(q)] = czero();
+      __syncthreads();
+      fft_smem<L, -1>(buf, tid, a.tw, TWN);
+      // B^dag P fold + spectral division, then r^ = v^ - w^
+      for (int k = tid; k < n; k += NT) {
+        cplx acc = czero();
+        for (int m = 0; m < s; ++m) {
+          const int kf = k + m * n;
+          acc = cadd(acc, cmulc(buf[spad(kf)], sym1(a, kf)));
+        }
+        aux[k] = csub(aux[k], cscale(acc, a.zinv[k]));
+      }
+      __syncthreads();
+      for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = cscale(cmul(aux[kf & (n - 1)], sym1(a, kf)), invL);
+      __syncthreads();
+      fft_smem<L, 1>(buf, tid, a.tw, TWN);
+    }
+    // ---- R: gather the collocation rows ----
+    for (int q = tid; q < L; q += NT) {
+      const int r = a.pos[q];
+      if (r >= 0) {
+        const cplx v = buf[spad(q)];
+        a.out[r + cre * a.ldout] = v.x;
+        if (has_im) a.out[r + cim * a.ldout] = v.y;
+      }
+    }
+  } else {
+    // ---- row input, E: zero padding onto the fine grid ----
+    for (int q = tid; q < L; q += NT) {
+      const int r = a.pos[q];
+      cplx v = czero();
+      if (r >= 0) v = make_double2(a.in[r + cre * a.ldin], has_im ? a.in[r + cim * a.ldin] : 0.0);
+      buf[spad(q)] = v;
+    }
+    __syncthreads();
+    fft_smem<L, -1>(buf, tid, a.tw, TWN);
+    for (int k = tid; k < n; k += NT) {
+      cplx acc = czero();
+      for (int m = 0; m < s; ++m) {
+        const int kf = k + m * n;
+        acc = cadd(acc, cmulc(buf[spad(kf)], sym1(a, kf)));
+      }
+      aux[k] = (OP == OP_AT) ? acc : cscale(acc, a.zinv[k]);
+    }
+    __syncthreads();
+    if constexpr (OP == OP_RESID) {
+      for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = cscale(cmul(aux[kf & (n - 1)], sym1(a, kf)), invL);
+    } else {
+      for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = aux[kf & (n - 1)];
+    }
+    __syncthreads();
+    fft_smem<L, 1>(buf, tid, a.tw, TWN);
+    if constexpr (OP == OP_RESID) {
+      for (int q = tid; q < L; q += NT) {
+        const int r = a.pos[q];
+        if (r >= 0) {
+          const cplx v = buf[spad(q)];
+          a.out[r + cre * a.ldout] = a.in[r + cre * a.ldin] - v.x;
+          if (has_im) a.out[r + cim * a.ldout] = a.in[r + cim * a.ldin] - v.y;
+        }
+      }
+    } else {
+      const double c = (OP == OP_ZSTAR) ? invL : invL / (double)s;
+      for (int j = tid; j < n; j += NT) {
+        const cplx v = buf[spad(j * s)];
+        a.out[j + cre * a.ldout] = v.x * c;
+        if (has_im) a.out[j + cim * a.ldout] = v.y * c;
+      }
+    }
+  }
+}
+
+template <int L>
+static az_status_t launch1s(const P1s& a, int op, int src, int64_t npairs, cudaStream_t st) {
+  const size_t sm = (size_t)(spad_len(L) + a.n) * sizeof(cplx);
+  const dim3 grid((unsigned)npairs), block(L / 8);
+#define AZ_L1S(OPV, SRCV) (az_smem_attr(k_chain1s<L, OPV, SRCV>, sm), k_chain1s<L, OPV, SRCV><<<grid, block, sm, st>>>(a))
+  if (op == OP_A) AZ_L1S(OP_A, SRC_VEC);
+  else if (op == OP_STEP1 && src == SRC_PROBE) AZ_L1S(OP_STEP1, SRC_PROBE);
+  else if (op == OP_STEP1) AZ_L1S(OP_STEP1, SRC_VEC);
+  else if (op == OP_AT) AZ_L1S(OP_AT, SRC_VEC);
+  else if (op == OP_ZSTAR) AZ_L1S(OP_ZSTAR, SRC_VEC);
+  else AZ_L1S(OP_RESID, SRC_VEC);
+#undef AZ_L1S
+  AZ_LAUNCH_CHECK();
+  return AZ_OK;
+}
+
+az_status_t az1s_apply(az_plan_s* p, int op, int src, const double* in, int64_t ldin, double* out,
+                       int64_t ldout, int64_t nvec, int64_t col0, cudaStream_t st) {
+  P1s a;
+  a.W0 = p->d_W0;
+  a.W2 = p->d_W2;
+  a.zinv = p->d_zinv;
+  a.pos = p->d_pos;
+  a.tw = p->d_tw;
+  a.lap = p->op == AZ_ROW_LAPLACIAN;
+  a.alpha = p->alpha;
+  a.n = (int)p->n;
+  a.s = (int)p->s;
+  a.seed = p->seed;
+  a.in = in;
+  a.ldin = ldin;
+  a.out = out;
+  a.ldout = ldout;
+  a.nvec = nvec;
+  a.col0 = col0;
+  const int64_t npairs = (nvec + 1) / 2;
+  switch (p->L) {
+    case 16: return launch1s<16>(a, op, src, npairs, st);
+    case 32: return launch1s<32>(a, op, src, npairs, st);
+    case 64: return launch1s<64>(a, op, src, npairs, st);
+    case 128: return launch1s<128>(a, op, src, npairs, st);
+    case 256: return launch1s<256>(a, op, src, npairs, st);
+    case 512: return launch1s<512>(a, op, src, npairs, st);
+    case 1024: return launch1s<1024>(a, op, src, npairs, st);
+    case 2048: return launch1s<2048>(a, op, src, npairs, st);
+  }
+  az_set_error("1-D small layout: unsupported L = %lld", (long long)p->L);
+  return AZ_ERR_NOT_SUPPORTED;
+}

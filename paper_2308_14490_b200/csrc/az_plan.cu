@@ -1,0 +1,476 @@
+// libaz: plan creation (step 0 of PAPER.md Sec. 3.2.3), C ABI entry points and dispatch.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <cmath>
+#include <vector>
+
+#include "az_fft.cuh"
+#include "az_internal.h"
+
+// ---------------------------------------------------------------------------------------
+// error / instrumentation plumbing
+// ---------------------------------------------------------------------------------------
+static thread_local char g_err[1024] = "";
+static std::atomic<int64_t> g_launches{0};
+
+void az_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+void az_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+extern "C" const char* az_last_error(void) { return g_err; }
+extern "C" int64_t az_launch_count(int reset) {
+  return reset ? g_launches.exchange(0) : g_launches.load();
+}
+extern "C" const char* az_status_string(az_status_t s) {
+  switch (s) {
+    case AZ_OK: return "AZ_OK";
+    case AZ_ERR_INVALID_ARGUMENT: return "AZ_ERR_INVALID_ARGUMENT";
+    case AZ_ERR_OVERSAMPLING: return "AZ_ERR_OVERSAMPLING";
+    case AZ_ERR_SINGULAR_SYMBOL: return "AZ_ERR_SINGULAR_SYMBOL";
+    case AZ_ERR_OUT_OF_MEMORY: return "AZ_ERR_OUT_OF_MEMORY";
+    case AZ_ERR_CUDA: return "AZ_ERR_CUDA";
+    case AZ_ERR_NOT_SUPPORTED: return "AZ_ERR_NOT_SUPPORTED";
+    case AZ_ERR_WORKSPACE: return "AZ_ERR_WORKSPACE";
+    case AZ_WARN_SKETCH_SATURATED: return "AZ_WARN_SKETCH_SATURATED";
+  }
+  return "AZ_UNKNOWN";
+}
+
+#define AZ_ARG(cond, ...)                 \
+  do {                                    \
+    if (!(cond)) {                        \
+      az_set_error(__VA_ARGS__);          \
+      return AZ_ERR_INVALID_ARGUMENT;     \
+    }                                     \
+  } while (0)
+
+// ---------------------------------------------------------------------------------------
+// generic batched in-place FFT of contiguous vectors (symbol tables)
+// ---------------------------------------------------------------------------------------
+template <int L, int DIR>
+__global__ void k_fft_rows(cplx* data, int64_t count, const cplx* __restrict__ tw) {
+  extern __shared__ cplx sm[];
+  constexpr int TPF = L / 8;
+  const int nf = blockDim.x / TPF;
+  const int f = threadIdx.x / TPF, j = threadIdx.x % TPF;
+  const int64_t row = (int64_t)blockIdx.x * nf + f;
+  cplx* buf = sm + f * spad_len(L);
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int i = j + t * TPF;
+    buf[spad(i)] = row < count ? data[row * L + i] : czero();
+  }
+  __syncthreads();
+  fft_smem<L, DIR>(buf, j, tw, TWN);
+  if (row < count) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int i = j + t * TPF;
+      data[row * L + i] = buf[spad(i)];
+    }
+  }
+}
+
+template <int L>
+static az_status_t fft_rows_launch(const cplx* tw, cplx* data, int64_t count, int dir, cudaStream_t st) {
+  constexpr int TPF = L / 8;
+  const int nf = TPF >= 256 ? 1 : 256 / TPF;
+  const size_t sm = (size_t)nf * spad_len(L) * sizeof(cplx);
+  if (dir < 0)
+    k_fft_rows<L, -1><<<az_div_up(count, nf), nf * TPF, sm, st>>>(data, count, tw);
+  else
+    k_fft_rows<L, 1><<<az_div_up(count, nf), nf * TPF, sm, st>>>(data, count, tw);
+  AZ_LAUNCH_CHECK();
+  return AZ_OK;
+}
+
+az_status_t az_fft_batch(const cplx* tw, cplx* data, int64_t len, int64_t count, int dir, cudaStream_t st) {
+  switch (len) {
+    case 8: return fft_rows_launch<8>(tw, data, count, dir, st);
+    case 16: return fft_rows_launch<16>(tw, data, count, dir, st);
+    case 32: return fft_rows_launch<32>(tw, data, count, dir, st);
+    case 64: return fft_rows_launch<64>(tw, data, count, dir, st);
+    case 128: return fft_rows_launch<128>(tw, data, count, dir, st);
+    case 256: return fft_rows_launch<256>(tw, data, count, dir, st);
+    case 512: return fft_rows_launch<512>(tw, data, count, dir, st);
+    case 1024: return fft_rows_launch<1024>(tw, data, count, dir, st);
+    case 2048: return fft_rows_launch<2048>(tw, data, count, dir, st);
+  }
+  az_set_error("az_fft_batch: unsupported length %lld", (long long)len);
+  return AZ_ERR_NOT_SUPPORTED;
+}
+
+// ---------------------------------------------------------------------------------------
+// step-0 kernels: twiddles, kernel samples, sigma^2, thresholded pseudo-inverse weights
+// ---------------------------------------------------------------------------------------
+__global__ void k_twiddles(cplx* tw, int twn, cplx* hi, cplx* lo, int64_t Lbig, int nhi, int nlo) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double s, c;
+  if (i < twn) {
+    sincospi(-2.0 * (double)i / (double)twn, &s, &c);
+    tw[i] = make_double2(c, s);
+  }
+  if (hi && i < nhi) {   // e^{-2 pi i (h 2^TW4B) / Lbig}
+    const int64_t t = (i << TW4B) % Lbig;
+    sincospi(-2.0 * (double)t / (double)Lbig, &s, &c);
+    hi[i] = make_double2(c, s);
+  }
+  if (lo && i < nlo) {
+    sincospi(-2.0 * (double)i / (double)Lbig, &s, &c);
+    lo[i] = make_double2(c, s);
+  }
+}
+
+// Lemma 3 on the fine grid: w[q] = phi^per(q h_L) (order 0 or 2), q in [0, L).
+__global__ void k_samples(cplx* out, int64_t L, double hL, double eps, double T, int order) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < L) out[q] = make_double2(az_phi_per((double)q * hL, eps, T, order), 0.0);
+}
+
+// Four-step layout of the same samples: natural index x = n1 * L2 + n2 (stored as is).
+
+struct SymArgs {
+  const cplx* W0;
+  const cplx* W2;
+  int lap;
+  double alpha;
+};
+
+AZ_D cplx sym_1d(const SymArgs& a, int64_t kf) {
+  return a.lap ? cscale(a.W2[kf], a.alpha) : a.W0[kf];
+}
+AZ_D cplx sym_2d(const SymArgs& a, int64_t kx, int64_t ky) {
+  if (!a.lap) return cmul(a.W0[kx], a.W0[ky]);
+  return cscale(cadd(cmul(a.W2[kx], a.W0[ky]), cmul(a.W0[kx], a.W2[ky])), a.alpha);
+}
+
+AZ_D void atomic_max_pos(double* addr, double v) {   // v >= 0
+  atomicMax((unsigned long long*)addr, (unsigned long long)__double_as_longlong(v));
+}
+AZ_D void atomic_min_pos(double* addr, double v) {
+  atomicMin((unsigned long long*)addr, (unsigned long long)__double_as_longlong(v));
+}
+
+// sigma^2(k) = sum over the s^d aliases of |W(k + m n)|^2 (diag of B*B)
+__global__ void k_sigma2(double* sig2, double* smax, SymArgs a, int layout, int64_t n, int64_t s,
+                         int64_t N1, int64_t N2, int64_t L2) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double acc = 0.0;
+  int64_t N = layout == AZ_LAYOUT_2D ? n * n : n;
+  if (k < N) {
+    if (layout == AZ_LAYOUT_1D_SMALL) {
+      for (int64_t m = 0; m < s; ++m) {
+        const cplx w = sym_1d(a, k + m * n);
+        acc += w.x * w.x + w.y * w.y;
+      }
+    } else if (layout == AZ_LAYOUT_1D_FOURSTEP) {
+      const int64_t k1 = k / N2, k2 = k % N2;
+      for (int64_t m = 0; m < s; ++m) {
+        const cplx w = sym_1d(a, k1 * L2 + k2 + m * N2);
+        acc += w.x * w.x + w.y * w.y;
+      }
+    } else {
+      const int64_t kx = k / n, ky = k % n;
+      for (int64_t mx = 0; mx < s; ++mx)
+        for (int64_t my = 0; my < s; ++my) {
+          const cplx w = sym_2d(a, kx + mx * n, ky + my * n);
+          acc += w.x * w.x + w.y * w.y;
+        }
+    }
+    sig2[k] = acc;
+  }
+  // block max
+  __shared__ double red[256];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomic_max_pos(smax, red[0]);
+}
+
+// Thresholded pseudo-inverse weight (PAPER.md:190-209 + the eigenvalue threshold):
+// zinv(k) = 1/sigma^2(k) if sigma(k) > rcond * sigma_max else 0.
+__global__ void k_zinv(double* zinv, const double* sig2, int64_t N, const double* smax, double rcond,
+                       unsigned long long* ndrop, double* smin) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  const double thr = rcond * rcond * (*smax);
+  const double v = sig2[k];
+  if (v > thr && v > 0.0) {
+    zinv[k] = 1.0 / v;
+    atomic_min_pos(smin, v);
+  } else {
+    zinv[k] = 0.0;
+    atomicAdd(ndrop, 1ull);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// plan create / destroy / query
+// ---------------------------------------------------------------------------------------
+static bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+static int ilog2(int64_t v) { int k = 0; while ((int64_t(1) << k) < v) ++k; return k; }
+
+static void plan_free(az_plan_s* p) {
+  if (!p) return;
+  void* ptrs[] = {p->d_mask, p->d_pos, p->d_W0, p->d_W2, p->d_zinv, p->d_tw, p->d_tw4hi,
+                  p->d_tw4lo, p->d_bxy, p->d_C1, p->d_G, p->d_solve_ws};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  if (p->h_stage) cudaFreeHost(p->h_stage);
+  delete p;
+}
+
+template <class T>
+static az_status_t dalloc(T** ptr, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)ptr, count * sizeof(T));
+  if (e != cudaSuccess) {
+    az_set_error("cudaMalloc(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+    return AZ_ERR_OUT_OF_MEMORY;
+  }
+  return AZ_OK;
+}
+
+static az_status_t plan_build(az_plan_s* p, const az_plan_desc_t* d, cudaStream_t st) {
+  // ---- mask -> row index map (pos) ----
+  std::vector<int32_t> pos(p->G);
+  int64_t M = 0;
+  for (int64_t g = 0; g < p->G; ++g) pos[g] = d->mask[g] ? (int32_t)(M++) : -1;
+  p->M = M;
+  if (p->M + p->Mb <= p->N) {
+    az_set_error("oversampling insufficient: M + Mb = %lld <= N = %lld (PAPER.md:124)",
+                 (long long)(p->M + p->Mb), (long long)p->N);
+    return AZ_ERR_OVERSAMPLING;
+  }
+  AZ_TRY(dalloc(&p->d_mask, p->G));
+  AZ_TRY(dalloc(&p->d_pos, p->G));
+  AZ_CUDA_CHECK(cudaMemcpyAsync(p->d_mask, d->mask, p->G, cudaMemcpyHostToDevice, st));
+  AZ_CUDA_CHECK(cudaMemcpyAsync(p->d_pos, pos.data(), p->G * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  if (p->Mb) {
+    AZ_TRY(dalloc(&p->d_bxy, p->Mb * 2));
+    AZ_CUDA_CHECK(cudaMemcpyAsync(p->d_bxy, d->boundary_xy, p->Mb * 2 * sizeof(double),
+                                  cudaMemcpyHostToDevice, st));
+  }
+  // ---- twiddles ----
+  AZ_TRY(dalloc(&p->d_tw, TWN));
+  int nhi = 0, nlo = 0;
+  if (p->layout == AZ_LAYOUT_1D_FOURSTEP) {
+    nlo = 1 << TW4B;
+    nhi = (int)((p->L + nlo - 1) >> TW4B);
+    AZ_TRY(dalloc(&p->d_tw4hi, nhi));
+    AZ_TRY(dalloc(&p->d_tw4lo, nlo));
+  }
+  {
+    const int64_t cnt = std::max<int64_t>(TWN, std::max(nhi, nlo));
+    k_twiddles<<<az_div_up(cnt, 256), 256, 0, st>>>(p->d_tw, TWN, p->d_tw4hi, p->d_tw4lo, p->L, nhi, nlo);
+    AZ_LAUNCH_CHECK();
+  }
+  // ---- symbol tables: fine-grid kernel samples and their DFT (Lemma 3) ----
+  const double hL = 2.0 * p->T / (double)p->L;
+  const int lap = p->op == AZ_ROW_LAPLACIAN;
+  AZ_TRY(dalloc(&p->d_W0, p->L));
+  if (lap) AZ_TRY(dalloc(&p->d_W2, p->L));
+  for (int order = 0; order <= (lap ? 2 : 0); order += 2) {
+    cplx* W = order == 0 ? p->d_W0 : p->d_W2;
+    k_samples<<<az_div_up(p->L, 256), 256, 0, st>>>(W, p->L, hL, p->eps, p->T, order);
+    AZ_LAUNCH_CHECK();
+    if (p->layout == AZ_LAYOUT_1D_FOURSTEP)
+      AZ_TRY(az1f_fft_fine_forward(p, W, st));
+    else
+      AZ_TRY(az_fft_batch(p->d_tw, W, p->L, 1, -1, st));
+  }
+  // ---- sigma^2, max, thresholded inverse ----
+  double* d_sig2;
+  double* d_red;   // [0] smax, [1] smin, [2] ndrop (as u64)
+  AZ_TRY(dalloc(&p->d_zinv, p->N));
+  AZ_TRY(dalloc(&d_sig2, p->N));
+  AZ_TRY(dalloc(&d_red, 3));
+  double init[3] = {0.0, INFINITY, 0.0};
+  unsigned long long z = 0;
+  memcpy(&init[2], &z, sizeof(z));
+  AZ_CUDA_CHECK(cudaMemcpyAsync(d_red, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  SymArgs a{p->d_W0, p->d_W2, lap, p->alpha};
+  k_sigma2<<<az_div_up(p->N, 256), 256, 0, st>>>(d_sig2, d_red, a, p->layout, p->n, p->s, p->N1, p->N2, p->L2);
+  AZ_LAUNCH_CHECK();
+  k_zinv<<<az_div_up(p->N, 256), 256, 0, st>>>(p->d_zinv, d_sig2, p->N, d_red, p->rcond,
+                                               (unsigned long long*)(d_red + 2), d_red + 1);
+  AZ_LAUNCH_CHECK();
+  double out[3];
+  AZ_CUDA_CHECK(cudaMemcpyAsync(out, d_red, sizeof(out), cudaMemcpyDeviceToHost, st));
+  AZ_CUDA_CHECK(cudaStreamSynchronize(st));
+  cudaFree(d_sig2);
+  cudaFree(d_red);
+  unsigned long long nd;
+  memcpy(&nd, &out[2], sizeof(nd));
+  p->sigma_max2 = out[0];
+  p->sigma_min_kept2 = out[1];
+  p->n_dropped = (int64_t)nd;
+  if (!(p->sigma_max2 > 0.0)) {
+    az_set_error("singular symbol: max sigma = 0");
+    return AZ_ERR_SINGULAR_SYMBOL;
+  }
+  // ---- scratch for the multi-pass layouts ----
+  if (p->layout != AZ_LAYOUT_1D_SMALL) {
+    const int64_t per_pair = (p->G + p->N) * (int64_t)sizeof(cplx);
+    int64_t B = (int64_t)(256ll << 20) / per_pair;
+    B = std::max<int64_t>(1, std::min<int64_t>(B, 32));
+    p->Bmax = B;
+    AZ_TRY(dalloc(&p->d_C1, B * p->N));
+    AZ_TRY(dalloc(&p->d_G, B * p->G));
+  }
+  return AZ_OK;
+}
+
+extern "C" az_status_t az_plan_create(const az_plan_desc_t* d, void* stream, az_plan_t* out) {
+  AZ_ARG(d && out, "null descriptor or output");
+  *out = nullptr;
+  AZ_ARG(d->dim == 1 || d->dim == 2, "dim must be 1 or 2");
+  AZ_ARG(is_pow2(d->n), "n must be a power of two");
+  AZ_ARG(d->L == 1 || d->L == 2 || d->L == 4, "L (oversampling) must be 1, 2 or 4");
+  AZ_ARG(d->T > 0 && d->eps > 0, "T and eps must be positive");
+  AZ_ARG(d->mask, "mask is required");
+  AZ_ARG(d->op == AZ_ROW_VALUE || d->op == AZ_ROW_LAPLACIAN, "unknown row op");
+  AZ_ARG(d->n_boundary >= 0, "n_boundary < 0");
+  AZ_ARG(d->n_boundary == 0 || d->boundary_xy, "boundary points missing");
+  AZ_ARG(d->zstar_rcond >= 0 && d->zstar_rcond < 1, "zstar_rcond must be in [0, 1)");
+  const int64_t L = d->n * d->L;
+  if (d->dim == 1) {
+    if (d->n < 16 || d->n > (1 << 21) || d->n_boundary != 0) {
+      az_set_error("1-D: need 16 <= n <= 2^21 and no boundary rows");
+      return AZ_ERR_NOT_SUPPORTED;
+    }
+  } else {
+    if (d->n < 8 || L > 2048) {
+      az_set_error("2-D: need n >= 8 and L*n <= 2048");
+      return AZ_ERR_NOT_SUPPORTED;
+    }
+  }
+  az_plan_s* p = new az_plan_s();
+  p->dim = d->dim;
+  p->n = d->n;
+  p->s = d->L;
+  p->L = L;
+  p->N = d->dim == 1 ? d->n : d->n * d->n;
+  p->G = d->dim == 1 ? L : L * L;
+  p->Mb = d->n_boundary;
+  p->T = d->T;
+  p->eps = d->eps;
+  p->alpha = d->op == AZ_ROW_LAPLACIAN ? d->row_scale : 1.0;
+  p->beta = d->boundary_weight;
+  p->rcond = d->zstar_rcond;
+  p->seed = d->seed;
+  p->op = d->op;
+  if (d->dim == 2) {
+    p->layout = AZ_LAYOUT_2D;
+  } else if (L <= 2048) {
+    p->layout = AZ_LAYOUT_1D_SMALL;
+  } else {
+    p->layout = AZ_LAYOUT_1D_FOURSTEP;
+    const int k = ilog2(d->n);
+    p->N1 = int64_t(1) << ((k + 1) / 2);
+    p->N2 = d->n / p->N1;
+    p->L2 = p->N2 * p->s;
+    if (p->L2 > 2048 || p->N1 > 2048 || p->N2 < 8 || p->N1 < 8) {
+      delete p;
+      az_set_error("1-D four-step: unsupported factorisation");
+      return AZ_ERR_NOT_SUPPORTED;
+    }
+  }
+  az_status_t s = plan_build(p, d, (cudaStream_t)stream);
+  if (s != AZ_OK) {
+    plan_free(p);
+    return s;
+  }
+  *out = p;
+  return AZ_OK;
+}
+
+extern "C" az_status_t az_plan_destroy(az_plan_t p) {
+  plan_free(p);
+  return AZ_OK;
+}
+
+extern "C" az_status_t az_plan_query(az_plan_t p, az_plan_info_t* info) {
+  AZ_ARG(p && info, "null plan or info");
+  // unitary normalisation of Lemma 3: singular values of A^c are sqrt(sigma^2_fine / s^d)
+  // with the fine-grid DFT W.
+  const double sd = p->dim == 1 ? (double)p->s : (double)(p->s * p->s);
+  info->N = p->N;
+  info->M = p->M;
+  info->Mb = p->Mb;
+  info->sigma_max = std::sqrt(p->sigma_max2 / sd);
+  info->sigma_min_kept = std::sqrt(p->sigma_min_kept2 / sd);
+  info->n_dropped = p->n_dropped;
+  info->zstar_norm = 1.0 / info->sigma_min_kept;
+  return AZ_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// operator entry points
+// ---------------------------------------------------------------------------------------
+static az_status_t dispatch(az_plan_s* p, int op, int src, const double* in, int64_t ldin, double* out,
+                            int64_t ldout, int64_t nvec, int64_t col0, cudaStream_t st) {
+  if (nvec == 0) return AZ_OK;
+  switch (p->layout) {
+    case AZ_LAYOUT_1D_SMALL: return az1s_apply(p, op, src, in, ldin, out, ldout, nvec, col0, st);
+    case AZ_LAYOUT_1D_FOURSTEP: return az1f_apply(p, op, src, in, ldin, out, ldout, nvec, col0, st);
+    default: return az2_apply(p, op, src, in, ldin, out, ldout, nvec, col0, st);
+  }
+}
+
+static az_status_t check_io(az_plan_s* p, const void* in, int64_t ldin, int64_t rin, const void* out,
+                            int64_t ldout, int64_t rout, int64_t nvec) {
+  AZ_ARG(p, "null plan");
+  AZ_ARG(nvec >= 0, "nvec < 0");
+  if (nvec == 0) return AZ_OK;
+  AZ_ARG(in && out, "null vector pointer");
+  AZ_ARG(ldin >= rin && ldout >= rout, "leading dimension too small (ldin %lld < %lld or ldout %lld < %lld)",
+         (long long)ldin, (long long)rin, (long long)ldout, (long long)rout);
+  return AZ_OK;
+}
+
+extern "C" az_status_t az_apply_A(az_plan_t p, const double* x, int64_t ldx, double* y, int64_t ldy,
+                                  int64_t nvec, void* stream) {
+  AZ_TRY(check_io(p, x, ldx, p ? p->N : 0, y, ldy, p ? p->M + p->Mb : 0, nvec));
+  return dispatch(p, OP_A, SRC_VEC, x, ldx, y, ldy, nvec, 0, (cudaStream_t)stream);
+}
+extern "C" az_status_t az_apply_At(az_plan_t p, const double* y, int64_t ldy, double* x, int64_t ldx,
+                                   int64_t nvec, void* stream) {
+  AZ_TRY(check_io(p, y, ldy, p ? p->M + p->Mb : 0, x, ldx, p ? p->N : 0, nvec));
+  return dispatch(p, OP_AT, SRC_VEC, y, ldy, x, ldx, nvec, 0, (cudaStream_t)stream);
+}
+extern "C" az_status_t az_apply_Zstar(az_plan_t p, const double* y, int64_t ldy, double* x, int64_t ldx,
+                                      int64_t nvec, void* stream) {
+  AZ_TRY(check_io(p, y, ldy, p ? p->M + p->Mb : 0, x, ldx, p ? p->N : 0, nvec));
+  return dispatch(p, OP_ZSTAR, SRC_VEC, y, ldy, x, ldx, nvec, 0, (cudaStream_t)stream);
+}
+extern "C" az_status_t az_apply_step1(az_plan_t p, const double* v, int64_t ldv, double* y, int64_t ldy,
+                                      int64_t nvec, void* stream) {
+  AZ_TRY(check_io(p, v, ldv, p ? p->N : 0, y, ldy, p ? p->M + p->Mb : 0, nvec));
+  return dispatch(p, OP_STEP1, SRC_VEC, v, ldv, y, ldy, nvec, 0, (cudaStream_t)stream);
+}
+extern "C" az_status_t az_apply_resid(az_plan_t p, const double* b, int64_t ldb, double* y, int64_t ldy,
+                                      int64_t nvec, void* stream) {
+  AZ_TRY(check_io(p, b, ldb, p ? p->M + p->Mb : 0, y, ldy, p ? p->M + p->Mb : 0, nvec));
+  AZ_ARG(b != y, "az_apply_resid: in-place (b == y) is not supported");
+  return dispatch(p, OP_RESID, SRC_VEC, b, ldb, y, ldy, nvec, 0, (cudaStream_t)stream);
+}
+extern "C" az_status_t az_sketch(az_plan_t p, int64_t col0, int64_t ncols, double* S, int64_t ldS,
+                                 void* stream) {
+  AZ_ARG(p, "null plan");
+  AZ_ARG(col0 >= 0 && ncols >= 0, "negative column range");
+  if (ncols == 0) return AZ_OK;
+  AZ_ARG(S && ldS >= p->M + p->Mb, "bad S / ldS");
+  return dispatch(p, OP_STEP1, SRC_PROBE, nullptr, 0, S, ldS, ncols, col0, (cudaStream_t)stream);
+}
