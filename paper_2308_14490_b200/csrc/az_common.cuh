@@ -24,8 +24,8 @@ AZ_HD cplx czero() { return make_double2(0.0, 0.0); }
 
 // Shared-memory padding: one 16-byte pad every 8 complex elements makes the Stockham
 // stride-8 writes bank-conflict free (8 lanes x 16 B cover all 32 banks).
-AZ_HD int spad(int i) { return i + (i >> 3); }
-AZ_HD int spad_len(int L) { return L + (L >> 3) + 1; }   // +1 staggers consecutive FFT buffers
+AZ_HD constexpr int spad(int i) { return i + (i >> 3); }
+AZ_HD constexpr int spad_len(int L) { return L + (L >> 3) + 1; }   // +1 staggers consecutive FFT buffers
 
 // --------------------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al. SC'11) and the probe generator.
@@ -124,8 +124,8 @@ inline cudaError_t az_smem_attr(K kernel, size_t bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-#define AZ_TRY(expr)                                                           \
+#define AZ_TRY(...)                                                            \
   do {                                                                         \
-    az_status_t _s = (expr);                                                   \
+    az_status_t _s = (__VA_ARGS__);                                            \
     if (_s != AZ_OK) return _s;                                                \
   } while (0)

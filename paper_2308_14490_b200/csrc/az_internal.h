@@ -41,6 +41,9 @@ struct az_plan_s {
   cplx* d_tw4hi = nullptr;      // four-step twiddles e^{-2 pi i (h 2^TW4B) / L}
   cplx* d_tw4lo = nullptr;      // e^{-2 pi i l / L}
   double* d_bxy = nullptr;      // Mb x 2 boundary points
+  int win = 0;                  // boundary stencil width (centres per axis), <= 64
+  double* d_bw = nullptr;       // Mb x 2 x 64 separable stencil weights phi^per(x_b - c_j)
+  int32_t* d_bj = nullptr;      // Mb x 2 first centre index of the window (mod n on use)
   // scratch for the pass kernels
   int64_t Bmax = 0;             // max vector PAIRS per batch
   cplx* d_C1 = nullptr;         // Bmax * N complex

@@ -4,6 +4,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <vector>
@@ -135,7 +136,25 @@ __global__ void k_samples(cplx* out, int64_t L, double hL, double eps, double T,
   if (q < L) out[q] = make_double2(az_phi_per((double)q * hL, eps, T, order), 0.0);
 }
 
-// Four-step layout of the same samples: natural index x = n1 * L2 + n2 (stored as is).
+// Boundary stencils (CS1 step 6): for boundary point b and axis d, the window of centres
+// j = j0 .. j0 + win - 1 (mod n) around x_b and the weights phi^per(x_b - c_j).
+__global__ void k_stencil(const double* bxy, int64_t Mb, int n, double T, double h, double eps, int win,
+                          double* bw, int32_t* bj) {
+  const int b = blockIdx.x, d = blockIdx.y, t = threadIdx.x;
+  if (b >= Mb) return;
+  const double x = bxy[2 * b + d];
+  const int half = (win - 1) / 2;
+  const int j0 = (int)rint((x + T) / h) - half;
+  if (t == 0) bj[2 * b + d] = j0;
+  if (t < 64) {
+    double w = 0.0;
+    if (t < win) {
+      const int j = ((j0 + t) % n + n) % n;
+      w = az_phi_per(x - (-T + j * h), eps, T, 0);
+    }
+    bw[(2 * b + d) * 64 + t] = w;
+  }
+}
 
 struct SymArgs {
   const cplx* W0;
@@ -224,7 +243,7 @@ static int ilog2(int64_t v) { int k = 0; while ((int64_t(1) << k) < v) ++k; retu
 static void plan_free(az_plan_s* p) {
   if (!p) return;
   void* ptrs[] = {p->d_mask, p->d_pos, p->d_W0, p->d_W2, p->d_zinv, p->d_tw, p->d_tw4hi,
-                  p->d_tw4lo, p->d_bxy, p->d_C1, p->d_G, p->d_solve_ws};
+                  p->d_tw4lo, p->d_bxy, p->d_bw, p->d_bj, p->d_C1, p->d_G, p->d_solve_ws};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->h_stage) cudaFreeHost(p->h_stage);
@@ -261,6 +280,19 @@ static az_status_t plan_build(az_plan_s* p, const az_plan_desc_t* d, cudaStream_
     AZ_TRY(dalloc(&p->d_bxy, p->Mb * 2));
     AZ_CUDA_CHECK(cudaMemcpyAsync(p->d_bxy, d->boundary_xy, p->Mb * 2 * sizeof(double),
                                   cudaMemcpyHostToDevice, st));
+    // phi(r) < e^-40 beyond r = sqrt(40)/eps: window of 2 ceil(sqrt(40)/(eps h)) + 3 centres
+    const double h = 2.0 * p->T / (double)p->n;
+    int half = (int)std::ceil(std::sqrt(40.0) / (p->eps * h)) + 1;
+    p->win = (int)std::min<int64_t>(2 * half + 1, p->n);   // all n centres when the window wraps
+    if (p->win > 64) {
+      az_set_error("boundary stencil wider than 64 centres (eps*h too small)");
+      return AZ_ERR_NOT_SUPPORTED;
+    }
+    AZ_TRY(dalloc(&p->d_bw, p->Mb * 2 * 64));
+    AZ_TRY(dalloc(&p->d_bj, p->Mb * 2));
+    k_stencil<<<dim3((unsigned)p->Mb, 2), 64, 0, st>>>(p->d_bxy, p->Mb, (int)p->n, p->T, h, p->eps, p->win,
+                                                      p->d_bw, p->d_bj);
+    AZ_LAUNCH_CHECK();
   }
   // ---- twiddles ----
   AZ_TRY(dalloc(&p->d_tw, TWN));
@@ -351,8 +383,8 @@ extern "C" az_status_t az_plan_create(const az_plan_desc_t* d, void* stream, az_
       return AZ_ERR_NOT_SUPPORTED;
     }
   } else {
-    if (d->n < 8 || L > 2048) {
-      az_set_error("2-D: need n >= 8 and L*n <= 2048");
+    if (d->n < 8 || L > 2048 || d->L != 2) {
+      az_set_error("2-D: need n >= 8, L = 2 and L*n <= 2048");
       return AZ_ERR_NOT_SUPPORTED;
     }
   }
