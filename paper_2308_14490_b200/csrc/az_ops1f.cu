@@ -1,0 +1,397 @@
+// 1-D operators for large n (c2: n = 2^20, fine grid L = 2^21) with the four-step layout.
+//
+// Coefficient vector x[n1 N2 + n2] is an N1 x N2 row-major matrix, the fine grid an N1 x L2 one
+// (L2 = s N2).  A length-n DFT is: column FFTs (length N1, along n1), twiddle e^{-2 pi i n2 k1/n},
+// row FFTs (length N2) -> spectrum X[k1][k2] at frequency k = k1 + N1 k2 ("transposed order").
+// The fine spectrum is kept in the same order, kf = k1 + N1 k2', so the s aliases k + m n of a
+// coefficient frequency sit in the SAME row k1 (k2' = k2 + m N2): expansion and folding are
+// row-local and no transpose pass is ever needed.  W and zinv are stored in these orders.
+//
+// Passes (one kernel each, over a batch of vector pairs packed as complex):
+//   C1  cols (N1):  coefficient input -> FFT_N1 -> twiddle                    -> C1 buffer
+//   R2  rows:       FFT_N2 -> [keep v^] -> expand x W/L -> IFFT_L2 -> twiddle   -> G
+//   C3  cols (N1):  IFFT_N1 -> E R (mask) -> FFT_N1 -> twiddle                -> G
+//   R4  rows:       FFT_L2 -> fold conj(W) x zinv -> (r^ = v^ - w^) -> expand -> IFFT_L2 -> twiddle
+//                   (Z*, A^T: fold -> IFFT_N2 -> twiddle -> C1)
+//   C5  cols (N1):  IFFT_N1 -> R (gather rows) [b - . for I - A Z*]
+//   Z1  cols (N1):  E (scatter rows) -> FFT_N1 -> twiddle                     -> G
+//   Z3  cols (N1):  IFFT_N1 -> coefficient output
+#include <algorithm>
+
+#include "az_fft.cuh"
+#include "az_internal.h"
+
+struct P1f {
+  const cplx* W0;
+  const cplx* W2;
+  const double* zinv;
+  const int32_t* pos;
+  const uint8_t* mask;
+  const cplx* tw;
+  const cplx* t4hi;
+  const cplx* t4lo;
+  int lap;
+  double alpha;
+  int64_t n, L;
+  int N1, N2, L2, s;
+  int64_t M;
+  uint64_t seed;
+  cplx* C1;
+  cplx* G;
+  const double* in;
+  int64_t ldin;
+  double* out;
+  int64_t ldout;
+  int64_t nvec, col0, pair0;
+};
+
+AZ_D cplx sym1f(const P1f& a, int64_t idx) { return a.lap ? cscale(a.W2[idx], a.alpha) : a.W0[idx]; }
+
+// e^{DIR 2 pi i t / L} for t in [0, L)
+template <int DIR>
+AZ_D cplx tw4(const P1f& a, int64_t t) {
+  cplx w = cmul(__ldg(&a.t4hi[t >> TW4B]), __ldg(&a.t4lo[t & ((1 << TW4B) - 1)]));
+  if (DIR > 0) w.y = -w.y;
+  return w;
+}
+
+struct Cols1 {
+  int64_t cre, cim;
+  bool has_im;
+};
+AZ_D Cols1 pcols(const P1f& a, int b) {
+  Cols1 c;
+  c.cre = 2 * (a.pair0 + b);
+  c.cim = c.cre + 1;
+  c.has_im = c.cim < a.nvec;
+  return c;
+}
+
+// ------------------------------------------------------------------------------------------
+// column passes: a CTA owns TC adjacent columns of an N1-row matrix
+// ------------------------------------------------------------------------------------------
+enum { FC_IN_COEF = 0, FC_FINE_MASK = 1, FC_OUT_GATHER = 2, FC_OUT_RESID = 3, FC_IN_ROWS = 4, FC_OUT_COEF = 5,
+       FC_FWD_G = 6 };
+
+template <int NC, int TC, int KIND, int SRC>
+__global__ void __launch_bounds__(TC * NC / 8) k1f_cols(P1f a, double cout) {
+  extern __shared__ cplx sm[];
+  constexpr int TPF = NC / 8;
+  constexpr int PL = spad_len(NC);
+  constexpr int NT = TC * TPF;
+  const int tid = threadIdx.x, f = tid / TPF, j = tid % TPF;
+  const int b = blockIdx.y;
+  const int c0 = blockIdx.x * TC;
+  const Cols1 cc = pcols(a, b);
+  const bool coef = (KIND == FC_IN_COEF || KIND == FC_OUT_COEF);
+  const int W = coef ? a.N2 : a.L2;                    // row length of the matrix
+  cplx* C1b = a.C1 + (int64_t)b * a.n;
+  cplx* Gb = a.G + (int64_t)b * a.L;
+  // twiddle period and the scale of the column index in it
+  const int64_t tmul = coef ? a.s : 1;                 // e^{-2 pi i n2 k1 / n} = e^{-2 pi i (s n2 k1) / L}
+
+  // ---- load ----
+  if constexpr (KIND == FC_IN_COEF) {
+    if constexpr (SRC == SRC_PROBE) {
+      for (int e = tid; e < NC * TC / 2; e += NT) {
+        const int row = e / (TC / 2), c = 2 * (e % (TC / 2));
+        const int64_t i = (int64_t)row * W + c0 + c;       // even natural index
+        const cpair pr = probe_cplx_pair((uint64_t)(i >> 1), (uint64_t)(a.col0 + cc.cre), (uint64_t)(a.col0 + cc.cim),
+                                         cc.has_im, a.seed);
+        sm[c * PL + spad(row)] = pr.a;
+        sm[(c + 1) * PL + spad(row)] = pr.b;
+      }
+    } else {
+      for (int e = tid; e < NC * TC; e += NT) {
+        const int row = e / TC, c = e % TC;
+        const int64_t i = (int64_t)row * W + c0 + c;
+        sm[c * PL + spad(row)] = make_double2(a.in[i + cc.cre * a.ldin], cc.has_im ? a.in[i + cc.cim * a.ldin] : 0.0);
+      }
+    }
+  } else if constexpr (KIND == FC_IN_ROWS) {
+    for (int e = tid; e < NC * TC; e += NT) {
+      const int row = e / TC, c = e % TC;
+      const int r = a.pos[(int64_t)row * W + c0 + c];
+      cplx v = czero();
+      if (r >= 0) v = make_double2(a.in[r + cc.cre * a.ldin], cc.has_im ? a.in[r + cc.cim * a.ldin] : 0.0);
+      sm[c * PL + spad(row)] = v;
+    }
+  } else {
+    const cplx* src = coef ? C1b : Gb;
+    for (int e = tid; e < NC * TC; e += NT) {
+      const int row = e / TC, c = e % TC;
+      sm[c * PL + spad(row)] = src[(int64_t)row * W + c0 + c];
+    }
+  }
+  __syncthreads();
+  cplx* buf = sm + f * PL;
+
+  // ---- transforms ----
+  if constexpr (KIND == FC_IN_COEF || KIND == FC_IN_ROWS || KIND == FC_FWD_G) {
+    fft_smem<NC, -1>(buf, j, a.tw, TWN);
+  } else if constexpr (KIND == FC_FINE_MASK) {
+    fft_smem<NC, 1>(buf, j, a.tw, TWN);
+    for (int e = tid; e < NC * TC; e += NT) {
+      const int row = e / TC, c = e % TC;
+      if (!a.mask[(int64_t)row * W + c0 + c]) sm[c * PL + spad(row)] = czero();
+    }
+    __syncthreads();
+    fft_smem<NC, -1>(buf, j, a.tw, TWN);
+  } else {
+    fft_smem<NC, 1>(buf, j, a.tw, TWN);
+  }
+
+  // ---- store ----
+  if constexpr (KIND == FC_IN_COEF || KIND == FC_IN_ROWS || KIND == FC_FINE_MASK || KIND == FC_FWD_G) {
+    cplx* dst = (KIND == FC_IN_COEF) ? C1b : Gb;
+    for (int e = tid; e < NC * TC; e += NT) {
+      const int k1 = e / TC, c = e % TC;
+      const int64_t t = ((int64_t)k1 * (c0 + c) * tmul) % a.L;
+      dst[(int64_t)k1 * W + c0 + c] = cmul(sm[c * PL + spad(k1)], tw4<-1>(a, t));
+    }
+  } else if constexpr (KIND == FC_OUT_GATHER || KIND == FC_OUT_RESID) {
+    for (int e = tid; e < NC * TC; e += NT) {
+      const int row = e / TC, c = e % TC;
+      const int r = a.pos[(int64_t)row * W + c0 + c];
+      if (r >= 0) {
+        const cplx v = sm[c * PL + spad(row)];
+        if constexpr (KIND == FC_OUT_RESID) {
+          a.out[r + cc.cre * a.ldout] = a.in[r + cc.cre * a.ldin] - v.x;
+          if (cc.has_im) a.out[r + cc.cim * a.ldout] = a.in[r + cc.cim * a.ldin] - v.y;
+        } else {
+          a.out[r + cc.cre * a.ldout] = v.x;
+          if (cc.has_im) a.out[r + cc.cim * a.ldout] = v.y;
+        }
+      }
+    }
+  } else {   // FC_OUT_COEF
+    for (int e = tid; e < NC * TC; e += NT) {
+      const int row = e / TC, c = e % TC;
+      const int64_t i = (int64_t)row * W + c0 + c;
+      const cplx v = sm[c * PL + spad(row)];
+      a.out[i + cc.cre * a.ldout] = v.x * cout;
+      if (cc.has_im) a.out[i + cc.cim * a.ldout] = v.y * cout;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// row passes: a CTA owns RPC rows k1; threads per row = NR2/8 (NR2 = N2), L2-FFTs use V = s.
+// ------------------------------------------------------------------------------------------
+enum { FR_EXPAND = 0, FR_EXPAND_KEEP = 1, FR_STEP1 = 2, FR_RESID = 3, FR_ZSTAR = 4, FR_AT = 5 };
+
+template <int NR2, int LR2, int RPC, int KIND>
+__global__ void __launch_bounds__(RPC * NR2 / 8) k1f_rows(P1f a, int nrows) {
+  extern __shared__ cplx sm[];
+  constexpr int TPF = NR2 / 8;
+  constexpr int PLN = spad_len(NR2), PLL = spad_len(LR2);
+  constexpr int S = LR2 / NR2;
+  const int f = threadIdx.x / TPF, j = threadIdx.x % TPF;
+  const int k1 = blockIdx.x * RPC + f;
+  const bool live = k1 < nrows;
+  const int b = blockIdx.y;
+  cplx* bN = sm + f * (PLN + PLL);
+  cplx* bL = bN + PLN;
+  cplx* C1b = a.C1 + (int64_t)b * a.n;
+  cplx* Gb = a.G + (int64_t)b * a.L;
+  const double invL = 1.0 / (double)a.L;
+  const int64_t rowW = (int64_t)k1 * LR2;             // row offset in W / G
+  const int64_t rowC = (int64_t)k1 * NR2;             // row offset in C1 / zinv
+
+  if constexpr (KIND == FR_EXPAND || KIND == FR_EXPAND_KEEP) {
+    for (int e = j; e < NR2; e += TPF) bN[spad(e)] = live ? C1b[rowC + e] : czero();
+    __syncthreads();
+    fft_smem<NR2, -1>(bN, j, a.tw, TWN);
+    if (KIND == FR_EXPAND_KEEP && live)
+      for (int e = j; e < NR2; e += TPF) C1b[rowC + e] = bN[spad(e)];
+  } else {
+    for (int e = j; e < LR2; e += TPF) bL[spad(e)] = live ? Gb[rowW + e] : czero();
+    __syncthreads();
+    fft_smem<LR2, -1, TPF>(bL, j, a.tw, TWN);
+    for (int k2 = j; k2 < NR2; k2 += TPF) {
+      cplx acc = czero();
+      if (live) {
+#pragma unroll
+        for (int m = 0; m < S; ++m) acc = cadd(acc, cmulc(bL[spad(k2 + m * NR2)], sym1f(a, rowW + k2 + m * NR2)));
+        if (KIND != FR_AT) acc = cscale(acc, a.zinv[rowC + k2]);
+        if (KIND == FR_STEP1) acc = csub(C1b[rowC + k2], acc);
+      }
+      bN[spad(k2)] = acc;
+    }
+    __syncthreads();
+  }
+  if constexpr (KIND == FR_ZSTAR || KIND == FR_AT) {
+    fft_smem<NR2, 1>(bN, j, a.tw, TWN);
+    if (live)
+      for (int n2 = j; n2 < NR2; n2 += TPF) {
+        const int64_t t = ((int64_t)n2 * k1 * S) % a.L;     // e^{+2 pi i n2 k1 / n}
+        C1b[rowC + n2] = cmul(bN[spad(n2)], tw4<1>(a, t));
+      }
+  } else {
+    for (int e = j; e < LR2; e += TPF) bL[spad(e)] = cscale(cmul(bN[spad(e & (NR2 - 1))], sym1f(a, rowW + e)), invL);
+    __syncthreads();
+    fft_smem<LR2, 1, TPF>(bL, j, a.tw, TWN);
+    if (live)
+      for (int n2 = j; n2 < LR2; n2 += TPF) {
+        const int64_t t = ((int64_t)n2 * k1) % a.L;          // e^{+2 pi i n2' k1 / L}
+        Gb[rowW + n2] = cmul(bL[spad(n2)], tw4<1>(a, t));
+      }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// host orchestration
+// ------------------------------------------------------------------------------------------
+template <int NC, int KIND, int SRC>
+static az_status_t fcols(const P1f& a, int ncols, int nb, double cout, cudaStream_t st) {
+  constexpr int TC0 = 4096 / NC;
+  constexpr int TC = TC0 < 2 ? 2 : (TC0 > 16 ? 16 : TC0);
+  const size_t sm = (size_t)TC * spad_len(NC) * sizeof(cplx);
+  auto kern = k1f_cols<NC, TC, KIND, SRC>;
+  AZ_CUDA_CHECK(az_smem_attr(kern, sm));
+  kern<<<dim3(az_div_up(ncols, TC), nb), TC * NC / 8, sm, st>>>(a, cout);
+  AZ_LAUNCH_CHECK();
+  return AZ_OK;
+}
+
+template <int NR2, int KIND>
+static az_status_t frows(const P1f& a, int nb, cudaStream_t st) {
+  constexpr int LR2 = 2 * NR2;
+  constexpr int RPC0 = 2048 / NR2;
+  constexpr int RPC = RPC0 < 1 ? 1 : (RPC0 > 32 ? 32 : RPC0);
+  const size_t sm = (size_t)RPC * (spad_len(NR2) + spad_len(LR2)) * sizeof(cplx);
+  auto kern = k1f_rows<NR2, LR2, RPC, KIND>;
+  AZ_CUDA_CHECK(az_smem_attr(kern, sm));
+  kern<<<dim3(az_div_up(a.N1, RPC), nb), RPC * NR2 / 8, sm, st>>>(a, a.N1);
+  AZ_LAUNCH_CHECK();
+  return AZ_OK;
+}
+
+template <int NC, int NR2>
+static az_status_t run1f(const P1f& a0, int op, int src, int64_t npairs, int64_t Bmax, cudaStream_t st) {
+  const int N2 = NR2, L2 = 2 * NR2;
+  for (int64_t p0 = 0; p0 < npairs; p0 += Bmax) {
+    P1f a = a0;
+    a.pair0 = p0;
+    const int nb = (int)std::min<int64_t>(Bmax, npairs - p0);
+    switch (op) {
+      case OP_A:
+        AZ_TRY(fcols<NC, FC_IN_COEF, SRC_VEC>(a, N2, nb, 1.0, st));
+        AZ_TRY(frows<NR2, FR_EXPAND>(a, nb, st));
+        AZ_TRY(fcols<NC, FC_OUT_GATHER, SRC_VEC>(a, L2, nb, 1.0, st));
+        break;
+      case OP_STEP1:
+        if (src == SRC_PROBE)
+          AZ_TRY(fcols<NC, FC_IN_COEF, SRC_PROBE>(a, N2, nb, 1.0, st));
+        else
+          AZ_TRY(fcols<NC, FC_IN_COEF, SRC_VEC>(a, N2, nb, 1.0, st));
+        AZ_TRY(frows<NR2, FR_EXPAND_KEEP>(a, nb, st));
+        AZ_TRY(fcols<NC, FC_FINE_MASK, SRC_VEC>(a, L2, nb, 1.0, st));
+        AZ_TRY(frows<NR2, FR_STEP1>(a, nb, st));
+        AZ_TRY(fcols<NC, FC_OUT_GATHER, SRC_VEC>(a, L2, nb, 1.0, st));
+        break;
+      case OP_RESID:
+        AZ_TRY(fcols<NC, FC_IN_ROWS, SRC_VEC>(a, L2, nb, 1.0, st));
+        AZ_TRY(frows<NR2, FR_RESID>(a, nb, st));
+        AZ_TRY(fcols<NC, FC_OUT_RESID, SRC_VEC>(a, L2, nb, 1.0, st));
+        break;
+      case OP_ZSTAR:
+        AZ_TRY(fcols<NC, FC_IN_ROWS, SRC_VEC>(a, L2, nb, 1.0, st));
+        AZ_TRY(frows<NR2, FR_ZSTAR>(a, nb, st));
+        AZ_TRY(fcols<NC, FC_OUT_COEF, SRC_VEC>(a, N2, nb, 1.0 / (double)a.n, st));
+        break;
+      case OP_AT:
+        AZ_TRY(fcols<NC, FC_IN_ROWS, SRC_VEC>(a, L2, nb, 1.0, st));
+        AZ_TRY(frows<NR2, FR_AT>(a, nb, st));
+        AZ_TRY(fcols<NC, FC_OUT_COEF, SRC_VEC>(a, N2, nb, 1.0 / (double)a.L, st));
+        break;
+    }
+  }
+  return AZ_OK;
+}
+
+static P1f make_p1f(az_plan_s* p) {
+  P1f a;
+  a.W0 = p->d_W0;
+  a.W2 = p->d_W2;
+  a.zinv = p->d_zinv;
+  a.pos = p->d_pos;
+  a.mask = p->d_mask;
+  a.tw = p->d_tw;
+  a.t4hi = p->d_tw4hi;
+  a.t4lo = p->d_tw4lo;
+  a.lap = p->op == AZ_ROW_LAPLACIAN;
+  a.alpha = p->alpha;
+  a.n = p->n;
+  a.L = p->L;
+  a.N1 = (int)p->N1;
+  a.N2 = (int)p->N2;
+  a.L2 = (int)p->L2;
+  a.s = (int)p->s;
+  a.M = p->M;
+  a.seed = p->seed;
+  a.C1 = p->d_C1;
+  a.G = p->d_G;
+  a.in = nullptr;
+  a.out = nullptr;
+  a.ldin = a.ldout = 0;
+  a.nvec = a.col0 = a.pair0 = 0;
+  return a;
+}
+
+#define AZ_1F_DISPATCH(FN, ...)                                                        \
+  switch (p->N1 * 4096 + p->N2) {                                                      \
+    case 64 * 4096 + 32: return FN<64, 32>(__VA_ARGS__);                               \
+    case 128 * 4096 + 64: return FN<128, 64>(__VA_ARGS__);                             \
+    case 256 * 4096 + 128: return FN<256, 128>(__VA_ARGS__);                           \
+    case 512 * 4096 + 256: return FN<512, 256>(__VA_ARGS__);                           \
+    case 1024 * 4096 + 512: return FN<1024, 512>(__VA_ARGS__);                         \
+    case 2048 * 4096 + 1024: return FN<2048, 1024>(__VA_ARGS__);                       \
+    case 64 * 4096 + 64: return FN<64, 64>(__VA_ARGS__);                               \
+    case 128 * 4096 + 128: return FN<128, 128>(__VA_ARGS__);                           \
+    case 256 * 4096 + 256: return FN<256, 256>(__VA_ARGS__);                           \
+    case 512 * 4096 + 512: return FN<512, 512>(__VA_ARGS__);                           \
+    case 1024 * 4096 + 1024: return FN<1024, 1024>(__VA_ARGS__);                       \
+  }                                                                                    \
+  az_set_error("four-step: unsupported N1 x N2 = %lld x %lld", (long long)p->N1, (long long)p->N2); \
+  return AZ_ERR_NOT_SUPPORTED;
+
+az_status_t az1f_apply(az_plan_s* p, int op, int src, const double* in, int64_t ldin, double* out,
+                       int64_t ldout, int64_t nvec, int64_t col0, cudaStream_t st) {
+  if (p->s != 2) {
+    az_set_error("four-step layout supports L = 2 only");
+    return AZ_ERR_NOT_SUPPORTED;
+  }
+  P1f a = make_p1f(p);
+  a.in = in;
+  a.ldin = ldin;
+  a.out = out;
+  a.ldout = ldout;
+  a.nvec = nvec;
+  a.col0 = col0;
+  const int64_t npairs = (nvec + 1) / 2;
+  AZ_1F_DISPATCH(run1f, a, op, src, npairs, p->Bmax, st)
+}
+
+// Forward length-L DFT of the fine-grid samples stored in natural order, result in the
+// transposed four-step order [k1][k2'] (the symbol table W, step 0).
+__global__ void k1f_copy(cplx* dst, const cplx* src, int64_t L) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < L) dst[i] = src[i];
+}
+
+template <int NC, int NR2>
+static az_status_t fine_forward(az_plan_s* p, cplx* W, cudaStream_t st) {
+  P1f a = make_p1f(p);
+  k1f_copy<<<az_div_up(p->L, 256), 256, 0, st>>>(a.G, W, p->L);
+  AZ_LAUNCH_CHECK();
+  AZ_TRY(fcols<NC, FC_FWD_G, SRC_VEC>(a, 2 * NR2, 1, 1.0, st));      // FFT_N1 + twiddle
+  AZ_TRY(az_fft_batch(p->d_tw, a.G, 2 * NR2, p->N1, -1, st));        // FFT_L2 along rows
+  k1f_copy<<<az_div_up(p->L, 256), 256, 0, st>>>(W, a.G, p->L);
+  AZ_LAUNCH_CHECK();
+  return AZ_OK;
+}
+
+az_status_t az1f_fft_fine_forward(az_plan_s* p, cplx* W, cudaStream_t st) {
+  AZ_1F_DISPATCH(fine_forward, p, W, st)
+}

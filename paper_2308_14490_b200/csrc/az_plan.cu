@@ -308,6 +308,15 @@ static az_status_t plan_build(az_plan_s* p, const az_plan_desc_t* d, cudaStream_
     k_twiddles<<<az_div_up(cnt, 256), 256, 0, st>>>(p->d_tw, TWN, p->d_tw4hi, p->d_tw4lo, p->L, nhi, nlo);
     AZ_LAUNCH_CHECK();
   }
+  // ---- scratch for the multi-pass layouts ----
+  if (p->layout != AZ_LAYOUT_1D_SMALL) {
+    const int64_t per_pair = (p->G + p->N) * (int64_t)sizeof(cplx);
+    int64_t B = (int64_t)(256ll << 20) / per_pair;
+    B = std::max<int64_t>(1, std::min<int64_t>(B, 32));
+    p->Bmax = B;
+    AZ_TRY(dalloc(&p->d_C1, B * p->N));
+    AZ_TRY(dalloc(&p->d_G, B * p->G));
+  }
   // ---- symbol tables: fine-grid kernel samples and their DFT (Lemma 3) ----
   const double hL = 2.0 * p->T / (double)p->L;
   const int lap = p->op == AZ_ROW_LAPLACIAN;
@@ -351,15 +360,6 @@ static az_status_t plan_build(az_plan_s* p, const az_plan_desc_t* d, cudaStream_
   if (!(p->sigma_max2 > 0.0)) {
     az_set_error("singular symbol: max sigma = 0");
     return AZ_ERR_SINGULAR_SYMBOL;
-  }
-  // ---- scratch for the multi-pass layouts ----
-  if (p->layout != AZ_LAYOUT_1D_SMALL) {
-    const int64_t per_pair = (p->G + p->N) * (int64_t)sizeof(cplx);
-    int64_t B = (int64_t)(256ll << 20) / per_pair;
-    B = std::max<int64_t>(1, std::min<int64_t>(B, 32));
-    p->Bmax = B;
-    AZ_TRY(dalloc(&p->d_C1, B * p->N));
-    AZ_TRY(dalloc(&p->d_G, B * p->G));
   }
   return AZ_OK;
 }

@@ -1,8 +1,5 @@
 // Temporary stubs (replaced as the layouts land).
 #include "az_internal.h"
-az_status_t az1f_apply(az_plan_s*, int, int, const double*, int64_t, double*, int64_t, int64_t, int64_t, cudaStream_t) {
-  az_set_error("four-step layout not built yet"); return AZ_ERR_NOT_SUPPORTED; }
-az_status_t az1f_fft_fine_forward(az_plan_s*, cplx*, cudaStream_t) { az_set_error("four-step not built"); return AZ_ERR_NOT_SUPPORTED; }
 extern "C" az_status_t az_omega_apply(az_plan_t, int64_t, int64_t, const double*, int64_t, int64_t, double*, int64_t, int, void*) {
   az_set_error("not built yet"); return AZ_ERR_NOT_SUPPORTED; }
 extern "C" az_status_t az_qr_r(az_plan_t, double*, int64_t, int64_t, int64_t, double*, int64_t, void*, size_t, void*) {

@@ -25,6 +25,9 @@ CASES = [
     ("interval_n1024", I.make_config("interval", 1024)),
     ("interval_n256_s4", I.make_config("interval", 256, s=4)),
     ("box1d_n128", I.make_config("box1d", 128)),
+    ("interval_n2048_4step", I.make_config("interval", 2048)),
+    ("interval_n8192_4step", I.make_config("interval", 8192)),
+    ("box1d_n4096_4step", I.make_config("box1d", 4096)),
     ("disk_n8", I.make_config("disk", 8)),
     ("disk_n32", I.make_config("disk", 32)),
     ("star_n16", I.make_config("star", 16)),
@@ -38,7 +41,7 @@ def setup(request):
     from paper_2308_14490_b200.api import Plan
     name, cfg = request.param
     plan = Plan.from_config(cfg)
-    prob = OA.make_problem(cfg, "dense")
+    prob = OA.make_problem(cfg, "dense" if cfg.N <= 2048 else "fft")
     A = OD.assemble_A(cfg)
     return cfg, plan, prob, A
 
@@ -154,3 +157,35 @@ def test_probe_generator_bitwise_reproducible(setup):
     assert torch.equal(s1, s2)
     s3 = plan.sketch(2, 2)       # same global columns -> same values
     assert torch.equal(s1[:, 2:4], s3)
+
+
+@pytest.mark.parametrize("name", ["c2"])
+def test_full_size_sampled_and_normwise(name):
+    """BASELINE full size (c2: n = 2^20, fine grid 2^21) in the bench's launch configuration:
+    sampled rows of A x against the windowed exact row sums, and the composite operators
+    against the FFT oracle normwise."""
+    from paper_2308_14490_b200.api import Plan
+    cfg = I.get_config(name)
+    plan = Plan.from_config(cfg)
+    prob = OA.make_problem(cfg, "fft")
+    rng = np.random.default_rng(0)
+    x = I.gaussian_matrix(cfg.N, 2, 3)
+    y = _host(plan.apply_A(_dev(x)))
+    rows = np.argwhere(I.mask(cfg).reshape(-1)).ravel()
+    for r in rng.choice(plan.M, 64, replace=False):
+        cols, vals = OD.A_row_entries(cfg, rows[r], half_width=40)
+        ref = vals @ x[cols]
+        assert np.all(np.abs(y[r] - ref) <= 1e-12 * np.abs(vals) @ np.abs(x[cols]))
+    ref = prob.apply_A(x)
+    assert _rel(y, ref) <= 1e-12
+    nA = plan.sigma_max
+    S = _host(plan.sketch(0, 4))
+    Om = OP.probes(cfg.N, [0, 1, 2, 3], cfg.seed)
+    refS = OA.step1_apply(prob, Om)
+    for c in range(4):
+        assert np.linalg.norm(S[:, c] - refS[:, c]) <= 1e-12 * nA * nA * plan.zstar_norm * np.linalg.norm(Om[:, c])
+    b = I.rhs(cfg)[:, :3]
+    z = _host(plan.apply_Zstar(_dev(b)))
+    refz = prob.apply_Zstar(b)
+    for c in range(3):
+        assert np.linalg.norm(z[:, c] - refz[:, c]) <= 1e-12 * plan.zstar_norm * np.linalg.norm(b[:, c])
