@@ -175,8 +175,17 @@ def evaluate(cfg: I.Config, x: np.ndarray, grid: I.TestGrid) -> np.ndarray:
     c = I.center_axis(cfg)
     X = x.reshape(cfg.N, -1)
     if cfg.dim == 1:
-        Phi = periodized(grid.axes[0][:, None] - c[None, :], cfg.eps, cfg.T, 0)
-        return (Phi @ X)[grid.inside]
+        t = grid.axes[0]
+        if cfg.n <= 4096:
+            Phi = periodized(t[:, None] - c[None, :], cfg.eps, cfg.T, 0)
+            return (Phi @ X)[grid.inside]
+        # large n: the sum over centres within +-W of each point (phi^per < 1e-170 beyond W = 40
+        # centres at eps h = 0.5); the omitted terms are below binary64 resolution of the sum
+        W = 40
+        j0 = np.rint((t + cfg.T) / cfg.h).astype(np.int64)
+        js = (j0[:, None] + np.arange(-W, W + 1)[None, :]) % cfg.n
+        Phi = periodized(t[:, None] - c[js], cfg.eps, cfg.T, 0)
+        return np.einsum("pw,pwr->pr", Phi, X[js])[grid.inside]
     Px = periodized(grid.axes[0][:, None] - c[None, :], cfg.eps, cfg.T, 0)
     Py = periodized(grid.axes[1][:, None] - c[None, :], cfg.eps, cfg.T, 0)
     out = []

@@ -461,6 +461,11 @@ static az_status_t dispatch(az_plan_s* p, int op, int src, const double* in, int
   }
 }
 
+az_status_t az_apply_op(az_plan_s* p, int op, const double* in, int64_t ldin, double* out, int64_t ldout,
+                        int64_t nvec, cudaStream_t st) {
+  return dispatch(p, op, SRC_VEC, in, ldin, out, ldout, nvec, 0, st);
+}
+
 static az_status_t check_io(az_plan_s* p, const void* in, int64_t ldin, int64_t rin, const void* out,
                             int64_t ldout, int64_t rout, int64_t nvec) {
   AZ_ARG(p, "null plan");

@@ -1,0 +1,238 @@
+// R factor of a tall matrix by Householder TSQR (the "SVD of an (r+p)-by-M
+// matrix" is computed as QR of the M x (r+p) sketch followed by an SVD of the small R).
+//
+// Stage 1: each CTA streams its contiguous row range through a structured Householder QR of
+// [R; chunk] (R upper triangular, chunk = MC rows held in registers): for column j the
+// reflector is H = I - tau v v^T with v = [e_j ; y] (LAPACK dlarfg convention), applied to the
+// columns l > j of R and of the chunk.  No Q is formed (only R is needed: the right-hand sides
+// ride along as extra columns, so R's last columns hold Q^T b').
+// Stage 2..: the per-CTA R factors are stacked and reduced by the same kernel in groups until
+// one R remains (a fixed-shape reduction tree: the result does not depend on timing).
+//
+// Layout inside a CTA: 16 warps; warp w owns columns l = w + 16 c (c < KC); lane owns rows
+// lane + 32 r (r < RPL) of the chunk.  R lives in shared memory, packed column-major upper
+// triangle; each R column is only ever touched by its owner warp, so the only block-wide
+// barrier per column step is the broadcast of the reflector (double-buffered).
+#include <algorithm>
+
+#include "az_internal.h"
+
+AZ_D int pk(int i, int l) { return (l * (l + 1)) / 2 + i; }   // R[i][l], i <= l
+
+AZ_D double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct QRIn {
+  const double* A;
+  int64_t m;        // rows
+  int k;            // columns
+  int64_t ld;       // column stride
+  int64_t rb;       // rows per block of the stacked input (row r at (r / rb) * bstride + (r % rb))
+  int64_t bstride;
+  int64_t rows_per_cta;
+  double* Rout;     // per CTA k x k column-major (ld = k)
+};
+
+template <int KC, int RPL>
+__global__ void __launch_bounds__(512, 1) k_tsqr(QRIn q) {
+  constexpr int MC = 32 * RPL;
+  extern __shared__ double sm[];
+  const int k = q.k;
+  double* R = sm;                                // k (k+1) / 2
+  double* vb = R + (k * (k + 1)) / 2;            // 2 x MC
+  double* tb = vb + 2 * MC;                      // 2
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < (k * (k + 1)) / 2; i += blockDim.x) R[i] = 0.0;
+  const int64_t r0 = (int64_t)blockIdx.x * q.rows_per_cta;
+  const int64_t r1 = (q.m < r0 + q.rows_per_cta) ? q.m : r0 + q.rows_per_cta;
+  double x[KC][RPL];
+  __syncthreads();
+
+  for (int64_t base = r0; base < r1; base += MC) {
+#pragma unroll
+    for (int c = 0; c < KC; ++c) {
+      const int l = w + 16 * c;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int64_t row = base + lane + 32 * r;
+        double v = 0.0;
+        if (row < r1 && l < k) v = q.A[(row / q.rb) * q.bstride + (row % q.rb) + (int64_t)l * q.ld];
+        x[c][r] = v;
+      }
+    }
+    for (int j = 0; j < k; ++j) {
+      const int o = j & 15, cj = j >> 4;
+      double* vj = vb + (j & 1) * MC;
+      if (w == o) {
+        double xs[RPL];
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) xs[r] = 0.0;
+#pragma unroll
+        for (int c = 0; c < KC; ++c)
+          if (c == cj) {
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) {
+              xs[r] = x[c][r];
+              x[c][r] = 0.0;
+            }
+          }
+        double sig = 0.0;
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) sig = fma(xs[r], xs[r], sig);
+        sig = warp_sum(sig);
+        const double alpha = R[pk(j, j)];
+        double tau = 0.0, scale = 0.0, beta = alpha;
+        if (sig > 0.0) {
+          const double nrm = sqrt(fma(alpha, alpha, sig));
+          beta = alpha >= 0.0 ? -nrm : nrm;
+          tau = (beta - alpha) / beta;
+          scale = 1.0 / (alpha - beta);
+        }
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) vj[lane + 32 * r] = xs[r] * scale;
+        __syncwarp();
+        if (lane == 0) {
+          R[pk(j, j)] = beta;
+          tb[j & 1] = tau;
+        }
+      }
+      __syncthreads();
+      const double tau = tb[j & 1];
+      if (tau != 0.0) {
+        double v[RPL];
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) v[r] = vj[lane + 32 * r];
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {
+          const int l = w + 16 * c;
+          if (l > j && l < k) {
+            double p = 0.0;
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) p = fma(v[r], x[c][r], p);
+            p = warp_sum(p);
+            const double rjl = R[pk(j, l)];
+            const double wv = rjl + p;
+            const double tw = tau * wv;
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) x[c][r] = fma(-tw, v[r], x[c][r]);
+            __syncwarp();
+            if (lane == 0) R[pk(j, l)] = rjl - tw;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  double* Ro = q.Rout + (int64_t)blockIdx.x * k * k;
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    const int i = e % k, l = e / k;
+    Ro[e] = i <= l ? R[pk(i, l)] : 0.0;
+  }
+}
+
+static int g_sms = 0;
+static int num_sms() {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  return g_sms;
+}
+
+template <int KC, int RPL>
+static az_status_t tsqr_launch(const QRIn& q, int nblocks, cudaStream_t st) {
+  constexpr int MC = 32 * RPL;
+  const size_t sm = ((size_t)q.k * (q.k + 1) / 2 + 2 * MC + 2) * sizeof(double);
+  auto kern = k_tsqr<KC, RPL>;
+  AZ_CUDA_CHECK(az_smem_attr(kern, sm));
+  kern<<<nblocks, 512, sm, st>>>(q);
+  AZ_LAUNCH_CHECK();
+  return AZ_OK;
+}
+
+static az_status_t tsqr_pass(const QRIn& q, int nblocks, cudaStream_t st) {
+  if (q.k <= 32) return tsqr_launch<2, 8>(q, nblocks, st);
+  if (q.k <= 64) return tsqr_launch<4, 8>(q, nblocks, st);
+  if (q.k <= 128) return tsqr_launch<8, 4>(q, nblocks, st);
+  az_set_error("tsqr: k = %d > 128 not supported by the single-pass TSQR", q.k);
+  return AZ_ERR_NOT_SUPPORTED;
+}
+
+size_t az_qr_ws_bytes(int64_t m, int64_t k) {
+  const int64_t P = std::max<int64_t>(1, std::min<int64_t>(num_sms(), (m + 127) / 128));
+  return (size_t)(2 * P * k * k) * sizeof(double) + 256;
+}
+
+__global__ void k_copy_R(const double* Rin, int k, double* R, int64_t ldr) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < k * k) R[(e / k) * ldr + (e % k)] = Rin[e];
+}
+
+az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R, int64_t ldr,
+                         void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (k > 128) {
+    az_set_error("az_qr_r: k = %lld > 128 (blocked Householder path not built)", (long long)k);
+    return AZ_ERR_NOT_SUPPORTED;
+  }
+  if (ws_bytes < az_qr_ws_bytes(m, k)) {
+    az_set_error("az_qr_r: workspace too small");
+    return AZ_ERR_WORKSPACE;
+  }
+  const int64_t P = std::max<int64_t>(1, std::min<int64_t>(num_sms(), (m + 127) / 128));
+  double* buf[2] = {(double*)ws, (double*)ws + P * k * k};
+  QRIn q;
+  q.A = A;
+  q.m = m;
+  q.k = (int)k;
+  q.ld = lda;
+  q.rb = m;
+  q.bstride = 0;
+  q.rows_per_cta = (m + P - 1) / P;
+  q.Rout = buf[0];
+  AZ_TRY(tsqr_pass(q, (int)P, st));
+  int64_t cur = P;
+  int which = 0;
+  // fixed-shape reduction tree: groups of 4 R factors
+  while (cur > 1) {
+    const int64_t G = 4;
+    const int64_t next = (cur + G - 1) / G;
+    QRIn t;
+    t.A = buf[which];
+    t.m = cur * k;
+    t.k = (int)k;
+    t.ld = k;
+    t.rb = k;
+    t.bstride = k * k;
+    t.rows_per_cta = G * k;
+    t.Rout = buf[which ^ 1];
+    AZ_TRY(tsqr_pass(t, (int)next, st));
+    which ^= 1;
+    cur = next;
+  }
+  k_copy_R<<<az_div_up(k * k, 256), 256, 0, st>>>(buf[which], (int)k, R, ldr);
+  AZ_LAUNCH_CHECK();
+  return AZ_OK;
+}
+
+extern "C" az_status_t az_qr_workspace_size(int64_t m, int64_t k, size_t* bytes) {
+  if (!bytes || m < 0 || k < 0) {
+    az_set_error("az_qr_workspace_size: bad arguments");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  *bytes = az_qr_ws_bytes(m, k);
+  return AZ_OK;
+}
+
+extern "C" az_status_t az_qr_r(az_plan_t, double* A, int64_t m, int64_t k, int64_t lda, double* R, int64_t ldr,
+                               void* ws, size_t ws_bytes, void* stream) {
+  if (!A || !R || m < 1 || k < 1 || lda < m || ldr < k) {
+    az_set_error("az_qr_r: bad arguments");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  return az_qr_r_impl(A, m, k, lda, R, ldr, ws, ws_bytes, (cudaStream_t)stream);
+}

@@ -1,0 +1,324 @@
+// The AZ solve (Alg. 1) and the probe-regeneration GEMM x = Omega y.
+//
+//   b'  = (I - A Z*) b                                    (az_apply_resid)
+//   S   = (A - A Z* A) Omega, Omega in blocks of R probes (az_sketch, Philox on the fly)
+//   Rf  = R factor of [S | b']                            (TSQR; rows never permuted)
+//   y   = V_k Sigma_k^-1 U_k^T (Q^T b')                   (one-sided Jacobi on R_S)
+//   x2  = Omega y                                         (this file, Omega regenerated)
+//   x   = x2 + Z* (b - A x2)                              (step 2 + step 3)
+// Probe blocks are added while the sketch is saturated, rank > probes - p (p = 10),
+// up to max_blocks (reading R5).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "az_internal.h"
+
+// ------------------------------------------------------------------------------------------
+// x (+)= Omega[:, col0 : col0 + ncols] y   (a9 of SURVEY.md §8(a))
+// CTA tile: 128 rows (64 row pairs) x all nrhs <= 64 columns; Omega tile generated into smem.
+// ------------------------------------------------------------------------------------------
+constexpr int OM_ROWS = 128;
+constexpr int OM_JT = 16;
+
+__global__ void __launch_bounds__(256) k_omega_apply(int64_t N, int64_t col0, int ncols, const double* y, int64_t ldy,
+                                                     int nrhs, double* x, int64_t ldx, int accumulate, uint64_t seed) {
+  __shared__ double om[OM_JT][OM_ROWS + 1];
+  __shared__ double ys[OM_JT][64];
+  const int tid = threadIdx.x;
+  const int64_t row0 = (int64_t)blockIdx.x * OM_ROWS;
+  // thread -> (4 rows, up to 8 rhs): 32 row groups x 8 rhs groups
+  const int rg = tid & 31, cg = tid >> 5;
+  double acc[4][8];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[a][c] = 0.0;
+  for (int j0 = 0; j0 < ncols; j0 += OM_JT) {
+    __syncthreads();
+    // Omega tile: OM_ROWS/2 row pairs x OM_JT columns
+    for (int e = tid; e < (OM_ROWS / 2) * OM_JT; e += blockDim.x) {
+      const int pr = e % (OM_ROWS / 2), jj = e / (OM_ROWS / 2);
+      const int64_t i = row0 + 2 * pr;
+      double2 z = make_double2(0.0, 0.0);
+      if (j0 + jj < ncols && i < N) z = probe_pair((uint64_t)(i >> 1), (uint64_t)(col0 + j0 + jj), seed);
+      om[jj][2 * pr] = z.x;
+      om[jj][2 * pr + 1] = (i + 1 < N) ? z.y : 0.0;
+    }
+    for (int e = tid; e < OM_JT * 64; e += blockDim.x) {
+      const int jj = e / 64, c = e % 64;
+      ys[jj][c] = (j0 + jj < ncols && c < nrhs) ? y[(int64_t)c * ldy + j0 + jj] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int jj = 0; jj < OM_JT; ++jj) {
+      double o[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) o[a] = om[jj][rg + 32 * a];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const double yv = ys[jj][cg + 8 * c];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) acc[a][c] = fma(o[a], yv, acc[a][c]);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int64_t i = row0 + rg + 32 * a;
+    if (i >= N) continue;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int cc = cg + 8 * c;
+      if (cc < nrhs) {
+        double* px = x + (int64_t)cc * ldx + i;
+        *px = accumulate ? *px + acc[a][c] : acc[a][c];
+      }
+    }
+  }
+}
+
+static az_status_t omega_apply(az_plan_s* p, int64_t col0, int64_t ncols, const double* y, int64_t ldy,
+                               int64_t nrhs, double* x, int64_t ldx, int accumulate, cudaStream_t st) {
+  for (int64_t c0 = 0; c0 < nrhs; c0 += 64) {
+    const int nr = (int)std::min<int64_t>(64, nrhs - c0);
+    k_omega_apply<<<az_div_up(p->N, OM_ROWS), 256, 0, st>>>(p->N, col0, (int)ncols, y + c0 * ldy, ldy, nr,
+                                                            x + c0 * ldx, ldx, accumulate, p->seed);
+    AZ_LAUNCH_CHECK();
+  }
+  return AZ_OK;
+}
+
+extern "C" az_status_t az_omega_apply(az_plan_t p, int64_t col0, int64_t ncols, const double* y, int64_t ldy,
+                                      int64_t nrhs, double* x, int64_t ldx, int accumulate, void* stream) {
+  if (!p || col0 < 0 || ncols < 0 || nrhs < 0 || (nrhs && (!x || ldx < p->N)) || (ncols && nrhs && (!y || ldy < ncols))) {
+    az_set_error("az_omega_apply: bad arguments");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  return omega_apply(p, col0, ncols, y, ldy, nrhs, x, ldx, accumulate, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------------------------------
+// small elementwise kernels
+// ------------------------------------------------------------------------------------------
+__global__ void k_copy_cols(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  const int64_t r = e % rows, c = e / rows;
+  dst[c * ldd + r] = src[c * lds + r];
+}
+__global__ void k_sub_cols(const double* b, int64_t ldb, double* y, int64_t ldy, int64_t rows, int64_t cols) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  const int64_t r = e % rows, c = e / rows;
+  y[c * ldy + r] = b[c * ldb + r] - y[c * ldy + r];       // y <- b - y
+}
+__global__ void k_add_cols(const double* a, int64_t lda, double* x, int64_t ldx, int64_t rows, int64_t cols) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  const int64_t r = e % rows, c = e / rows;
+  x[c * ldx + r] += a[c * lda + r];
+}
+
+// ------------------------------------------------------------------------------------------
+// workspace layout
+// ------------------------------------------------------------------------------------------
+struct SolveWS {
+  double* S;     // rows x (Rmax + nrhs)
+  double* bp;    // rows x nrhs : b'
+  double* Rf;    // kt x kt
+  double* y;     // Rmax x nrhs
+  double* sig;   // Rmax
+  double* tmp;   // rows x nrhs
+  double* x2;    // N x nrhs
+  void* qrws;
+  size_t qrbytes;
+  void* svdws;
+  size_t svdbytes;
+  size_t total;
+};
+
+static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+static SolveWS layout(az_plan_s* p, int64_t nrhs, int64_t R, int32_t max_blocks, char* base) {
+  SolveWS w;
+  const int64_t rows = p->M + p->Mb;
+  const int64_t Rmax = R * max_blocks;
+  const int64_t kt = Rmax + nrhs;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* ptr = base ? base + off : nullptr;
+    off += align256(bytes);
+    return ptr;
+  };
+  w.S = (double*)take(sizeof(double) * rows * kt);
+  w.bp = (double*)take(sizeof(double) * rows * nrhs);
+  w.Rf = (double*)take(sizeof(double) * kt * kt);
+  w.y = (double*)take(sizeof(double) * Rmax * nrhs);
+  w.sig = (double*)take(sizeof(double) * Rmax);
+  w.tmp = (double*)take(sizeof(double) * rows * nrhs);
+  w.x2 = (double*)take(sizeof(double) * p->N * nrhs);
+  w.qrbytes = az_qr_ws_bytes(rows, kt);
+  w.qrws = take(w.qrbytes);
+  w.svdbytes = az_tsvd_ws_bytes(Rmax, nrhs);
+  w.svdws = take(w.svdbytes);
+  w.total = off;
+  return w;
+}
+
+extern "C" az_status_t az_solve_workspace_size(az_plan_t p, int64_t nrhs, int64_t R, int32_t max_blocks, size_t* bytes) {
+  if (!p || !bytes || nrhs < 1 || R < 1 || max_blocks < 1) {
+    az_set_error("az_solve_workspace_size: bad arguments");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  *bytes = layout(p, nrhs, R, max_blocks, nullptr).total;
+  return AZ_OK;
+}
+
+struct Ev {
+  cudaEvent_t e[8];
+  Ev() {
+    for (auto& x : e) cudaEventCreate(&x);
+  }
+  ~Ev() {
+    for (auto& x : e) cudaEventDestroy(x);
+  }
+};
+
+static double ms_between(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return (double)ms;
+}
+
+az_status_t az_apply_op(az_plan_s* p, int op, const double* in, int64_t ldin, double* out, int64_t ldout,
+                        int64_t nvec, cudaStream_t st);
+
+extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, double* x, int64_t ldx, int64_t nrhs,
+                                double theta, int64_t R, int32_t max_blocks, void* workspace, size_t ws_bytes,
+                                az_solve_report_t* report, void* stream) {
+  if (!p || !b || !x || nrhs < 1 || R < 2 || max_blocks < 1 || !(theta >= 0.0) || ldb < p->M + p->Mb || ldx < p->N) {
+    az_set_error("az_solve: bad arguments");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  if (R % 2) {
+    az_set_error("az_solve: R must be even (probe pairs)");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  SolveWS w = layout(p, nrhs, R, max_blocks, nullptr);
+  if (!workspace || ws_bytes < w.total) {
+    az_set_error("az_solve: workspace too small (%zu < %zu)", ws_bytes, w.total);
+    return AZ_ERR_WORKSPACE;
+  }
+  w = layout(p, nrhs, R, max_blocks, (char*)workspace);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t rows = p->M + p->Mb;
+  const int pfix = 10;
+  Ev ev;
+  cudaEventRecord(ev.e[0], st);
+  // ---- right-hand side b' = (I - A Z*) b ----
+  AZ_TRY(az_apply_op(p, OP_RESID, b, ldb, w.bp, rows, nrhs, st));
+  cudaEventRecord(ev.e[1], st);
+  double ms_sketch = 0, ms_qr = 0, ms_svd = 0;
+  int64_t rank = 0, nb = 0;
+  bool saturated = false;
+  for (nb = 1; nb <= max_blocks; ++nb) {
+    const int64_t kp = nb * R;                 // probe columns
+    const int64_t kt = kp + nrhs;
+    cudaEvent_t e0 = ev.e[2], e1 = ev.e[3], e2 = ev.e[4], e3 = ev.e[5];
+    cudaEventRecord(e0, st);
+    AZ_TRY(az_sketch(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, st));
+    k_copy_cols<<<az_div_up(rows * nrhs, 256), 256, 0, st>>>(w.bp, rows, w.S + kp * rows, rows, rows, nrhs);
+    AZ_LAUNCH_CHECK();
+    cudaEventRecord(e1, st);
+    AZ_TRY(az_qr_r_impl(w.S, rows, kt, rows, w.Rf, kt, w.qrws, w.qrbytes, st));
+    cudaEventRecord(e2, st);
+    AZ_TRY(az_tsvd_impl(w.Rf, kt, kp, nrhs, theta, w.y, kp, w.sig, &rank, w.svdws, w.svdbytes, st));
+    cudaEventRecord(e3, st);
+    cudaEventSynchronize(e3);
+    ms_sketch += ms_between(e0, e1);
+    ms_qr += ms_between(e1, e2);
+    ms_svd += ms_between(e2, e3);
+    saturated = rank > kp - pfix;
+    if (!saturated || nb == max_blocks) break;
+  }
+  if (nb > max_blocks) nb = max_blocks;
+  const int64_t kp = nb * R;
+  cudaEventRecord(ev.e[6], st);
+  // ---- x2 = Omega y ; x = x2 + Z* (b - A x2) ----
+  AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, p->N, 0, st));
+  AZ_TRY(az_apply_op(p, OP_A, w.x2, p->N, w.tmp, rows, nrhs, st));
+  k_sub_cols<<<az_div_up(rows * nrhs, 256), 256, 0, st>>>(b, ldb, w.tmp, rows, rows, nrhs);
+  AZ_LAUNCH_CHECK();
+  AZ_TRY(az_apply_op(p, OP_ZSTAR, w.tmp, rows, x, ldx, nrhs, st));
+  k_add_cols<<<az_div_up(p->N * nrhs, 256), 256, 0, st>>>(w.x2, p->N, x, ldx, p->N, nrhs);
+  AZ_LAUNCH_CHECK();
+  cudaEventRecord(ev.e[7], st);
+  AZ_CUDA_CHECK(cudaEventSynchronize(ev.e[7]));
+  if (report) {
+    double sg[1] = {0};
+    report->rank_used = rank;
+    report->probes_used = kp;
+    report->saturated = saturated ? 1 : 0;
+    AZ_CUDA_CHECK(cudaMemcpy(sg, w.sig, sizeof(double), cudaMemcpyDeviceToHost));
+    report->sigma_first = sg[0];
+    report->sigma_last_kept = 0;
+    if (rank > 0) AZ_CUDA_CHECK(cudaMemcpy(&report->sigma_last_kept, w.sig + rank - 1, sizeof(double), cudaMemcpyDeviceToHost));
+    report->ms_rhs = ms_between(ev.e[0], ev.e[1]);
+    report->ms_sketch = ms_sketch;
+    report->ms_qr = ms_qr;
+    report->ms_svd = ms_svd;
+    report->ms_step2 = ms_between(ev.e[6], ev.e[7]);
+    report->ms_total = ms_between(ev.e[0], ev.e[7]);
+  }
+  return saturated ? AZ_WARN_SKETCH_SATURATED : AZ_OK;
+}
+
+// Host-buffer convenience (end-to-end timing: host->device copy of b, solve, device->host x).
+extern "C" az_status_t az_solve_host(az_plan_t p, const double* b_host, double* x_host, int64_t nrhs, double theta,
+                                     int64_t R, int32_t max_blocks, az_solve_report_t* report, void* stream) {
+  if (!p || !b_host || !x_host || nrhs < 1) {
+    az_set_error("az_solve_host: bad arguments");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t rows = p->M + p->Mb;
+  size_t need = 0;
+  AZ_TRY(az_solve_workspace_size(p, nrhs, R, max_blocks, &need));
+  const size_t bbytes = sizeof(double) * rows * nrhs, xbytes = sizeof(double) * p->N * nrhs;
+  const size_t total = align256(need) + align256(bbytes) + align256(xbytes);
+  if (p->d_solve_ws_bytes < total) {
+    if (p->d_solve_ws) cudaFree(p->d_solve_ws);
+    p->d_solve_ws = nullptr;
+    p->d_solve_ws_bytes = 0;
+    if (cudaMalloc(&p->d_solve_ws, total) != cudaSuccess) {
+      az_set_error("az_solve_host: cudaMalloc(%zu) failed", total);
+      return AZ_ERR_OUT_OF_MEMORY;
+    }
+    p->d_solve_ws_bytes = total;
+  }
+  const size_t hb = bbytes + xbytes;
+  if (p->h_stage_bytes < hb) {
+    if (p->h_stage) cudaFreeHost(p->h_stage);
+    p->h_stage = nullptr;
+    p->h_stage_bytes = 0;
+    if (cudaMallocHost((void**)&p->h_stage, hb) != cudaSuccess) {
+      az_set_error("az_solve_host: cudaMallocHost(%zu) failed", hb);
+      return AZ_ERR_OUT_OF_MEMORY;
+    }
+    p->h_stage_bytes = hb;
+  }
+  char* base = (char*)p->d_solve_ws;
+  double* db = (double*)(base + align256(need));
+  double* dx = (double*)(base + align256(need) + align256(bbytes));
+  memcpy(p->h_stage, b_host, bbytes);
+  AZ_CUDA_CHECK(cudaMemcpyAsync(db, p->h_stage, bbytes, cudaMemcpyHostToDevice, st));
+  az_status_t s = az_solve(p, db, rows, dx, p->N, nrhs, theta, R, max_blocks, base, need, report, stream);
+  if (s != AZ_OK && s != AZ_WARN_SKETCH_SATURATED) return s;
+  double* hx = p->h_stage + rows * nrhs;
+  AZ_CUDA_CHECK(cudaMemcpyAsync(hx, dx, xbytes, cudaMemcpyDeviceToHost, st));
+  AZ_CUDA_CHECK(cudaStreamSynchronize(st));
+  memcpy(x_host, hx, xbytes);
+  return s;
+}

@@ -1,0 +1,167 @@
+// Truncated least squares on the QR-reduced sketch ("followed by the SVD of an
+// (r+p)-by-M matrix"; "threshold-truncated SVD ... solve min ||S y - rhs||").
+//
+// With Rf = [R_S | c] from the TSQR of [S | b'], R_S = U Sigma V^T and
+//   y = V_k Sigma_k^-1 U_k^T c,   k = #{ sigma_i > theta sigma_1 }.
+// We run one-sided (Hestenes) Jacobi on B = R_S^T: B W -> columns mutually orthogonal, so
+// R_S^T = U' Sigma W^T, R_S = W Sigma U'^T: the rotations W are the LEFT singular vectors of
+// R_S and are applied to the rows of c on the fly (c <- W^T c), and the right singular vectors
+// are the normalised columns of B W.  Then y = sum_{kept i} (B W)_i (W^T c)_i / sigma_i^2.
+// One-sided Jacobi is accurate to high relative precision in the small singular values, which
+// is what the threshold decision needs.  Parallel (round-robin) ordering: r/2 disjoint pairs
+// per round, one warp per pair.
+#include <algorithm>
+
+#include "az_internal.h"
+
+AZ_D double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int64_t ldr, int r, int nrhs,
+                                                          double theta, double* y, int64_t ldy, double* sig_out,
+                                                          int64_t* rank_dev, int max_sweeps) {
+  extern __shared__ double sm[];
+  double* B = sm;                      // r x r, column i at B + i * r
+  double* Cm = B + r * r;              // r x nrhs, row p, column c at Cm[c * r + p]
+  double* nrm2 = Cm + r * nrhs;        // r
+  __shared__ int rot_count;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int w = tid >> 5, lane = tid & 31, nw = nth >> 5;
+  for (int e = tid; e < r * r; e += nth) {
+    const int i = e / r, t = e % r;    // B[t][i] = R_S[i][t]
+    B[e] = Rf[(int64_t)t * ldr + i];
+  }
+  for (int e = tid; e < r * nrhs; e += nth) {
+    const int c = e / r, p = e % r;
+    Cm[e] = Rf[(int64_t)(r + c) * ldr + p];
+  }
+  __syncthreads();
+  const int n = r + (r & 1);           // padded to even
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) rot_count = 0;
+    __syncthreads();
+    for (int round = 0; round < n - 1; ++round) {
+      for (int pi = w; pi < n / 2; pi += nw) {
+        int p, q;
+        if (pi == 0) {
+          p = round;
+          q = n - 1;
+        } else {
+          p = (round + pi) % (n - 1);
+          q = (round - pi + (n - 1)) % (n - 1);
+        }
+        if (p > q) { const int t = p; p = q; q = t; }
+        if (q >= r) continue;
+        double* bp = B + (int64_t)p * r;
+        double* bq = B + (int64_t)q * r;
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int t = lane; t < r; t += 32) {
+          const double xp = bp[t], xq = bq[t];
+          a = fma(xp, xp, a);
+          b = fma(xq, xq, b);
+          g = fma(xp, xq, g);
+        }
+        a = wsum(a);
+        b = wsum(b);
+        g = wsum(g);
+        if (g == 0.0 || !(fabs(g) > 1e-15 * sqrt(a) * sqrt(b))) continue;
+        const double zeta = (b - a) / (2.0 * g);
+        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+        for (int t = lane; t < r; t += 32) {
+          const double xp = bp[t], xq = bq[t];
+          bp[t] = cs * xp - sn * xq;
+          bq[t] = sn * xp + cs * xq;
+        }
+        for (int c = lane; c < nrhs; c += 32) {
+          const double cp = Cm[c * r + p], cq = Cm[c * r + q];
+          Cm[c * r + p] = cs * cp - sn * cq;
+          Cm[c * r + q] = sn * cp + cs * cq;
+        }
+        if (lane == 0) atomicAdd(&rot_count, 1);
+      }
+      __syncthreads();
+    }
+    if (rot_count == 0) break;
+    __syncthreads();
+  }
+  // singular values = column norms of B W
+  for (int i = w; i < r; i += nw) {
+    double a = 0.0;
+    for (int t = lane; t < r; t += 32) a = fma(B[i * r + t], B[i * r + t], a);
+    a = wsum(a);
+    if (lane == 0) nrm2[i] = a;
+  }
+  __syncthreads();
+  double smax2 = 0.0;
+  for (int i = 0; i < r; ++i) smax2 = fmax(smax2, nrm2[i]);
+  const double thr2 = theta * theta * smax2;
+  // y[t][c] = sum_{kept i} B[t][i] C[i][c] / sigma_i^2
+  for (int e = tid; e < r * nrhs; e += nth) {
+    const int c = e / r, t = e % r;
+    double acc = 0.0;
+    for (int i = 0; i < r; ++i) {
+      const double s2 = nrm2[i];
+      if (s2 > thr2 && s2 > 0.0) acc = fma(B[i * r + t], Cm[c * r + i] / s2, acc);
+    }
+    y[(int64_t)c * ldy + t] = acc;
+  }
+  // sorted singular values (rank by counting) and the kept count
+  for (int i = tid; i < r; i += nth) {
+    int pos = 0;
+    for (int t = 0; t < r; ++t)
+      if (nrm2[t] > nrm2[i] || (nrm2[t] == nrm2[i] && t < i)) ++pos;
+    if (sig_out) sig_out[pos] = sqrt(nrm2[i]);
+  }
+  if (tid == 0) {
+    int64_t kk = 0;
+    for (int i = 0; i < r; ++i) kk += (nrm2[i] > thr2 && nrm2[i] > 0.0);
+    *rank_dev = kk;
+  }
+}
+
+size_t az_tsvd_ws_bytes(int64_t r, int64_t nrhs) { return 256; }
+
+az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta, double* y,
+                         int64_t ldy, double* sigma_out, int64_t* rank_out, void* ws, size_t ws_bytes,
+                         cudaStream_t st) {
+  const size_t sm = (size_t)(r * r + r * nrhs + r) * sizeof(double);
+  if (sm > 220 * 1024) {
+    az_set_error("az_tsvd_solve: r = %lld, nrhs = %lld exceed the single-CTA Jacobi (multi-CTA path not built)",
+                 (long long)r, (long long)nrhs);
+    return AZ_ERR_NOT_SUPPORTED;
+  }
+  if (ws_bytes < az_tsvd_ws_bytes(r, nrhs)) {
+    az_set_error("az_tsvd_solve: workspace too small");
+    return AZ_ERR_WORKSPACE;
+  }
+  int64_t* d_rank = (int64_t*)ws;
+  AZ_CUDA_CHECK(az_smem_attr(k_jacobi_small, sm));
+  const int nth = std::min<int64_t>(1024, std::max<int64_t>(64, 32 * ((r + 1) / 2)));
+  k_jacobi_small<<<1, nth, sm, st>>>(Rf, ldr, (int)r, (int)nrhs, theta, y, ldy, sigma_out, d_rank, 60);
+  AZ_LAUNCH_CHECK();
+  if (rank_out) {
+    AZ_CUDA_CHECK(cudaMemcpyAsync(rank_out, d_rank, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    AZ_CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+  return AZ_OK;
+}
+
+extern "C" az_status_t az_tsvd_workspace_size(int64_t r, int64_t nrhs, size_t* bytes) {
+  if (!bytes) return AZ_ERR_INVALID_ARGUMENT;
+  *bytes = az_tsvd_ws_bytes(r, nrhs);
+  return AZ_OK;
+}
+
+extern "C" az_status_t az_tsvd_solve(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta,
+                                     double* y, int64_t ldy, double* sigma_out, int64_t* rank_out, void* ws,
+                                     size_t ws_bytes, void* stream) {
+  if (!Rf || !y || r < 1 || nrhs < 0 || ldr < r || ldy < r || !(theta >= 0) || !ws) {
+    az_set_error("az_tsvd_solve: bad arguments");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  return az_tsvd_impl(Rf, ldr, r, nrhs, theta, y, ldy, sigma_out, rank_out, ws, ws_bytes, (cudaStream_t)stream);
+}
