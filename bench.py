@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""bench.py -- AZ solves/s on BASELINE config 2 (1-D, N = 2^20 centres, L = 2, 64 RHS, R = 64
+probes, tol 1e-12) on B200, with the roofline of the dominant kernel and the CPU oracle beside it.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+One "step" = one az_solve (Alg. 1: b' = (I - A Z*) b, the 64-probe sketch
+(A - A Z* A) Omega, TSQR + truncated SVD, x2 = Omega y, step 2 x = x2 + Z*(b - A x2)) over the
+config's whole RHS batch, inputs resident in HBM.  Multi-GPU (torchrun): every rank solves its own
+independent c2 problem (weak scaling, no data-path collective); the time is
+the max over ranks.  The reference arm (--impl reference) times the CPU oracle (oracle/, the
+paper's algorithm with numpy FFTs) on a bounded sample of the same workload, scaled to one solve.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2308_14490_b200 import inputs as I  # noqa: E402
+
+METRIC = "AZ solves/s"
+UNIT = "solves/s"
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # SMs x FP64 FMA/clk/SM x 2 x max clock
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+# ------------------------------------------------------------------------------------------
+# algorithmic bytes / flops per unit (per complex vector PAIR for the pass kernels), DESIGN.md
+# "Algorithmic bytes per kernel".  n = coefficient length, L = fine length, M = rows.
+# ------------------------------------------------------------------------------------------
+def kernel_model(name, cfg, M, k_cols):
+    n = cfg.N
+    L = cfg.N * cfg.s ** cfg.dim
+    C = 16  # bytes per complex128
+    hbm = {
+        "1f_cols_in_coef": C * n,                      # probes generated on chip; write spectrum
+        "1f_rows_expand_keep": 2 * C * n + C * L,
+        "1f_rows_expand": C * n + C * L,
+        "1f_cols_fine_mask": 2 * C * L + L,            # read + write fine grid, read mask (1 B)
+        "1f_rows_step1": 2 * C * L + C * n + 8 * n,    # fine grid in/out, v^ and zinv in
+        "1f_rows_resid": 2 * C * L + 8 * n,
+        "1f_rows_zstar": C * L + C * n + 8 * n,
+        "1f_cols_out_gather": C * L + 4 * L + 2 * 8 * M,   # fine grid + row map in, 2 columns out
+        "1f_cols_out_resid": C * L + 4 * L + 4 * 8 * M,
+        "1f_cols_in_rows": 4 * L + 2 * 8 * M + C * L,
+        "1f_cols_out_coef": C * n + 2 * 8 * n,
+    }
+    if name in hbm:
+        return "hbm", hbm[name]
+    if name == "tsqr_leaf":
+        return "alu", 2.0 * k_cols * k_cols     # flops per row (units = rows)
+    if name == "omega_apply":
+        return "alu", 2.0                       # flops per (row x column x rhs) unit
+    return None, None
+
+
+# ------------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ------------------------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------------------------------
+# CPU oracle sample (cpu_baseline and --impl reference)
+# ------------------------------------------------------------------------------------------
+def oracle_sample(cfg, R):
+    """Time the oracle (oracle/az.py, paper's algorithm with numpy FFTs, fp64) on a bounded sample
+    of the workload and scale to one full solve: 2 probes of the sketch, 2 RHS of b' and step 2,
+    2 probe columns of Omega y, and the dense SVD of an (M x R) matrix at full size."""
+    from oracle import az as OA
+    from oracle import philox as OP
+    t0 = time.perf_counter()
+    prob = OA.make_problem(cfg, "fft")
+    t_setup = time.perf_counter() - t0
+    b = I.rhs(cfg)
+    nr = cfg.nrhs
+    t = time.perf_counter()
+    Om = OP.probes(cfg.N, [0, 1], cfg.seed)
+    t_gen2 = time.perf_counter() - t
+    t = time.perf_counter()
+    S2 = OA.step1_apply(prob, Om)
+    t_probe2 = time.perf_counter() - t
+    t = time.perf_counter()
+    bp = OA.resid_apply(prob, b[:, :2])
+    x1 = prob.apply_Zstar(b[:, :2] - prob.apply_A(np.zeros((cfg.N, 2))))
+    t_rhs2 = time.perf_counter() - t
+    rng = np.random.default_rng(0)
+    Sfull = rng.standard_normal((S2.shape[0], R))
+    t = time.perf_counter()
+    np.linalg.svd(Sfull, full_matrices=False)
+    t_svd = time.perf_counter() - t
+    est = (R / 2) * (t_gen2 + t_probe2) + (nr / 2) * t_rhs2 + t_svd + (R / 2) * t_gen2
+    sample = (f"oracle (numpy FFT AZ, fp64) on {cfg.name}: 2 probes + 2 RHS + 2 Omega columns + dense SVD "
+              f"{S2.shape[0]}x{R}, scaled to {R} probes and {nr} RHS; measured {t_gen2 + t_probe2 + t_rhs2 + t_svd:.1f} s")
+    return est, sample, t_setup
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count()
+    ests = []
+    sample = ""
+    for _ in range(args.steps):
+        est, sample, _ = oracle_sample(cfg, cfg.R)
+        ests.append(est)
+    sec = statistics.mean(ests)
+    value = 1.0 / sec
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "n": cfg.n, "L": cfg.s, "nrhs": cfg.nrhs, "R": cfg.R, "tol": cfg.tol},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------
+def run_ours(args, cfg):
+    import torch
+    from paper_2308_14490_b200 import api
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    theta = max(cfg.tol * 1e-2, 1e-12)
+    max_blocks = 1 if cfg.dim == 1 else 8
+
+    plan = api.Plan.from_config(cfg)
+    b_host = I.rhs(cfg)
+    b = torch.from_numpy(b_host).to(dev)
+    b = api.colmajor(b)
+    x = api.empty_colmajor(plan.N, cfg.nrhs, dev)
+    ws = torch.empty(plan.solve_workspace_bytes(cfg.nrhs, cfg.R, max_blocks), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # > L2 (126 MB)
+
+    def step():
+        return plan.solve(b, theta, cfg.R, max_blocks, x=x, workspace=ws)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+
+    clocks = Clocks(local)
+    api.launch_count(reset=True)
+    api.trace_enable(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    reps = []
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)                       # evict L2 between timed iterations (not timed)
+        ev[i][0].record(stream)
+        _, rep = step()
+        ev[i][1].record(stream)
+        reps.append(rep)
+    torch.cuda.synchronize()
+    launches = api.launch_count()
+    trace = api.trace_report()
+    api.trace_enable(False)
+    clk = clocks.stop()
+    ms = [a.elapsed_time(bb) for a, bb in ev]
+    ms_step = sum(ms) / len(ms)
+    if dist:
+        t = torch.tensor([ms_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+
+    # ---- end to end through the host-buffer entry point (pinned host memory) ----
+    bh = torch.from_numpy(np.asfortranarray(b_host)).t().contiguous().pin_memory().t()
+    xh = torch.empty((cfg.nrhs, plan.N), dtype=torch.float64).pin_memory().t()
+    for _ in range(2):
+        plan.solve_host(bh, theta, cfg.R, max_blocks, x=xh)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ke = max(2, min(args.steps, 5))
+    e0.record(stream)
+    for _ in range(ke):
+        plan.solve_host(bh, theta, cfg.R, max_blocks, x=xh)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / ke
+    if dist:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    if rank != 0:
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (live CUDA-event trace over the timed region) ----
+    peaks, peak_src = measured_peaks()
+    kcols = reps[-1]["probes"] + cfg.nrhs
+    dom = max(trace.items(), key=lambda kv: kv[1][1])
+    name, (cnt, tot_ms, units) = dom
+    bound, per_unit = kernel_model(name, cfg, plan.M, kcols)
+    roof = {"kernel": name, "launches": cnt, "ms_total": tot_ms, "share_of_step": tot_ms / sum(ms)}
+    if bound == "hbm":
+        achieved = per_unit * units / (tot_ms * 1e-3) / 1e9
+        roof.update({"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "peak_source": peak_src})
+    elif bound == "alu":
+        achieved = per_unit * units / (tot_ms * 1e-3) / 1e12
+        roof.update({"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FP64_PEAK_TFLOPS,
+                     "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz (DESIGN.md)"})
+    else:
+        roof.update({"bound": None, "achieved": None, "peak": None, "unit": None, "frac": None})
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get(name)
+        except Exception:
+            traffic = None
+    roof["traffic"] = traffic
+    # per-kernel table (share of the step)
+    kernels = {k: {"launches": v[0], "ms_per_step": v[1] / args.steps, "units": v[2]} for k, v in
+               sorted(trace.items(), key=lambda kv: -kv[1][1])}
+
+    rep = reps[-1]
+    value = world * 1000.0 / ms_step
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        est, sample, _ = oracle_sample(cfg, cfg.R)
+        cpu = {"value": 1.0 / est, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": sample}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "n": cfg.n, "L": cfg.s, "dim": cfg.dim, "nrhs": cfg.nrhs, "R": cfg.R,
+                   "tol": cfg.tol, "theta": theta, "max_blocks": max_blocks, "parallelism": f"replicas{world}",
+                   "l2": "flushed between timed steps (256 MB write); S alone is 1.07 GB"},
+        "probe_applies_per_s": world * rep["probes"] / (rep["ms_sketch"] * 1e-3) if rep["ms_sketch"] else None,
+        "rhs_per_s": value * cfg.nrhs,
+        "stages_ms": {k: rep[k] for k in ("ms_rhs", "ms_sketch", "ms_qr", "ms_svd", "ms_step2", "ms_total")},
+        "rank": rep["rank"], "probes": rep["probes"], "saturated": rep["saturated"],
+        "roofline": roof,
+        "kernels": kernels,
+        "cpu_baseline": cpu,
+        "e2e": {"value": world * 1000.0 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(b_host.nbytes),
+                "d2h_bytes_per_step": int(plan.N * cfg.nrhs * 8), "ms_per_step": e2e_ms},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = I.get_config(args.config)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

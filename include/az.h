@@ -176,6 +176,13 @@ const char* az_last_error(void);
  * for the bench's gpu_launches field). */
 int64_t az_launch_count(int reset);
 
+/* Per-kernel CUDA-event tracing for measurement (bench.py roofline): when enabled, every libaz
+ * launch is bracketed by two events on its stream.  az_trace_report synchronises those events
+ * and writes "name count total_ms\n" lines into buf (NUL-terminated, truncated to len).
+ * Tracing adds two event records per launch; it is off by default. */
+int az_trace_enable(int on);
+int az_trace_report(char* buf, int len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -81,6 +81,10 @@ def lib():
         fn.restype = C.c_int
     L.az_status_string.restype = C.c_char_p
     L.az_last_error.restype = C.c_char_p
+    L.az_trace_enable.argtypes = [C.c_int]
+    L.az_trace_enable.restype = C.c_int
+    L.az_trace_report.argtypes = [C.c_char_p, C.c_int]
+    L.az_trace_report.restype = C.c_int
     L.az_launch_count.argtypes = [C.c_int]
     L.az_launch_count.restype = C.c_int64
     _lib = L
@@ -91,7 +95,7 @@ EXPORTED = ["az_plan_create", "az_plan_destroy", "az_plan_query", "az_apply_A", 
             "az_apply_Zstar", "az_apply_step1", "az_apply_resid", "az_sketch", "az_omega_apply",
             "az_qr_r", "az_qr_workspace_size", "az_tsvd_solve", "az_tsvd_workspace_size",
             "az_solve_workspace_size", "az_solve", "az_solve_host", "az_status_string",
-            "az_last_error", "az_launch_count"]
+            "az_last_error", "az_launch_count", "az_trace_enable", "az_trace_report"]
 
 
 def check(fn: str, status: int, allow=(AZ_OK,)):

@@ -158,12 +158,26 @@ class Plan:
                    allow=(_lib.AZ_OK, _lib.AZ_WARN_SKETCH_SATURATED))
         return x, _report(rep, st)
 
-    def solve_host(self, b: np.ndarray, theta: float, R: int, max_blocks: int = 1, stream=None):
-        b = np.asfortranarray(b, dtype=np.float64)
-        nrhs = 1 if b.ndim == 1 else b.shape[1]
-        x = np.empty((self.N, nrhs), dtype=np.float64, order="F")
+    def solve_host(self, b, theta: float, R: int, max_blocks: int = 1, x=None, stream=None):
+        """End-to-end solve on HOST buffers (host->device copy of b, solve, device->host copy of x
+        inside the call).  b, x: numpy arrays or CPU torch tensors in column-major layout; pinned
+        torch tensors (pin_memory=True) are copied by DMA directly."""
+        if isinstance(b, torch.Tensor):
+            nrhs = 1 if b.dim() == 1 else b.shape[1]
+            if b.dim() == 2 and b.stride(0) != 1:
+                raise ValueError("b must be column-major")
+            pb = b.data_ptr()
+            if x is None:
+                x = torch.empty((nrhs, self.N), dtype=torch.float64, pin_memory=True).t()
+            px = x.data_ptr()
+        else:
+            b = np.asfortranarray(b, dtype=np.float64)
+            nrhs = 1 if b.ndim == 1 else b.shape[1]
+            if x is None:
+                x = np.empty((self.N, nrhs), dtype=np.float64, order="F")
+            pb, px = b.ctypes.data, x.ctypes.data
         rep = _lib.SolveReport()
-        st = check("az_solve_host", lib().az_solve_host(self._h, C.c_void_p(b.ctypes.data), C.c_void_p(x.ctypes.data),
+        st = check("az_solve_host", lib().az_solve_host(self._h, C.c_void_p(pb), C.c_void_p(px),
                                                         nrhs, theta, R, max_blocks, C.byref(rep), _stream(stream)),
                    allow=(_lib.AZ_OK, _lib.AZ_WARN_SKETCH_SATURATED))
         return x, _report(rep, st)
@@ -208,3 +222,20 @@ def tsvd_solve(Rf: torch.Tensor, r: int, nrhs: int, theta: float, stream=None):
 
 def launch_count(reset: bool = False) -> int:
     return lib().az_launch_count(int(reset))
+
+
+def trace_enable(on: bool = True) -> None:
+    """Bracket every libaz launch with CUDA events on its stream (measurement only)."""
+    lib().az_trace_enable(int(on))
+
+
+def trace_report() -> dict:
+    """{kernel name: (launches, total ms, units)} since trace_enable (synchronises the events)."""
+    n = lib().az_trace_report(None, 0)
+    buf = C.create_string_buffer(n + 1)
+    lib().az_trace_report(buf, n + 1)
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms, units = line.split()
+        out[name] = (int(cnt), float(ms), int(units))
+    return out

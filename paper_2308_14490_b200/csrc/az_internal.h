@@ -88,4 +88,13 @@ az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs,
 size_t az_tsvd_ws_bytes(int64_t r, int64_t nrhs);
 
 
+// Optional per-launch CUDA-event tracing (az_trace_enable): records an event pair around each
+// traced launch on the launching stream; az_trace_report sums the durations per kernel name.
+struct AzTrace {
+  AzTrace(const char* name, cudaStream_t st, int64_t units = 0);
+  ~AzTrace();
+  int slot;
+  cudaStream_t st;
+};
+
 inline unsigned az_div_up(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }

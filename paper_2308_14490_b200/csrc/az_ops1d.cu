@@ -151,6 +151,7 @@ template <int L>
 static az_status_t launch1s(const P1s& a, int op, int src, int64_t npairs, cudaStream_t st) {
   const size_t sm = (size_t)(spad_len(L) + a.n) * sizeof(cplx);
   const dim3 grid((unsigned)npairs), block(L / 8);
+  AzTrace tr("1d_chain", st, npairs);
 #define AZ_L1S(OPV, SRCV) (az_smem_attr(k_chain1s<L, OPV, SRCV>, sm), k_chain1s<L, OPV, SRCV><<<grid, block, sm, st>>>(a))
   if (op == OP_A) AZ_L1S(OP_A, SRC_VEC);
   else if (op == OP_STEP1 && src == SRC_PROBE) AZ_L1S(OP_STEP1, SRC_PROBE);

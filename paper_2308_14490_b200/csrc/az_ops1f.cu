@@ -249,6 +249,9 @@ static az_status_t fcols(const P1f& a, int ncols, int nb, double cout, cudaStrea
   const size_t sm = (size_t)TC * spad_len(NC) * sizeof(cplx);
   auto kern = k1f_cols<NC, TC, KIND, SRC>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
+  static const char* names[] = {"1f_cols_in_coef", "1f_cols_fine_mask", "1f_cols_out_gather", "1f_cols_out_resid",
+                                "1f_cols_in_rows", "1f_cols_out_coef", "1f_cols_fwd"};
+  AzTrace tr(names[KIND], st, nb);
   kern<<<dim3(az_div_up(ncols, TC), nb), TC * NC / 8, sm, st>>>(a, cout);
   AZ_LAUNCH_CHECK();
   return AZ_OK;
@@ -262,6 +265,9 @@ static az_status_t frows(const P1f& a, int nb, cudaStream_t st) {
   const size_t sm = (size_t)RPC * (spad_len(NR2) + spad_len(LR2)) * sizeof(cplx);
   auto kern = k1f_rows<NR2, LR2, RPC, KIND>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
+  static const char* names[] = {"1f_rows_expand", "1f_rows_expand_keep", "1f_rows_step1", "1f_rows_resid",
+                                "1f_rows_zstar", "1f_rows_at"};
+  AzTrace tr(names[KIND], st, nb);
   kern<<<dim3(az_div_up(a.N1, RPC), nb), RPC * NR2 / 8, sm, st>>>(a, a.N1);
   AZ_LAUNCH_CHECK();
   return AZ_OK;

@@ -352,6 +352,9 @@ static az_status_t rows(const P2& a, int nrows, int nb, double cout, cudaStream_
   const size_t sm = (size_t)RPC * spad_len(LEN) * sizeof(cplx);
   auto kern = k2_rows<LEN, KIND, SRC>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
+  static const char* names[] = {"2d_rows_in_coef", "2d_rows_fine_mask", "2d_rows_out_gather", "2d_rows_out_resid",
+                                "2d_rows_in_rows", "2d_rows_out_coef", "2d_rows_coef_w"};
+  AzTrace tr(names[KIND], st, nb);
   kern<<<dim3(az_div_up(nrows, RPC), nb), RPC * TPF, sm, st>>>(a, nrows, cout);
   AZ_LAUNCH_CHECK();
   return AZ_OK;
@@ -365,6 +368,9 @@ static az_status_t cols(const P2& a, int nb, cudaStream_t st) {
   const size_t sm = (size_t)TC * (spad_len(NN) + spad_len(LL)) * sizeof(cplx);
   auto kern = k2_cols<NN, LL, TC, KIND, WANT_W>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
+  static const char* names[] = {"2d_cols_expand", "2d_cols_expand_keep", "2d_cols_step1", "2d_cols_resid",
+                                "2d_cols_zstar", "2d_cols_at"};
+  AzTrace tr(names[KIND], st, nb);
   kern<<<dim3(az_div_up(NN, TC), nb), TC * NN / 8, sm, st>>>(a);
   AZ_LAUNCH_CHECK();
   return AZ_OK;
@@ -385,6 +391,7 @@ static az_status_t run2d(const P2& a0, int op, int src, int64_t npairs, int64_t 
         AZ_TRY((cols<NN, CK_EXPAND, 0>(a, nb, st)));
         AZ_TRY(rows<LL, RK_OUT_GATHER, SRC_VEC>(a, LL, nb, 1.0, st));
         if (bnd) {
+          AzTrace tr("2d_boundary", st, nb);
           k2_boundary_rows<1, 0><<<dim3((unsigned)a.Mb, nb), 32, 0, st>>>(a);
           AZ_LAUNCH_CHECK();
         }
@@ -403,6 +410,7 @@ static az_status_t run2d(const P2& a0, int op, int src, int64_t npairs, int64_t 
         AZ_TRY(rows<LL, RK_OUT_GATHER, SRC_VEC>(a, LL, nb, 1.0, st));
         if (bnd) {
           AZ_TRY(rows<NN, RK_COEF_W, SRC_VEC>(a, NN, nb, 1.0 / n2, st));
+          AzTrace tr("2d_boundary", st, nb);
           k2_boundary_rows<0, 0><<<dim3((unsigned)a.Mb, nb), 32, 0, st>>>(a);
           AZ_LAUNCH_CHECK();
         }
@@ -416,6 +424,7 @@ static az_status_t run2d(const P2& a0, int op, int src, int64_t npairs, int64_t 
         AZ_TRY(rows<LL, RK_OUT_RESID, SRC_VEC>(a, LL, nb, 1.0, st));
         if (bnd) {
           AZ_TRY(rows<NN, RK_COEF_W, SRC_VEC>(a, NN, nb, 1.0 / n2, st));
+          AzTrace tr("2d_boundary", st, nb);
           k2_boundary_rows<0, 1><<<dim3((unsigned)a.Mb, nb), 32, 0, st>>>(a);
           AZ_LAUNCH_CHECK();
         }
@@ -430,6 +439,7 @@ static az_status_t run2d(const P2& a0, int op, int src, int64_t npairs, int64_t 
         AZ_TRY((cols<NN, CK_AT, 0>(a, nb, st)));
         AZ_TRY(rows<NN, RK_OUT_COEF, SRC_VEC>(a, NN, nb, 1.0 / ((double)LL * LL), st));
         if (bnd) {
+          AzTrace tr("2d_boundary", st, nb);
           k2_boundary_adjoint<<<dim3((unsigned)a.Mb, nb), 32, 0, st>>>(a);
           AZ_LAUNCH_CHECK();
         }

@@ -27,6 +27,78 @@ void az_set_error(const char* fmt, ...) {
 void az_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 extern "C" const char* az_last_error(void) { return g_err; }
+
+// ---- tracing ----
+#include <map>
+#include <mutex>
+#include <string>
+namespace {
+struct TraceRec {
+  std::string name;
+  cudaEvent_t e0, e1;
+  int64_t units;
+};
+std::mutex g_tr_mu;
+bool g_tr_on = false;
+std::vector<TraceRec> g_tr;
+size_t g_tr_used = 0;
+}  // namespace
+
+AzTrace::AzTrace(const char* name, cudaStream_t s, int64_t units) : slot(-1), st(s) {
+  if (!g_tr_on) return;
+  std::lock_guard<std::mutex> lk(g_tr_mu);
+  if (g_tr_used == g_tr.size()) {
+    TraceRec r;
+    cudaEventCreate(&r.e0);
+    cudaEventCreate(&r.e1);
+    g_tr.push_back(r);
+  }
+  slot = (int)g_tr_used++;
+  g_tr[slot].name = name;
+  g_tr[slot].units = units;
+  cudaEventRecord(g_tr[slot].e0, st);
+}
+AzTrace::~AzTrace() {
+  if (slot >= 0) cudaEventRecord(g_tr[slot].e1, st);
+}
+
+extern "C" int az_trace_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_tr_mu);
+  g_tr_on = on != 0;
+  g_tr_used = 0;
+  return 0;
+}
+
+extern "C" int az_trace_report(char* buf, int len) {
+  std::lock_guard<std::mutex> lk(g_tr_mu);
+  struct Agg {
+    int64_t count = 0, units = 0;
+    double ms = 0.0;
+  };
+  std::map<std::string, Agg> agg;
+  for (size_t i = 0; i < g_tr_used; ++i) {
+    cudaEventSynchronize(g_tr[i].e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g_tr[i].e0, g_tr[i].e1);
+    auto& a = agg[g_tr[i].name];
+    a.count += 1;
+    a.ms += ms;
+    a.units += g_tr[i].units;
+  }
+  std::string out;
+  char line[256];
+  for (auto& kv : agg) {
+    snprintf(line, sizeof(line), "%s %lld %.6f %lld\n", kv.first.c_str(), (long long)kv.second.count, kv.second.ms,
+             (long long)kv.second.units);
+    out += line;
+  }
+  if (buf && len > 0) {
+    const size_t n = std::min<size_t>(out.size(), (size_t)len - 1);
+    memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return (int)out.size();
+}
 extern "C" int64_t az_launch_count(int reset) {
   return reset ? g_launches.exchange(0) : g_launches.load();
 }

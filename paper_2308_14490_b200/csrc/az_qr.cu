@@ -150,6 +150,7 @@ static az_status_t tsqr_launch(const QRIn& q, int nblocks, cudaStream_t st) {
   const size_t sm = ((size_t)q.k * (q.k + 1) / 2 + 2 * MC + 2) * sizeof(double);
   auto kern = k_tsqr<KC, RPL>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
+  AzTrace tr(q.bstride ? "tsqr_merge" : "tsqr_leaf", st, q.m);
   kern<<<nblocks, 512, sm, st>>>(q);
   AZ_LAUNCH_CHECK();
   return AZ_OK;

@@ -83,6 +83,7 @@ static az_status_t omega_apply(az_plan_s* p, int64_t col0, int64_t ncols, const 
                                int64_t nrhs, double* x, int64_t ldx, int accumulate, cudaStream_t st) {
   for (int64_t c0 = 0; c0 < nrhs; c0 += 64) {
     const int nr = (int)std::min<int64_t>(64, nrhs - c0);
+    AzTrace tr("omega_apply", st, p->N * ncols * nr);
     k_omega_apply<<<az_div_up(p->N, OM_ROWS), 256, 0, st>>>(p->N, col0, (int)ncols, y + c0 * ldy, ldy, nr,
                                                             x + c0 * ldx, ldx, accumulate, p->seed);
     AZ_LAUNCH_CHECK();
@@ -229,7 +230,10 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
     cudaEvent_t e0 = ev.e[2], e1 = ev.e[3], e2 = ev.e[4], e3 = ev.e[5];
     cudaEventRecord(e0, st);
     AZ_TRY(az_sketch(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, st));
-    k_copy_cols<<<az_div_up(rows * nrhs, 256), 256, 0, st>>>(w.bp, rows, w.S + kp * rows, rows, rows, nrhs);
+    {
+      AzTrace tr("elementwise", st);
+      k_copy_cols<<<az_div_up(rows * nrhs, 256), 256, 0, st>>>(w.bp, rows, w.S + kp * rows, rows, rows, nrhs);
+    }
     AZ_LAUNCH_CHECK();
     cudaEventRecord(e1, st);
     AZ_TRY(az_qr_r_impl(w.S, rows, kt, rows, w.Rf, kt, w.qrws, w.qrbytes, st));
@@ -249,10 +253,16 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   // ---- x2 = Omega y ; x = x2 + Z* (b - A x2) ----
   AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, p->N, 0, st));
   AZ_TRY(az_apply_op(p, OP_A, w.x2, p->N, w.tmp, rows, nrhs, st));
-  k_sub_cols<<<az_div_up(rows * nrhs, 256), 256, 0, st>>>(b, ldb, w.tmp, rows, rows, nrhs);
+  {
+    AzTrace tr("elementwise", st);
+    k_sub_cols<<<az_div_up(rows * nrhs, 256), 256, 0, st>>>(b, ldb, w.tmp, rows, rows, nrhs);
+  }
   AZ_LAUNCH_CHECK();
   AZ_TRY(az_apply_op(p, OP_ZSTAR, w.tmp, rows, x, ldx, nrhs, st));
-  k_add_cols<<<az_div_up(p->N * nrhs, 256), 256, 0, st>>>(w.x2, p->N, x, ldx, p->N, nrhs);
+  {
+    AzTrace tr("elementwise", st);
+    k_add_cols<<<az_div_up(p->N * nrhs, 256), 256, 0, st>>>(w.x2, p->N, x, ldx, p->N, nrhs);
+  }
   AZ_LAUNCH_CHECK();
   cudaEventRecord(ev.e[7], st);
   AZ_CUDA_CHECK(cudaEventSynchronize(ev.e[7]));
@@ -298,27 +308,14 @@ extern "C" az_status_t az_solve_host(az_plan_t p, const double* b_host, double* 
     }
     p->d_solve_ws_bytes = total;
   }
-  const size_t hb = bbytes + xbytes;
-  if (p->h_stage_bytes < hb) {
-    if (p->h_stage) cudaFreeHost(p->h_stage);
-    p->h_stage = nullptr;
-    p->h_stage_bytes = 0;
-    if (cudaMallocHost((void**)&p->h_stage, hb) != cudaSuccess) {
-      az_set_error("az_solve_host: cudaMallocHost(%zu) failed", hb);
-      return AZ_ERR_OUT_OF_MEMORY;
-    }
-    p->h_stage_bytes = hb;
-  }
   char* base = (char*)p->d_solve_ws;
   double* db = (double*)(base + align256(need));
   double* dx = (double*)(base + align256(need) + align256(bbytes));
-  memcpy(p->h_stage, b_host, bbytes);
-  AZ_CUDA_CHECK(cudaMemcpyAsync(db, p->h_stage, bbytes, cudaMemcpyHostToDevice, st));
+  // direct DMA when the caller's buffers are pinned (cudaHostAlloc / torch pin_memory)
+  AZ_CUDA_CHECK(cudaMemcpyAsync(db, b_host, bbytes, cudaMemcpyHostToDevice, st));
   az_status_t s = az_solve(p, db, rows, dx, p->N, nrhs, theta, R, max_blocks, base, need, report, stream);
   if (s != AZ_OK && s != AZ_WARN_SKETCH_SATURATED) return s;
-  double* hx = p->h_stage + rows * nrhs;
-  AZ_CUDA_CHECK(cudaMemcpyAsync(hx, dx, xbytes, cudaMemcpyDeviceToHost, st));
+  AZ_CUDA_CHECK(cudaMemcpyAsync(x_host, dx, xbytes, cudaMemcpyDeviceToHost, st));
   AZ_CUDA_CHECK(cudaStreamSynchronize(st));
-  memcpy(x_host, hx, xbytes);
   return s;
 }

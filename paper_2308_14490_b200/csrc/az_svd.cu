@@ -141,6 +141,7 @@ az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs,
   int64_t* d_rank = (int64_t*)ws;
   AZ_CUDA_CHECK(az_smem_attr(k_jacobi_small, sm));
   const int nth = std::min<int64_t>(1024, std::max<int64_t>(64, 32 * ((r + 1) / 2)));
+  AzTrace tr("jacobi_svd", st);
   k_jacobi_small<<<1, nth, sm, st>>>(Rf, ldr, (int)r, (int)nrhs, theta, y, ldy, sigma_out, d_rank, 60);
   AZ_LAUNCH_CHECK();
   if (rank_out) {
