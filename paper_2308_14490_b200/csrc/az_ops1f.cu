@@ -74,7 +74,7 @@ enum { FC_IN_COEF = 0, FC_FINE_MASK = 1, FC_OUT_GATHER = 2, FC_OUT_RESID = 3, FC
        FC_FWD_G = 6 };
 
 template <int NC, int TC, int KIND, int SRC>
-__global__ void __launch_bounds__(TC * NC / 8) k1f_cols(P1f a, double cout) {
+__global__ void __launch_bounds__(TC * NC / 8, (TC * NC / 8) <= 512 ? 2 : 1) k1f_cols(P1f a, double cout) {
   extern __shared__ cplx sm[];
   constexpr int TPF = NC / 8;
   constexpr int PL = spad_len(NC);
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(TC * NC / 8) k1f_cols(P1f a, double cout) {
     cplx* dst = (KIND == FC_IN_COEF) ? C1b : Gb;
     for (int e = tid; e < NC * TC; e += NT) {
       const int k1 = e / TC, c = e % TC;
-      const int64_t t = ((int64_t)k1 * (c0 + c) * tmul) % a.L;
+      const int64_t t = ((int64_t)k1 * (c0 + c) * tmul) & (a.L - 1);
       dst[(int64_t)k1 * W + c0 + c] = cmul(sm[c * PL + spad(k1)], tw4<-1>(a, t));
     }
   } else if constexpr (KIND == FC_OUT_GATHER || KIND == FC_OUT_RESID) {
@@ -181,17 +181,20 @@ __global__ void __launch_bounds__(TC * NC / 8) k1f_cols(P1f a, double cout) {
 enum { FR_EXPAND = 0, FR_EXPAND_KEEP = 1, FR_STEP1 = 2, FR_RESID = 3, FR_ZSTAR = 4, FR_AT = 5 };
 
 template <int NR2, int LR2, int RPC, int KIND>
-__global__ void __launch_bounds__(RPC * NR2 / 8) k1f_rows(P1f a, int nrows) {
+__global__ void __launch_bounds__(RPC * LR2 / 8, (RPC * LR2 / 8) <= 256 ? 3 : 1) k1f_rows(P1f a, int nrows) {
   extern __shared__ cplx sm[];
-  constexpr int TPF = NR2 / 8;
+  constexpr int TPF = LR2 / 8;           // threads per row (length-L2 FFTs, 8 values per thread)
+  constexpr int TPN = NR2 / 8;           // threads per length-N2 FFT; the other half runs a scratch slot
   constexpr int PLN = spad_len(NR2), PLL = spad_len(LR2);
   constexpr int S = LR2 / NR2;
   const int f = threadIdx.x / TPF, j = threadIdx.x % TPF;
   const int k1 = blockIdx.x * RPC + f;
   const bool live = k1 < nrows;
   const int b = blockIdx.y;
-  cplx* bN = sm + f * (PLN + PLL);
-  cplx* bL = bN + PLN;
+  cplx* bL = sm + f * (PLL + S * PLN);
+  cplx* bN = bL + PLL;                               // real slot; scratch slots follow
+  cplx* bNj = bN + (j / TPN) * PLN;                  // this thread's N2-FFT slot
+  const int jn = j % TPN;
   cplx* C1b = a.C1 + (int64_t)b * a.n;
   cplx* Gb = a.G + (int64_t)b * a.L;
   const double invL = 1.0 / (double)a.L;
@@ -201,13 +204,13 @@ __global__ void __launch_bounds__(RPC * NR2 / 8) k1f_rows(P1f a, int nrows) {
   if constexpr (KIND == FR_EXPAND || KIND == FR_EXPAND_KEEP) {
     for (int e = j; e < NR2; e += TPF) bN[spad(e)] = live ? C1b[rowC + e] : czero();
     __syncthreads();
-    fft_smem<NR2, -1>(bN, j, a.tw, TWN);
+    fft_smem<NR2, -1>(bNj, jn, a.tw, TWN);
     if (KIND == FR_EXPAND_KEEP && live)
       for (int e = j; e < NR2; e += TPF) C1b[rowC + e] = bN[spad(e)];
   } else {
     for (int e = j; e < LR2; e += TPF) bL[spad(e)] = live ? Gb[rowW + e] : czero();
     __syncthreads();
-    fft_smem<LR2, -1, TPF>(bL, j, a.tw, TWN);
+    fft_smem<LR2, -1>(bL, j, a.tw, TWN);
     for (int k2 = j; k2 < NR2; k2 += TPF) {
       cplx acc = czero();
       if (live) {
@@ -221,19 +224,19 @@ __global__ void __launch_bounds__(RPC * NR2 / 8) k1f_rows(P1f a, int nrows) {
     __syncthreads();
   }
   if constexpr (KIND == FR_ZSTAR || KIND == FR_AT) {
-    fft_smem<NR2, 1>(bN, j, a.tw, TWN);
+    fft_smem<NR2, 1>(bNj, jn, a.tw, TWN);
     if (live)
       for (int n2 = j; n2 < NR2; n2 += TPF) {
-        const int64_t t = ((int64_t)n2 * k1 * S) % a.L;     // e^{+2 pi i n2 k1 / n}
+        const int64_t t = ((int64_t)n2 * k1 * S) & (a.L - 1);     // e^{+2 pi i n2 k1 / n}
         C1b[rowC + n2] = cmul(bN[spad(n2)], tw4<1>(a, t));
       }
   } else {
     for (int e = j; e < LR2; e += TPF) bL[spad(e)] = cscale(cmul(bN[spad(e & (NR2 - 1))], sym1f(a, rowW + e)), invL);
     __syncthreads();
-    fft_smem<LR2, 1, TPF>(bL, j, a.tw, TWN);
+    fft_smem<LR2, 1>(bL, j, a.tw, TWN);
     if (live)
       for (int n2 = j; n2 < LR2; n2 += TPF) {
-        const int64_t t = ((int64_t)n2 * k1) % a.L;          // e^{+2 pi i n2' k1 / L}
+        const int64_t t = ((int64_t)n2 * k1) & (a.L - 1);          // e^{+2 pi i n2' k1 / L}
         Gb[rowW + n2] = cmul(bL[spad(n2)], tw4<1>(a, t));
       }
   }
@@ -260,15 +263,15 @@ static az_status_t fcols(const P1f& a, int ncols, int nb, double cout, cudaStrea
 template <int NR2, int KIND>
 static az_status_t frows(const P1f& a, int nb, cudaStream_t st) {
   constexpr int LR2 = 2 * NR2;
-  constexpr int RPC0 = 2048 / NR2;
+  constexpr int RPC0 = 2048 / LR2;
   constexpr int RPC = RPC0 < 1 ? 1 : (RPC0 > 32 ? 32 : RPC0);
-  const size_t sm = (size_t)RPC * (spad_len(NR2) + spad_len(LR2)) * sizeof(cplx);
+  const size_t sm = (size_t)RPC * (spad_len(LR2) + 2 * spad_len(NR2)) * sizeof(cplx);
   auto kern = k1f_rows<NR2, LR2, RPC, KIND>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   static const char* names[] = {"1f_rows_expand", "1f_rows_expand_keep", "1f_rows_step1", "1f_rows_resid",
                                 "1f_rows_zstar", "1f_rows_at"};
   AzTrace tr(names[KIND], st, nb);
-  kern<<<dim3(az_div_up(a.N1, RPC), nb), RPC * NR2 / 8, sm, st>>>(a, a.N1);
+  kern<<<dim3(az_div_up(a.N1, RPC), nb), RPC * LR2 / 8, sm, st>>>(a, a.N1);
   AZ_LAUNCH_CHECK();
   return AZ_OK;
 }

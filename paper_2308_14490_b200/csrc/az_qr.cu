@@ -105,21 +105,33 @@ __global__ void __launch_bounds__(512, 1) k_tsqr(QRIn q) {
         double v[RPL];
 #pragma unroll
         for (int r = 0; r < RPL; ++r) v[r] = vj[lane + 32 * r];
+        // all owned columns at once: KC independent dot products, interleaved warp reductions
+        double p[KC];
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {
+          p[c] = 0.0;
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) p[c] = fma(v[r], x[c][r], p[c]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int c = 0; c < KC; ++c) p[c] += __shfl_xor_sync(0xffffffffu, p[c], o);
+        double rj[KC];
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {
+          const int l = w + 16 * c;
+          rj[c] = (l > j && l < k) ? R[pk(j, l)] : 0.0;
+        }
+        __syncwarp();
 #pragma unroll
         for (int c = 0; c < KC; ++c) {
           const int l = w + 16 * c;
           if (l > j && l < k) {
-            double p = 0.0;
-#pragma unroll
-            for (int r = 0; r < RPL; ++r) p = fma(v[r], x[c][r], p);
-            p = warp_sum(p);
-            const double rjl = R[pk(j, l)];
-            const double wv = rjl + p;
-            const double tw = tau * wv;
+            const double tw = tau * (rj[c] + p[c]);
 #pragma unroll
             for (int r = 0; r < RPL; ++r) x[c][r] = fma(-tw, v[r], x[c][r]);
-            __syncwarp();
-            if (lane == 0) R[pk(j, l)] = rjl - tw;
+            if (lane == 0) R[pk(j, l)] = rj[c] - tw;
           }
         }
       }

@@ -40,9 +40,25 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
   }
   __syncthreads();
   const int n = r + (r & 1);           // padded to even
+  __shared__ double smax2_sweep;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
-    if (tid == 0) rot_count = 0;
+    // column norms at the start of the sweep: pairs whose smaller column is far below the
+    // truncation level (1e-3 theta sigma_1) cannot change the kept part and are skipped
+    for (int i = w; i < r; i += nw) {
+      double a = 0.0;
+      for (int t = lane; t < r; t += 32) a = fma(B[i * r + t], B[i * r + t], a);
+      a = wsum(a);
+      if (lane == 0) nrm2[i] = a;
+    }
     __syncthreads();
+    if (tid == 0) {
+      double m = 0.0;
+      for (int i = 0; i < r; ++i) m = fmax(m, nrm2[i]);
+      smax2_sweep = m;
+      rot_count = 0;
+    }
+    __syncthreads();
+    const double negl = (1e-3 * theta) * (1e-3 * theta) * smax2_sweep;
     for (int round = 0; round < n - 1; ++round) {
       for (int pi = w; pi < n / 2; pi += nw) {
         int p, q;
@@ -67,7 +83,7 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
         a = wsum(a);
         b = wsum(b);
         g = wsum(g);
-        if (g == 0.0 || !(fabs(g) > 1e-15 * sqrt(a) * sqrt(b))) continue;
+        if (g == 0.0 || !(fabs(g) > 1e-15 * sqrt(a) * sqrt(b)) || fmin(a, b) < negl) continue;
         const double zeta = (b - a) / (2.0 * g);
         const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
