@@ -87,6 +87,21 @@ az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs,
                          void* ws, size_t ws_bytes, cudaStream_t st);
 size_t az_tsvd_ws_bytes(int64_t r, int64_t nrhs);
 
+// --- wide (2-D) dense path: blocked Householder QR (az_qrw.cu), block Jacobi SVD (az_svdw.cu)
+constexpr int64_t AZ_NARROW_MAX = 128;    // k <= this: single-pass TSQR / single-CTA Jacobi
+int64_t az_qrw_panel_width();
+size_t az_qrw_ws_bytes(int64_t m, int64_t ncols_max);
+az_status_t az_qrw_apply(const double* V, int64_t ldv, int64_t m, const int64_t* pj0, const int* pnb,
+                         const double* Tbuf, int64_t p0, int64_t p1, double* C, int64_t ldc, int64_t nt, void* ws,
+                         size_t ws_bytes, cudaStream_t st);
+az_status_t az_qrw_factor(double* A, int64_t lda, int64_t m, int64_t c0, int64_t c1, double* Tbuf, int64_t* pj0,
+                          int* pnb, int64_t* np, void* ws, size_t ws_bytes, cudaStream_t st);
+az_status_t az_qrw_extract_R(const double* A, int64_t lda, int64_t k, double* R, int64_t ldr, cudaStream_t st);
+size_t az_tsvdw_ws_bytes(int64_t r, int64_t nrhs);
+az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta, double* y,
+                          int64_t ldy, double* sigma_out, int64_t* rank_out, void* ws, size_t ws_bytes,
+                          cudaStream_t st, int max_sweeps, int* sweeps_out);
+
 
 // Optional per-launch CUDA-event tracing (az_trace_enable): records an event pair around each
 // traced launch on the launching stream; az_trace_report sums the durations per kernel name.

@@ -74,7 +74,7 @@ enum { FC_IN_COEF = 0, FC_FINE_MASK = 1, FC_OUT_GATHER = 2, FC_OUT_RESID = 3, FC
        FC_FWD_G = 6 };
 
 template <int NC, int TC, int KIND, int SRC>
-__global__ void __launch_bounds__(TC * NC / 8, (TC * NC / 8) <= 512 ? 2 : 1) k1f_cols(P1f a, double cout) {
+__global__ void __launch_bounds__(TC * NC / 8, (TC * NC / 8) <= 256 ? 2 : 1) k1f_cols(P1f a, double cout) {
   extern __shared__ cplx sm[];
   constexpr int TPF = NC / 8;
   constexpr int PL = spad_len(NC);
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(TC * NC / 8, (TC * NC / 8) <= 512 ? 2 : 1) k1f
 enum { FR_EXPAND = 0, FR_EXPAND_KEEP = 1, FR_STEP1 = 2, FR_RESID = 3, FR_ZSTAR = 4, FR_AT = 5 };
 
 template <int NR2, int LR2, int RPC, int KIND>
-__global__ void __launch_bounds__(RPC * LR2 / 8, (RPC * LR2 / 8) <= 256 ? 3 : 1) k1f_rows(P1f a, int nrows) {
+__global__ void __launch_bounds__(RPC * LR2 / 8, (RPC * LR2 / 8) <= 256 ? 2 : 1) k1f_rows(P1f a, int nrows) {
   extern __shared__ cplx sm[];
   constexpr int TPF = LR2 / 8;           // threads per row (length-L2 FFTs, 8 values per thread)
   constexpr int TPN = NR2 / 8;           // threads per length-N2 FFT; the other half runs a scratch slot

@@ -14,6 +14,7 @@
 // triangle; each R column is only ever touched by its owner warp, so the only block-wide
 // barrier per column step is the broadcast of the reflector (double-buffered).
 #include <algorithm>
+#include <vector>
 
 #include "az_internal.h"
 
@@ -176,9 +177,28 @@ static az_status_t tsqr_pass(const QRIn& q, int nblocks, cudaStream_t st) {
   return AZ_ERR_NOT_SUPPORTED;
 }
 
+static size_t a256q(size_t v) { return (v + 255) & ~(size_t)255; }
+
 size_t az_qr_ws_bytes(int64_t m, int64_t k) {
+  if (k > AZ_NARROW_MAX) {   // wide: T factors of every panel + the blocked-update workspace
+    const int64_t QBw = az_qrw_panel_width();
+    const int64_t np = (k + QBw - 1) / QBw;
+    return a256q((size_t)np * QBw * QBw * sizeof(double)) + az_qrw_ws_bytes(m, k);
+  }
   const int64_t P = std::max<int64_t>(1, std::min<int64_t>(num_sms(), (m + 127) / 128));
   return (size_t)(2 * P * k * k) * sizeof(double) + 256;
+}
+
+static az_status_t qr_r_wide(double* A, int64_t m, int64_t k, int64_t lda, double* R, int64_t ldr, void* ws,
+                             size_t ws_bytes, cudaStream_t st) {
+  const int64_t QBw = az_qrw_panel_width();
+  const int64_t np = (k + QBw - 1) / QBw;
+  const size_t tb = a256q((size_t)np * QBw * QBw * sizeof(double));
+  std::vector<int64_t> pj0(np);
+  std::vector<int> pnb(np);
+  int64_t cnt = 0;
+  AZ_TRY(az_qrw_factor(A, lda, m, 0, k, (double*)ws, pj0.data(), pnb.data(), &cnt, (char*)ws + tb, ws_bytes - tb, st));
+  return az_qrw_extract_R(A, lda, k, R, ldr, st);
 }
 
 __global__ void k_copy_R(const double* Rin, int k, double* R, int64_t ldr) {
@@ -188,13 +208,16 @@ __global__ void k_copy_R(const double* Rin, int k, double* R, int64_t ldr) {
 
 az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R, int64_t ldr,
                          void* ws, size_t ws_bytes, cudaStream_t st) {
-  if (k > 128) {
-    az_set_error("az_qr_r: k = %lld > 128 (blocked Householder path not built)", (long long)k);
-    return AZ_ERR_NOT_SUPPORTED;
-  }
   if (ws_bytes < az_qr_ws_bytes(m, k)) {
     az_set_error("az_qr_r: workspace too small");
     return AZ_ERR_WORKSPACE;
+  }
+  if (k > AZ_NARROW_MAX) {
+    if (k > m) {
+      az_set_error("az_qr_r: blocked path needs m >= k (m = %lld, k = %lld)", (long long)m, (long long)k);
+      return AZ_ERR_NOT_SUPPORTED;
+    }
+    return qr_r_wide(A, m, k, lda, R, ldr, ws, ws_bytes, st);
   }
   const int64_t P = std::max<int64_t>(1, std::min<int64_t>(num_sms(), (m + 127) / 128));
   double* buf[2] = {(double*)ws, (double*)ws + P * k * k};

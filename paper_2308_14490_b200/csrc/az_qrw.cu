@@ -1,0 +1,425 @@
+// Blocked Householder QR for the wide sketches of the 2-D configs (SURVEY.md §8(a) a7:
+// "tall-skinny QR of [S | b']", k = probes + nrhs up to ~12k columns; "SVD of an
+// (r+p)-by-M matrix ... O(r^2 M)").  Only R (and Q^T b') is needed; Q stays implicit as
+// compact-WY panels  H_p = I - V_p T_p V_p^T  (Schreiber & Van Loan), V_p stored below the diagonal
+// of the factored columns (LAPACK dgeqrf layout, unit diagonal implicit), T_p in a side buffer.
+//
+// Per panel of QB = 64 columns:
+//   k_qr_panel  (cooperative, one CTA per SM): column-by-column Householder (dlarfg convention,
+//               beta = -sign(alpha) ||x||) over the panel; each CTA owns a contiguous row range and
+//               touches only its rows, so the only cross-CTA traffic is two partial-sum vectors per
+//               column (2 grid barriers per column).  The same dot products give T (dlarft, forward
+//               columnwise: T[0:j, j] = -tau_j T[0:j, 0:j] V[:, 0:j]^T v_j).
+//   trailing update  C <- (I - V T^T V^T) C = C - V (T^T (V^T C)):  split-K DMMA GEMM for V^T C,
+//               an ordered reduction fused with T^T, and a DMMA rank-64 update; all reductions run in
+//               a fixed order, so R is bitwise reproducible.
+// New probe blocks are added incrementally: the previous panels are applied to the new columns
+// (az_qrw_apply), then the new columns are factored (az_qrw_factor); the right-hand sides b' get the
+// same treatment, so their top rows end up as Q^T b'.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "az_internal.h"
+#include "az_mma.cuh"
+
+namespace cg = cooperative_groups;
+
+constexpr int QB = 64;            // panel width
+constexpr int PANEL_THREADS = 512;
+
+AZ_D double qr_warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct PanelArgs {
+  double* A;
+  int64_t lda, m;   // rows of A
+  int64_t j0;       // first column (and diagonal row) of the panel
+  int nb;           // panel columns (<= QB)
+  int64_t chunk;    // rows per CTA
+  double* T;        // QB x QB out (column-major)
+  double* part;     // gridDim.x * (1 + QB) partial sums
+};
+
+__global__ void __launch_bounds__(PANEL_THREADS, 1) k_qr_panel(PanelArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[PANEL_THREADS / 32];
+  __shared__ double dsum[QB];
+  __shared__ double Ts[QB * QB];
+  __shared__ double sc[3];
+  const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  constexpr int NW = PANEL_THREADS / 32;
+  const int64_t rb = a.j0 + (int64_t)c * a.chunk;
+  const int64_t re = min(a.m, rb + a.chunk);
+  double* R1 = a.part;          // G
+  double* R2 = a.part + G;      // G x QB
+  for (int e = tid; e < QB * QB; e += PANEL_THREADS) Ts[e] = 0.0;
+  for (int j = 0; j < a.nb; ++j) {
+    const int64_t jc = a.j0 + j;
+    double* col = a.A + jc * a.lda;
+    const int64_t rlo = max(rb, jc + 1);
+    const bool owner = jc >= rb && jc < re;
+    // ---- phase A: ||x(jc+1:m)||^2 partial ----
+    double s = 0.0;
+    for (int64_t r = rlo + tid; r < re; r += PANEL_THREADS) s = fma(col[r], col[r], s);
+    s = qr_warp_sum(s);
+    if (lane == 0) red[w] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int i = 0; i < NW; ++i) t += red[i];
+      R1[c] = t;
+    }
+    grid.sync();
+    // ---- phase B: reflector (every CTA computes the same numbers in the same order) ----
+    if (tid == 0) {
+      double sig = 0.0;
+      for (int i = 0; i < G; ++i) sig += R1[i];
+      const double alpha = col[jc];
+      double beta = alpha, tau = 0.0, scale = 0.0;
+      if (sig > 0.0) {
+        const double nrm = sqrt(fma(alpha, alpha, sig));
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      sc[0] = beta;
+      sc[1] = tau;
+      sc[2] = scale;
+    }
+    __syncthreads();
+    const double scale = sc[2];
+    for (int64_t r = rlo + tid; r < re; r += PANEL_THREADS) col[r] *= scale;
+    __syncthreads();
+    // ---- phase C: d_l = v_j^T A[:, l] over rows >= jc (v_j[jc] = 1), every panel column l != j ----
+    for (int l = w; l < a.nb; l += NW) {
+      if (l == j) continue;
+      const double* cl = a.A + (a.j0 + l) * a.lda;
+      double d = 0.0;
+      for (int64_t r = rlo + lane; r < re; r += 32) d = fma(col[r], cl[r], d);
+      d = qr_warp_sum(d);
+      if (lane == 0) R2[(int64_t)c * QB + l] = d + (owner ? cl[jc] : 0.0);
+    }
+    grid.sync();
+    // ---- phase D: apply H_j to the remaining panel columns; extend T ----
+    const double tau = sc[1];
+    for (int l = tid; l < a.nb; l += PANEL_THREADS) {
+      double t = 0.0;
+      if (l != j)
+        for (int i = 0; i < G; ++i) t += R2[(int64_t)i * QB + l];
+      dsum[l] = t;
+    }
+    __syncthreads();
+    if (tau != 0.0) {
+      const int64_t nr = re - rlo;
+      const int ncl = a.nb - j - 1;
+      if (nr > 0)
+        for (int64_t e = tid; e < nr * ncl; e += PANEL_THREADS) {
+          const int l = j + 1 + (int)(e / nr);
+          const int64_t r = rlo + e % nr;
+          a.A[(a.j0 + l) * a.lda + r] = fma(-tau * dsum[l], col[r], a.A[(a.j0 + l) * a.lda + r]);
+        }
+      if (owner)
+        for (int l = j + 1 + tid; l < a.nb; l += PANEL_THREADS) a.A[(a.j0 + l) * a.lda + jc] -= tau * dsum[l];
+    }
+    if (owner && tid == 0) col[jc] = sc[0];
+    // T[0:j, j] = -tau T[0:j, 0:j] d[0:j];  T[j][j] = tau
+    if (c == 0) {
+      for (int i = tid; i < j; i += PANEL_THREADS) {
+        double t = 0.0;
+        for (int q = i; q < j; ++q) t = fma(Ts[q * QB + i], dsum[q], t);
+        Ts[j * QB + i] = -tau * t;
+      }
+      if (tid == 0) Ts[j * QB + j] = tau;
+    }
+    __syncthreads();
+  }
+  if (c == 0)
+    for (int e = tid; e < QB * QB; e += PANEL_THREADS) a.T[e] = Ts[e];
+}
+
+// ------------------------------------------------------------------------------------------
+// V element (row r, panel column l) with the implicit unit diagonal / zero upper part.
+// ------------------------------------------------------------------------------------------
+AZ_D double v_elem(const double* A, int64_t lda, int64_t j0, int nb, int64_t r, int l) {
+  if (l >= nb) return 0.0;
+  const int64_t d = r - j0;
+  if (d < QB) {
+    if (d == l) return 1.0;
+    if (d < l) return 0.0;
+  }
+  return A[(j0 + l) * lda + r];
+}
+
+struct UpdArgs {
+  const double* V;   // the factored matrix holding the panel (column j0.. of it)
+  int64_t ldv;
+  int64_t j0;        // panel's first column == first active row
+  int nb;
+  int64_t m;         // rows
+  double* C;         // target columns (rows indexed like V)
+  int64_t ldc;
+  int64_t nt;        // target column count
+  int64_t kchunk;    // rows per split-K chunk
+  double* Wpart;     // KC x QB x nt
+  double* Wfin;      // QB x nt (column-major, ld QB)
+  const double* T;   // QB x QB
+};
+
+// Wpart[kc] = V^T C over rows [j0 + kc kchunk, ...): CTA tile 64 (panel cols) x 64 (target cols).
+constexpr int VT_BK = 32, VT_S = 36;
+__global__ void __launch_bounds__(256) k_qr_vtc(UpdArgs a) {
+  __shared__ double smv[2 * QB * VT_S];
+  double* As = smv;                  // IMAJ [m = panel col][k = row]
+  double* Bs = smv + QB * VT_S;      // IMAJ [n = target col][k = row]
+  static_assert(4 * 32 * 33 <= 2 * QB * VT_S, "reduction scratch must fit in the operand tiles");
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wm = w & 1, wn = (w >> 1) & 1, wk = w >> 2;
+  const int64_t n0 = (int64_t)blockIdx.x * 64;
+  const int kc = blockIdx.y;
+  const int64_t r0 = a.j0 + (int64_t)kc * a.kchunk;
+  const int64_t r1 = min(a.m, r0 + a.kchunk);
+  double acc[4][4][2];
+  acc_zero(acc);
+  // per-thread load slots: 64 x 32 tile = 2048 elements = 8 per thread; k fastest
+  const int lk = tid & 31, li = tid >> 5;   // element (i = li + 8 t, k = lk)
+  for (int64_t rr = r0; rr < r1; rr += VT_BK) {
+    const int64_t r = rr + lk;
+    double va[8], vb[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int i = li + 8 * t;
+      va[t] = r < r1 ? v_elem(a.V, a.ldv, a.j0, a.nb, r, i) : 0.0;
+      vb[t] = (r < r1 && n0 + i < a.nt) ? a.C[(n0 + i) * a.ldc + r] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      As[(li + 8 * t) * VT_S + lk] = va[t];
+      Bs[(li + 8 * t) * VT_S + lk] = vb[t];
+    }
+    __syncthreads();
+    warp_mma<4, 4, IMAJ, IMAJ>(acc, As, VT_S, Bs, VT_S, wm * 32, wn * 32, wk * 16, 16, lane);
+  }
+  // reduce the two k halves: warps wk = 1 write, wk = 0 add (scratch reuses the operand tiles)
+  __syncthreads();
+  double* rs = smv + (w & 3) * 32 * 33;
+  if (wk == 1) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) rs[acc_row(0, i, lane) * 33 + acc_col(0, j, e, lane)] = acc[i][j][e];
+  }
+  __syncthreads();
+  if (wk == 0) {
+    double* W = a.Wpart + (int64_t)kc * QB * a.nt;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int ml = acc_row(0, i, lane), nl = acc_col(0, j, e, lane);
+          const int64_t n = n0 + wn * 32 + nl;
+          if (n < a.nt) W[n * QB + wm * 32 + ml] = acc[i][j][e] + rs[ml * 33 + nl];
+        }
+  }
+}
+
+// Wfin[:, n] = T^T sum_kc Wpart[kc][:, n]   (ordered sum; 4 target columns per CTA, 64 threads each)
+__global__ void __launch_bounds__(256) k_qr_wred(UpdArgs a, int KC) {
+  __shared__ double Ts[QB * QB];
+  __shared__ double ws[4][QB];
+  const int tid = threadIdx.x, l = tid & 63, g = tid >> 6;
+  for (int e = tid; e < QB * QB; e += 256) Ts[e] = a.T[e];
+  const int64_t n = (int64_t)blockIdx.x * 4 + g;
+  double s = 0.0;
+  if (n < a.nt)
+    for (int kc = 0; kc < KC; ++kc) s += a.Wpart[(int64_t)kc * QB * a.nt + n * QB + l];
+  ws[g][l] = s;
+  __syncthreads();
+  if (n < a.nt) {
+    double t = 0.0;
+    for (int i = 0; i <= l; ++i) t = fma(Ts[l * QB + i], ws[g][i], t);   // (T^T)[l][i] = T[i][l]
+    a.Wfin[n * QB + l] = t;
+  }
+}
+
+// C[rows j0.., n] -= V[rows, 0:QB] Wfin[0:QB, n]: CTA tile 128 rows x 64 columns, K = QB at once.
+constexpr int UP_SA = 132, UP_SB = 68;
+__global__ void __launch_bounds__(256) k_qr_upd(UpdArgs a) {
+  extern __shared__ double sm[];
+  double* As = sm;                    // KMAJ [k = panel col][m = row], stride 132
+  double* Bs = sm + QB * UP_SA;       // IMAJ [n = target col][k], stride 68
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wm = w & 3, wn = w >> 2;
+  const int64_t rbase = a.j0 + (int64_t)blockIdx.x * 128;
+  const int64_t n0 = (int64_t)blockIdx.y * 64;
+  for (int e = tid; e < QB * 128; e += 256) {
+    const int l = e >> 7, ri = e & 127;
+    const int64_t r = rbase + ri;
+    As[l * UP_SA + ri] = r < a.m ? v_elem(a.V, a.ldv, a.j0, a.nb, r, l) : 0.0;
+  }
+  for (int e = tid; e < QB * 64; e += 256) {
+    const int n = e >> 6, l = e & 63;
+    Bs[n * UP_SB + l] = (n0 + n < a.nt) ? a.Wfin[(n0 + n) * QB + l] : 0.0;
+  }
+  __syncthreads();
+  double acc[4][4][2];
+  acc_zero(acc);
+  warp_mma<4, 4, KMAJ, IMAJ>(acc, As, UP_SA, Bs, UP_SB, wm * 32, wn * 32, 0, QB, lane);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t r = rbase + acc_row(wm * 32, i, lane);
+        const int64_t n = n0 + acc_col(wn * 32, j, e, lane);
+        if (r < a.m && n < a.nt) a.C[n * a.ldc + r] -= acc[i][j][e];
+      }
+}
+
+// ------------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------------
+static int qrw_sms() {
+  static int s = 0;
+  if (!s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+    if (s <= 0) s = 148;
+  }
+  return s;
+}
+
+static int64_t qrw_kc(int64_t rows) {   // split-K chunks for V^T C
+  return std::max<int64_t>(1, std::min<int64_t>(4 * qrw_sms(), (rows + 255) / 256));
+}
+
+// workspace: [panel partials | Wpart (KC x QB x nt) | Wfin (QB x nt)]
+static size_t qrw_part_bytes() { return ((size_t)qrw_sms() * (1 + QB) * sizeof(double) + 255) & ~(size_t)255; }
+
+size_t az_qrw_ws_bytes(int64_t m, int64_t ncols_max) {
+  const int64_t KC = qrw_kc(m);
+  const int64_t nt = std::max<int64_t>(ncols_max, 64);
+  return qrw_part_bytes() + (size_t)(KC + 1) * QB * nt * sizeof(double) + 256;
+}
+
+// Apply panels [p0, p1) of the factored matrix V (panel p = columns p QB ..) to the target columns.
+// Panel p starts at column pj0[p] (== its first active row) and has pnb[p] columns; its T is at
+// Tbuf + p QB^2.
+az_status_t az_qrw_apply(const double* V, int64_t ldv, int64_t m, const int64_t* pj0, const int* pnb,
+                         const double* Tbuf, int64_t p0, int64_t p1, double* C, int64_t ldc, int64_t nt, void* ws,
+                         size_t ws_bytes, cudaStream_t st) {
+  if (nt <= 0) return AZ_OK;
+  if (ws_bytes < az_qrw_ws_bytes(m, nt)) {
+    az_set_error("az_qrw_apply: workspace too small");
+    return AZ_ERR_WORKSPACE;
+  }
+  const size_t ups = (size_t)(QB * UP_SA + 64 * UP_SB) * sizeof(double);
+  AZ_CUDA_CHECK(az_smem_attr(k_qr_upd, ups));
+  for (int64_t p = p0; p < p1; ++p) {
+    UpdArgs u;
+    u.V = V;
+    u.ldv = ldv;
+    u.j0 = pj0[p];
+    u.nb = pnb[p];
+    u.m = m;
+    u.C = C;
+    u.ldc = ldc;
+    u.nt = nt;
+    const int64_t rows = m - u.j0;
+    if (rows <= 0) break;
+    const int64_t KC = qrw_kc(rows);
+    u.kchunk = (rows + KC - 1) / KC;
+    u.Wpart = (double*)((char*)ws + qrw_part_bytes());
+    u.Wfin = u.Wpart + (size_t)KC * QB * nt;
+    u.T = Tbuf + p * QB * QB;
+    {
+      AzTrace tr("qrw_vtc", st, 2 * rows * u.nb * nt);
+      k_qr_vtc<<<dim3(az_div_up(nt, 64), (unsigned)KC), 256, 0, st>>>(u);
+      AZ_LAUNCH_CHECK();
+    }
+    {
+      AzTrace tr("qrw_wred", st);
+      k_qr_wred<<<az_div_up(nt, 4), 256, 0, st>>>(u, (int)KC);
+      AZ_LAUNCH_CHECK();
+    }
+    {
+      AzTrace tr("qrw_upd", st, 2 * rows * u.nb * nt);
+      k_qr_upd<<<dim3(az_div_up(rows, 128), az_div_up(nt, 64)), 256, ups, st>>>(u);
+      AZ_LAUNCH_CHECK();
+    }
+  }
+  return AZ_OK;
+}
+
+// Factor columns [c0, c1) of A (columns < c0 already factored and applied to these columns).
+// Appends the new panels to (pj0, pnb) starting at index *np (capacity checked by the caller).
+az_status_t az_qrw_factor(double* A, int64_t lda, int64_t m, int64_t c0, int64_t c1, double* Tbuf, int64_t* pj0,
+                          int* pnb, int64_t* np, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (c1 > m) {
+    az_set_error("az_qrw_factor: more columns (%lld) than rows (%lld)", (long long)c1, (long long)m);
+    return AZ_ERR_NOT_SUPPORTED;
+  }
+  if (ws_bytes < az_qrw_ws_bytes(m, c1 - c0)) {
+    az_set_error("az_qrw_factor: workspace too small");
+    return AZ_ERR_WORKSPACE;
+  }
+  int maxb = 0;
+  AZ_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, k_qr_panel, PANEL_THREADS, 0));
+  if (maxb < 1) {
+    az_set_error("az_qrw_factor: panel kernel cannot be resident");
+    return AZ_ERR_CUDA;
+  }
+  double* part = (double*)ws;
+  for (int64_t j0 = c0; j0 < c1; j0 += QB) {
+    PanelArgs pa;
+    pa.A = A;
+    pa.lda = lda;
+    pa.m = m;
+    pa.j0 = j0;
+    pa.nb = (int)std::min<int64_t>(QB, c1 - j0);
+    const int64_t rows = m - j0;
+    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(qrw_sms(), (rows + 127) / 128));
+    pa.chunk = (rows + G - 1) / G;
+    const int64_t p = (*np)++;
+    pj0[p] = j0;
+    pnb[p] = pa.nb;
+    pa.T = Tbuf + p * QB * QB;
+    pa.part = part;
+    void* args[] = {&pa};
+    {
+      AzTrace tr("qrw_panel", st, rows * pa.nb);
+      AZ_CUDA_CHECK(cudaLaunchCooperativeKernel((void*)k_qr_panel, dim3((unsigned)G), dim3(PANEL_THREADS), args, 0, st));
+      az_count_launch();
+    }
+    const int64_t nt = c1 - (j0 + pa.nb);
+    if (nt > 0)
+      AZ_TRY(az_qrw_apply(A, lda, m, pj0, pnb, Tbuf, p, p + 1, A + (j0 + pa.nb) * lda, lda, nt, ws, ws_bytes, st));
+  }
+  return AZ_OK;
+}
+
+// R (k x k, upper; strict lower zeroed) out of the factored matrix.
+__global__ void k_qrw_extract_R(const double* A, int64_t lda, int64_t k, double* R, int64_t ldr) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= k * k) return;
+  const int64_t i = e % k, l = e / k;
+  R[l * ldr + i] = i <= l ? A[l * lda + i] : 0.0;
+}
+
+az_status_t az_qrw_extract_R(const double* A, int64_t lda, int64_t k, double* R, int64_t ldr, cudaStream_t st) {
+  k_qrw_extract_R<<<az_div_up(k * k, 256), 256, 0, st>>>(A, lda, k, R, ldr);
+  AZ_LAUNCH_CHECK();
+  return AZ_OK;
+}
+
+int64_t az_qrw_panel_width() { return QB; }

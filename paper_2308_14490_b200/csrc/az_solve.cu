@@ -137,6 +137,9 @@ struct SolveWS {
   size_t qrbytes;
   void* svdws;
   size_t svdbytes;
+  double* Tb;    // wide path: T factors of every panel
+  int64_t maxpanels;
+  bool wide;
   size_t total;
 };
 
@@ -160,7 +163,17 @@ static SolveWS layout(az_plan_s* p, int64_t nrhs, int64_t R, int32_t max_blocks,
   w.sig = (double*)take(sizeof(double) * Rmax);
   w.tmp = (double*)take(sizeof(double) * rows * nrhs);
   w.x2 = (double*)take(sizeof(double) * p->N * nrhs);
-  w.qrbytes = az_qr_ws_bytes(rows, kt);
+  w.wide = kt > AZ_NARROW_MAX;
+  if (w.wide) {
+    const int64_t QBw = az_qrw_panel_width();
+    w.maxpanels = max_blocks * ((R + QBw - 1) / QBw);
+    w.Tb = (double*)take(sizeof(double) * w.maxpanels * QBw * QBw);
+    w.qrbytes = az_qrw_ws_bytes(rows, std::max<int64_t>(R, nrhs));
+  } else {
+    w.maxpanels = 0;
+    w.Tb = nullptr;
+    w.qrbytes = az_qr_ws_bytes(rows, kt);
+  }
   w.qrws = take(w.qrbytes);
   w.svdbytes = az_tsvd_ws_bytes(Rmax, nrhs);
   w.svdws = take(w.svdbytes);
@@ -199,12 +212,8 @@ az_status_t az_apply_op(az_plan_s* p, int op, const double* in, int64_t ldin, do
 extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, double* x, int64_t ldx, int64_t nrhs,
                                 double theta, int64_t R, int32_t max_blocks, void* workspace, size_t ws_bytes,
                                 az_solve_report_t* report, void* stream) {
-  if (!p || !b || !x || nrhs < 1 || R < 2 || max_blocks < 1 || !(theta >= 0.0) || ldb < p->M + p->Mb || ldx < p->N) {
+  if (!p || !b || !x || nrhs < 1 || R < 1 || max_blocks < 1 || !(theta >= 0.0) || ldb < p->M + p->Mb || ldx < p->N) {
     az_set_error("az_solve: bad arguments");
-    return AZ_ERR_INVALID_ARGUMENT;
-  }
-  if (R % 2) {
-    az_set_error("az_solve: R must be even (probe pairs)");
     return AZ_ERR_INVALID_ARGUMENT;
   }
   SolveWS w = layout(p, nrhs, R, max_blocks, nullptr);
@@ -224,19 +233,40 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   double ms_sketch = 0, ms_qr = 0, ms_svd = 0;
   int64_t rank = 0, nb = 0;
   bool saturated = false;
+  // wide path (2-D): incremental blocked Householder; panels of earlier blocks are applied to
+  // each new block, and every panel is applied to b' (which becomes Q^T b' in its top rows)
+  std::vector<int64_t> pj0(w.maxpanels);
+  std::vector<int> pnb(w.maxpanels);
+  int64_t np = 0;
   for (nb = 1; nb <= max_blocks; ++nb) {
     const int64_t kp = nb * R;                 // probe columns
     const int64_t kt = kp + nrhs;
     cudaEvent_t e0 = ev.e[2], e1 = ev.e[3], e2 = ev.e[4], e3 = ev.e[5];
     cudaEventRecord(e0, st);
     AZ_TRY(az_sketch(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, st));
-    {
+    if (!w.wide) {
       AzTrace tr("elementwise", st);
       k_copy_cols<<<az_div_up(rows * nrhs, 256), 256, 0, st>>>(w.bp, rows, w.S + kp * rows, rows, rows, nrhs);
+      AZ_LAUNCH_CHECK();
     }
-    AZ_LAUNCH_CHECK();
     cudaEventRecord(e1, st);
-    AZ_TRY(az_qr_r_impl(w.S, rows, kt, rows, w.Rf, kt, w.qrws, w.qrbytes, st));
+    if (!w.wide) {
+      AZ_TRY(az_qr_r_impl(w.S, rows, kt, rows, w.Rf, kt, w.qrws, w.qrbytes, st));
+    } else {
+      if (kp > rows) {
+        az_set_error("az_solve: %lld probe columns exceed the %lld rows", (long long)kp, (long long)rows);
+        return AZ_ERR_NOT_SUPPORTED;
+      }
+      double* Snew = w.S + (nb - 1) * R * rows;
+      AZ_TRY(az_qrw_apply(w.S, rows, rows, pj0.data(), pnb.data(), w.Tb, 0, np, Snew, rows, R, w.qrws, w.qrbytes, st));
+      const int64_t np0 = np;
+      AZ_TRY(az_qrw_factor(w.S, rows, rows, (nb - 1) * R, kp, w.Tb, pj0.data(), pnb.data(), &np, w.qrws, w.qrbytes, st));
+      AZ_TRY(az_qrw_apply(w.S, rows, rows, pj0.data(), pnb.data(), w.Tb, np0, np, w.bp, rows, nrhs, w.qrws, w.qrbytes, st));
+      AZ_TRY(az_qrw_extract_R(w.S, rows, kp, w.Rf, kt, st));
+      AzTrace tr("elementwise", st);
+      k_copy_cols<<<az_div_up(kp * nrhs, 256), 256, 0, st>>>(w.bp, rows, w.Rf + kp * kt, kt, kp, nrhs);
+      AZ_LAUNCH_CHECK();
+    }
     cudaEventRecord(e2, st);
     AZ_TRY(az_tsvd_impl(w.Rf, kt, kp, nrhs, theta, w.y, kp, w.sig, &rank, w.svdws, w.svdbytes, st));
     cudaEventRecord(e3, st);

@@ -139,11 +139,14 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
   }
 }
 
-size_t az_tsvd_ws_bytes(int64_t r, int64_t nrhs) { return 256; }
+size_t az_tsvd_ws_bytes(int64_t r, int64_t nrhs) {
+  return r > AZ_NARROW_MAX ? az_tsvdw_ws_bytes(r, nrhs) : 256;
+}
 
 az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta, double* y,
                          int64_t ldy, double* sigma_out, int64_t* rank_out, void* ws, size_t ws_bytes,
                          cudaStream_t st) {
+  if (r > AZ_NARROW_MAX) return az_tsvdw_impl(Rf, ldr, r, nrhs, theta, y, ldy, sigma_out, rank_out, ws, ws_bytes, st, 40, nullptr);
   const size_t sm = (size_t)(r * r + r * nrhs + r) * sizeof(double);
   if (sm > 220 * 1024) {
     az_set_error("az_tsvd_solve: r = %lld, nrhs = %lld exceed the single-CTA Jacobi (multi-CTA path not built)",

@@ -1,0 +1,434 @@
+// Truncated SVD solve for wide sketches (r > 128, "followed by
+// the SVD"): block one-sided Jacobi on B = R_S^T with DMMA Gram matrices.
+//
+// As in az_svd.cu, one-sided Jacobi orthogonalises the columns of B = R_S^T:  B W = U' Sigma, so
+// R_S = W Sigma U'^T, W holds the left singular vectors of R_S and is applied to c = Q^T b' on the
+// fly (c <- W^T c); finally y = sum_{sigma_i > theta sigma_1} (B W)_i (W^T c)_i / sigma_i^2.
+// Block version (columns in blocks of BW = 32, pairs of blocks -> X = [B_i B_j], r x 64):
+//   G = X^T X                      (DMMA, fixed-order reduction)
+//   G = V diag V^T                 (cyclic two-sided Jacobi on G in shared memory)
+//   X <- X V,   c_pair <- V^T c_pair
+// All block pairs of a round-robin round are disjoint and run as one launch (one CTA per pair);
+// a sweep is nblk - 1 rounds.  Convergence: max over pairs of |G_pq| / sqrt(G_pp G_qq) below
+// tol = 4 u sqrt(r) (the rounding level of a length-r dot product of orthogonal columns), ignoring
+// columns whose norm is far below the truncation level (1e-3 theta sigma_1), which cannot change
+// the kept part of the solution (same skip rule as az_svd.cu).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "az_internal.h"
+#include "az_mma.cuh"
+
+constexpr int BW = 32;        // columns per block
+constexpr int PW = 2 * BW;    // pair width
+constexpr int GS = PW + 1;    // G stride (conflict-free row and column access)
+constexpr int VS = PW + 4;    // V stride (B operand, KMAJ)
+constexpr int XS = PW + 4;    // X tile stride
+constexpr int GK = 32, GKS = GK + 4;   // Gram staging: [col][k], stride 36
+
+struct BJArgs {
+  double* B;        // r x r, column-major, ld = r
+  int64_t r;
+  double* C;        // r x nrhs, ld = r
+  int nrhs;
+  int nblk;         // column blocks (padded to even in the schedule)
+  const double* smax2;    // max squared column norm at the start of the sweep
+  double theta;
+  unsigned long long* off;  // max relative off-diagonal seen this sweep (double bits, >= 0)
+  double tol;               // rotate while |G_pq| > tol sqrt(G_pp G_qq)
+  int inner_sweeps;
+};
+
+AZ_D void pair_of(int round, int pi, int n, int& p, int& q) {
+  if (pi == 0) {
+    p = round;
+    q = n - 1;
+  } else {
+    p = (round + pi) % (n - 1);
+    q = (round - pi + (n - 1)) % (n - 1);
+  }
+  if (p > q) {
+    const int t = p;
+    p = q;
+    q = t;
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
+  extern __shared__ double sm[];
+  double* G = sm;                     // PW x GS
+  double* V = G + PW * GS;            // PW x VS  (V[t][p] at t * VS + p)
+  double* X = V + PW * VS;            // staging: Gram [col][k] (PW x GKS) / update [col][row] (PW x XS)
+  double* Cs = X + PW * XS;           // PW x nrhs (C rows of the pair)
+  __shared__ double rc[PW / 2], rs[PW / 2];
+  __shared__ int rp[PW / 2], rq[PW / 2];
+  __shared__ int any_rot;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int n = a.nblk + (a.nblk & 1);
+  int bi, bj;
+  pair_of(round, blockIdx.x, n, bi, bj);
+  if (bj >= a.nblk) return;
+  const int64_t r = a.r;
+  // column of X -> column of B (or -1 past the end)
+  auto bcol = [&](int c) -> int64_t {
+    const int64_t col = (c < BW) ? (int64_t)bi * BW + c : (int64_t)bj * BW + (c - BW);
+    return col < r ? col : -1;
+  };
+  // ---------------- Gram G = X^T X ----------------
+  {
+    const int wm = w & 1, wn = (w >> 1) & 1, wk = w >> 2;
+    double acc[4][4][2];
+    acc_zero(acc);
+    const int lk = tid & 31, li = tid >> 5;
+    int64_t colp[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) colp[t] = bcol(li + 8 * t);
+    for (int64_t k0 = 0; k0 < r; k0 += GK) {
+      const int64_t k = k0 + lk;
+      double v[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) v[t] = (k < r && colp[t] >= 0) ? a.B[colp[t] * r + k] : 0.0;
+      __syncthreads();
+#pragma unroll
+      for (int t = 0; t < 8; ++t) X[(li + 8 * t) * GKS + lk] = v[t];
+      __syncthreads();
+      warp_mma<4, 4, IMAJ, IMAJ>(acc, X, GKS, X, GKS, wm * 32, wn * 32, wk * 16, 16, lane);
+    }
+    // reduce k halves into G
+    if (wk == 1)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            G[acc_row(wm * 32, i, lane) * GS + acc_col(wn * 32, j, e, lane)] = acc[i][j][e];
+    __syncthreads();
+    if (wk == 0)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            G[acc_row(wm * 32, i, lane) * GS + acc_col(wn * 32, j, e, lane)] += acc[i][j][e];
+    __syncthreads();
+  }
+  // ---------------- convergence measure over the pair's cross and intra terms ----------------
+  const double negl = (1e-3 * a.theta) * (1e-3 * a.theta) * (*a.smax2);
+  {
+    double mx = 0.0;
+    for (int e = tid; e < PW * PW; e += 256) {
+      const int p = e / PW, q = e % PW;
+      if (p < q) {
+        const double gp = G[p * GS + p], gq = G[q * GS + q];
+        if (fmin(gp, gq) >= negl && gp > 0.0 && gq > 0.0) mx = fmax(mx, fabs(G[p * GS + q]) / sqrt(gp * gq));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0 && mx > 0.0) atomicMax(a.off, (unsigned long long)__double_as_longlong(mx));
+    if (tid == 0) any_rot = 0;
+    __syncthreads();
+    if (lane == 0 && mx > a.tol) atomicOr(&any_rot, 1);
+    __syncthreads();
+    if (!any_rot) return;     // pair already orthogonal: X and c unchanged
+  }
+  // ---------------- eigen-decomposition of G by cyclic Jacobi ----------------
+  for (int e = tid; e < PW * PW; e += 256) V[(e / PW) * VS + (e % PW)] = (e / PW == e % PW) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int sw = 0; sw < a.inner_sweeps; ++sw) {
+    if (tid == 0) any_rot = 0;
+    __syncthreads();
+    for (int rd = 0; rd < PW - 1; ++rd) {
+      if (tid < PW / 2) {
+        int p, q;
+        pair_of(rd, tid, PW, p, q);
+        const double gp = G[p * GS + p], gq = G[q * GS + q], g = G[p * GS + q];
+        double c = 1.0, s = 0.0;
+        if (g != 0.0 && fabs(g) > a.tol * sqrt(gp * gq) && fmin(gp, gq) >= negl) {
+          const double zeta = (gq - gp) / (2.0 * g);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          c = 1.0 / sqrt(1.0 + t * t);
+          s = c * t;
+          any_rot = 1;
+        }
+        rc[tid] = c;
+        rs[tid] = s;
+        rp[tid] = p;
+        rq[tid] = q;
+      }
+      __syncthreads();
+      // rows p, q of G
+      for (int e = tid; e < (PW / 2) * PW; e += 256) {
+        const int k = e / PW, t = e % PW;
+        const double c = rc[k], s = rs[k];
+        if (s == 0.0) continue;
+        const int p = rp[k], q = rq[k];
+        const double xp = G[p * GS + t], xq = G[q * GS + t];
+        G[p * GS + t] = c * xp - s * xq;
+        G[q * GS + t] = s * xp + c * xq;
+      }
+      __syncthreads();
+      // columns p, q of G and of V
+      for (int e = tid; e < (PW / 2) * PW; e += 256) {
+        const int k = e / PW, t = e % PW;
+        const double c = rc[k], s = rs[k];
+        if (s == 0.0) continue;
+        const int p = rp[k], q = rq[k];
+        const double xp = G[t * GS + p], xq = G[t * GS + q];
+        G[t * GS + p] = c * xp - s * xq;
+        G[t * GS + q] = s * xp + c * xq;
+        const double vp = V[t * VS + p], vq = V[t * VS + q];
+        V[t * VS + p] = c * vp - s * vq;
+        V[t * VS + q] = s * vp + c * vq;
+      }
+      __syncthreads();
+    }
+    if (!any_rot) break;
+  }
+  // ---------------- X <- X V over row tiles of 64 ----------------
+  {
+    const int wm = w & 1, wn = w >> 1;       // warp tile 32 rows x 16 cols
+    const int lr = tid & 63, lc = tid >> 6;  // load: element (row lr, col lc + 4 t)
+    for (int64_t r0 = 0; r0 < r; r0 += 64) {
+      __syncthreads();
+      for (int t = 0; t < 16; ++t) {
+        const int c = lc + 4 * t;
+        const int64_t col = bcol(c);
+        const int64_t row = r0 + lr;
+        X[c * XS + lr] = (col >= 0 && row < r) ? a.B[col * r + row] : 0.0;
+      }
+      __syncthreads();
+      double acc[4][2][2];
+      acc_zero(acc);
+      warp_mma<4, 2, KMAJ, KMAJ>(acc, X, XS, V, VS, wm * 32, wn * 16, 0, PW, lane);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int64_t row = r0 + acc_row(wm * 32, i, lane);
+            const int64_t col = bcol(acc_col(wn * 16, j, e, lane));
+            if (col >= 0 && row < r) a.B[col * r + row] = acc[i][j][e];
+          }
+    }
+  }
+  // ---------------- c rows of the pair <- V^T c ----------------
+  if (a.nrhs > 0) {
+    __syncthreads();
+    for (int e = tid; e < PW * a.nrhs; e += 256) {
+      const int k = e % PW, c = e / PW;
+      const int64_t row = bcol(k);
+      Cs[c * PW + k] = row >= 0 ? a.C[(int64_t)c * r + row] : 0.0;
+    }
+    __syncthreads();
+    for (int e = tid; e < PW * a.nrhs; e += 256) {
+      const int nn = e % PW, c = e / PW;
+      const int64_t row = bcol(nn);
+      if (row < 0) continue;
+      double t = 0.0;
+      for (int k = 0; k < PW; ++k) t = fma(V[k * VS + nn], Cs[c * PW + k], t);
+      a.C[(int64_t)c * r + row] = t;
+    }
+  }
+}
+
+// squared column norms of B and their max
+__global__ void __launch_bounds__(256) k_bjac_colnorms(const double* B, int64_t r, double* nrm2) {
+  const int64_t col = blockIdx.x;
+  double s = 0.0;
+  for (int64_t t = threadIdx.x; t < r; t += 256) s = fma(B[col * r + t], B[col * r + t], s);
+  __shared__ double red[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < 8; ++i) t += red[i];
+    nrm2[col] = t;
+  }
+}
+
+__global__ void k_bjac_max(const double* nrm2, int64_t r, double* smax2, unsigned long long* off) {
+  __shared__ double red[32];
+  double m = 0.0;
+  for (int64_t i = threadIdx.x; i < r; i += blockDim.x) m = fmax(m, nrm2[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = fmax(t, red[i]);
+    *smax2 = t;
+    *off = 0ull;
+  }
+}
+
+// y[t][c] = sum_{kept i} B[t][i] C[i][c] / nrm2[i]   (kept: nrm2 > theta^2 smax2); 32 rhs per CTA
+__global__ void __launch_bounds__(256) k_bjac_solve(const double* B, const double* C, const double* nrm2,
+                                                    const double* smax2, int64_t r, int nrhs, double theta,
+                                                    double* y, int64_t ldy) {
+  __shared__ double Ds[64][33];   // D[i][c] for 64 i
+  const int64_t t = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int c0 = blockIdx.y * 32;
+  const int nc = min(32, nrhs - c0);
+  const double thr2 = theta * theta * (*smax2);
+  double acc[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+  for (int64_t i0 = 0; i0 < r; i0 += 64) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 64 * 32; e += 256) {
+      const int ii = e % 64, c = e / 64;
+      const int64_t i = i0 + ii;
+      double d = 0.0;
+      if (i < r && c < nc) {
+        const double s2 = nrm2[i];
+        if (s2 > thr2 && s2 > 0.0) d = C[(int64_t)(c0 + c) * r + i] / s2;
+      }
+      Ds[ii][c] = d;
+    }
+    __syncthreads();
+    if (t < r)
+      for (int ii = 0; ii < 64 && i0 + ii < r; ++ii) {
+        const double b = B[(i0 + ii) * r + t];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) acc[c] = fma(b, Ds[ii][c], acc[c]);
+      }
+  }
+  if (t < r)
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      if (c < nc) y[(int64_t)(c0 + c) * ldy + t] = acc[c];
+}
+
+// sorted singular values (rank by counting) and the kept count
+__global__ void k_bjac_sigma(const double* nrm2, const double* smax2, int64_t r, double theta, double* sig_out,
+                             int64_t* rank_dev) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const double thr2 = theta * theta * (*smax2);
+  if (i < r) {
+    const double v = nrm2[i];
+    int64_t pos = 0;
+    for (int64_t t = 0; t < r; ++t) {
+      const double u = nrm2[t];
+      pos += (u > v || (u == v && t < i));
+    }
+    if (sig_out) sig_out[pos] = sqrt(v);
+    if (v > thr2 && v > 0.0) atomicAdd((unsigned long long*)rank_dev, 1ull);
+  }
+}
+
+// B = R_S^T, C = c
+__global__ void k_bjac_load(const double* Rf, int64_t ldr, int64_t r, int nrhs, double* B, double* C) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < r * r) {
+    const int64_t i = e % r, t = e / r;   // B[t][i] = R_S[i][t] -> B(col i, row t) at i * r + t
+    B[i * r + t] = (i <= t) ? Rf[t * ldr + i] : 0.0;
+  }
+  if (e < r * nrhs) {
+    const int64_t p = e % r, c = e / r;
+    C[c * r + p] = Rf[(r + c) * ldr + p];
+  }
+}
+
+static size_t a256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+size_t az_tsvdw_ws_bytes(int64_t r, int64_t nrhs) {
+  return a256(sizeof(double) * r * r) + a256(sizeof(double) * r * nrhs) + a256(sizeof(double) * r) + 1024;
+}
+
+az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta, double* y,
+                          int64_t ldy, double* sigma_out, int64_t* rank_out, void* ws, size_t ws_bytes,
+                          cudaStream_t st, int max_sweeps, int* sweeps_out) {
+  if (ws_bytes < az_tsvdw_ws_bytes(r, nrhs)) {
+    az_set_error("az_tsvd_solve (block Jacobi): workspace too small");
+    return AZ_ERR_WORKSPACE;
+  }
+  char* p = (char*)ws;
+  double* B = (double*)p;
+  p += a256(sizeof(double) * r * r);
+  double* C = (double*)p;
+  p += a256(sizeof(double) * r * nrhs);
+  double* nrm2 = (double*)p;
+  p += a256(sizeof(double) * r);
+  double* smax2 = (double*)p;
+  unsigned long long* off = (unsigned long long*)(p + 64);
+  int64_t* d_rank = (int64_t*)(p + 128);
+  {
+    AzTrace tr("bjac_load", st);
+    k_bjac_load<<<az_div_up(r * std::max<int64_t>(r, nrhs), 256), 256, 0, st>>>(Rf, ldr, r, (int)nrhs, B, C);
+    AZ_LAUNCH_CHECK();
+  }
+  const int nblk = (int)((r + BW - 1) / BW);
+  const int n = nblk + (nblk & 1);
+  const size_t smem = (size_t)(PW * GS + PW * VS + PW * XS + PW * std::max<int64_t>(nrhs, 1)) * sizeof(double);
+  if (smem > 227 * 1024) {
+    az_set_error("az_tsvd_solve: nrhs = %lld too large for the block Jacobi kernel", (long long)nrhs);
+    return AZ_ERR_NOT_SUPPORTED;
+  }
+  AZ_CUDA_CHECK(az_smem_attr(k_bjac_round, smem));
+  BJArgs a;
+  a.B = B;
+  a.r = r;
+  a.C = C;
+  a.nrhs = (int)nrhs;
+  a.nblk = nblk;
+  a.smax2 = smax2;
+  a.theta = theta;
+  a.off = off;
+  a.tol = 4.0 * 1.1102230246251565e-16 * std::sqrt((double)r);
+  a.inner_sweeps = 10;
+  int sw = 0;
+  for (; sw < max_sweeps; ++sw) {
+    {
+      AzTrace tr("bjac_norms", st);
+      k_bjac_colnorms<<<(unsigned)r, 256, 0, st>>>(B, r, nrm2);
+      AZ_LAUNCH_CHECK();
+      k_bjac_max<<<1, 1024, 0, st>>>(nrm2, r, smax2, off);
+      AZ_LAUNCH_CHECK();
+    }
+    for (int rd = 0; rd < n - 1; ++rd) {
+      AzTrace tr("bjac_round", st, 16 * r * BW * BW * (n / 2));
+      k_bjac_round<<<n / 2, 256, smem, st>>>(a, rd);
+      AZ_LAUNCH_CHECK();
+    }
+    unsigned long long h_off = 0;
+    AZ_CUDA_CHECK(cudaMemcpyAsync(&h_off, off, sizeof(h_off), cudaMemcpyDeviceToHost, st));
+    AZ_CUDA_CHECK(cudaStreamSynchronize(st));
+    double offd;
+    memcpy(&offd, &h_off, sizeof(offd));
+    if (offd <= a.tol) {
+      ++sw;
+      break;
+    }
+  }
+  if (sweeps_out) *sweeps_out = sw;
+  {
+    AzTrace tr("bjac_norms", st);
+    k_bjac_colnorms<<<(unsigned)r, 256, 0, st>>>(B, r, nrm2);
+    AZ_LAUNCH_CHECK();
+    k_bjac_max<<<1, 1024, 0, st>>>(nrm2, r, smax2, off);
+    AZ_LAUNCH_CHECK();
+  }
+  {
+    AzTrace tr("bjac_solve", st, 2 * r * r * nrhs);
+    k_bjac_solve<<<dim3(az_div_up(r, 256), az_div_up(nrhs, 32)), 256, 0, st>>>(B, C, nrm2, smax2, r, (int)nrhs,
+                                                                               theta, y, ldy);
+    AZ_LAUNCH_CHECK();
+  }
+  AZ_CUDA_CHECK(cudaMemsetAsync(d_rank, 0, sizeof(int64_t), st));
+  k_bjac_sigma<<<az_div_up(r, 256), 256, 0, st>>>(nrm2, smax2, r, theta, sigma_out, d_rank);
+  AZ_LAUNCH_CHECK();
+  if (rank_out) {
+    AZ_CUDA_CHECK(cudaMemcpyAsync(rank_out, d_rank, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    AZ_CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+  return AZ_OK;
+}

@@ -1,0 +1,118 @@
+"""GPU parity of the wide dense path used by the 2-D configs (SURVEY.md §8(a) a7-a8 with
+k > 128 columns): blocked Householder QR (az_qrw.cu) and block one-sided Jacobi SVD
+(az_svdw.cu), then whole 2-D solves against the oracle (O1 dense TSVD, O2 Alg. 1 step by step)
+on reduced members of the c3/c5 (disk) and c4 (star, Laplacian + Dirichlet rows) families."""
+import numpy as np
+import pytest
+
+from paper_2308_14490_b200 import inputs as I
+from oracle import az as OA
+from oracle import dense as OD
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _dev(a):
+    return torch.from_numpy(np.asfortranarray(a)).cuda()
+
+
+def _host(t):
+    return t.cpu().numpy()
+
+
+def _graded(m, k, seed, lo=-14):
+    rng = np.random.default_rng(seed)
+    U, _ = np.linalg.qr(rng.standard_normal((m, k)))
+    V, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    sig = np.logspace(0, lo, k)
+    return (U * sig) @ V.T, sig
+
+
+@pytest.mark.parametrize("m,k", [(600, 129), (3000, 200), (4099, 517), (20000, 256), (1500, 1500)])
+def test_qr_r_wide(m, k):
+    from paper_2308_14490_b200.api import qr_r
+    A, sig = _graded(m, k, m + k)
+    R = _host(qr_r(_dev(A)))
+    assert np.allclose(np.tril(R, -1), 0)
+    # backward stability: R^T R = A^T A up to O(u ||A||^2)
+    assert np.linalg.norm(R.T @ R - A.T @ A) <= 1e-13 * np.linalg.norm(A) ** 2
+    sR = np.linalg.svd(R, compute_uv=False)
+    assert np.max(np.abs(sR - sig)) <= 1e-13 * sig[0]
+    # R agrees with LAPACK's Householder R up to row signs
+    Rl = np.linalg.qr(A, mode="r")
+    D = np.sign(np.diag(R)) * np.sign(np.diag(Rl))
+    assert np.linalg.norm(D[:, None] * R - Rl) <= 1e-12 * np.linalg.norm(Rl)
+
+
+def test_qr_r_wide_bitwise_reproducible():
+    from paper_2308_14490_b200.api import qr_r
+    A, _ = _graded(5000, 300, 7)
+    R1 = _host(qr_r(_dev(A)))
+    R2 = _host(qr_r(_dev(A)))
+    assert np.array_equal(R1, R2)
+
+
+@pytest.mark.parametrize("r,nrhs", [(129, 1), (200, 8), (517, 3), (1024, 64)])
+def test_tsvd_solve_wide(r, nrhs):
+    from paper_2308_14490_b200.api import tsvd_solve
+    rng = np.random.default_rng(r)
+    U, _ = np.linalg.qr(rng.standard_normal((r, r)))
+    V, _ = np.linalg.qr(rng.standard_normal((r, r)))
+    sig = np.concatenate([np.logspace(0, -9, r // 2), np.logspace(-14, -16, r - r // 2)])   # clear gap
+    RS = np.triu(np.linalg.qr((U * sig) @ V.T, mode="r"))   # upper triangular, same singular values
+    c = rng.standard_normal((r, nrhs))
+    Rf = np.hstack([RS, c])
+    y, s, k = tsvd_solve(_dev(Rf), r, nrhs, 1e-12)
+    y, s = _host(y), _host(s)
+    assert k == r // 2
+    Uf, sf, Vt = np.linalg.svd(RS)
+    assert np.max(np.abs(s - sf)) <= 1e-13 * sf[0]
+    ref = Vt[:k].T @ ((Uf[:, :k].T @ c) / sf[:k, None])
+    assert np.linalg.norm(y - ref) <= 100 * 1.1e-16 * (sf[0] / sf[k - 1]) * np.linalg.norm(ref)
+
+
+def _approx_err(cfg, x, ref_x, grid):
+    f = OA.evaluate(cfg, x, grid)
+    fr = OA.evaluate(cfg, ref_x, grid)
+    return np.max(np.abs(f - fr), axis=0) / np.max(np.abs(fr), axis=0)
+
+
+# reduced members of the 2-D families; R = the family's block rule, adaptive blocks (reading R5)
+WIDE_CASES = [("disk_n32", I.make_config("disk", 32), 8),
+              ("star_n32", I.make_config("star", 32), 8),
+              ("disk_n32_nrhs3", I.make_config("disk", 32, nrhs=3, R=128), 12)]
+
+
+@pytest.mark.parametrize("name,cfg,max_blocks", WIDE_CASES, ids=[c[0] for c in WIDE_CASES])
+def test_solve_2d_matches_oracle(name, cfg, max_blocks):
+    from paper_2308_14490_b200.api import Plan
+    plan = Plan.from_config(cfg)
+    b = I.rhs(cfg)
+    theta = max(cfg.tol * 1e-2, 1e-12)
+    x, rep = plan.solve(_dev(b), theta, cfg.R, max_blocks)
+    x = _host(x)
+    assert not rep["saturated"], rep
+    grid = I.test_grid(cfg)
+    A = OD.assemble_A(cfg)
+    # O1: dense truncated SVD (the plain definition)
+    xo, _, _ = OA.tsvd_lsq(A, b, cfg.tol)
+    res = np.linalg.norm(A @ x - b, axis=0) / np.linalg.norm(b, axis=0)
+    ro = np.linalg.norm(A @ xo - b, axis=0) / np.linalg.norm(b, axis=0)
+    # F3 reading: within 2x of the oracle's; the absolute 1e-8 bar applies where the oracle meets it
+    # (a reduced n = 32 disk is itself only resolved to ~2e-7)
+    assert np.all(res <= np.maximum(2 * ro, 1e-12)), (res, ro)
+    assert np.all((res <= 1e-8) | (ro > 0.5e-8)), (res, ro)
+    # O1 determinacy: the oracle's own spread between tol and tol / 100
+    xo2, _, _ = OA.tsvd_lsq(A, b, cfg.tol / 100)
+    det = _approx_err(cfg, xo2, xo, grid)
+    err = _approx_err(cfg, x, xo, grid)
+    assert np.all(err <= np.maximum(1e-9, 2 * det)), (err, det)
+    # O2: same algorithm step by step (same Philox probes, same block rule).  In 2-D the sketch
+    # singular values below ~1e-10 sigma_1 are rounding noise of K (||Z*|| ~ 5e6),
+    # so the count above theta = 1e-12 (and hence the probe count) is not a determined quantity
+    # (several correct results): only the approximant is compared.
+    prob = OA.make_problem(cfg, "fft")
+    r2 = OA.az_solve(prob, b, theta, cfg.R, cfg.seed, max_blocks=max_blocks)
+    err2 = _approx_err(cfg, x, r2.x.reshape(cfg.N, -1), grid)
+    assert np.all(err2 <= np.maximum(1e-9, 2 * det)), (err2, det)
