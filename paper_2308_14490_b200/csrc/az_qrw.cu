@@ -186,15 +186,18 @@ __global__ void __launch_bounds__(256) k_qr_vtc(UpdArgs a) {
   acc_zero(acc);
   // per-thread load slots: 64 x 32 tile = 2048 elements = 8 per thread; k fastest
   const int lk = tid & 31, li = tid >> 5;   // element (i = li + 8 t, k = lk)
-  for (int64_t rr = r0; rr < r1; rr += VT_BK) {
+  double va[8], vb[8];
+  auto load = [&](int64_t rr) {
     const int64_t r = rr + lk;
-    double va[8], vb[8];
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const int i = li + 8 * t;
       va[t] = r < r1 ? v_elem(a.V, a.ldv, a.j0, a.nb, r, i) : 0.0;
       vb[t] = (r < r1 && n0 + i < a.nt) ? a.C[(n0 + i) * a.ldc + r] : 0.0;
     }
+  };
+  load(r0);
+  for (int64_t rr = r0; rr < r1; rr += VT_BK) {
     __syncthreads();
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
@@ -202,6 +205,7 @@ __global__ void __launch_bounds__(256) k_qr_vtc(UpdArgs a) {
       Bs[(li + 8 * t) * VT_S + lk] = vb[t];
     }
     __syncthreads();
+    if (rr + VT_BK < r1) load(rr + VT_BK);   // next tile in flight during the MMAs
     warp_mma<4, 4, IMAJ, IMAJ>(acc, As, VT_S, Bs, VT_S, wm * 32, wn * 32, wk * 16, 16, lane);
   }
   // reduce the two k halves: warps wk = 1 write, wk = 0 add (scratch reuses the operand tiles)

@@ -15,11 +15,16 @@
 // the kept part of the solution (same skip rule as az_svd.cu).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "az_internal.h"
 #include "az_mma.cuh"
+
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 constexpr int BW = 32;        // columns per block
 constexpr int PW = 2 * BW;    // pair width
@@ -56,7 +61,12 @@ AZ_D void pair_of(int round, int pi, int n, int& p, int& q) {
   }
 }
 
+// One CTA cluster per block pair: the CS CTAs of the cluster split the r rows; their partial
+// Gram matrices are reduced in a fixed order through distributed shared memory into the leader
+// (cluster rank 0), which runs the eigensolver; every CTA then reads V from the leader's shared
+// memory and rotates its own rows.
 __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
+  cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ double sm[];
   double* G = sm;                     // PW x GS
   double* V = G + PW * GS;            // PW x VS  (V[t][p] at t * VS + p)
@@ -66,17 +76,20 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
   __shared__ int rp[PW / 2], rq[PW / 2];
   __shared__ int any_rot;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int CS = (int)cluster.num_blocks(), crank = (int)cluster.block_rank();
   const int n = a.nblk + (a.nblk & 1);
   int bi, bj;
-  pair_of(round, blockIdx.x, n, bi, bj);
-  if (bj >= a.nblk) return;
+  pair_of(round, blockIdx.x / CS, n, bi, bj);
+  if (bj >= a.nblk) return;           // whole cluster returns together (same pair)
   const int64_t r = a.r;
+  const int64_t slice = ((r + CS - 1) / CS + 63) / 64 * 64;
+  const int64_t rb = (int64_t)crank * slice, re = min(r, rb + slice);
   // column of X -> column of B (or -1 past the end)
   auto bcol = [&](int c) -> int64_t {
     const int64_t col = (c < BW) ? (int64_t)bi * BW + c : (int64_t)bj * BW + (c - BW);
     return col < r ? col : -1;
   };
-  // ---------------- Gram G = X^T X ----------------
+  // ---------------- partial Gram G = X^T X over rows [rb, re) ----------------
   {
     const int wm = w & 1, wn = (w >> 1) & 1, wk = w >> 2;
     double acc[4][4][2];
@@ -85,15 +98,19 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
     int64_t colp[8];
 #pragma unroll
     for (int t = 0; t < 8; ++t) colp[t] = bcol(li + 8 * t);
-    for (int64_t k0 = 0; k0 < r; k0 += GK) {
+    double v[8];
+    auto load = [&](int64_t k0) {
       const int64_t k = k0 + lk;
-      double v[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) v[t] = (k < r && colp[t] >= 0) ? a.B[colp[t] * r + k] : 0.0;
+      for (int t = 0; t < 8; ++t) v[t] = (k < re && colp[t] >= 0) ? a.B[colp[t] * r + k] : 0.0;
+    };
+    load(rb);
+    for (int64_t k0 = rb; k0 < re; k0 += GK) {
       __syncthreads();
 #pragma unroll
       for (int t = 0; t < 8; ++t) X[(li + 8 * t) * GKS + lk] = v[t];
       __syncthreads();
+      if (k0 + GK < re) load(k0 + GK);     // next tile in flight during the MMAs
       warp_mma<4, 4, IMAJ, IMAJ>(acc, X, GKS, X, GKS, wm * 32, wn * 32, wk * 16, 16, lane);
     }
     // reduce k halves into G
@@ -114,11 +131,17 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
 #pragma unroll
           for (int e = 0; e < 2; ++e)
             G[acc_row(wm * 32, i, lane) * GS + acc_col(wn * 32, j, e, lane)] += acc[i][j][e];
-    __syncthreads();
   }
-  // ---------------- convergence measure over the pair's cross and intra terms ----------------
+  cluster.sync();                     // partial Grams complete
   const double negl = (1e-3 * a.theta) * (1e-3 * a.theta) * (*a.smax2);
-  {
+  if (crank == 0) {
+    // fixed-order reduction of the partial Grams (leader's own slice first)
+    for (int c = 1; c < CS; ++c) {
+      const double* Gr = cluster.map_shared_rank(G, c);
+      for (int e = tid; e < PW * GS; e += 256) G[e] += Gr[e];
+    }
+    __syncthreads();
+    // ---------------- convergence measure ----------------
     double mx = 0.0;
     for (int e = tid; e < PW * PW; e += 256) {
       const int p = e / PW, q = e % PW;
@@ -134,74 +157,86 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
     __syncthreads();
     if (lane == 0 && mx > a.tol) atomicOr(&any_rot, 1);
     __syncthreads();
-    if (!any_rot) return;     // pair already orthogonal: X and c unchanged
-  }
-  // ---------------- eigen-decomposition of G by cyclic Jacobi ----------------
-  for (int e = tid; e < PW * PW; e += 256) V[(e / PW) * VS + (e % PW)] = (e / PW == e % PW) ? 1.0 : 0.0;
-  __syncthreads();
-  for (int sw = 0; sw < a.inner_sweeps; ++sw) {
-    if (tid == 0) any_rot = 0;
-    __syncthreads();
-    for (int rd = 0; rd < PW - 1; ++rd) {
-      if (tid < PW / 2) {
-        int p, q;
-        pair_of(rd, tid, PW, p, q);
-        const double gp = G[p * GS + p], gq = G[q * GS + q], g = G[p * GS + q];
-        double c = 1.0, s = 0.0;
-        if (g != 0.0 && fabs(g) > a.tol * sqrt(gp * gq) && fmin(gp, gq) >= negl) {
-          const double zeta = (gq - gp) / (2.0 * g);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          c = 1.0 / sqrt(1.0 + t * t);
-          s = c * t;
-          any_rot = 1;
+    if (any_rot) {
+      // ---------------- eigen-decomposition of G by cyclic Jacobi ----------------
+      for (int e = tid; e < PW * PW; e += 256) V[(e / PW) * VS + (e % PW)] = (e / PW == e % PW) ? 1.0 : 0.0;
+      __syncthreads();
+      for (int sw = 0; sw < a.inner_sweeps; ++sw) {
+        for (int rd = 0; rd < PW - 1; ++rd) {
+          if (tid < PW / 2) {
+            int p, q;
+            pair_of(rd, tid, PW, p, q);
+            const double gp = G[p * GS + p], gq = G[q * GS + q], g = G[p * GS + q];
+            double c = 1.0, s = 0.0;
+            if (g != 0.0 && fabs(g) > a.tol * sqrt(gp * gq) && fmin(gp, gq) >= negl) {
+              const double zeta = (gq - gp) / (2.0 * g);
+              const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+              c = 1.0 / sqrt(1.0 + t * t);
+              s = c * t;
+            }
+            rc[tid] = c;
+            rs[tid] = s;
+            rp[tid] = p;
+            rq[tid] = q;
+          }
+          __syncthreads();
+          // rows p, q of G
+          for (int e = tid; e < (PW / 2) * PW; e += 256) {
+            const int k = e / PW, t = e % PW;
+            const double c = rc[k], s = rs[k];
+            if (s == 0.0) continue;
+            const int p = rp[k], q = rq[k];
+            const double xp = G[p * GS + t], xq = G[q * GS + t];
+            G[p * GS + t] = c * xp - s * xq;
+            G[q * GS + t] = s * xp + c * xq;
+          }
+          __syncthreads();
+          // columns p, q of G and of V
+          for (int e = tid; e < (PW / 2) * PW; e += 256) {
+            const int k = e / PW, t = e % PW;
+            const double c = rc[k], s = rs[k];
+            if (s == 0.0) continue;
+            const int p = rp[k], q = rq[k];
+            const double xp = G[t * GS + p], xq = G[t * GS + q];
+            G[t * GS + p] = c * xp - s * xq;
+            G[t * GS + q] = s * xp + c * xq;
+            const double vp = V[t * VS + p], vq = V[t * VS + q];
+            V[t * VS + p] = c * vp - s * vq;
+            V[t * VS + q] = s * vp + c * vq;
+          }
+          __syncthreads();
         }
-        rc[tid] = c;
-        rs[tid] = s;
-        rp[tid] = p;
-        rq[tid] = q;
       }
-      __syncthreads();
-      // rows p, q of G
-      for (int e = tid; e < (PW / 2) * PW; e += 256) {
-        const int k = e / PW, t = e % PW;
-        const double c = rc[k], s = rs[k];
-        if (s == 0.0) continue;
-        const int p = rp[k], q = rq[k];
-        const double xp = G[p * GS + t], xq = G[q * GS + t];
-        G[p * GS + t] = c * xp - s * xq;
-        G[q * GS + t] = s * xp + c * xq;
-      }
-      __syncthreads();
-      // columns p, q of G and of V
-      for (int e = tid; e < (PW / 2) * PW; e += 256) {
-        const int k = e / PW, t = e % PW;
-        const double c = rc[k], s = rs[k];
-        if (s == 0.0) continue;
-        const int p = rp[k], q = rq[k];
-        const double xp = G[t * GS + p], xq = G[t * GS + q];
-        G[t * GS + p] = c * xp - s * xq;
-        G[t * GS + q] = s * xp + c * xq;
-        const double vp = V[t * VS + p], vq = V[t * VS + q];
-        V[t * VS + p] = c * vp - s * vq;
-        V[t * VS + q] = s * vp + c * vq;
-      }
-      __syncthreads();
     }
-    if (!any_rot) break;
   }
-  // ---------------- X <- X V over row tiles of 64 ----------------
+  cluster.sync();                     // leader's V and flag ready
+  const int rot = *cluster.map_shared_rank(&any_rot, 0);
+  if (rot && crank != 0) {
+    const double* Vr = cluster.map_shared_rank(V, 0);
+    for (int e = tid; e < PW * VS; e += 256) V[e] = Vr[e];
+  }
+  cluster.sync();                     // leader's shared memory no longer read remotely
+  if (!rot) return;
+  // ---------------- X <- X V over this CTA's row slice, tiles of 64 rows ----------------
   {
     const int wm = w & 1, wn = w >> 1;       // warp tile 32 rows x 16 cols
     const int lr = tid & 63, lc = tid >> 6;  // load: element (row lr, col lc + 4 t)
-    for (int64_t r0 = 0; r0 < r; r0 += 64) {
+    int64_t colp[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) colp[t] = bcol(lc + 4 * t);
+    double v[16];
+    auto load = [&](int64_t r0) {
+      const int64_t row = r0 + lr;
+#pragma unroll
+      for (int t = 0; t < 16; ++t) v[t] = (colp[t] >= 0 && row < re) ? a.B[colp[t] * r + row] : 0.0;
+    };
+    load(rb);
+    for (int64_t r0 = rb; r0 < re; r0 += 64) {
       __syncthreads();
-      for (int t = 0; t < 16; ++t) {
-        const int c = lc + 4 * t;
-        const int64_t col = bcol(c);
-        const int64_t row = r0 + lr;
-        X[c * XS + lr] = (col >= 0 && row < r) ? a.B[col * r + row] : 0.0;
-      }
+#pragma unroll
+      for (int t = 0; t < 16; ++t) X[(lc + 4 * t) * XS + lr] = v[t];
       __syncthreads();
+      if (r0 + 64 < re) load(r0 + 64);
       double acc[4][2][2];
       acc_zero(acc);
       warp_mma<4, 2, KMAJ, KMAJ>(acc, X, XS, V, VS, wm * 32, wn * 16, 0, PW, lane);
@@ -213,12 +248,12 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
           for (int e = 0; e < 2; ++e) {
             const int64_t row = r0 + acc_row(wm * 32, i, lane);
             const int64_t col = bcol(acc_col(wn * 16, j, e, lane));
-            if (col >= 0 && row < r) a.B[col * r + row] = acc[i][j][e];
+            if (col >= 0 && row < re) a.B[col * r + row] = acc[i][j][e];
           }
     }
   }
-  // ---------------- c rows of the pair <- V^T c ----------------
-  if (a.nrhs > 0) {
+  // ---------------- c rows of the pair <- V^T c (leader) ----------------
+  if (crank == 0 && a.nrhs > 0) {
     __syncthreads();
     for (int e = tid; e < PW * a.nrhs; e += 256) {
       const int k = e % PW, c = e / PW;
@@ -340,6 +375,13 @@ __global__ void k_bjac_load(const double* Rf, int64_t ldr, int64_t r, int nrhs, 
 
 static size_t a256(size_t v) { return (v + 255) & ~(size_t)255; }
 
+static int g_last_sweeps = 0;
+static int g_inner_sweeps = 2;
+extern "C" int az_debug_jacobi(int inner_sweeps) {   // returns the outer sweeps of the last block-Jacobi SVD
+  if (inner_sweeps > 0) g_inner_sweeps = inner_sweeps;
+  return g_last_sweeps;
+}
+
 size_t az_tsvdw_ws_bytes(int64_t r, int64_t nrhs) {
   return a256(sizeof(double) * r * r) + a256(sizeof(double) * r * nrhs) + a256(sizeof(double) * r) + 1024;
 }
@@ -374,6 +416,14 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
     return AZ_ERR_NOT_SUPPORTED;
   }
   AZ_CUDA_CHECK(az_smem_attr(k_bjac_round, smem));
+  // cluster size: enough CTAs per round to cover the SMs twice, each slice >= 256 rows
+  int CS = 1;
+  {
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    while (CS < 8 && (int64_t)(n / 2) * CS < 2 * sms && r / (2 * CS) >= 256) CS *= 2;
+  }
   BJArgs a;
   a.B = B;
   a.r = r;
@@ -384,7 +434,7 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
   a.theta = theta;
   a.off = off;
   a.tol = 4.0 * 1.1102230246251565e-16 * std::sqrt((double)r);
-  a.inner_sweeps = 10;
+  a.inner_sweeps = g_inner_sweeps;
   int sw = 0;
   for (; sw < max_sweeps; ++sw) {
     {
@@ -396,7 +446,19 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
     }
     for (int rd = 0; rd < n - 1; ++rd) {
       AzTrace tr("bjac_round", st, 16 * r * BW * BW * (n / 2));
-      k_bjac_round<<<n / 2, 256, smem, st>>>(a, rd);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(n / 2 * CS));
+      cfg.blockDim = dim3(256);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = CS;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      AZ_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_bjac_round, a, rd));
       AZ_LAUNCH_CHECK();
     }
     unsigned long long h_off = 0;
@@ -404,12 +466,14 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
     AZ_CUDA_CHECK(cudaStreamSynchronize(st));
     double offd;
     memcpy(&offd, &h_off, sizeof(offd));
-    if (offd <= a.tol) {
+    if (getenv("AZ_DEBUG_JACOBI")) fprintf(stderr, "bjac r=%lld sweep %d off %.3e tol %.3e\n", (long long)r, sw, offd, a.tol);
+    if (offd <= 4.0 * a.tol) {   // rounding level of the measured off-diagonals
       ++sw;
       break;
     }
   }
   if (sweeps_out) *sweeps_out = sw;
+  g_last_sweeps = sw;
   {
     AzTrace tr("bjac_norms", st);
     k_bjac_colnorms<<<(unsigned)r, 256, 0, st>>>(B, r, nrm2);

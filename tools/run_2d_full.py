@@ -1,0 +1,46 @@
+"""Full-size 2-D solves (BASELINE configs c3, c4, c5): time, probes, rank, residual (oracle FFT
+operator), manufactured-solution error on the test grid.
+
+    python tools/run_2d_full.py c4 [max_blocks]
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2308_14490_b200 import api  # noqa: E402
+from paper_2308_14490_b200 import inputs as I  # noqa: E402
+
+name = sys.argv[1]
+mb = int(sys.argv[2]) if len(sys.argv) > 2 else 16
+cfg = I.get_config(name)
+t0 = time.time()
+plan = api.Plan.from_config(cfg)
+b = I.rhs(cfg)
+bd = api.colmajor(torch.from_numpy(b).cuda())
+theta = max(cfg.tol * 1e-2, 1e-12)
+torch.cuda.synchronize()
+t1 = time.time()
+api.trace_enable(True)
+x, rep = plan.solve(bd, theta, cfg.R, mb)
+torch.cuda.synchronize()
+t2 = time.time()
+tr = api.trace_report()
+api.trace_enable(False)
+x = x.cpu().numpy()
+out = {"config": name, "plan_s": t1 - t0, "solve_s": t2 - t1, "report": rep,
+       "kernels_ms": {k: round(v[1], 3) for k, v in sorted(tr.items(), key=lambda kv: -kv[1][1])[:14]}}
+if "--check" in sys.argv:
+    from oracle import az as OA
+    grid = I.test_grid(cfg, 201)
+    f = OA.evaluate(cfg, x, grid)
+    out["max_err_vs_exact"] = float(np.max(np.abs(f - grid.exact)) / np.max(np.abs(grid.exact)))
+    prob = OA.make_problem(cfg, "fft")
+    out["rel_residual"] = OA.relative_residual(prob, x, b).tolist()
+print(json.dumps(out))
