@@ -18,7 +18,7 @@
 //   Z3  cols (N1):  IFFT_N1 -> coefficient output
 #include <algorithm>
 
-#include "az_fft.cuh"
+#include "az_fftr.cuh"
 #include "az_internal.h"
 
 struct P1f {
@@ -68,176 +68,181 @@ AZ_D Cols1 pcols(const P1f& a, int b) {
 }
 
 // ------------------------------------------------------------------------------------------
-// column passes: a CTA owns TC adjacent columns of an N1-row matrix
+// column passes: a CTA owns TC adjacent columns of an N1-row matrix; each column FFT is computed
+// by T = NC / 16 threads holding 16 values each (az_fftr.cuh), element e of thread j = row j + e T.
+// Thread t -> (column c = t mod TC, j = t / TC): a warp reads TC consecutive complex values of
+// 32 / TC rows per access.
 // ------------------------------------------------------------------------------------------
 enum { FC_IN_COEF = 0, FC_FINE_MASK = 1, FC_OUT_GATHER = 2, FC_OUT_RESID = 3, FC_IN_ROWS = 4, FC_OUT_COEF = 5,
        FC_FWD_G = 6 };
 
+constexpr int EC = 16;    // values per thread in the column FFTs
+
 template <int NC, int TC, int KIND, int SRC>
-__global__ void __launch_bounds__(TC * NC / 8, (TC * NC / 8) <= 256 ? 2 : 1) k1f_cols(P1f a, double cout) {
+__global__ void __launch_bounds__(TC * (NC / EC), 2) k1f_cols(P1f a, double cout) {
   extern __shared__ cplx sm[];
-  constexpr int TPF = NC / 8;
-  constexpr int PL = spad_len(NC);
-  constexpr int NT = TC * TPF;
-  const int tid = threadIdx.x, f = tid / TPF, j = tid % TPF;
+  constexpr int T = NC / EC;
+  const int tid = threadIdx.x, c = tid % TC, j = tid / TC;
   const int b = blockIdx.y;
   const int c0 = blockIdx.x * TC;
+  const int col = c0 + c;
   const Cols1 cc = pcols(a, b);
   const bool coef = (KIND == FC_IN_COEF || KIND == FC_OUT_COEF);
   const int W = coef ? a.N2 : a.L2;                    // row length of the matrix
   cplx* C1b = a.C1 + (int64_t)b * a.n;
   cplx* Gb = a.G + (int64_t)b * a.L;
-  // twiddle period and the scale of the column index in it
   const int64_t tmul = coef ? a.s : 1;                 // e^{-2 pi i n2 k1 / n} = e^{-2 pi i (s n2 k1) / L}
+  cplx* buf = sm + c * fftr::padded_len(NC);
+  cplx v[EC];
 
-  // ---- load ----
-  if constexpr (KIND == FC_IN_COEF) {
-    if constexpr (SRC == SRC_PROBE) {
-      for (int e = tid; e < NC * TC / 2; e += NT) {
-        const int row = e / (TC / 2), c = 2 * (e % (TC / 2));
-        const int64_t i = (int64_t)row * W + c0 + c;       // even natural index
-        const cpair pr = probe_cplx_pair((uint64_t)(i >> 1), (uint64_t)(a.col0 + cc.cre), (uint64_t)(a.col0 + cc.cim),
-                                         cc.has_im, a.seed);
-        sm[c * PL + spad(row)] = pr.a;
-        sm[(c + 1) * PL + spad(row)] = pr.b;
-      }
-    } else {
-      for (int e = tid; e < NC * TC; e += NT) {
-        const int row = e / TC, c = e % TC;
-        const int64_t i = (int64_t)row * W + c0 + c;
-        sm[c * PL + spad(row)] = make_double2(a.in[i + cc.cre * a.ldin], cc.has_im ? a.in[i + cc.cim * a.ldin] : 0.0);
-      }
+  // ---- load (element e: row j + e T) ----
+  if constexpr (KIND == FC_IN_COEF && SRC == SRC_PROBE) {
+    // lanes (2m, 2m+1) hold columns (col, col + 1), col even: the even lane draws the real-part
+    // probe pair of the two columns, the odd lane the imaginary-part pair, and they swap halves.
+    const bool odd = c & 1;
+#pragma unroll
+    for (int e = 0; e < EC; ++e) {
+      const int64_t i = (int64_t)(j + e * T) * W + (col & ~1);
+      double2 z = make_double2(0.0, 0.0);
+      if (!odd || cc.has_im) z = probe_pair((uint64_t)(i >> 1), (uint64_t)(a.col0 + (odd ? cc.cim : cc.cre)), a.seed);
+      const double send = odd ? z.x : z.y;
+      const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
+      v[e] = odd ? make_double2(recv, z.y) : make_double2(z.x, recv);
+    }
+  } else if constexpr (KIND == FC_IN_COEF) {
+#pragma unroll
+    for (int e = 0; e < EC; ++e) {
+      const int64_t i = (int64_t)(j + e * T) * W + col;
+      v[e] = make_double2(a.in[i + cc.cre * a.ldin], cc.has_im ? a.in[i + cc.cim * a.ldin] : 0.0);
     }
   } else if constexpr (KIND == FC_IN_ROWS) {
-    for (int e = tid; e < NC * TC; e += NT) {
-      const int row = e / TC, c = e % TC;
-      const int r = a.pos[(int64_t)row * W + c0 + c];
-      cplx v = czero();
-      if (r >= 0) v = make_double2(a.in[r + cc.cre * a.ldin], cc.has_im ? a.in[r + cc.cim * a.ldin] : 0.0);
-      sm[c * PL + spad(row)] = v;
+#pragma unroll
+    for (int e = 0; e < EC; ++e) {
+      const int r = a.pos[(int64_t)(j + e * T) * W + col];
+      v[e] = r >= 0 ? make_double2(a.in[r + cc.cre * a.ldin], cc.has_im ? a.in[r + cc.cim * a.ldin] : 0.0) : czero();
     }
   } else {
     const cplx* src = coef ? C1b : Gb;
-    for (int e = tid; e < NC * TC; e += NT) {
-      const int row = e / TC, c = e % TC;
-      sm[c * PL + spad(row)] = src[(int64_t)row * W + c0 + c];
-    }
+#pragma unroll
+    for (int e = 0; e < EC; ++e) v[e] = src[(int64_t)(j + e * T) * W + col];
   }
-  __syncthreads();
-  cplx* buf = sm + f * PL;
+  uint32_t mbits = 0;   // FC_FINE_MASK: the 16 mask bytes of this thread, packed
+  if constexpr (KIND == FC_FINE_MASK) {
+#pragma unroll
+    for (int e = 0; e < EC; ++e) mbits |= (a.mask[(int64_t)(j + e * T) * W + col] ? 1u : 0u) << e;
+  }
 
   // ---- transforms ----
   if constexpr (KIND == FC_IN_COEF || KIND == FC_IN_ROWS || KIND == FC_FWD_G) {
-    fft_smem<NC, -1>(buf, j, a.tw, TWN);
+    fftr::fft<NC, EC, -1>(v, j, buf, a.tw, TWN);
   } else if constexpr (KIND == FC_FINE_MASK) {
-    fft_smem<NC, 1>(buf, j, a.tw, TWN);
-    for (int e = tid; e < NC * TC; e += NT) {
-      const int row = e / TC, c = e % TC;
-      if (!a.mask[(int64_t)row * W + c0 + c]) sm[c * PL + spad(row)] = czero();
-    }
-    __syncthreads();
-    fft_smem<NC, -1>(buf, j, a.tw, TWN);
+    fftr::fft<NC, EC, 1>(v, j, buf, a.tw, TWN);
+#pragma unroll
+    for (int e = 0; e < EC; ++e)
+      if (!((mbits >> e) & 1u)) v[e] = czero();
+    fftr::fft<NC, EC, -1>(v, j, buf, a.tw, TWN);
   } else {
-    fft_smem<NC, 1>(buf, j, a.tw, TWN);
+    fftr::fft<NC, EC, 1>(v, j, buf, a.tw, TWN);
   }
 
   // ---- store ----
   if constexpr (KIND == FC_IN_COEF || KIND == FC_IN_ROWS || KIND == FC_FINE_MASK || KIND == FC_FWD_G) {
     cplx* dst = (KIND == FC_IN_COEF) ? C1b : Gb;
-    for (int e = tid; e < NC * TC; e += NT) {
-      const int k1 = e / TC, c = e % TC;
-      const int64_t t = ((int64_t)k1 * (c0 + c) * tmul) & (a.L - 1);
-      dst[(int64_t)k1 * W + c0 + c] = cmul(sm[c * PL + spad(k1)], tw4<-1>(a, t));
+#pragma unroll
+    for (int e = 0; e < EC; ++e) {
+      const int k1 = j + e * T;
+      const int64_t t = ((int64_t)k1 * col * tmul) & (a.L - 1);
+      dst[(int64_t)k1 * W + col] = cmul(v[e], tw4<-1>(a, t));
     }
   } else if constexpr (KIND == FC_OUT_GATHER || KIND == FC_OUT_RESID) {
-    for (int e = tid; e < NC * TC; e += NT) {
-      const int row = e / TC, c = e % TC;
-      const int r = a.pos[(int64_t)row * W + c0 + c];
+#pragma unroll
+    for (int e = 0; e < EC; ++e) {
+      const int r = a.pos[(int64_t)(j + e * T) * W + col];
       if (r >= 0) {
-        const cplx v = sm[c * PL + spad(row)];
         if constexpr (KIND == FC_OUT_RESID) {
-          a.out[r + cc.cre * a.ldout] = a.in[r + cc.cre * a.ldin] - v.x;
-          if (cc.has_im) a.out[r + cc.cim * a.ldout] = a.in[r + cc.cim * a.ldin] - v.y;
+          a.out[r + cc.cre * a.ldout] = a.in[r + cc.cre * a.ldin] - v[e].x;
+          if (cc.has_im) a.out[r + cc.cim * a.ldout] = a.in[r + cc.cim * a.ldin] - v[e].y;
         } else {
-          a.out[r + cc.cre * a.ldout] = v.x;
-          if (cc.has_im) a.out[r + cc.cim * a.ldout] = v.y;
+          a.out[r + cc.cre * a.ldout] = v[e].x;
+          if (cc.has_im) a.out[r + cc.cim * a.ldout] = v[e].y;
         }
       }
     }
   } else {   // FC_OUT_COEF
-    for (int e = tid; e < NC * TC; e += NT) {
-      const int row = e / TC, c = e % TC;
-      const int64_t i = (int64_t)row * W + c0 + c;
-      const cplx v = sm[c * PL + spad(row)];
-      a.out[i + cc.cre * a.ldout] = v.x * cout;
-      if (cc.has_im) a.out[i + cc.cim * a.ldout] = v.y * cout;
+#pragma unroll
+    for (int e = 0; e < EC; ++e) {
+      const int64_t i = (int64_t)(j + e * T) * W + col;
+      a.out[i + cc.cre * a.ldout] = v[e].x * cout;
+      if (cc.has_im) a.out[i + cc.cim * a.ldout] = v[e].y * cout;
     }
   }
 }
 
 // ------------------------------------------------------------------------------------------
-// row passes: a CTA owns RPC rows k1; threads per row = NR2/8 (NR2 = N2), L2-FFTs use V = s.
+// row passes: a CTA owns RPC rows k1; T = LR2 / 16 = NR2 / 8 threads per row.  Length-LR2
+// transforms hold 16 values per thread, length-NR2 ones 8, so element e of the coefficient
+// spectrum (k2 = j + e T) and its alias k2 + NR2 (element e + 8 of the fine spectrum) are in the
+// same thread: fold, expand, the symbol multiply and the v^ - w^ update are all thread-local.
 // ------------------------------------------------------------------------------------------
 enum { FR_EXPAND = 0, FR_EXPAND_KEEP = 1, FR_STEP1 = 2, FR_RESID = 3, FR_ZSTAR = 4, FR_AT = 5 };
 
 template <int NR2, int LR2, int RPC, int KIND>
-__global__ void __launch_bounds__(RPC * LR2 / 8, (RPC * LR2 / 8) <= 256 ? 2 : 1) k1f_rows(P1f a, int nrows) {
+__global__ void __launch_bounds__(RPC * (LR2 / 16), 2) k1f_rows(P1f a, int nrows) {
   extern __shared__ cplx sm[];
-  constexpr int TPF = LR2 / 8;           // threads per row (length-L2 FFTs, 8 values per thread)
-  constexpr int TPN = NR2 / 8;           // threads per length-N2 FFT; the other half runs a scratch slot
-  constexpr int PLN = spad_len(NR2), PLL = spad_len(LR2);
-  constexpr int S = LR2 / NR2;
-  const int f = threadIdx.x / TPF, j = threadIdx.x % TPF;
+  static_assert(LR2 == 2 * NR2, "four-step rows: L = 2 only");
+  constexpr int T = LR2 / 16;
+  const int f = threadIdx.x / T, j = threadIdx.x % T;
   const int k1 = blockIdx.x * RPC + f;
   const bool live = k1 < nrows;
   const int b = blockIdx.y;
-  cplx* bL = sm + f * (PLL + S * PLN);
-  cplx* bN = bL + PLL;                               // real slot; scratch slots follow
-  cplx* bNj = bN + (j / TPN) * PLN;                  // this thread's N2-FFT slot
-  const int jn = j % TPN;
+  cplx* buf = sm + f * fftr::padded_len(LR2);
   cplx* C1b = a.C1 + (int64_t)b * a.n;
   cplx* Gb = a.G + (int64_t)b * a.L;
   const double invL = 1.0 / (double)a.L;
-  const int64_t rowW = (int64_t)k1 * LR2;             // row offset in W / G
-  const int64_t rowC = (int64_t)k1 * NR2;             // row offset in C1 / zinv
+  const int64_t rowW = (int64_t)(live ? k1 : 0) * LR2;     // row offset in W / G
+  const int64_t rowC = (int64_t)(live ? k1 : 0) * NR2;     // row offset in C1 / zinv
+  cplx vn[8];
+  cplx vl[16];
 
   if constexpr (KIND == FR_EXPAND || KIND == FR_EXPAND_KEEP) {
-    for (int e = j; e < NR2; e += TPF) bN[spad(e)] = live ? C1b[rowC + e] : czero();
-    __syncthreads();
-    fft_smem<NR2, -1>(bNj, jn, a.tw, TWN);
-    if (KIND == FR_EXPAND_KEEP && live)
-      for (int e = j; e < NR2; e += TPF) C1b[rowC + e] = bN[spad(e)];
-  } else {
-    for (int e = j; e < LR2; e += TPF) bL[spad(e)] = live ? Gb[rowW + e] : czero();
-    __syncthreads();
-    fft_smem<LR2, -1>(bL, j, a.tw, TWN);
-    for (int k2 = j; k2 < NR2; k2 += TPF) {
-      cplx acc = czero();
-      if (live) {
 #pragma unroll
-        for (int m = 0; m < S; ++m) acc = cadd(acc, cmulc(bL[spad(k2 + m * NR2)], sym1f(a, rowW + k2 + m * NR2)));
-        if (KIND != FR_AT) acc = cscale(acc, a.zinv[rowC + k2]);
-        if (KIND == FR_STEP1) acc = csub(C1b[rowC + k2], acc);
-      }
-      bN[spad(k2)] = acc;
+    for (int e = 0; e < 8; ++e) vn[e] = live ? C1b[rowC + j + e * T] : czero();
+    fftr::fft<NR2, 8, -1>(vn, j, buf, a.tw, TWN);
+    if (KIND == FR_EXPAND_KEEP && live)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) C1b[rowC + j + e * T] = vn[e];
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) vl[e] = live ? Gb[rowW + j + e * T] : czero();
+    fftr::fft<LR2, 16, -1>(vl, j, buf, a.tw, TWN);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int k2 = j + e * T;
+      cplx acc = cadd(cmulc(vl[e], sym1f(a, rowW + k2)), cmulc(vl[e + 8], sym1f(a, rowW + k2 + NR2)));
+      if (KIND != FR_AT) acc = cscale(acc, a.zinv[rowC + k2]);
+      if (KIND == FR_STEP1) acc = csub(C1b[rowC + k2], acc);
+      vn[e] = acc;
     }
-    __syncthreads();
   }
   if constexpr (KIND == FR_ZSTAR || KIND == FR_AT) {
-    fft_smem<NR2, 1>(bNj, jn, a.tw, TWN);
+    fftr::fft<NR2, 8, 1>(vn, j, buf, a.tw, TWN);
     if (live)
-      for (int n2 = j; n2 < NR2; n2 += TPF) {
-        const int64_t t = ((int64_t)n2 * k1 * S) & (a.L - 1);     // e^{+2 pi i n2 k1 / n}
-        C1b[rowC + n2] = cmul(bN[spad(n2)], tw4<1>(a, t));
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int n2 = j + e * T;
+        const int64_t t = ((int64_t)n2 * k1 * 2) & (a.L - 1);     // e^{+2 pi i n2 k1 / n}
+        C1b[rowC + n2] = cmul(vn[e], tw4<1>(a, t));
       }
   } else {
-    for (int e = j; e < LR2; e += TPF) bL[spad(e)] = cscale(cmul(bN[spad(e & (NR2 - 1))], sym1f(a, rowW + e)), invL);
-    __syncthreads();
-    fft_smem<LR2, 1>(bL, j, a.tw, TWN);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) vl[e] = cscale(cmul(vn[e & 7], sym1f(a, rowW + j + e * T)), invL);
+    fftr::fft<LR2, 16, 1>(vl, j, buf, a.tw, TWN);
     if (live)
-      for (int n2 = j; n2 < LR2; n2 += TPF) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int n2 = j + e * T;
         const int64_t t = ((int64_t)n2 * k1) & (a.L - 1);          // e^{+2 pi i n2' k1 / L}
-        Gb[rowW + n2] = cmul(bL[spad(n2)], tw4<1>(a, t));
+        Gb[rowW + n2] = cmul(vl[e], tw4<1>(a, t));
       }
   }
 }
@@ -247,15 +252,16 @@ __global__ void __launch_bounds__(RPC * LR2 / 8, (RPC * LR2 / 8) <= 256 ? 2 : 1)
 // ------------------------------------------------------------------------------------------
 template <int NC, int KIND, int SRC>
 static az_status_t fcols(const P1f& a, int ncols, int nb, double cout, cudaStream_t st) {
-  constexpr int TC0 = 4096 / NC;
+  constexpr int T = NC / EC;
+  constexpr int TC0 = 256 / T;
   constexpr int TC = TC0 < 2 ? 2 : (TC0 > 16 ? 16 : TC0);
-  const size_t sm = (size_t)TC * spad_len(NC) * sizeof(cplx);
+  const size_t sm = (size_t)TC * fftr::padded_len(NC) * sizeof(cplx);
   auto kern = k1f_cols<NC, TC, KIND, SRC>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   static const char* names[] = {"1f_cols_in_coef", "1f_cols_fine_mask", "1f_cols_out_gather", "1f_cols_out_resid",
                                 "1f_cols_in_rows", "1f_cols_out_coef", "1f_cols_fwd"};
   AzTrace tr(names[KIND], st, nb);
-  kern<<<dim3(az_div_up(ncols, TC), nb), TC * NC / 8, sm, st>>>(a, cout);
+  kern<<<dim3(az_div_up(ncols, TC), nb), TC * T, sm, st>>>(a, cout);
   AZ_LAUNCH_CHECK();
   return AZ_OK;
 }
@@ -263,15 +269,16 @@ static az_status_t fcols(const P1f& a, int ncols, int nb, double cout, cudaStrea
 template <int NR2, int KIND>
 static az_status_t frows(const P1f& a, int nb, cudaStream_t st) {
   constexpr int LR2 = 2 * NR2;
-  constexpr int RPC0 = 2048 / LR2;
-  constexpr int RPC = RPC0 < 1 ? 1 : (RPC0 > 32 ? 32 : RPC0);
-  const size_t sm = (size_t)RPC * (spad_len(LR2) + 2 * spad_len(NR2)) * sizeof(cplx);
+  constexpr int T = LR2 / 16;
+  constexpr int RPC0 = 256 / T;
+  constexpr int RPC = RPC0 < 1 ? 1 : (RPC0 > 64 ? 64 : RPC0);
+  const size_t sm = (size_t)RPC * fftr::padded_len(LR2) * sizeof(cplx);
   auto kern = k1f_rows<NR2, LR2, RPC, KIND>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   static const char* names[] = {"1f_rows_expand", "1f_rows_expand_keep", "1f_rows_step1", "1f_rows_resid",
                                 "1f_rows_zstar", "1f_rows_at"};
   AzTrace tr(names[KIND], st, nb);
-  kern<<<dim3(az_div_up(a.N1, RPC), nb), RPC * LR2 / 8, sm, st>>>(a, a.N1);
+  kern<<<dim3(az_div_up(a.N1, RPC), nb), RPC * T, sm, st>>>(a, a.N1);
   AZ_LAUNCH_CHECK();
   return AZ_OK;
 }

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -383,7 +384,9 @@ static az_status_t plan_build(az_plan_s* p, const az_plan_desc_t* d, cudaStream_
   // ---- scratch for the multi-pass layouts ----
   if (p->layout != AZ_LAYOUT_1D_SMALL) {
     const int64_t per_pair = (p->G + p->N) * (int64_t)sizeof(cplx);
-    int64_t B = (int64_t)(256ll << 20) / per_pair;
+    int64_t scratch_mb = 256;
+    if (const char* e = getenv("AZ_SCRATCH_MB")) scratch_mb = std::max<int64_t>(1, atoll(e));
+    int64_t B = (scratch_mb << 20) / per_pair;
     B = std::max<int64_t>(1, std::min<int64_t>(B, 32));
     p->Bmax = B;
     AZ_TRY(dalloc(&p->d_C1, B * p->N));
