@@ -80,7 +80,7 @@ az_status_t az_fft_batch(const cplx* tw, cplx* data, int64_t len, int64_t count,
 
 // --- QR / SVD / solve
 az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R, int64_t ldr,
-                         void* ws, size_t ws_bytes, cudaStream_t st);
+                         void* ws, size_t ws_bytes, cudaStream_t st, int64_t k1 = 0);
 size_t az_qr_ws_bytes(int64_t m, int64_t k);
 az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta,
                          double* y, int64_t ldy, double* sigma_out, int64_t* rank_out,

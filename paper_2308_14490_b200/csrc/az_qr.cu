@@ -30,6 +30,7 @@ struct QRIn {
   const double* A;
   int64_t m;        // rows
   int k;            // columns
+  int k1;           // leading columns to triangularise (the rest are only transformed: Q^T b')
   int64_t ld;       // column stride
   int64_t rb;       // rows per block of the stacked input (row r at (r / rb) * bstride + (r % rb))
   int64_t bstride;
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(512, 1) k_tsqr(QRIn q) {
         x[c][r] = v;
       }
     }
-    for (int j = 0; j < k; ++j) {
+    for (int j = 0; j < q.k1; ++j) {
       const int o = j & 15, cj = j >> 4;
       double* vj = vb + (j & 1) * MC;
       if (w == o) {
@@ -114,34 +115,47 @@ __global__ void __launch_bounds__(512, 1) k_tsqr(QRIn q) {
 #pragma unroll
           for (int r = 0; r < RPL; ++r) p[c] = fma(v[r], x[c][r], p[c]);
         }
+        // transpose-reduce: KC - 1 + (5 - log2 KC) shuffles instead of 5 KC; afterwards lane L holds
+        // the full dot of column slot L / (32 / KC)
+        constexpr int LPC = 32 / KC;   // lanes per column slot after the halving levels
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
+        for (int o = 16, n = KC; n > 1; o >>= 1, n >>= 1) {
+          const bool hi = lane & o;
 #pragma unroll
-          for (int c = 0; c < KC; ++c) p[c] += __shfl_xor_sync(0xffffffffu, p[c], o);
-        double rj[KC];
-#pragma unroll
-        for (int c = 0; c < KC; ++c) {
-          const int l = w + 16 * c;
-          rj[c] = (l > j && l < k) ? R[pk(j, l)] : 0.0;
+          for (int i = 0; i < n / 2; ++i) {
+            const double send = hi ? p[i] : p[i + n / 2];
+            const double keep = hi ? p[i + n / 2] : p[i];
+            p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
         }
+        double dsum = p[0];
+#pragma unroll
+        for (int o = LPC / 2; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+        const int cs = lane / LPC;
+        const int ls = w + 16 * cs;
+        const bool live = ls > j && ls < k;
+        const double rjs = live ? R[pk(j, ls)] : 0.0;
+        const double tws = live ? tau * (rjs + dsum) : 0.0;
         __syncwarp();
+        if (live && (lane & (LPC - 1)) == 0) R[pk(j, ls)] = rjs - tws;
 #pragma unroll
         for (int c = 0; c < KC; ++c) {
           const int l = w + 16 * c;
+          const double tw = __shfl_sync(0xffffffffu, tws, c * LPC);
           if (l > j && l < k) {
-            const double tw = tau * (rj[c] + p[c]);
 #pragma unroll
             for (int r = 0; r < RPL; ++r) x[c][r] = fma(-tw, v[r], x[c][r]);
-            if (lane == 0) R[pk(j, l)] = rj[c] - tw;
           }
         }
       }
     }
   }
   __syncthreads();
-  double* Ro = q.Rout + (int64_t)blockIdx.x * k * k;
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-    const int i = e % k, l = e / k;
+  // top k1 rows of R (k1 x k, ld k1)
+  const int k1 = q.k1;
+  double* Ro = q.Rout + (int64_t)blockIdx.x * k1 * k;
+  for (int e = threadIdx.x; e < k1 * k; e += blockDim.x) {
+    const int i = e % k1, l = e / k1;
     Ro[e] = i <= l ? R[pk(i, l)] : 0.0;
   }
 }
@@ -201,13 +215,16 @@ static az_status_t qr_r_wide(double* A, int64_t m, int64_t k, int64_t lda, doubl
   return az_qrw_extract_R(A, lda, k, R, ldr, st);
 }
 
-__global__ void k_copy_R(const double* Rin, int k, double* R, int64_t ldr) {
+__global__ void k_copy_R(const double* Rin, int k1, int k, double* R, int64_t ldr) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < k * k) R[(e / k) * ldr + (e % k)] = Rin[e];
+  if (e < k1 * k) R[(e / k1) * ldr + (e % k1)] = Rin[e];
 }
 
+// k1 < k: only the leading k1 columns are triangularised and only the top k1 rows of R are
+// returned (R[:k1, k1:] = (Q^T A[:, k1:])[:k1], e.g. Q^T b' for the right-hand sides riding along).
 az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R, int64_t ldr,
-                         void* ws, size_t ws_bytes, cudaStream_t st) {
+                         void* ws, size_t ws_bytes, cudaStream_t st, int64_t k1) {
+  if (k1 <= 0 || k1 > k) k1 = k;
   if (ws_bytes < az_qr_ws_bytes(m, k)) {
     az_set_error("az_qr_r: workspace too small");
     return AZ_ERR_WORKSPACE;
@@ -225,6 +242,7 @@ az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R
   q.A = A;
   q.m = m;
   q.k = (int)k;
+  q.k1 = (int)k1;
   q.ld = lda;
   q.rb = m;
   q.bstride = 0;
@@ -239,18 +257,19 @@ az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R
     const int64_t next = (cur + G - 1) / G;
     QRIn t;
     t.A = buf[which];
-    t.m = cur * k;
+    t.m = cur * k1;
     t.k = (int)k;
-    t.ld = k;
-    t.rb = k;
-    t.bstride = k * k;
-    t.rows_per_cta = G * k;
+    t.k1 = (int)k1;
+    t.ld = k1;
+    t.rb = k1;
+    t.bstride = k1 * k;
+    t.rows_per_cta = G * k1;
     t.Rout = buf[which ^ 1];
     AZ_TRY(tsqr_pass(t, (int)next, st));
     which ^= 1;
     cur = next;
   }
-  k_copy_R<<<az_div_up(k * k, 256), 256, 0, st>>>(buf[which], (int)k, R, ldr);
+  k_copy_R<<<az_div_up(k1 * k, 256), 256, 0, st>>>(buf[which], (int)k1, (int)k, R, ldr);
   AZ_LAUNCH_CHECK();
   return AZ_OK;
 }
@@ -270,5 +289,5 @@ extern "C" az_status_t az_qr_r(az_plan_t, double* A, int64_t m, int64_t k, int64
     az_set_error("az_qr_r: bad arguments");
     return AZ_ERR_INVALID_ARGUMENT;
   }
-  return az_qr_r_impl(A, m, k, lda, R, ldr, ws, ws_bytes, (cudaStream_t)stream);
+  return az_qr_r_impl(A, m, k, lda, R, ldr, ws, ws_bytes, (cudaStream_t)stream, k);
 }

@@ -251,7 +251,7 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
     }
     cudaEventRecord(e1, st);
     if (!w.wide) {
-      AZ_TRY(az_qr_r_impl(w.S, rows, kt, rows, w.Rf, kt, w.qrws, w.qrbytes, st));
+      AZ_TRY(az_qr_r_impl(w.S, rows, kt, rows, w.Rf, kt, w.qrws, w.qrbytes, st, kp));
     } else {
       if (kp > rows) {
         az_set_error("az_solve: %lld probe columns exceed the %lld rows", (long long)kp, (long long)rows);

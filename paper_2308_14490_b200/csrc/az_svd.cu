@@ -20,6 +20,8 @@ AZ_D double wsum(double v) {
   return v;
 }
 
+__device__ int g_small_sweeps;
+
 __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int64_t ldr, int r, int nrhs,
                                                           double theta, double* y, int64_t ldy, double* sig_out,
                                                           int64_t* rank_dev, int max_sweeps) {
@@ -28,6 +30,8 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
   double* Cm = B + r * r;              // r x nrhs, row p, column c at Cm[c * r + p]
   double* nrm2 = Cm + r * nrhs;        // r
   __shared__ int rot_count;
+  __shared__ unsigned long long off_bits;   // max |g| / sqrt(a b) over the sweep (double bits)
+  const double tol = 1.1102230246251565e-16 * sqrt((double)r);   // rotation threshold
   const int tid = threadIdx.x, nth = blockDim.x;
   const int w = tid >> 5, lane = tid & 31, nw = nth >> 5;
   for (int e = tid; e < r * r; e += nth) {
@@ -56,6 +60,7 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
       for (int i = 0; i < r; ++i) m = fmax(m, nrm2[i]);
       smax2_sweep = m;
       rot_count = 0;
+      off_bits = 0ull;
     }
     __syncthreads();
     const double negl = (1e-3 * theta) * (1e-3 * theta) * smax2_sweep;
@@ -83,7 +88,10 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
         a = wsum(a);
         b = wsum(b);
         g = wsum(g);
-        if (g == 0.0 || !(fabs(g) > 1e-15 * sqrt(a) * sqrt(b)) || fmin(a, b) < negl) continue;
+        if (fmin(a, b) < negl || g == 0.0) continue;
+        const double rel = fabs(g) / (sqrt(a) * sqrt(b));
+        if (lane == 0) atomicMax(&off_bits, (unsigned long long)__double_as_longlong(rel));
+        if (!(rel > tol)) continue;
         const double zeta = (b - a) / (2.0 * g);
         const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
@@ -101,7 +109,9 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
       }
       __syncthreads();
     }
-    if (rot_count == 0) break;
+    // converged: no rotation, or every measured off-diagonal at the rounding level of the dots
+    if (tid == 0) g_small_sweeps = sweep + 1;
+    if (rot_count == 0 || __longlong_as_double((long long)off_bits) <= 8.0 * tol) break;
     __syncthreads();
   }
   // singular values = column norms of B W
@@ -137,6 +147,12 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
     for (int i = 0; i < r; ++i) kk += (nrm2[i] > thr2 && nrm2[i] > 0.0);
     *rank_dev = kk;
   }
+}
+
+extern "C" int az_debug_small_sweeps() {
+  int v = -1;
+  cudaMemcpyFromSymbol(&v, g_small_sweeps, sizeof(int));
+  return v;
 }
 
 size_t az_tsvd_ws_bytes(int64_t r, int64_t nrhs) {
