@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
                                                           int64_t* rank_dev, int max_sweeps) {
   extern __shared__ double sm[];
   double* B = sm;                      // r x r, column i at B + i * r
-  double* Cm = B + r * r;              // r x nrhs, row p, column c at Cm[c * r + p]
+  double* Cm = B + r * r;              // r x nrhs, row p, column c at Cm[p * nrhs + c] (rows contiguous)
   double* nrm2 = Cm + r * nrhs;        // r
   __shared__ int rot_count;
   __shared__ unsigned long long off_bits;   // max |g| / sqrt(a b) over the sweep (double bits)
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
   }
   for (int e = tid; e < r * nrhs; e += nth) {
     const int c = e / r, p = e % r;
-    Cm[e] = Rf[(int64_t)(r + c) * ldr + p];
+    Cm[p * nrhs + c] = Rf[(int64_t)(r + c) * ldr + p];
   }
   __syncthreads();
   const int n = r + (r & 1);           // padded to even
@@ -89,21 +89,23 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
         b = wsum(b);
         g = wsum(g);
         if (fmin(a, b) < negl || g == 0.0) continue;
-        const double rel = fabs(g) / (sqrt(a) * sqrt(b));
-        if (lane == 0) atomicMax(&off_bits, (unsigned long long)__double_as_longlong(rel));
-        if (!(rel > tol)) continue;
-        const double zeta = (b - a) / (2.0 * g);
-        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+        const double g2 = g * g, ab = a * b;
+        if (lane == 0) atomicMax(&off_bits, (unsigned long long)__double_as_longlong(sqrt(g2 / ab)));
+        if (!(g2 > tol * tol * ab)) continue;
+        // tan of the rotation angle, t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (b - a) / 2g,
+        // written without the intermediate division: t = 2 g sign(b - a) / (|b - a| + sqrt((b - a)^2 + 4 g^2))
+        const double d = b - a;
+        const double tt = (d >= 0.0 ? 2.0 * g : -2.0 * g) / (fabs(d) + sqrt(fma(d, d, 4.0 * g2)));
+        const double cs = rsqrt(fma(tt, tt, 1.0)), sn = cs * tt;
         for (int t = lane; t < r; t += 32) {
           const double xp = bp[t], xq = bq[t];
           bp[t] = cs * xp - sn * xq;
           bq[t] = sn * xp + cs * xq;
         }
         for (int c = lane; c < nrhs; c += 32) {
-          const double cp = Cm[c * r + p], cq = Cm[c * r + q];
-          Cm[c * r + p] = cs * cp - sn * cq;
-          Cm[c * r + q] = sn * cp + cs * cq;
+          const double cp = Cm[p * nrhs + c], cq = Cm[q * nrhs + c];
+          Cm[p * nrhs + c] = cs * cp - sn * cq;
+          Cm[q * nrhs + c] = sn * cp + cs * cq;
         }
         if (lane == 0) atomicAdd(&rot_count, 1);
       }
@@ -131,7 +133,7 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
     double acc = 0.0;
     for (int i = 0; i < r; ++i) {
       const double s2 = nrm2[i];
-      if (s2 > thr2 && s2 > 0.0) acc = fma(B[i * r + t], Cm[c * r + i] / s2, acc);
+      if (s2 > thr2 && s2 > 0.0) acc = fma(B[i * r + t], Cm[i * nrhs + c] / s2, acc);
     }
     y[(int64_t)c * ldy + t] = acc;
   }
