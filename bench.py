@@ -45,7 +45,7 @@ def measured_peaks():
 # algorithmic bytes / flops per unit (per complex vector PAIR for the pass kernels), DESIGN.md
 # "Algorithmic bytes per kernel".  n = coefficient length, L = fine length, M = rows.
 # ------------------------------------------------------------------------------------------
-def kernel_model(name, cfg, M, k_cols):
+def kernel_model(name, cfg, M, k_cols, k1=None):
     n = cfg.N
     L = cfg.N * cfg.s ** cfg.dim
     C = 16  # bytes per complex128
@@ -65,7 +65,10 @@ def kernel_model(name, cfg, M, k_cols):
     if name in hbm:
         return "hbm", hbm[name]
     if name == "tsqr_leaf":
-        return "alu", 2.0 * k_cols * k_cols     # flops per row (units = rows)
+        # Householder on [S | b'] triangularising the k1 probe columns: per row and reflector j a
+        # dot product and an axpy over the k - j - 1 trailing columns (4 flops each) plus the norm
+        k1 = k_cols if k1 is None else k1
+        return "alu", float(sum(4 * (k_cols - j - 1) + 2 for j in range(k1)))   # flops per row
     if name == "omega_apply":
         return "alu", 2.0                       # flops per (row x column x rhs) unit
     return None, None
@@ -182,6 +185,14 @@ def run_ours(args, cfg):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", init_method="env://")
+    elif args.sharded:          # the sharded path is collective even on one GPU
+        import socket
+        import torch.distributed as dist
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     theta = max(cfg.tol * 1e-2, 1e-12)
@@ -195,8 +206,17 @@ def run_ours(args, cfg):
     ws = torch.empty(plan.solve_workspace_bytes(cfg.nrhs, cfg.R, max_blocks), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # > L2 (126 MB)
 
-    def step():
-        return plan.solve(b, theta, cfg.R, max_blocks, x=x, workspace=ws)
+    if args.sharded:
+        from paper_2308_14490_b200 import dist as D
+        ops = D.GpuOps(plan)
+
+        def step(bb=None):
+            xs, r = D.solve_sharded(ops, b if bb is None else bb, theta, cfg.R, max_blocks)
+            return xs, dict(r, ms_rhs=0.0, ms_sketch=0.0, ms_qr=0.0, ms_svd=0.0, ms_step2=0.0, ms_total=0.0,
+                            sigma_first=0.0, sigma_last_kept=0.0)
+    else:
+        def step():
+            return plan.solve(b, theta, cfg.R, max_blocks, x=x, workspace=ws)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -231,14 +251,24 @@ def run_ours(args, cfg):
     # ---- end to end through the host-buffer entry point (pinned host memory) ----
     bh = torch.from_numpy(np.asfortranarray(b_host)).t().contiguous().pin_memory().t()
     xh = torch.empty((cfg.nrhs, plan.N), dtype=torch.float64).pin_memory().t()
+    if args.sharded:
+        bd = torch.empty_like(b)
+
+        def e2e_step():
+            bd.copy_(bh, non_blocking=True)
+            xs, _ = step(bd)
+            xh.copy_(xs, non_blocking=True)
+    else:
+        def e2e_step():
+            plan.solve_host(bh, theta, cfg.R, max_blocks, x=xh)
     for _ in range(2):
-        plan.solve_host(bh, theta, cfg.R, max_blocks, x=xh)
+        e2e_step()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ke = max(2, min(args.steps, 5))
     e0.record(stream)
     for _ in range(ke):
-        plan.solve_host(bh, theta, cfg.R, max_blocks, x=xh)
+        e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / ke
@@ -258,7 +288,7 @@ def run_ours(args, cfg):
     kcols = reps[-1]["probes"] + cfg.nrhs
     dom = max(trace.items(), key=lambda kv: kv[1][1])
     name, (cnt, tot_ms, units) = dom
-    bound, per_unit = kernel_model(name, cfg, plan.M, kcols)
+    bound, per_unit = kernel_model(name, cfg, plan.M, kcols, reps[-1]["probes"])
     roof = {"kernel": name, "launches": cnt, "ms_total": tot_ms, "share_of_step": tot_ms / sum(ms)}
     if bound == "hbm":
         achieved = per_unit * units / (tot_ms * 1e-3) / 1e9
@@ -280,31 +310,48 @@ def run_ours(args, cfg):
         except Exception:
             traffic = None
     roof["traffic"] = traffic
+    # aggregate HBM roofline of the FFT operator passes (SURVEY.md §8(d) pass model)
+    fb, ft = 0.0, 0.0
+    for k, (c_, t_, u_) in trace.items():
+        bnd, pu = kernel_model(k, cfg, plan.M, kcols)
+        if bnd == "hbm":
+            fb += pu * u_
+            ft += t_
+    roof_fft = None
+    if ft > 0:
+        ach = fb / (ft * 1e-3) / 1e9
+        roof_fft = {"kernels": "all FFT operator passes", "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
+                    "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "share_of_step": ft / sum(ms),
+                    "bytes_per_step": fb / args.steps, "peak_source": peak_src}
     # per-kernel table (share of the step)
     kernels = {k: {"launches": v[0], "ms_per_step": v[1] / args.steps, "units": v[2]} for k, v in
                sorted(trace.items(), key=lambda kv: -kv[1][1])}
 
     rep = reps[-1]
-    value = world * 1000.0 / ms_step
+    value = (1 if args.sharded else world) * 1000.0 / ms_step
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         est, sample, _ = oracle_sample(cfg, cfg.R)
         cpu = {"value": 1.0 / est, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": sample}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if args.sharded else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": cfg.name, "n": cfg.n, "L": cfg.s, "dim": cfg.dim, "nrhs": cfg.nrhs, "R": cfg.R,
-                   "tol": cfg.tol, "theta": theta, "max_blocks": max_blocks, "parallelism": f"replicas{world}",
+                   "tol": cfg.tol, "theta": theta, "max_blocks": max_blocks,
+                   "parallelism": (f"probe+rhs sharded over {world} (all-to-all re-block)" if args.sharded
+                                   else f"replicas{world}"),
                    "l2": "flushed between timed steps (256 MB write); S alone is 1.07 GB"},
         "probe_applies_per_s": world * rep["probes"] / (rep["ms_sketch"] * 1e-3) if rep["ms_sketch"] else None,
         "rhs_per_s": value * cfg.nrhs,
         "stages_ms": {k: rep[k] for k in ("ms_rhs", "ms_sketch", "ms_qr", "ms_svd", "ms_step2", "ms_total")},
         "rank": rep["rank"], "probes": rep["probes"], "saturated": rep["saturated"],
         "roofline": roof,
+        "roofline_fft_passes": roof_fft,
         "kernels": kernels,
         "cpu_baseline": cpu,
-        "e2e": {"value": world * 1000.0 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(b_host.nbytes),
+        "e2e": {"value": (1 if args.sharded else world) * 1000.0 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(b_host.nbytes),
                 "d2h_bytes_per_step": int(plan.N * cfg.nrhs * 8), "ms_per_step": e2e_ms},
         "gpu_launches": int(launches),
         "clocks": clk,
@@ -323,6 +370,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="one solve sharded over the ranks (probe/RHS columns + all-to-all re-block, strong "
+                         "scaling) instead of independent replicas (weak scaling)")
     args = ap.parse_args()
     cfg = I.get_config(args.config)
     if args.impl == "reference":

@@ -124,13 +124,19 @@ az_status_t az_omega_apply(az_plan_t plan, int64_t col0, int64_t ncols, const do
                            int64_t nrhs, double* x, int64_t ldx, int accumulate, void* stream);
 
 /* R factor of a tall matrix by Householder TSQR (no Q is formed; "SVD of an
- * (r+p)-by-M matrix" done as QR + small SVD).  A: m x k DEVICE column-major (ld lda), k <= 256
- * for the single-pass TSQR; larger k uses blocked Householder (A is overwritten).
+ * (r+p)-by-M matrix" done as QR + small SVD).  A: m x k DEVICE column-major (ld lda), k <= 128
+ * for the single-pass TSQR; larger k uses blocked Householder (A is overwritten, needs m >= k).
  * Rout: k x k upper-triangular DEVICE, leading dimension ldr (strict lower part zeroed).
  * Rows may be in any order (QR is row-permutation equivariant).                              */
 az_status_t az_qr_r(az_plan_t plan, double* A, int64_t m, int64_t k, int64_t lda,
                     double* Rout, int64_t ldr, void* workspace, size_t ws_bytes, void* stream);
 az_status_t az_qr_workspace_size(int64_t m, int64_t k, size_t* bytes);
+/* Same, triangularising only the leading k1 <= k columns (k <= 128, single-pass TSQR): Rout is
+ * k1 x k = [R_11 | (Q_1^T A[:, k1:])[:k1]], i.e. the right-hand sides riding along in the last
+ * k - k1 columns come out as Q^T b' (the multi-GPU solve merges such factors from row blocks).
+ * Workspace as for az_qr_r(m, k).  AZ_ERR_NOT_SUPPORTED if k > 128 and k1 < k.                 */
+az_status_t az_qr_r_partial(az_plan_t plan, double* A, int64_t m, int64_t k, int64_t k1, int64_t lda,
+                            double* Rout, int64_t ldr, void* workspace, size_t ws_bytes, void* stream);
 
 /* Truncated least squares on the QR-reduced sketch: with Rf = [R_S | c] (R_S: r x r upper
  * triangular, c: r x nrhs = (Q^T b')[:r]), compute R_S = U Sigma V^T (one-sided Jacobi SVD),

@@ -204,6 +204,21 @@ def qr_r(A: torch.Tensor, stream=None) -> torch.Tensor:
     return R
 
 
+def qr_r_partial(A: torch.Tensor, k1: int, stream=None) -> torch.Tensor:
+    """[R_11 | (Q^T A[:, k1:])[:k1]] (k1 x k) of a tall column-major A (m x k, k <= 128);
+    A is overwritten."""
+    pa, lda, k = _mat(A)
+    m = A.shape[0]
+    ws = C.c_size_t()
+    check("az_qr_workspace_size", lib().az_qr_workspace_size(m, k, C.byref(ws)))
+    w = torch.empty(max(ws.value, 1), dtype=torch.uint8, device=A.device)
+    R = empty_colmajor(k1, k, A.device)
+    pr, ldr, _ = _mat(R)
+    check("az_qr_r_partial", lib().az_qr_r_partial(None, C.c_void_p(pa), m, k, k1, lda, C.c_void_p(pr), ldr,
+                                                   C.c_void_p(w.data_ptr()), w.numel(), _stream(stream)))
+    return R
+
+
 def tsvd_solve(Rf: torch.Tensor, r: int, nrhs: int, theta: float, stream=None):
     """y = V_k Sigma_k^-1 U_k^T c from Rf = [R_S | c] (r x (r + nrhs)); returns (y, sigma, k)."""
     pr, ldr, _ = _mat(Rf)

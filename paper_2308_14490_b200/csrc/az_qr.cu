@@ -291,3 +291,16 @@ extern "C" az_status_t az_qr_r(az_plan_t, double* A, int64_t m, int64_t k, int64
   }
   return az_qr_r_impl(A, m, k, lda, R, ldr, ws, ws_bytes, (cudaStream_t)stream, k);
 }
+
+extern "C" az_status_t az_qr_r_partial(az_plan_t, double* A, int64_t m, int64_t k, int64_t k1, int64_t lda, double* R,
+                                       int64_t ldr, void* ws, size_t ws_bytes, void* stream) {
+  if (!A || !R || m < 1 || k < 1 || k1 < 1 || k1 > k || lda < m || ldr < k1) {
+    az_set_error("az_qr_r_partial: bad arguments");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  if (k > AZ_NARROW_MAX && k1 < k) {
+    az_set_error("az_qr_r_partial: k1 < k needs k <= %lld", (long long)AZ_NARROW_MAX);
+    return AZ_ERR_NOT_SUPPORTED;
+  }
+  return az_qr_r_impl(A, m, k, lda, R, ldr, ws, ws_bytes, (cudaStream_t)stream, k1);
+}

@@ -1,0 +1,157 @@
+"""Multi-process (gloo, world size 2, CPU) tests of the sharded solve's host logic
+(paper_2308_14490_b200/dist.py): shard ranges, the all-to-all re-block of the
+column-sharded sketch into row blocks, the merge of the per-block R factors, and the whole
+orchestration -- with a CPU backend built from the oracle standing in for libaz (the GPU kernels
+behind the same calls are covered by the -m gpu tests)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2308_14490_b200 import dist as D
+from paper_2308_14490_b200 import inputs as I
+from oracle import az as OA
+from oracle import philox as OP
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _cm(a):
+    return torch.from_numpy(np.asfortranarray(a))
+
+
+class CpuOps:
+    """Oracle-backed stand-in for libaz (test infrastructure only)."""
+
+    def __init__(self, cfg):
+        self.cfg = cfg
+        self.prob = OA.make_problem(cfg, "fft")
+        self.rows, self.N = self.prob.M + self.prob.Mb, cfg.N
+
+    @staticmethod
+    def contig(t):
+        return t
+
+    def resid(self, b):
+        return _cm(OA.resid_apply(self.prob, b.numpy()))
+
+    def sketch(self, col0, ncols):
+        om = OP.probes(self.N, list(range(col0, col0 + ncols)), self.cfg.seed)
+        return _cm(OA.step1_apply(self.prob, om))
+
+    def qr_partial(self, A, k1):
+        A = A.numpy()
+        m, k = A.shape
+        if m < k:
+            A = np.vstack([A, np.zeros((k - m, k))])
+        Rr = np.linalg.qr(A, mode="r")
+        return _cm(Rr[:k1])
+
+    def tsvd(self, Rf, r, nrhs, theta):
+        Rf = Rf.numpy()
+        U, s, Vt = np.linalg.svd(Rf[:r, :r])
+        kk = int(np.sum(s > theta * s[0]))
+        y = Vt[:kk].T @ ((U[:, :kk].T @ Rf[:r, r:r + nrhs]) / s[:kk, None])
+        return _cm(y), torch.from_numpy(s), kk
+
+    def omega_apply(self, col0, y):
+        om = OP.probes(self.N, list(range(col0, col0 + y.shape[0])), self.cfg.seed)
+        return _cm(om @ y.numpy())
+
+    def apply_A(self, x):
+        return _cm(self.prob.apply_A(x.numpy()))
+
+    def apply_Zstar(self, y):
+        return _cm(self.prob.apply_Zstar(y.numpy()))
+
+
+def test_split_is_balanced_partition():
+    for n in [0, 1, 7, 64, 1000003]:
+        for G in [1, 2, 3, 8]:
+            b = D.split(n, G)
+            assert b[0] == 0 and b[-1] == n and all(b[i] <= b[i + 1] for i in range(G))
+            assert max(b[i + 1] - b[i] for i in range(G)) - min(b[i + 1] - b[i] for i in range(G)) <= 1
+
+
+def _worker(rank, world, port, fn, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, fn(rank, world)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(fn, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fn, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return [out[r] for r in range(world)]
+
+
+def _reblock_case(rank, world):
+    rng = np.random.default_rng(0)
+    rows, kp, nrhs = 37, 5, 3
+    full = rng.standard_normal((rows, kp + nrhs))
+    ps, qs = D.split(kp, world), D.split(nrhs, world)
+    mine = np.hstack([full[:, ps[rank]:ps[rank + 1]], full[:, kp + qs[rank]:kp + qs[rank + 1]]])
+    owner = []
+    for g in range(world):
+        owner.append((g, ps[g], ps[g + 1]))
+        owner.append((g, kp + qs[g], kp + qs[g + 1]))
+    rs = D.split(rows, world)
+    A = D.reblock(_cm(mine), owner, kp + nrhs, rs)
+    return np.array_equal(A.numpy(), full[rs[rank]:rs[rank + 1]])
+
+
+def test_reblock_world2():
+    assert all(_run(_reblock_case))
+
+
+def _solve_case(rank, world):
+    cfg = I.make_config("interval", 256, nrhs=3, R=40)
+    ops = CpuOps(cfg)
+    b = _cm(I.rhs(cfg))
+    x, rep = D.solve_sharded(ops, b, 1e-12, cfg.R, max_blocks=4)
+    return x.numpy(), rep
+
+
+def _solve_case_1(rank, world):
+    return _solve_case(rank, world)
+
+
+def test_solve_sharded_world2_matches_single_and_oracle():
+    res2 = _run(_solve_case, 2)
+    res1 = _run(_solve_case_1, 1)
+    x0, rep0 = res2[0]
+    x1, rep1 = res2[1]
+    xs, reps = res1[0]
+    assert np.array_equal(x0, x1)                       # x replicated on every rank
+    assert rep0 == rep1 and rep0["probes"] == reps["probes"] and not rep0["saturated"]
+    cfg = I.make_config("interval", 256, nrhs=3, R=40)
+    grid = I.test_grid(cfg)
+    f2, f1 = OA.evaluate(cfg, x0, grid), OA.evaluate(cfg, xs, grid)
+    assert np.max(np.abs(f2 - f1)) <= 1e-10 * np.max(np.abs(f1))
+    prob = OA.make_problem(cfg, "fft")
+    b = I.rhs(cfg)
+    r2 = OA.az_solve(prob, b, 1e-12, cfg.R, cfg.seed, max_blocks=4)
+    fo = OA.evaluate(cfg, r2.x.reshape(cfg.N, -1), grid)
+    assert np.max(np.abs(f2 - fo)) <= 1e-9 * np.max(np.abs(fo))
+    assert abs(rep0["rank"] - r2.rank) <= 1

@@ -143,3 +143,29 @@ def test_solve_c2_full_size():
     prob = OA.make_problem(cfg, "fft")
     res = OA.relative_residual(prob, x[:, :4], b[:, :4])
     assert np.all(res <= 1e-8)
+
+
+@pytest.mark.parametrize("name,cfg,max_blocks", [("c1", I.get_config("c1"), 4),
+                                                 ("interval_n4096_4step", I.make_config("interval", 4096, nrhs=6, R=40), 4)])
+def test_solve_sharded_nccl_world1_matches_az_solve(name, cfg, max_blocks):
+    """The multi-GPU orchestration (dist.py) over NCCL at world size 1 on the GPU kernels: same
+    approximant as the single-call az_solve (the N > 1 host logic is covered by tests/test_dist.py)."""
+    import socket
+    import torch.distributed as dist
+    from paper_2308_14490_b200.api import Plan, colmajor
+    from paper_2308_14490_b200 import dist as D
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        plan = Plan.from_config(cfg)
+        b = _dev(I.rhs(cfg))
+        x1, rep1 = plan.solve(b, 1e-12, cfg.R, max_blocks)
+        xs, reps = D.solve_sharded(D.GpuOps(plan), colmajor(b), 1e-12, cfg.R, max_blocks)
+        assert reps["probes"] == rep1["probes"] and abs(reps["rank"] - rep1["rank"]) <= 1
+        grid = I.test_grid(cfg)
+        assert np.all(_approx_err(cfg, _host(xs), _host(x1), grid) <= 1e-10)
+    finally:
+        dist.destroy_process_group()
