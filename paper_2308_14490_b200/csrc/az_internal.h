@@ -36,6 +36,8 @@ struct az_plan_s {
   int32_t* d_pos = nullptr;     // G: row index of an interior grid point, -1 outside
   cplx* d_W0 = nullptr;         // fine symbol, order 0 (per axis length L; four-step: [N1][L2])
   cplx* d_W2 = nullptr;         // fine symbol, order 2 (Laplacian)
+  double* d_Wr = nullptr;       // four-step layout: the row symbol (W0, or alpha W2) as a real table
+                                // (phi^per samples are real and even, so W is real up to rounding)
   double* d_zinv = nullptr;     // N: 1/sigma^2(k) if kept else 0 (coefficient spectrum order)
   cplx* d_tw = nullptr;         // TWN-point twiddle table e^{-2 pi i t / TWN}
   cplx* d_tw4hi = nullptr;      // four-step twiddles e^{-2 pi i (h 2^TW4B) / L}

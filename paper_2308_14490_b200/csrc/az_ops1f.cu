@@ -17,6 +17,7 @@
 //   Z1  cols (N1):  E (scatter rows) -> FFT_N1 -> twiddle                     -> G
 //   Z3  cols (N1):  IFFT_N1 -> coefficient output
 #include <algorithm>
+#include <cstdlib>
 
 #include "az_fftr.cuh"
 #include "az_internal.h"
@@ -25,6 +26,7 @@ struct P1f {
   const cplx* W0;
   const cplx* W2;
   const double* zinv;
+  const double* Wr;      // real row symbol (plan d_Wr)
   const int32_t* pos;
   const uint8_t* mask;
   const cplx* tw;
@@ -76,10 +78,10 @@ AZ_D Cols1 pcols(const P1f& a, int b) {
 enum { FC_IN_COEF = 0, FC_FINE_MASK = 1, FC_OUT_GATHER = 2, FC_OUT_RESID = 3, FC_IN_ROWS = 4, FC_OUT_COEF = 5,
        FC_FWD_G = 6 };
 
-constexpr int EC = 16;    // values per thread in the column FFTs
-
-template <int NC, int TC, int KIND, int SRC>
-__global__ void __launch_bounds__(TC * (NC / EC), 2) k1f_cols(P1f a, double cout) {
+// EC = values per thread in the column FFTs (16: fewer exchanges; 8: half the registers, more
+// resident warps); MINB = CTAs per SM the register budget is sized for.
+template <int NC, int TC, int KIND, int SRC, int EC, int MINB>
+__global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double cout) {
   extern __shared__ cplx sm[];
   constexpr int T = NC / EC;
   const int tid = threadIdx.x, c = tid % TC, j = tid / TC;
@@ -130,6 +132,7 @@ __global__ void __launch_bounds__(TC * (NC / EC), 2) k1f_cols(P1f a, double cout
   if constexpr (KIND == FC_FINE_MASK) {
 #pragma unroll
     for (int e = 0; e < EC; ++e) mbits |= (a.mask[(int64_t)(j + e * T) * W + col] ? 1u : 0u) << e;
+    static_assert(EC <= 32, "mask bits");
   }
 
   // ---- transforms ----
@@ -148,11 +151,14 @@ __global__ void __launch_bounds__(TC * (NC / EC), 2) k1f_cols(P1f a, double cout
   // ---- store ----
   if constexpr (KIND == FC_IN_COEF || KIND == FC_IN_ROWS || KIND == FC_FINE_MASK || KIND == FC_FWD_G) {
     cplx* dst = (KIND == FC_IN_COEF) ? C1b : Gb;
+    // twiddle e^{-2 pi i k1 col tmul / L} for k1 = j + e T by recurrence in e (<= EC - 1 products)
+    cplx w = tw4<-1>(a, ((int64_t)j * col * tmul) & (a.L - 1));
+    const cplx ws = tw4<-1>(a, ((int64_t)T * col * tmul) & (a.L - 1));
 #pragma unroll
     for (int e = 0; e < EC; ++e) {
       const int k1 = j + e * T;
-      const int64_t t = ((int64_t)k1 * col * tmul) & (a.L - 1);
-      dst[(int64_t)k1 * W + col] = cmul(v[e], tw4<-1>(a, t));
+      dst[(int64_t)k1 * W + col] = cmul(v[e], w);
+      w = cmul(w, ws);
     }
   } else if constexpr (KIND == FC_OUT_GATHER || KIND == FC_OUT_RESID) {
 #pragma unroll
@@ -186,11 +192,12 @@ __global__ void __launch_bounds__(TC * (NC / EC), 2) k1f_cols(P1f a, double cout
 // ------------------------------------------------------------------------------------------
 enum { FR_EXPAND = 0, FR_EXPAND_KEEP = 1, FR_STEP1 = 2, FR_RESID = 3, FR_ZSTAR = 4, FR_AT = 5 };
 
-template <int NR2, int LR2, int RPC, int KIND>
-__global__ void __launch_bounds__(RPC * (LR2 / 16), 2) k1f_rows(P1f a, int nrows) {
+template <int NR2, int LR2, int RPC, int KIND, int EL, int MINB>
+__global__ void __launch_bounds__(RPC * (LR2 / EL), MINB) k1f_rows(P1f a, int nrows) {
   extern __shared__ cplx sm[];
   static_assert(LR2 == 2 * NR2, "four-step rows: L = 2 only");
-  constexpr int T = LR2 / 16;
+  constexpr int EN = EL / 2;            // values per thread of the length-NR2 transforms
+  constexpr int T = LR2 / EL;
   const int f = threadIdx.x / T, j = threadIdx.x % T;
   const int k1 = blockIdx.x * RPC + f;
   const bool live = k1 < nrows;
@@ -201,62 +208,77 @@ __global__ void __launch_bounds__(RPC * (LR2 / 16), 2) k1f_rows(P1f a, int nrows
   const double invL = 1.0 / (double)a.L;
   const int64_t rowW = (int64_t)(live ? k1 : 0) * LR2;     // row offset in W / G
   const int64_t rowC = (int64_t)(live ? k1 : 0) * NR2;     // row offset in C1 / zinv
-  cplx vn[8];
-  cplx vl[16];
+  cplx vn[EN];
+  cplx vl[EL];
 
   if constexpr (KIND == FR_EXPAND || KIND == FR_EXPAND_KEEP) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) vn[e] = live ? C1b[rowC + j + e * T] : czero();
-    fftr::fft<NR2, 8, -1>(vn, j, buf, a.tw, TWN);
+    for (int e = 0; e < EN; ++e) vn[e] = live ? C1b[rowC + j + e * T] : czero();
+    fftr::fft<NR2, EN, -1>(vn, j, buf, a.tw, TWN);
     if (KIND == FR_EXPAND_KEEP && live)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) C1b[rowC + j + e * T] = vn[e];
+      for (int e = 0; e < EN; ++e) C1b[rowC + j + e * T] = vn[e];
   } else {
 #pragma unroll
-    for (int e = 0; e < 16; ++e) vl[e] = live ? Gb[rowW + j + e * T] : czero();
-    fftr::fft<LR2, 16, -1>(vl, j, buf, a.tw, TWN);
+    for (int e = 0; e < EL; ++e) vl[e] = live ? Gb[rowW + j + e * T] : czero();
+    fftr::fft<LR2, EL, -1>(vl, j, buf, a.tw, TWN);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < EN; ++e) {
       const int k2 = j + e * T;
-      cplx acc = cadd(cmulc(vl[e], sym1f(a, rowW + k2)), cmulc(vl[e + 8], sym1f(a, rowW + k2 + NR2)));
+      cplx acc = cadd(cscale(vl[e], a.Wr[rowW + k2]), cscale(vl[e + EN], a.Wr[rowW + k2 + NR2]));
       if (KIND != FR_AT) acc = cscale(acc, a.zinv[rowC + k2]);
       if (KIND == FR_STEP1) acc = csub(C1b[rowC + k2], acc);
       vn[e] = acc;
     }
   }
   if constexpr (KIND == FR_ZSTAR || KIND == FR_AT) {
-    fftr::fft<NR2, 8, 1>(vn, j, buf, a.tw, TWN);
-    if (live)
+    fftr::fft<NR2, EN, 1>(vn, j, buf, a.tw, TWN);
+    if (live) {
+      // e^{+2 pi i n2 k1 / n} = e^{+2 pi i (2 n2 k1) / L}, n2 = j + e T, by recurrence in e
+      cplx w = tw4<1>(a, ((int64_t)j * k1 * 2) & (a.L - 1));
+      const cplx ws = tw4<1>(a, ((int64_t)T * k1 * 2) & (a.L - 1));
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int n2 = j + e * T;
-        const int64_t t = ((int64_t)n2 * k1 * 2) & (a.L - 1);     // e^{+2 pi i n2 k1 / n}
-        C1b[rowC + n2] = cmul(vn[e], tw4<1>(a, t));
+      for (int e = 0; e < EN; ++e) {
+        C1b[rowC + j + e * T] = cmul(vn[e], w);
+        w = cmul(w, ws);
       }
+    }
   } else {
 #pragma unroll
-    for (int e = 0; e < 16; ++e) vl[e] = cscale(cmul(vn[e & 7], sym1f(a, rowW + j + e * T)), invL);
-    fftr::fft<LR2, 16, 1>(vl, j, buf, a.tw, TWN);
-    if (live)
+    for (int e = 0; e < EL; ++e) vl[e] = cscale(vn[e & (EN - 1)], a.Wr[rowW + j + e * T] * invL);
+    fftr::fft<LR2, EL, 1>(vl, j, buf, a.tw, TWN);
+    if (live) {
+      // e^{+2 pi i n2' k1 / L}, n2' = j + e T, by recurrence in e
+      cplx w = tw4<1>(a, ((int64_t)j * k1) & (a.L - 1));
+      const cplx ws = tw4<1>(a, ((int64_t)T * k1) & (a.L - 1));
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int n2 = j + e * T;
-        const int64_t t = ((int64_t)n2 * k1) & (a.L - 1);          // e^{+2 pi i n2' k1 / L}
-        Gb[rowW + n2] = cmul(vl[e], tw4<1>(a, t));
+      for (int e = 0; e < EL; ++e) {
+        Gb[rowW + j + e * T] = cmul(vl[e], w);
+        w = cmul(w, ws);
       }
+    }
   }
 }
 
 // ------------------------------------------------------------------------------------------
 // host orchestration
 // ------------------------------------------------------------------------------------------
-template <int NC, int KIND, int SRC>
-static az_status_t fcols(const P1f& a, int ncols, int nb, double cout, cudaStream_t st) {
+static int fft_e() {   // AZ_FFT_E=8 selects the 8-values-per-thread variant (tuning knob)
+  static int e = 0;
+  if (!e) {
+    const char* v = getenv("AZ_FFT_E");
+    e = (v && atoi(v) == 8) ? 8 : 16;
+  }
+  return e;
+}
+
+template <int NC, int KIND, int SRC, int EC, int MINB>
+static az_status_t fcols_e(const P1f& a, int ncols, int nb, double cout, cudaStream_t st) {
   constexpr int T = NC / EC;
-  constexpr int TC0 = 256 / T;
+  constexpr int TC0 = (EC == 8 ? 512 : 256) / T;
   constexpr int TC = TC0 < 2 ? 2 : (TC0 > 16 ? 16 : TC0);
   const size_t sm = (size_t)TC * fftr::padded_len(NC) * sizeof(cplx);
-  auto kern = k1f_cols<NC, TC, KIND, SRC>;
+  auto kern = k1f_cols<NC, TC, KIND, SRC, EC, MINB>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   static const char* names[] = {"1f_cols_in_coef", "1f_cols_fine_mask", "1f_cols_out_gather", "1f_cols_out_resid",
                                 "1f_cols_in_rows", "1f_cols_out_coef", "1f_cols_fwd"};
@@ -266,14 +288,20 @@ static az_status_t fcols(const P1f& a, int ncols, int nb, double cout, cudaStrea
   return AZ_OK;
 }
 
-template <int NR2, int KIND>
-static az_status_t frows(const P1f& a, int nb, cudaStream_t st) {
+template <int NC, int KIND, int SRC>
+static az_status_t fcols(const P1f& a, int ncols, int nb, double cout, cudaStream_t st) {
+  if (fft_e() == 8) return fcols_e<NC, KIND, SRC, 8, 4>(a, ncols, nb, cout, st);
+  return fcols_e<NC, KIND, SRC, 16, 2>(a, ncols, nb, cout, st);
+}
+
+template <int NR2, int KIND, int EL, int MINB>
+static az_status_t frows_e(const P1f& a, int nb, cudaStream_t st) {
   constexpr int LR2 = 2 * NR2;
-  constexpr int T = LR2 / 16;
+  constexpr int T = LR2 / EL;
   constexpr int RPC0 = 256 / T;
   constexpr int RPC = RPC0 < 1 ? 1 : (RPC0 > 64 ? 64 : RPC0);
   const size_t sm = (size_t)RPC * fftr::padded_len(LR2) * sizeof(cplx);
-  auto kern = k1f_rows<NR2, LR2, RPC, KIND>;
+  auto kern = k1f_rows<NR2, LR2, RPC, KIND, EL, MINB>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   static const char* names[] = {"1f_rows_expand", "1f_rows_expand_keep", "1f_rows_step1", "1f_rows_resid",
                                 "1f_rows_zstar", "1f_rows_at"};
@@ -281,6 +309,12 @@ static az_status_t frows(const P1f& a, int nb, cudaStream_t st) {
   kern<<<dim3(az_div_up(a.N1, RPC), nb), RPC * T, sm, st>>>(a, a.N1);
   AZ_LAUNCH_CHECK();
   return AZ_OK;
+}
+
+template <int NR2, int KIND>
+static az_status_t frows(const P1f& a, int nb, cudaStream_t st) {
+  if (fft_e() == 8) return frows_e<NR2, KIND, 8, 4>(a, nb, st);
+  return frows_e<NR2, KIND, 16, 2>(a, nb, st);
 }
 
 template <int NC, int NR2>
@@ -331,6 +365,7 @@ static P1f make_p1f(az_plan_s* p) {
   a.W0 = p->d_W0;
   a.W2 = p->d_W2;
   a.zinv = p->d_zinv;
+  a.Wr = p->d_Wr;
   a.pos = p->d_pos;
   a.mask = p->d_mask;
   a.tw = p->d_tw;

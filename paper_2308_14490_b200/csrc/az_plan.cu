@@ -204,6 +204,13 @@ __global__ void k_twiddles(cplx* tw, int twn, cplx* hi, cplx* lo, int64_t Lbig, 
 }
 
 // Lemma 3 on the fine grid: w[q] = phi^per(q h_L) (order 0 or 2), q in [0, L).
+// real part of the row symbol (the imaginary part of the DFT of the real even kernel samples is
+// rounding noise)
+__global__ void k_real_sym(double* Wr, const cplx* W0, const cplx* W2, int lap, double alpha, int64_t L) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < L) Wr[i] = lap ? alpha * W2[i].x : W0[i].x;
+}
+
 __global__ void k_samples(cplx* out, int64_t L, double hL, double eps, double T, int order) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q < L) out[q] = make_double2(az_phi_per((double)q * hL, eps, T, order), 0.0);
@@ -315,7 +322,7 @@ static int ilog2(int64_t v) { int k = 0; while ((int64_t(1) << k) < v) ++k; retu
 
 static void plan_free(az_plan_s* p) {
   if (!p) return;
-  void* ptrs[] = {p->d_mask, p->d_pos, p->d_W0, p->d_W2, p->d_zinv, p->d_tw, p->d_tw4hi,
+  void* ptrs[] = {p->d_mask, p->d_pos, p->d_W0, p->d_W2, p->d_Wr, p->d_zinv, p->d_tw, p->d_tw4hi,
                   p->d_tw4lo, p->d_bxy, p->d_bw, p->d_bj, p->d_C1, p->d_G, p->d_solve_ws};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -405,6 +412,11 @@ static az_status_t plan_build(az_plan_s* p, const az_plan_desc_t* d, cudaStream_
       AZ_TRY(az1f_fft_fine_forward(p, W, st));
     else
       AZ_TRY(az_fft_batch(p->d_tw, W, p->L, 1, -1, st));
+  }
+  if (p->layout == AZ_LAYOUT_1D_FOURSTEP) {
+    AZ_TRY(dalloc(&p->d_Wr, p->L));
+    k_real_sym<<<az_div_up(p->L, 256), 256, 0, st>>>(p->d_Wr, p->d_W0, p->d_W2, lap, p->alpha, p->L);
+    AZ_LAUNCH_CHECK();
   }
   // ---- sigma^2, max, thresholded inverse ----
   double* d_sig2;
