@@ -49,17 +49,19 @@ def kernel_model(name, cfg, M, k_cols, k1=None):
     n = cfg.N
     L = cfg.N * cfg.s ** cfg.dim
     C = 16  # bytes per complex128
+    # 1-D intervals: the mask is one run of the grid, so no row-map / mask bytes are read
+    pos_b, mask_b = (0, 0) if cfg.dim == 1 else (4, 1)
     hbm = {
         "1f_cols_in_coef": C * n,                      # probes generated on chip; write spectrum
         "1f_rows_expand_keep": 2 * C * n + C * L,
         "1f_rows_expand": C * n + C * L,
-        "1f_cols_fine_mask": 2 * C * L + L,            # read + write fine grid, read mask (1 B)
+        "1f_cols_fine_mask": 2 * C * L + mask_b * L,   # read + write fine grid, read mask (1 B)
         "1f_rows_step1": 2 * C * L + C * n + 8 * n,    # fine grid in/out, v^ and zinv in
         "1f_rows_resid": 2 * C * L + 8 * n,
         "1f_rows_zstar": C * L + C * n + 8 * n,
-        "1f_cols_out_gather": C * L + 4 * L + 2 * 8 * M,   # fine grid + row map in, 2 columns out
-        "1f_cols_out_resid": C * L + 4 * L + 4 * 8 * M,
-        "1f_cols_in_rows": 4 * L + 2 * 8 * M + C * L,
+        "1f_cols_out_gather": C * L + pos_b * L + 2 * 8 * M,   # fine grid + row map in, 2 columns out
+        "1f_cols_out_resid": C * L + pos_b * L + 4 * 8 * M,
+        "1f_cols_in_rows": pos_b * L + 2 * 8 * M + C * L,
         "1f_cols_out_coef": C * n + 2 * 8 * n,
     }
     if name in hbm:

@@ -34,6 +34,8 @@ struct az_plan_s {
   // device tables
   uint8_t* d_mask = nullptr;    // G
   int32_t* d_pos = nullptr;     // G: row index of an interior grid point, -1 outside
+  int64_t run0 = -1, run1 = -1; // the mask is the single run [run0, run1) of the natural grid order
+                                // (1-D intervals): row = g - run0, no table lookups
   cplx* d_W0 = nullptr;         // fine symbol, order 0 (per axis length L; four-step: [N1][L2])
   cplx* d_W2 = nullptr;         // fine symbol, order 2 (Laplacian)
   double* d_Wr = nullptr;       // four-step layout: the row symbol (W0, or alpha W2) as a real table

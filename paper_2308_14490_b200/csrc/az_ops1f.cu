@@ -29,6 +29,7 @@ struct P1f {
   const double* Wr;      // real row symbol (plan d_Wr)
   const int32_t* pos;
   const uint8_t* mask;
+  int64_t run0, run1;    // single-run mask (plan run0/run1), else run0 < 0
   const cplx* tw;
   const cplx* t4hi;
   const cplx* t4lo;
@@ -47,7 +48,11 @@ struct P1f {
   int64_t nvec, col0, pair0;
 };
 
-AZ_D cplx sym1f(const P1f& a, int64_t idx) { return a.lap ? cscale(a.W2[idx], a.alpha) : a.W0[idx]; }
+// row of the fine grid point g (natural order), -1 outside Omega
+AZ_D int row_of(const P1f& a, int64_t g) {
+  if (a.run0 >= 0) return (g >= a.run0 && g < a.run1) ? (int)(g - a.run0) : -1;
+  return a.pos[g];
+}
 
 // e^{DIR 2 pi i t / L} for t in [0, L)
 template <int DIR>
@@ -120,7 +125,7 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
   } else if constexpr (KIND == FC_IN_ROWS) {
 #pragma unroll
     for (int e = 0; e < EC; ++e) {
-      const int r = a.pos[(int64_t)(j + e * T) * W + col];
+      const int r = row_of(a, (int64_t)(j + e * T) * W + col);
       v[e] = r >= 0 ? make_double2(a.in[r + cc.cre * a.ldin], cc.has_im ? a.in[r + cc.cim * a.ldin] : 0.0) : czero();
     }
   } else {
@@ -131,7 +136,11 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
   uint32_t mbits = 0;   // FC_FINE_MASK: the 16 mask bytes of this thread, packed
   if constexpr (KIND == FC_FINE_MASK) {
 #pragma unroll
-    for (int e = 0; e < EC; ++e) mbits |= (a.mask[(int64_t)(j + e * T) * W + col] ? 1u : 0u) << e;
+    for (int e = 0; e < EC; ++e) {
+      const int64_t g = (int64_t)(j + e * T) * W + col;
+      const bool in = a.run0 >= 0 ? (g >= a.run0 && g < a.run1) : a.mask[g] != 0;
+      mbits |= (in ? 1u : 0u) << e;
+    }
     static_assert(EC <= 32, "mask bits");
   }
 
@@ -163,7 +172,7 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
   } else if constexpr (KIND == FC_OUT_GATHER || KIND == FC_OUT_RESID) {
 #pragma unroll
     for (int e = 0; e < EC; ++e) {
-      const int r = a.pos[(int64_t)(j + e * T) * W + col];
+      const int r = row_of(a, (int64_t)(j + e * T) * W + col);
       if (r >= 0) {
         if constexpr (KIND == FC_OUT_RESID) {
           a.out[r + cc.cre * a.ldout] = a.in[r + cc.cre * a.ldin] - v[e].x;
@@ -263,11 +272,12 @@ __global__ void __launch_bounds__(RPC * (LR2 / EL), MINB) k1f_rows(P1f a, int nr
 // ------------------------------------------------------------------------------------------
 // host orchestration
 // ------------------------------------------------------------------------------------------
-static int fft_e() {   // AZ_FFT_E=8 selects the 8-values-per-thread variant (tuning knob)
+static int fft_e() {   // tuning knob: AZ_FFT_E=8 (8 values per thread), 17 (16 values, 8 columns per CTA)
   static int e = 0;
   if (!e) {
     const char* v = getenv("AZ_FFT_E");
-    e = (v && atoi(v) == 8) ? 8 : 16;
+    e = v ? atoi(v) : 16;
+    if (e != 8 && e != 17) e = 16;
   }
   return e;
 }
@@ -275,7 +285,7 @@ static int fft_e() {   // AZ_FFT_E=8 selects the 8-values-per-thread variant (tu
 template <int NC, int KIND, int SRC, int EC, int MINB>
 static az_status_t fcols_e(const P1f& a, int ncols, int nb, double cout, cudaStream_t st) {
   constexpr int T = NC / EC;
-  constexpr int TC0 = (EC == 8 ? 512 : 256) / T;
+  constexpr int TC0 = (EC == 8 || MINB == 1 ? 512 : 256) / T;
   constexpr int TC = TC0 < 2 ? 2 : (TC0 > 16 ? 16 : TC0);
   const size_t sm = (size_t)TC * fftr::padded_len(NC) * sizeof(cplx);
   auto kern = k1f_cols<NC, TC, KIND, SRC, EC, MINB>;
@@ -291,6 +301,7 @@ static az_status_t fcols_e(const P1f& a, int ncols, int nb, double cout, cudaStr
 template <int NC, int KIND, int SRC>
 static az_status_t fcols(const P1f& a, int ncols, int nb, double cout, cudaStream_t st) {
   if (fft_e() == 8) return fcols_e<NC, KIND, SRC, 8, 4>(a, ncols, nb, cout, st);
+  if (fft_e() == 17) return fcols_e<NC, KIND, SRC, 16, 1>(a, ncols, nb, cout, st);
   return fcols_e<NC, KIND, SRC, 16, 2>(a, ncols, nb, cout, st);
 }
 
@@ -367,6 +378,8 @@ static P1f make_p1f(az_plan_s* p) {
   a.zinv = p->d_zinv;
   a.Wr = p->d_Wr;
   a.pos = p->d_pos;
+  a.run0 = p->run0;
+  a.run1 = p->run1;
   a.mask = p->d_mask;
   a.tw = p->d_tw;
   a.t4hi = p->d_tw4hi;

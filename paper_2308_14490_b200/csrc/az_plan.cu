@@ -347,6 +347,18 @@ static az_status_t plan_build(az_plan_s* p, const az_plan_desc_t* d, cudaStream_
   int64_t M = 0;
   for (int64_t g = 0; g < p->G; ++g) pos[g] = d->mask[g] ? (int32_t)(M++) : -1;
   p->M = M;
+  {
+    int64_t first = -1, last = -1;
+    for (int64_t g = 0; g < p->G; ++g)
+      if (d->mask[g]) {
+        if (first < 0) first = g;
+        last = g;
+      }
+    if (first >= 0 && last - first + 1 == M) {
+      p->run0 = first;
+      p->run1 = last + 1;
+    }
+  }
   if (p->M + p->Mb <= p->N) {
     az_set_error("oversampling insufficient: M + Mb = %lld <= N = %lld (PAPER.md:124)",
                  (long long)(p->M + p->Mb), (long long)p->N);
