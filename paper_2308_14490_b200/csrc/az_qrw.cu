@@ -117,10 +117,10 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) k_qr_panel(PanelArgs a) {
       const int64_t nr = re - rlo;
       const int ncl = a.nb - j - 1;
       if (nr > 0)
-        for (int64_t e = tid; e < nr * ncl; e += PANEL_THREADS) {
-          const int l = j + 1 + (int)(e / nr);
-          const int64_t r = rlo + e % nr;
-          a.A[(a.j0 + l) * a.lda + r] = fma(-tau * dsum[l], col[r], a.A[(a.j0 + l) * a.lda + r]);
+        for (int l = j + 1; l < j + 1 + ncl; ++l) {     // columns outer, rows across threads (no div/mod)
+          double* cl = a.A + (a.j0 + l) * a.lda;
+          const double wl = -tau * dsum[l];
+          for (int64_t r = rlo + tid; r < re; r += PANEL_THREADS) cl[r] = fma(wl, col[r], cl[r]);
         }
       if (owner)
         for (int l = j + 1 + tid; l < a.nb; l += PANEL_THREADS) a.A[(a.j0 + l) * a.lda + jc] -= tau * dsum[l];

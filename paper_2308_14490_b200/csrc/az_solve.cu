@@ -238,6 +238,7 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   std::vector<int64_t> pj0(w.maxpanels);
   std::vector<int> pnb(w.maxpanels);
   int64_t np = 0;
+  double s1lo = 0.0;   // lower bound on sigma_1 of the sketch's R factor
   for (nb = 1; nb <= max_blocks; ++nb) {
     const int64_t kp = nb * R;                 // probe columns
     const int64_t kt = kp + nrhs;
@@ -268,7 +269,33 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
       AZ_LAUNCH_CHECK();
     }
     cudaEventRecord(e2, st);
-    AZ_TRY(az_tsvd_impl(w.Rf, kt, kp, nrhs, theta, w.y, kp, w.sig, &rank, w.svdws, w.svdbytes, st));
+    bool full_svd = true;
+    if (w.wide && nb >= 2 && nb < max_blocks) {
+      // Cheap saturation pre-test (reading R5): with R_b = [[R11, R12], [0, R22]] and
+      // R22 the new block's R x R corner, sigma_{kp-R+j}(R_b) <= sigma_j(R22) (R_b minus a rank
+      // kp - R matrix), so rank_t(S) <= kp - R + rank_t(R22) for any threshold t.  With
+      // t = theta * s1lo, s1lo <= sigma_1(R_b) (singular values of the leading block and of R22
+      // are lower bounds), k22 <= R - p proves the sketch unsaturated; otherwise the full SVD is
+      // skipped and another block is drawn (a possibly extra block, never a missing one).
+      const int64_t off = (nb - 1) * R;
+      int64_t k22 = 0;
+      AZ_TRY(az_tsvd_impl(w.Rf + off * kt + off, kt, R, 0, 0.0, w.y, R, w.sig, &k22, w.svdws, w.svdbytes, st));
+      std::vector<double> s22(R);
+      AZ_CUDA_CHECK(cudaMemcpyAsync(s22.data(), w.sig, sizeof(double) * R, cudaMemcpyDeviceToHost, st));
+      AZ_CUDA_CHECK(cudaStreamSynchronize(st));
+      s1lo = std::max(s1lo, s22[0]);
+      k22 = 0;
+      for (int64_t i = 0; i < R; ++i) k22 += s22[i] > theta * s1lo;
+      full_svd = k22 <= R - pfix;
+      rank = kp;   // not computed: treated as saturated unless the full SVD runs
+    }
+    if (full_svd) {
+      AZ_TRY(az_tsvd_impl(w.Rf, kt, kp, nrhs, theta, w.y, kp, w.sig, &rank, w.svdws, w.svdbytes, st));
+      double s1 = 0.0;
+      AZ_CUDA_CHECK(cudaMemcpyAsync(&s1, w.sig, sizeof(double), cudaMemcpyDeviceToHost, st));
+      AZ_CUDA_CHECK(cudaStreamSynchronize(st));
+      s1lo = std::max(s1lo, s1);
+    }
     cudaEventRecord(e3, st);
     cudaEventSynchronize(e3);
     ms_sketch += ms_between(e0, e1);

@@ -44,6 +44,7 @@ struct BJArgs {
   unsigned long long* off;  // max relative off-diagonal seen this sweep (double bits, >= 0)
   double tol;               // rotate while |G_pq| > tol sqrt(G_pp G_qq)
   int inner_sweeps;
+  long long* dbg;           // optional phase timestamps (cluster 0, rank 0): 8 x clock64
 };
 
 AZ_D void pair_of(int round, int pi, int n, int& p, int& q) {
@@ -89,6 +90,8 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
     const int64_t col = (c < BW) ? (int64_t)bi * BW + c : (int64_t)bj * BW + (c - BW);
     return col < r ? col : -1;
   };
+  const bool dbg = a.dbg && blockIdx.x == 0 && threadIdx.x == 0;
+  if (dbg) a.dbg[0] = clock64();
   // ---------------- partial Gram G = X^T X over rows [rb, re) ----------------
   {
     const int wm = w & 1, wn = (w >> 1) & 1, wk = w >> 2;
@@ -132,15 +135,28 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
           for (int e = 0; e < 2; ++e)
             G[acc_row(wm * 32, i, lane) * GS + acc_col(wn * 32, j, e, lane)] += acc[i][j][e];
   }
+  if (dbg) a.dbg[1] = clock64();
   cluster.sync();                     // partial Grams complete
+  if (dbg) a.dbg[2] = clock64();
   const double negl = (1e-3 * a.theta) * (1e-3 * a.theta) * (*a.smax2);
-  if (crank == 0) {
-    // fixed-order reduction of the partial Grams (leader's own slice first)
-    for (int c = 1; c < CS; ++c) {
-      const double* Gr = cluster.map_shared_rank(G, c);
-      for (int e = tid; e < PW * GS; e += 256) G[e] += Gr[e];
+  if (CS > 1) {
+    // distributed fixed-order reduction: CTA c sums its slice of the entries over ranks 0..CS-1
+    // and writes the sums into the leader's staging buffer X (free at this point)
+    double* Xl = cluster.map_shared_rank(X, 0);
+    const int per = (PW * GS + CS - 1) / CS;
+    const int e0 = crank * per, e1 = min(PW * GS, e0 + per);
+    for (int e = e0 + tid; e < e1; e += 256) {
+      double t = 0.0;
+      for (int c = 0; c < CS; ++c) t += cluster.map_shared_rank(G, c)[e];
+      Xl[e] = t;
     }
-    __syncthreads();
+    cluster.sync();
+    if (crank == 0) {
+      for (int e = tid; e < PW * GS; e += 256) G[e] = X[e];
+      __syncthreads();
+    }
+  }
+  if (crank == 0) {
     // ---------------- convergence measure ----------------
     double mx = 0.0;
     for (int e = tid; e < PW * PW; e += 256) {
@@ -159,56 +175,78 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
     __syncthreads();
     if (any_rot) {
       // ---------------- eigen-decomposition of G by cyclic Jacobi ----------------
+      // 8 threads per rotation pair (32 disjoint pairs per round): each thread recomputes the
+      // pair's (c, s) itself (no broadcast), then rotates 8 of the 64 entries of rows p, q
+      // (phase A) and of columns p, q of G and V (phase B): two barriers per round.
       for (int e = tid; e < PW * PW; e += 256) V[(e / PW) * VS + (e % PW)] = (e / PW == e % PW) ? 1.0 : 0.0;
-      __syncthreads();
+      __shared__ int rot_any;
+      const int pk = tid >> 3, sub = tid & 7;
+      const double tol2 = a.tol * a.tol;
       for (int sw = 0; sw < a.inner_sweeps; ++sw) {
+        if (tid == 0) rot_any = 0;
+        __syncthreads();
         for (int rd = 0; rd < PW - 1; ++rd) {
-          if (tid < PW / 2) {
-            int p, q;
-            pair_of(rd, tid, PW, p, q);
-            const double gp = G[p * GS + p], gq = G[q * GS + q], g = G[p * GS + q];
-            double c = 1.0, s = 0.0;
-            if (g != 0.0 && fabs(g) > a.tol * sqrt(gp * gq) && fmin(gp, gq) >= negl) {
-              const double zeta = (gq - gp) / (2.0 * g);
-              const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-              c = 1.0 / sqrt(1.0 + t * t);
-              s = c * t;
+          if (dbg && rd == 5 && sw == 0) a.dbg[0] = clock64();
+          int p, q;
+          pair_of(rd, pk, PW, p, q);
+          const double gp = G[p * GS + p], gq = G[q * GS + q], g = G[p * GS + q];
+          double c = 1.0, sn = 0.0;
+          const double g2 = g * g;
+          const bool rot_pq = g != 0.0 && g2 > tol2 * gp * gq && fmin(gp, gq) >= negl;
+          if (rot_pq) {
+            // t = tan = 2 g sign(d) / (|d| + sqrt(d^2 + 4 g^2)), d = G_qq - G_pp
+            const double d = gq - gp;
+            const double t = (d >= 0.0 ? 2.0 * g : -2.0 * g) / (fabs(d) + sqrt(fma(d, d, 4.0 * g2)));
+            c = rsqrt(fma(t, t, 1.0));
+            sn = c * t;
+            if (sub == 0) rot_any = 1;
+          }
+          if (dbg && rd == 5 && sw == 0) a.dbg[6] = clock64();
+          __syncthreads();   // every pair has read its 2 x 2 block before any row is rotated
+          if (dbg && rd == 5 && sw == 0) a.dbg[7] = clock64();
+          // all loads of a phase are issued before its first store (no load waits on a store)
+          if (rot_pq) {
+            double xp[PW / 8], xq[PW / 8];
+#pragma unroll
+            for (int i = 0; i < PW / 8; ++i) {
+              const int t = sub + 8 * i;     // interleaved: 8 consecutive banks per pair
+              xp[i] = G[p * GS + t];
+              xq[i] = G[q * GS + t];
             }
-            rc[tid] = c;
-            rs[tid] = s;
-            rp[tid] = p;
-            rq[tid] = q;
+#pragma unroll
+            for (int i = 0; i < PW / 8; ++i) {
+              const int t = sub + 8 * i;
+              G[p * GS + t] = c * xp[i] - sn * xq[i];
+              G[q * GS + t] = sn * xp[i] + c * xq[i];
+            }
           }
           __syncthreads();
-          // rows p, q of G
-          for (int e = tid; e < (PW / 2) * PW; e += 256) {
-            const int k = e / PW, t = e % PW;
-            const double c = rc[k], s = rs[k];
-            if (s == 0.0) continue;
-            const int p = rp[k], q = rq[k];
-            const double xp = G[p * GS + t], xq = G[q * GS + t];
-            G[p * GS + t] = c * xp - s * xq;
-            G[q * GS + t] = s * xp + c * xq;
-          }
-          __syncthreads();
-          // columns p, q of G and of V
-          for (int e = tid; e < (PW / 2) * PW; e += 256) {
-            const int k = e / PW, t = e % PW;
-            const double c = rc[k], s = rs[k];
-            if (s == 0.0) continue;
-            const int p = rp[k], q = rq[k];
-            const double xp = G[t * GS + p], xq = G[t * GS + q];
-            G[t * GS + p] = c * xp - s * xq;
-            G[t * GS + q] = s * xp + c * xq;
-            const double vp = V[t * VS + p], vq = V[t * VS + q];
-            V[t * VS + p] = c * vp - s * vq;
-            V[t * VS + q] = s * vp + c * vq;
+          if (rot_pq) {
+            double xp[PW / 8], xq[PW / 8], vp[PW / 8], vq[PW / 8];
+#pragma unroll
+            for (int i = 0; i < PW / 8; ++i) {
+              const int t = sub + 8 * i;
+              xp[i] = G[t * GS + p];
+              xq[i] = G[t * GS + q];
+              vp[i] = V[t * VS + p];
+              vq[i] = V[t * VS + q];
+            }
+#pragma unroll
+            for (int i = 0; i < PW / 8; ++i) {
+              const int t = sub + 8 * i;
+              G[t * GS + p] = c * xp[i] - sn * xq[i];
+              G[t * GS + q] = sn * xp[i] + c * xq[i];
+              V[t * VS + p] = c * vp[i] - sn * vq[i];
+              V[t * VS + q] = sn * vp[i] + c * vq[i];
+            }
           }
           __syncthreads();
         }
+        if (!rot_any) break;
       }
     }
   }
+  if (dbg) a.dbg[3] = clock64();
   cluster.sync();                     // leader's V and flag ready
   const int rot = *cluster.map_shared_rank(&any_rot, 0);
   if (rot && crank != 0) {
@@ -216,6 +254,7 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
     for (int e = tid; e < PW * VS; e += 256) V[e] = Vr[e];
   }
   cluster.sync();                     // leader's shared memory no longer read remotely
+  if (dbg) a.dbg[4] = clock64();
   if (!rot) return;
   // ---------------- X <- X V over this CTA's row slice, tiles of 64 rows ----------------
   {
@@ -252,6 +291,7 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
           }
     }
   }
+  if (dbg) a.dbg[5] = clock64();
   // ---------------- c rows of the pair <- V^T c (leader) ----------------
   if (crank == 0 && a.nrhs > 0) {
     __syncthreads();
@@ -376,7 +416,7 @@ __global__ void k_bjac_load(const double* Rf, int64_t ldr, int64_t r, int nrhs, 
 static size_t a256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 static int g_last_sweeps = 0;
-static int g_inner_sweeps = 2;
+static int g_inner_sweeps = 1;
 extern "C" int az_debug_jacobi(int inner_sweeps) {   // returns the outer sweeps of the last block-Jacobi SVD
   if (inner_sweeps > 0) g_inner_sweeps = inner_sweeps;
   return g_last_sweeps;
@@ -435,6 +475,13 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
   a.off = off;
   a.tol = 4.0 * 1.1102230246251565e-16 * std::sqrt((double)r);
   a.inner_sweeps = g_inner_sweeps;
+  a.dbg = nullptr;
+  static long long* d_dbg = nullptr;
+  const bool want_dbg = getenv("AZ_DEBUG_JACOBI") != nullptr;
+  if (want_dbg) {
+    if (!d_dbg) cudaMalloc(&d_dbg, 8 * sizeof(long long));
+    a.dbg = d_dbg;
+  }
   int sw = 0;
   for (; sw < max_sweeps; ++sw) {
     {
@@ -466,7 +513,12 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
     AZ_CUDA_CHECK(cudaStreamSynchronize(st));
     double offd;
     memcpy(&offd, &h_off, sizeof(offd));
-    if (getenv("AZ_DEBUG_JACOBI")) fprintf(stderr, "bjac r=%lld sweep %d off %.3e tol %.3e\n", (long long)r, sw, offd, a.tol);
+    if (want_dbg) {
+      long long h[8];
+      cudaMemcpy(h, d_dbg, sizeof(h), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "bjac r=%lld CS=%d sweep %d off %.3e tol %.3e | last round clocks: eig %lld wait2 %lld | inner round: param %lld sync1 %lld\n",
+              (long long)r, CS, sw, offd, a.tol, h[3] - h[2], h[4] - h[3], h[6] - h[0], h[7] - h[6]);
+    }
     if (offd <= 4.0 * a.tol) {   // rounding level of the measured off-diagonals
       ++sw;
       break;
@@ -481,7 +533,7 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
     k_bjac_max<<<1, 1024, 0, st>>>(nrm2, r, smax2, off);
     AZ_LAUNCH_CHECK();
   }
-  {
+  if (nrhs > 0) {
     AzTrace tr("bjac_solve", st, 2 * r * r * nrhs);
     k_bjac_solve<<<dim3(az_div_up(r, 256), az_div_up(nrhs, 32)), 256, 0, st>>>(B, C, nrm2, smax2, r, (int)nrhs,
                                                                                theta, y, ldy);
