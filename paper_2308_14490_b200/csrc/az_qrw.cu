@@ -26,6 +26,7 @@
 namespace cg = cooperative_groups;
 
 constexpr int QB = 64;            // panel width
+constexpr int QB0 = 8;            // base panel width of the recursive panel factorisation
 constexpr int PANEL_THREADS = 512;
 
 AZ_D double qr_warp_sum(double v) {
@@ -75,9 +76,11 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) k_qr_panel(PanelArgs a) {
     }
     grid.sync();
     // ---- phase B: reflector (every CTA computes the same numbers in the same order) ----
-    if (tid == 0) {
+    if (w == 0) {
+      // fixed-order cross-CTA sum: lane-strided partials, then a fixed shuffle tree
       double sig = 0.0;
-      for (int i = 0; i < G; ++i) sig += R1[i];
+      for (int i = lane; i < G; i += 32) sig += R1[i];
+      sig = qr_warp_sum(sig);
       const double alpha = col[jc];
       double beta = alpha, tau = 0.0, scale = 0.0;
       if (sig > 0.0) {
@@ -86,9 +89,11 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) k_qr_panel(PanelArgs a) {
         tau = (beta - alpha) / beta;
         scale = 1.0 / (alpha - beta);
       }
-      sc[0] = beta;
-      sc[1] = tau;
-      sc[2] = scale;
+      if (lane == 0) {
+        sc[0] = beta;
+        sc[1] = tau;
+        sc[2] = scale;
+      }
     }
     __syncthreads();
     const double scale = sc[2];
@@ -106,11 +111,12 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) k_qr_panel(PanelArgs a) {
     grid.sync();
     // ---- phase D: apply H_j to the remaining panel columns; extend T ----
     const double tau = sc[1];
-    for (int l = tid; l < a.nb; l += PANEL_THREADS) {
+    for (int l = w; l < a.nb; l += NW) {   // one warp per column, lanes over the CTAs' partials
       double t = 0.0;
       if (l != j)
-        for (int i = 0; i < G; ++i) t += R2[(int64_t)i * QB + l];
-      dsum[l] = t;
+        for (int i = lane; i < G; i += 32) t += R2[(int64_t)i * QB + l];
+      t = qr_warp_sum(t);
+      if (lane == 0) dsum[l] = t;
     }
     __syncthreads();
     if (tau != 0.0) {
@@ -254,39 +260,150 @@ __global__ void __launch_bounds__(256) k_qr_wred(UpdArgs a, int KC) {
   }
 }
 
-// C[rows j0.., n] -= V[rows, 0:QB] Wfin[0:QB, n]: CTA tile 128 rows x 64 columns, K = QB at once.
+// C[rows j0.., n] -= V[rows, 0:QB] Wfin[0:QB, n]: a CTA owns 128 rows and sweeps all target
+// columns in tiles of 64, so its V tile is read from HBM once.  The accumulators start from C
+// (DMMA computes D = A B + C with A = -V), and the next tile's C fragments and W' tile are
+// fetched into registers while the current tile's MMAs run.
 constexpr int UP_SA = 132, UP_SB = 68;
-__global__ void __launch_bounds__(256) k_qr_upd(UpdArgs a) {
+__global__ void __launch_bounds__(256, 2) k_qr_upd(UpdArgs a) {
   extern __shared__ double sm[];
-  double* As = sm;                    // KMAJ [k = panel col][m = row], stride 132
+  double* As = sm;                    // KMAJ [k = panel col][m = row], stride 132 (holds -V)
   double* Bs = sm + QB * UP_SA;       // IMAJ [n = target col][k], stride 68
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int wm = w & 3, wn = w >> 2;
   const int64_t rbase = a.j0 + (int64_t)blockIdx.x * 128;
-  const int64_t n0 = (int64_t)blockIdx.y * 64;
   for (int e = tid; e < QB * 128; e += 256) {
     const int l = e >> 7, ri = e & 127;
     const int64_t r = rbase + ri;
-    As[l * UP_SA + ri] = r < a.m ? v_elem(a.V, a.ldv, a.j0, a.nb, r, l) : 0.0;
+    As[l * UP_SA + ri] = r < a.m ? -v_elem(a.V, a.ldv, a.j0, a.nb, r, l) : 0.0;
   }
-  for (int e = tid; e < QB * 64; e += 256) {
-    const int n = e >> 6, l = e & 63;
-    Bs[n * UP_SB + l] = (n0 + n < a.nt) ? a.Wfin[(n0 + n) * QB + l] : 0.0;
+  double acc[4][4][2];
+  double wv[16];
+  auto load_tile = [&](int64_t n0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t r = rbase + acc_row(wm * 32, i, lane);
+          const int64_t n = n0 + acc_col(wn * 32, j, e, lane);
+          acc[i][j][e] = (r < a.m && n < a.nt) ? a.C[n * a.ldc + r] : 0.0;
+        }
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int e = tid + 256 * t, n = e >> 6, l = e & 63;
+      wv[t] = (n0 + n < a.nt) ? a.Wfin[(n0 + n) * QB + l] : 0.0;
+    }
+  };
+  load_tile(0);
+  for (int64_t n0 = 0; n0 < a.nt; n0 += 64) {
+    __syncthreads();                  // previous tile's MMAs are done with Bs
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int e = tid + 256 * t, n = e >> 6, l = e & 63;
+      Bs[n * UP_SB + l] = wv[t];
+    }
+    __syncthreads();
+    double cur[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        cur[i][j][0] = acc[i][j][0];
+        cur[i][j][1] = acc[i][j][1];
+      }
+    if (n0 + 64 < a.nt) load_tile(n0 + 64);   // next C fragments and W' tile in flight
+    warp_mma<4, 4, KMAJ, IMAJ>(cur, As, UP_SA, Bs, UP_SB, wm * 32, wn * 32, 0, QB, lane);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t r = rbase + acc_row(wm * 32, i, lane);
+          const int64_t n = n0 + acc_col(wn * 32, j, e, lane);
+          if (r < a.m && n < a.nt) a.C[n * a.ldc + r] = cur[i][j][e];
+        }
   }
-  __syncthreads();
+}
+
+
+// ------------------------------------------------------------------------------------------
+// T of a QB-wide panel from its Gram matrix: Gv = V^T V (split-K DMMA partials over row chunks,
+// V with the implicit unit diagonal), then the dlarft recurrence
+//   T[j][j] = tau_j,  T[0:j, j] = -tau_j T[0:j, 0:j] Gv[0:j, j]
+// with tau_j read off the diagonals of the base-panel T factors.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_qr_vtv(UpdArgs a) {
+  __shared__ double Xs[QB * VT_S];   // IMAJ [col][k]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wm = w & 1, wn = (w >> 1) & 1, wk = w >> 2;
+  const int kc = blockIdx.x;
+  const int64_t r0 = a.j0 + (int64_t)kc * a.kchunk;
+  const int64_t r1 = min(a.m, r0 + a.kchunk);
   double acc[4][4][2];
   acc_zero(acc);
-  warp_mma<4, 4, KMAJ, IMAJ>(acc, As, UP_SA, Bs, UP_SB, wm * 32, wn * 32, 0, QB, lane);
+  const int lk = tid & 31, li = tid >> 5;
+  double v[8];
+  auto load = [&](int64_t rr) {
+    const int64_t r = rr + lk;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+    for (int t = 0; t < 8; ++t) v[t] = r < r1 ? v_elem(a.V, a.ldv, a.j0, a.nb, r, li + 8 * t) : 0.0;
+  };
+  load(r0);
+  for (int64_t rr = r0; rr < r1; rr += VT_BK) {
+    __syncthreads();
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int t = 0; t < 8; ++t) Xs[(li + 8 * t) * VT_S + lk] = v[t];
+    __syncthreads();
+    if (rr + VT_BK < r1) load(rr + VT_BK);
+    warp_mma<4, 4, IMAJ, IMAJ>(acc, Xs, VT_S, Xs, VT_S, wm * 32, wn * 32, wk * 16, 16, lane);
+  }
+  double* W = a.Wpart + (int64_t)kc * QB * QB;
+  // the two k halves: the first writes the partial, the second adds to it
+  if (wk == 0)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int64_t r = rbase + acc_row(wm * 32, i, lane);
-        const int64_t n = n0 + acc_col(wn * 32, j, e, lane);
-        if (r < a.m && n < a.nt) a.C[n * a.ldc + r] -= acc[i][j][e];
-      }
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) W[acc_col(wn * 32, j, e, lane) * QB + acc_row(wm * 32, i, lane)] = acc[i][j][e];
+  __syncthreads();
+  if (wk == 1)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) W[acc_col(wn * 32, j, e, lane) * QB + acc_row(wm * 32, i, lane)] += acc[i][j][e];
+}
+
+__global__ void __launch_bounds__(256) k_qr_tbuild(const double* Wpart, int KC, const double* Tslots, int nb,
+                                                    double* T) {
+  extern __shared__ double smt[];
+  double* Gv = smt;              // QB x QB
+  double* Ts = smt + QB * QB;    // QB x QB
+  __shared__ double tau[QB];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < QB * QB; e += 256) {
+    double t = 0.0;
+    for (int kc = 0; kc < KC; ++kc) t += Wpart[(int64_t)kc * QB * QB + e];
+    Gv[e] = t;
+    Ts[e] = 0.0;
+  }
+  for (int j = tid; j < QB; j += 256) tau[j] = j < nb ? Tslots[(j / QB0) * QB * QB + (j % QB0) * QB + (j % QB0)] : 0.0;
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    if (tid < j) {
+      double t = 0.0;
+      for (int q = tid; q < j; ++q) t = fma(Ts[q * QB + tid], Gv[j * QB + q], t);   // (T Gv[:, j])[tid]
+      Ts[j * QB + tid] = -tau[j] * t;
+    }
+    if (tid == 0) Ts[j * QB + j] = tau[j];
+    __syncthreads();
+  }
+  for (int e = tid; e < QB * QB; e += 256) T[e] = Ts[e];
 }
 
 // ------------------------------------------------------------------------------------------
@@ -308,7 +425,11 @@ static int64_t qrw_kc(int64_t rows) {   // split-K chunks for V^T C
 }
 
 // workspace: [panel partials | Wpart (KC x QB x nt) | Wfin (QB x nt)]
-static size_t qrw_part_bytes() { return ((size_t)qrw_sms() * (1 + QB) * sizeof(double) + 255) & ~(size_t)255; }
+static size_t qrw_part_bytes() {
+  // panel partial sums + (QB / QB0) base-panel T slots
+  return (((size_t)qrw_sms() * (1 + QB) * sizeof(double) + 255) & ~(size_t)255) +
+         (size_t)(QB / QB0) * QB * QB * sizeof(double);
+}
 
 size_t az_qrw_ws_bytes(int64_t m, int64_t ncols_max) {
   const int64_t KC = qrw_kc(m);
@@ -343,7 +464,7 @@ az_status_t az_qrw_apply(const double* V, int64_t ldv, int64_t m, const int64_t*
     if (rows <= 0) break;
     const int64_t KC = qrw_kc(rows);
     u.kchunk = (rows + KC - 1) / KC;
-    u.Wpart = (double*)((char*)ws + qrw_part_bytes());
+    u.Wpart = (double*)((char*)ws + qrw_part_bytes());   // (also the V^T V partials of k_qr_vtv)
     u.Wfin = u.Wpart + (size_t)KC * QB * nt;
     u.T = Tbuf + p * QB * QB;
     {
@@ -358,7 +479,7 @@ az_status_t az_qrw_apply(const double* V, int64_t ldv, int64_t m, const int64_t*
     }
     {
       AzTrace tr("qrw_upd", st, 2 * rows * u.nb * nt);
-      k_qr_upd<<<dim3(az_div_up(rows, 128), az_div_up(nt, 64)), 256, ups, st>>>(u);
+      k_qr_upd<<<az_div_up(rows, 128), 256, ups, st>>>(u);
       AZ_LAUNCH_CHECK();
     }
   }
@@ -384,30 +505,62 @@ az_status_t az_qrw_factor(double* A, int64_t lda, int64_t m, int64_t c0, int64_t
     return AZ_ERR_CUDA;
   }
   double* part = (double*)ws;
+  double* Tslots = (double*)((char*)ws + (((size_t)qrw_sms() * (1 + QB) * sizeof(double) + 255) & ~(size_t)255));
   for (int64_t j0 = c0; j0 < c1; j0 += QB) {
-    PanelArgs pa;
-    pa.A = A;
-    pa.lda = lda;
-    pa.m = m;
-    pa.j0 = j0;
-    pa.nb = (int)std::min<int64_t>(QB, c1 - j0);
-    const int64_t rows = m - j0;
-    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(qrw_sms(), (rows + 127) / 128));
-    pa.chunk = (rows + G - 1) / G;
+    const int nbp = (int)std::min<int64_t>(QB, c1 - j0);
     const int64_t p = (*np)++;
     pj0[p] = j0;
-    pnb[p] = pa.nb;
-    pa.T = Tbuf + p * QB * QB;
-    pa.part = part;
-    void* args[] = {&pa};
-    {
-      AzTrace tr("qrw_panel", st, rows * pa.nb);
-      AZ_CUDA_CHECK(cudaLaunchCooperativeKernel((void*)k_qr_panel, dim3((unsigned)G), dim3(PANEL_THREADS), args, 0, st));
-      az_count_launch();
+    pnb[p] = nbp;
+    // recursive panel: QB0-wide base panels factored column by column (the base panel stays
+    // L2-resident), each applied to the rest of the QB panel through the blocked update
+    for (int b0 = 0; b0 < nbp; b0 += QB0) {
+      PanelArgs pa;
+      pa.A = A;
+      pa.lda = lda;
+      pa.m = m;
+      pa.j0 = j0 + b0;
+      pa.nb = std::min(QB0, nbp - b0);
+      const int64_t rows = m - pa.j0;
+      const int64_t G = std::max<int64_t>(1, std::min<int64_t>(qrw_sms(), (rows + 127) / 128));
+      pa.chunk = (rows + G - 1) / G;
+      pa.T = Tslots + (b0 / QB0) * QB * QB;
+      pa.part = part;
+      void* args[] = {&pa};
+      {
+        AzTrace tr("qrw_panel", st, rows * pa.nb);
+        AZ_CUDA_CHECK(cudaLaunchCooperativeKernel((void*)k_qr_panel, dim3((unsigned)G), dim3(PANEL_THREADS), args, 0, st));
+        az_count_launch();
+      }
+      const int64_t rest = nbp - (b0 + pa.nb);
+      if (rest > 0) {
+        const int64_t bj0 = pa.j0;
+        const int bnb = pa.nb;
+        AZ_TRY(az_qrw_apply(A, lda, m, &bj0, &bnb, pa.T, 0, 1, A + (pa.j0 + pa.nb) * lda, lda, rest, ws, ws_bytes, st));
+      }
     }
-    const int64_t nt = c1 - (j0 + pa.nb);
+    // T of the whole QB panel from V^T V and the base taus
+    {
+      UpdArgs u;
+      u.V = A;
+      u.ldv = lda;
+      u.j0 = j0;
+      u.nb = nbp;
+      u.m = m;
+      const int64_t rows = m - j0;
+      const int64_t KC = qrw_kc(rows);
+      u.kchunk = (rows + KC - 1) / KC;
+      u.Wpart = (double*)((char*)ws + qrw_part_bytes());
+      AzTrace tr("qrw_tbuild", st);
+      k_qr_vtv<<<(unsigned)KC, 256, 0, st>>>(u);
+      AZ_LAUNCH_CHECK();
+      const size_t tsm = 2 * QB * QB * sizeof(double);
+      AZ_CUDA_CHECK(az_smem_attr(k_qr_tbuild, tsm));
+      k_qr_tbuild<<<1, 256, tsm, st>>>(u.Wpart, (int)KC, Tslots, nbp, Tbuf + p * QB * QB);
+      AZ_LAUNCH_CHECK();
+    }
+    const int64_t nt = c1 - (j0 + nbp);
     if (nt > 0)
-      AZ_TRY(az_qrw_apply(A, lda, m, pj0, pnb, Tbuf, p, p + 1, A + (j0 + pa.nb) * lda, lda, nt, ws, ws_bytes, st));
+      AZ_TRY(az_qrw_apply(A, lda, m, pj0, pnb, Tbuf, p, p + 1, A + (j0 + nbp) * lda, lda, nt, ws, ws_bytes, st));
   }
   return AZ_OK;
 }

@@ -14,11 +14,19 @@ g = torch.Generator(device="cuda").manual_seed(0)
 if mode == "qr":
     m, k = int(sys.argv[2]), int(sys.argv[3])
     A = api.colmajor(torch.randn(m, k, dtype=torch.float64, device="cuda", generator=g))
+    A2 = A.clone()
+    api.qr_r(A2)
     torch.cuda.synchronize(); t = time.time()
+    api.trace_enable(True)
     R = api.qr_r(A)
     torch.cuda.synchronize()
     dt = time.time() - t
+    tr = api.trace_report()
+    api.trace_enable(False)
     print(f"qr {m}x{k}: {dt*1e3:.1f} ms, {2*m*k*k/dt/1e12:.2f} TFLOP/s (2mk^2)")
+    for name, (c, ms, u) in sorted(tr.items(), key=lambda kv: -kv[1][1]):
+        extra = f" {u*1e-9/ms:.1f} TFLOP/s" if name in ("qrw_vtc", "qrw_upd") else ""
+        print(f"  {name:12s} {c:5d} launches {ms:9.2f} ms{extra}")
 else:
     r, nrhs = int(sys.argv[2]), int(sys.argv[3])
     X = torch.randn(2 * r, r, dtype=torch.float64, device="cuda", generator=g)
