@@ -219,6 +219,26 @@ __global__ void __launch_bounds__(RPC * (LR2 / EL), MINB) k1f_rows(P1f a, int nr
   const int64_t rowC = (int64_t)(live ? k1 : 0) * NR2;     // row offset in C1 / zinv
   cplx vn[EN];
   cplx vl[EL];
+  // the row's symbol / 1/sigma^2 / v^ inputs are copied into shared memory with cp.async at kernel
+  // start, so their DRAM latency overlaps the first transform instead of stalling the fold
+  constexpr bool NEED_Z = (KIND == FR_STEP1 || KIND == FR_RESID || KIND == FR_ZSTAR);
+  constexpr bool NEED_C = (KIND == FR_STEP1);
+  double* pre = reinterpret_cast<double*>(sm + RPC * fftr::padded_len(LR2)) + f * (LR2 + 3 * NR2);
+  double* Ws = pre;                 // LR2 real symbol values of the row
+  double* Zs = pre + LR2;           // NR2 values of 1/sigma^2
+  cplx* Cs = reinterpret_cast<cplx*>(pre + LR2 + NR2);   // NR2 values of v^
+  if (live) {
+    auto cp16 = [](void* dst, const void* src) {
+      const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+    };
+    for (int i = j; i < LR2 / 2; i += T) cp16(Ws + 2 * i, a.Wr + rowW + 2 * i);
+    if constexpr (NEED_Z)
+      for (int i = j; i < NR2 / 2; i += T) cp16(Zs + 2 * i, a.zinv + rowC + 2 * i);
+    if constexpr (NEED_C)
+      for (int i = j; i < NR2; i += T) cp16(Cs + i, C1b + rowC + i);
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
 
   if constexpr (KIND == FR_EXPAND || KIND == FR_EXPAND_KEEP) {
 #pragma unroll
@@ -227,16 +247,20 @@ __global__ void __launch_bounds__(RPC * (LR2 / EL), MINB) k1f_rows(P1f a, int nr
     if (KIND == FR_EXPAND_KEEP && live)
 #pragma unroll
       for (int e = 0; e < EN; ++e) C1b[rowC + j + e * T] = vn[e];
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
   } else {
 #pragma unroll
     for (int e = 0; e < EL; ++e) vl[e] = live ? Gb[rowW + j + e * T] : czero();
     fftr::fft<LR2, EL, -1>(vl, j, buf, a.tw, TWN);
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
 #pragma unroll
     for (int e = 0; e < EN; ++e) {
       const int k2 = j + e * T;
-      cplx acc = cadd(cscale(vl[e], a.Wr[rowW + k2]), cscale(vl[e + EN], a.Wr[rowW + k2 + NR2]));
-      if (KIND != FR_AT) acc = cscale(acc, a.zinv[rowC + k2]);
-      if (KIND == FR_STEP1) acc = csub(C1b[rowC + k2], acc);
+      cplx acc = cadd(cscale(vl[e], Ws[k2]), cscale(vl[e + EN], Ws[k2 + NR2]));
+      if constexpr (KIND != FR_AT) acc = cscale(acc, Zs[k2]);
+      if constexpr (KIND == FR_STEP1) acc = csub(Cs[k2], acc);
       vn[e] = acc;
     }
   }
@@ -254,7 +278,7 @@ __global__ void __launch_bounds__(RPC * (LR2 / EL), MINB) k1f_rows(P1f a, int nr
     }
   } else {
 #pragma unroll
-    for (int e = 0; e < EL; ++e) vl[e] = cscale(vn[e & (EN - 1)], a.Wr[rowW + j + e * T] * invL);
+    for (int e = 0; e < EL; ++e) vl[e] = cscale(vn[e & (EN - 1)], Ws[j + e * T] * invL);
     fftr::fft<LR2, EL, 1>(vl, j, buf, a.tw, TWN);
     if (live) {
       // e^{+2 pi i n2' k1 / L}, n2' = j + e T, by recurrence in e
@@ -309,9 +333,9 @@ template <int NR2, int KIND, int EL, int MINB>
 static az_status_t frows_e(const P1f& a, int nb, cudaStream_t st) {
   constexpr int LR2 = 2 * NR2;
   constexpr int T = LR2 / EL;
-  constexpr int RPC0 = 256 / T;
+  constexpr int RPC0 = 128 / T;
   constexpr int RPC = RPC0 < 1 ? 1 : (RPC0 > 64 ? 64 : RPC0);
-  const size_t sm = (size_t)RPC * fftr::padded_len(LR2) * sizeof(cplx);
+  const size_t sm = (size_t)RPC * (fftr::padded_len(LR2) * sizeof(cplx) + (LR2 + 3 * NR2) * sizeof(double));
   auto kern = k1f_rows<NR2, LR2, RPC, KIND, EL, MINB>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   static const char* names[] = {"1f_rows_expand", "1f_rows_expand_keep", "1f_rows_step1", "1f_rows_resid",
@@ -325,7 +349,7 @@ static az_status_t frows_e(const P1f& a, int nb, cudaStream_t st) {
 template <int NR2, int KIND>
 static az_status_t frows(const P1f& a, int nb, cudaStream_t st) {
   if (fft_e() == 8) return frows_e<NR2, KIND, 8, 4>(a, nb, st);
-  return frows_e<NR2, KIND, 16, 2>(a, nb, st);
+  return frows_e<NR2, KIND, 16, 3>(a, nb, st);
 }
 
 template <int NC, int NR2>
