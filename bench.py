@@ -250,6 +250,33 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
 
+    # ---- factorisation reuse: factor once, then solve with new RHS ----
+    factored = None
+    if not args.sharded:
+        fe0, fe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fe0.record(stream)
+        fac = api.Factor(plan, theta, cfg.R, max_blocks)
+        fe1.record(stream)
+        torch.cuda.synchronize()
+        fws = torch.empty(fac.workspace_bytes(cfg.nrhs), dtype=torch.uint8, device=dev)
+        for _ in range(2):
+            fac.solve(b, x=x, workspace=fws)
+        torch.cuda.synchronize()
+        kf = max(3, min(args.steps, 10))
+        fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(kf)]
+        for i in range(kf):
+            flush.fill_(i & 0xFF)
+            fev[i][0].record(stream)
+            fac.solve(b, x=x, workspace=fws)
+            fev[i][1].record(stream)
+        torch.cuda.synchronize()
+        fms = sum(a.elapsed_time(bb) for a, bb in fev) / kf
+        factored = {"solves_per_s": world * 1000.0 / fms, "ms_per_solve": fms, "ms_factorize": fe0.elapsed_time(fe1),
+                    "probes": fac.report["probes"], "rank": fac.report["rank"],
+                    "note": "az_solve_factored: b', Q^T b' from the stored panels, y = P (Q^T b'), Omega y, step 2"}
+        fac.close()
+        del fws
+
     # ---- end to end through the host-buffer entry point (pinned host memory) ----
     bh = torch.from_numpy(np.asfortranarray(b_host)).t().contiguous().pin_memory().t()
     xh = torch.empty((cfg.nrhs, plan.N), dtype=torch.float64).pin_memory().t()
@@ -351,6 +378,7 @@ def run_ours(args, cfg):
         "rank": rep["rank"], "probes": rep["probes"], "saturated": rep["saturated"],
         "roofline": roof,
         "roofline_fft_passes": roof_fft,
+        "factored": factored,
         "kernels": kernels,
         "cpu_baseline": cpu,
         "e2e": {"value": (1 if args.sharded else world) * 1000.0 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(b_host.nbytes),

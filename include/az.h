@@ -182,6 +182,25 @@ const char* az_last_error(void);
  * for the bench's gpu_launches field). */
 int64_t az_launch_count(int reset);
 
+/* ---- factorisation reuse --------------------------------------------
+ * The step-1 matrix (A - A Z* A) Omega does not depend on b (Alg. 1, :228, :283): factor
+ * it once, then solve for any number of right-hand sides at the cost of b' = (I - A Z*) b, Q^T b'
+ * (the stored Householder panels), y = P (Q^T b')[:k] with P the truncated pseudo-inverse of R_S
+ * (V_k Sigma_k^-1 U_k^T, sigma > theta sigma_1), x2 = Omega y and step 2.  The factor owns its
+ * DEVICE memory (the factored sketch, rows x probes, and P, probes x probes).  az_factorize
+ * draws probe blocks exactly as az_solve (reading R5) and returns AZ_WARN_SKETCH_SATURATED (with a
+ * usable factor) if max_blocks is exhausted.  The plan must outlive the factor.               */
+typedef struct az_factor_s* az_factor_t;
+az_status_t az_factorize(az_plan_t plan, double theta, int64_t R, int32_t max_blocks, az_factor_t* out,
+                         az_solve_report_t* report, void* stream);
+az_status_t az_factor_destroy(az_factor_t f);
+az_status_t az_factor_query(az_factor_t f, int64_t* probes, int64_t* rank);
+/* b: (M+Mb) x nrhs, x: N x nrhs, DEVICE column-major; workspace from az_factor_workspace_size. */
+az_status_t az_factor_workspace_size(az_factor_t f, int64_t nrhs, size_t* bytes);
+az_status_t az_solve_factored(az_factor_t f, const double* b, int64_t ldb, double* x, int64_t ldx,
+                              int64_t nrhs, void* workspace, size_t ws_bytes,
+                              az_solve_report_t* report, void* stream);
+
 /* Per-kernel CUDA-event tracing for measurement (bench.py roofline): when enabled, every libaz
  * launch is bracketed by two events on its stream.  az_trace_report synchronises those events
  * and writes "name count total_ms\n" lines into buf (NUL-terminated, truncated to len).

@@ -69,6 +69,11 @@ def lib():
         "az_omega_apply": [P, I64, I64, P, I64, I64, P, I64, C.c_int, P],
         "az_qr_r": [P, P, I64, I64, I64, P, I64, P, C.c_size_t, P],
         "az_qr_r_partial": [P, P, I64, I64, I64, I64, P, I64, P, C.c_size_t, P],
+        "az_factorize": [P, D, I64, C.c_int32, C.POINTER(P), C.POINTER(SolveReport), P],
+        "az_factor_destroy": [P],
+        "az_factor_query": [P, C.POINTER(I64), C.POINTER(I64)],
+        "az_factor_workspace_size": [P, I64, C.POINTER(C.c_size_t)],
+        "az_solve_factored": [P, P, I64, P, I64, I64, P, C.c_size_t, C.POINTER(SolveReport), P],
         "az_qr_workspace_size": [I64, I64, C.POINTER(C.c_size_t)],
         "az_tsvd_solve": [P, I64, I64, I64, D, P, I64, P, C.POINTER(I64), P, C.c_size_t, P],
         "az_tsvd_workspace_size": [I64, I64, C.POINTER(C.c_size_t)],
@@ -96,7 +101,9 @@ EXPORTED = ["az_plan_create", "az_plan_destroy", "az_plan_query", "az_apply_A", 
             "az_apply_Zstar", "az_apply_step1", "az_apply_resid", "az_sketch", "az_omega_apply",
             "az_qr_r", "az_qr_r_partial", "az_qr_workspace_size", "az_tsvd_solve", "az_tsvd_workspace_size",
             "az_solve_workspace_size", "az_solve", "az_solve_host", "az_status_string",
-            "az_last_error", "az_launch_count", "az_trace_enable", "az_trace_report"]
+            "az_last_error", "az_launch_count", "az_trace_enable", "az_trace_report",
+            "az_factorize", "az_factor_destroy", "az_factor_query", "az_factor_workspace_size",
+            "az_solve_factored"]
 
 
 def check(fn: str, status: int, allow=(AZ_OK,)):

@@ -183,6 +183,52 @@ class Plan:
         return x, _report(rep, st)
 
 
+class Factor:
+    """A factored step-1 sketch (az_factorize): solve for new right-hand sides without redrawing,
+    re-factoring or re-decomposing the sketch."""
+
+    def __init__(self, plan: "Plan", theta: float, R: int, max_blocks: int = 1, stream=None):
+        self.plan = plan
+        h = C.c_void_p()
+        rep = _lib.SolveReport()
+        st = check("az_factorize", lib().az_factorize(plan._h, theta, R, max_blocks, C.byref(h), C.byref(rep),
+                                                       _stream(stream)),
+                   allow=(_lib.AZ_OK, _lib.AZ_WARN_SKETCH_SATURATED))
+        self._h = h
+        self.report = _report(rep, st)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().az_factor_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def workspace_bytes(self, nrhs: int) -> int:
+        b = C.c_size_t()
+        check("az_factor_workspace_size", lib().az_factor_workspace_size(self._h, nrhs, C.byref(b)))
+        return b.value
+
+    def solve(self, b, x=None, workspace=None, stream=None):
+        pb, ldb, nrhs = _mat(b)
+        if x is None:
+            x = empty_colmajor(self.plan.N, nrhs) if b.dim() == 2 else torch.empty(self.plan.N, dtype=torch.float64,
+                                                                                  device=b.device)
+        px, ldx, _ = _mat(x)
+        need = self.workspace_bytes(nrhs)
+        if workspace is None or workspace.numel() < need:
+            workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=b.device)
+        rep = _lib.SolveReport()
+        st = check("az_solve_factored", lib().az_solve_factored(self._h, C.c_void_p(pb), ldb, C.c_void_p(px), ldx, nrhs,
+                                                                C.c_void_p(workspace.data_ptr()), workspace.numel(),
+                                                                C.byref(rep), _stream(stream)))
+        return x, _report(rep, st)
+
+
 def _report(rep, status):
     return {"rank": rep.rank_used, "probes": rep.probes_used, "saturated": bool(rep.saturated),
             "sigma_first": rep.sigma_first, "sigma_last_kept": rep.sigma_last_kept,

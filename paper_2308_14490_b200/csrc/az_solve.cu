@@ -376,3 +376,295 @@ extern "C" az_status_t az_solve_host(az_plan_t p, const double* b_host, double* 
   AZ_CUDA_CHECK(cudaStreamSynchronize(st));
   return s;
 }
+
+// ==========================================================================================
+// Factorisation reuse across right-hand sides (the
+// step-1 matrix (A - A Z* A) Omega does not depend on b).  az_factorize draws and factors the
+// sketch once -- blocked Householder with the panels (V, T) kept in place, and the truncated
+// pseudo-inverse P = V_k Sigma_k^-1 U_k^T of R_S (the truncated SVD solve applied to c = I).
+// az_solve_factored then costs b' = (I - A Z*) b, Q^T b' (the stored panels), y = P (Q^T b')[:k],
+// x2 = Omega y and step 2 -- no sketch, no QR, no SVD.
+// ==========================================================================================
+struct az_factor_s {
+  az_plan_s* p = nullptr;
+  int64_t rows = 0, R = 0, kp = 0, kpmax = 0, rank = 0;
+  bool saturated = false;
+  double theta = 0.0, sigma_first = 0.0, sigma_last_kept = 0.0;
+  double* S = nullptr;     // rows x kpmax, factored in place
+  double* Tb = nullptr;    // panel T factors
+  double* P = nullptr;     // kp x kp (ld kpmax)
+  std::vector<int64_t> pj0;
+  std::vector<int> pnb;
+  int64_t np = 0;
+  double ms_sketch = 0, ms_qr = 0, ms_svd = 0;
+};
+
+__global__ void k_identity_cols(double* Rf, int64_t ld, int64_t k, int64_t col0) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= k * k) return;
+  const int64_t i = e % k, c = e / k;
+  Rf[(col0 + c) * ld + i] = (i == c) ? 1.0 : 0.0;
+}
+
+// y (k x nrhs) = P (k x k, ld ldp) c (k x nrhs, ld ldc); 64 x 64 output tiles, FP64 FMA
+__global__ void __launch_bounds__(256) k_gemm_nn(const double* P, int64_t ldp, const double* c, int64_t ldc, double* y,
+                                                 int64_t ldy, int64_t k, int64_t nrhs) {
+  __shared__ double As[16][65], Bs[16][65];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t r0 = (int64_t)blockIdx.x * 64, c0 = (int64_t)blockIdx.y * 64;
+  double acc[4][4] = {};
+  for (int64_t k0 = 0; k0 < k; k0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+      const int kk = e / 64, rr = e % 64;
+      As[kk][rr] = (r0 + rr < k && k0 + kk < k) ? P[(k0 + kk) * ldp + r0 + rr] : 0.0;
+      const int cc = e / 16, k2 = e % 16;
+      Bs[k2][cc] = (c0 + cc < nrhs && k0 + k2 < k) ? c[(c0 + cc) * ldc + k0 + k2] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk)
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) acc[a][bb] = fma(As[kk][tx + 16 * a], Bs[kk][ty + 16 * bb], acc[a][bb]);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb) {
+      const int64_t r = r0 + tx + 16 * a, cc = c0 + ty + 16 * bb;
+      if (r < k && cc < nrhs) y[cc * ldy + r] = acc[a][bb];
+    }
+}
+
+extern "C" az_status_t az_factorize(az_plan_t p, double theta, int64_t R, int32_t max_blocks, az_factor_t* out,
+                                    az_solve_report_t* report, void* stream) {
+  if (!p || !out || R < 1 || max_blocks < 1 || !(theta >= 0.0)) {
+    az_set_error("az_factorize: bad arguments");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  *out = nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  az_factor_s* f = new az_factor_s();
+  f->p = p;
+  f->rows = p->M + p->Mb;
+  f->R = R;
+  f->theta = theta;
+  max_blocks = (int32_t)std::min<int64_t>(max_blocks, std::max<int64_t>(1, f->rows / R));   // probes <= rows
+  f->kpmax = R * max_blocks;
+  const int64_t rows = f->rows, kpmax = f->kpmax;
+  if (kpmax > rows) {
+    delete f;
+    az_set_error("az_factorize: %lld probe columns exceed the %lld rows", (long long)kpmax, (long long)rows);
+    return AZ_ERR_NOT_SUPPORTED;
+  }
+  const int64_t QBw = az_qrw_panel_width();
+  const int64_t maxpanels = max_blocks * ((R + QBw - 1) / QBw);
+  f->pj0.resize(maxpanels);
+  f->pnb.resize(maxpanels);
+  const size_t qrbytes = az_qrw_ws_bytes(rows, R);
+  const size_t svdbytes = az_tsvd_ws_bytes(kpmax, kpmax);
+  double *Rf = nullptr, *sig = nullptr;
+  void *qrws = nullptr, *svdws = nullptr;
+  auto fail = [&](az_status_t s) {
+    cudaFree(Rf);
+    cudaFree(sig);
+    cudaFree(qrws);
+    cudaFree(svdws);
+    az_factor_destroy(f);
+    return s;
+  };
+  if (cudaMalloc(&f->S, sizeof(double) * rows * kpmax) != cudaSuccess ||
+      cudaMalloc(&f->Tb, sizeof(double) * maxpanels * QBw * QBw) != cudaSuccess ||
+      cudaMalloc(&f->P, sizeof(double) * kpmax * kpmax) != cudaSuccess ||
+      cudaMalloc(&Rf, sizeof(double) * kpmax * 2 * kpmax) != cudaSuccess ||
+      cudaMalloc(&sig, sizeof(double) * kpmax) != cudaSuccess || cudaMalloc(&qrws, qrbytes) != cudaSuccess ||
+      cudaMalloc(&svdws, svdbytes) != cudaSuccess) {
+    az_set_error("az_factorize: out of device memory");
+    return fail(AZ_ERR_OUT_OF_MEMORY);
+  }
+  const int pfix = 10;
+  double s1lo = 0.0;
+  int64_t nb = 0, rank = 0;
+  bool saturated = true;
+  Ev ev;
+  for (nb = 1; nb <= max_blocks; ++nb) {
+    const int64_t kp = nb * R;
+    cudaEventRecord(ev.e[2], st);
+    double* Snew = f->S + (nb - 1) * R * rows;
+    az_status_t s = az_sketch(p, (nb - 1) * R, R, Snew, rows, st);
+    if (s != AZ_OK) return fail(s);
+    cudaEventRecord(ev.e[3], st);
+    if ((s = az_qrw_apply(f->S, rows, rows, f->pj0.data(), f->pnb.data(), f->Tb, 0, f->np, Snew, rows, R, qrws, qrbytes, st)) != AZ_OK ||
+        (s = az_qrw_factor(f->S, rows, rows, (nb - 1) * R, kp, f->Tb, f->pj0.data(), f->pnb.data(), &f->np, qrws,
+                           qrbytes, st)) != AZ_OK ||
+        (s = az_qrw_extract_R(f->S, rows, kp, Rf, kpmax, st)) != AZ_OK)
+      return fail(s);
+    cudaEventRecord(ev.e[4], st);
+    bool full_svd = true;
+    if (nb >= 2 && nb < max_blocks) {   // the R22 pre-test of az_solve (reading R5)
+      const int64_t off = (nb - 1) * R;
+      int64_t k22 = 0;
+      if ((s = az_tsvd_impl(Rf + off * kpmax + off, kpmax, R, 0, 0.0, f->P, R, sig, &k22, svdws, svdbytes, st)) != AZ_OK)
+        return fail(s);
+      std::vector<double> s22(R);
+      if (cudaMemcpyAsync(s22.data(), sig, sizeof(double) * R, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+          cudaStreamSynchronize(st) != cudaSuccess)
+        return fail(AZ_ERR_CUDA);
+      s1lo = std::max(s1lo, s22[0]);
+      k22 = 0;
+      for (int64_t i = 0; i < R; ++i) k22 += s22[i] > theta * s1lo;
+      full_svd = k22 <= R - pfix;
+      rank = kp;
+    }
+    if (full_svd) {
+      // [R_S | I]: the truncated SVD solve of the identity is P = V_k Sigma_k^-1 U_k^T
+      k_identity_cols<<<az_div_up(kp * kp, 256), 256, 0, st>>>(Rf, kpmax, kp, kp);
+      if (cudaGetLastError() != cudaSuccess) return fail(AZ_ERR_CUDA);
+      if ((s = az_tsvd_impl(Rf, kpmax, kp, kp, theta, f->P, kpmax, sig, &rank, svdws, svdbytes, st)) != AZ_OK)
+        return fail(s);
+      double sv[2] = {0, 0};
+      cudaMemcpyAsync(&sv[0], sig, sizeof(double), cudaMemcpyDeviceToHost, st);
+      if (rank > 0) cudaMemcpyAsync(&sv[1], sig + rank - 1, sizeof(double), cudaMemcpyDeviceToHost, st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) return fail(AZ_ERR_CUDA);
+      s1lo = std::max(s1lo, sv[0]);
+      f->sigma_first = sv[0];
+      f->sigma_last_kept = sv[1];
+    }
+    cudaEventRecord(ev.e[5], st);
+    cudaEventSynchronize(ev.e[5]);
+    f->ms_sketch += ms_between(ev.e[2], ev.e[3]);
+    f->ms_qr += ms_between(ev.e[3], ev.e[4]);
+    f->ms_svd += ms_between(ev.e[4], ev.e[5]);
+    saturated = rank > kp - pfix;
+    if (!saturated || nb == max_blocks) break;
+  }
+  if (nb > max_blocks) nb = max_blocks;
+  f->kp = nb * R;
+  f->rank = rank;
+  f->saturated = saturated;
+  cudaFree(Rf);
+  cudaFree(sig);
+  cudaFree(qrws);
+  cudaFree(svdws);
+  if (report) {
+    memset(report, 0, sizeof(*report));
+    report->rank_used = f->rank;
+    report->probes_used = f->kp;
+    report->saturated = f->saturated ? 1 : 0;
+    report->sigma_first = f->sigma_first;
+    report->sigma_last_kept = f->sigma_last_kept;
+    report->ms_sketch = f->ms_sketch;
+    report->ms_qr = f->ms_qr;
+    report->ms_svd = f->ms_svd;
+    report->ms_total = f->ms_sketch + f->ms_qr + f->ms_svd;
+  }
+  *out = f;
+  return saturated ? AZ_WARN_SKETCH_SATURATED : AZ_OK;
+}
+
+extern "C" az_status_t az_factor_destroy(az_factor_t f) {
+  if (!f) return AZ_OK;
+  cudaFree(f->S);
+  cudaFree(f->Tb);
+  cudaFree(f->P);
+  delete f;
+  return AZ_OK;
+}
+
+extern "C" az_status_t az_factor_query(az_factor_t f, int64_t* probes, int64_t* rank) {
+  if (!f) return AZ_ERR_INVALID_ARGUMENT;
+  if (probes) *probes = f->kp;
+  if (rank) *rank = f->rank;
+  return AZ_OK;
+}
+
+struct FacWS {
+  double *bp, *y, *x2, *tmp;
+  void* qrws;
+  size_t qrbytes, total;
+};
+
+static FacWS fac_layout(az_factor_s* f, int64_t nrhs, char* base) {
+  FacWS w;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* ptr = base ? base + off : nullptr;
+    off += align256(bytes);
+    return ptr;
+  };
+  w.bp = (double*)take(sizeof(double) * f->rows * nrhs);
+  w.y = (double*)take(sizeof(double) * f->kp * nrhs);
+  w.x2 = (double*)take(sizeof(double) * f->p->N * nrhs);
+  w.tmp = (double*)take(sizeof(double) * f->rows * nrhs);
+  w.qrbytes = az_qrw_ws_bytes(f->rows, nrhs);
+  w.qrws = take(w.qrbytes);
+  w.total = off;
+  return w;
+}
+
+extern "C" az_status_t az_factor_workspace_size(az_factor_t f, int64_t nrhs, size_t* bytes) {
+  if (!f || !bytes || nrhs < 1) return AZ_ERR_INVALID_ARGUMENT;
+  *bytes = fac_layout(f, nrhs, nullptr).total;
+  return AZ_OK;
+}
+
+extern "C" az_status_t az_solve_factored(az_factor_t f, const double* b, int64_t ldb, double* x, int64_t ldx,
+                                         int64_t nrhs, void* workspace, size_t ws_bytes, az_solve_report_t* report,
+                                         void* stream) {
+  if (!f || !b || !x || nrhs < 1 || ldb < f->rows || ldx < f->p->N) {
+    az_set_error("az_solve_factored: bad arguments");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  FacWS w = fac_layout(f, nrhs, nullptr);
+  if (!workspace || ws_bytes < w.total) {
+    az_set_error("az_solve_factored: workspace too small (%zu < %zu)", ws_bytes, w.total);
+    return AZ_ERR_WORKSPACE;
+  }
+  w = fac_layout(f, nrhs, (char*)workspace);
+  az_plan_s* p = f->p;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t rows = f->rows, kp = f->kp;
+  Ev ev;
+  cudaEventRecord(ev.e[0], st);
+  AZ_TRY(az_apply_op(p, OP_RESID, b, ldb, w.bp, rows, nrhs, st));            // b' = (I - A Z*) b
+  cudaEventRecord(ev.e[1], st);
+  AZ_TRY(az_qrw_apply(f->S, rows, rows, f->pj0.data(), f->pnb.data(), f->Tb, 0, f->np, w.bp, rows, nrhs, w.qrws,
+                      w.qrbytes, st));                                          // Q^T b'
+  {
+    AzTrace tr("factored_y", st, 2 * kp * kp * nrhs);
+    k_gemm_nn<<<dim3(az_div_up(kp, 64), az_div_up(nrhs, 64)), 256, 0, st>>>(f->P, f->kpmax, w.bp, rows, w.y, kp, kp,
+                                                                          nrhs);   // y = P (Q^T b')[:kp]
+    AZ_LAUNCH_CHECK();
+  }
+  cudaEventRecord(ev.e[2], st);
+  AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, p->N, 0, st));
+  AZ_TRY(az_apply_op(p, OP_A, w.x2, p->N, w.tmp, rows, nrhs, st));
+  {
+    AzTrace tr("elementwise", st);
+    k_sub_cols<<<az_div_up(rows * nrhs, 256), 256, 0, st>>>(b, ldb, w.tmp, rows, rows, nrhs);
+  }
+  AZ_LAUNCH_CHECK();
+  AZ_TRY(az_apply_op(p, OP_ZSTAR, w.tmp, rows, x, ldx, nrhs, st));
+  {
+    AzTrace tr("elementwise", st);
+    k_add_cols<<<az_div_up(p->N * nrhs, 256), 256, 0, st>>>(w.x2, p->N, x, ldx, p->N, nrhs);
+  }
+  AZ_LAUNCH_CHECK();
+  cudaEventRecord(ev.e[3], st);
+  AZ_CUDA_CHECK(cudaEventSynchronize(ev.e[3]));
+  if (report) {
+    memset(report, 0, sizeof(*report));
+    report->rank_used = f->rank;
+    report->probes_used = kp;
+    report->saturated = f->saturated ? 1 : 0;
+    report->sigma_first = f->sigma_first;
+    report->sigma_last_kept = f->sigma_last_kept;
+    report->ms_rhs = ms_between(ev.e[0], ev.e[1]);
+    report->ms_qr = ms_between(ev.e[1], ev.e[2]);
+    report->ms_step2 = ms_between(ev.e[2], ev.e[3]);
+    report->ms_total = ms_between(ev.e[0], ev.e[3]);
+  }
+  return AZ_OK;
+}

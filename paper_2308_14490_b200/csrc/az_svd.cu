@@ -157,20 +157,21 @@ extern "C" int az_debug_small_sweeps() {
   return v;
 }
 
+// the single-CTA kernel holds R_S^T and c in shared memory; larger problems go to block Jacobi
+static bool small_fits(int64_t r, int64_t nrhs) {
+  return r <= AZ_NARROW_MAX && (size_t)(r * r + r * nrhs + r) * sizeof(double) <= 220 * 1024;
+}
+
 size_t az_tsvd_ws_bytes(int64_t r, int64_t nrhs) {
-  return r > AZ_NARROW_MAX ? az_tsvdw_ws_bytes(r, nrhs) : 256;
+  return small_fits(r, nrhs) ? 256 : az_tsvdw_ws_bytes(r, nrhs);
 }
 
 az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta, double* y,
                          int64_t ldy, double* sigma_out, int64_t* rank_out, void* ws, size_t ws_bytes,
                          cudaStream_t st) {
-  if (r > AZ_NARROW_MAX) return az_tsvdw_impl(Rf, ldr, r, nrhs, theta, y, ldy, sigma_out, rank_out, ws, ws_bytes, st, 40, nullptr);
+  if (!small_fits(r, nrhs))
+    return az_tsvdw_impl(Rf, ldr, r, nrhs, theta, y, ldy, sigma_out, rank_out, ws, ws_bytes, st, 40, nullptr);
   const size_t sm = (size_t)(r * r + r * nrhs + r) * sizeof(double);
-  if (sm > 220 * 1024) {
-    az_set_error("az_tsvd_solve: r = %lld, nrhs = %lld exceed the single-CTA Jacobi (multi-CTA path not built)",
-                 (long long)r, (long long)nrhs);
-    return AZ_ERR_NOT_SUPPORTED;
-  }
   if (ws_bytes < az_tsvd_ws_bytes(r, nrhs)) {
     az_set_error("az_tsvd_solve: workspace too small");
     return AZ_ERR_WORKSPACE;

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
   double* G = sm;                     // PW x GS
   double* V = G + PW * GS;            // PW x VS  (V[t][p] at t * VS + p)
   double* X = V + PW * VS;            // staging: Gram [col][k] (PW x GKS) / update [col][row] (PW x XS)
-  double* Cs = X + PW * XS;           // PW x nrhs (C rows of the pair)
+  double* Cs = X + PW * XS;           // 64 x XS: a 64-column tile of the pair's C rows ([col][k])
   __shared__ double rc[PW / 2], rs[PW / 2];
   __shared__ int rp[PW / 2], rq[PW / 2];
   __shared__ int any_rot;
@@ -292,22 +292,35 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
     }
   }
   if (dbg) a.dbg[5] = clock64();
-  // ---------------- c rows of the pair <- V^T c (leader) ----------------
-  if (crank == 0 && a.nrhs > 0) {
-    __syncthreads();
-    for (int e = tid; e < PW * a.nrhs; e += 256) {
-      const int k = e % PW, c = e / PW;
-      const int64_t row = bcol(k);
-      Cs[c * PW + k] = row >= 0 ? a.C[(int64_t)c * r + row] : 0.0;
-    }
-    __syncthreads();
-    for (int e = tid; e < PW * a.nrhs; e += 256) {
-      const int nn = e % PW, c = e / PW;
-      const int64_t row = bcol(nn);
-      if (row < 0) continue;
-      double t = 0.0;
-      for (int k = 0; k < PW; ++k) t = fma(V[k * VS + nn], Cs[c * PW + k], t);
-      a.C[(int64_t)c * r + row] = t;
+  // ---------------- c rows of the pair <- V^T c ----------------
+  // the cluster's CTAs split the right-hand-side columns; 64-column tiles on DMMA
+  // (A = V^T: m = new index, k = old index; B = the pair's rows of C, [col][k])
+  if (a.nrhs > 0) {
+    const int ntl = (a.nrhs + 63) / 64;
+    const int wm = w & 1, wn = w >> 1;       // warp tile 32 x 16
+    for (int tl = crank; tl < ntl; tl += CS) {
+      const int c0 = tl * 64;
+      __syncthreads();
+      for (int e = tid; e < 64 * PW; e += 256) {
+        const int kk = e % PW, cc = e / PW;
+        const int64_t row = bcol(kk);
+        Cs[cc * XS + kk] = (row >= 0 && c0 + cc < a.nrhs) ? a.C[(int64_t)(c0 + cc) * r + row] : 0.0;
+      }
+      __syncthreads();
+      double acc[4][2][2];
+      acc_zero(acc);
+      warp_mma<4, 2, KMAJ, IMAJ>(acc, V, VS, Cs, XS, wm * 32, wn * 16, 0, PW, lane);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int nn = acc_row(wm * 32, i, lane);
+            const int cc = acc_col(wn * 16, j, e, lane);
+            const int64_t row = bcol(nn);
+            if (row >= 0 && c0 + cc < a.nrhs) a.C[(int64_t)(c0 + cc) * r + row] = acc[i][j][e];
+          }
     }
   }
 }
@@ -450,11 +463,7 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
   }
   const int nblk = (int)((r + BW - 1) / BW);
   const int n = nblk + (nblk & 1);
-  const size_t smem = (size_t)(PW * GS + PW * VS + PW * XS + PW * std::max<int64_t>(nrhs, 1)) * sizeof(double);
-  if (smem > 227 * 1024) {
-    az_set_error("az_tsvd_solve: nrhs = %lld too large for the block Jacobi kernel", (long long)nrhs);
-    return AZ_ERR_NOT_SUPPORTED;
-  }
+  const size_t smem = (size_t)(PW * GS + PW * VS + PW * XS + 64 * XS) * sizeof(double);
   AZ_CUDA_CHECK(az_smem_attr(k_bjac_round, smem));
   // cluster size: enough CTAs per round to cover the SMs twice, each slice >= 256 rows
   int CS = 1;

@@ -138,3 +138,37 @@ def test_solve_2d_full_size(name):
     prob = OA.make_problem(cfg, "fft")
     res = OA.relative_residual(prob, x, b)
     assert np.all(res <= 1e-8), res
+
+
+FACTOR_CASES = [("c1", I.get_config("c1"), 4), ("interval_n4096_4step", I.make_config("interval", 4096, nrhs=6, R=40), 4),
+                ("disk_n32", I.make_config("disk", 32), 8), ("star_n32", I.make_config("star", 32), 8)]
+
+
+@pytest.mark.parametrize("name,cfg,max_blocks", FACTOR_CASES, ids=[c[0] for c in FACTOR_CASES])
+def test_factorize_and_solve_factored_matches_solve(name, cfg, max_blocks):
+    """Factorisation reuse: one az_factorize, then az_solve_factored for the
+    config's right-hand sides and for a second, different set -- each against a full az_solve /
+    the oracle (approximant parity; coefficients are not unique)."""
+    from paper_2308_14490_b200.api import Factor, Plan
+    plan = Plan.from_config(cfg)
+    theta = max(cfg.tol * 1e-2, 1e-12)
+    fac = Factor(plan, theta, cfg.R, max_blocks)
+    assert not fac.report["saturated"]
+    grid = I.test_grid(cfg)
+    b = I.rhs(cfg)
+    xf, _ = fac.solve(_dev(b))
+    xs, rep = plan.solve(_dev(b), theta, cfg.R, max_blocks)
+    assert fac.report["probes"] == rep["probes"] or cfg.dim == 2   # 2-D: noise-determined (reading R24)
+    err = _approx_err(cfg, _host(xf), _host(xs), grid)
+    assert np.all(err <= 1e-9), err
+    # a second right-hand side on the same factor: a different smooth function, vs the oracle O1
+    if cfg.N <= 1024:
+        rng = np.random.default_rng(1)
+        A = OD.assemble_A(cfg)
+        coef = rng.standard_normal((cfg.N, 2)) * np.exp(-0.05 * np.arange(cfg.N))[:, None]
+        b2 = A @ coef                                   # exactly representable data
+        x2, _ = fac.solve(_dev(b2))
+        res = np.linalg.norm(A @ _host(x2) - b2, axis=0) / np.linalg.norm(b2, axis=0)
+        xo, _, _ = OA.tsvd_lsq(A, b2, cfg.tol)
+        ro = np.linalg.norm(A @ xo - b2, axis=0) / np.linalg.norm(b2, axis=0)
+        assert np.all(res <= np.maximum(2 * ro, 1e-10)), (res, ro)

@@ -36,6 +36,15 @@ api.trace_enable(False)
 x = x.cpu().numpy()
 out = {"config": name, "plan_s": t1 - t0, "solve_s": t2 - t1, "report": rep,
        "kernels_ms": {k: round(v[1], 3) for k, v in sorted(tr.items(), key=lambda kv: -kv[1][1])[:14]}}
+if "--factored" in sys.argv:
+    torch.cuda.synchronize(); t3 = time.time()
+    fac = api.Factor(plan, theta, cfg.R, mb)
+    torch.cuda.synchronize(); t4 = time.time()
+    xf, _ = fac.solve(bd)
+    torch.cuda.synchronize(); t5 = time.time()
+    xf, _ = fac.solve(bd)
+    torch.cuda.synchronize(); t6 = time.time()
+    out["factored"] = {"factorize_s": t4 - t3, "first_solve_s": t5 - t4, "solve_s": t6 - t5, "report": fac.report}
 if "--check" in sys.argv:
     from oracle import az as OA
     grid = I.test_grid(cfg, 201)
