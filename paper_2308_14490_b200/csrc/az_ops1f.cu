@@ -43,6 +43,8 @@ struct P1f {
   cplx* G;
   const double* in;
   int64_t ldin;
+  const double* in2;     // second input (the right-hand sides b of the fused step-2 chain)
+  int64_t ldin2;
   double* out;
   int64_t ldout;
   int64_t nvec, col0, pair0;
@@ -81,7 +83,10 @@ AZ_D Cols1 pcols(const P1f& a, int b) {
 // 32 / TC rows per access.
 // ------------------------------------------------------------------------------------------
 enum { FC_IN_COEF = 0, FC_FINE_MASK = 1, FC_OUT_GATHER = 2, FC_OUT_RESID = 3, FC_IN_ROWS = 4, FC_OUT_COEF = 5,
-       FC_FWD_G = 6 };
+       FC_FWD_G = 6, FC_RESID_MID = 7, FC_OUT_COEF_ADD = 8 };
+// FC_RESID_MID: IFFT_N1 -> r = b - (A x) on Omega, 0 outside -> FFT_N1 -> twiddle  (the A -> b - A x ->
+//               Z* junction of step 2 in one pass, no row vector written or read)
+// FC_OUT_COEF_ADD: IFFT_N1 -> x = x2 + (.) / n  (the closing addition of step 2)
 
 // EC = values per thread in the column FFTs (16: fewer exchanges; 8: half the registers, more
 // resident warps); MINB = CTAs per SM the register budget is sized for.
@@ -94,7 +99,7 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
   const int c0 = blockIdx.x * TC;
   const int col = c0 + c;
   const Cols1 cc = pcols(a, b);
-  const bool coef = (KIND == FC_IN_COEF || KIND == FC_OUT_COEF);
+  const bool coef = (KIND == FC_IN_COEF || KIND == FC_OUT_COEF || KIND == FC_OUT_COEF_ADD);
   const int W = coef ? a.N2 : a.L2;                    // row length of the matrix
   cplx* C1b = a.C1 + (int64_t)b * a.n;
   cplx* Gb = a.G + (int64_t)b * a.L;
@@ -147,6 +152,16 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
   // ---- transforms ----
   if constexpr (KIND == FC_IN_COEF || KIND == FC_IN_ROWS || KIND == FC_FWD_G) {
     fftr::fft<NC, EC, -1>(v, j, buf, a.tw, TWN);
+  } else if constexpr (KIND == FC_RESID_MID) {
+    fftr::fft<NC, EC, 1>(v, j, buf, a.tw, TWN);
+#pragma unroll
+    for (int e = 0; e < EC; ++e) {
+      const int r = row_of(a, (int64_t)(j + e * T) * W + col);
+      v[e] = r >= 0 ? make_double2(a.in2[r + cc.cre * a.ldin2] - v[e].x,
+                                   cc.has_im ? a.in2[r + cc.cim * a.ldin2] - v[e].y : 0.0)
+                    : czero();
+    }
+    fftr::fft<NC, EC, -1>(v, j, buf, a.tw, TWN);
   } else if constexpr (KIND == FC_FINE_MASK) {
     fftr::fft<NC, EC, 1>(v, j, buf, a.tw, TWN);
 #pragma unroll
@@ -158,7 +173,8 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
   }
 
   // ---- store ----
-  if constexpr (KIND == FC_IN_COEF || KIND == FC_IN_ROWS || KIND == FC_FINE_MASK || KIND == FC_FWD_G) {
+  if constexpr (KIND == FC_IN_COEF || KIND == FC_IN_ROWS || KIND == FC_FINE_MASK || KIND == FC_FWD_G ||
+                KIND == FC_RESID_MID) {
     cplx* dst = (KIND == FC_IN_COEF) ? C1b : Gb;
     // twiddle e^{-2 pi i k1 col tmul / L} for k1 = j + e T by recurrence in e (<= EC - 1 products)
     cplx w = tw4<-1>(a, ((int64_t)j * col * tmul) & (a.L - 1));
@@ -182,6 +198,13 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
           if (cc.has_im) a.out[r + cc.cim * a.ldout] = v[e].y;
         }
       }
+    }
+  } else if constexpr (KIND == FC_OUT_COEF_ADD) {
+#pragma unroll
+    for (int e = 0; e < EC; ++e) {
+      const int64_t i = (int64_t)(j + e * T) * W + col;
+      a.out[i + cc.cre * a.ldout] = fma(v[e].x, cout, a.in[i + cc.cre * a.ldin]);
+      if (cc.has_im) a.out[i + cc.cim * a.ldout] = fma(v[e].y, cout, a.in[i + cc.cim * a.ldin]);
     }
   } else {   // FC_OUT_COEF
 #pragma unroll
@@ -315,7 +338,8 @@ static az_status_t fcols_e(const P1f& a, int ncols, int nb, double cout, cudaStr
   auto kern = k1f_cols<NC, TC, KIND, SRC, EC, MINB>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   static const char* names[] = {"1f_cols_in_coef", "1f_cols_fine_mask", "1f_cols_out_gather", "1f_cols_out_resid",
-                                "1f_cols_in_rows", "1f_cols_out_coef", "1f_cols_fwd"};
+                                "1f_cols_in_rows", "1f_cols_out_coef", "1f_cols_fwd", "1f_cols_resid_mid",
+                                "1f_cols_out_coef_add"};
   AzTrace tr(names[KIND], st, nb);
   kern<<<dim3(az_div_up(ncols, TC), nb), TC * T, sm, st>>>(a, cout);
   AZ_LAUNCH_CHECK();
@@ -385,6 +409,13 @@ static az_status_t run1f(const P1f& a0, int op, int src, int64_t npairs, int64_t
         AZ_TRY(frows<NR2, FR_ZSTAR>(a, nb, st));
         AZ_TRY(fcols<NC, FC_OUT_COEF, SRC_VEC>(a, N2, nb, 1.0 / (double)a.n, st));
         break;
+      case OP_STEP2:   // x = x2 + Z* (b - A x2): in = x2, in2 = b, out = x
+        AZ_TRY(fcols<NC, FC_IN_COEF, SRC_VEC>(a, N2, nb, 1.0, st));
+        AZ_TRY(frows<NR2, FR_EXPAND>(a, nb, st));
+        AZ_TRY(fcols<NC, FC_RESID_MID, SRC_VEC>(a, L2, nb, 1.0, st));
+        AZ_TRY(frows<NR2, FR_ZSTAR>(a, nb, st));
+        AZ_TRY(fcols<NC, FC_OUT_COEF_ADD, SRC_VEC>(a, N2, nb, 1.0 / (double)a.n, st));
+        break;
       case OP_AT:
         AZ_TRY(fcols<NC, FC_IN_ROWS, SRC_VEC>(a, L2, nb, 1.0, st));
         AZ_TRY(frows<NR2, FR_AT>(a, nb, st));
@@ -421,6 +452,8 @@ static P1f make_p1f(az_plan_s* p) {
   a.C1 = p->d_C1;
   a.G = p->d_G;
   a.in = nullptr;
+  a.in2 = nullptr;
+  a.ldin2 = 0;
   a.out = nullptr;
   a.ldin = a.ldout = 0;
   a.nvec = a.col0 = a.pair0 = 0;
@@ -482,4 +515,21 @@ static az_status_t fine_forward(az_plan_s* p, cplx* W, cudaStream_t st) {
 
 az_status_t az1f_fft_fine_forward(az_plan_s* p, cplx* W, cudaStream_t st) {
   AZ_1F_DISPATCH(fine_forward, p, W, st)
+}
+
+// Step 2 of Alg. 1 for the four-step layout in five passes:
+//   x = x2 + Z* (b - A x2)
+az_status_t az1f_step2(az_plan_s* p, const double* x2, int64_t ldx2, const double* b, int64_t ldb, double* x,
+                       int64_t ldx, int64_t nvec, cudaStream_t st) {
+  P1f a = make_p1f(p);
+  a.in = x2;
+  a.ldin = ldx2;
+  a.in2 = b;
+  a.ldin2 = ldb;
+  a.out = x;
+  a.ldout = ldx;
+  a.nvec = nvec;
+  a.col0 = 0;
+  const int64_t npairs = (nvec + 1) / 2;
+  AZ_1F_DISPATCH(run1f, a, OP_STEP2, SRC_VEC, npairs, p->Bmax, st)
 }

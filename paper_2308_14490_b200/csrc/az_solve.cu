@@ -209,6 +209,27 @@ static double ms_between(cudaEvent_t a, cudaEvent_t b) {
 az_status_t az_apply_op(az_plan_s* p, int op, const double* in, int64_t ldin, double* out, int64_t ldout,
                         int64_t nvec, cudaStream_t st);
 
+// Step 2 + 3 of Alg. 1: x = x2 + Z* (b - A x2).  Four-step layout: one fused
+// five-pass chain (az1f_step2); otherwise A, b - A x2, Z*, + x2.  tmp: (M + Mb) x nrhs scratch.
+static az_status_t step2(az_plan_s* p, const double* x2, const double* b, int64_t ldb, double* x, int64_t ldx,
+                         double* tmp, int64_t nrhs, cudaStream_t st) {
+  if (p->layout == AZ_LAYOUT_1D_FOURSTEP) return az1f_step2(p, x2, p->N, b, ldb, x, ldx, nrhs, st);
+  const int64_t rows = p->M + p->Mb;
+  AZ_TRY(az_apply_op(p, OP_A, x2, p->N, tmp, rows, nrhs, st));
+  {
+    AzTrace tr("elementwise", st);
+    k_sub_cols<<<az_div_up(rows * nrhs, 256), 256, 0, st>>>(b, ldb, tmp, rows, rows, nrhs);
+  }
+  AZ_LAUNCH_CHECK();
+  AZ_TRY(az_apply_op(p, OP_ZSTAR, tmp, rows, x, ldx, nrhs, st));
+  {
+    AzTrace tr("elementwise", st);
+    k_add_cols<<<az_div_up(p->N * nrhs, 256), 256, 0, st>>>(x2, p->N, x, ldx, p->N, nrhs);
+  }
+  AZ_LAUNCH_CHECK();
+  return AZ_OK;
+}
+
 extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, double* x, int64_t ldx, int64_t nrhs,
                                 double theta, int64_t R, int32_t max_blocks, void* workspace, size_t ws_bytes,
                                 az_solve_report_t* report, void* stream) {
@@ -227,8 +248,9 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   const int pfix = 10;
   Ev ev;
   cudaEventRecord(ev.e[0], st);
-  // ---- right-hand side b' = (I - A Z*) b ----
-  AZ_TRY(az_apply_op(p, OP_RESID, b, ldb, w.bp, rows, nrhs, st));
+  // ---- right-hand side b' = (I - A Z*) b (narrow single-block solve: straight into S) ----
+  const bool bp_in_S = !w.wide && max_blocks == 1;
+  AZ_TRY(az_apply_op(p, OP_RESID, b, ldb, bp_in_S ? w.S + R * rows : w.bp, rows, nrhs, st));
   cudaEventRecord(ev.e[1], st);
   double ms_sketch = 0, ms_qr = 0, ms_svd = 0;
   int64_t rank = 0, nb = 0;
@@ -245,7 +267,7 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
     cudaEvent_t e0 = ev.e[2], e1 = ev.e[3], e2 = ev.e[4], e3 = ev.e[5];
     cudaEventRecord(e0, st);
     AZ_TRY(az_sketch(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, st));
-    if (!w.wide) {
+    if (!w.wide && !bp_in_S) {
       AzTrace tr("elementwise", st);
       k_copy_cols<<<az_div_up(rows * nrhs, 256), 256, 0, st>>>(w.bp, rows, w.S + kp * rows, rows, rows, nrhs);
       AZ_LAUNCH_CHECK();
@@ -309,18 +331,7 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   cudaEventRecord(ev.e[6], st);
   // ---- x2 = Omega y ; x = x2 + Z* (b - A x2) ----
   AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, p->N, 0, st));
-  AZ_TRY(az_apply_op(p, OP_A, w.x2, p->N, w.tmp, rows, nrhs, st));
-  {
-    AzTrace tr("elementwise", st);
-    k_sub_cols<<<az_div_up(rows * nrhs, 256), 256, 0, st>>>(b, ldb, w.tmp, rows, rows, nrhs);
-  }
-  AZ_LAUNCH_CHECK();
-  AZ_TRY(az_apply_op(p, OP_ZSTAR, w.tmp, rows, x, ldx, nrhs, st));
-  {
-    AzTrace tr("elementwise", st);
-    k_add_cols<<<az_div_up(p->N * nrhs, 256), 256, 0, st>>>(w.x2, p->N, x, ldx, p->N, nrhs);
-  }
-  AZ_LAUNCH_CHECK();
+  AZ_TRY(step2(p, w.x2, b, ldb, x, ldx, w.tmp, nrhs, st));
   cudaEventRecord(ev.e[7], st);
   AZ_CUDA_CHECK(cudaEventSynchronize(ev.e[7]));
   if (report) {
@@ -640,18 +651,7 @@ extern "C" az_status_t az_solve_factored(az_factor_t f, const double* b, int64_t
   }
   cudaEventRecord(ev.e[2], st);
   AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, p->N, 0, st));
-  AZ_TRY(az_apply_op(p, OP_A, w.x2, p->N, w.tmp, rows, nrhs, st));
-  {
-    AzTrace tr("elementwise", st);
-    k_sub_cols<<<az_div_up(rows * nrhs, 256), 256, 0, st>>>(b, ldb, w.tmp, rows, rows, nrhs);
-  }
-  AZ_LAUNCH_CHECK();
-  AZ_TRY(az_apply_op(p, OP_ZSTAR, w.tmp, rows, x, ldx, nrhs, st));
-  {
-    AzTrace tr("elementwise", st);
-    k_add_cols<<<az_div_up(p->N * nrhs, 256), 256, 0, st>>>(w.x2, p->N, x, ldx, p->N, nrhs);
-  }
-  AZ_LAUNCH_CHECK();
+  AZ_TRY(step2(p, w.x2, b, ldb, x, ldx, w.tmp, nrhs, st));
   cudaEventRecord(ev.e[3], st);
   AZ_CUDA_CHECK(cudaEventSynchronize(ev.e[3]));
   if (report) {
