@@ -75,6 +75,8 @@ typedef struct {
   double boundary_weight;      /* beta: boundary rows are beta * phi_j(x_b) */
   double zstar_rcond;          /* Z* keeps modes with sigma(k) > rcond * max sigma (reading R3) */
   uint64_t seed;               /* Philox key of the probe matrix Omega */
+  double k0sq;                 /* Helmholtz term: LAPLACIAN rows are alpha (Delta + k0^2) phi_j
+                                  (PAPER.md:694-722 1-D ODE, 730-806 2-D; 0 = Poisson).  Ignored for VALUE. */
 } az_plan_desc_t;
 
 typedef struct {

@@ -66,7 +66,7 @@ def make_problem(cfg: I.Config, backend: str = "fft", dense_A: Optional[np.ndarr
     M = int(msk.sum())
     Mb = cfg.n_boundary
     N = cfg.N
-    sym = C.Symbol(cfg.dim, cfg.n, cfg.s, cfg.eps, cfg.T, cfg.row_op, alpha=cfg.row_scale,
+    sym = C.Symbol(cfg.dim, cfg.n, cfg.s, cfg.eps, cfg.T, cfg.row_op, alpha=cfg.row_scale, k0sq=cfg.k0sq,
                    backend="ld" if backend == "dense" else "fft")
     ops = C.PeriodicOperators(sym, cfg.tol)
     Ab = None

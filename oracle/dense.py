@@ -25,14 +25,15 @@ def assemble_rows(cfg: I.Config, pts: np.ndarray, kind: str) -> np.ndarray:
     """Rows of A at `pts` (1-D: (m,), 2-D: (m, 2)).
 
     kind "value":     phi_j(x)                                      (PAPER.md:136, 558-565)
-    kind "laplacian": alpha (phi_jx'' phi_jy + phi_jx phi_jy'')     (k0^2 = 0)
+    kind "laplacian": alpha (phi_jx'' phi_jy + phi_jx phi_jy'' + k0^2 phi_jx phi_jy)
+                      1-D: alpha (phi_j'' + k0^2 phi_j)
     """
     c = I.center_axis(cfg)
     eps, T = cfg.eps, cfg.T
     if cfg.dim == 1:
         if kind == "value":
             return _Phi(pts, c, eps, T, 0)
-        return cfg.row_scale * _Phi(pts, c, eps, T, 2)
+        return cfg.row_scale * (_Phi(pts, c, eps, T, 2) + cfg.k0sq * _Phi(pts, c, eps, T, 0))
     X0 = _Phi(pts[:, 0], c, eps, T, 0)
     Y0 = _Phi(pts[:, 1], c, eps, T, 0)
     if kind == "value":
@@ -41,6 +42,8 @@ def assemble_rows(cfg: I.Config, pts: np.ndarray, kind: str) -> np.ndarray:
     X2 = _Phi(pts[:, 0], c, eps, T, 2)
     Y2 = _Phi(pts[:, 1], c, eps, T, 2)
     L = X2[:, :, None] * Y0[:, None, :] + X0[:, :, None] * Y2[:, None, :]
+    if cfg.k0sq:
+        L = L + cfg.k0sq * (X0[:, :, None] * Y0[:, None, :])
     return cfg.row_scale * L.reshape(pts.shape[0], -1)
 
 
@@ -87,7 +90,7 @@ def A_row_entries(cfg: I.Config, i_grid, half_width: int = 40):
         js = np.unique(js)
         vals = periodized(g[q] - c[js], cfg.eps, cfg.T, kind)
         if kind:
-            vals = cfg.row_scale * vals
+            vals = cfg.row_scale * (vals + cfg.k0sq * periodized(g[q] - c[js], cfg.eps, cfg.T, 0))
         return js, vals
     qx, qy = i_grid
     jx = np.unique(np.arange(qx // s - half_width, qx // s + half_width + 1) % n)
@@ -97,7 +100,8 @@ def A_row_entries(cfg: I.Config, i_grid, half_width: int = 40):
     if kind:
         x2 = periodized(g[qx] - c[jx], cfg.eps, cfg.T, 2)
         y2 = periodized(g[qy] - c[jy], cfg.eps, cfg.T, 2)
-        V = cfg.row_scale * (x2[:, None] * y0[None, :] + x0[:, None] * y2[None, :])
+        V = cfg.row_scale * (x2[:, None] * y0[None, :] + x0[:, None] * y2[None, :]
+                             + cfg.k0sq * x0[:, None] * y0[None, :])
     else:
         V = x0[:, None] * y0[None, :]
     cols = (jx[:, None] * n + jy[None, :]).ravel()

@@ -51,13 +51,15 @@ class Plan:
 
     def __init__(self, *, dim: int, n: int, L: int, T: float, eps: float, op: int = 0,
                  row_scale: float = 1.0, mask: np.ndarray, boundary_xy: Optional[np.ndarray] = None,
-                 boundary_weight: float = 0.0, zstar_rcond: float = 1e-10, seed: int = 0, stream=None):
+                 boundary_weight: float = 0.0, zstar_rcond: float = 1e-10, seed: int = 0, k0sq: float = 0.0,
+                 stream=None):
         self._mask = np.ascontiguousarray(mask, dtype=np.uint8)
         bxy = np.zeros((0, 2)) if boundary_xy is None else boundary_xy
         self._bxy = np.ascontiguousarray(bxy, dtype=np.float64)
         d = _lib.PlanDesc()
         d.dim, d.n, d.L, d.T, d.eps = dim, n, L, T, eps
         d.op, d.row_scale = op, row_scale
+        d.k0sq = k0sq
         d.mask = self._mask.ctypes.data
         d.n_boundary = self._bxy.shape[0]
         d.boundary_xy = self._bxy.ctypes.data if self._bxy.shape[0] else None
@@ -81,7 +83,8 @@ class Plan:
         return cls(dim=cfg.dim, n=cfg.n, L=cfg.s, T=cfg.T, eps=cfg.eps, op=cfg.row_op,
                    row_scale=cfg.row_scale, mask=I.mask(cfg).reshape(-1),
                    boundary_xy=I.boundary_points(cfg) if cfg.n_boundary else None,
-                   boundary_weight=cfg.boundary_weight, zstar_rcond=cfg.tol, seed=cfg.seed, stream=stream)
+                   boundary_weight=cfg.boundary_weight, zstar_rcond=cfg.tol, seed=cfg.seed,
+                   k0sq=getattr(cfg, "k0sq", 0.0), stream=stream)
 
     def close(self):
         if getattr(self, "_h", None):

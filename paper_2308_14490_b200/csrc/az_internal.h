@@ -26,6 +26,7 @@ struct az_plan_s {
   int64_t N, G;             // n^dim, L^dim
   int64_t M, Mb;
   double T, eps, alpha, beta, rcond;
+  double k0sq = 0.0;            // Helmholtz term of LAPLACIAN rows
   uint64_t seed;
   int op;
   int layout;

@@ -21,6 +21,7 @@ struct P1s {
   const int32_t* pos;
   const cplx* tw;
   int lap;
+  double k0sq;
   double alpha;
   int n, s;
   uint64_t seed;
@@ -32,7 +33,9 @@ struct P1s {
   int64_t col0;
 };
 
-AZ_D cplx sym1(const P1s& a, int kf) { return a.lap ? cscale(a.W2[kf], a.alpha) : a.W0[kf]; }
+AZ_D cplx sym1(const P1s& a, int kf) {
+  return a.lap ? cscale(cadd(a.W2[kf], cscale(a.W0[kf], a.k0sq)), a.alpha) : a.W0[kf];
+}
 
 template <int L, int OP, int SRC>
 __global__ void __launch_bounds__(L / 8) k_chain1s(P1s a) {
@@ -173,6 +176,7 @@ az_status_t az1s_apply(az_plan_s* p, int op, int src, const double* in, int64_t 
   a.pos = p->d_pos;
   a.tw = p->d_tw;
   a.lap = p->op == AZ_ROW_LAPLACIAN;
+  a.k0sq = p->k0sq;
   a.alpha = p->alpha;
   a.n = (int)p->n;
   a.s = (int)p->s;

@@ -34,6 +34,7 @@ struct P2 {
   const double* bw;
   const int32_t* bj;
   int lap;
+  double k0sq;
   double alpha, beta, eps, T, h;
   int n, s, L;
   int64_t M, Mb, N, GG;
@@ -50,9 +51,11 @@ struct P2 {
   int win;        // boundary window half-width (centres per axis)
 };
 
+// alpha (W2x W0y + W0x W2y + k0^2 W0x W0y) for LAPLACIAN / Helmholtz rows
 AZ_D cplx sym2(const P2& a, int kx, int ky) {
   if (!a.lap) return cmul(a.W0[kx], a.W0[ky]);
-  return cscale(cadd(cmul(a.W2[kx], a.W0[ky]), cmul(a.W0[kx], a.W2[ky])), a.alpha);
+  const cplx w00 = cmul(a.W0[kx], a.W0[ky]);
+  return cscale(cadd(cadd(cmul(a.W2[kx], a.W0[ky]), cmul(a.W0[kx], a.W2[ky])), cscale(w00, a.k0sq)), a.alpha);
 }
 
 struct Cols {
@@ -461,6 +464,7 @@ az_status_t az2_apply(az_plan_s* p, int op, int src, const double* in, int64_t l
   a.bw = p->d_bw;
   a.bj = p->d_bj;
   a.lap = p->op == AZ_ROW_LAPLACIAN;
+  a.k0sq = p->k0sq;
   a.alpha = p->alpha;
   a.beta = p->beta;
   a.eps = p->eps;

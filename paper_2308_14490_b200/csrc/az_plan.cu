@@ -206,9 +206,9 @@ __global__ void k_twiddles(cplx* tw, int twn, cplx* hi, cplx* lo, int64_t Lbig, 
 // Lemma 3 on the fine grid: w[q] = phi^per(q h_L) (order 0 or 2), q in [0, L).
 // real part of the row symbol (the imaginary part of the DFT of the real even kernel samples is
 // rounding noise)
-__global__ void k_real_sym(double* Wr, const cplx* W0, const cplx* W2, int lap, double alpha, int64_t L) {
+__global__ void k_real_sym(double* Wr, const cplx* W0, const cplx* W2, int lap, double alpha, double k0sq, int64_t L) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < L) Wr[i] = lap ? alpha * W2[i].x : W0[i].x;
+  if (i < L) Wr[i] = lap ? alpha * fma(k0sq, W0[i].x, W2[i].x) : W0[i].x;
 }
 
 __global__ void k_samples(cplx* out, int64_t L, double hL, double eps, double T, int order) {
@@ -241,14 +241,18 @@ struct SymArgs {
   const cplx* W2;
   int lap;
   double alpha;
+  double k0sq;
 };
 
+// row symbols: VALUE rows W0; LAPLACIAN rows alpha (W2 + k0^2 W0) in 1-D and
+// alpha (W2x W0y + W0x W2y + k0^2 W0x W0y) in 2-D
 AZ_D cplx sym_1d(const SymArgs& a, int64_t kf) {
-  return a.lap ? cscale(a.W2[kf], a.alpha) : a.W0[kf];
+  return a.lap ? cscale(cadd(a.W2[kf], cscale(a.W0[kf], a.k0sq)), a.alpha) : a.W0[kf];
 }
 AZ_D cplx sym_2d(const SymArgs& a, int64_t kx, int64_t ky) {
   if (!a.lap) return cmul(a.W0[kx], a.W0[ky]);
-  return cscale(cadd(cmul(a.W2[kx], a.W0[ky]), cmul(a.W0[kx], a.W2[ky])), a.alpha);
+  const cplx w00 = cmul(a.W0[kx], a.W0[ky]);
+  return cscale(cadd(cadd(cmul(a.W2[kx], a.W0[ky]), cmul(a.W0[kx], a.W2[ky])), cscale(w00, a.k0sq)), a.alpha);
 }
 
 AZ_D void atomic_max_pos(double* addr, double v) {   // v >= 0
@@ -427,7 +431,7 @@ static az_status_t plan_build(az_plan_s* p, const az_plan_desc_t* d, cudaStream_
   }
   if (p->layout == AZ_LAYOUT_1D_FOURSTEP) {
     AZ_TRY(dalloc(&p->d_Wr, p->L));
-    k_real_sym<<<az_div_up(p->L, 256), 256, 0, st>>>(p->d_Wr, p->d_W0, p->d_W2, lap, p->alpha, p->L);
+    k_real_sym<<<az_div_up(p->L, 256), 256, 0, st>>>(p->d_Wr, p->d_W0, p->d_W2, lap, p->alpha, p->k0sq, p->L);
     AZ_LAUNCH_CHECK();
   }
   // ---- sigma^2, max, thresholded inverse ----
@@ -440,7 +444,7 @@ static az_status_t plan_build(az_plan_s* p, const az_plan_desc_t* d, cudaStream_
   unsigned long long z = 0;
   memcpy(&init[2], &z, sizeof(z));
   AZ_CUDA_CHECK(cudaMemcpyAsync(d_red, init, sizeof(init), cudaMemcpyHostToDevice, st));
-  SymArgs a{p->d_W0, p->d_W2, lap, p->alpha};
+  SymArgs a{p->d_W0, p->d_W2, lap, p->alpha, p->k0sq};
   k_sigma2<<<az_div_up(p->N, 256), 256, 0, st>>>(d_sig2, d_red, a, p->layout, p->n, p->s, p->N1, p->N2, p->L2);
   AZ_LAUNCH_CHECK();
   k_zinv<<<az_div_up(p->N, 256), 256, 0, st>>>(p->d_zinv, d_sig2, p->N, d_red, p->rcond,
@@ -498,6 +502,7 @@ extern "C" az_status_t az_plan_create(const az_plan_desc_t* d, void* stream, az_
   p->T = d->T;
   p->eps = d->eps;
   p->alpha = d->op == AZ_ROW_LAPLACIAN ? d->row_scale : 1.0;
+  p->k0sq = d->op == AZ_ROW_LAPLACIAN ? d->k0sq : 0.0;
   p->beta = d->boundary_weight;
   p->rcond = d->zstar_rcond;
   p->seed = d->seed;

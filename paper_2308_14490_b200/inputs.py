@@ -55,6 +55,7 @@ class Config:
     boundary_weight: float = 0.0   # beta (config 4: 10)
     n_boundary: int = 0            # M_b
     T: float = 1.0
+    k0sq: float = 0.0              # Helmholtz term of the LAPLACIAN rows (0 = Poisson)
 
     @property
     def h(self) -> float:
@@ -106,6 +107,13 @@ def make_config(family: str, n: int, *, nrhs: int = 1, R: Optional[int] = None,
         return Config(name or f"star_n{n}", 2, n, s, "star", ROW_LAPLACIAN, nrhs,
                       R if R is not None else 8 * n, seed, 1e-10,
                       boundary_weight=10.0, n_boundary=4 * n)
+    if family == "helm":
+        # 2-D Helmholtz Delta u + k0^2 u = f on the star domain,
+        # the c4 geometry and weights with k0^2 = 25 (k0 = 5: k0^2 is not an eigenvalue of the
+        # manufactured u = sin3x cos2y, whose -Delta eigenvalue is 13)
+        return Config(name or f"helm_n{n}", 2, n, s, "star", ROW_LAPLACIAN, nrhs,
+                      R if R is not None else 8 * n, seed, 1e-10,
+                      boundary_weight=10.0, n_boundary=4 * n, k0sq=25.0)
     raise ValueError(f"unknown family {family!r}")
 
 
@@ -210,9 +218,9 @@ def exact_functions(cfg: Config) -> List[Callable]:
             for k in range(1, cfg.nrhs + 1)]
 
 
-def _laplacian_of_u(x, y):
-    # u = sin(3x) cos(2y)  =>  Delta u = -(9 + 4) u  (BASELINE configs[3] "f=Delta u")
-    return -13.0 * np.sin(3 * x) * np.cos(2 * y)
+def _laplacian_of_u(x, y, k0sq=0.0):
+    # u = sin(3x) cos(2y)  =>  Delta u + k0^2 u = (k0^2 - 13) u  (BASELINE configs[3] "f=Delta u": k0 = 0)
+    return (k0sq - 13.0) * np.sin(3 * x) * np.cos(2 * y)
 
 
 def rhs(cfg: Config) -> np.ndarray:
@@ -227,7 +235,7 @@ def rhs(cfg: Config) -> np.ndarray:
     Mb = cfg.n_boundary
     b = np.zeros((M + Mb, cfg.nrhs), dtype=np.float64, order="F")
     if cfg.row_op == ROW_LAPLACIAN:
-        b[:M, 0] = cfg.row_scale * _laplacian_of_u(pts[:, 0], pts[:, 1])
+        b[:M, 0] = cfg.row_scale * _laplacian_of_u(pts[:, 0], pts[:, 1], cfg.k0sq)
         bp = boundary_points(cfg)
         b[M:, 0] = cfg.boundary_weight * fns[0](bp[:, 0], bp[:, 1])
         return b

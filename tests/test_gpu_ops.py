@@ -32,6 +32,7 @@ CASES = [
     ("disk_n32", I.make_config("disk", 32)),
     ("star_n16", I.make_config("star", 16)),
     ("star_n32", I.make_config("star", 32)),
+    ("helm_n16", I.make_config("helm", 16)),      # Helmholtz rows, k0^2 = 25
     ("box2d_n16", I.make_config("box2d", 16)),
 ]
 
@@ -68,7 +69,7 @@ def test_plan_info(setup):
 
 def prob_sigma2(cfg):
     from oracle import circulant as C
-    sym = C.Symbol(cfg.dim, cfg.n, cfg.s, cfg.eps, cfg.T, cfg.row_op, alpha=cfg.row_scale)
+    sym = C.Symbol(cfg.dim, cfg.n, cfg.s, cfg.eps, cfg.T, cfg.row_op, alpha=cfg.row_scale, k0sq=cfg.k0sq)
     return sym.sigma2
 
 

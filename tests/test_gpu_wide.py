@@ -81,6 +81,7 @@ def _approx_err(cfg, x, ref_x, grid):
 # reduced members of the 2-D families; R = the family's block rule, adaptive blocks (reading R5)
 WIDE_CASES = [("disk_n32", I.make_config("disk", 32), 8),
               ("star_n32", I.make_config("star", 32), 8),
+              ("helm_n32", I.make_config("helm", 32), 8),      # SURVEY.md §8(f) f2 (2-D Helmholtz)
               ("disk_n32_nrhs3", I.make_config("disk", 32, nrhs=3, R=128), 12)]
 
 

@@ -14,8 +14,8 @@ from oracle import kernel as K
 from paper_2308_14490_b200 import inputs as I
 
 
-def _cfg(dim, n, s=2, domain="box", row_op=0, eps_h=0.5):
-    c = I.Config("t", dim, n, s, domain, row_op, 1, 8, 0, 1e-10)
+def _cfg(dim, n, s=2, domain="box", row_op=0, eps_h=0.5, k0sq=0.0):
+    c = I.Config("t", dim, n, s, domain, row_op, 1, 8, 0, 1e-10, k0sq=k0sq)
     return c
 
 
@@ -64,13 +64,15 @@ def test_min_of_d1_at_half():
     assert int(np.argmin(d[0].real)) == n // 2
 
 
-@pytest.mark.parametrize("dim,n,row_op", [(1, 32, 0), (1, 64, 0), (2, 8, 0), (2, 8, 1)])
-def test_lemma3_singular_values(dim, n, row_op):
-    """Singular values of the entrywise A^c (LAPACK) = sqrt(sum_i |d_i(k)|^2)."""
-    cfg = _cfg(dim, n, row_op=row_op)
+@pytest.mark.parametrize("dim,n,row_op,k0sq", [(1, 32, 0, 0.0), (1, 64, 0, 0.0), (2, 8, 0, 0.0), (2, 8, 1, 0.0),
+                                               (1, 32, 1, 25.0), (2, 8, 1, 25.0), (2, 16, 1, 7.0)])
+def test_lemma3_singular_values(dim, n, row_op, k0sq):
+    """Singular values of the entrywise A^c (LAPACK) = sqrt(sum_i |d_i(k)|^2); with k0^2 > 0 this pins
+    the Helmholtz rows alpha (Delta + k0^2) phi of the dense assembly and of the symbol together."""
+    cfg = _cfg(dim, n, row_op=row_op, k0sq=k0sq)
     Ac = D.assemble_Ac(cfg)
     sv = np.linalg.svd(Ac, compute_uv=False)
-    sym = C.Symbol(dim, n, 2, cfg.eps, cfg.T, row_op, alpha=cfg.row_scale)
+    sym = C.Symbol(dim, n, 2, cfg.eps, cfg.T, row_op, alpha=cfg.row_scale, k0sq=k0sq)
     ours = np.sort(np.sqrt(sym.sigma2))[::-1]
     assert np.max(np.abs(sv - ours)) < 1e-13 * sv[0]
 
@@ -201,3 +203,28 @@ def test_dense_A_rows_match_window_entries():
     row = np.zeros(cfg.N)
     row[cols] = vals
     assert np.allclose(row, A[5], rtol=1e-14, atol=1e-300)
+
+
+@pytest.mark.parametrize("k0sq", [0.0, 25.0])
+def test_helmholtz_rows_are_the_operator_applied_to_the_expansion(k0sq):
+    """PAPER.md:741-752 (and :698 in 1-D): a LAPLACIAN row at x applied to coefficients c equals
+    alpha (Delta u + k0^2 u)(x) for u = sum_j c_j phi_j -- checked against a 4th-order finite
+    difference Laplacian of the value rows (independent of the order-2 kernel formula)."""
+    n = 16
+    cfg = _cfg(2, n, row_op=1, k0sq=k0sq)
+    rng = np.random.default_rng(3)
+    c = rng.standard_normal(cfg.N)
+    x = np.array([[0.13, -0.27], [-0.41, 0.05]])
+    hd = 1e-3
+
+    def u(p):
+        return D.assemble_rows(cfg, p, "value") @ c
+
+    lap = np.zeros(len(x))
+    for ax in range(2):
+        e = np.zeros(2)
+        e[ax] = hd
+        lap += (-u(x + 2 * e) + 16 * u(x + e) - 30 * u(x) + 16 * u(x - e) - u(x - 2 * e)) / (12 * hd * hd)
+    rows = D.assemble_rows(cfg, x, "laplacian") @ c
+    ref = cfg.row_scale * (lap + k0sq * u(x))
+    assert np.allclose(rows, ref, rtol=1e-6, atol=1e-6 * np.abs(cfg.row_scale) * np.max(np.abs(lap)))
