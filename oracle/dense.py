@@ -31,6 +31,9 @@ def assemble_rows(cfg: I.Config, pts: np.ndarray, kind: str) -> np.ndarray:
     c = I.center_axis(cfg)
     eps, T = cfg.eps, cfg.T
     if cfg.dim == 1:
+        pts = np.asarray(pts, dtype=np.float64)
+        if pts.ndim == 2:          # (m, 1) boundary points
+            pts = pts[:, 0]
         if kind == "value":
             return _Phi(pts, c, eps, T, 0)
         return cfg.row_scale * (_Phi(pts, c, eps, T, 2) + cfg.k0sq * _Phi(pts, c, eps, T, 0))

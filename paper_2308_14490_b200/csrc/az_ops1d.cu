@@ -31,7 +31,27 @@ struct P1s {
   int64_t ldout;
   int64_t nvec;
   int64_t col0;
+  // boundary rows (1-D ODE): rows M .. M + Mb - 1 are beta phi_j(x_b);
+  // window of win centres starting at bj[2 b] with weights bw[2 b * 64 + t]
+  int64_t M, Mb;
+  double beta;
+  int win;
+  const double* bw;
+  const int32_t* bj;
 };
+
+// beta sum_t bw[b][t] coef[(j0_b + t) mod n] for boundary point b, by one thread (win <= 64 terms;
+// the CTA of a short transform can be smaller than a warp); coef(j) callable
+template <class F>
+AZ_D cplx boundary_dot(const P1s& a, int b, F coef) {
+  cplx acc = czero();
+  const int j0 = a.bj[2 * b];
+  for (int t = 0; t < a.win; ++t) {
+    const int j = ((j0 + t) % a.n + a.n) % a.n;
+    acc = cadd(acc, cscale(coef(j), a.bw[2 * b * 64 + t]));
+  }
+  return cscale(acc, a.beta);
+}
 
 AZ_D cplx sym1(const P1s& a, int kf) {
   return a.lap ? cscale(cadd(a.W2[kf], cscale(a.W0[kf], a.k0sq)), a.alpha) : a.W0[kf];
@@ -49,6 +69,16 @@ __global__ void __launch_bounds__(L / 8) k_chain1s(P1s a) {
   const bool has_im = cim < a.nvec;
   const double invL = 1.0 / (double)L;
 
+  // boundary rows that only need the coefficient input
+  if constexpr (OP == OP_A) {
+    for (int bp = tid; bp < a.Mb; bp += NT) {
+      const cplx yb = boundary_dot(a, bp, [&](int j) {
+        return make_double2(a.in[j + cre * a.ldin], has_im ? a.in[j + cim * a.ldin] : 0.0);
+      });
+      a.out[a.M + bp + cre * a.ldout] = yb.x;
+      if (has_im) a.out[a.M + bp + cim * a.ldout] = yb.y;
+    }
+  }
   if constexpr (OP == OP_A || OP == OP_STEP1) {
     // ---- coefficient input, zero-stuffed onto the fine grid ----
     for (int q = tid; q < L; q += NT) buf[spad(q)] = czero();
@@ -91,6 +121,19 @@ __global__ void __launch_bounds__(L / 8) k_chain1s(P1s a) {
         aux[k] = csub(aux[k], cscale(acc, a.zinv[k]));
       }
       __syncthreads();
+      if (a.Mb > 0) {
+        // boundary rows of (A - A Z* A) v = A^b r, r = v - Z* A v: r from its spectrum r^ (aux),
+        // IFFT_L(extend r^)[s j] / L = r_j
+        for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = aux[kf & (n - 1)];
+        __syncthreads();
+        fft_smem<L, 1>(buf, tid, a.tw, TWN);
+        for (int bp = tid; bp < a.Mb; bp += NT) {
+          const cplx yb = boundary_dot(a, bp, [&](int j) { return cscale(buf[spad(j * s)], invL); });
+          a.out[a.M + bp + cre * a.ldout] = yb.x;
+          if (has_im) a.out[a.M + bp + cim * a.ldout] = yb.y;
+        }
+        __syncthreads();
+      }
       for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = cscale(cmul(aux[kf & (n - 1)], sym1(a, kf)), invL);
       __syncthreads();
       fft_smem<L, 1>(buf, tid, a.tw, TWN);
@@ -124,6 +167,19 @@ __global__ void __launch_bounds__(L / 8) k_chain1s(P1s a) {
     }
     __syncthreads();
     if constexpr (OP == OP_RESID) {
+      if (a.Mb > 0) {
+        // boundary rows of (I - A Z*) b: b_b - A^b w, w = Z* b from its spectrum (aux)
+        for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = aux[kf & (n - 1)];
+        __syncthreads();
+        fft_smem<L, 1>(buf, tid, a.tw, TWN);
+        for (int bp = tid; bp < a.Mb; bp += NT) {
+          const cplx yb = boundary_dot(a, bp, [&](int j) { return cscale(buf[spad(j * s)], invL); });
+          const int64_t r = a.M + bp;
+          a.out[r + cre * a.ldout] = a.in[r + cre * a.ldin] - yb.x;
+          if (has_im) a.out[r + cim * a.ldout] = a.in[r + cim * a.ldin] - yb.y;
+        }
+        __syncthreads();
+      }
       for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = cscale(cmul(aux[kf & (n - 1)], sym1(a, kf)), invL);
     } else {
       for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = aux[kf & (n - 1)];
@@ -142,9 +198,18 @@ __global__ void __launch_bounds__(L / 8) k_chain1s(P1s a) {
     } else {
       const double c = (OP == OP_ZSTAR) ? invL : invL / (double)s;
       for (int j = tid; j < n; j += NT) {
-        const cplx v = buf[spad(j * s)];
-        a.out[j + cre * a.ldout] = v.x * c;
-        if (has_im) a.out[j + cim * a.ldout] = v.y * c;
+        cplx v = cscale(buf[spad(j * s)], c);
+        if (OP == OP_AT)   // + (A^b)^T y_b: beta phi_j(x_b) y_b over the boundary windows covering j
+          for (int bp = 0; bp < a.Mb; ++bp) {
+            const int t = ((j - a.bj[2 * bp]) % n + n) % n;
+            if (t < a.win) {
+              const double wgt = a.beta * a.bw[2 * bp * 64 + t];
+              const int64_t r = a.M + bp;
+              v = cadd(v, make_double2(wgt * a.in[r + cre * a.ldin], has_im ? wgt * a.in[r + cim * a.ldin] : 0.0));
+            }
+          }
+        a.out[j + cre * a.ldout] = v.x;
+        if (has_im) a.out[j + cim * a.ldout] = v.y;
       }
     }
   }
@@ -187,6 +252,12 @@ az_status_t az1s_apply(az_plan_s* p, int op, int src, const double* in, int64_t 
   a.ldout = ldout;
   a.nvec = nvec;
   a.col0 = col0;
+  a.M = p->M;
+  a.Mb = p->Mb;
+  a.beta = p->beta;
+  a.win = p->win;
+  a.bw = p->d_bw;
+  a.bj = p->d_bj;
   const int64_t npairs = (nvec + 1) / 2;
   switch (p->L) {
     case 16: return launch1s<16>(a, op, src, npairs, st);

@@ -218,11 +218,11 @@ __global__ void k_samples(cplx* out, int64_t L, double hL, double eps, double T,
 
 // Boundary stencils (CS1 step 6): for boundary point b and axis d, the window of centres
 // j = j0 .. j0 + win - 1 (mod n) around x_b and the weights phi^per(x_b - c_j).
-__global__ void k_stencil(const double* bxy, int64_t Mb, int n, double T, double h, double eps, int win,
+__global__ void k_stencil(const double* bxy, int64_t Mb, int dim, int n, double T, double h, double eps, int win,
                           double* bw, int32_t* bj) {
   const int b = blockIdx.x, d = blockIdx.y, t = threadIdx.x;
   if (b >= Mb) return;
-  const double x = bxy[2 * b + d];
+  const double x = bxy[dim * b + d];
   const int half = (win - 1) / 2;
   const int j0 = (int)rint((x + T) / h) - half;
   if (t == 0) bj[2 * b + d] = j0;
@@ -374,7 +374,7 @@ static az_status_t plan_build(az_plan_s* p, const az_plan_desc_t* d, cudaStream_
   AZ_CUDA_CHECK(cudaMemcpyAsync(p->d_pos, pos.data(), p->G * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   if (p->Mb) {
     AZ_TRY(dalloc(&p->d_bxy, p->Mb * 2));
-    AZ_CUDA_CHECK(cudaMemcpyAsync(p->d_bxy, d->boundary_xy, p->Mb * 2 * sizeof(double),
+    AZ_CUDA_CHECK(cudaMemcpyAsync(p->d_bxy, d->boundary_xy, p->Mb * p->dim * sizeof(double),
                                   cudaMemcpyHostToDevice, st));
     // phi(r) < e^-40 beyond r = sqrt(40)/eps: window of 2 ceil(sqrt(40)/(eps h)) + 3 centres
     const double h = 2.0 * p->T / (double)p->n;
@@ -386,8 +386,8 @@ static az_status_t plan_build(az_plan_s* p, const az_plan_desc_t* d, cudaStream_
     }
     AZ_TRY(dalloc(&p->d_bw, p->Mb * 2 * 64));
     AZ_TRY(dalloc(&p->d_bj, p->Mb * 2));
-    k_stencil<<<dim3((unsigned)p->Mb, 2), 64, 0, st>>>(p->d_bxy, p->Mb, (int)p->n, p->T, h, p->eps, p->win,
-                                                      p->d_bw, p->d_bj);
+    k_stencil<<<dim3((unsigned)p->Mb, (unsigned)p->dim), 64, 0, st>>>(p->d_bxy, p->Mb, p->dim, (int)p->n, p->T, h,
+                                                                      p->eps, p->win, p->d_bw, p->d_bj);
     AZ_LAUNCH_CHECK();
   }
   // ---- twiddles ----
@@ -481,8 +481,8 @@ extern "C" az_status_t az_plan_create(const az_plan_desc_t* d, void* stream, az_
   AZ_ARG(d->zstar_rcond >= 0 && d->zstar_rcond < 1, "zstar_rcond must be in [0, 1)");
   const int64_t L = d->n * d->L;
   if (d->dim == 1) {
-    if (d->n < 16 || d->n > (1 << 21) || d->n_boundary != 0) {
-      az_set_error("1-D: need 16 <= n <= 2^21 and no boundary rows");
+    if (d->n < 16 || d->n > (1 << 21) || (d->n_boundary != 0 && L > 2048)) {
+      az_set_error("1-D: need 16 <= n <= 2^21; boundary rows (ODE) need L n <= 2048");
       return AZ_ERR_NOT_SUPPORTED;
     }
   } else {

@@ -107,6 +107,12 @@ def make_config(family: str, n: int, *, nrhs: int = 1, R: Optional[int] = None,
         return Config(name or f"star_n{n}", 2, n, s, "star", ROW_LAPLACIAN, nrhs,
                       R if R is not None else 8 * n, seed, 1e-10,
                       boundary_weight=10.0, n_boundary=4 * n)
+    if family == "ode":
+        # SURVEY.md §8(f) f2, PAPER.md Example 6.1 (:694-705, Fig. 8 :823-830): u'' + k^2 u = 0 on [-1, 1],
+        # u(+-1) = sin(+-n/5), k = n/5, box T = 1.5, s = 2; Dirichlet rows at the two endpoints (beta = 1)
+        return Config(name or f"ode_n{n}", 1, n, s, "ode", ROW_LAPLACIAN, nrhs,
+                      R if R is not None else 40, seed, 1e-10,
+                      boundary_weight=1.0, n_boundary=2, T=1.5, k0sq=(n / 5.0) ** 2)
     if family == "helm":
         # 2-D Helmholtz Delta u + k0^2 u = f on the star domain,
         # the c4 geometry and weights with k0^2 = 25 (k0 = 5: k0^2 is not an eigenvalue of the
@@ -149,6 +155,8 @@ def _in_domain(domain: str, x: np.ndarray, y: Optional[np.ndarray] = None) -> np
     # Closed membership, computed in binary64 exactly as SURVEY.md §8(c-4) #13 states.
     if domain == "interval":
         return (-0.5 <= x) & (x <= 0.5)
+    if domain == "ode":
+        return (-1.0 <= x) & (x <= 1.0)
     if domain == "box":
         return np.ones(np.broadcast(x, x if y is None else y).shape, dtype=bool)
     if domain == "disk":
@@ -188,6 +196,8 @@ def boundary_points(cfg: Config) -> np.ndarray:
     """(M_b, 2) boundary points, theta_k = 2 pi k / M_b (SURVEY.md §8(c-4) #12)."""
     if cfg.n_boundary == 0:
         return np.zeros((0, max(cfg.dim, 1)), dtype=np.float64)
+    if cfg.domain == "ode":
+        return np.array([[-1.0], [1.0]])
     if cfg.domain != "star":
         raise ValueError("boundary points are defined for the star domain only")
     th = 2.0 * np.pi * np.arange(cfg.n_boundary, dtype=np.float64) / cfg.n_boundary
@@ -205,6 +215,9 @@ def exact_functions(cfg: Config) -> List[Callable]:
     For the Poisson config this is the manufactured solution u (the approximant is
     u's expansion); for approximation configs it is f itself.
     """
+    if cfg.row_op == ROW_LAPLACIAN and cfg.dim == 1:
+        kk = cfg.n / 5.0
+        return [lambda x: np.sin(kk * x)]
     if cfg.row_op == ROW_LAPLACIAN:
         return [lambda x, y: np.sin(3 * x) * np.cos(2 * y)]
     if cfg.dim == 1:
@@ -234,6 +247,11 @@ def rhs(cfg: Config) -> np.ndarray:
     M = pts.shape[0]
     Mb = cfg.n_boundary
     b = np.zeros((M + Mb, cfg.nrhs), dtype=np.float64, order="F")
+    if cfg.row_op == ROW_LAPLACIAN and cfg.dim == 1:
+        # u'' + k^2 u = 0 for u = sin(k x): interior data 0, boundary data beta u(+-1)
+        b[:M, 0] = 0.0
+        b[M:, 0] = cfg.boundary_weight * fns[0](boundary_points(cfg)[:, 0])
+        return b
     if cfg.row_op == ROW_LAPLACIAN:
         b[:M, 0] = cfg.row_scale * _laplacian_of_u(pts[:, 0], pts[:, 1], cfg.k0sq)
         bp = boundary_points(cfg)
@@ -259,7 +277,8 @@ def test_grid(cfg: Config, points_1d: Optional[int] = None) -> TestGrid:
     fns = exact_functions(cfg)
     if cfg.dim == 1:
         m = points_1d or (2001 if cfg.n <= 4096 else 65537)
-        t = np.linspace(-0.5, 0.5, m) if cfg.domain == "interval" else np.linspace(-1, 1, m, endpoint=False)
+        t = (np.linspace(-0.5, 0.5, m) if cfg.domain == "interval" else
+             np.linspace(-1, 1, m) if cfg.domain == "ode" else np.linspace(-1, 1, m, endpoint=False))
         inside = np.ones(m, dtype=bool)
         ex = np.stack([f(t) for f in fns], axis=1)
         return TestGrid((t,), inside, ex)

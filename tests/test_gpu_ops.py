@@ -33,6 +33,8 @@ CASES = [
     ("star_n16", I.make_config("star", 16)),
     ("star_n32", I.make_config("star", 32)),
     ("helm_n16", I.make_config("helm", 16)),      # Helmholtz rows, k0^2 = 25
+    ("ode_n64", I.make_config("ode", 64)),        # f2: 1-D ODE, two Dirichlet rows, box T = 1.5
+    ("ode_n256", I.make_config("ode", 256)),
     ("box2d_n16", I.make_config("box2d", 16)),
 ]
 

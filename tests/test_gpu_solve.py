@@ -84,6 +84,7 @@ def _approx_err(cfg, x, ref_x, grid):
 
 
 SOLVE_CASES = [("c1", I.get_config("c1"), 4), ("interval_n512", I.make_config("interval", 512, R=40), 4),
+               ("ode_n128", I.make_config("ode", 128), 4),      # SURVEY.md §8(f) f2, PAPER.md Example 6.1
                ("interval_n4096_4step", I.make_config("interval", 4096, nrhs=6, R=40), 4)]
 
 
