@@ -165,7 +165,14 @@ class GpuOps:
     def qr_partial(self, A, k1):
         from .api import qr_r, qr_r_partial
         A = self.contig(A)
-        return qr_r_partial(A, k1) if A.shape[1] <= 128 else qr_r(A)[:k1]
+        if A.shape[1] <= 128:
+            return qr_r_partial(A, k1)
+        if A.shape[0] < A.shape[1]:     # the blocked path needs m >= k: zero rows leave R unchanged
+            Z = colmajor_empty(A.shape[1], A.shape[1], A)
+            Z.zero_()
+            Z[:A.shape[0]] = A
+            A = Z
+        return qr_r(A)[:k1]
 
     def tsvd(self, Rf, r, nrhs, theta):
         from .api import tsvd_solve

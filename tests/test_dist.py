@@ -155,3 +155,36 @@ def test_solve_sharded_world2_matches_single_and_oracle():
     fo = OA.evaluate(cfg, r2.x.reshape(cfg.N, -1), grid)
     assert np.max(np.abs(f2 - fo)) <= 1e-9 * np.max(np.abs(fo))
     assert abs(rep0["rank"] - r2.rank) <= 1
+
+
+def _solve_case_2d(rank, world):
+    cfg = I.make_config("star", 16)
+    ops = CpuOps(cfg)
+    b = _cm(I.rhs(cfg))
+    x, rep = D.solve_sharded(ops, b, 1e-12, cfg.R, max_blocks=8)
+    return x.numpy(), rep
+
+
+def test_solve_sharded_world2_2d_star():
+    """The same orchestration on a 2-D Poisson member (star, Laplacian + Dirichlet rows)."""
+    res2 = _run(_solve_case_2d, 2)
+    x0, rep0 = res2[0]
+    x1, _ = res2[1]
+    assert np.array_equal(x0, x1) and not rep0["saturated"]
+    cfg = I.make_config("star", 16)
+    grid = I.test_grid(cfg)
+    prob = OA.make_problem(cfg, "fft")
+    b = I.rhs(cfg)
+    r2 = OA.az_solve(prob, b, 1e-12, cfg.R, cfg.seed, max_blocks=8)
+    f2, fo = OA.evaluate(cfg, x0, grid), OA.evaluate(cfg, r2.x.reshape(cfg.N, -1), grid)
+    # bar: max(1e-9, 2 delta_det) with the dense oracle's own determinacy (SURVEY.md §8(c) F4)
+    from oracle import dense as OD
+    A = OD.assemble_A(cfg)
+    xa, _, _ = OA.tsvd_lsq(A, b, cfg.tol)
+    xb, _, _ = OA.tsvd_lsq(A, b, cfg.tol / 100)
+    fa, fb = OA.evaluate(cfg, xa, grid), OA.evaluate(cfg, xb, grid)
+    det = np.max(np.abs(fa - fb)) / np.max(np.abs(fa))
+    assert np.max(np.abs(f2 - fo)) <= max(1e-9, 2 * det) * np.max(np.abs(fo)), det
+    res = np.linalg.norm(A @ x0 - b, axis=0) / np.linalg.norm(b, axis=0)
+    ro = np.linalg.norm(A @ xa - b, axis=0) / np.linalg.norm(b, axis=0)
+    assert np.all(res <= np.maximum(2 * ro, 1e-12)), (res, ro)   # reading R8 / F3

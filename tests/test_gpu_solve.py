@@ -147,7 +147,8 @@ def test_solve_c2_full_size():
 
 
 @pytest.mark.parametrize("name,cfg,max_blocks", [("c1", I.get_config("c1"), 4),
-                                                 ("interval_n4096_4step", I.make_config("interval", 4096, nrhs=6, R=40), 4)])
+                                                 ("interval_n4096_4step", I.make_config("interval", 4096, nrhs=6, R=40), 4),
+                                                 ("star_n32", I.make_config("star", 32), 8)])
 def test_solve_sharded_nccl_world1_matches_az_solve(name, cfg, max_blocks):
     """The multi-GPU orchestration (dist.py) over NCCL at world size 1 on the GPU kernels: same
     approximant as the single-call az_solve (the N > 1 host logic is covered by tests/test_dist.py)."""
@@ -165,8 +166,12 @@ def test_solve_sharded_nccl_world1_matches_az_solve(name, cfg, max_blocks):
         b = _dev(I.rhs(cfg))
         x1, rep1 = plan.solve(b, 1e-12, cfg.R, max_blocks)
         xs, reps = D.solve_sharded(D.GpuOps(plan), colmajor(b), 1e-12, cfg.R, max_blocks)
-        assert reps["probes"] == rep1["probes"] and abs(reps["rank"] - rep1["rank"]) <= 1
         grid = I.test_grid(cfg)
-        assert np.all(_approx_err(cfg, _host(xs), _host(x1), grid) <= 1e-10)
+        if cfg.dim == 1:
+            assert reps["probes"] == rep1["probes"] and abs(reps["rank"] - rep1["rank"]) <= 1
+            assert np.all(_approx_err(cfg, _host(xs), _host(x1), grid) <= 1e-10)
+        else:   # 2-D: the probe count is noise-determined (reading R24); approximants agree to the bar
+            assert not reps["saturated"]
+            assert np.all(_approx_err(cfg, _host(xs), _host(x1), grid) <= 1e-8)
     finally:
         dist.destroy_process_group()
