@@ -56,6 +56,7 @@ class Config:
     n_boundary: int = 0            # M_b
     T: float = 1.0
     k0sq: float = 0.0              # Helmholtz term of the LAPLACIAN rows (0 = Poisson)
+    eps_h: float = 0.5             # eps * h: 0.5 in every BASELINE config; the paper's regime is eps_h_paper(tau0)
 
     @property
     def h(self) -> float:
@@ -63,8 +64,8 @@ class Config:
 
     @property
     def eps(self) -> float:
-        # BASELINE: eps = 0.5 / h  (SURVEY.md §0 naming trap 3)
-        return 0.5 / self.h
+        # BASELINE: eps = 0.5 / h  (SURVEY.md §0 naming trap 3); eps_h overrides for the paper's regime
+        return self.eps_h / self.h
 
     @property
     def grid_n(self) -> int:
@@ -88,9 +89,27 @@ def _disk_R(n: int, s: int) -> int:
     return int(round(1.5 * math.pi * 0.8 * s * n))
 
 
+def eps_h_paper(tau0: float) -> float:
+    """The paper's shape-parameter regime eps = c N with c from Eq. (4),
+    c = pi / (2 T sqrt(2 log(1 + tau0^-2))), h = 2T/N:  eps h = pi / sqrt(2 log(1 + tau0^-2)).
+    (the paper uses tau0 = 1e-10 in 1-D and 1e-5 in 2-D.)"""
+    return math.pi / math.sqrt(2.0 * math.log1p(tau0 ** -2))
+
+
 def make_config(family: str, n: int, *, nrhs: int = 1, R: Optional[int] = None,
-                seed: int = 0, s: int = 2, name: Optional[str] = None) -> Config:
-    """Members of the BASELINE families at any size (reduced members for parity)."""
+                seed: int = 0, s: int = 2, name: Optional[str] = None, eps_h: Optional[float] = None) -> Config:
+    """Members of the BASELINE families at any size (reduced members for parity); eps_h overrides
+    eps * h (default 0.5)."""
+    return _with_eps(_make_config(family, n, nrhs=nrhs, R=R, seed=seed, s=s, name=name), eps_h)
+
+
+def _make_config(family: str, n: int, *, nrhs: int = 1, R: Optional[int] = None,
+                 seed: int = 0, s: int = 2, name: Optional[str] = None) -> Config:
+    if family.endswith("_paper"):
+        # the same family in the paper's own eps regime (tau0 = 1e-10 in 1-D, 1e-5 in 2-D)
+        base = family[:-len("_paper")]
+        c = make_config(base, n, nrhs=nrhs, R=R, seed=seed, s=s, name=name or f"{base}_paper_n{n}")
+        return dataclasses.replace(c, eps_h=eps_h_paper(1e-10 if c.dim == 1 else 1e-5))
     if family == "interval":
         return Config(name or f"interval_n{n}", 1, n, s, "interval", ROW_VALUE, nrhs,
                       R if R is not None else 40, seed, 1e-12)
@@ -121,6 +140,10 @@ def make_config(family: str, n: int, *, nrhs: int = 1, R: Optional[int] = None,
                       R if R is not None else 8 * n, seed, 1e-10,
                       boundary_weight=10.0, n_boundary=4 * n, k0sq=25.0)
     raise ValueError(f"unknown family {family!r}")
+
+
+def _with_eps(c: Config, eps_h: Optional[float]) -> Config:
+    return c if eps_h is None else dataclasses.replace(c, eps_h=eps_h)
 
 
 # BASELINE.json configs[0..4]

@@ -173,3 +173,37 @@ def test_factorize_and_solve_factored_matches_solve(name, cfg, max_blocks):
         xo, _, _ = OA.tsvd_lsq(A, b2, cfg.tol)
         ro = np.linalg.norm(A @ xo - b2, axis=0) / np.linalg.norm(b2, axis=0)
         assert np.all(res <= np.maximum(2 * ro, 1e-10)), (res, ro)
+
+
+PAPER_EPS_CASES = [("interval_paper_n256", I.make_config("interval_paper", 256), 4),
+                   ("interval_paper_n1024", I.make_config("interval_paper", 1024), 8),
+                   ("disk_paper_n32", I.make_config("disk_paper", 32), 12),
+                   ("star_paper_n32", I.make_config("star_paper", 32), 12)]
+
+
+@pytest.mark.parametrize("name,cfg,max_blocks", PAPER_EPS_CASES, ids=[c[0] for c in PAPER_EPS_CASES])
+def test_paper_eps_regime(name, cfg, max_blocks):
+    """the paper's own shape parameter eps = cN with c from Eq. (4) (tau0 = 1e-10 in
+    1-D, 1e-5 in 2-D), where ||Z*|| reaches 1e8-1e9.  Judged against O1 (the
+    dense truncated SVD) with its own determinacy as the bar (F4), the residual against O1's (F3), and
+    in 1-D the step-1 rank against Theorem 7's bound 4W."""
+    from paper_2308_14490_b200.api import Plan
+    from oracle import kernel as K
+    plan = Plan.from_config(cfg)
+    b = I.rhs(cfg)
+    theta = max(cfg.tol * 1e-2, 1e-12)
+    x, rep = plan.solve(_dev(b), theta, cfg.R, max_blocks)
+    x = _host(x)
+    assert not rep["saturated"]
+    A = OD.assemble_A(cfg)
+    grid = I.test_grid(cfg)
+    xo, _, _ = OA.tsvd_lsq(A, b, cfg.tol)
+    xo2, _, _ = OA.tsvd_lsq(A, b, cfg.tol / 100)
+    det = _approx_err(cfg, xo2, xo, grid)
+    err = _approx_err(cfg, x, xo, grid)
+    assert np.all(err <= np.maximum(1e-9, 2 * det)), (err, det)
+    res = np.linalg.norm(A @ x - b, axis=0) / np.linalg.norm(b, axis=0)
+    ro = np.linalg.norm(A @ xo - b, axis=0) / np.linalg.norm(b, axis=0)
+    assert np.all(res <= np.maximum(2 * ro, 1e-12)), (res, ro)
+    if cfg.dim == 1:
+        assert rep["rank"] <= 4 * K.theorem7_W(theta, 1e-10)
