@@ -162,11 +162,12 @@ def test_probe_generator_bitwise_reproducible(setup):
     assert torch.equal(s1[:, 2:4], s3)
 
 
-@pytest.mark.parametrize("name", ["c2"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
 def test_full_size_sampled_and_normwise(name):
-    """BASELINE full size (c2: n = 2^20, fine grid 2^21) in the bench's launch configuration:
-    sampled rows of A x against the windowed exact row sums, and the composite operators
-    against the FFT oracle normwise."""
+    """BASELINE full sizes (c2: n = 2^20, fine grid 2^21; c3/c4/c5: 256^2 / 128^2 / 512^2 centres)
+    in the bench's launch configuration: sampled rows of A x against the windowed exact row sums
+    (interior and, for c4, boundary rows), and the composite operators against the FFT oracle
+    normwise (reading R9)."""
     from paper_2308_14490_b200.api import Plan
     cfg = I.get_config(name)
     plan = Plan.from_config(cfg)
@@ -175,10 +176,18 @@ def test_full_size_sampled_and_normwise(name):
     x = I.gaussian_matrix(cfg.N, 2, 3)
     y = _host(plan.apply_A(_dev(x)))
     rows = np.argwhere(I.mask(cfg).reshape(-1)).ravel()
+    gn = cfg.grid_n
     for r in rng.choice(plan.M, 64, replace=False):
-        cols, vals = OD.A_row_entries(cfg, rows[r], half_width=40)
+        g = rows[r] if cfg.dim == 1 else (rows[r] // gn, rows[r] % gn)
+        cols, vals = OD.A_row_entries(cfg, g, half_width=40 if cfg.dim == 1 else 16)
         ref = vals @ x[cols]
         assert np.all(np.abs(y[r] - ref) <= 1e-12 * np.abs(vals) @ np.abs(x[cols]))
+    if cfg.n_boundary:
+        bpts = I.boundary_points(cfg)
+        for i in rng.choice(cfg.n_boundary, 8, replace=False):
+            rowv = OD.boundary_row(cfg, bpts[i])
+            ref = rowv @ x
+            assert np.all(np.abs(y[plan.M + i] - ref) <= 1e-12 * np.abs(rowv) @ np.abs(x))
     ref = prob.apply_A(x)
     assert _rel(y, ref) <= 1e-12
     nA = plan.sigma_max
@@ -190,5 +199,5 @@ def test_full_size_sampled_and_normwise(name):
     b = I.rhs(cfg)[:, :3]
     z = _host(plan.apply_Zstar(_dev(b)))
     refz = prob.apply_Zstar(b)
-    for c in range(3):
+    for c in range(b.shape[1]):
         assert np.linalg.norm(z[:, c] - refz[:, c]) <= 1e-12 * plan.zstar_norm * np.linalg.norm(b[:, c])

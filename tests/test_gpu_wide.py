@@ -119,7 +119,7 @@ def test_solve_2d_matches_oracle(name, cfg, max_blocks):
     assert np.all(err2 <= np.maximum(1e-9, 2 * det)), (err2, det)
 
 
-@pytest.mark.parametrize("name", ["c4", "c3"])
+@pytest.mark.parametrize("name", ["c4", "c3", "c5"])
 def test_solve_2d_full_size(name):
     """BASELINE configs 3 and 4 at full size.  The dense oracle is infeasible here (c3: 69 GB dense A;
     c4: ~700 s dense SVD), so parity is pinned by the manufactured solution and
@@ -129,10 +129,10 @@ def test_solve_2d_full_size(name):
     cfg = I.get_config(name)
     plan = Plan.from_config(cfg)
     b = I.rhs(cfg)
-    x, rep = plan.solve(_dev(b), max(cfg.tol * 1e-2, 1e-12), cfg.R, 16)
+    x, rep = plan.solve(_dev(b), max(cfg.tol * 1e-2, 1e-12), cfg.R, 16 if cfg.n < 512 else 6)
     x = _host(x)
     assert not rep["saturated"] and rep["rank"] <= rep["probes"] - 10
-    grid = I.test_grid(cfg, 201)
+    grid = I.test_grid(cfg, 201 if cfg.n < 512 else 101)
     f = OA.evaluate(cfg, x, grid)
     err = np.max(np.abs(f - grid.exact), axis=0) / np.max(np.abs(grid.exact), axis=0)
     assert np.all(err <= 1e-8), err
