@@ -184,6 +184,16 @@ const char* az_last_error(void);
  * for the bench's gpu_launches field). */
 int64_t az_launch_count(int reset);
 
+/* Pipelined host-buffer solves (the e2e path): enqueue H2D of b_host (an internal upload stream),
+ * az_solve on `stream` (no report, no host synchronisation when max_blocks == 1) and D2H into
+ * x_host (an internal download stream), then return.  Two internal device slots let a call's
+ * upload and the previous call's download overlap the current solve.  x_host is valid after
+ * az_plan_sync.  Host buffers should be pinned (cudaHostAlloc / torch pin_memory); b_host must not
+ * be modified until az_plan_sync.  Same shapes as az_solve_host.                             */
+az_status_t az_solve_host_pipelined(az_plan_t plan, const double* b_host, double* x_host, int64_t nrhs,
+                                    double theta, int64_t R, int32_t max_blocks, void* stream);
+az_status_t az_plan_sync(az_plan_t plan);
+
 /* ---- factorisation reuse --------------------------------------------
  * The step-1 matrix (A - A Z* A) Omega does not depend on b (Alg. 1, :228, :283): factor
  * it once, then solve for any number of right-hand sides at the cost of b' = (I - A Z*) b, Q^T b'

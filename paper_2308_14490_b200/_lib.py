@@ -71,6 +71,8 @@ def lib():
         "az_qr_r": [P, P, I64, I64, I64, P, I64, P, C.c_size_t, P],
         "az_qr_r_partial": [P, P, I64, I64, I64, I64, P, I64, P, C.c_size_t, P],
         "az_factorize": [P, D, I64, C.c_int32, C.POINTER(P), C.POINTER(SolveReport), P],
+        "az_solve_host_pipelined": [P, P, P, I64, D, I64, C.c_int32, P],
+        "az_plan_sync": [P],
         "az_factor_destroy": [P],
         "az_factor_query": [P, C.POINTER(I64), C.POINTER(I64)],
         "az_factor_workspace_size": [P, I64, C.POINTER(C.c_size_t)],
@@ -104,7 +106,7 @@ EXPORTED = ["az_plan_create", "az_plan_destroy", "az_plan_query", "az_apply_A", 
             "az_solve_workspace_size", "az_solve", "az_solve_host", "az_status_string",
             "az_last_error", "az_launch_count", "az_trace_enable", "az_trace_report",
             "az_factorize", "az_factor_destroy", "az_factor_query", "az_factor_workspace_size",
-            "az_solve_factored"]
+            "az_solve_factored", "az_solve_host_pipelined", "az_plan_sync"]
 
 
 def check(fn: str, status: int, allow=(AZ_OK,)):

@@ -232,6 +232,28 @@ class Factor:
         return x, _report(rep, st)
 
 
+def _host_ptr(t, what):
+    if not isinstance(t, torch.Tensor) or t.is_cuda or t.dtype != torch.float64:
+        raise TypeError(f"{what}: expected a float64 CPU (pinned) tensor")
+    if t.dim() == 2 and t.stride(0) != 1:
+        raise ValueError(f"{what}: must be column-major")
+    return t.data_ptr()
+
+
+def solve_host_pipelined(plan: "Plan", b, x, theta: float, R: int, max_blocks: int = 1, stream=None):
+    """az_solve_host_pipelined: enqueue upload of b (pinned host), solve, download into x (pinned
+    host) and return; call plan_sync(plan) before reading x."""
+    nrhs = 1 if b.dim() == 1 else b.shape[1]
+    check("az_solve_host_pipelined", lib().az_solve_host_pipelined(
+        plan._h, C.c_void_p(_host_ptr(b, "b")), C.c_void_p(_host_ptr(x, "x")), nrhs, theta, R, max_blocks,
+        _stream(stream)), allow=(_lib.AZ_OK, _lib.AZ_WARN_SKETCH_SATURATED))
+    return x
+
+
+def plan_sync(plan: "Plan"):
+    check("az_plan_sync", lib().az_plan_sync(plan._h))
+
+
 def _report(rep, status):
     return {"rank": rep.rank_used, "probes": rep.probes_used, "saturated": bool(rep.saturated),
             "sigma_first": rep.sigma_first, "sigma_last_kept": rep.sigma_last_kept,

@@ -19,6 +19,9 @@ enum az_op_t { OP_A = 0, OP_AT = 1, OP_ZSTAR = 2, OP_STEP1 = 3, OP_RESID = 4, OP
 // Input sources for coefficient-space entry.
 enum az_src_t { SRC_VEC = 0, SRC_PROBE = 1 };
 
+struct az_pipe_s;   // az_solve_host_pipelined state (az_solve.cu)
+void az_pipe_destroy(struct az_plan_s* p);
+
 struct az_plan_s {
   // geometry
   int dim;
@@ -61,6 +64,7 @@ struct az_plan_s {
   size_t h_stage_bytes = 0;
   void* d_solve_ws = nullptr;
   size_t d_solve_ws_bytes = 0;
+  az_pipe_s* pipe = nullptr;
 };
 
 constexpr int TWN = 2048;

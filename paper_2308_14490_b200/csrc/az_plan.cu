@@ -325,6 +325,7 @@ static bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 static int ilog2(int64_t v) { int k = 0; while ((int64_t(1) << k) < v) ++k; return k; }
 
 static void plan_free(az_plan_s* p) {
+  if (p) az_pipe_destroy(p);
   if (!p) return;
   void* ptrs[] = {p->d_mask, p->d_pos, p->d_W0, p->d_W2, p->d_Wr, p->d_zinv, p->d_tw, p->d_tw4hi,
                   p->d_tw4lo, p->d_bxy, p->d_bw, p->d_bj, p->d_C1, p->d_G, p->d_solve_ws};

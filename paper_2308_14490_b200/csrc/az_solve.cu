@@ -9,6 +9,9 @@
 // Probe blocks are added while the sketch is saturated, rank > probes - p (p = 10),
 // up to max_blocks (reading R5).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -246,12 +249,19 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t rows = p->M + p->Mb;
   const int pfix = 10;
+  // no report and a single probe block: nothing needs to come back to the host, so the whole solve
+  // is enqueued without a host synchronisation (az_solve_host_pipelined relies on this)
+  const bool async_mode = report == nullptr && max_blocks == 1;
+  static const bool dbg_host = getenv("AZ_DEBUG_HOST") != nullptr;
+  auto hnow = []() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  const double th0 = dbg_host ? hnow() : 0.0;
   Ev ev;
   cudaEventRecord(ev.e[0], st);
   // ---- right-hand side b' = (I - A Z*) b (narrow single-block solve: straight into S) ----
   const bool bp_in_S = !w.wide && max_blocks == 1;
   AZ_TRY(az_apply_op(p, OP_RESID, b, ldb, bp_in_S ? w.S + R * rows : w.bp, rows, nrhs, st));
   cudaEventRecord(ev.e[1], st);
+  if (dbg_host) fprintf(stderr, "az_solve host: resid issued +%.2f ms\n", hnow() - th0);
   double ms_sketch = 0, ms_qr = 0, ms_svd = 0;
   int64_t rank = 0, nb = 0;
   bool saturated = false;
@@ -273,6 +283,7 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
       AZ_LAUNCH_CHECK();
     }
     cudaEventRecord(e1, st);
+    if (dbg_host) fprintf(stderr, "az_solve host: sketch issued +%.2f ms\n", hnow() - th0);
     if (!w.wide) {
       AZ_TRY(az_qr_r_impl(w.S, rows, kt, rows, w.Rf, kt, w.qrws, w.qrbytes, st, kp));
     } else {
@@ -291,6 +302,7 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
       AZ_LAUNCH_CHECK();
     }
     cudaEventRecord(e2, st);
+    if (dbg_host) fprintf(stderr, "az_solve host: qr issued +%.2f ms\n", hnow() - th0);
     bool full_svd = true;
     if (w.wide && nb >= 2 && nb < max_blocks) {
       // Cheap saturation pre-test (reading R5): with R_b = [[R11, R12], [0, R22]] and
@@ -312,27 +324,35 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
       rank = kp;   // not computed: treated as saturated unless the full SVD runs
     }
     if (full_svd) {
-      AZ_TRY(az_tsvd_impl(w.Rf, kt, kp, nrhs, theta, w.y, kp, w.sig, &rank, w.svdws, w.svdbytes, st));
-      double s1 = 0.0;
-      AZ_CUDA_CHECK(cudaMemcpyAsync(&s1, w.sig, sizeof(double), cudaMemcpyDeviceToHost, st));
-      AZ_CUDA_CHECK(cudaStreamSynchronize(st));
-      s1lo = std::max(s1lo, s1);
+      AZ_TRY(az_tsvd_impl(w.Rf, kt, kp, nrhs, theta, w.y, kp, w.sig, async_mode ? nullptr : &rank, w.svdws,
+                          w.svdbytes, st));
+      if (w.wide && nb < max_blocks) {   // sigma_1 lower bound for the next block's pre-test
+        double s1 = 0.0;
+        AZ_CUDA_CHECK(cudaMemcpyAsync(&s1, w.sig, sizeof(double), cudaMemcpyDeviceToHost, st));
+        AZ_CUDA_CHECK(cudaStreamSynchronize(st));
+        s1lo = std::max(s1lo, s1);
+      }
     }
     cudaEventRecord(e3, st);
-    cudaEventSynchronize(e3);
-    ms_sketch += ms_between(e0, e1);
-    ms_qr += ms_between(e1, e2);
-    ms_svd += ms_between(e2, e3);
-    saturated = rank > kp - pfix;
+    if (!async_mode) {
+      cudaEventSynchronize(e3);
+      ms_sketch += ms_between(e0, e1);
+      ms_qr += ms_between(e1, e2);
+      ms_svd += ms_between(e2, e3);
+    }
+    saturated = !async_mode && rank > kp - pfix;
     if (!saturated || nb == max_blocks) break;
   }
   if (nb > max_blocks) nb = max_blocks;
   const int64_t kp = nb * R;
+  if (dbg_host) fprintf(stderr, "az_solve host: svd issued +%.2f ms\n", hnow() - th0);
   cudaEventRecord(ev.e[6], st);
   // ---- x2 = Omega y ; x = x2 + Z* (b - A x2) ----
   AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, p->N, 0, st));
   AZ_TRY(step2(p, w.x2, b, ldb, x, ldx, w.tmp, nrhs, st));
   cudaEventRecord(ev.e[7], st);
+  if (dbg_host) fprintf(stderr, "az_solve host: all issued +%.2f ms\n", hnow() - th0);
+  if (async_mode) return AZ_OK;
   AZ_CUDA_CHECK(cudaEventSynchronize(ev.e[7]));
   if (report) {
     double sg[1] = {0};
@@ -666,5 +686,106 @@ extern "C" az_status_t az_solve_factored(az_factor_t f, const double* b, int64_t
     report->ms_step2 = ms_between(ev.e[2], ev.e[3]);
     report->ms_total = ms_between(ev.e[0], ev.e[3]);
   }
+  return AZ_OK;
+}
+
+// ==========================================================================================
+// Pipelined host-buffer solves: az_solve_host_pipelined enqueues H2D of b (upload stream),
+// the solve (caller's stream) and D2H of x (download stream) and returns; consecutive calls
+// overlap one step's upload and the previous step's download with the current solve (two device
+// slots).  x_host holds the result once az_plan_sync returns.  Host buffers should be pinned.
+// ==========================================================================================
+struct az_pipe_s {
+  cudaStream_t up = nullptr, down = nullptr;
+  double* bdev[2] = {nullptr, nullptr};
+  double* xdev[2] = {nullptr, nullptr};
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  cudaEvent_t ev_up[2], ev_solved[2], ev_down[2];
+  int slot = 0;
+  int64_t nrhs = 0, R = 0;
+  int32_t mb = 0;
+};
+
+static void pipe_free(az_pipe_s* q) {
+  if (!q) return;
+  if (q->up) cudaStreamSynchronize(q->up);
+  if (q->down) cudaStreamSynchronize(q->down);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(q->bdev[i]);
+    cudaFree(q->xdev[i]);
+    cudaEventDestroy(q->ev_up[i]);
+    cudaEventDestroy(q->ev_solved[i]);
+    cudaEventDestroy(q->ev_down[i]);
+  }
+  cudaFree(q->ws);
+  if (q->up) cudaStreamDestroy(q->up);
+  if (q->down) cudaStreamDestroy(q->down);
+  delete q;
+}
+
+void az_pipe_destroy(az_plan_s* p) {
+  pipe_free(p->pipe);
+  p->pipe = nullptr;
+}
+
+extern "C" az_status_t az_solve_host_pipelined(az_plan_t p, const double* b_host, double* x_host, int64_t nrhs,
+                                               double theta, int64_t R, int32_t max_blocks, void* stream) {
+  if (!p || !b_host || !x_host || nrhs < 1 || R < 1 || max_blocks < 1) {
+    az_set_error("az_solve_host_pipelined: bad arguments");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t rows = p->M + p->Mb;
+  az_pipe_s* q = p->pipe;
+  if (!q || q->nrhs != nrhs || q->R != R || q->mb != max_blocks) {
+    az_pipe_destroy(p);
+    q = new az_pipe_s();
+    p->pipe = q;
+    q->nrhs = nrhs;
+    q->R = R;
+    q->mb = max_blocks;
+    AZ_TRY(az_solve_workspace_size(p, nrhs, R, max_blocks, &q->ws_bytes));
+    bool ok = cudaStreamCreateWithFlags(&q->up, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&q->down, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaMalloc(&q->ws, q->ws_bytes) == cudaSuccess;
+    for (int i = 0; i < 2 && ok; ++i)
+      ok = cudaMalloc(&q->bdev[i], sizeof(double) * rows * nrhs) == cudaSuccess &&
+           cudaMalloc(&q->xdev[i], sizeof(double) * p->N * nrhs) == cudaSuccess &&
+           cudaEventCreateWithFlags(&q->ev_up[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&q->ev_solved[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&q->ev_down[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+      az_pipe_destroy(p);
+      az_set_error("az_solve_host_pipelined: out of device memory");
+      return AZ_ERR_OUT_OF_MEMORY;
+    }
+  }
+  const int sl = q->slot;
+  q->slot ^= 1;
+  // upload after the solve that last read this slot has finished
+  AZ_CUDA_CHECK(cudaStreamWaitEvent(q->up, q->ev_solved[sl], 0));
+  AZ_CUDA_CHECK(cudaMemcpyAsync(q->bdev[sl], b_host, sizeof(double) * rows * nrhs, cudaMemcpyHostToDevice, q->up));
+  AZ_CUDA_CHECK(cudaEventRecord(q->ev_up[sl], q->up));
+  // solve once the upload is in and the slot's previous result has been downloaded
+  AZ_CUDA_CHECK(cudaStreamWaitEvent(st, q->ev_up[sl], 0));
+  AZ_CUDA_CHECK(cudaStreamWaitEvent(st, q->ev_down[sl], 0));
+  az_status_t s = az_solve(p, q->bdev[sl], rows, q->xdev[sl], p->N, nrhs, theta, R, max_blocks, q->ws, q->ws_bytes,
+                           nullptr, stream);
+  if (s != AZ_OK && s != AZ_WARN_SKETCH_SATURATED) return s;
+  AZ_CUDA_CHECK(cudaEventRecord(q->ev_solved[sl], st));
+  AZ_CUDA_CHECK(cudaStreamWaitEvent(q->down, q->ev_solved[sl], 0));
+  AZ_CUDA_CHECK(cudaMemcpyAsync(x_host, q->xdev[sl], sizeof(double) * p->N * nrhs, cudaMemcpyDeviceToHost, q->down));
+  AZ_CUDA_CHECK(cudaEventRecord(q->ev_down[sl], q->down));
+  return s;
+}
+
+extern "C" az_status_t az_plan_sync(az_plan_t p) {
+  if (!p) return AZ_ERR_INVALID_ARGUMENT;
+  if (p->pipe) {
+    AZ_CUDA_CHECK(cudaStreamSynchronize(p->pipe->up));
+    AZ_CUDA_CHECK(cudaStreamSynchronize(p->pipe->down));
+  }
+  AZ_CUDA_CHECK(cudaDeviceSynchronize());
   return AZ_OK;
 }

@@ -175,3 +175,24 @@ def test_solve_sharded_nccl_world1_matches_az_solve(name, cfg, max_blocks):
             assert np.all(_approx_err(cfg, _host(xs), _host(x1), grid) <= 1e-8)
     finally:
         dist.destroy_process_group()
+
+
+def test_solve_host_pipelined_matches_solve():
+    """az_solve_host_pipelined (the e2e path): several enqueued host-buffer solves with different
+    right-hand sides, results after az_plan_sync equal to az_solve's (AZ is linear in b for a fixed
+    sketch; scaling b by a power of two scales every rounded operation exactly, so x(c b) = c x(b)
+    bitwise for c = 1, 2, -4)."""
+    from paper_2308_14490_b200 import api
+    cfg = I.make_config("interval", 4096, nrhs=6, R=40)
+    plan = api.Plan.from_config(cfg)
+    b = I.rhs(cfg)
+    x_ref, _ = plan.solve(_dev(b), 1e-12, cfg.R, 1)
+    x_ref = _host(x_ref)
+    cs = (1.0, 2.0, -4.0)
+    bs = [torch.from_numpy(np.asfortranarray(c * b)).t().contiguous().pin_memory().t() for c in cs]
+    xs = [torch.empty((cfg.nrhs, cfg.N), dtype=torch.float64).pin_memory().t() for _ in range(3)]
+    for bb, xx in zip(bs, xs):
+        api.solve_host_pipelined(plan, bb, xx, 1e-12, cfg.R, 1)
+    api.plan_sync(plan)
+    for c, xx in zip(cs, xs):
+        assert np.array_equal(xx.numpy(), c * x_ref)
