@@ -105,6 +105,9 @@ size_t az_qrw_ws_bytes(int64_t m, int64_t ncols_max);
 az_status_t az_qrw_apply(const double* V, int64_t ldv, int64_t m, const int64_t* pj0, const int* pnb,
                          const double* Tbuf, int64_t p0, int64_t p1, double* C, int64_t ldc, int64_t nt, void* ws,
                          size_t ws_bytes, cudaStream_t st);
+az_status_t az_qrw_apply_q(const double* V, int64_t ldv, int64_t m, const int64_t* pj0, const int* pnb,
+                           const double* Tbuf, int64_t p0, int64_t p1, double* C, int64_t ldc, int64_t nt, void* ws,
+                           size_t ws_bytes, cudaStream_t st);
 az_status_t az_qrw_factor(double* A, int64_t lda, int64_t m, int64_t c0, int64_t c1, double* Tbuf, int64_t* pj0,
                           int* pnb, int64_t* np, void* ws, size_t ws_bytes, cudaStream_t st);
 az_status_t az_qrw_extract_R(const double* A, int64_t lda, int64_t k, double* R, int64_t ldr, cudaStream_t st);

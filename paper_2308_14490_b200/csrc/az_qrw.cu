@@ -173,6 +173,7 @@ struct UpdArgs {
   double* Wpart;     // KC x QB x nt
   double* Wfin;      // QB x nt (column-major, ld QB)
   const double* T;   // QB x QB
+  int applyQ;        // 0: C <- Q^T C (W' = T^T W), 1: C <- Q C (W' = T W)
 };
 
 // Wpart[kc] = V^T C over rows [j0 + kc kchunk, ...): CTA tile 64 (panel cols) x 64 (target cols).
@@ -255,7 +256,10 @@ __global__ void __launch_bounds__(256) k_qr_wred(UpdArgs a, int KC) {
   __syncthreads();
   if (n < a.nt) {
     double t = 0.0;
-    for (int i = 0; i <= l; ++i) t = fma(Ts[l * QB + i], ws[g][i], t);   // (T^T)[l][i] = T[i][l]
+    if (!a.applyQ)
+      for (int i = 0; i <= l; ++i) t = fma(Ts[l * QB + i], ws[g][i], t);    // (T^T)[l][i] = T[i][l]
+    else
+      for (int i = l; i < QB; ++i) t = fma(Ts[i * QB + l], ws[g][i], t);    // T[l][i], i >= l
     a.Wfin[n * QB + l] = t;
   }
 }
@@ -440,9 +444,26 @@ size_t az_qrw_ws_bytes(int64_t m, int64_t ncols_max) {
 // Apply panels [p0, p1) of the factored matrix V (panel p = columns p QB ..) to the target columns.
 // Panel p starts at column pj0[p] (== its first active row) and has pnb[p] columns; its T is at
 // Tbuf + p QB^2.
+static az_status_t qrw_apply_dir(const double* V, int64_t ldv, int64_t m, const int64_t* pj0, const int* pnb,
+                                 const double* Tbuf, int64_t p0, int64_t p1, double* C, int64_t ldc, int64_t nt,
+                                 void* ws, size_t ws_bytes, cudaStream_t st, int applyQ);
+
 az_status_t az_qrw_apply(const double* V, int64_t ldv, int64_t m, const int64_t* pj0, const int* pnb,
                          const double* Tbuf, int64_t p0, int64_t p1, double* C, int64_t ldc, int64_t nt, void* ws,
                          size_t ws_bytes, cudaStream_t st) {
+  return qrw_apply_dir(V, ldv, m, pj0, pnb, Tbuf, p0, p1, C, ldc, nt, ws, ws_bytes, st, 0);
+}
+
+// C <- Q C with Q = H_(p0) ... H_(p1-1): panels in reverse order, W' = T W
+az_status_t az_qrw_apply_q(const double* V, int64_t ldv, int64_t m, const int64_t* pj0, const int* pnb,
+                           const double* Tbuf, int64_t p0, int64_t p1, double* C, int64_t ldc, int64_t nt, void* ws,
+                           size_t ws_bytes, cudaStream_t st) {
+  return qrw_apply_dir(V, ldv, m, pj0, pnb, Tbuf, p0, p1, C, ldc, nt, ws, ws_bytes, st, 1);
+}
+
+static az_status_t qrw_apply_dir(const double* V, int64_t ldv, int64_t m, const int64_t* pj0, const int* pnb,
+                                 const double* Tbuf, int64_t p0, int64_t p1, double* C, int64_t ldc, int64_t nt,
+                                 void* ws, size_t ws_bytes, cudaStream_t st, int applyQ) {
   if (nt <= 0) return AZ_OK;
   if (ws_bytes < az_qrw_ws_bytes(m, nt)) {
     az_set_error("az_qrw_apply: workspace too small");
@@ -450,8 +471,10 @@ az_status_t az_qrw_apply(const double* V, int64_t ldv, int64_t m, const int64_t*
   }
   const size_t ups = (size_t)(QB * UP_SA + 64 * UP_SB) * sizeof(double);
   AZ_CUDA_CHECK(az_smem_attr(k_qr_upd, ups));
-  for (int64_t p = p0; p < p1; ++p) {
+  for (int64_t pi = 0; pi < p1 - p0; ++pi) {
+    const int64_t p = applyQ ? p1 - 1 - pi : p0 + pi;
     UpdArgs u;
+    u.applyQ = applyQ;
     u.V = V;
     u.ldv = ldv;
     u.j0 = pj0[p];
@@ -461,7 +484,7 @@ az_status_t az_qrw_apply(const double* V, int64_t ldv, int64_t m, const int64_t*
     u.ldc = ldc;
     u.nt = nt;
     const int64_t rows = m - u.j0;
-    if (rows <= 0) break;
+    if (rows <= 0) continue;
     const int64_t KC = qrw_kc(rows);
     u.kchunk = (rows + KC - 1) / KC;
     u.Wpart = (double*)((char*)ws + qrw_part_bytes());   // (also the V^T V partials of k_qr_vtv)
@@ -541,6 +564,7 @@ az_status_t az_qrw_factor(double* A, int64_t lda, int64_t m, int64_t c0, int64_t
     // T of the whole QB panel from V^T V and the base taus
     {
       UpdArgs u;
+      u.applyQ = 0;
       u.V = A;
       u.ldv = lda;
       u.j0 = j0;

@@ -313,7 +313,7 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
       // skipped and another block is drawn (a possibly extra block, never a missing one).
       const int64_t off = (nb - 1) * R;
       int64_t k22 = 0;
-      AZ_TRY(az_tsvd_impl(w.Rf + off * kt + off, kt, R, 0, 0.0, w.y, R, w.sig, &k22, w.svdws, w.svdbytes, st));
+      AZ_TRY(az_tsvd_impl(w.Rf + off * kt + off, kt, R, 0, theta, w.y, R, w.sig, &k22, w.svdws, w.svdbytes, st));
       std::vector<double> s22(R);
       AZ_CUDA_CHECK(cudaMemcpyAsync(s22.data(), w.sig, sizeof(double) * R, cudaMemcpyDeviceToHost, st));
       AZ_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -537,7 +537,7 @@ extern "C" az_status_t az_factorize(az_plan_t p, double theta, int64_t R, int32_
     if (nb >= 2 && nb < max_blocks) {   // the R22 pre-test of az_solve (reading R5)
       const int64_t off = (nb - 1) * R;
       int64_t k22 = 0;
-      if ((s = az_tsvd_impl(Rf + off * kpmax + off, kpmax, R, 0, 0.0, f->P, R, sig, &k22, svdws, svdbytes, st)) != AZ_OK)
+      if ((s = az_tsvd_impl(Rf + off * kpmax + off, kpmax, R, 0, theta, f->P, R, sig, &k22, svdws, svdbytes, st)) != AZ_OK)
         return fail(s);
       std::vector<double> s22(R);
       if (cudaMemcpyAsync(s22.data(), sig, sizeof(double) * R, cudaMemcpyDeviceToHost, st) != cudaSuccess ||

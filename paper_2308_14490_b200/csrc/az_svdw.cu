@@ -435,8 +435,44 @@ extern "C" int az_debug_jacobi(int inner_sweeps) {   // returns the outer sweeps
   return g_last_sweeps;
 }
 
+// QR preconditioning (Drmac & Veselic): R_S^T = Q2 R2, R2^T = Q3 R3, so R_S = Q3 R3 Q2^T and
+// pinv(R_S) c = Q2 pinv(R3) (Q3^T c).  One-sided Jacobi on R3^T needs markedly fewer sweeps than on
+// R_S^T; the two extra QRs cost ~2.7 r^3 flops against 8 r^3 per sweep.  AZ_BJAC_PRECOND=0 disables.
+static bool bjac_precond() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AZ_BJAC_PRECOND");
+    v = (e && *e == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+static size_t tsvdw_pre_bytes(int64_t r, int64_t nrhs) {
+  if (!bjac_precond()) return 0;
+  const int64_t QBw = az_qrw_panel_width();
+  const int64_t np = (r + QBw - 1) / QBw;
+  return 2 * a256(sizeof(double) * r * r) + 2 * a256(sizeof(double) * np * QBw * QBw) +
+         a256(sizeof(double) * r * std::max<int64_t>(nrhs, 1)) + a256(az_qrw_ws_bytes(r, std::max<int64_t>(r, nrhs)));
+}
+
 size_t az_tsvdw_ws_bytes(int64_t r, int64_t nrhs) {
-  return a256(sizeof(double) * r * r) + a256(sizeof(double) * r * nrhs) + a256(sizeof(double) * r) + 1024;
+  return a256(sizeof(double) * r * r) + a256(sizeof(double) * r * nrhs) + a256(sizeof(double) * r) + 1024 +
+         tsvdw_pre_bytes(r, nrhs);
+}
+
+// dst (r x r, ld r) = upper triangle of src (ld lds) transposed: dst[i][j] = src[j][i] for j <= i
+__global__ void k_upper_T(const double* src, int64_t lds, int64_t r, double* dst) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= r * r) return;
+  const int64_t i = e % r, j = e / r;   // dst column j, row i
+  dst[j * r + i] = (j <= i) ? src[i * lds + j] : 0.0;
+}
+
+__global__ void k_copy_block(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  const int64_t i = e % rows, c = e / rows;
+  dst[c * ldd + i] = src[c * lds + i];
 }
 
 az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta, double* y,
@@ -456,22 +492,69 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
   double* smax2 = (double*)p;
   unsigned long long* off = (unsigned long long*)(p + 64);
   int64_t* d_rank = (int64_t*)(p + 128);
+  // ---- optional QR preconditioning ----
+  const bool pre = bjac_precond();
+  double *M2 = nullptr, *M3 = nullptr, *T2 = nullptr, *T3 = nullptr, *Z = nullptr;
+  void* qws = nullptr;
+  size_t qbytes = 0;
+  std::vector<int64_t> pj2, pj3;
+  std::vector<int> pn2, pn3;
+  int64_t np2 = 0, np3 = 0;
+  if (pre) {
+    const int64_t QBw = az_qrw_panel_width();
+    const int64_t npm = (r + QBw - 1) / QBw;
+    char* q = p + 1024;
+    auto take = [&](size_t bytes) {
+      char* ptr = q;
+      q += a256(bytes);
+      return ptr;
+    };
+    M2 = (double*)take(sizeof(double) * r * r);
+    M3 = (double*)take(sizeof(double) * r * r);
+    T2 = (double*)take(sizeof(double) * npm * QBw * QBw);
+    T3 = (double*)take(sizeof(double) * npm * QBw * QBw);
+    Z = (double*)take(sizeof(double) * r * std::max<int64_t>(nrhs, 1));
+    qbytes = az_qrw_ws_bytes(r, std::max<int64_t>(r, nrhs));
+    qws = take(qbytes);
+    pj2.resize(npm);
+    pj3.resize(npm);
+    pn2.resize(npm);
+    pn3.resize(npm);
+    AzTrace tr("bjac_precond", st, 2 * r * r * r);
+    k_upper_T<<<az_div_up(r * r, 256), 256, 0, st>>>(Rf, ldr, r, M2);                 // R_S^T
+    AZ_LAUNCH_CHECK();
+    AZ_TRY(az_qrw_factor(M2, r, r, 0, r, T2, pj2.data(), pn2.data(), &np2, qws, qbytes, st));   // = Q2 R2
+    k_upper_T<<<az_div_up(r * r, 256), 256, 0, st>>>(M2, r, r, M3);                    // R2^T
+    AZ_LAUNCH_CHECK();
+    AZ_TRY(az_qrw_factor(M3, r, r, 0, r, T3, pj3.data(), pn3.data(), &np3, qws, qbytes, st));   // = Q3 R3
+    if (nrhs > 0) {
+      k_copy_block<<<az_div_up(r * nrhs, 256), 256, 0, st>>>(Rf + r * ldr, ldr, C, r, r, nrhs);
+      AZ_LAUNCH_CHECK();
+      AZ_TRY(az_qrw_apply(M3, r, r, pj3.data(), pn3.data(), T3, 0, np3, C, r, nrhs, qws, qbytes, st));   // Q3^T c
+    }
+  }
   {
     AzTrace tr("bjac_load", st);
-    k_bjac_load<<<az_div_up(r * std::max<int64_t>(r, nrhs), 256), 256, 0, st>>>(Rf, ldr, r, (int)nrhs, B, C);
+    if (pre)   // B = R3^T; C already holds Q3^T c
+      k_bjac_load<<<az_div_up(r * r, 256), 256, 0, st>>>(M3, r, r, 0, B, C);
+    else
+      k_bjac_load<<<az_div_up(r * std::max<int64_t>(r, nrhs), 256), 256, 0, st>>>(Rf, ldr, r, (int)nrhs, B, C);
     AZ_LAUNCH_CHECK();
   }
   const int nblk = (int)((r + BW - 1) / BW);
   const int n = nblk + (nblk & 1);
   const size_t smem = (size_t)(PW * GS + PW * VS + PW * XS + 64 * XS) * sizeof(double);
   AZ_CUDA_CHECK(az_smem_attr(k_bjac_round, smem));
-  // cluster size: enough CTAs per round to cover the SMs twice, each slice >= 256 rows
+  // cluster size: the largest power of two with all CTAs of a round in ONE wave (every wave pays
+  // the leader's eigensolver latency once), each slice >= 256 rows.  AZ_BJAC_CS overrides.
   int CS = 1;
   {
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    while (CS < 8 && (int64_t)(n / 2) * CS < 2 * sms && r / (2 * CS) >= 256) CS *= 2;
+    while (CS < 8 && (int64_t)(n / 2) * CS * 2 <= sms && r / (2 * CS) >= 256) CS *= 2;
+    if (const char* e = getenv("AZ_BJAC_CS"))
+      if (*e) CS = std::max(1, std::min(8, atoi(e)));
   }
   BJArgs a;
   a.B = B;
@@ -544,9 +627,15 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
   }
   if (nrhs > 0) {
     AzTrace tr("bjac_solve", st, 2 * r * r * nrhs);
+    // preconditioned: z = pinv(R3) (Q3^T c), then y = Q2 z
     k_bjac_solve<<<dim3(az_div_up(r, 256), az_div_up(nrhs, 32)), 256, 0, st>>>(B, C, nrm2, smax2, r, (int)nrhs,
-                                                                               theta, y, ldy);
+                                                                               theta, pre ? Z : y, pre ? r : ldy);
     AZ_LAUNCH_CHECK();
+    if (pre) {
+      k_copy_block<<<az_div_up(r * nrhs, 256), 256, 0, st>>>(Z, r, y, ldy, r, nrhs);
+      AZ_LAUNCH_CHECK();
+      AZ_TRY(az_qrw_apply_q(M2, r, r, pj2.data(), pn2.data(), T2, 0, np2, y, ldy, nrhs, qws, qbytes, st));
+    }
   }
   AZ_CUDA_CHECK(cudaMemsetAsync(d_rank, 0, sizeof(int64_t), st));
   k_bjac_sigma<<<az_div_up(r, 256), 256, 0, st>>>(nrm2, smax2, r, theta, sigma_out, d_rank);
