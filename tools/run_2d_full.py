@@ -37,6 +37,7 @@ x = x.cpu().numpy()
 out = {"config": name, "plan_s": t1 - t0, "solve_s": t2 - t1, "report": rep,
        "kernels_ms": {k: round(v[1], 3) for k, v in sorted(tr.items(), key=lambda kv: -kv[1][1])[:14]}}
 if "--factored" in sys.argv:
+    torch.cuda.empty_cache()          # the solve's workspace goes back to the driver for the factor
     torch.cuda.synchronize(); t3 = time.time()
     fac = api.Factor(plan, theta, cfg.R, mb)
     torch.cuda.synchronize(); t4 = time.time()
