@@ -111,6 +111,19 @@ az_status_t az_qrw_apply_q(const double* V, int64_t ldv, int64_t m, const int64_
 az_status_t az_qrw_factor(double* A, int64_t lda, int64_t m, int64_t c0, int64_t c1, double* Tbuf, int64_t* pj0,
                           int* pnb, int64_t* np, void* ws, size_t ws_bytes, cudaStream_t st);
 az_status_t az_qrw_extract_R(const double* A, int64_t lda, int64_t k, double* R, int64_t ldr, cudaStream_t st);
+// Q1 = Q [I_kp; 0] formed in place of the factored columns [0, kp) (LAPACK dorgqr order: panels
+// from the last to the first); every panel must start below kp and end at or before it
+az_status_t az_qrw_form_q(double* A, int64_t lda, int64_t m, const int64_t* pj0, const int* pnb, const double* Tbuf,
+                          int64_t np, int64_t kp, void* ws, size_t ws_bytes, cudaStream_t st);
+
+// growable device buffer on the virtual-memory API (az_vmm.cu); nullptr when unavailable
+struct az_vbuf_s;
+az_vbuf_s* az_vbuf_reserve(size_t max_bytes);
+void* az_vbuf_ptr(az_vbuf_s* v);
+bool az_vbuf_ensure(az_vbuf_s* v, size_t bytes);
+void az_vbuf_trim(az_vbuf_s* v, size_t bytes);
+size_t az_vbuf_mapped(az_vbuf_s* v);
+void az_vbuf_free(az_vbuf_s* v);
 size_t az_tsvdw_ws_bytes(int64_t r, int64_t nrhs);
 az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta, double* y,
                           int64_t ldy, double* sigma_out, int64_t* rank_out, void* ws, size_t ws_bytes,

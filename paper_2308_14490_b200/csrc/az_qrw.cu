@@ -589,6 +589,96 @@ az_status_t az_qrw_factor(double* A, int64_t lda, int64_t m, int64_t c0, int64_t
   return AZ_OK;
 }
 
+// ------------------------------------------------------------------------------------------
+// Explicit Q1 in place (dorgqr): with the panels after p already turned into columns of Q, panel p
+// is applied to them (rows j0.. of those columns are zero above their own panel start) and its own
+// columns become  H_p [I; 0] = [I; 0] - V (T V_top^T)  (V_top = the unit-lower nb x nb top of V):
+// row r of the result needs only row r of V, so it overwrites V in place; rows < j0 become zero.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_qr_orgm(const double* A, int64_t lda, int64_t j0, int nb, const double* T,
+                                                 double* M) {
+  // M[l][c] = sum_i T[l][i] V_top[c][i]  (T column-major QB x QB; M column-major QB x QB)
+  for (int e = threadIdx.x; e < QB * QB; e += blockDim.x) {
+    const int l = e % QB, c = e / QB;
+    double t = 0.0;
+    if (l < nb && c < nb)
+      for (int i = l; i <= c && i < nb; ++i) {   // T upper (i >= l), V_top[c][i] nonzero for i <= c
+        const double vt = (i == c) ? 1.0 : A[(j0 + i) * lda + j0 + c];
+        t = fma(T[i * QB + l], vt, t);
+      }
+    M[c * QB + l] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_qr_orgrows(double* A, int64_t lda, int64_t m, int64_t j0, int nb,
+                                                    const double* M) {
+  __shared__ double Vs[32][QB + 1];
+  const double* Ms = M;     // 32 KB, warp-uniform reads: served from L1
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t r = j0 + (int64_t)blockIdx.x * 32 + lane;
+  for (int l = w; l < nb; l += 8) {
+    double v = 0.0;
+    if (r < m) v = (r - j0 == l) ? 1.0 : (r - j0 > l ? A[(j0 + l) * lda + r] : 0.0);
+    Vs[lane][l] = v;
+  }
+  __syncthreads();
+  double acc[QB / 8];
+#pragma unroll
+  for (int t = 0; t < QB / 8; ++t) acc[t] = 0.0;
+  for (int l = 0; l < nb; ++l) {
+    const double v = Vs[lane][l];
+#pragma unroll
+    for (int t = 0; t < QB / 8; ++t) acc[t] = fma(v, __ldg(Ms + (w + 8 * t) * QB + l), acc[t]);
+  }
+  if (r < m) {
+#pragma unroll
+    for (int t = 0; t < QB / 8; ++t) {
+      const int c = w + 8 * t;
+      if (c < nb) A[(j0 + c) * lda + r] = ((r - j0 == c) ? 1.0 : 0.0) - acc[t];
+    }
+  }
+}
+
+az_status_t az_qrw_form_q(double* A, int64_t lda, int64_t m, const int64_t* pj0, const int* pnb, const double* Tbuf,
+                          int64_t np, int64_t kp, void* ws, size_t ws_bytes, cudaStream_t st) {
+  int64_t npk = 0;
+  while (npk < np && pj0[npk] < kp) ++npk;
+  for (int64_t p = 0; p < npk; ++p)
+    if (pj0[p] + pnb[p] > kp || (p > 0 && pj0[p] != pj0[p - 1] + pnb[p - 1]) || (p == 0 && pj0[0] != 0)) {
+      az_set_error("az_qrw_form_q: panels do not tile columns [0, %lld)", (long long)kp);
+      return AZ_ERR_NOT_SUPPORTED;
+    }
+  if (npk == 0 || pj0[npk - 1] + pnb[npk - 1] != kp) {
+    az_set_error("az_qrw_form_q: panels do not tile columns [0, %lld)", (long long)kp);
+    return AZ_ERR_NOT_SUPPORTED;
+  }
+  if (ws_bytes < az_qrw_ws_bytes(m, QB)) {
+    az_set_error("az_qrw_form_q: workspace too small");
+    return AZ_ERR_WORKSPACE;
+  }
+  // M lives in the first base-panel T slot of the workspace (unused outside az_qrw_factor)
+  double* M = (double*)((char*)ws + (((size_t)qrw_sms() * (1 + QB) * sizeof(double) + 255) & ~(size_t)255));
+  for (int64_t p = npk - 1; p >= 0; --p) {
+    const int64_t j0 = pj0[p];
+    const int nb = pnb[p];
+    const int64_t nt = kp - (j0 + nb);
+    // the trailing columns: a column block of at most ws-sized width at a time
+    for (int64_t c0 = 0; c0 < nt;) {
+      int64_t w = nt - c0;
+      while (w > QB && ws_bytes < az_qrw_ws_bytes(m, w)) w = (w + 1) / 2;
+      AZ_TRY(az_qrw_apply_q(A, lda, m, pj0, pnb, Tbuf, p, p + 1, A + (j0 + nb + c0) * lda, lda, w, ws, ws_bytes, st));
+      c0 += w;
+    }
+    AzTrace tr("qrw_orgqr", st, 2 * (m - j0) * nb * nb);
+    k_qr_orgm<<<1, 256, 0, st>>>(A, lda, j0, nb, Tbuf + p * QB * QB, M);
+    AZ_LAUNCH_CHECK();
+    k_qr_orgrows<<<az_div_up(m - j0, 32), 256, 0, st>>>(A, lda, m, j0, nb, M);
+    AZ_LAUNCH_CHECK();
+    if (j0 > 0) AZ_CUDA_CHECK(cudaMemset2DAsync(A + j0 * lda, lda * sizeof(double), 0, j0 * sizeof(double), nb, st));
+  }
+  return AZ_OK;
+}
+
 // R (k x k, upper; strict lower zeroed) out of the factored matrix.
 __global__ void k_qrw_extract_R(const double* A, int64_t lda, int64_t k, double* R, int64_t ldr) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

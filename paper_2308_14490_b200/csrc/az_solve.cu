@@ -424,6 +424,9 @@ struct az_factor_s {
   double* S = nullptr;     // rows x kpmax, factored in place
   double* Tb = nullptr;    // panel T factors
   double* P = nullptr;     // kp x kp (ld kpmax)
+  az_vbuf_s* Svb = nullptr;   // S's virtual range (physical HBM mapped per probe block), else cudaMalloc
+  double* Q1 = nullptr;    // explicit leading kp columns of Q (rows x kp): S's own columns, in place
+  double* Om = nullptr;    // explicit probes Omega (N x kp), the same Philox values as on the fly
   std::vector<int64_t> pj0;
   std::vector<int> pnb;
   int64_t np = 0;
@@ -437,9 +440,20 @@ __global__ void k_identity_cols(double* Rf, int64_t ld, int64_t k, int64_t col0)
   Rf[(col0 + c) * ld + i] = (i == c) ? 1.0 : 0.0;
 }
 
-// y (k x nrhs) = P (k x k, ld ldp) c (k x nrhs, ld ldc); 64 x 64 output tiles, FP64 FMA
-__global__ void __launch_bounds__(256) k_gemm_nn(const double* P, int64_t ldp, const double* c, int64_t ldc, double* y,
-                                                 int64_t ldy, int64_t k, int64_t nrhs) {
+// Omega[:, col0 .. col0 + ncols) explicitly (N x ncols, ld N): the probe generator of a1
+__global__ void k_omega_fill(int64_t N, int64_t col0, int64_t ncols, double* Om, uint64_t seed) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t npair = (N + 1) / 2;
+  if (e >= npair * ncols) return;
+  const int64_t m = e % npair, j = e / npair;
+  const double2 z = probe_pair((uint64_t)m, (uint64_t)(col0 + j), seed);
+  Om[j * N + 2 * m] = z.x;
+  if (2 * m + 1 < N) Om[j * N + 2 * m + 1] = z.y;
+}
+
+// Y (m x n) = A (m x k, ld lda) B (k x n, ld ldb), n <= 64 per grid column; 64 x 64 tiles, FP64 FMA
+__global__ void __launch_bounds__(256) k_gemm_mn(const double* A, int64_t lda, const double* Bm, int64_t ldb, double* Y,
+                                                 int64_t ldy, int64_t m, int64_t k, int64_t n) {
   __shared__ double As[16][65], Bs[16][65];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int64_t r0 = (int64_t)blockIdx.x * 64, c0 = (int64_t)blockIdx.y * 64;
@@ -447,9 +461,9 @@ __global__ void __launch_bounds__(256) k_gemm_nn(const double* P, int64_t ldp, c
   for (int64_t k0 = 0; k0 < k; k0 += 16) {
     for (int e = threadIdx.x; e < 16 * 64; e += 256) {
       const int kk = e / 64, rr = e % 64;
-      As[kk][rr] = (r0 + rr < k && k0 + kk < k) ? P[(k0 + kk) * ldp + r0 + rr] : 0.0;
+      As[kk][rr] = (r0 + rr < m && k0 + kk < k) ? A[(k0 + kk) * lda + r0 + rr] : 0.0;
       const int cc = e / 16, k2 = e % 16;
-      Bs[k2][cc] = (c0 + cc < nrhs && k0 + k2 < k) ? c[(c0 + cc) * ldc + k0 + k2] : 0.0;
+      Bs[k2][cc] = (c0 + cc < n && k0 + k2 < k) ? Bm[(c0 + cc) * ldb + k0 + k2] : 0.0;
     }
     __syncthreads();
 #pragma unroll
@@ -465,8 +479,190 @@ __global__ void __launch_bounds__(256) k_gemm_nn(const double* P, int64_t ldp, c
 #pragma unroll
     for (int bb = 0; bb < 4; ++bb) {
       const int64_t r = r0 + tx + 16 * a, cc = c0 + ty + 16 * bb;
-      if (r < k && cc < nrhs) y[cc * ldy + r] = acc[a][bb];
+      if (r < m && cc < n) Y[cc * ldy + r] = acc[a][bb];
     }
+}
+
+// Wpart[kc] (k x n) = A[rows of chunk kc]^T B[rows of chunk kc]: split-K over the m rows, 64 x 64
+// output tiles (A: m x k, B: m x n, column-major); FP64 FMA
+__global__ void __launch_bounds__(256) k_gemm_tn_part(const double* A, int64_t lda, const double* Bm, int64_t ldb,
+                                                      double* Wpart, int64_t m, int64_t k, int64_t n, int64_t kchunk) {
+  __shared__ double As[16][65], Bs[16][65];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t i0 = (int64_t)blockIdx.x * 64, c0 = (int64_t)blockIdx.y * 64;
+  const int64_t rb = (int64_t)blockIdx.z * kchunk, re = min(m, rb + kchunk);
+  double acc[4][4] = {};
+  for (int64_t q0 = rb; q0 < re; q0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+      const int rr = e % 16, cc = e / 16;
+      As[rr][cc] = (q0 + rr < re && i0 + cc < k) ? A[(i0 + cc) * lda + q0 + rr] : 0.0;
+      Bs[rr][cc] = (q0 + rr < re && c0 + cc < n) ? Bm[(c0 + cc) * ldb + q0 + rr] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int rr = 0; rr < 16; ++rr)
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) acc[a][bb] = fma(As[rr][tx + 16 * a], Bs[rr][ty + 16 * bb], acc[a][bb]);
+    __syncthreads();
+  }
+  double* W = Wpart + (int64_t)blockIdx.z * k * n;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb) {
+      const int64_t i = i0 + tx + 16 * a, cc = c0 + ty + 16 * bb;
+      if (i < k && cc < n) W[cc * k + i] = acc[a][bb];
+    }
+}
+
+// Memory-bound forms of the two factored-solve products for few right-hand sides (NR <= 8 per
+// pass): every element of the tall factor is read once per pass, the small operand is staged in
+// shared memory, and the split over the long dimension is summed in a fixed order (k_sum_parts).
+//
+// part[z][r][i] = sum_{q in row chunk z} A[q, i] B[q, r]      (A: m x k, B: m x NR, col-major)
+template <int NR>
+__global__ void __launch_bounds__(256, 2) k_tsgemv_tn(const double* A, int64_t lda, const double* Bm, int64_t ldb,
+                                                   double* part, int64_t m, int64_t k, int64_t nrhs_total, int rc) {
+  extern __shared__ double bs[];                 // rc x NR, column r at bs + r * rc
+  const int64_t q0 = (int64_t)blockIdx.y * rc;
+  const int rn = (int)(m - q0 < rc ? m - q0 : (int64_t)rc);
+  for (int e = threadIdx.x; e < rc * NR; e += 256) {
+    const int r = e / rc, q = e % rc;
+    bs[e] = q < rn ? Bm[(int64_t)r * ldb + q0 + q] : 0.0;
+  }
+  __syncthreads();
+  // a warp takes 4 columns at a time, so each staged b' value read from shared memory feeds 4
+  // loaded elements (one read per element would make the pass shared-memory bound at NR = 8)
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t cend = (k < (int64_t)blockIdx.x * 64 + 64 ? k : (int64_t)blockIdx.x * 64 + 64);
+  for (int64_t i0 = (int64_t)blockIdx.x * 64 + 4 * w; i0 < cend; i0 += 32) {
+    const double* a[4];
+    bool ok[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      ok[c] = i0 + c < cend;
+      a[c] = A + (ok[c] ? i0 + c : i0) * lda + q0;
+    }
+    double acc[4][NR];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) acc[c][r] = 0.0;
+    int q = lane;
+    for (; q + 3 * 32 < rn; q += 4 * 32) {
+      double v[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[u][c] = ok[c] ? __ldcs(a[c] + q + 32 * u) : 0.0;   // streamed once
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          const double bv = bs[r * rc + q + 32 * u];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[c][r] = fma(v[u][c], bv, acc[c][r]);
+        }
+    }
+    for (; q < rn; q += 32) {
+      double v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = ok[c] ? __ldcs(a[c] + q) : 0.0;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const double bv = bs[r * rc + q];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[c][r] = fma(v[c], bv, acc[c][r]);
+      }
+    }
+    // warp reduction of the V = 4 NRP partial sums by recursive halving: each step trades half of
+    // the values with the partner lane, so V - 1 + (5 - log2 V) shuffles instead of 5 V
+    constexpr int NRP = NR <= 1 ? 1 : NR <= 2 ? 2 : NR <= 4 ? 4 : 8, V = 4 * NRP;
+    constexpr int LV = V == 4 ? 2 : V == 8 ? 3 : V == 16 ? 4 : 5;
+    double vals[V];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int r = 0; r < NRP; ++r) vals[c * NRP + r] = r < NR ? acc[c][r] : 0.0;
+#pragma unroll
+    for (int t = 0; t < LV; ++t) {
+      const int sft = 16 >> t, h = V >> (t + 1);
+      const bool up = (lane & sft) != 0;
+#pragma unroll
+      for (int i = 0; i < h; ++i) {
+        const double send = up ? vals[i] : vals[i + h];
+        const double keep = up ? vals[i + h] : vals[i];
+        vals[i] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+      }
+    }
+#pragma unroll
+    for (int o = (16 >> LV); o > 0; o >>= 1) vals[0] += __shfl_xor_sync(0xffffffffu, vals[0], o);
+    if ((lane & ((32 >> LV) - 1)) == 0) {
+      const int idx = lane >> (5 - LV), c = idx / NRP, r = idx % NRP;
+      if (r < NR && ok[c]) part[((int64_t)blockIdx.y * nrhs_total + r) * k + i0 + c] = vals[0];
+    }
+  }
+}
+
+// part[z][r][j] = sum_{i in column chunk z} A[j, i] y[i, r]   (A: m x k col-major, y: k x NR)
+template <int NR>
+__global__ void __launch_bounds__(256) k_tsgemv_nn(const double* A, int64_t lda, const double* y, int64_t ldy,
+                                                   double* part, int64_t m, int64_t k, int64_t nrhs_total, int kc) {
+  extern __shared__ double ys[];                 // kc x NR, row i at ys + i * NR
+  const int64_t i0 = (int64_t)blockIdx.y * kc;
+  const int kn = (int)(k - i0 < kc ? k - i0 : (int64_t)kc);
+  for (int e = threadIdx.x; e < kc * NR; e += 256) {
+    const int i = e / NR, r = e % NR;
+    ys[e] = i < kn ? y[(int64_t)r * ldy + i0 + i] : 0.0;
+  }
+  __syncthreads();
+  const int64_t j0 = (int64_t)blockIdx.x * 512 + threadIdx.x;
+  const bool ok0 = j0 < m, ok1 = j0 + 256 < m;
+  double acc0[NR], acc1[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) acc0[r] = acc1[r] = 0.0;
+  const double* a = A + i0 * lda;
+  int i = 0;
+  for (; i + 4 <= kn; i += 4) {
+    double v0[4], v1[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      v0[u] = ok0 ? __ldcs(a + (int64_t)(i + u) * lda + j0) : 0.0;
+      v1[u] = ok1 ? __ldcs(a + (int64_t)(i + u) * lda + j0 + 256) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const double yy = ys[(i + u) * NR + r];
+        acc0[r] = fma(v0[u], yy, acc0[r]);
+        acc1[r] = fma(v1[u], yy, acc1[r]);
+      }
+  }
+  for (; i < kn; ++i) {
+    const double v0 = ok0 ? a[(int64_t)i * lda + j0] : 0.0, v1 = ok1 ? a[(int64_t)i * lda + j0 + 256] : 0.0;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      acc0[r] = fma(v0, ys[i * NR + r], acc0[r]);
+      acc1[r] = fma(v1, ys[i * NR + r], acc1[r]);
+    }
+  }
+  double* pz = part + (int64_t)blockIdx.y * nrhs_total * m;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    if (ok0) pz[r * m + j0] = acc0[r];
+    if (ok1) pz[r * m + j0 + 256] = acc1[r];
+  }
+}
+
+__global__ void k_sum_parts(const double* Wpart, int64_t KC, int64_t len, double* out, int64_t k, int64_t ldo) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= len) return;
+  double t = 0.0;
+  for (int64_t kc = 0; kc < KC; ++kc) t += Wpart[kc * len + e];   // fixed order
+  out[(e / k) * ldo + (e % k)] = t;
 }
 
 extern "C" az_status_t az_factorize(az_plan_t p, double theta, int64_t R, int32_t max_blocks, az_factor_t* out,
@@ -506,7 +702,11 @@ extern "C" az_status_t az_factorize(az_plan_t p, double theta, int64_t R, int32_
     az_factor_destroy(f);
     return s;
   };
-  if (cudaMalloc(&f->S, sizeof(double) * rows * kpmax) != cudaSuccess ||
+  // S grows by one probe block at a time: reserve the address range for kpmax columns and map HBM
+  // per block, so a factorisation that stops early never holds the unused tail
+  f->Svb = az_vbuf_reserve(sizeof(double) * rows * kpmax);
+  if (f->Svb) f->S = (double*)az_vbuf_ptr(f->Svb);
+  if ((!f->Svb && cudaMalloc(&f->S, sizeof(double) * rows * kpmax) != cudaSuccess) ||
       cudaMalloc(&f->Tb, sizeof(double) * maxpanels * QBw * QBw) != cudaSuccess ||
       cudaMalloc(&f->P, sizeof(double) * kpmax * kpmax) != cudaSuccess ||
       cudaMalloc(&Rf, sizeof(double) * kpmax * 2 * kpmax) != cudaSuccess ||
@@ -524,6 +724,10 @@ extern "C" az_status_t az_factorize(az_plan_t p, double theta, int64_t R, int32_
     const int64_t kp = nb * R;
     cudaEventRecord(ev.e[2], st);
     double* Snew = f->S + (nb - 1) * R * rows;
+    if (f->Svb && !az_vbuf_ensure(f->Svb, sizeof(double) * rows * kp)) {
+      az_set_error("az_factorize: out of device memory (probe block %lld)", (long long)nb);
+      return fail(AZ_ERR_OUT_OF_MEMORY);
+    }
     az_status_t s = az_sketch(p, (nb - 1) * R, R, Snew, rows, st);
     if (s != AZ_OK) return fail(s);
     cudaEventRecord(ev.e[3], st);
@@ -577,8 +781,36 @@ extern "C" az_status_t az_factorize(az_plan_t p, double theta, int64_t R, int32_
   f->saturated = saturated;
   cudaFree(Rf);
   cudaFree(sig);
-  cudaFree(qrws);
   cudaFree(svdws);
+  Rf = sig = nullptr;
+  svdws = nullptr;
+  // explicit Q1 = Q [I_kp; 0], formed in place of S's first kp columns (the panels' V and T are not
+  // needed afterwards), and Omega (N x kp): a factored solve then streams each once instead of
+  // re-applying every Householder panel and regenerating the probes.  S's unused tail is returned
+  // first; Omega is kept only if it fits, else it is regenerated per solve.
+  {
+    const char* fe = getenv("AZ_FACTOR_EXPLICIT");
+    if (!(fe && fe[0] == '0')) {
+      const int64_t kp = f->kp;
+      if (cudaStreamSynchronize(st) != cudaSuccess) return fail(AZ_ERR_CUDA);
+      if (f->Svb) az_vbuf_trim(f->Svb, sizeof(double) * rows * kp);
+      az_status_t s2 = az_qrw_form_q(f->S, rows, rows, f->pj0.data(), f->pnb.data(), f->Tb, f->np, kp, qrws, qrbytes, st);
+      if (s2 != AZ_OK) return fail(s2);
+      f->Q1 = f->S;
+      cudaFree(f->Tb);
+      f->Tb = nullptr;
+      if (cudaMalloc(&f->Om, sizeof(double) * p->N * kp) == cudaSuccess) {
+        AzTrace tr("omega_fill", st);
+        k_omega_fill<<<az_div_up(((p->N + 1) / 2) * kp, 256), 256, 0, st>>>(p->N, 0, kp, f->Om, p->seed);
+        if (cudaGetLastError() != cudaSuccess) return fail(AZ_ERR_CUDA);
+      } else {
+        cudaGetLastError();
+        f->Om = nullptr;
+      }
+      if (cudaStreamSynchronize(st) != cudaSuccess) return fail(AZ_ERR_CUDA);
+    }
+  }
+  cudaFree(qrws);
   if (report) {
     memset(report, 0, sizeof(*report));
     report->rank_used = f->rank;
@@ -597,9 +829,13 @@ extern "C" az_status_t az_factorize(az_plan_t p, double theta, int64_t R, int32_
 
 extern "C" az_status_t az_factor_destroy(az_factor_t f) {
   if (!f) return AZ_OK;
-  cudaFree(f->S);
+  if (f->Svb)
+    az_vbuf_free(f->Svb);
+  else
+    cudaFree(f->S);
   cudaFree(f->Tb);
   cudaFree(f->P);
+  cudaFree(f->Om);
   delete f;
   return AZ_OK;
 }
@@ -611,8 +847,64 @@ extern "C" az_status_t az_factor_query(az_factor_t f, int64_t* probes, int64_t* 
   return AZ_OK;
 }
 
+// the memory-bound tsgemv passes below this many right-hand sides, tiled FMA GEMMs above
+static bool fac_small(int64_t nrhs) { return nrhs <= 16; }      // Q1^T b'
+static bool fac_small_nn(int64_t nrhs) { return nrhs <= 40; }   // P c, Omega y
+
+static int nr_slots(int64_t nrhs) {
+  const int64_t r = std::min<int64_t>(8, nrhs);
+  return r <= 1 ? 1 : r <= 2 ? 2 : r <= 4 ? 4 : 8;
+}
+
+// split of the tsgemv_nn product Y (m x nrhs) = A (m x k) y: column chunk kc (y chunk staged in
+// <= 32 KB of shared memory), enough chunks to give ~4 CTAs per SM
+static int64_t nn_kc(int64_t m, int64_t k, int64_t nrhs) {
+  const int64_t zc = std::max<int64_t>(1, az_div_up(4 * 148, az_div_up(m, 512)));
+  return std::min<int64_t>(4096 / nr_slots(nrhs), std::max<int64_t>(32, az_div_up(az_div_up(k, zc), 32) * 32));
+}
+static int64_t nn_part_elems(int64_t m, int64_t k, int64_t nrhs) {
+  return fac_small_nn(nrhs) ? az_div_up(k, nn_kc(m, k, nrhs)) * m * nrhs : 0;
+}
+
+// Y (m x nrhs, ld ldo) = A (m x k, ld lda) y (k x nrhs, ld ldy)
+static az_status_t nn_product(const double* A, int64_t lda, int64_t m, int64_t k, const double* y, int64_t ldy,
+                              double* Y, int64_t ldo, int64_t nrhs, double* part, cudaStream_t st) {
+  if (!fac_small_nn(nrhs)) {
+    k_gemm_mn<<<dim3(az_div_up(m, 64), az_div_up(nrhs, 64)), 256, 0, st>>>(A, lda, y, ldy, Y, ldo, m, k, nrhs);
+    AZ_LAUNCH_CHECK();
+    return AZ_OK;
+  }
+  const int64_t kc = nn_kc(m, k, nrhs), KCn = az_div_up(k, kc);
+  for (int64_t g0 = 0; g0 < nrhs; g0 += 8) {
+    const int nr = (int)std::min<int64_t>(8, nrhs - g0);
+    const size_t smn = sizeof(double) * kc * nr;
+    const dim3 gn(az_div_up(m, 512), (unsigned)KCn);
+#define AZ_TSGEMV_NN(NR)                                                                                    \
+  case NR:                                                                                                  \
+    AZ_CUDA_CHECK(az_smem_attr(k_tsgemv_nn<NR>, smn));                                                      \
+    k_tsgemv_nn<NR><<<gn, 256, smn, st>>>(A, lda, y + g0 * ldy, ldy, part + g0 * m, m, k, nrhs, (int)kc); \
+    break;
+    switch (nr) {
+      AZ_TSGEMV_NN(1)
+      AZ_TSGEMV_NN(2)
+      AZ_TSGEMV_NN(3)
+      AZ_TSGEMV_NN(4)
+      AZ_TSGEMV_NN(5)
+      AZ_TSGEMV_NN(6)
+      AZ_TSGEMV_NN(7)
+      AZ_TSGEMV_NN(8)
+    }
+#undef AZ_TSGEMV_NN
+    AZ_LAUNCH_CHECK();
+  }
+  k_sum_parts<<<az_div_up(m * nrhs, 256), 256, 0, st>>>(part, KCn, m * nrhs, Y, m, ldo);
+  AZ_LAUNCH_CHECK();
+  return AZ_OK;
+}
+
 struct FacWS {
-  double *bp, *y, *x2, *tmp;
+  double *bp, *y, *x2, *tmp, *c, *part;
+  int64_t KC, rc, KCt;   // tiled split-K count; tsgemv row chunk and count
   void* qrws;
   size_t qrbytes, total;
 };
@@ -629,8 +921,15 @@ static FacWS fac_layout(az_factor_s* f, int64_t nrhs, char* base) {
   w.y = (double*)take(sizeof(double) * f->kp * nrhs);
   w.x2 = (double*)take(sizeof(double) * f->p->N * nrhs);
   w.tmp = (double*)take(sizeof(double) * f->rows * nrhs);
-  w.qrbytes = az_qrw_ws_bytes(f->rows, nrhs);
-  w.qrws = take(w.qrbytes);
+  w.c = (double*)take(sizeof(double) * f->kp * nrhs);
+  w.KC = std::max<int64_t>(1, std::min<int64_t>(64, f->rows / 4096));
+  w.rc = 8192 / nr_slots(nrhs);                        // 64 KB of staged b' per CTA
+  w.KCt = az_div_up(f->rows, w.rc);
+  const int64_t parts = std::max({(fac_small(nrhs) ? w.KCt : w.KC) * f->kp * nrhs,
+                                  nn_part_elems(f->kp, f->kp, nrhs), nn_part_elems(f->p->N, f->kp, nrhs)});
+  w.part = (double*)take(sizeof(double) * parts);
+  w.qrbytes = f->Q1 ? 0 : az_qrw_ws_bytes(f->rows, nrhs);
+  w.qrws = f->Q1 ? nullptr : take(w.qrbytes);
   w.total = off;
   return w;
 }
@@ -661,16 +960,64 @@ extern "C" az_status_t az_solve_factored(az_factor_t f, const double* b, int64_t
   cudaEventRecord(ev.e[0], st);
   AZ_TRY(az_apply_op(p, OP_RESID, b, ldb, w.bp, rows, nrhs, st));            // b' = (I - A Z*) b
   cudaEventRecord(ev.e[1], st);
-  AZ_TRY(az_qrw_apply(f->S, rows, rows, f->pj0.data(), f->pnb.data(), f->Tb, 0, f->np, w.bp, rows, nrhs, w.qrws,
-                      w.qrbytes, st));                                          // Q^T b'
-  {
-    AzTrace tr("factored_y", st, 2 * kp * kp * nrhs);
-    k_gemm_nn<<<dim3(az_div_up(kp, 64), az_div_up(nrhs, 64)), 256, 0, st>>>(f->P, f->kpmax, w.bp, rows, w.y, kp, kp,
-                                                                          nrhs);   // y = P (Q^T b')[:kp]
-    AZ_LAUNCH_CHECK();
+  if (!f->Q1) {
+    // compact form: Q^T b' through the Householder panels, y = P (Q^T b')[:kp], x2 = Omega y regenerated
+    AZ_TRY(az_qrw_apply(f->S, rows, rows, f->pj0.data(), f->pnb.data(), f->Tb, 0, f->np, w.bp, rows, nrhs, w.qrws,
+                        w.qrbytes, st));
+    {
+      AzTrace tr("factored_y", st, 2 * kp * kp * nrhs);
+      AZ_TRY(nn_product(f->P, f->kpmax, kp, kp, w.bp, rows, w.y, kp, nrhs, w.part, st));   // y = P (Q^T b')[:kp]
+    }
+    cudaEventRecord(ev.e[2], st);
+    AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, p->N, 0, st));
+  } else {
+    // c = Q1^T b' (split-K over the rows, ordered reduction), y = P c, x2 = Omega y
+    {
+    AzTrace tr("fac_qtb", st, sizeof(double) * (rows + kp) * kp);
+    if (fac_small(nrhs)) {
+      for (int64_t g0 = 0; g0 < nrhs; g0 += 8) {
+        const int nr = (int)std::min<int64_t>(8, nrhs - g0);
+        const size_t smt = sizeof(double) * w.rc * nr;
+        const dim3 gt(az_div_up(kp, 64), w.KCt);
+#define AZ_TSGEMV_TN(NR)                                                                                         \
+  case NR:                                                                                                       \
+    AZ_CUDA_CHECK(az_smem_attr(k_tsgemv_tn<NR>, smt));                                                           \
+    k_tsgemv_tn<NR><<<gt, 256, smt, st>>>(f->Q1, rows, w.bp + g0 * rows, rows, w.part + g0 * kp, rows, kp, nrhs, \
+                                          (int)w.rc);                                                           \
+    break;
+        switch (nr) {
+          AZ_TSGEMV_TN(1)
+          AZ_TSGEMV_TN(2)
+          AZ_TSGEMV_TN(3)
+          AZ_TSGEMV_TN(4)
+          AZ_TSGEMV_TN(5)
+          AZ_TSGEMV_TN(6)
+          AZ_TSGEMV_TN(7)
+          AZ_TSGEMV_TN(8)
+        }
+#undef AZ_TSGEMV_TN
+        AZ_LAUNCH_CHECK();
+      }
+      k_sum_parts<<<az_div_up(kp * nrhs, 256), 256, 0, st>>>(w.part, w.KCt, kp * nrhs, w.c, kp, kp);
+      AZ_LAUNCH_CHECK();
+    } else {
+      const int64_t kchunk = (rows + w.KC - 1) / w.KC;
+      k_gemm_tn_part<<<dim3(az_div_up(kp, 64), az_div_up(nrhs, 64), (unsigned)w.KC), 256, 0, st>>>(
+          f->Q1, rows, w.bp, rows, w.part, rows, kp, nrhs, kchunk);
+      AZ_LAUNCH_CHECK();
+      k_sum_parts<<<az_div_up(kp * nrhs, 256), 256, 0, st>>>(w.part, w.KC, kp * nrhs, w.c, kp, kp);
+      AZ_LAUNCH_CHECK();
+    }
+    AZ_TRY(nn_product(f->P, f->kpmax, kp, kp, w.c, kp, w.y, kp, nrhs, w.part, st));   // y = P c
+    }
+    cudaEventRecord(ev.e[2], st);
+    const int64_t N = p->N;
+    AzTrace tr2("fac_omega_y", st, sizeof(double) * N * kp);
+    if (!f->Om)
+      AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, N, 0, st));   // Omega did not fit: regenerated
+    else
+      AZ_TRY(nn_product(f->Om, N, N, kp, w.y, kp, w.x2, N, nrhs, w.part, st));
   }
-  cudaEventRecord(ev.e[2], st);
-  AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, p->N, 0, st));
   AZ_TRY(step2(p, w.x2, b, ldb, x, ldx, w.tmp, nrhs, st));
   cudaEventRecord(ev.e[3], st);
   AZ_CUDA_CHECK(cudaEventSynchronize(ev.e[3]));

@@ -1,0 +1,5 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_wide.py -m gpu -x -q -k "factor" > gpurun_out/pytest_fac.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_fac.log
+timeout 600 python tools/run_2d_full.py c4 16 --factored > gpurun_out/fac_c4.json 2> gpurun_out/fac_c4.err
+timeout 900 python tools/run_2d_full.py c3 16 --factored > gpurun_out/fac_c3.json 2> gpurun_out/fac_c3.err
+timeout 1200 python tools/run_2d_full.py c5 8 --factored > gpurun_out/fac_c5.json 2> gpurun_out/fac_c5.err

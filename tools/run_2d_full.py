@@ -28,12 +28,12 @@ theta = max(cfg.tol * 1e-2, 1e-12)
 torch.cuda.synchronize()
 t1 = time.time()
 api.trace_enable(True)
-x, rep = plan.solve(bd, theta, cfg.R, mb)
+x, rep = (None, {}) if "--fac-only" in sys.argv else plan.solve(bd, theta, cfg.R, mb)
 torch.cuda.synchronize()
 t2 = time.time()
 tr = api.trace_report()
 api.trace_enable(False)
-x = x.cpu().numpy()
+x = x.cpu().numpy() if x is not None else None
 out = {"config": name, "plan_s": t1 - t0, "solve_s": t2 - t1, "report": rep,
        "kernels_ms": {k: round(v[1], 3) for k, v in sorted(tr.items(), key=lambda kv: -kv[1][1])[:14]}}
 if "--factored" in sys.argv:
@@ -43,9 +43,32 @@ if "--factored" in sys.argv:
     torch.cuda.synchronize(); t4 = time.time()
     xf, _ = fac.solve(bd)
     torch.cuda.synchronize(); t5 = time.time()
-    xf, _ = fac.solve(bd)
+    api.trace_enable(True)
+    xf, frep = fac.solve(bd)
     torch.cuda.synchronize(); t6 = time.time()
-    out["factored"] = {"factorize_s": t4 - t3, "first_solve_s": t5 - t4, "solve_s": t6 - t5, "report": fac.report}
+    ftr = api.trace_report()
+    api.trace_enable(False)
+    # factored solves for several right-hand-side counts (the config's b tiled), CUDA-event timed
+    sweep = {}
+    for a in sys.argv:
+        if a.startswith("--fac-nrhs="):
+            for q in [int(v) for v in a.split("=")[1].split(",")]:
+                bq = api.colmajor(bd[:, [j % bd.shape[1] for j in range(q)]].contiguous())
+                fac.solve(bq)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                api.trace_enable(True)
+                e0.record()
+                for _ in range(3):
+                    fac.solve(bq)
+                e1.record(); torch.cuda.synchronize()
+                qtr = api.trace_report()
+                api.trace_enable(False)
+                gbs = {k: round(v[2] / (v[1] / 1e3) / 1e9, 1) for k, v in qtr.items() if k.startswith("fac_") and v[1] > 0}
+                sweep[q] = {"ms": e0.elapsed_time(e1) / 3, "GB/s": gbs,
+                            "kernels_ms": {k: round(v[1] / 3, 3) for k, v in sorted(qtr.items(), key=lambda kv: -kv[1][1])[:4]}}
+    out["factored"] = {"factorize_s": t4 - t3, "nrhs_sweep": sweep, "first_solve_s": t5 - t4, "solve_s": t6 - t5, "report": fac.report,
+                       "solve_report": frep,
+                       "kernels_ms": {k: round(v[1], 3) for k, v in sorted(ftr.items(), key=lambda kv: -kv[1][1])[:12]}}
 if "--check" in sys.argv:
     from oracle import az as OA
     grid = I.test_grid(cfg, 201)
