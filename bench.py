@@ -271,9 +271,15 @@ def run_ours(args, cfg):
             fev[i][1].record(stream)
         torch.cuda.synchronize()
         fms = sum(a.elapsed_time(bb) for a, bb in fev) / kf
+        api.trace_enable(True)
+        fac.solve(b, x=x, workspace=fws)
+        ftr = api.trace_report()
+        api.trace_enable(False)
         factored = {"solves_per_s": world * 1000.0 / fms, "ms_per_solve": fms, "ms_factorize": fe0.elapsed_time(fe1),
                     "probes": fac.report["probes"], "rank": fac.report["rank"],
-                    "note": "az_solve_factored: b', Q^T b' from the stored panels, y = P (Q^T b'), Omega y, step 2"}
+                    "kernels_ms": {k: round(v[1], 3) for k, v in sorted(ftr.items(), key=lambda kv: -kv[1][1])[:8]},
+                    "note": "az_solve_factored: b' = (I - A Z*) b, c = Q1^T b' (Q1 explicit, formed at factorisation), "
+                            "y = P c, x2 = Omega y (Omega stored), step 2"}
         fac.close()
         del fws
 

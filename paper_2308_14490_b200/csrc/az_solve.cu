@@ -922,7 +922,9 @@ static FacWS fac_layout(az_factor_s* f, int64_t nrhs, char* base) {
   w.x2 = (double*)take(sizeof(double) * f->p->N * nrhs);
   w.tmp = (double*)take(sizeof(double) * f->rows * nrhs);
   w.c = (double*)take(sizeof(double) * f->kp * nrhs);
-  w.KC = std::max<int64_t>(1, std::min<int64_t>(64, f->rows / 4096));
+  // tiled split-K: enough row chunks for ~2 CTAs per SM over the (kp / 64) x (nrhs / 64) output tiles
+  const int64_t tiles = (int64_t)az_div_up(f->kp, 64) * az_div_up(nrhs, 64);
+  w.KC = std::max<int64_t>(1, std::min<int64_t>(az_div_up(2 * 148, tiles), f->rows / 1024));
   w.rc = 8192 / nr_slots(nrhs);                        // 64 KB of staged b' per CTA
   w.KCt = az_div_up(f->rows, w.rc);
   const int64_t parts = std::max({(fac_small(nrhs) ? w.KCt : w.KC) * f->kp * nrhs,
