@@ -59,7 +59,7 @@ typedef enum {
 /* Plan descriptor.  Box [-T, T)^dim, n centres per axis c_j = -T + j 2T/n,
  * oversampled grid of L*n points per axis x_q = -T + q 2T/(L n).
  * Supported: dim = 1 with n a power of two in [16, 2^21]; dim = 2 with n a power of two in
- * [8, 1024]; L in {1, 2, 4} with L*n <= 2048 per 2-D axis. */
+ * [8, 1024] (and n_y, see below); L in {1, 2, 4} (2-D: L = 2) with L*n <= 2048 per 2-D axis. */
 typedef struct {
   int32_t dim;                 /* 1 or 2 */
   int64_t n;                   /* centres per axis (paper N, N^x = N^y) */
@@ -77,6 +77,11 @@ typedef struct {
   uint64_t seed;               /* Philox key of the probe matrix Omega */
   double k0sq;                 /* Helmholtz term: LAPLACIAN rows are alpha (Delta + k0^2) phi_j
                                   (PAPER.md:694-722 1-D ODE, 730-806 2-D; 0 = Poisson).  Ignored for VALUE. */
+  int64_t n_y;                 /* 2-D anisotropic boxes ("N = N^x N^y", 644-647): centres along y,
+                                  a power of two with n/2 <= n_y <= 2n and L*n_y <= 2048; 0 = n.  The box is
+                                  [-T, T) x [-T_y, T_y), centres c_j = (-T + jx 2T/n, -T_y + jy 2T_y/n_y),
+                                  column j = jx n_y + jy; the mask is (L n) x (L n_y), x outer.  Ignored in 1-D. */
+  double T_y;                  /* half-period along y (0 = T).  eps is one isotropic shape parameter. */
 } az_plan_desc_t;
 
 typedef struct {

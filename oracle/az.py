@@ -67,7 +67,7 @@ def make_problem(cfg: I.Config, backend: str = "fft", dense_A: Optional[np.ndarr
     Mb = cfg.n_boundary
     N = cfg.N
     sym = C.Symbol(cfg.dim, cfg.n, cfg.s, cfg.eps, cfg.T, cfg.row_op, alpha=cfg.row_scale, k0sq=cfg.k0sq,
-                   backend="ld" if backend == "dense" else "fft")
+                   backend="ld" if backend == "dense" else "fft", n_y=cfg.ny, T_y=cfg.Ty)
     ops = C.PeriodicOperators(sym, cfg.tol)
     Ab = None
     if Mb:
@@ -187,10 +187,10 @@ def evaluate(cfg: I.Config, x: np.ndarray, grid: I.TestGrid) -> np.ndarray:
         Phi = periodized(t[:, None] - c[js], cfg.eps, cfg.T, 0)
         return np.einsum("pw,pwr->pr", Phi, X[js])[grid.inside]
     Px = periodized(grid.axes[0][:, None] - c[None, :], cfg.eps, cfg.T, 0)
-    Py = periodized(grid.axes[1][:, None] - c[None, :], cfg.eps, cfg.T, 0)
+    Py = periodized(grid.axes[1][:, None] - I.center_axis(cfg, 1)[None, :], cfg.eps, cfg.Ty, 0)
     out = []
     for r in range(X.shape[1]):
-        F = Px @ X[:, r].reshape(cfg.n, cfg.n) @ Py.T
+        F = Px @ X[:, r].reshape(cfg.n, cfg.ny) @ Py.T
         out.append(F[grid.inside])
     return np.stack(out, axis=1)
 

@@ -131,34 +131,45 @@ def poisson_closed_form(eps: float, T: float, n: int, s: int, q_max: int = 8) ->
 # --------------------------------------------------------------------------------------
 
 class Symbol:
-    """Diagonals of B for a dim-d problem, shape (P, n^d) with P = s^d phases.
+    """Diagonals of B for a dim-d problem, shape (P, N) with P = s^d phases, N = n (1-D) or
+    N^x N^y (2-D; the y axis may have its own N^y and T^y, "N = N^x N^y").
 
     Phase p enumerates (p_x, p_y) row-major; frequency index (k_x, k_y) row-major.
     """
 
     def __init__(self, dim: int, n: int, s: int, eps: float, T: float, row_op: int,
                  alpha: float = 1.0, k0sq: float = 0.0, backend: str = "fft",
-                 diag_fn=None):
+                 diag_fn=None, n_y: int = 0, T_y: float = 0.0):
         self.dim, self.n, self.s, self.eps, self.T = dim, n, s, eps, T
+        self.ny, self.Ty = (n_y or n), (T_y or T)
         self.backend = backend
         dt = LD if backend == "ld" else np.float64
-        d0 = diagonals(kernel_samples(eps, T, n, s, 0, dt), backend) if diag_fn is None else diag_fn(0)
+
+        def axis_d(order, nn, TT, axis):
+            if diag_fn is not None:
+                return diag_fn(order) if axis == 0 or (nn, TT) == (n, T) else diag_fn(order, axis)
+            return diagonals(kernel_samples(eps, TT, nn, s, order, dt), backend)
+
+        d0 = axis_d(0, n, T, 0)
         if dim == 1:
             if row_op != 0:
-                d2 = diagonals(kernel_samples(eps, T, n, s, 2, dt), backend) if diag_fn is None else diag_fn(2)
+                d2 = axis_d(2, n, T, 0)
                 self.d = alpha * (d2 + k0sq * d0)          # 1-D ODE rows (PAPER.md:698), normalised
             else:
                 self.d = d0
         else:
+            ny = self.ny
+            d0y = axis_d(0, ny, self.Ty, 1)                # B^y: the y axis' own samples (N^y, T^y)
             if row_op == 0:
                 # B = B^x (x) B^y  (PAPER.md:577)
-                self.d = np.einsum("ak,bl->abkl", d0, d0).reshape(s * s, n * n)
+                self.d = np.einsum("ak,bl->abkl", d0, d0y).reshape(s * s, n * ny)
             else:
-                d2 = diagonals(kernel_samples(eps, T, n, s, 2, dt), backend) if diag_fn is None else diag_fn(2)
+                d2 = axis_d(2, n, T, 0)
+                d2y = axis_d(2, ny, self.Ty, 1)
                 # B = B2^x (x) B0^y + B0^x (x) B2^y + k0^2 B0^x (x) B0^y  (PAPER.md:796-801)
-                t = (np.einsum("ak,bl->abkl", d2, d0) + np.einsum("ak,bl->abkl", d0, d2)
-                     + k0sq * np.einsum("ak,bl->abkl", d0, d0))
-                self.d = alpha * t.reshape(s * s, n * n)
+                t = (np.einsum("ak,bl->abkl", d2, d0y) + np.einsum("ak,bl->abkl", d0, d2y)
+                     + k0sq * np.einsum("ak,bl->abkl", d0, d0y))
+                self.d = alpha * t.reshape(s * s, n * ny)
         self.sigma2 = (np.abs(self.d) ** 2).sum(axis=0)   # diag of B*B (PAPER.md:806)
 
     def pinv(self, rcond: float):
@@ -188,36 +199,38 @@ def _F_axis(x: np.ndarray, axis: int, backend: str, inverse: bool) -> np.ndarray
     return np.moveaxis(xm @ M.T, -1, axis)
 
 
-def _to_phases(g: np.ndarray, dim: int, n: int, s: int) -> np.ndarray:
-    """Pi (per axis) on a natural-order grid vector: returns (P, n^d) phase blocks."""
+def _to_phases(g: np.ndarray, dim: int, n: int, s: int, ny: int = 0) -> np.ndarray:
+    """Pi (per axis) on a natural-order grid vector: returns (P, N) phase blocks."""
     if dim == 1:
         return g.reshape(n, s).T.copy()
-    G = g.reshape(n, s, n, s)               # [k_x, p_x, k_y, p_y]
-    return G.transpose(1, 3, 0, 2).reshape(s * s, n * n).copy()
+    ny = ny or n
+    G = g.reshape(n, s, ny, s)              # [k_x, p_x, k_y, p_y]
+    return G.transpose(1, 3, 0, 2).reshape(s * s, n * ny).copy()
 
 
-def _from_phases(c: np.ndarray, dim: int, n: int, s: int) -> np.ndarray:
-    """Pi^T: (P, n^d) phase blocks back to the natural-order grid vector."""
+def _from_phases(c: np.ndarray, dim: int, n: int, s: int, ny: int = 0) -> np.ndarray:
+    """Pi^T: (P, N) phase blocks back to the natural-order grid vector."""
     if dim == 1:
         return c.T.reshape(-1).copy()
-    G = c.reshape(s, s, n, n).transpose(2, 0, 3, 1)
+    ny = ny or n
+    G = c.reshape(s, s, n, ny).transpose(2, 0, 3, 1)
     return G.reshape(-1).copy()
 
 
-def _F_coeff(a: np.ndarray, dim: int, n: int, backend: str, inverse: bool) -> np.ndarray:
+def _F_coeff(a: np.ndarray, dim: int, n: int, backend: str, inverse: bool, ny: int = 0) -> np.ndarray:
     if dim == 1:
         return _F_axis(a, 0, backend, inverse)
-    A = a.reshape(n, n)
+    A = a.reshape(n, ny or n)
     A = _F_axis(A, 0, backend, inverse)
     A = _F_axis(A, 1, backend, inverse)
     return A.reshape(-1)
 
 
-def _P_blocks(c: np.ndarray, dim: int, n: int, backend: str, inverse: bool) -> np.ndarray:
+def _P_blocks(c: np.ndarray, dim: int, n: int, backend: str, inverse: bool, ny: int = 0) -> np.ndarray:
     """P = blockdiag(F*) (inverse=True) or P* = blockdiag(F) (inverse=False), per phase block."""
     if dim == 1:
         return _F_axis(c, 1, backend, inverse)
-    C = c.reshape(c.shape[0], n, n)
+    C = c.reshape(c.shape[0], n, ny or n)
     C = _F_axis(C, 1, backend, inverse)
     C = _F_axis(C, 2, backend, inverse)
     return C.reshape(c.shape[0], -1)
@@ -230,20 +243,21 @@ class PeriodicOperators:
         self.sym = sym
         self.dt, self.n_dropped = sym.pinv(rcond)
         self.dim, self.n, self.s, self.backend = sym.dim, sym.n, sym.s, sym.backend
+        self.ny = sym.ny
 
     def apply_Ac(self, a: np.ndarray) -> np.ndarray:
         """A^c a = Pi^T P* B F* a  (natural-order full grid output)."""
-        y = _F_coeff(a, self.dim, self.n, self.backend, inverse=True)          # F* a
-        c = self.sym.d * y[None, :]                                           # B
-        c = _P_blocks(c, self.dim, self.n, self.backend, inverse=False)        # P*
-        return _from_phases(c, self.dim, self.n, self.s)                      # Pi^T
+        y = _F_coeff(a, self.dim, self.n, self.backend, inverse=True, ny=self.ny)        # F* a
+        c = self.sym.d * y[None, :]                                                     # B
+        c = _P_blocks(c, self.dim, self.n, self.backend, inverse=False, ny=self.ny)      # P*
+        return _from_phases(c, self.dim, self.n, self.s, ny=self.ny)                    # Pi^T
 
     def apply_Zstar_grid(self, g: np.ndarray) -> np.ndarray:
         """Z* restricted to a grid vector already extended by zeros (E applied): F B^dag P Pi g."""
-        c = _to_phases(g, self.dim, self.n, self.s)                           # Pi
-        c = _P_blocks(c, self.dim, self.n, self.backend, inverse=True)         # P
-        y = (self.dt * c).sum(axis=0)                                         # B^dag
-        return _F_coeff(y, self.dim, self.n, self.backend, inverse=False)     # F
+        c = _to_phases(g, self.dim, self.n, self.s, ny=self.ny)                         # Pi
+        c = _P_blocks(c, self.dim, self.n, self.backend, inverse=True, ny=self.ny)       # P
+        y = (self.dt * c).sum(axis=0)                                                   # B^dag
+        return _F_coeff(y, self.dim, self.n, self.backend, inverse=False, ny=self.ny)   # F
 
     def zstar_norm(self) -> float:
         """||Z*||_2 = 1 / (smallest kept singular value of A^c) (unitary F, P)."""

@@ -30,6 +30,7 @@ def assemble_rows(cfg: I.Config, pts: np.ndarray, kind: str) -> np.ndarray:
     """
     c = I.center_axis(cfg)
     eps, T = cfg.eps, cfg.T
+    cy, Ty = I.center_axis(cfg, 1), cfg.Ty          # 2-D: the y axis has its own centres and period
     if cfg.dim == 1:
         pts = np.asarray(pts, dtype=np.float64)
         if pts.ndim == 2:          # (m, 1) boundary points
@@ -38,12 +39,12 @@ def assemble_rows(cfg: I.Config, pts: np.ndarray, kind: str) -> np.ndarray:
             return _Phi(pts, c, eps, T, 0)
         return cfg.row_scale * (_Phi(pts, c, eps, T, 2) + cfg.k0sq * _Phi(pts, c, eps, T, 0))
     X0 = _Phi(pts[:, 0], c, eps, T, 0)
-    Y0 = _Phi(pts[:, 1], c, eps, T, 0)
+    Y0 = _Phi(pts[:, 1], cy, eps, Ty, 0)
     if kind == "value":
-        # entry (i, jx*n + jy) = phi(x_i - c_jx) phi(y_i - c_jy)
+        # entry (i, jx*n_y + jy) = phi(x_i - c_jx) phi(y_i - c_jy)
         return (X0[:, :, None] * Y0[:, None, :]).reshape(pts.shape[0], -1)
     X2 = _Phi(pts[:, 0], c, eps, T, 2)
-    Y2 = _Phi(pts[:, 1], c, eps, T, 2)
+    Y2 = _Phi(pts[:, 1], cy, eps, Ty, 2)
     L = X2[:, :, None] * Y0[:, None, :] + X0[:, :, None] * Y2[:, None, :]
     if cfg.k0sq:
         L = L + cfg.k0sq * (X0[:, :, None] * Y0[:, None, :])
@@ -66,7 +67,7 @@ def assemble_Ac(cfg: I.Config) -> np.ndarray:
     kind = "laplacian" if cfg.row_op == I.ROW_LAPLACIAN else "value"
     if cfg.dim == 1:
         return assemble_rows(cfg, g, kind)
-    X, Y = np.meshgrid(g, g, indexing="ij")
+    X, Y = np.meshgrid(g, I.grid_axis(cfg, 1), indexing="ij")
     return assemble_rows(cfg, np.stack([X.ravel(), Y.ravel()], axis=1), kind)
 
 
@@ -96,16 +97,17 @@ def A_row_entries(cfg: I.Config, i_grid, half_width: int = 40):
             vals = cfg.row_scale * (vals + cfg.k0sq * periodized(g[q] - c[js], cfg.eps, cfg.T, 0))
         return js, vals
     qx, qy = i_grid
+    ny, gy, cy, Ty = cfg.ny, I.grid_axis(cfg, 1), I.center_axis(cfg, 1), cfg.Ty
     jx = np.unique(np.arange(qx // s - half_width, qx // s + half_width + 1) % n)
-    jy = np.unique(np.arange(qy // s - half_width, qy // s + half_width + 1) % n)
+    jy = np.unique(np.arange(qy // s - half_width, qy // s + half_width + 1) % ny)
     x0 = periodized(g[qx] - c[jx], cfg.eps, cfg.T, 0)
-    y0 = periodized(g[qy] - c[jy], cfg.eps, cfg.T, 0)
+    y0 = periodized(gy[qy] - cy[jy], cfg.eps, Ty, 0)
     if kind:
         x2 = periodized(g[qx] - c[jx], cfg.eps, cfg.T, 2)
-        y2 = periodized(g[qy] - c[jy], cfg.eps, cfg.T, 2)
+        y2 = periodized(gy[qy] - cy[jy], cfg.eps, Ty, 2)
         V = cfg.row_scale * (x2[:, None] * y0[None, :] + x0[:, None] * y2[None, :]
                              + cfg.k0sq * x0[:, None] * y0[None, :])
     else:
         V = x0[:, None] * y0[None, :]
-    cols = (jx[:, None] * n + jy[None, :]).ravel()
+    cols = (jx[:, None] * ny + jy[None, :]).ravel()
     return cols, V.ravel()

@@ -52,7 +52,7 @@ class Plan:
     def __init__(self, *, dim: int, n: int, L: int, T: float, eps: float, op: int = 0,
                  row_scale: float = 1.0, mask: np.ndarray, boundary_xy: Optional[np.ndarray] = None,
                  boundary_weight: float = 0.0, zstar_rcond: float = 1e-10, seed: int = 0, k0sq: float = 0.0,
-                 stream=None):
+                 n_y: int = 0, T_y: float = 0.0, stream=None):
         self._mask = np.ascontiguousarray(mask, dtype=np.uint8)
         bxy = np.zeros((0, 2)) if boundary_xy is None else boundary_xy
         self._bxy = np.ascontiguousarray(bxy, dtype=np.float64)
@@ -60,6 +60,7 @@ class Plan:
         d.dim, d.n, d.L, d.T, d.eps = dim, n, L, T, eps
         d.op, d.row_scale = op, row_scale
         d.k0sq = k0sq
+        d.n_y, d.T_y = n_y, T_y
         d.mask = self._mask.ctypes.data
         d.n_boundary = self._bxy.shape[0]
         d.boundary_xy = self._bxy.ctypes.data if self._bxy.shape[0] else None
@@ -84,7 +85,8 @@ class Plan:
                    row_scale=cfg.row_scale, mask=I.mask(cfg).reshape(-1),
                    boundary_xy=I.boundary_points(cfg) if cfg.n_boundary else None,
                    boundary_weight=cfg.boundary_weight, zstar_rcond=cfg.tol, seed=cfg.seed,
-                   k0sq=getattr(cfg, "k0sq", 0.0), stream=stream)
+                   k0sq=getattr(cfg, "k0sq", 0.0), n_y=cfg.n_y if cfg.dim == 2 else 0,
+                   T_y=cfg.T_y if cfg.dim == 2 else 0.0, stream=stream)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -25,10 +25,12 @@ void az_pipe_destroy(struct az_plan_s* p);
 struct az_plan_s {
   // geometry
   int dim;
-  int64_t n, s, L;          // L = s n grid points per axis
-  int64_t N, G;             // n^dim, L^dim
+  int64_t n, s, L;          // L = s n grid points per axis (2-D: the x axis)
+  int64_t ny = 0, Ly = 0;   // 2-D: centres / grid points along y (== n, L for square boxes)
+  int64_t N, G;             // n (1-D) or n ny; L (1-D) or L Ly
   int64_t M, Mb;
   double T, eps, alpha, beta, rcond;
+  double Ty = 0.0;          // 2-D: half-period along y
   double k0sq = 0.0;            // Helmholtz term of LAPLACIAN rows
   uint64_t seed;
   int op;
@@ -42,6 +44,8 @@ struct az_plan_s {
                                 // (1-D intervals): row = g - run0, no table lookups
   cplx* d_W0 = nullptr;         // fine symbol, order 0 (per axis length L; four-step: [N1][L2])
   cplx* d_W2 = nullptr;         // fine symbol, order 2 (Laplacian)
+  cplx* d_W0y = nullptr;        // 2-D: the y axis' symbols (alias d_W0 / d_W2 when the box is square)
+  cplx* d_W2y = nullptr;
   double* d_Wr = nullptr;       // four-step layout: the row symbol (W0, or alpha W2) as a real table
                                 // (phi^per samples are real and even, so W is real up to rounding)
   double* d_zinv = nullptr;     // N: 1/sigma^2(k) if kept else 0 (coefficient spectrum order)
@@ -49,7 +53,8 @@ struct az_plan_s {
   cplx* d_tw4hi = nullptr;      // four-step twiddles e^{-2 pi i (h 2^TW4B) / L}
   cplx* d_tw4lo = nullptr;      // e^{-2 pi i l / L}
   double* d_bxy = nullptr;      // Mb x 2 boundary points
-  int win = 0;                  // boundary stencil width (centres per axis), <= 64
+  int win = 0;                  // boundary stencil width (centres along x; 1-D: the axis), <= 64
+  int win_y = 0;                // 2-D: along y
   double* d_bw = nullptr;       // Mb x 2 x 64 separable stencil weights phi^per(x_b - c_j)
   int32_t* d_bj = nullptr;      // Mb x 2 first centre index of the window (mod n on use)
   // scratch for the pass kernels

@@ -27,6 +27,8 @@
 struct P2 {
   const cplx* W0;
   const cplx* W2;
+  const cplx* W0y;   // the y axis' symbols (== W0 / W2 for square boxes)
+  const cplx* W2y;
   const double* zinv;
   const int32_t* pos;
   const uint8_t* mask;
@@ -36,7 +38,8 @@ struct P2 {
   int lap;
   double k0sq;
   double alpha, beta, eps, T, h;
-  int n, s, L;
+  int n, s, L;      // x axis (the column passes)
+  int ny, Ly;       // y axis (the row passes, contiguous)
   int64_t M, Mb, N, GG;
   uint64_t seed;
   cplx* C1;
@@ -48,14 +51,14 @@ struct P2 {
   int64_t nvec;
   int64_t col0;
   int64_t pair0;
-  int win;        // boundary window half-width (centres per axis)
+  int win, win_y;   // boundary windows (centres along x / y)
 };
 
 // alpha (W2x W0y + W0x W2y + k0^2 W0x W0y) for LAPLACIAN / Helmholtz rows
 AZ_D cplx sym2(const P2& a, int kx, int ky) {
-  if (!a.lap) return cmul(a.W0[kx], a.W0[ky]);
-  const cplx w00 = cmul(a.W0[kx], a.W0[ky]);
-  return cscale(cadd(cadd(cmul(a.W2[kx], a.W0[ky]), cmul(a.W0[kx], a.W2[ky])), cscale(w00, a.k0sq)), a.alpha);
+  if (!a.lap) return cmul(a.W0[kx], a.W0y[ky]);
+  const cplx w00 = cmul(a.W0[kx], a.W0y[ky]);
+  return cscale(cadd(cadd(cmul(a.W2[kx], a.W0y[ky]), cmul(a.W0[kx], a.W2y[ky])), cscale(w00, a.k0sq)), a.alpha);
 }
 
 struct Cols {
@@ -96,7 +99,7 @@ __global__ void __launch_bounds__(256) k2_rows(P2 a, int nrows, double cout) {
       for (int e = j; e < LEN / 2; e += TPF) {
         cpair pr = {czero(), czero()};
         if (live) {
-          const int64_t i = (int64_t)row * a.n + 2 * e;
+          const int64_t i = (int64_t)row * a.ny + 2 * e;
           pr = probe_cplx_pair((uint64_t)(i >> 1), (uint64_t)(a.col0 + cc.cre), (uint64_t)(a.col0 + cc.cim),
                                cc.has_im, a.seed);
         }
@@ -107,7 +110,7 @@ __global__ void __launch_bounds__(256) k2_rows(P2 a, int nrows, double cout) {
       for (int e = j; e < LEN; e += TPF) {
         cplx v = czero();
         if (live) {
-          const int64_t i = (int64_t)row * a.n + e;
+          const int64_t i = (int64_t)row * a.ny + e;
           v.x = a.in[i + cc.cre * a.ldin];
           v.y = cc.has_im ? a.in[i + cc.cim * a.ldin] : 0.0;
         }
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(256) k2_rows(P2 a, int nrows, double cout) {
     for (int e = j; e < LEN; e += TPF) {
       cplx v = czero();
       if (live) {
-        const int r = a.pos[(int64_t)row * a.L + e];
+        const int r = a.pos[(int64_t)row * a.Ly + e];
         if (r >= 0) {
           v.x = a.in[r + cc.cre * a.ldin];
           v.y = cc.has_im ? a.in[r + cc.cim * a.ldin] : 0.0;
@@ -127,9 +130,9 @@ __global__ void __launch_bounds__(256) k2_rows(P2 a, int nrows, double cout) {
       buf[spad(e)] = v;
     }
   } else if constexpr (KIND == RK_OUT_COEF || KIND == RK_COEF_W) {
-    for (int e = j; e < LEN; e += TPF) buf[spad(e)] = live ? C1b[(int64_t)row * a.n + e] : czero();
+    for (int e = j; e < LEN; e += TPF) buf[spad(e)] = live ? C1b[(int64_t)row * a.ny + e] : czero();
   } else {   // fine rows
-    for (int e = j; e < LEN; e += TPF) buf[spad(e)] = live ? Gb[(int64_t)row * a.L + e] : czero();
+    for (int e = j; e < LEN; e += TPF) buf[spad(e)] = live ? Gb[(int64_t)row * a.Ly + e] : czero();
   }
   __syncthreads();
 
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(256) k2_rows(P2 a, int nrows, double cout) {
   } else if constexpr (KIND == RK_FINE_MASK) {
     fft_smem<LEN, 1>(buf, j, a.tw, TWN);
     for (int e = j; e < LEN; e += TPF)
-      if (!live || !a.mask[(int64_t)row * a.L + e]) buf[spad(e)] = czero();
+      if (!live || !a.mask[(int64_t)row * a.Ly + e]) buf[spad(e)] = czero();
     __syncthreads();
     fft_smem<LEN, -1>(buf, j, a.tw, TWN);
   } else {
@@ -149,12 +152,12 @@ __global__ void __launch_bounds__(256) k2_rows(P2 a, int nrows, double cout) {
   if (!live) return;
   // ---- store ----
   if constexpr (KIND == RK_IN_COEF) {
-    for (int e = j; e < LEN; e += TPF) C1b[(int64_t)row * a.n + e] = buf[spad(e)];
+    for (int e = j; e < LEN; e += TPF) C1b[(int64_t)row * a.ny + e] = buf[spad(e)];
   } else if constexpr (KIND == RK_IN_ROWS || KIND == RK_FINE_MASK) {
-    for (int e = j; e < LEN; e += TPF) Gb[(int64_t)row * a.L + e] = buf[spad(e)];
+    for (int e = j; e < LEN; e += TPF) Gb[(int64_t)row * a.Ly + e] = buf[spad(e)];
   } else if constexpr (KIND == RK_OUT_GATHER || KIND == RK_OUT_RESID) {
     for (int e = j; e < LEN; e += TPF) {
-      const int r = a.pos[(int64_t)row * a.L + e];
+      const int r = a.pos[(int64_t)row * a.Ly + e];
       if (r >= 0) {
         const cplx v = buf[spad(e)];
         if constexpr (KIND == RK_OUT_RESID) {
@@ -168,13 +171,13 @@ __global__ void __launch_bounds__(256) k2_rows(P2 a, int nrows, double cout) {
     }
   } else if constexpr (KIND == RK_OUT_COEF) {
     for (int e = j; e < LEN; e += TPF) {
-      const int64_t i = (int64_t)row * a.n + e;
+      const int64_t i = (int64_t)row * a.ny + e;
       const cplx v = buf[spad(e)];
       a.out[i + cc.cre * a.ldout] = v.x * cout;
       if (cc.has_im) a.out[i + cc.cim * a.ldout] = v.y * cout;
     }
   } else {   // RK_COEF_W: spatial coefficients of the pair, kept in C1 for the boundary rows
-    for (int e = j; e < LEN; e += TPF) C1b[(int64_t)row * a.n + e] = cscale(buf[spad(e)], cout);
+    for (int e = j; e < LEN; e += TPF) C1b[(int64_t)row * a.ny + e] = cscale(buf[spad(e)], cout);
   }
 }
 
@@ -194,24 +197,25 @@ __global__ void __launch_bounds__(TC * NN / 8) k2_cols(P2 a) {
   const int f = tid / TPF, j = tid % TPF;
   const int b = blockIdx.y;
   const int c0 = blockIdx.x * TC;
-  const int n = NN, L = LL, s = LL / NN;
+  const int n = NN, s = LL / NN;        // x axis
+  const int ny = a.ny, Ly = a.Ly;       // y axis: row strides of the coefficient / fine arrays
   cplx* bufN = sm;
   cplx* bufL = sm + TC * PLN;
   cplx* C1b = a.C1 + (int64_t)b * a.N;
   cplx* Gb = a.G + (int64_t)b * a.GG;
-  const double cA = 1.0 / ((double)L * (double)L);
+  const double cA = 1.0 / ((double)LL * (double)Ly);
 
   if constexpr (KIND == CK_EXPAND || KIND == CK_EXPAND_KEEP) {
     for (int e = tid; e < NN * TC; e += NT) {
       const int row = e / TC, c = e % TC;
-      bufN[c * PLN + spad(row)] = C1b[(int64_t)row * n + c0 + c];
+      bufN[c * PLN + spad(row)] = C1b[(int64_t)row * ny + c0 + c];
     }
     __syncthreads();
     fft_smem<NN, -1>(bufN + f * PLN, j, a.tw, TWN);
     if constexpr (KIND == CK_EXPAND_KEEP) {
       for (int e = tid; e < NN * TC; e += NT) {
         const int row = e / TC, c = e % TC;
-        C1b[(int64_t)row * n + c0 + c] = bufN[c * PLN + spad(row)];
+        C1b[(int64_t)row * ny + c0 + c] = bufN[c * PLN + spad(row)];
       }
     }
   } else {
@@ -220,13 +224,13 @@ __global__ void __launch_bounds__(TC * NN / 8) k2_cols(P2 a) {
     for (int my = 0; my < s; ++my) {
       for (int e = tid; e < LL * TC; e += NT) {
         const int row = e / TC, c = e % TC;
-        bufL[c * PLL + spad(row)] = Gb[(int64_t)row * L + c0 + c + my * n];
+        bufL[c * PLL + spad(row)] = Gb[(int64_t)row * Ly + c0 + c + my * ny];
       }
       __syncthreads();
       fft_smem<LL, -1, TPF>(bufL + f * PLL, j, a.tw, TWN);
       for (int e = tid; e < NN * TC; e += NT) {
         const int kx = e / TC, c = e % TC;
-        const int kyf = c0 + c + my * n;
+        const int kyf = c0 + c + my * ny;
         cplx acc = bufN[c * PLN + spad(kx)];
         for (int mx = 0; mx < s; ++mx) {
           const int kxf = kx + mx * n;
@@ -238,7 +242,7 @@ __global__ void __launch_bounds__(TC * NN / 8) k2_cols(P2 a) {
     }
     for (int e = tid; e < NN * TC; e += NT) {
       const int kx = e / TC, c = e % TC;
-      const int64_t k = (int64_t)kx * n + c0 + c;
+      const int64_t k = (int64_t)kx * ny + c0 + c;
       cplx v = bufN[c * PLN + spad(kx)];
       if constexpr (KIND != CK_AT) v = cscale(v, a.zinv[k]);
       if constexpr (KIND == CK_STEP1) v = csub(C1b[k], v);       // r^ = v^ - w^
@@ -252,14 +256,14 @@ __global__ void __launch_bounds__(TC * NN / 8) k2_cols(P2 a) {
     for (int my = 0; my < s; ++my) {
       for (int e = tid; e < LL * TC; e += NT) {
         const int kxf = e / TC, c = e % TC;
-        const int kyf = c0 + c + my * n;
+        const int kyf = c0 + c + my * ny;
         bufL[c * PLL + spad(kxf)] = cscale(cmul(bufN[c * PLN + spad(kxf & (n - 1))], sym2(a, kxf, kyf)), cA);
       }
       __syncthreads();
       fft_smem<LL, 1, TPF>(bufL + f * PLL, j, a.tw, TWN);
       for (int e = tid; e < LL * TC; e += NT) {
         const int row = e / TC, c = e % TC;
-        Gb[(int64_t)row * L + c0 + c + my * n] = bufL[c * PLL + spad(row)];
+        Gb[(int64_t)row * Ly + c0 + c + my * ny] = bufL[c * PLL + spad(row)];
       }
       __syncthreads();
     }
@@ -268,7 +272,7 @@ __global__ void __launch_bounds__(TC * NN / 8) k2_cols(P2 a) {
     fft_smem<NN, 1>(bufN + f * PLN, j, a.tw, TWN);
     for (int e = tid; e < NN * TC; e += NT) {
       const int row = e / TC, c = e % TC;
-      C1b[(int64_t)row * n + c0 + c] = bufN[c * PLN + spad(row)];
+      C1b[(int64_t)row * ny + c0 + c] = bufN[c * PLN + spad(row)];
     }
   }
 }
@@ -283,17 +287,17 @@ __global__ void k2_boundary_rows(P2 a) {
   const int bp = blockIdx.x, b = blockIdx.y, lane = threadIdx.x;
   const Cols cc = pair_cols(a, b);
   const cplx* C1b = a.C1 + (int64_t)b * a.N;
-  const int n = a.n, W = a.win;
+  const int n = a.n, ny = a.ny, W = a.win, Wy = a.win_y;
   const double* wx = a.bw + (2 * bp) * 64;
   const double* wy = a.bw + (2 * bp + 1) * 64;
   const int jx0 = a.bj[2 * bp], jy0 = a.bj[2 * bp + 1];
   cplx acc = czero();
-  for (int l = lane; l < W; l += 32) {
-    const int jy = ((jy0 + l) % n + n) % n;
+  for (int l = lane; l < Wy; l += 32) {
+    const int jy = ((jy0 + l) % ny + ny) % ny;
     const double py = wy[l];
     for (int t = 0; t < W; ++t) {
       const int jx = ((jx0 + t) % n + n) % n;
-      const int64_t i = (int64_t)jx * n + jy;
+      const int64_t i = (int64_t)jx * ny + jy;
       cplx w;
       if (FROM_INPUT) {
         w.x = a.in[i + cc.cre * a.ldin];
@@ -325,20 +329,20 @@ __global__ void k2_boundary_rows(P2 a) {
 __global__ void k2_boundary_adjoint(P2 a) {
   const int bp = blockIdx.x, b = blockIdx.y, lane = threadIdx.x;
   const Cols cc = pair_cols(a, b);
-  const int n = a.n, W = a.win;
+  const int n = a.n, ny = a.ny, W = a.win, Wy = a.win_y;
   const double* wx = a.bw + (2 * bp) * 64;
   const double* wy = a.bw + (2 * bp + 1) * 64;
   const int jx0 = a.bj[2 * bp], jy0 = a.bj[2 * bp + 1];
   const int64_t r = a.M + bp;
   const double vre = a.beta * a.in[r + cc.cre * a.ldin];
   const double vim = cc.has_im ? a.beta * a.in[r + cc.cim * a.ldin] : 0.0;
-  for (int l = lane; l < W; l += 32) {
-    const int jy = ((jy0 + l) % n + n) % n;
+  for (int l = lane; l < Wy; l += 32) {
+    const int jy = ((jy0 + l) % ny + ny) % ny;
     const double py = wy[l];
     for (int t = 0; t < W; ++t) {
       const int jx = ((jx0 + t) % n + n) % n;
       const double w = wx[t] * py;
-      const int64_t i = (int64_t)jx * n + jy;
+      const int64_t i = (int64_t)jx * ny + jy;
       atomicAdd(&a.out[i + cc.cre * a.ldout], vre * w);
       if (cc.has_im) atomicAdd(&a.out[i + cc.cim * a.ldout], vim * w);
     }
@@ -363,26 +367,27 @@ static az_status_t rows(const P2& a, int nrows, int nb, double cout, cudaStream_
   return AZ_OK;
 }
 
-template <int NN, int KIND, int WANT_W>
+template <int NN, int NY, int KIND, int WANT_W>
 static az_status_t cols(const P2& a, int nb, cudaStream_t st) {
   constexpr int LL = 2 * NN;
   constexpr int TC0 = 2048 / NN;
-  constexpr int TC = TC0 < 2 ? 2 : (TC0 > NN ? NN : TC0);
+  constexpr int TC1 = TC0 < 2 ? 2 : (TC0 > NN ? NN : TC0);
+  constexpr int TC = TC1 > NY ? NY : TC1;   // adjacent y columns per CTA
   const size_t sm = (size_t)TC * (spad_len(NN) + spad_len(LL)) * sizeof(cplx);
   auto kern = k2_cols<NN, LL, TC, KIND, WANT_W>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   static const char* names[] = {"2d_cols_expand", "2d_cols_expand_keep", "2d_cols_step1", "2d_cols_resid",
                                 "2d_cols_zstar", "2d_cols_at"};
   AzTrace tr(names[KIND], st, nb);
-  kern<<<dim3(az_div_up(NN, TC), nb), TC * NN / 8, sm, st>>>(a);
+  kern<<<dim3(az_div_up(NY, TC), nb), TC * NN / 8, sm, st>>>(a);
   AZ_LAUNCH_CHECK();
   return AZ_OK;
 }
 
-template <int NN>
+template <int NN, int NY>
 static az_status_t run2d(const P2& a0, int op, int src, int64_t npairs, int64_t Bmax, cudaStream_t st) {
-  constexpr int LL = 2 * NN;
-  const double n2 = (double)NN * NN;
+  constexpr int LL = 2 * NN, LY = 2 * NY;   // x: column passes; y: row passes
+  const double n2 = (double)NN * NY;
   for (int64_t p0 = 0; p0 < npairs; p0 += Bmax) {
     P2 a = a0;
     a.pair0 = p0;
@@ -390,9 +395,9 @@ static az_status_t run2d(const P2& a0, int op, int src, int64_t npairs, int64_t 
     const bool bnd = a.Mb > 0;
     switch (op) {
       case OP_A:
-        AZ_TRY(rows<NN, RK_IN_COEF, SRC_VEC>(a, NN, nb, 1.0, st));
-        AZ_TRY((cols<NN, CK_EXPAND, 0>(a, nb, st)));
-        AZ_TRY(rows<LL, RK_OUT_GATHER, SRC_VEC>(a, LL, nb, 1.0, st));
+        AZ_TRY(rows<NY, RK_IN_COEF, SRC_VEC>(a, NN, nb, 1.0, st));
+        AZ_TRY((cols<NN, NY, CK_EXPAND, 0>(a, nb, st)));
+        AZ_TRY(rows<LY, RK_OUT_GATHER, SRC_VEC>(a, LL, nb, 1.0, st));
         if (bnd) {
           AzTrace tr("2d_boundary", st, nb);
           k2_boundary_rows<1, 0><<<dim3((unsigned)a.Mb, nb), 32, 0, st>>>(a);
@@ -401,46 +406,46 @@ static az_status_t run2d(const P2& a0, int op, int src, int64_t npairs, int64_t 
         break;
       case OP_STEP1:
         if (src == SRC_PROBE)
-          AZ_TRY(rows<NN, RK_IN_COEF, SRC_PROBE>(a, NN, nb, 1.0, st));
+          AZ_TRY(rows<NY, RK_IN_COEF, SRC_PROBE>(a, NN, nb, 1.0, st));
         else
-          AZ_TRY(rows<NN, RK_IN_COEF, SRC_VEC>(a, NN, nb, 1.0, st));
-        AZ_TRY((cols<NN, CK_EXPAND_KEEP, 0>(a, nb, st)));
-        AZ_TRY(rows<LL, RK_FINE_MASK, SRC_VEC>(a, LL, nb, 1.0, st));
+          AZ_TRY(rows<NY, RK_IN_COEF, SRC_VEC>(a, NN, nb, 1.0, st));
+        AZ_TRY((cols<NN, NY, CK_EXPAND_KEEP, 0>(a, nb, st)));
+        AZ_TRY(rows<LY, RK_FINE_MASK, SRC_VEC>(a, LL, nb, 1.0, st));
         if (bnd)
-          AZ_TRY((cols<NN, CK_STEP1, 1>(a, nb, st)));
+          AZ_TRY((cols<NN, NY, CK_STEP1, 1>(a, nb, st)));
         else
-          AZ_TRY((cols<NN, CK_STEP1, 0>(a, nb, st)));
-        AZ_TRY(rows<LL, RK_OUT_GATHER, SRC_VEC>(a, LL, nb, 1.0, st));
+          AZ_TRY((cols<NN, NY, CK_STEP1, 0>(a, nb, st)));
+        AZ_TRY(rows<LY, RK_OUT_GATHER, SRC_VEC>(a, LL, nb, 1.0, st));
         if (bnd) {
-          AZ_TRY(rows<NN, RK_COEF_W, SRC_VEC>(a, NN, nb, 1.0 / n2, st));
+          AZ_TRY(rows<NY, RK_COEF_W, SRC_VEC>(a, NN, nb, 1.0 / n2, st));
           AzTrace tr("2d_boundary", st, nb);
           k2_boundary_rows<0, 0><<<dim3((unsigned)a.Mb, nb), 32, 0, st>>>(a);
           AZ_LAUNCH_CHECK();
         }
         break;
       case OP_RESID:
-        AZ_TRY(rows<LL, RK_IN_ROWS, SRC_VEC>(a, LL, nb, 1.0, st));
+        AZ_TRY(rows<LY, RK_IN_ROWS, SRC_VEC>(a, LL, nb, 1.0, st));
         if (bnd)
-          AZ_TRY((cols<NN, CK_RESID, 1>(a, nb, st)));
+          AZ_TRY((cols<NN, NY, CK_RESID, 1>(a, nb, st)));
         else
-          AZ_TRY((cols<NN, CK_RESID, 0>(a, nb, st)));
-        AZ_TRY(rows<LL, RK_OUT_RESID, SRC_VEC>(a, LL, nb, 1.0, st));
+          AZ_TRY((cols<NN, NY, CK_RESID, 0>(a, nb, st)));
+        AZ_TRY(rows<LY, RK_OUT_RESID, SRC_VEC>(a, LL, nb, 1.0, st));
         if (bnd) {
-          AZ_TRY(rows<NN, RK_COEF_W, SRC_VEC>(a, NN, nb, 1.0 / n2, st));
+          AZ_TRY(rows<NY, RK_COEF_W, SRC_VEC>(a, NN, nb, 1.0 / n2, st));
           AzTrace tr("2d_boundary", st, nb);
           k2_boundary_rows<0, 1><<<dim3((unsigned)a.Mb, nb), 32, 0, st>>>(a);
           AZ_LAUNCH_CHECK();
         }
         break;
       case OP_ZSTAR:
-        AZ_TRY(rows<LL, RK_IN_ROWS, SRC_VEC>(a, LL, nb, 1.0, st));
-        AZ_TRY((cols<NN, CK_ZSTAR, 0>(a, nb, st)));
-        AZ_TRY(rows<NN, RK_OUT_COEF, SRC_VEC>(a, NN, nb, 1.0 / n2, st));
+        AZ_TRY(rows<LY, RK_IN_ROWS, SRC_VEC>(a, LL, nb, 1.0, st));
+        AZ_TRY((cols<NN, NY, CK_ZSTAR, 0>(a, nb, st)));
+        AZ_TRY(rows<NY, RK_OUT_COEF, SRC_VEC>(a, NN, nb, 1.0 / n2, st));
         break;
       case OP_AT:
-        AZ_TRY(rows<LL, RK_IN_ROWS, SRC_VEC>(a, LL, nb, 1.0, st));
-        AZ_TRY((cols<NN, CK_AT, 0>(a, nb, st)));
-        AZ_TRY(rows<NN, RK_OUT_COEF, SRC_VEC>(a, NN, nb, 1.0 / ((double)LL * LL), st));
+        AZ_TRY(rows<LY, RK_IN_ROWS, SRC_VEC>(a, LL, nb, 1.0, st));
+        AZ_TRY((cols<NN, NY, CK_AT, 0>(a, nb, st)));
+        AZ_TRY(rows<NY, RK_OUT_COEF, SRC_VEC>(a, NN, nb, 1.0 / ((double)LL * LY), st));
         if (bnd) {
           AzTrace tr("2d_boundary", st, nb);
           k2_boundary_adjoint<<<dim3((unsigned)a.Mb, nb), 32, 0, st>>>(a);
@@ -457,6 +462,8 @@ az_status_t az2_apply(az_plan_s* p, int op, int src, const double* in, int64_t l
   P2 a;
   a.W0 = p->d_W0;
   a.W2 = p->d_W2;
+  a.W0y = p->d_W0y;
+  a.W2y = p->d_W2y;
   a.zinv = p->d_zinv;
   a.pos = p->d_pos;
   a.mask = p->d_mask;
@@ -473,6 +480,8 @@ az_status_t az2_apply(az_plan_s* p, int op, int src, const double* in, int64_t l
   a.n = (int)p->n;
   a.s = (int)p->s;
   a.L = (int)p->L;
+  a.ny = (int)p->ny;
+  a.Ly = (int)p->Ly;
   a.M = p->M;
   a.Mb = p->Mb;
   a.N = p->N;
@@ -488,21 +497,22 @@ az_status_t az2_apply(az_plan_s* p, int op, int src, const double* in, int64_t l
   a.col0 = col0;
   a.pair0 = 0;
   a.win = p->win;
+  a.win_y = p->win_y;
   const int64_t npairs = (nvec + 1) / 2;
   if (p->s != 2) {
     az_set_error("2-D layout supports L = 2 only");
     return AZ_ERR_NOT_SUPPORTED;
   }
-  switch (p->n) {
-    case 8: return run2d<8>(a, op, src, npairs, p->Bmax, st);
-    case 16: return run2d<16>(a, op, src, npairs, p->Bmax, st);
-    case 32: return run2d<32>(a, op, src, npairs, p->Bmax, st);
-    case 64: return run2d<64>(a, op, src, npairs, p->Bmax, st);
-    case 128: return run2d<128>(a, op, src, npairs, p->Bmax, st);
-    case 256: return run2d<256>(a, op, src, npairs, p->Bmax, st);
-    case 512: return run2d<512>(a, op, src, npairs, p->Bmax, st);
-    case 1024: return run2d<1024>(a, op, src, npairs, p->Bmax, st);
-  }
+  // square boxes, and anisotropic ones with n_y = n / 2 or 2 n
+#define AZ_RUN2D(NX, NY) \
+  if (p->n == NX && p->ny == NY) return run2d<NX, NY>(a, op, src, npairs, p->Bmax, st);
+  AZ_RUN2D(8, 8) AZ_RUN2D(16, 16) AZ_RUN2D(32, 32) AZ_RUN2D(64, 64) AZ_RUN2D(128, 128) AZ_RUN2D(256, 256)
+  AZ_RUN2D(512, 512) AZ_RUN2D(1024, 1024)
+  AZ_RUN2D(16, 8) AZ_RUN2D(32, 16) AZ_RUN2D(64, 32) AZ_RUN2D(128, 64) AZ_RUN2D(256, 128) AZ_RUN2D(512, 256)
+  AZ_RUN2D(1024, 512)
+  AZ_RUN2D(8, 16) AZ_RUN2D(16, 32) AZ_RUN2D(32, 64) AZ_RUN2D(64, 128) AZ_RUN2D(128, 256) AZ_RUN2D(256, 512)
+  AZ_RUN2D(512, 1024)
+#undef AZ_RUN2D
   az_set_error("2-D: unsupported n");
   return AZ_ERR_NOT_SUPPORTED;
 }

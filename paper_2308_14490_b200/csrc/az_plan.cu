@@ -218,9 +218,9 @@ __global__ void k_samples(cplx* out, int64_t L, double hL, double eps, double T,
 
 // Boundary stencils (CS1 step 6): for boundary point b and axis d, the window of centres
 // j = j0 .. j0 + win - 1 (mod n) around x_b and the weights phi^per(x_b - c_j).
-__global__ void k_stencil(const double* bxy, int64_t Mb, int dim, int n, double T, double h, double eps, int win,
-                          double* bw, int32_t* bj) {
-  const int b = blockIdx.x, d = blockIdx.y, t = threadIdx.x;
+__global__ void k_stencil(const double* bxy, int64_t Mb, int dim, int d, int n, double T, double h, double eps,
+                          int win, double* bw, int32_t* bj) {
+  const int b = blockIdx.x, t = threadIdx.x;
   if (b >= Mb) return;
   const double x = bxy[dim * b + d];
   const int half = (win - 1) / 2;
@@ -242,6 +242,8 @@ struct SymArgs {
   int lap;
   double alpha;
   double k0sq;
+  const cplx* W0y;   // 2-D: the y axis' tables
+  const cplx* W2y;
 };
 
 // row symbols: VALUE rows W0; LAPLACIAN rows alpha (W2 + k0^2 W0) in 1-D and
@@ -250,9 +252,9 @@ AZ_D cplx sym_1d(const SymArgs& a, int64_t kf) {
   return a.lap ? cscale(cadd(a.W2[kf], cscale(a.W0[kf], a.k0sq)), a.alpha) : a.W0[kf];
 }
 AZ_D cplx sym_2d(const SymArgs& a, int64_t kx, int64_t ky) {
-  if (!a.lap) return cmul(a.W0[kx], a.W0[ky]);
-  const cplx w00 = cmul(a.W0[kx], a.W0[ky]);
-  return cscale(cadd(cadd(cmul(a.W2[kx], a.W0[ky]), cmul(a.W0[kx], a.W2[ky])), cscale(w00, a.k0sq)), a.alpha);
+  if (!a.lap) return cmul(a.W0[kx], a.W0y[ky]);
+  const cplx w00 = cmul(a.W0[kx], a.W0y[ky]);
+  return cscale(cadd(cadd(cmul(a.W2[kx], a.W0y[ky]), cmul(a.W0[kx], a.W2y[ky])), cscale(w00, a.k0sq)), a.alpha);
 }
 
 AZ_D void atomic_max_pos(double* addr, double v) {   // v >= 0
@@ -264,10 +266,10 @@ AZ_D void atomic_min_pos(double* addr, double v) {
 
 // sigma^2(k) = sum over the s^d aliases of |W(k + m n)|^2 (diag of B*B)
 __global__ void k_sigma2(double* sig2, double* smax, SymArgs a, int layout, int64_t n, int64_t s,
-                         int64_t N1, int64_t N2, int64_t L2) {
+                         int64_t N1, int64_t N2, int64_t L2, int64_t ny) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double acc = 0.0;
-  int64_t N = layout == AZ_LAYOUT_2D ? n * n : n;
+  int64_t N = layout == AZ_LAYOUT_2D ? n * ny : n;
   if (k < N) {
     if (layout == AZ_LAYOUT_1D_SMALL) {
       for (int64_t m = 0; m < s; ++m) {
@@ -281,10 +283,10 @@ __global__ void k_sigma2(double* sig2, double* smax, SymArgs a, int layout, int6
         acc += w.x * w.x + w.y * w.y;
       }
     } else {
-      const int64_t kx = k / n, ky = k % n;
+      const int64_t kx = k / ny, ky = k % ny;
       for (int64_t mx = 0; mx < s; ++mx)
         for (int64_t my = 0; my < s; ++my) {
-          const cplx w = sym_2d(a, kx + mx * n, ky + my * n);
+          const cplx w = sym_2d(a, kx + mx * n, ky + my * ny);
           acc += w.x * w.x + w.y * w.y;
         }
     }
@@ -327,8 +329,10 @@ static int ilog2(int64_t v) { int k = 0; while ((int64_t(1) << k) < v) ++k; retu
 static void plan_free(az_plan_s* p) {
   if (p) az_pipe_destroy(p);
   if (!p) return;
-  void* ptrs[] = {p->d_mask, p->d_pos, p->d_W0, p->d_W2, p->d_Wr, p->d_zinv, p->d_tw, p->d_tw4hi,
-                  p->d_tw4lo, p->d_bxy, p->d_bw, p->d_bj, p->d_C1, p->d_G, p->d_solve_ws};
+  if (p->d_W0y == p->d_W0) p->d_W0y = nullptr;   // aliases of the x tables (square boxes)
+  if (p->d_W2y == p->d_W2) p->d_W2y = nullptr;
+  void* ptrs[] = {p->d_mask, p->d_pos, p->d_W0, p->d_W2, p->d_W0y, p->d_W2y, p->d_Wr, p->d_zinv, p->d_tw,
+                  p->d_tw4hi, p->d_tw4lo, p->d_bxy, p->d_bw, p->d_bj, p->d_C1, p->d_G, p->d_solve_ws};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->h_stage) cudaFreeHost(p->h_stage);
@@ -377,19 +381,27 @@ static az_status_t plan_build(az_plan_s* p, const az_plan_desc_t* d, cudaStream_
     AZ_TRY(dalloc(&p->d_bxy, p->Mb * 2));
     AZ_CUDA_CHECK(cudaMemcpyAsync(p->d_bxy, d->boundary_xy, p->Mb * p->dim * sizeof(double),
                                   cudaMemcpyHostToDevice, st));
-    // phi(r) < e^-40 beyond r = sqrt(40)/eps: window of 2 ceil(sqrt(40)/(eps h)) + 3 centres
-    const double h = 2.0 * p->T / (double)p->n;
-    int half = (int)std::ceil(std::sqrt(40.0) / (p->eps * h)) + 1;
-    p->win = (int)std::min<int64_t>(2 * half + 1, p->n);   // all n centres when the window wraps
-    if (p->win > 64) {
+    // phi(r) < e^-40 beyond r = sqrt(40)/eps: window of 2 ceil(sqrt(40)/(eps h)) + 3 centres per axis
+    auto window = [&](int64_t nn, double TT) {
+      const double h = 2.0 * TT / (double)nn;
+      const int half = (int)std::ceil(std::sqrt(40.0) / (p->eps * h)) + 1;
+      return (int)std::min<int64_t>(2 * half + 1, nn);   // all centres when the window wraps
+    };
+    p->win = window(p->n, p->T);
+    p->win_y = p->dim == 2 ? window(p->ny, p->Ty) : 0;
+    if (p->win > 64 || p->win_y > 64) {
       az_set_error("boundary stencil wider than 64 centres (eps*h too small)");
       return AZ_ERR_NOT_SUPPORTED;
     }
     AZ_TRY(dalloc(&p->d_bw, p->Mb * 2 * 64));
     AZ_TRY(dalloc(&p->d_bj, p->Mb * 2));
-    k_stencil<<<dim3((unsigned)p->Mb, (unsigned)p->dim), 64, 0, st>>>(p->d_bxy, p->Mb, p->dim, (int)p->n, p->T, h,
-                                                                      p->eps, p->win, p->d_bw, p->d_bj);
-    AZ_LAUNCH_CHECK();
+    for (int d = 0; d < p->dim; ++d) {
+      const int64_t nn = d == 0 ? p->n : p->ny;
+      const double TT = d == 0 ? p->T : p->Ty;
+      k_stencil<<<(unsigned)p->Mb, 64, 0, st>>>(p->d_bxy, p->Mb, p->dim, d, (int)nn, TT, 2.0 * TT / (double)nn, p->eps,
+                                                d == 0 ? p->win : p->win_y, p->d_bw, p->d_bj);
+      AZ_LAUNCH_CHECK();
+    }
   }
   // ---- twiddles ----
   AZ_TRY(dalloc(&p->d_tw, TWN));
@@ -416,19 +428,30 @@ static az_status_t plan_build(az_plan_s* p, const az_plan_desc_t* d, cudaStream_
     AZ_TRY(dalloc(&p->d_C1, B * p->N));
     AZ_TRY(dalloc(&p->d_G, B * p->G));
   }
-  // ---- symbol tables: fine-grid kernel samples and their DFT (Lemma 3) ----
-  const double hL = 2.0 * p->T / (double)p->L;
+  // ---- symbol tables: fine-grid kernel samples and their DFT (Lemma 3), per axis ----
   const int lap = p->op == AZ_ROW_LAPLACIAN;
-  AZ_TRY(dalloc(&p->d_W0, p->L));
-  if (lap) AZ_TRY(dalloc(&p->d_W2, p->L));
-  for (int order = 0; order <= (lap ? 2 : 0); order += 2) {
-    cplx* W = order == 0 ? p->d_W0 : p->d_W2;
-    k_samples<<<az_div_up(p->L, 256), 256, 0, st>>>(W, p->L, hL, p->eps, p->T, order);
-    AZ_LAUNCH_CHECK();
-    if (p->layout == AZ_LAYOUT_1D_FOURSTEP)
-      AZ_TRY(az1f_fft_fine_forward(p, W, st));
-    else
-      AZ_TRY(az_fft_batch(p->d_tw, W, p->L, 1, -1, st));
+  const bool aniso = p->dim == 2 && (p->ny != p->n || p->Ty != p->T);
+  for (int axis = 0; axis < (aniso ? 2 : 1); ++axis) {
+    const int64_t LL = axis == 0 ? p->L : p->Ly;
+    const double TT = axis == 0 ? p->T : p->Ty;
+    const double hL = 2.0 * TT / (double)LL;
+    cplx** W0 = axis == 0 ? &p->d_W0 : &p->d_W0y;
+    cplx** W2 = axis == 0 ? &p->d_W2 : &p->d_W2y;
+    AZ_TRY(dalloc(W0, LL));
+    if (lap) AZ_TRY(dalloc(W2, LL));
+    for (int order = 0; order <= (lap ? 2 : 0); order += 2) {
+      cplx* W = order == 0 ? *W0 : *W2;
+      k_samples<<<az_div_up(LL, 256), 256, 0, st>>>(W, LL, hL, p->eps, TT, order);
+      AZ_LAUNCH_CHECK();
+      if (p->layout == AZ_LAYOUT_1D_FOURSTEP)
+        AZ_TRY(az1f_fft_fine_forward(p, W, st));
+      else
+        AZ_TRY(az_fft_batch(p->d_tw, W, LL, 1, -1, st));
+    }
+  }
+  if (!aniso) {
+    p->d_W0y = p->d_W0;
+    p->d_W2y = p->d_W2;
   }
   if (p->layout == AZ_LAYOUT_1D_FOURSTEP) {
     AZ_TRY(dalloc(&p->d_Wr, p->L));
@@ -445,8 +468,9 @@ static az_status_t plan_build(az_plan_s* p, const az_plan_desc_t* d, cudaStream_
   unsigned long long z = 0;
   memcpy(&init[2], &z, sizeof(z));
   AZ_CUDA_CHECK(cudaMemcpyAsync(d_red, init, sizeof(init), cudaMemcpyHostToDevice, st));
-  SymArgs a{p->d_W0, p->d_W2, lap, p->alpha, p->k0sq};
-  k_sigma2<<<az_div_up(p->N, 256), 256, 0, st>>>(d_sig2, d_red, a, p->layout, p->n, p->s, p->N1, p->N2, p->L2);
+  SymArgs a{p->d_W0, p->d_W2, lap, p->alpha, p->k0sq, p->d_W0y, p->d_W2y};
+  k_sigma2<<<az_div_up(p->N, 256), 256, 0, st>>>(d_sig2, d_red, a, p->layout, p->n, p->s, p->N1, p->N2, p->L2,
+                                                 p->ny);
   AZ_LAUNCH_CHECK();
   k_zinv<<<az_div_up(p->N, 256), 256, 0, st>>>(p->d_zinv, d_sig2, p->N, d_red, p->rcond,
                                                (unsigned long long*)(d_red + 2), d_red + 1);
@@ -491,14 +515,24 @@ extern "C" az_status_t az_plan_create(const az_plan_desc_t* d, void* stream, az_
       az_set_error("2-D: need n >= 8, L = 2 and L*n <= 2048");
       return AZ_ERR_NOT_SUPPORTED;
     }
+    AZ_ARG(d->n_y >= 0 && d->T_y >= 0, "n_y and T_y must be >= 0");
+    const int64_t ny = d->n_y ? d->n_y : d->n;
+    AZ_ARG(is_pow2(ny), "n_y must be a power of two");
+    if (ny < 8 || ny * d->L > 2048 || 2 * ny < d->n || ny > 2 * d->n) {
+      az_set_error("2-D: need n_y >= 8, L*n_y <= 2048 and n/2 <= n_y <= 2n");
+      return AZ_ERR_NOT_SUPPORTED;
+    }
   }
   az_plan_s* p = new az_plan_s();
   p->dim = d->dim;
   p->n = d->n;
   p->s = d->L;
   p->L = L;
-  p->N = d->dim == 1 ? d->n : d->n * d->n;
-  p->G = d->dim == 1 ? L : L * L;
+  p->ny = d->dim == 2 && d->n_y ? d->n_y : d->n;
+  p->Ly = p->ny * d->L;
+  p->Ty = d->dim == 2 && d->T_y > 0 ? d->T_y : d->T;
+  p->N = d->dim == 1 ? d->n : d->n * p->ny;
+  p->G = d->dim == 1 ? L : L * p->Ly;
   p->Mb = d->n_boundary;
   p->T = d->T;
   p->eps = d->eps;

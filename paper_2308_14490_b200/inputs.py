@@ -57,10 +57,24 @@ class Config:
     T: float = 1.0
     k0sq: float = 0.0              # Helmholtz term of the LAPLACIAN rows (0 = Poisson)
     eps_h: float = 0.5             # eps * h: 0.5 in every BASELINE config; the paper's regime is eps_h_paper(tau0)
+    n_y: int = 0                   # 2-D anisotropic boxes: centers along y (0 = n)
+    T_y: float = 0.0               # half-period along y (0 = T); the box is [-T, T) x [-T_y, T_y)
+
+    @property
+    def ny(self) -> int:
+        return self.n_y or self.n
+
+    @property
+    def Ty(self) -> float:
+        return self.T_y or self.T
 
     @property
     def h(self) -> float:
         return 2.0 * self.T / self.n
+
+    @property
+    def hy(self) -> float:
+        return 2.0 * self.Ty / self.ny
 
     @property
     def eps(self) -> float:
@@ -73,7 +87,7 @@ class Config:
 
     @property
     def N(self) -> int:
-        return self.n ** self.dim
+        return self.n if self.dim == 1 else self.n * self.ny
 
     @property
     def row_scale(self) -> float:
@@ -139,6 +153,28 @@ def _make_config(family: str, n: int, *, nrhs: int = 1, R: Optional[int] = None,
         return Config(name or f"helm_n{n}", 2, n, s, "star", ROW_LAPLACIAN, nrhs,
                       R if R is not None else 8 * n, seed, 1e-10,
                       boundary_weight=10.0, n_boundary=4 * n, k0sq=25.0)
+    if family == "ellipse":
+        # SURVEY.md §8(f) f3, PAPER.md:644-647 (Fig. 7): the ellipse x^2 + 4 y^2 <= 1 in the anisotropic
+        # box T^x = 1.4, T^y = 0.7 with N^x = 2 N^y (the paper's N^x = 100, N^y = 50 give h^x = h^y;
+        # power-of-two N here), f = sin(N^x x / 10 + N^y y / 10), value rows.  R: 1.5 x the collocation
+        # points along the boundary (the disk rule of BASELINE configs[2] applied to the ellipse's
+        # perimeter, Ramanujan's approximation)
+        per = math.pi * (3 * 1.5 - math.sqrt((3 + 0.5) * (1 + 1.5)))
+        return Config(name or f"ellipse_n{n}", 2, n, s, "ellipse", ROW_VALUE, nrhs,
+                      R if R is not None else int(round(1.5 * per * s * n / 2.8)), seed, 1e-10,
+                      T=1.4, n_y=n // 2, T_y=0.7)
+    if family == "ellipse_t":
+        # the same ellipse with the long axis along y (4 x^2 + y^2 <= 1, T^x = 0.7, T^y = 1.4, N^y = 2 N^x):
+        # exercises the other orientation of the anisotropic passes
+        per = math.pi * (3 * 1.5 - math.sqrt((3 + 0.5) * (1 + 1.5)))
+        return Config(name or f"ellipse_t_n{n}", 2, n, s, "ellipse_t", ROW_VALUE, nrhs,
+                      R if R is not None else int(round(1.5 * per * s * 2 * n / 2.8)), seed, 1e-10,
+                      T=0.7, n_y=2 * n, T_y=1.4)
+    if family == "ellipse_bvp":
+        # Poisson on the ellipse in the anisotropic box (c4's row operator, Dirichlet rows beta = 10 at
+        # 4 N^x boundary points): the boundary windows differ per axis
+        c = _make_config("ellipse", n, nrhs=nrhs, R=R, seed=seed, s=s, name=name or f"ellipse_bvp_n{n}")
+        return dataclasses.replace(c, row_op=ROW_LAPLACIAN, boundary_weight=10.0, n_boundary=4 * n)
     raise ValueError(f"unknown family {family!r}")
 
 
@@ -164,14 +200,16 @@ def get_config(name: str) -> Config:
 # geometry data (inputs, not method)
 # --------------------------------------------------------------------------------------
 
-def grid_axis(cfg: Config) -> np.ndarray:
-    """Oversampled grid coordinates along one axis, x_q = -T + q*2T/(s n)."""
-    L = cfg.grid_n
-    return -cfg.T + np.arange(L, dtype=np.float64) * (2.0 * cfg.T / L)
+def grid_axis(cfg: Config, axis: int = 0) -> np.ndarray:
+    """Oversampled grid coordinates along one axis, x_q = -T + q*2T/(s n) (axis 1: T_y, n_y)."""
+    T, n = (cfg.T, cfg.n) if axis == 0 else (cfg.Ty, cfg.ny)
+    L = cfg.s * n
+    return -T + np.arange(L, dtype=np.float64) * (2.0 * T / L)
 
 
-def center_axis(cfg: Config) -> np.ndarray:
-    return -cfg.T + np.arange(cfg.n, dtype=np.float64) * cfg.h
+def center_axis(cfg: Config, axis: int = 0) -> np.ndarray:
+    T, n = (cfg.T, cfg.n) if axis == 0 else (cfg.Ty, cfg.ny)
+    return -T + np.arange(n, dtype=np.float64) * (2.0 * T / n)
 
 
 def _in_domain(domain: str, x: np.ndarray, y: Optional[np.ndarray] = None) -> np.ndarray:
@@ -186,18 +224,22 @@ def _in_domain(domain: str, x: np.ndarray, y: Optional[np.ndarray] = None) -> np
         return x * x + y * y <= 0.64
     if domain == "star":
         return np.hypot(x, y) <= 0.6 + 0.15 * np.cos(5.0 * np.arctan2(y, x))
+    if domain == "ellipse":
+        return x * x + 4.0 * y * y <= 1.0
+    if domain == "ellipse_t":
+        return 4.0 * x * x + y * y <= 1.0
     raise ValueError(domain)
 
 
 def mask(cfg: Config) -> np.ndarray:
     """uint8 collocation mask on the full oversampled grid, natural row-major order.
 
-    1-D: shape (s n,).  2-D: shape (s n, s n), x outer.
+    1-D: shape (s n,).  2-D: shape (s n, s n_y), x outer.
     """
     g = grid_axis(cfg)
     if cfg.dim == 1:
         return _in_domain(cfg.domain, g).astype(np.uint8)
-    X, Y = np.meshgrid(g, g, indexing="ij")
+    X, Y = np.meshgrid(g, grid_axis(cfg, 1), indexing="ij")
     return _in_domain(cfg.domain, X, Y).astype(np.uint8)
 
 
@@ -207,7 +249,7 @@ def collocation_points(cfg: Config) -> np.ndarray:
     m = mask(cfg).astype(bool)
     if cfg.dim == 1:
         return g[m]
-    X, Y = np.meshgrid(g, g, indexing="ij")
+    X, Y = np.meshgrid(g, grid_axis(cfg, 1), indexing="ij")
     return np.stack([X[m], Y[m]], axis=1)
 
 
@@ -221,9 +263,11 @@ def boundary_points(cfg: Config) -> np.ndarray:
         return np.zeros((0, max(cfg.dim, 1)), dtype=np.float64)
     if cfg.domain == "ode":
         return np.array([[-1.0], [1.0]])
-    if cfg.domain != "star":
-        raise ValueError("boundary points are defined for the star domain only")
     th = 2.0 * np.pi * np.arange(cfg.n_boundary, dtype=np.float64) / cfg.n_boundary
+    if cfg.domain == "ellipse":
+        return np.stack([np.cos(th), 0.5 * np.sin(th)], axis=1)
+    if cfg.domain != "star":
+        raise ValueError("boundary points are defined for the star and ellipse domains only")
     r = star_radius(th)
     return np.stack([r * np.cos(th), r * np.sin(th)], axis=1)
 
@@ -248,6 +292,10 @@ def exact_functions(cfg: Config) -> List[Callable]:
             return [lambda x: np.exp(x) * np.cos(8 * x)]
         return [(lambda k: (lambda x: np.cos(k * x) * np.exp(-x * x)))(k)
                 for k in range(1, cfg.nrhs + 1)]
+    if cfg.domain in ("ellipse", "ellipse_t"):
+        # PAPER.md:644 f(x, y) = sin(N^x x / 10 + N^y y / 10); extra columns shift the phase
+        kx, ky = cfg.n / 10.0, cfg.ny / 10.0
+        return [(lambda k: (lambda x, y: np.sin(kx * x + ky * y + k)))(k) for k in range(cfg.nrhs)]
     if cfg.nrhs == 1:
         return [lambda x, y: np.exp(x + y) * np.sin(3 * x) * np.cos(2 * y)]
     return [(lambda k: (lambda x, y: np.cos(k * x + y) * np.exp(-(x * x + y * y))))(k)
@@ -306,12 +354,18 @@ def test_grid(cfg: Config, points_1d: Optional[int] = None) -> TestGrid:
         ex = np.stack([f(t) for f in fns], axis=1)
         return TestGrid((t,), inside, ex)
     m = points_1d or 401
-    lim = {"disk": 0.8, "star": 0.75, "box": 1.0}[cfg.domain]
-    t = np.linspace(-lim, lim, m) if cfg.domain != "box" else np.linspace(-1, 1, m, endpoint=False)
-    X, Y = np.meshgrid(t, t, indexing="ij")
+    if cfg.domain == "ellipse":
+        t, u = np.linspace(-1.0, 1.0, m), np.linspace(-0.5, 0.5, (m + 1) // 2)
+    elif cfg.domain == "ellipse_t":
+        t, u = np.linspace(-0.5, 0.5, (m + 1) // 2), np.linspace(-1.0, 1.0, m)
+    else:
+        lim = {"disk": 0.8, "star": 0.75, "box": 1.0}[cfg.domain]
+        t = np.linspace(-lim, lim, m) if cfg.domain != "box" else np.linspace(-1, 1, m, endpoint=False)
+        u = t
+    X, Y = np.meshgrid(t, u, indexing="ij")
     inside = _in_domain(cfg.domain, X, Y)
     ex = np.stack([f(X[inside], Y[inside]) for f in fns], axis=1)
-    return TestGrid((t, t), inside, ex)
+    return TestGrid((t, u), inside, ex)
 
 
 def gaussian_matrix(rows: int, cols: int, seed: int) -> np.ndarray:

@@ -36,6 +36,12 @@ CASES = [
     ("ode_n64", I.make_config("ode", 64)),        # f2: 1-D ODE, two Dirichlet rows, box T = 1.5
     ("ode_n256", I.make_config("ode", 256)),
     ("box2d_n16", I.make_config("box2d", 16)),
+    # anisotropic boxes (T^x != T^y, N^x != N^y), both orientations, and the
+    # Poisson + Dirichlet-row variant whose boundary windows differ per axis
+    ("ellipse_n32", I.make_config("ellipse", 32)),
+    ("ellipse_t_n16", I.make_config("ellipse_t", 16)),
+    ("ellipse_bvp_n32", I.make_config("ellipse_bvp", 32)),
+    ("ellipse_paper_n16", I.make_config("ellipse", 16, eps_h=I.eps_h_paper(1e-5))),
 ]
 
 
@@ -71,7 +77,8 @@ def test_plan_info(setup):
 
 def prob_sigma2(cfg):
     from oracle import circulant as C
-    sym = C.Symbol(cfg.dim, cfg.n, cfg.s, cfg.eps, cfg.T, cfg.row_op, alpha=cfg.row_scale, k0sq=cfg.k0sq)
+    sym = C.Symbol(cfg.dim, cfg.n, cfg.s, cfg.eps, cfg.T, cfg.row_op, alpha=cfg.row_scale, k0sq=cfg.k0sq,
+                   n_y=cfg.ny, T_y=cfg.Ty)
     return sym.sigma2
 
 

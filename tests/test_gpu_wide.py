@@ -82,7 +82,12 @@ def _approx_err(cfg, x, ref_x, grid):
 WIDE_CASES = [("disk_n32", I.make_config("disk", 32), 8),
               ("star_n32", I.make_config("star", 32), 8),
               ("helm_n32", I.make_config("helm", 32), 8),      # SURVEY.md §8(f) f2 (2-D Helmholtz)
-              ("disk_n32_nrhs3", I.make_config("disk", 32, nrhs=3, R=128), 12)]
+              ("disk_n32_nrhs3", I.make_config("disk", 32, nrhs=3, R=128), 12),
+              # anisotropic boxes
+              ("ellipse_n32", I.make_config("ellipse", 32), 8),
+              ("ellipse_t_n16", I.make_config("ellipse_t", 16), 8),
+              ("ellipse_bvp_n32", I.make_config("ellipse_bvp", 32), 8),
+              ("ellipse_n64", I.make_config("ellipse", 64), 8)]
 
 
 @pytest.mark.parametrize("name,cfg,max_blocks", WIDE_CASES, ids=[c[0] for c in WIDE_CASES])

@@ -228,3 +228,75 @@ def test_helmholtz_rows_are_the_operator_applied_to_the_expansion(k0sq):
     rows = D.assemble_rows(cfg, x, "laplacian") @ c
     ref = cfg.row_scale * (lap + k0sq * u(x))
     assert np.allclose(rows, ref, rtol=1e-6, atol=1e-6 * np.abs(cfg.row_scale) * np.max(np.abs(lap)))
+
+
+# ---- anisotropic boxes (T^x != T^y, N^x != N^y) ----
+
+def _acfg(n, ny, T, Ty, row_op=0, eps_h=0.5):
+    import dataclasses
+    base = I.make_config("box2d", n, eps_h=eps_h)
+    return dataclasses.replace(base, n_y=ny, T=T, T_y=Ty, row_op=row_op)
+
+
+@pytest.mark.parametrize("n,ny,T,Ty,row_op,backend", [(16, 8, 1.4, 0.7, 0, "fft"), (8, 16, 0.7, 1.4, 0, "fft"),
+                                                     (16, 8, 1.4, 0.7, 1, "fft"), (8, 4, 1.4, 0.9, 1, "ld"),
+                                                     (16, 4, 1.0, 1.3, 0, "ld")])
+def test_aniso_apply_Ac_matches_entrywise(n, ny, T, Ty, row_op, backend):
+    """A^c = Pi^T P* B F* with B = B^x (x) B^y from each axis' own (N, T) equals the entrywise
+    matrix of the per-axis periodised kernels."""
+    cfg = _acfg(n, ny, T, Ty, row_op)
+    Ac = D.assemble_Ac(cfg)
+    assert Ac.shape == (4 * n * ny, n * ny)
+    sym = C.Symbol(2, n, 2, cfg.eps, T, row_op, alpha=cfg.row_scale, backend=backend, n_y=ny, T_y=Ty)
+    ops = C.PeriodicOperators(sym, 0.0)
+    a = np.random.default_rng(n + ny).standard_normal(n * ny)
+    y = np.real(ops.apply_Ac(a)).astype(np.float64)
+    ref = Ac @ a
+    assert np.linalg.norm(y - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("row_op", [0, 1])
+def test_aniso_axis_swap_invariance(row_op):
+    """Swapping the roles of x and y (N^x <-> N^y, T^x <-> T^y) transposes every grid and
+    coefficient array: the FFT-built operators of the two configurations agree after the
+    index permutation.  Catches an axis mixed up anywhere in the 2-D factorisation."""
+    a_cfg, b_cfg = _acfg(16, 8, 1.4, 0.7, row_op), _acfg(8, 16, 0.7, 1.4, row_op)
+    b_cfg = __import__("dataclasses").replace(b_cfg, eps_h=a_cfg.eps * b_cfg.h)   # same eps in both
+    assert abs(a_cfg.eps - b_cfg.eps) < 1e-12 * a_cfg.eps
+    ops = []
+    for c in (a_cfg, b_cfg):
+        sym = C.Symbol(2, c.n, 2, c.eps, c.T, row_op, alpha=c.row_scale, n_y=c.ny, T_y=c.Ty)
+        ops.append(C.PeriodicOperators(sym, 1e-10))
+    a = np.random.default_rng(5).standard_normal((16, 8))
+    ya = np.real(ops[0].apply_Ac(a.reshape(-1))).reshape(32, 16)
+    yb = np.real(ops[1].apply_Ac(a.T.reshape(-1))).reshape(16, 32)
+    assert np.linalg.norm(ya - yb.T) <= 1e-13 * np.linalg.norm(ya)
+    g = np.random.default_rng(6).standard_normal((32, 16))
+    za = np.real(ops[0].apply_Zstar_grid(g.reshape(-1))).reshape(16, 8)
+    zb = np.real(ops[1].apply_Zstar_grid(g.T.reshape(-1))).reshape(8, 16)
+    assert np.linalg.norm(za - zb.T) <= 1e-12 * np.linalg.norm(za)
+
+
+@pytest.mark.parametrize("row_op", [0, 1])
+def test_aniso_lemma3_singular_values(row_op):
+    """Singular values of the entrywise anisotropic A^c (LAPACK) = sqrt(sum_i |d_i(k)|^2)."""
+    cfg = _acfg(16, 8, 1.4, 0.7, row_op)
+    sv = np.linalg.svd(D.assemble_Ac(cfg), compute_uv=False)
+    sym = C.Symbol(2, 16, 2, cfg.eps, 1.4, row_op, alpha=cfg.row_scale, n_y=8, T_y=0.7)
+    ours = np.sort(np.sqrt(sym.sigma2))[::-1]
+    assert np.max(np.abs(sv - ours)) < 1e-13 * sv[0]
+
+
+def test_aniso_zstar_full_box_is_pseudo_inverse():
+    """Omega = the anisotropic box (E = I): Z* = F B^dag P Pi is the pseudo-inverse of A^c."""
+    cfg = _acfg(8, 4, 1.4, 0.7, 0, eps_h=1.0)
+    Ac = D.assemble_Ac(cfg)
+    sym = C.Symbol(2, 8, 2, cfg.eps, 1.4, 0, backend="ld", n_y=4, T_y=0.7)
+    ops = C.PeriodicOperators(sym, 0.0)
+    L = Ac.shape[0]
+    Z = np.stack([np.real(ops.apply_Zstar_grid(np.eye(L, dtype=C.LD)[:, i])).astype(np.float64)
+                  for i in range(L)], axis=1)
+    cond = np.linalg.cond(Ac)
+    ref = np.linalg.pinv(Ac, rcond=1e-15)
+    assert np.linalg.norm(Z - ref) <= 1e-15 * cond * cond * np.linalg.norm(ref) + 1e-12
+    assert np.linalg.norm(Ac @ Z @ Ac - Ac) <= 1e-14 * cond * np.linalg.norm(Ac)

@@ -19,7 +19,7 @@ from paper_2308_14490_b200 import inputs as I  # noqa: E402
 
 name = sys.argv[1]
 mb = int(sys.argv[2]) if len(sys.argv) > 2 else 16
-cfg = I.get_config(name)
+cfg = I.get_config(name) if name in I.CONFIGS else I.make_config(name.split(':')[0], int(name.split(':')[1]))
 t0 = time.time()
 plan = api.Plan.from_config(cfg)
 b = I.rhs(cfg)
