@@ -22,6 +22,17 @@ AZ_D double wsum(double v) {
 
 __device__ int g_small_sweeps;
 
+AZ_D double hsum(double v) {   // sum over the 16 lanes of a half warp
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One CTA, r <= 16 EPL.  A pair (p, q) of columns of B = R_S^T is handled by a HALF warp, each lane
+// holding EPL entries of both columns in registers for the round: the round is issue-bound on the
+// one SM, so the instruction count per pair is what matters (no modulo arithmetic, unrolled
+// element loops, 4-level reductions, no shared atomics).
+template <int EPL>
 __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int64_t ldr, int r, int nrhs,
                                                           double theta, double* y, int64_t ldy, double* sig_out,
                                                           int64_t* rank_dev, int max_sweeps) {
@@ -29,11 +40,14 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
   double* B = sm;                      // r x r, column i at B + i * r
   double* Cm = B + r * r;              // r x nrhs, row p, column c at Cm[p * nrhs + c] (rows contiguous)
   double* nrm2 = Cm + r * nrhs;        // r
-  __shared__ int rot_count;
-  __shared__ unsigned long long off_bits;   // max |g| / sqrt(a b) over the sweep (double bits)
+  // per-half-warp sweep statistics, reduced once per sweep
+  __shared__ int rot_h[64];
+  __shared__ double off_h[64];
+  __shared__ double smax2_sweep;
   const double tol = 1.1102230246251565e-16 * sqrt((double)r);   // rotation threshold
   const int tid = threadIdx.x, nth = blockDim.x;
   const int w = tid >> 5, lane = tid & 31, nw = nth >> 5;
+  const int hw = tid >> 4, hl = tid & 15, nh = nth >> 4;   // half warps
   for (int e = tid; e < r * r; e += nth) {
     const int i = e / r, t = e % r;    // B[t][i] = R_S[i][t]
     B[e] = Rf[(int64_t)t * ldr + i];
@@ -44,7 +58,6 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
   }
   __syncthreads();
   const int n = r + (r & 1);           // padded to even
-  __shared__ double smax2_sweep;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     // column norms at the start of the sweep: pairs whose smaller column is far below the
     // truncation level (1e-3 theta sigma_1) cannot change the kept part and are skipped
@@ -59,61 +72,85 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
       double m = 0.0;
       for (int i = 0; i < r; ++i) m = fmax(m, nrm2[i]);
       smax2_sweep = m;
-      rot_count = 0;
-      off_bits = 0ull;
     }
     __syncthreads();
     const double negl = (1e-3 * theta) * (1e-3 * theta) * smax2_sweep;
+    double off_me = 0.0;
+    int rot_me = 0;
     for (int round = 0; round < n - 1; ++round) {
-      for (int pi = w; pi < n / 2; pi += nw) {
-        int p, q;
-        if (pi == 0) {
+      // both halves of a warp run the same trip count (the shuffles span the whole warp)
+      for (int base = hw & ~1; base < n / 2; base += nh) {
+        const int pi = base + (hw & 1);
+        int p = 0, q = r;   // a missing pair (pi >= n / 2) falls through with q = r, i.e. !pair_ok
+        if (pi >= n / 2) {
+        } else if (pi == 0) {
           p = round;
           q = n - 1;
         } else {
-          p = (round + pi) % (n - 1);
-          q = (round - pi + (n - 1)) % (n - 1);
+          p = round + pi;
+          if (p >= n - 1) p -= n - 1;
+          q = round - pi;
+          if (q < 0) q += n - 1;
         }
         if (p > q) { const int t = p; p = q; q = t; }
-        if (q >= r) continue;
+        const bool pair_ok = q < r;
         double* bp = B + (int64_t)p * r;
         double* bq = B + (int64_t)q * r;
+        double xp[EPL], xq[EPL];
         double a = 0.0, b = 0.0, g = 0.0;
-        for (int t = lane; t < r; t += 32) {
-          const double xp = bp[t], xq = bq[t];
-          a = fma(xp, xp, a);
-          b = fma(xq, xq, b);
-          g = fma(xp, xq, g);
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          const int t = hl + 16 * e;
+          const bool in = pair_ok && t < r;
+          xp[e] = in ? bp[t] : 0.0;
+          xq[e] = in ? bq[t] : 0.0;
+          a = fma(xp[e], xp[e], a);
+          b = fma(xq[e], xq[e], b);
+          g = fma(xp[e], xq[e], g);
         }
-        a = wsum(a);
-        b = wsum(b);
-        g = wsum(g);
-        if (fmin(a, b) < negl || g == 0.0) continue;
+        a = hsum(a);
+        b = hsum(b);
+        g = hsum(g);
+        if (!pair_ok || fmin(a, b) < negl || g == 0.0) continue;
         const double g2 = g * g, ab = a * b;
-        if (lane == 0) atomicMax(&off_bits, (unsigned long long)__double_as_longlong(sqrt(g2 / ab)));
+        off_me = fmax(off_me, g2 / ab);
         if (!(g2 > tol * tol * ab)) continue;
         // tan of the rotation angle, t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (b - a) / 2g,
         // written without the intermediate division: t = 2 g sign(b - a) / (|b - a| + sqrt((b - a)^2 + 4 g^2))
         const double d = b - a;
         const double tt = (d >= 0.0 ? 2.0 * g : -2.0 * g) / (fabs(d) + sqrt(fma(d, d, 4.0 * g2)));
         const double cs = rsqrt(fma(tt, tt, 1.0)), sn = cs * tt;
-        for (int t = lane; t < r; t += 32) {
-          const double xp = bp[t], xq = bq[t];
-          bp[t] = cs * xp - sn * xq;
-          bq[t] = sn * xp + cs * xq;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          const int t = hl + 16 * e;
+          if (t < r) {
+            bp[t] = cs * xp[e] - sn * xq[e];
+            bq[t] = sn * xp[e] + cs * xq[e];
+          }
         }
-        for (int c = lane; c < nrhs; c += 32) {
+        for (int c = hl; c < nrhs; c += 16) {
           const double cp = Cm[p * nrhs + c], cq = Cm[q * nrhs + c];
           Cm[p * nrhs + c] = cs * cp - sn * cq;
           Cm[q * nrhs + c] = sn * cp + cs * cq;
         }
-        if (lane == 0) atomicAdd(&rot_count, 1);
+        ++rot_me;
       }
       __syncthreads();
     }
+    if (hl == 0) {
+      rot_h[hw] = rot_me;
+      off_h[hw] = off_me;
+    }
+    __syncthreads();
+    int rots = 0;
+    double offm = 0.0;
+    for (int i = 0; i < nh; ++i) {
+      rots += rot_h[i];
+      offm = fmax(offm, off_h[i]);
+    }
     // converged: no rotation, or every measured off-diagonal at the rounding level of the dots
     if (tid == 0) g_small_sweeps = sweep + 1;
-    if (rot_count == 0 || __longlong_as_double((long long)off_bits) <= 8.0 * tol) break;
+    if (rots == 0 || sqrt(offm) <= 8.0 * tol) break;
     __syncthreads();
   }
   // singular values = column norms of B W
@@ -177,10 +214,21 @@ az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs,
     return AZ_ERR_WORKSPACE;
   }
   int64_t* d_rank = (int64_t*)ws;
-  AZ_CUDA_CHECK(az_smem_attr(k_jacobi_small, sm));
-  const int nth = std::min<int64_t>(1024, std::max<int64_t>(64, 32 * ((r + 1) / 2)));
+  // one half warp per pair: n / 2 pairs -> 16 (n / 2) threads, whole warps, at most 1024
+  const int nth = (int)std::min<int64_t>(1024, std::max<int64_t>(64, 32 * ((r + 3) / 4)));
   AzTrace tr("jacobi_svd", st);
-  k_jacobi_small<<<1, nth, sm, st>>>(Rf, ldr, (int)r, (int)nrhs, theta, y, ldy, sigma_out, d_rank, 60);
+#define AZ_JS(E)                                                                                       \
+  {                                                                                                    \
+    AZ_CUDA_CHECK(az_smem_attr(k_jacobi_small<E>, sm));                                                \
+    k_jacobi_small<E><<<1, nth, sm, st>>>(Rf, ldr, (int)r, (int)nrhs, theta, y, ldy, sigma_out, d_rank, 60); \
+  }
+  if (r <= 32)
+    AZ_JS(2)
+  else if (r <= 64)
+    AZ_JS(4)
+  else
+    AZ_JS(8)
+#undef AZ_JS
   AZ_LAUNCH_CHECK();
   if (rank_out) {
     AZ_CUDA_CHECK(cudaMemcpyAsync(rank_out, d_rank, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
