@@ -329,10 +329,20 @@ static int fft_e() {   // tuning knob: AZ_FFT_E=8 (8 values per thread), 17 (16 
   return e;
 }
 
+static int fft_er() {   // rows: AZ_FFT_ER=8 (8 values per thread), default 16
+  static int e = 0;
+  if (!e) {
+    const char* v = getenv("AZ_FFT_ER");
+    e = v ? atoi(v) : 16;
+    if (e != 8) e = 16;
+  }
+  return e;
+}
+
 template <int NC, int KIND, int SRC, int EC, int MINB>
 static az_status_t fcols_e(const P1f& a, int ncols, int nb, double cout, cudaStream_t st) {
   constexpr int T = NC / EC;
-  constexpr int TC0 = (EC == 8 || MINB == 1 ? 512 : 256) / T;
+  constexpr int TC0 = (MINB == 1 ? 512 : 256) / T;
   constexpr int TC = TC0 < 2 ? 2 : (TC0 > 16 ? 16 : TC0);
   const size_t sm = (size_t)TC * fftr::padded_len(NC) * sizeof(cplx);
   auto kern = k1f_cols<NC, TC, KIND, SRC, EC, MINB>;
@@ -348,7 +358,7 @@ static az_status_t fcols_e(const P1f& a, int ncols, int nb, double cout, cudaStr
 
 template <int NC, int KIND, int SRC>
 static az_status_t fcols(const P1f& a, int ncols, int nb, double cout, cudaStream_t st) {
-  if (fft_e() == 8) return fcols_e<NC, KIND, SRC, 8, 4>(a, ncols, nb, cout, st);
+  if (fft_e() == 8) return fcols_e<NC, KIND, SRC, 8, 3>(a, ncols, nb, cout, st);
   if (fft_e() == 17) return fcols_e<NC, KIND, SRC, 16, 1>(a, ncols, nb, cout, st);
   return fcols_e<NC, KIND, SRC, 16, 2>(a, ncols, nb, cout, st);
 }
@@ -372,7 +382,7 @@ static az_status_t frows_e(const P1f& a, int nb, cudaStream_t st) {
 
 template <int NR2, int KIND>
 static az_status_t frows(const P1f& a, int nb, cudaStream_t st) {
-  if (fft_e() == 8) return frows_e<NR2, KIND, 8, 4>(a, nb, st);
+  if (fft_er() == 8) return frows_e<NR2, KIND, 8, 3>(a, nb, st);
   return frows_e<NR2, KIND, 16, 3>(a, nb, st);
 }
 
