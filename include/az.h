@@ -82,6 +82,10 @@ typedef struct {
                                   [-T, T) x [-T_y, T_y), centres c_j = (-T + jx 2T/n, -T_y + jy 2T_y/n_y),
                                   column j = jx n_y + jy; the mask is (L n) x (L n_y), x outer.  Ignored in 1-D. */
   double T_y;                  /* half-period along y (0 = T).  eps is one isotropic shape parameter. */
+  const double* boundary_coef; /* HOST, Mb x 4 row-major [a, b, n_x, n_y] (2-D only): boundary row k is
+                                  beta (a phi_j + b n . grad phi_j)(x_k) -- Dirichlet (a = 1, b = 0), Neumann
+                                  (a = 0) or Robin rows (the flower of PAPER.md:839-846: Neumann on the outer,
+                                  Dirichlet on the inner boundary).  NULL = all Dirichlet.  Deep-copied. */
 } az_plan_desc_t;
 
 typedef struct {

@@ -71,7 +71,7 @@ def make_problem(cfg: I.Config, backend: str = "fft", dense_A: Optional[np.ndarr
     ops = C.PeriodicOperators(sym, cfg.tol)
     Ab = None
     if Mb:
-        Ab = cfg.boundary_weight * D.assemble_rows(cfg, I.boundary_points(cfg), "value")
+        Ab = D.boundary_matrix(cfg)
 
     def zstar(y):
         y = np.asarray(y)

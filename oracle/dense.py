@@ -51,14 +51,32 @@ def assemble_rows(cfg: I.Config, pts: np.ndarray, kind: str) -> np.ndarray:
     return cfg.row_scale * L.reshape(pts.shape[0], -1)
 
 
+def boundary_matrix(cfg: I.Config, pts=None, coefs=None) -> np.ndarray:
+    """beta A^b: Dirichlet rows beta phi_j(x_b), or, where the plan gives Robin
+    coefficients [a, b, n_x, n_y] (the flower of PAPER.md:839-846), beta (a phi_j + b n . grad phi_j)(x_b)
+    with grad phi_j = (phi'(x - c_jx) phi(y - c_jy), phi(x - c_jx) phi'(y - c_jy))."""
+    pts = I.boundary_points(cfg) if pts is None else np.asarray(pts, dtype=np.float64)
+    coefs = I.boundary_coefs(cfg) if coefs is None else coefs
+    if coefs is None or cfg.dim == 1:
+        return cfg.boundary_weight * assemble_rows(cfg, pts, "value")
+    c, cy = I.center_axis(cfg), I.center_axis(cfg, 1)
+    X0 = _Phi(pts[:, 0], c, cfg.eps, cfg.T, 0)
+    Y0 = _Phi(pts[:, 1], cy, cfg.eps, cfg.Ty, 0)
+    X1 = _Phi(pts[:, 0], c, cfg.eps, cfg.T, 1)
+    Y1 = _Phi(pts[:, 1], cy, cfg.eps, cfg.Ty, 1)
+    a, b, nx, ny = (coefs[:, i][:, None, None] for i in range(4))
+    rows = a * X0[:, :, None] * Y0[:, None, :] + b * (nx * X1[:, :, None] * Y0[:, None, :]
+                                                     + ny * X0[:, :, None] * Y1[:, None, :])
+    return cfg.boundary_weight * rows.reshape(pts.shape[0], -1)
+
+
 def assemble_A(cfg: I.Config) -> np.ndarray:
     """A = [A^i ; beta A^b], shape (M + M_b, N)."""
     kind = "laplacian" if cfg.row_op == I.ROW_LAPLACIAN else "value"
     Ai = assemble_rows(cfg, I.collocation_points(cfg), kind)
     if cfg.n_boundary == 0:
         return Ai
-    Ab = cfg.boundary_weight * assemble_rows(cfg, I.boundary_points(cfg), "value")
-    return np.vstack([Ai, Ab])
+    return np.vstack([Ai, boundary_matrix(cfg)])
 
 
 def assemble_Ac(cfg: I.Config) -> np.ndarray:
@@ -71,9 +89,10 @@ def assemble_Ac(cfg: I.Config) -> np.ndarray:
     return assemble_rows(cfg, np.stack([X.ravel(), Y.ravel()], axis=1), kind)
 
 
-def boundary_row(cfg: I.Config, pt, window: int | None = None) -> np.ndarray:
-    """One boundary row beta * phi_j(x_b) (used for sampled parity at full size)."""
-    return cfg.boundary_weight * assemble_rows(cfg, np.asarray(pt, dtype=np.float64)[None, :], "value")[0]
+def boundary_row(cfg: I.Config, pt, window: int | None = None, coef=None) -> np.ndarray:
+    """One boundary row (used for sampled parity at full size)."""
+    pt = np.asarray(pt, dtype=np.float64)[None, :]
+    return boundary_matrix(cfg, pt, None if coef is None else np.asarray(coef, dtype=np.float64)[None, :])[0]
 
 
 def A_row_entries(cfg: I.Config, i_grid, half_width: int = 40):

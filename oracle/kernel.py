@@ -15,6 +15,14 @@ def phi(r, eps):
     return np.exp(-(eps * eps) * r * r)
 
 
+def phi1(r, eps):
+    """First derivative of Eq. (rbf): phi'(r) = -2 eps^2 r exp(-eps^2 r^2) -- the
+    Neumann rows n . grad phi_j of the flower example."""
+    r = np.asarray(r)
+    e2 = eps * eps
+    return -2.0 * e2 * r * np.exp(-e2 * r * r)
+
+
 def phi2(r, eps):
     """Second derivative: phi''(r) = -2 eps^2 exp(-eps^2 r^2) (1 - 2 eps^2 r^2)."""
     r = np.asarray(r)
@@ -31,16 +39,16 @@ def _m_max(eps: float, T: float) -> int:
 def periodized(x, eps, T, order: int = 0):
     """phi^per(x) = sum_m phi(x - 2 m T), PAPER.md:58-59 Eq. (periodic_rbf).
 
-    order 0 -> phi, order 2 -> phi'' (the periodisation of the
+    order 0 -> phi, 1 -> phi', 2 -> phi'' (the periodisation of the
     derivative is the derivative of the periodisation, term by term).
     All non-underflowing translates are summed.
     """
     x = np.asarray(x)
     if x.dtype != np.longdouble:
         x = x.astype(np.float64)
-    f = phi if order == 0 else phi2
-    if order not in (0, 2):
-        raise ValueError("order must be 0 or 2")
+    if order not in (0, 1, 2):
+        raise ValueError("order must be 0, 1 or 2")
+    f = (phi, phi1, phi2)[order]
     center = np.round(x / (2.0 * T))
     mm = _m_max(eps, T)
     out = np.zeros_like(x)

@@ -23,7 +23,8 @@ class PlanDesc(C.Structure):
                 ("eps", C.c_double), ("op", C.c_int32), ("row_scale", C.c_double),
                 ("mask", C.c_void_p), ("n_boundary", C.c_int64), ("boundary_xy", C.c_void_p),
                 ("boundary_weight", C.c_double), ("zstar_rcond", C.c_double), ("seed", C.c_uint64),
-                ("k0sq", C.c_double), ("n_y", C.c_int64), ("T_y", C.c_double)]
+                ("k0sq", C.c_double), ("n_y", C.c_int64), ("T_y", C.c_double),
+                ("boundary_coef", C.c_void_p)]
 
 
 class PlanInfo(C.Structure):

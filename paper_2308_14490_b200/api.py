@@ -52,7 +52,7 @@ class Plan:
     def __init__(self, *, dim: int, n: int, L: int, T: float, eps: float, op: int = 0,
                  row_scale: float = 1.0, mask: np.ndarray, boundary_xy: Optional[np.ndarray] = None,
                  boundary_weight: float = 0.0, zstar_rcond: float = 1e-10, seed: int = 0, k0sq: float = 0.0,
-                 n_y: int = 0, T_y: float = 0.0, stream=None):
+                 n_y: int = 0, T_y: float = 0.0, boundary_coef: Optional[np.ndarray] = None, stream=None):
         self._mask = np.ascontiguousarray(mask, dtype=np.uint8)
         bxy = np.zeros((0, 2)) if boundary_xy is None else boundary_xy
         self._bxy = np.ascontiguousarray(bxy, dtype=np.float64)
@@ -61,6 +61,10 @@ class Plan:
         d.op, d.row_scale = op, row_scale
         d.k0sq = k0sq
         d.n_y, d.T_y = n_y, T_y
+        self._bcoef = None if boundary_coef is None else np.ascontiguousarray(boundary_coef, dtype=np.float64)
+        if self._bcoef is not None and self._bcoef.shape != (self._bxy.shape[0], 4):
+            raise ValueError("boundary_coef must be (n_boundary, 4): [a, b, n_x, n_y] per point")
+        d.boundary_coef = self._bcoef.ctypes.data if self._bcoef is not None else None
         d.mask = self._mask.ctypes.data
         d.n_boundary = self._bxy.shape[0]
         d.boundary_xy = self._bxy.ctypes.data if self._bxy.shape[0] else None
@@ -86,7 +90,7 @@ class Plan:
                    boundary_xy=I.boundary_points(cfg) if cfg.n_boundary else None,
                    boundary_weight=cfg.boundary_weight, zstar_rcond=cfg.tol, seed=cfg.seed,
                    k0sq=getattr(cfg, "k0sq", 0.0), n_y=cfg.n_y if cfg.dim == 2 else 0,
-                   T_y=cfg.T_y if cfg.dim == 2 else 0.0, stream=stream)
+                   T_y=cfg.T_y if cfg.dim == 2 else 0.0, boundary_coef=I.boundary_coefs(cfg), stream=stream)
 
     def close(self):
         if getattr(self, "_h", None):

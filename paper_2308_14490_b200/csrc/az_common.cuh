@@ -86,6 +86,7 @@ AZ_HD double az_phi_per(double x, double eps, double T, int order) {
   for (int d = -mm; d <= mm; ++d) {
     const double r = x0 - d * P;
     double t = exp(-e2 * r * r);
+    if (order == 1) t *= -2.0 * e2 * r;
     if (order == 2) t *= -2.0 * e2 * (1.0 - 2.0 * e2 * r * r);
     acc += t;
   }

@@ -288,13 +288,16 @@ __global__ void k2_boundary_rows(P2 a) {
   const Cols cc = pair_cols(a, b);
   const cplx* C1b = a.C1 + (int64_t)b * a.N;
   const int n = a.n, ny = a.ny, W = a.win, Wy = a.win_y;
-  const double* wx = a.bw + (2 * bp) * 64;
-  const double* wy = a.bw + (2 * bp + 1) * 64;
+  // Robin form (k_stencil2): weight of centre (t, l) = P[t] Y0[l] + Q[t] Y1[l]
+  const double* wP = a.bw + (4 * bp + 0) * 64;
+  const double* wY0 = a.bw + (4 * bp + 1) * 64;
+  const double* wQ = a.bw + (4 * bp + 2) * 64;
+  const double* wY1 = a.bw + (4 * bp + 3) * 64;
   const int jx0 = a.bj[2 * bp], jy0 = a.bj[2 * bp + 1];
   cplx acc = czero();
   for (int l = lane; l < Wy; l += 32) {
     const int jy = ((jy0 + l) % ny + ny) % ny;
-    const double py = wy[l];
+    const double y0 = wY0[l], y1 = wY1[l];
     for (int t = 0; t < W; ++t) {
       const int jx = ((jx0 + t) % n + n) % n;
       const int64_t i = (int64_t)jx * ny + jy;
@@ -305,7 +308,7 @@ __global__ void k2_boundary_rows(P2 a) {
       } else {
         w = C1b[i];
       }
-      acc = cadd(acc, cscale(w, wx[t] * py));
+      acc = cadd(acc, cscale(w, fma(wP[t], y0, wQ[t] * y1)));
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -330,18 +333,20 @@ __global__ void k2_boundary_adjoint(P2 a) {
   const int bp = blockIdx.x, b = blockIdx.y, lane = threadIdx.x;
   const Cols cc = pair_cols(a, b);
   const int n = a.n, ny = a.ny, W = a.win, Wy = a.win_y;
-  const double* wx = a.bw + (2 * bp) * 64;
-  const double* wy = a.bw + (2 * bp + 1) * 64;
+  const double* wP = a.bw + (4 * bp + 0) * 64;
+  const double* wY0 = a.bw + (4 * bp + 1) * 64;
+  const double* wQ = a.bw + (4 * bp + 2) * 64;
+  const double* wY1 = a.bw + (4 * bp + 3) * 64;
   const int jx0 = a.bj[2 * bp], jy0 = a.bj[2 * bp + 1];
   const int64_t r = a.M + bp;
   const double vre = a.beta * a.in[r + cc.cre * a.ldin];
   const double vim = cc.has_im ? a.beta * a.in[r + cc.cim * a.ldin] : 0.0;
   for (int l = lane; l < Wy; l += 32) {
     const int jy = ((jy0 + l) % ny + ny) % ny;
-    const double py = wy[l];
+    const double y0 = wY0[l], y1 = wY1[l];
     for (int t = 0; t < W; ++t) {
       const int jx = ((jx0 + t) % n + n) % n;
-      const double w = wx[t] * py;
+      const double w = fma(wP[t], y0, wQ[t] * y1);
       const int64_t i = (int64_t)jx * ny + jy;
       atomicAdd(&a.out[i + cc.cre * a.ldout], vre * w);
       if (cc.has_im) atomicAdd(&a.out[i + cc.cim * a.ldout], vim * w);

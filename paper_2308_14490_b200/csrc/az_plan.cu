@@ -236,6 +236,46 @@ __global__ void k_stencil(const double* bxy, int64_t Mb, int dim, int d, int n, 
   }
 }
 
+// 2-D boundary rows in Robin form beta (a phi_j + b n . grad phi_j)(x_b) (PAPER.md:736-737 Dirichlet,
+// 839-846 Neumann): per point the x window [jx0, jx0 + win) and y window [jy0, jy0 + win_y) and four
+// separable weight vectors, row value = sum_t sum_l w[jx][jy] (P[t] Y0[l] + Q[t] Y1[l]) with
+//   P = a phi(x - c_x) + b n_x phi'(x - c_x),  Y0 = phi(y - c_y),  Q = phi(x - c_x),  Y1 = b n_y phi'(y - c_y).
+__global__ void k_stencil2(const double* bxy, const double* coef, int64_t Mb, int nx, int ny, double Tx, double Ty,
+                           double eps, int winx, int winy, double* bw, int32_t* bj) {
+  const int b = blockIdx.x, t = threadIdx.x;
+  if (b >= Mb) return;
+  const double x = bxy[2 * b], y = bxy[2 * b + 1];
+  const double ca = coef ? coef[4 * b] : 1.0, cb = coef ? coef[4 * b + 1] : 0.0;
+  const double nxv = coef ? coef[4 * b + 2] : 0.0, nyv = coef ? coef[4 * b + 3] : 0.0;
+  const double hx = 2.0 * Tx / nx, hy = 2.0 * Ty / ny;
+  const int jx0 = (int)rint((x + Tx) / hx) - (winx - 1) / 2;
+  const int jy0 = (int)rint((y + Ty) / hy) - (winy - 1) / 2;
+  if (t == 0) {
+    bj[2 * b] = jx0;
+    bj[2 * b + 1] = jy0;
+  }
+  if (t < 64) {
+    double P = 0.0, Q = 0.0, Y0 = 0.0, Y1 = 0.0;
+    if (t < winx) {
+      const int j = ((jx0 + t) % nx + nx) % nx;
+      const double r = x - (-Tx + j * hx);
+      const double f0 = az_phi_per(r, eps, Tx, 0);
+      Q = f0;
+      P = ca * f0 + (cb != 0.0 ? cb * nxv * az_phi_per(r, eps, Tx, 1) : 0.0);
+    }
+    if (t < winy) {
+      const int j = ((jy0 + t) % ny + ny) % ny;
+      const double r = y - (-Ty + j * hy);
+      Y0 = az_phi_per(r, eps, Ty, 0);
+      Y1 = cb != 0.0 ? cb * nyv * az_phi_per(r, eps, Ty, 1) : 0.0;
+    }
+    bw[(4 * b + 0) * 64 + t] = P;
+    bw[(4 * b + 1) * 64 + t] = Y0;
+    bw[(4 * b + 2) * 64 + t] = Q;
+    bw[(4 * b + 3) * 64 + t] = Y1;
+  }
+}
+
 struct SymArgs {
   const cplx* W0;
   const cplx* W2;
@@ -393,13 +433,26 @@ static az_status_t plan_build(az_plan_s* p, const az_plan_desc_t* d, cudaStream_
       az_set_error("boundary stencil wider than 64 centres (eps*h too small)");
       return AZ_ERR_NOT_SUPPORTED;
     }
-    AZ_TRY(dalloc(&p->d_bw, p->Mb * 2 * 64));
-    AZ_TRY(dalloc(&p->d_bj, p->Mb * 2));
-    for (int d = 0; d < p->dim; ++d) {
-      const int64_t nn = d == 0 ? p->n : p->ny;
-      const double TT = d == 0 ? p->T : p->Ty;
-      k_stencil<<<(unsigned)p->Mb, 64, 0, st>>>(p->d_bxy, p->Mb, p->dim, d, (int)nn, TT, 2.0 * TT / (double)nn, p->eps,
-                                                d == 0 ? p->win : p->win_y, p->d_bw, p->d_bj);
+    if (p->dim == 2) {
+      AZ_TRY(dalloc(&p->d_bw, p->Mb * 4 * 64));
+      AZ_TRY(dalloc(&p->d_bj, p->Mb * 2));
+      double* d_coef = nullptr;
+      if (d->boundary_coef) {
+        AZ_TRY(dalloc(&d_coef, p->Mb * 4));
+        AZ_CUDA_CHECK(cudaMemcpyAsync(d_coef, d->boundary_coef, p->Mb * 4 * sizeof(double), cudaMemcpyHostToDevice, st));
+      }
+      k_stencil2<<<(unsigned)p->Mb, 64, 0, st>>>(p->d_bxy, d_coef, p->Mb, (int)p->n, (int)p->ny, p->T, p->Ty, p->eps,
+                                                 p->win, p->win_y, p->d_bw, p->d_bj);
+      AZ_LAUNCH_CHECK();
+      if (d_coef) {
+        AZ_CUDA_CHECK(cudaStreamSynchronize(st));
+        cudaFree(d_coef);
+      }
+    } else {
+      AZ_TRY(dalloc(&p->d_bw, p->Mb * 2 * 64));
+      AZ_TRY(dalloc(&p->d_bj, p->Mb * 2));
+      k_stencil<<<(unsigned)p->Mb, 64, 0, st>>>(p->d_bxy, p->Mb, p->dim, 0, (int)p->n, p->T, 2.0 * p->T / (double)p->n,
+                                                p->eps, p->win, p->d_bw, p->d_bj);
       AZ_LAUNCH_CHECK();
     }
   }
@@ -504,6 +557,7 @@ extern "C" az_status_t az_plan_create(const az_plan_desc_t* d, void* stream, az_
   AZ_ARG(d->n_boundary >= 0, "n_boundary < 0");
   AZ_ARG(d->n_boundary == 0 || d->boundary_xy, "boundary points missing");
   AZ_ARG(d->zstar_rcond >= 0 && d->zstar_rcond < 1, "zstar_rcond must be in [0, 1)");
+  AZ_ARG(!d->boundary_coef || d->dim == 2, "boundary_coef (Robin / Neumann rows) is supported in 2-D only");
   const int64_t L = d->n * d->L;
   if (d->dim == 1) {
     if (d->n < 16 || d->n > (1 << 21) || (d->n_boundary != 0 && L > 2048)) {

@@ -59,6 +59,7 @@ class Config:
     eps_h: float = 0.5             # eps * h: 0.5 in every BASELINE config; the paper's regime is eps_h_paper(tau0)
     n_y: int = 0                   # 2-D anisotropic boxes: centers along y (0 = n)
     T_y: float = 0.0               # half-period along y (0 = T); the box is [-T, T) x [-T_y, T_y)
+    rhs_kind: str = ""             # "" = the family's default data; "mms" = manufactured solution (flower)
 
     @property
     def ny(self) -> int:
@@ -175,6 +176,17 @@ def _make_config(family: str, n: int, *, nrhs: int = 1, R: Optional[int] = None,
         # 4 N^x boundary points): the boundary windows differ per axis
         c = _make_config("ellipse", n, nrhs=nrhs, R=R, seed=seed, s=s, name=name or f"ellipse_bvp_n{n}")
         return dataclasses.replace(c, row_op=ROW_LAPLACIAN, boundary_weight=10.0, n_boundary=4 * n)
+    if family in ("flower", "flower_mms"):
+        # Delta u + 4 u = f on a smooth flower with a circular hole
+        # of diameter 0.2 cut out; homogeneous Neumann rows on the outer boundary (2 N points), Dirichlet
+        # rows on the inner one (N points), box [-1, 1]^2 (the paper: N = 100, 200 + 100 points).  The
+        # flower curve is not given: r = 0.7 + 0.1 cos 5 theta, hole centred at the origin (reading R29).
+        # "flower" is the paper's data (f = exp(-4((x + 0.3)^2 + y^2)^2), zero boundary data); "flower_mms"
+        # the same operator with the manufactured u = sin(2x + 3y) (inhomogeneous Neumann / Dirichlet data)
+        return Config(name or f"{family}_n{n}", 2, n, s, "flower", ROW_LAPLACIAN, nrhs,
+                      R if R is not None else 8 * n, seed, 1e-10,
+                      boundary_weight=10.0, n_boundary=3 * n, k0sq=4.0,
+                      rhs_kind="mms" if family == "flower_mms" else "")
     raise ValueError(f"unknown family {family!r}")
 
 
@@ -226,6 +238,9 @@ def _in_domain(domain: str, x: np.ndarray, y: Optional[np.ndarray] = None) -> np
         return np.hypot(x, y) <= 0.6 + 0.15 * np.cos(5.0 * np.arctan2(y, x))
     if domain == "ellipse":
         return x * x + 4.0 * y * y <= 1.0
+    if domain == "flower":
+        rr = np.hypot(x, y)
+        return (rr <= flower_radius(np.arctan2(y, x))) & (rr >= FLOWER_HOLE)
     if domain == "ellipse_t":
         return 4.0 * x * x + y * y <= 1.0
     raise ValueError(domain)
@@ -257,12 +272,52 @@ def star_radius(theta: np.ndarray) -> np.ndarray:
     return 0.6 + 0.15 * np.cos(5.0 * theta)
 
 
+FLOWER_HOLE = 0.1      # radius of the cut-out circle (diameter 0.2, PAPER.md:846)
+
+
+def flower_radius(theta: np.ndarray) -> np.ndarray:
+    return 0.7 + 0.1 * np.cos(5.0 * theta)
+
+
+def _flower_outer(m: int):
+    """m points on the flower curve, theta_k = 2 pi k / m, and the outward unit normals."""
+    th = 2.0 * np.pi * np.arange(m, dtype=np.float64) / m
+    r = flower_radius(th)
+    dr = -0.5 * np.sin(5.0 * th)
+    tx, ty = dr * np.cos(th) - r * np.sin(th), dr * np.sin(th) + r * np.cos(th)
+    nrm = np.hypot(tx, ty)
+    return np.stack([r * np.cos(th), r * np.sin(th)], axis=1), np.stack([ty / nrm, -tx / nrm], axis=1)
+
+
+def _flower_inner(m: int):
+    """m points on the hole's circle and the normals pointing out of the domain (into the hole)."""
+    th = 2.0 * np.pi * np.arange(m, dtype=np.float64) / m
+    c, s_ = np.cos(th), np.sin(th)
+    return np.stack([FLOWER_HOLE * c, FLOWER_HOLE * s_], axis=1), np.stack([-c, -s_], axis=1)
+
+
+def boundary_coefs(cfg: "Config") -> Optional[np.ndarray]:
+    """(M_b, 4) rows [a, b, n_x, n_y]: boundary row b is beta (a phi_j + b n . grad phi_j)(x_b)
+    (Robin form; Dirichlet a = 1, b = 0; Neumann a = 0, b = 1/eps -- reading R29 scales the normal
+    derivative by 1/eps so both row kinds are O(1)).  None: every boundary row is Dirichlet."""
+    if cfg.domain != "flower" or cfg.n_boundary == 0:
+        return None
+    no, ni = 2 * cfg.n, cfg.n
+    _, nout = _flower_outer(no)
+    _, nin = _flower_inner(ni)
+    co = np.concatenate([np.zeros((no, 1)), np.full((no, 1), 1.0 / cfg.eps), nout], axis=1)
+    ci = np.concatenate([np.ones((ni, 1)), np.zeros((ni, 1)), nin], axis=1)
+    return np.ascontiguousarray(np.vstack([co, ci]))
+
+
 def boundary_points(cfg: Config) -> np.ndarray:
     """(M_b, 2) boundary points, theta_k = 2 pi k / M_b (SURVEY.md §8(c-4) #12)."""
     if cfg.n_boundary == 0:
         return np.zeros((0, max(cfg.dim, 1)), dtype=np.float64)
     if cfg.domain == "ode":
         return np.array([[-1.0], [1.0]])
+    if cfg.domain == "flower":
+        return np.vstack([_flower_outer(2 * cfg.n)[0], _flower_inner(cfg.n)[0]])
     th = 2.0 * np.pi * np.arange(cfg.n_boundary, dtype=np.float64) / cfg.n_boundary
     if cfg.domain == "ellipse":
         return np.stack([np.cos(th), 0.5 * np.sin(th)], axis=1)
@@ -285,6 +340,9 @@ def exact_functions(cfg: Config) -> List[Callable]:
     if cfg.row_op == ROW_LAPLACIAN and cfg.dim == 1:
         kk = cfg.n / 5.0
         return [lambda x: np.sin(kk * x)]
+    if cfg.domain == "flower":
+        # the paper's flower problem has no closed-form solution: only the manufactured variant does
+        return [lambda x, y: np.sin(2 * x + 3 * y)] if cfg.rhs_kind == "mms" else []
     if cfg.row_op == ROW_LAPLACIAN:
         return [lambda x, y: np.sin(3 * x) * np.cos(2 * y)]
     if cfg.dim == 1:
@@ -323,6 +381,18 @@ def rhs(cfg: Config) -> np.ndarray:
         b[:M, 0] = 0.0
         b[M:, 0] = cfg.boundary_weight * fns[0](boundary_points(cfg)[:, 0])
         return b
+    if cfg.domain == "flower":
+        bp, bc = boundary_points(cfg), boundary_coefs(cfg)
+        if cfg.rhs_kind == "mms":
+            # u = sin(2x + 3y): Delta u + k0^2 u = (k0^2 - 13) u; n . grad u = (2 n_x + 3 n_y) cos(2x + 3y)
+            b[:M, 0] = cfg.row_scale * (cfg.k0sq - 13.0) * np.sin(2 * pts[:, 0] + 3 * pts[:, 1])
+            u = np.sin(2 * bp[:, 0] + 3 * bp[:, 1])
+            dn = (2 * bc[:, 2] + 3 * bc[:, 3]) * np.cos(2 * bp[:, 0] + 3 * bp[:, 1])
+            b[M:, 0] = cfg.boundary_weight * (bc[:, 0] * u + bc[:, 1] * dn)
+        else:
+            # f = exp(-4((x + 0.3)^2 + y^2)^2), homogeneous boundary data
+            b[:M, 0] = cfg.row_scale * np.exp(-4.0 * ((pts[:, 0] + 0.3) ** 2 + pts[:, 1] ** 2) ** 2)
+        return b
     if cfg.row_op == ROW_LAPLACIAN:
         b[:M, 0] = cfg.row_scale * _laplacian_of_u(pts[:, 0], pts[:, 1], cfg.k0sq)
         bp = boundary_points(cfg)
@@ -354,7 +424,9 @@ def test_grid(cfg: Config, points_1d: Optional[int] = None) -> TestGrid:
         ex = np.stack([f(t) for f in fns], axis=1)
         return TestGrid((t,), inside, ex)
     m = points_1d or 401
-    if cfg.domain == "ellipse":
+    if cfg.domain == "flower":
+        t = u = np.linspace(-0.9, 0.9, m)
+    elif cfg.domain == "ellipse":
         t, u = np.linspace(-1.0, 1.0, m), np.linspace(-0.5, 0.5, (m + 1) // 2)
     elif cfg.domain == "ellipse_t":
         t, u = np.linspace(-0.5, 0.5, (m + 1) // 2), np.linspace(-1.0, 1.0, m)
@@ -364,7 +436,8 @@ def test_grid(cfg: Config, points_1d: Optional[int] = None) -> TestGrid:
         u = t
     X, Y = np.meshgrid(t, u, indexing="ij")
     inside = _in_domain(cfg.domain, X, Y)
-    ex = np.stack([f(X[inside], Y[inside]) for f in fns], axis=1)
+    ex = (np.stack([f(X[inside], Y[inside]) for f in fns], axis=1) if fns else
+          np.zeros((int(inside.sum()), 0)))
     return TestGrid((t, u), inside, ex)
 
 

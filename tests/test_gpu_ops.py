@@ -42,6 +42,9 @@ CASES = [
     ("ellipse_t_n16", I.make_config("ellipse_t", 16)),
     ("ellipse_bvp_n32", I.make_config("ellipse_bvp", 32)),
     ("ellipse_paper_n16", I.make_config("ellipse", 16, eps_h=I.eps_h_paper(1e-5))),
+    # Helmholtz on the flower with a hole, Neumann (outer) + Dirichlet (inner) rows
+    ("flower_n16", I.make_config("flower", 16)),
+    ("flower_mms_n32", I.make_config("flower_mms", 32)),
 ]
 
 

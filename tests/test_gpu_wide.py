@@ -87,7 +87,11 @@ WIDE_CASES = [("disk_n32", I.make_config("disk", 32), 8),
               ("ellipse_n32", I.make_config("ellipse", 32), 8),
               ("ellipse_t_n16", I.make_config("ellipse_t", 16), 8),
               ("ellipse_bvp_n32", I.make_config("ellipse_bvp", 32), 8),
-              ("ellipse_n64", I.make_config("ellipse", 64), 8)]
+              ("ellipse_n64", I.make_config("ellipse", 64), 8),
+              # the flower (Neumann + Dirichlet rows), the paper's data and the
+              # manufactured variant
+              ("flower_n32", I.make_config("flower", 32), 8),
+              ("flower_mms_n32", I.make_config("flower_mms", 32), 8)]
 
 
 @pytest.mark.parametrize("name,cfg,max_blocks", WIDE_CASES, ids=[c[0] for c in WIDE_CASES])

@@ -59,6 +59,24 @@ def test_phi2_matches_finite_difference(eps):
     assert np.max(np.abs(fd - ex)) / scale < 1e-4
 
 
+@pytest.mark.parametrize("eps", [1.0, 3.0, 64.0])
+def test_phi1_matches_finite_difference_and_is_odd(eps):
+    """The order-1 periodisation (Neumann rows) is the derivative of phi^per:
+    4th-order central differences of order 0 agree, it is odd and 2T-periodic, and its sum over a
+    full period of samples vanishes (the derivative of a periodic function has zero mean)."""
+    rng = np.random.default_rng(2)
+    x = rng.uniform(-1, 1, 100)
+    h = 1e-3 / max(1.0, eps / 4)
+    f = lambda t: K.periodized(t, eps, 1.0)
+    fd = (-f(x + 2 * h) + 8 * f(x + h) - 8 * f(x - h) + f(x - 2 * h)) / (12 * h)
+    ex = K.periodized(x, eps, 1.0, 1)
+    assert np.max(np.abs(fd - ex)) / eps < 1e-7
+    assert np.allclose(K.periodized(-x, eps, 1.0, 1), -ex, rtol=1e-13, atol=1e-13 * eps)
+    assert np.allclose(K.periodized(x + 2.0, eps, 1.0, 1), ex, rtol=1e-12, atol=1e-12 * eps)
+    g = np.arange(-512, 512) / 512.0
+    assert abs(K.periodized(g, min(eps, 8.0), 1.0, 1).sum()) < 1e-10 * min(eps, 8.0)
+
+
 @pytest.mark.parametrize("order", [0, 2])
 def test_periodicity_and_evenness(order):
     x = np.linspace(-3, 3, 77)
