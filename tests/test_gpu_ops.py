@@ -172,14 +172,20 @@ def test_probe_generator_bitwise_reproducible(setup):
     assert torch.equal(s1[:, 2:4], s3)
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
-def test_full_size_sampled_and_normwise(name):
+FULL_CASES = [(n, I.get_config(n)) for n in ("c2", "c3", "c4", "c5")] + [
+    # the largest sizes the plan accepts: 1-D n = 2^21 (four-step 2048 x 1024), 2-D n = 1024 (2048^2 grid)
+    ("interval_n2^21", I.make_config("interval", 1 << 21, nrhs=3)),
+    ("disk_n1024", I.make_config("disk", 1024, nrhs=1)),
+]
+
+
+@pytest.mark.parametrize("name,cfg", FULL_CASES, ids=[c[0] for c in FULL_CASES])
+def test_full_size_sampled_and_normwise(name, cfg):
     """BASELINE full sizes (c2: n = 2^20, fine grid 2^21; c3/c4/c5: 256^2 / 128^2 / 512^2 centres)
     in the bench's launch configuration: sampled rows of A x against the windowed exact row sums
     (interior and, for c4, boundary rows), and the composite operators against the FFT oracle
     normwise (reading R9)."""
     from paper_2308_14490_b200.api import Plan
-    cfg = I.get_config(name)
     plan = Plan.from_config(cfg)
     prob = OA.make_problem(cfg, "fft")
     rng = np.random.default_rng(0)
@@ -211,3 +217,50 @@ def test_full_size_sampled_and_normwise(name):
     refz = prob.apply_Zstar(b)
     for c in range(b.shape[1]):
         assert np.linalg.norm(z[:, c] - refz[:, c]) <= 1e-12 * plan.zstar_norm * np.linalg.norm(b[:, c])
+
+
+def _plan_kwargs(cfg, **over):
+    kw = dict(dim=cfg.dim, n=cfg.n, L=cfg.s, T=cfg.T, eps=cfg.eps, op=cfg.row_op, row_scale=cfg.row_scale,
+              mask=I.mask(cfg).reshape(-1), boundary_xy=I.boundary_points(cfg) if cfg.n_boundary else None,
+              boundary_weight=cfg.boundary_weight, zstar_rcond=cfg.tol, seed=cfg.seed)
+    kw.update(over)
+    return kw
+
+
+@pytest.mark.parametrize("case", ["n_not_pow2", "n_too_large_1d", "n_too_large_2d", "L_3_in_2d", "ny_ratio_4",
+                                  "no_oversampling", "rcond_1", "robin_in_1d"])
+def test_plan_create_rejects_unsupported(case):
+    """Argument and size errors come back as status codes before any launch (az.h conventions)."""
+    from paper_2308_14490_b200._lib import AZError
+    from paper_2308_14490_b200.api import Plan
+    c1, d = I.make_config("interval", 64), I.make_config("disk", 16)
+    bad = {
+        "n_not_pow2": lambda: Plan(**_plan_kwargs(c1, n=48, mask=np.ones(96, np.uint8))),
+        "n_too_large_1d": lambda: Plan(**_plan_kwargs(c1, n=1 << 22, mask=np.ones(1 << 23, np.uint8))),
+        "n_too_large_2d": lambda: Plan(**_plan_kwargs(d, n=2048, mask=np.ones(4096 * 4096, np.uint8))),
+        "L_3_in_2d": lambda: Plan(**_plan_kwargs(d, L=3, mask=np.ones(48 * 48, np.uint8))),
+        "ny_ratio_4": lambda: Plan(**_plan_kwargs(d, n_y=64, mask=np.ones(32 * 128, np.uint8))),
+        "no_oversampling": lambda: Plan(**_plan_kwargs(c1, L=1, mask=np.ones(64, np.uint8))),
+        "rcond_1": lambda: Plan(**_plan_kwargs(c1, zstar_rcond=1.0)),
+        "robin_in_1d": lambda: Plan(**_plan_kwargs(I.make_config("ode", 64), boundary_xy=np.array([[-1.0], [1.0]]),
+                                                   boundary_coef=np.zeros((2, 4)))),
+    }[case]
+    with pytest.raises(AZError):
+        bad()
+
+
+def test_box_step1_operator_vanishes():
+    """Degenerate case of the method: Omega = the whole periodic box (E = R = I), where A Z* A = A
+    (Z* is the pseudo-inverse of A^c), so the step-1 operator and the step-1
+    right-hand side of data in the range of A vanish to rounding and the sketch has rank 0."""
+    from paper_2308_14490_b200.api import Plan
+    for cfg in (I.make_config("box1d", 4096), I.make_config("box2d", 32)):
+        plan = Plan.from_config(cfg)
+        v = I.gaussian_matrix(cfg.N, 3, 1)
+        y = _host(plan.apply_step1(_dev(v)))
+        Av = _host(plan.apply_A(_dev(v)))
+        assert np.linalg.norm(y) <= 1e-11 * plan.zstar_norm * plan.sigma_max * np.linalg.norm(Av)
+        # data in the range of A (the periodic box has no boundary, so f must be representable)
+        b = Av + 0.0
+        r = _host(plan.apply_resid(_dev(b)))
+        assert np.linalg.norm(r) <= 1e-11 * plan.zstar_norm * plan.sigma_max * np.linalg.norm(b)
