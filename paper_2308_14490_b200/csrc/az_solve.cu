@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "az_internal.h"
+#include "az_mma.cuh"
 
 // ------------------------------------------------------------------------------------------
 // x (+)= Omega[:, col0 : col0 + ncols] y   (a9 of SURVEY.md §8(a))
@@ -451,70 +452,104 @@ __global__ void k_omega_fill(int64_t N, int64_t col0, int64_t ncols, double* Om,
   if (2 * m + 1 < N) Om[j * N + 2 * m + 1] = z.y;
 }
 
-// Y (m x n) = A (m x k, ld lda) B (k x n, ld ldb), n <= 64 per grid column; 64 x 64 tiles, FP64 FMA
+// The two factored-solve products for many right-hand sides on the FP64 tensor path (DMMA
+// m8n8k4; same FP64 peak as DFMA on B200, but 256 multiply-adds per warp instruction).
+//
+// Y (m x n) = A (m x k, ld lda) B (k x n, ld ldb): CTA tile 64 rows x 64 columns, k in steps of 32;
+// warps 2 (rows) x 4 (columns), 32 x 16 each.
+constexpr int GS = 36;   // operand tile stride (== 4 mod 16: conflict-free fragments)
 __global__ void __launch_bounds__(256) k_gemm_mn(const double* A, int64_t lda, const double* Bm, int64_t ldb, double* Y,
                                                  int64_t ldy, int64_t m, int64_t k, int64_t n) {
-  __shared__ double As[16][65], Bs[16][65];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  __shared__ double As[32 * 68];   // KMAJ [k][row], stride 68 (== 4 mod 16)
+  __shared__ double Bs[32 * 68];   // KMAJ [k][col]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wm = w & 1, wn = w >> 1;
   const int64_t r0 = (int64_t)blockIdx.x * 64, c0 = (int64_t)blockIdx.y * 64;
-  double acc[4][4] = {};
-  for (int64_t k0 = 0; k0 < k; k0 += 16) {
-    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
-      const int kk = e / 64, rr = e % 64;
-      As[kk][rr] = (r0 + rr < m && k0 + kk < k) ? A[(k0 + kk) * lda + r0 + rr] : 0.0;
-      const int cc = e / 16, k2 = e % 16;
-      Bs[k2][cc] = (c0 + cc < n && k0 + k2 < k) ? Bm[(c0 + cc) * ldb + k0 + k2] : 0.0;
+  double acc[4][2][2];
+  acc_zero(acc);
+  for (int64_t k0 = 0; k0 < k; k0 += 32) {
+    __syncthreads();
+    for (int e = tid; e < 32 * 64; e += 256) {
+      const int kk = e >> 6, i = e & 63;      // A: rows contiguous in memory
+      As[kk * 68 + i] = (r0 + i < m && k0 + kk < k) ? A[(k0 + kk) * lda + r0 + i] : 0.0;
+      const int cc = e >> 5, k2 = e & 31;     // B: k contiguous in memory
+      Bs[k2 * 68 + cc] = (c0 + cc < n && k0 + k2 < k) ? Bm[(c0 + cc) * ldb + k0 + k2] : 0.0;
     }
     __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk)
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int bb = 0; bb < 4; ++bb) acc[a][bb] = fma(As[kk][tx + 16 * a], Bs[kk][ty + 16 * bb], acc[a][bb]);
-    __syncthreads();
+    warp_mma<4, 2, KMAJ, KMAJ>(acc, As, 68, Bs, 68, wm * 32, wn * 16, 0, 32, lane);
   }
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int bb = 0; bb < 4; ++bb) {
-      const int64_t r = r0 + tx + 16 * a, cc = c0 + ty + 16 * bb;
-      if (r < m && cc < n) Y[cc * ldy + r] = acc[a][bb];
-    }
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t r = r0 + acc_row(wm * 32, i, lane), cc = c0 + acc_col(wn * 16, j, e, lane);
+        if (r < m && cc < n) Y[cc * ldy + r] = acc[i][j][e];
+      }
 }
 
-// Wpart[kc] (k x n) = A[rows of chunk kc]^T B[rows of chunk kc]: split-K over the m rows, 64 x 64
-// output tiles (A: m x k, B: m x n, column-major); FP64 FMA
+// Wpart[kc] (k x n) = A[rows of chunk kc]^T B[rows of chunk kc]  (A: m x k, B: m x n, column-major):
+// CTA tile 64 (A columns) x 64 (B columns); warps 2 x 2 x 2 (the last splits each 32-row step in
+// halves, reduced through shared memory at the end)
 __global__ void __launch_bounds__(256) k_gemm_tn_part(const double* A, int64_t lda, const double* Bm, int64_t ldb,
                                                       double* Wpart, int64_t m, int64_t k, int64_t n, int64_t kchunk) {
-  __shared__ double As[16][65], Bs[16][65];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int64_t i0 = (int64_t)blockIdx.x * 64, c0 = (int64_t)blockIdx.y * 64;
+  __shared__ double smv[2 * 64 * GS];
+  double* As = smv;                 // IMAJ [A column][row]
+  double* Bs = smv + 64 * GS;       // IMAJ [B column][row]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wm = w & 1, wn = (w >> 1) & 1, wk = w >> 2;
+  const int64_t i0 = (int64_t)blockIdx.x * 64, n0 = (int64_t)blockIdx.y * 64;
   const int64_t rb = (int64_t)blockIdx.z * kchunk, re = min(m, rb + kchunk);
-  double acc[4][4] = {};
-  for (int64_t q0 = rb; q0 < re; q0 += 16) {
-    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
-      const int rr = e % 16, cc = e / 16;
-      As[rr][cc] = (q0 + rr < re && i0 + cc < k) ? A[(i0 + cc) * lda + q0 + rr] : 0.0;
-      Bs[rr][cc] = (q0 + rr < re && c0 + cc < n) ? Bm[(c0 + cc) * ldb + q0 + rr] : 0.0;
+  double acc[4][4][2];
+  acc_zero(acc);
+  const int lk = tid & 31, li = tid >> 5;   // load slots: element (column li + 8 t, row lk)
+  double va[8], vb[8];
+  auto load = [&](int64_t rr) {
+    const int64_t r = rr + lk;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int i = li + 8 * t;
+      va[t] = (r < re && i0 + i < k) ? A[(i0 + i) * lda + r] : 0.0;
+      vb[t] = (r < re && n0 + i < n) ? Bm[(n0 + i) * ldb + r] : 0.0;
+    }
+  };
+  if (rb < re) load(rb);
+  for (int64_t rr = rb; rr < re; rr += 32) {
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      As[(li + 8 * t) * GS + lk] = va[t];
+      Bs[(li + 8 * t) * GS + lk] = vb[t];
     }
     __syncthreads();
-#pragma unroll
-    for (int rr = 0; rr < 16; ++rr)
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int bb = 0; bb < 4; ++bb) acc[a][bb] = fma(As[rr][tx + 16 * a], Bs[rr][ty + 16 * bb], acc[a][bb]);
-    __syncthreads();
+    if (rr + 32 < re) load(rr + 32);   // next tile in flight during the MMAs
+    warp_mma<4, 4, IMAJ, IMAJ>(acc, As, GS, Bs, GS, wm * 32, wn * 32, wk * 16, 16, lane);
   }
-  double* W = Wpart + (int64_t)blockIdx.z * k * n;
+  __syncthreads();
+  double* rs = smv + (w & 3) * 32 * 33;   // reduce the two row halves (scratch reuses the tiles)
+  if (wk == 1) {
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int bb = 0; bb < 4; ++bb) {
-      const int64_t i = i0 + tx + 16 * a, cc = c0 + ty + 16 * bb;
-      if (i < k && cc < n) W[cc * k + i] = acc[a][bb];
-    }
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) rs[acc_row(0, i, lane) * 33 + acc_col(0, j, e, lane)] = acc[i][j][e];
+  }
+  __syncthreads();
+  if (wk == 0) {
+    double* W = Wpart + (int64_t)blockIdx.z * k * n;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int ml = acc_row(0, i, lane), nl = acc_col(0, j, e, lane);
+          const int64_t ii = i0 + wm * 32 + ml, nn = n0 + wn * 32 + nl;
+          if (ii < k && nn < n) W[nn * k + ii] = acc[i][j][e] + rs[ml * 33 + nl];
+        }
+  }
 }
 
 // Memory-bound forms of the two factored-solve products for few right-hand sides (NR <= 8 per
