@@ -14,7 +14,7 @@ enum az_layout_t {
 };
 
 // Operation selectors shared by the pass kernels.
-enum az_op_t { OP_A = 0, OP_AT = 1, OP_ZSTAR = 2, OP_STEP1 = 3, OP_RESID = 4, OP_STEP2 = 5 };
+enum az_op_t { OP_A = 0, OP_AT = 1, OP_ZSTAR = 2, OP_STEP1 = 3, OP_RESID = 4, OP_STEP2 = 5, OP_ZSTAR_ADD = 6 };
 
 // Input sources for coefficient-space entry.
 enum az_src_t { SRC_VEC = 0, SRC_PROBE = 1 };
@@ -86,6 +86,10 @@ az_status_t az1f_apply(az_plan_s* p, int op, int src, const double* in, int64_t 
 az_status_t az1f_fft_fine_forward(az_plan_s* p, cplx* data, cudaStream_t st);
 az_status_t az1f_step2(az_plan_s* p, const double* x2, int64_t ldx2, const double* b, int64_t ldb, double* x,
                        int64_t ldx, int64_t nvec, cudaStream_t st);
+az_status_t az1f_sketch_keep(az_plan_s* p, int64_t col0, int64_t ncols, double* S, int64_t ldS, double* AOm,
+                             int64_t ldA, cudaStream_t st);
+az_status_t az1f_zstar_add(az_plan_s* p, const double* r, int64_t ldr, const double* x2, int64_t ldx2, double* x,
+                           int64_t ldx, int64_t nvec, cudaStream_t st);
 
 // --- 2-D layout (az_ops2d.cu)
 az_status_t az2_apply(az_plan_s* p, int op, int src, const double* in, int64_t ldin, double* out,

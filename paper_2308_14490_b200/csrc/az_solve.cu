@@ -137,6 +137,7 @@ struct SolveWS {
   double* sig;   // Rmax
   double* tmp;   // rows x nrhs
   double* x2;    // N x nrhs
+  double* AOm;   // rows x Rmax: A Omega kept by the sketch (four-step narrow path), else null
   void* qrws;
   size_t qrbytes;
   void* svdws;
@@ -148,6 +149,22 @@ struct SolveWS {
 };
 
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+// Y = A B (or C - A B), DMMA tiles; defined with the factored-solve kernels below
+__global__ void k_gemm_mn(const double* A, int64_t lda, const double* Bm, int64_t ldb, double* Y, int64_t ldy, int64_t m,
+                          int64_t k, int64_t n, const double* C = nullptr, int64_t ldc = 0);
+__global__ void k_gemm_mn_small(const double* A, int64_t lda, const double* Bm, int64_t ldb, double* Y, int64_t ldy,
+                                int64_t m, int k, int n, const double* C, int64_t ldc);
+
+// four-step narrow solves keep A Omega from the sketch for step 2 (AZ_KEEP_AOMEGA=0 disables)
+static bool keep_aomega() {
+  static int k = -1;
+  if (k < 0) {
+    const char* e = getenv("AZ_KEEP_AOMEGA");
+    k = e ? atoi(e) : 1;
+  }
+  return k != 0;
+}
 
 static SolveWS layout(az_plan_s* p, int64_t nrhs, int64_t R, int32_t max_blocks, char* base) {
   SolveWS w;
@@ -168,6 +185,8 @@ static SolveWS layout(az_plan_s* p, int64_t nrhs, int64_t R, int32_t max_blocks,
   w.tmp = (double*)take(sizeof(double) * rows * nrhs);
   w.x2 = (double*)take(sizeof(double) * p->N * nrhs);
   w.wide = kt > AZ_NARROW_MAX;
+  w.AOm = (!w.wide && p->layout == AZ_LAYOUT_1D_FOURSTEP && keep_aomega()) ? (double*)take(sizeof(double) * rows * Rmax)
+                                                                          : nullptr;
   if (w.wide) {
     const int64_t QBw = az_qrw_panel_width();
     w.maxpanels = max_blocks * ((R + QBw - 1) / QBw);
@@ -277,7 +296,11 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
     const int64_t kt = kp + nrhs;
     cudaEvent_t e0 = ev.e[2], e1 = ev.e[3], e2 = ev.e[4], e3 = ev.e[5];
     cudaEventRecord(e0, st);
-    AZ_TRY(az_sketch(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, st));
+    if (w.AOm)
+      AZ_TRY(az1f_sketch_keep(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, w.AOm + (nb - 1) * R * rows, rows,
+                              st));
+    else
+      AZ_TRY(az_sketch(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, st));
     if (!w.wide && !bp_in_S) {
       AzTrace tr("elementwise", st);
       k_copy_cols<<<az_div_up(rows * nrhs, 256), 256, 0, st>>>(w.bp, rows, w.S + kp * rows, rows, rows, nrhs);
@@ -350,7 +373,27 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   cudaEventRecord(ev.e[6], st);
   // ---- x2 = Omega y ; x = x2 + Z* (b - A x2) ----
   AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, p->N, 0, st));
-  AZ_TRY(step2(p, w.x2, b, ldb, x, ldx, w.tmp, nrhs, st));
+  if (w.AOm) {
+    // r = b - A x2 = b - (A Omega) y (one DMMA GEMM), then x = x2 + Z* r (three passes)
+    {
+      AzTrace tr("resid_aomega", st, 2 * rows * kp * nrhs);
+      if (kp <= 64) {
+        const size_t gs = 2 * 64 * 68 * sizeof(double);
+        AZ_CUDA_CHECK(az_smem_attr(k_gemm_mn_small, gs));
+        for (int64_t c0 = 0; c0 < nrhs; c0 += 64)
+          k_gemm_mn_small<<<(unsigned)std::min<int64_t>(az_div_up(rows, 64), 3 * 148), 256, gs, st>>>(
+              w.AOm, rows, w.y + c0 * kp, kp, w.tmp + c0 * rows, rows, rows, (int)kp,
+              (int)std::min<int64_t>(64, nrhs - c0), b + c0 * ldb, ldb);
+      } else {
+        k_gemm_mn<<<dim3(az_div_up(rows, 64), az_div_up(nrhs, 64)), 256, 0, st>>>(w.AOm, rows, w.y, kp, w.tmp, rows,
+                                                                                 rows, kp, nrhs, b, ldb);
+      }
+      AZ_LAUNCH_CHECK();
+    }
+    AZ_TRY(az1f_zstar_add(p, w.tmp, rows, w.x2, p->N, x, ldx, nrhs, st));
+  } else {
+    AZ_TRY(step2(p, w.x2, b, ldb, x, ldx, w.tmp, nrhs, st));
+  }
   cudaEventRecord(ev.e[7], st);
   if (dbg_host) fprintf(stderr, "az_solve host: all issued +%.2f ms\n", hnow() - th0);
   if (async_mode) return AZ_OK;
@@ -459,7 +502,8 @@ __global__ void k_omega_fill(int64_t N, int64_t col0, int64_t ncols, double* Om,
 // warps 2 (rows) x 4 (columns), 32 x 16 each.
 constexpr int GS = 36;   // operand tile stride (== 4 mod 16: conflict-free fragments)
 __global__ void __launch_bounds__(256) k_gemm_mn(const double* A, int64_t lda, const double* Bm, int64_t ldb, double* Y,
-                                                 int64_t ldy, int64_t m, int64_t k, int64_t n) {
+                                                 int64_t ldy, int64_t m, int64_t k, int64_t n, const double* C,
+                                                 int64_t ldc) {   // C non-null: Y = C - A B
   __shared__ double As[32 * 68];   // KMAJ [k][row], stride 68 (== 4 mod 16)
   __shared__ double Bs[32 * 68];   // KMAJ [k][col]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -485,8 +529,73 @@ __global__ void __launch_bounds__(256) k_gemm_mn(const double* A, int64_t lda, c
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int64_t r = r0 + acc_row(wm * 32, i, lane), cc = c0 + acc_col(wn * 16, j, e, lane);
-        if (r < m && cc < n) Y[cc * ldy + r] = acc[i][j][e];
+        if (r < m && cc < n) Y[cc * ldy + r] = C ? C[cc * ldc + r] - acc[i][j][e] : acc[i][j][e];
       }
+}
+
+// Y = C - A B for a tall A (m x k) and a small B (k x n), k <= 64, n <= 64 (step 2 of the four-step
+// narrow solve: r = b - (A Omega) y): B is staged in shared memory once per CTA and the CTA walks
+// row tiles of 64 (grid-stride), so the small operand is not re-read per tile.
+__global__ void __launch_bounds__(256) k_gemm_mn_small(const double* A, int64_t lda, const double* Bm, int64_t ldb,
+                                                       double* Y, int64_t ldy, int64_t m, int k, int n, const double* C,
+                                                       int64_t ldc) {
+  extern __shared__ double gsm[];
+  double* As = gsm;                // KMAJ [k][row], 64 x 68
+  double* Bs = gsm + 64 * 68;      // KMAJ [k][col]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wm = w & 1, wn = w >> 1;
+  const int kp = (k + 3) & ~3;
+  for (int e = tid; e < 64 * 64; e += 256) {
+    const int cc = e >> 6, kk = e & 63;
+    Bs[kk * 68 + cc] = (cc < n && kk < k) ? Bm[(int64_t)cc * ldb + kk] : 0.0;
+  }
+  // the next row tile's A values and this tile's C fragments are fetched into registers while the
+  // current tile's MMAs run
+  double va[16], cf[4][2][2];
+  const int li = tid & 63, lk0 = tid >> 6;   // A element (row li, k = lk0 + 4 t)
+  auto load_a = [&](int64_t r0) {
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int kk = lk0 + 4 * t;
+      va[t] = (r0 + li < m && kk < k) ? A[(int64_t)kk * lda + r0 + li] : 0.0;
+    }
+  };
+  auto load_c = [&](int64_t r0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t r = r0 + acc_row(wm * 32, i, lane);
+          const int cc = acc_col(wn * 16, j, e, lane);
+          cf[i][j][e] = (C && r < m && cc < n) ? C[(int64_t)cc * ldc + r] : 0.0;
+        }
+  };
+  const int64_t stride = (int64_t)gridDim.x * 64;
+  int64_t r0 = (int64_t)blockIdx.x * 64;
+  if (r0 < m) load_a(r0);
+  for (; r0 < m; r0 += stride) {
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 16; ++t) As[(lk0 + 4 * t) * 68 + li] = va[t];
+    __syncthreads();
+    load_c(r0);
+    if (r0 + stride < m) load_a(r0 + stride);
+    double acc[4][2][2];
+    acc_zero(acc);
+    warp_mma<4, 2, KMAJ, KMAJ>(acc, As, 68, Bs, 68, wm * 32, wn * 16, 0, kp, lane);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t r = r0 + acc_row(wm * 32, i, lane);
+          const int cc = acc_col(wn * 16, j, e, lane);
+          if (r < m && cc < n) Y[(int64_t)cc * ldy + r] = C ? cf[i][j][e] - acc[i][j][e] : acc[i][j][e];
+        }
+  }
 }
 
 // Wpart[kc] (k x n) = A[rows of chunk kc]^T B[rows of chunk kc]  (A: m x k, B: m x n, column-major):
