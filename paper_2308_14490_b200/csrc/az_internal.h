@@ -87,7 +87,7 @@ az_status_t az1f_fft_fine_forward(az_plan_s* p, cplx* data, cudaStream_t st);
 az_status_t az1f_step2(az_plan_s* p, const double* x2, int64_t ldx2, const double* b, int64_t ldb, double* x,
                        int64_t ldx, int64_t nvec, cudaStream_t st);
 az_status_t az1f_sketch_keep(az_plan_s* p, int64_t col0, int64_t ncols, double* S, int64_t ldS, double* AOm,
-                             int64_t ldA, cudaStream_t st);
+                             int64_t ldA, double* Om, int64_t ldOm, cudaStream_t st);
 az_status_t az1f_zstar_add(az_plan_s* p, const double* r, int64_t ldr, const double* x2, int64_t ldx2, double* x,
                            int64_t ldx, int64_t nvec, cudaStream_t st);
 

@@ -49,6 +49,8 @@ struct P1f {
   int64_t ldout;
   double* aux;           // FC_FINE_MASK: optional copy of (A v) on the rows (the sketch keeps A Omega)
   int64_t ldaux;
+  double* aux2;          // FC_IN_COEF with probes: optional copy of the probe columns (the sketch keeps Omega)
+  int64_t ldaux2;
   int64_t nvec, col0, pair0;
 };
 
@@ -122,6 +124,14 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
       const double send = odd ? z.x : z.y;
       const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
       v[e] = odd ? make_double2(recv, z.y) : make_double2(z.x, recv);
+    }
+    if (a.aux2) {   // Omega itself, natural row order (x2 = Omega y later reads it instead of regenerating)
+#pragma unroll
+      for (int e = 0; e < EC; ++e) {
+        const int64_t i = (int64_t)(j + e * T) * W + col;
+        a.aux2[i + cc.cre * a.ldaux2] = v[e].x;
+        if (cc.has_im) a.aux2[i + cc.cim * a.ldaux2] = v[e].y;
+      }
     }
   } else if constexpr (KIND == FC_IN_COEF) {
 #pragma unroll
@@ -487,6 +497,8 @@ static P1f make_p1f(az_plan_s* p) {
   a.out = nullptr;
   a.aux = nullptr;
   a.ldaux = 0;
+  a.aux2 = nullptr;
+  a.ldaux2 = 0;
   a.ldin = a.ldout = 0;
   a.nvec = a.col0 = a.pair0 = 0;
   return a;
@@ -567,15 +579,18 @@ az_status_t az1f_step2(az_plan_s* p, const double* x2, int64_t ldx2, const doubl
 }
 
 // The sketch S = (A - A Z* A) Omega[:, col0 .. col0 + ncols) that also keeps A Omega on the rows
-// (AOm, rows x ncols): step 2 then forms b - A x2 = b - (A Omega) y with one small GEMM instead of
+// (AOm, rows x ncols) and Omega itself (Om, N x ncols, optional): step 2 then forms x2 = Omega y and
+// b - A x2 = b - (A Omega) y with two small GEMMs instead of regenerating the probes and running
 // three FFT passes over x2.
 az_status_t az1f_sketch_keep(az_plan_s* p, int64_t col0, int64_t ncols, double* S, int64_t ldS, double* AOm,
-                             int64_t ldA, cudaStream_t st) {
+                             int64_t ldA, double* Om, int64_t ldOm, cudaStream_t st) {
   P1f a = make_p1f(p);
   a.out = S;
   a.ldout = ldS;
   a.aux = AOm;
   a.ldaux = ldA;
+  a.aux2 = Om;
+  a.ldaux2 = ldOm;
   a.nvec = ncols;
   a.col0 = col0;
   const int64_t npairs = (ncols + 1) / 2;

@@ -138,6 +138,7 @@ struct SolveWS {
   double* tmp;   // rows x nrhs
   double* x2;    // N x nrhs
   double* AOm;   // rows x Rmax: A Omega kept by the sketch (four-step narrow path), else null
+  double* Om;    // N x Rmax: Omega kept by the sketch (same condition)
   void* qrws;
   size_t qrbytes;
   void* svdws;
@@ -185,8 +186,9 @@ static SolveWS layout(az_plan_s* p, int64_t nrhs, int64_t R, int32_t max_blocks,
   w.tmp = (double*)take(sizeof(double) * rows * nrhs);
   w.x2 = (double*)take(sizeof(double) * p->N * nrhs);
   w.wide = kt > AZ_NARROW_MAX;
-  w.AOm = (!w.wide && p->layout == AZ_LAYOUT_1D_FOURSTEP && keep_aomega()) ? (double*)take(sizeof(double) * rows * Rmax)
-                                                                          : nullptr;
+  const bool keep = !w.wide && p->layout == AZ_LAYOUT_1D_FOURSTEP && keep_aomega();
+  w.AOm = keep ? (double*)take(sizeof(double) * rows * Rmax) : nullptr;
+  w.Om = keep ? (double*)take(sizeof(double) * p->N * Rmax) : nullptr;
   if (w.wide) {
     const int64_t QBw = az_qrw_panel_width();
     w.maxpanels = max_blocks * ((R + QBw - 1) / QBw);
@@ -298,7 +300,7 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
     cudaEventRecord(e0, st);
     if (w.AOm)
       AZ_TRY(az1f_sketch_keep(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, w.AOm + (nb - 1) * R * rows, rows,
-                              st));
+                              w.Om + (nb - 1) * R * p->N, p->N, st));
     else
       AZ_TRY(az_sketch(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, st));
     if (!w.wide && !bp_in_S) {
@@ -372,7 +374,18 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   if (dbg_host) fprintf(stderr, "az_solve host: svd issued +%.2f ms\n", hnow() - th0);
   cudaEventRecord(ev.e[6], st);
   // ---- x2 = Omega y ; x = x2 + Z* (b - A x2) ----
-  AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, p->N, 0, st));
+  if (w.Om && kp <= 64) {
+    AzTrace tr("omega_apply", st, p->N * kp * nrhs);   // x2 = Omega y from the kept probes
+    const size_t gs = 2 * 64 * 68 * sizeof(double);
+    AZ_CUDA_CHECK(az_smem_attr(k_gemm_mn_small, gs));
+    for (int64_t c0 = 0; c0 < nrhs; c0 += 64)
+      k_gemm_mn_small<<<(unsigned)std::min<int64_t>(az_div_up(p->N, 64), 3 * 148), 256, gs, st>>>(
+          w.Om, p->N, w.y + c0 * kp, kp, w.x2 + c0 * p->N, p->N, p->N, (int)kp, (int)std::min<int64_t>(64, nrhs - c0),
+          nullptr, 0);
+    AZ_LAUNCH_CHECK();
+  } else {
+    AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, p->N, 0, st));
+  }
   if (w.AOm) {
     // r = b - A x2 = b - (A Omega) y (one DMMA GEMM), then x = x2 + Z* r (three passes)
     {
