@@ -484,6 +484,7 @@ struct az_factor_s {
   az_vbuf_s* Svb = nullptr;   // S's virtual range (physical HBM mapped per probe block), else cudaMalloc
   double* Q1 = nullptr;    // explicit leading kp columns of Q (rows x kp): S's own columns, in place
   double* Om = nullptr;    // explicit probes Omega (N x kp), the same Philox values as on the fly
+  double* AOm = nullptr;   // four-step layout, narrow probe counts: A Omega on the rows (rows x kpmax)
   std::vector<int64_t> pj0;
   std::vector<int> pnb;
   int64_t np = 0;
@@ -872,6 +873,13 @@ extern "C" az_status_t az_factorize(az_plan_t p, double theta, int64_t R, int32_
     az_set_error("az_factorize: out of device memory");
     return fail(AZ_ERR_OUT_OF_MEMORY);
   }
+  // four-step layout with at most 64 probes: keep A Omega (step 2 of a factored solve is then one
+  // small GEMM and three FFT passes)
+  if (p->layout == AZ_LAYOUT_1D_FOURSTEP && kpmax <= 64 && keep_aomega() &&
+      cudaMalloc(&f->AOm, sizeof(double) * rows * kpmax) != cudaSuccess) {
+    cudaGetLastError();
+    f->AOm = nullptr;
+  }
   const int pfix = 10;
   double s1lo = 0.0;
   int64_t nb = 0, rank = 0;
@@ -885,7 +893,9 @@ extern "C" az_status_t az_factorize(az_plan_t p, double theta, int64_t R, int32_
       az_set_error("az_factorize: out of device memory (probe block %lld)", (long long)nb);
       return fail(AZ_ERR_OUT_OF_MEMORY);
     }
-    az_status_t s = az_sketch(p, (nb - 1) * R, R, Snew, rows, st);
+    az_status_t s = f->AOm ? az1f_sketch_keep(p, (nb - 1) * R, R, Snew, rows, f->AOm + (nb - 1) * R * rows, rows,
+                                              nullptr, 0, st)
+                           : az_sketch(p, (nb - 1) * R, R, Snew, rows, st);
     if (s != AZ_OK) return fail(s);
     cudaEventRecord(ev.e[3], st);
     if ((s = az_qrw_apply(f->S, rows, rows, f->pj0.data(), f->pnb.data(), f->Tb, 0, f->np, Snew, rows, R, qrws, qrbytes, st)) != AZ_OK ||
@@ -993,6 +1003,7 @@ extern "C" az_status_t az_factor_destroy(az_factor_t f) {
   cudaFree(f->Tb);
   cudaFree(f->P);
   cudaFree(f->Om);
+  cudaFree(f->AOm);
   delete f;
   return AZ_OK;
 }
@@ -1177,7 +1188,21 @@ extern "C" az_status_t az_solve_factored(az_factor_t f, const double* b, int64_t
     else
       AZ_TRY(nn_product(f->Om, N, N, kp, w.y, kp, w.x2, N, nrhs, w.part, st));
   }
-  AZ_TRY(step2(p, w.x2, b, ldb, x, ldx, w.tmp, nrhs, st));
+  if (f->AOm && kp <= 64) {
+    {
+      AzTrace tr("resid_aomega", st, 2 * rows * kp * nrhs);
+      const size_t gs = 2 * 64 * 68 * sizeof(double);
+      AZ_CUDA_CHECK(az_smem_attr(k_gemm_mn_small, gs));
+      for (int64_t c0 = 0; c0 < nrhs; c0 += 64)
+        k_gemm_mn_small<<<(unsigned)std::min<int64_t>(az_div_up(rows, 64), 3 * 148), 256, gs, st>>>(
+            f->AOm, rows, w.y + c0 * kp, kp, w.tmp + c0 * rows, rows, rows, (int)kp,
+            (int)std::min<int64_t>(64, nrhs - c0), b + c0 * ldb, ldb);
+      AZ_LAUNCH_CHECK();
+    }
+    AZ_TRY(az1f_zstar_add(p, w.tmp, rows, w.x2, p->N, x, ldx, nrhs, st));
+  } else {
+    AZ_TRY(step2(p, w.x2, b, ldb, x, ldx, w.tmp, nrhs, st));
+  }
   cudaEventRecord(ev.e[3], st);
   AZ_CUDA_CHECK(cudaEventSynchronize(ev.e[3]));
   if (report) {

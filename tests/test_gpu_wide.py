@@ -151,6 +151,8 @@ def test_solve_2d_full_size(name):
 
 
 FACTOR_CASES = [("c1", I.get_config("c1"), 4), ("interval_n4096_4step", I.make_config("interval", 4096, nrhs=6, R=40), 4),
+                # one probe block of <= 64 on the four-step layout: the factor keeps A Omega (step 2 as a GEMM)
+                ("interval_n8192_4step_mb1", I.make_config("interval", 8192, nrhs=6, R=48), 1),
                 ("disk_n32", I.make_config("disk", 32), 8), ("star_n32", I.make_config("star", 32), 8)]
 
 
