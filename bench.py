@@ -45,17 +45,19 @@ def measured_peaks():
 # algorithmic bytes / flops per unit (per complex vector PAIR for the pass kernels), DESIGN.md
 # "Algorithmic bytes per kernel".  n = coefficient length, L = fine length, M = rows.
 # ------------------------------------------------------------------------------------------
-def kernel_model(name, cfg, M, k_cols, k1=None):
+def kernel_model(name, cfg, M, k_cols, k1=None, kept=False):
     n = cfg.N
     L = cfg.N * cfg.s ** cfg.dim
     C = 16  # bytes per complex128
     # 1-D intervals: the mask is one run of the grid, so no row-map / mask bytes are read
     pos_b, mask_b = (0, 0) if cfg.dim == 1 else (4, 1)
+    # kept: the four-step narrow solve stores Omega (probe pass) and A Omega (mask pass) for step 2
+    kw_om, kw_aom = (2 * 8 * n, 2 * 8 * M) if kept else (0, 0)
     hbm = {
-        "1f_cols_in_coef": C * n,                      # probes generated on chip; write spectrum
+        "1f_cols_in_coef": C * n + kw_om,              # probes generated on chip; write spectrum (+ Omega)
         "1f_rows_expand_keep": 2 * C * n + C * L,
         "1f_rows_expand": C * n + C * L,
-        "1f_cols_fine_mask": 2 * C * L + mask_b * L,   # read + write fine grid, read mask (1 B)
+        "1f_cols_fine_mask": 2 * C * L + mask_b * L + kw_aom,   # fine grid in/out, mask (1 B) (+ A Omega rows)
         "1f_rows_step1": 2 * C * L + C * n + 8 * n,    # fine grid in/out, v^ and zinv in
         "1f_rows_resid": 2 * C * L + 8 * n,
         "1f_rows_zstar": C * L + C * n + 8 * n,
@@ -63,6 +65,8 @@ def kernel_model(name, cfg, M, k_cols, k1=None):
         "1f_cols_out_resid": C * L + pos_b * L + 4 * 8 * M,
         "1f_cols_in_rows": pos_b * L + 2 * 8 * M + C * L,
         "1f_cols_out_coef": C * n + 2 * 8 * n,
+        "1f_cols_out_coef_add": C * n + 4 * 8 * n,             # spectrum + x2 in, x out
+        "1f_cols_resid_mid": 2 * C * L + 2 * 8 * M,            # fine grid in/out, b rows in
     }
     if name in hbm:
         return "hbm", hbm[name]
@@ -365,7 +369,10 @@ def run_ours(args, cfg):
     kcols = reps[-1]["probes"] + cfg.nrhs
     dom = max(trace.items(), key=lambda kv: kv[1][1])
     name, (cnt, tot_ms, units) = dom
-    bound, per_unit = kernel_model(name, cfg, plan.M, kcols, reps[-1]["probes"])
+    # the four-step narrow solve keeps Omega and A Omega from the sketch (az_solve.cu keep_aomega)
+    kept = (cfg.dim == 1 and cfg.N * cfg.s > 2048 and kcols <= 128
+            and os.environ.get("AZ_KEEP_AOMEGA", "1") != "0")
+    bound, per_unit = kernel_model(name, cfg, plan.M, kcols, reps[-1]["probes"], kept)
     roof = {"kernel": name, "launches": cnt, "ms_total": tot_ms, "share_of_step": tot_ms / sum(ms)}
     if bound == "hbm":
         achieved = per_unit * units / (tot_ms * 1e-3) / 1e9
@@ -390,7 +397,7 @@ def run_ours(args, cfg):
     # aggregate HBM roofline of the FFT operator passes (SURVEY.md §8(d) pass model)
     fb, ft = 0.0, 0.0
     for k, (c_, t_, u_) in trace.items():
-        bnd, pu = kernel_model(k, cfg, plan.M, kcols)
+        bnd, pu = kernel_model(k, cfg, plan.M, kcols, kept=kept)
         if bnd == "hbm":
             fb += pu * u_
             ft += t_
