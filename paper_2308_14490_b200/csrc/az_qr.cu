@@ -73,28 +73,48 @@ __global__ void __launch_bounds__(512, 1) k_tsqr(QRIn q) {
       const int o = j & 15, cj = j >> 4;
       double* vj = vb + (j & 1) * MC;
       if (w == o) {
-        double xs[RPL];
-#pragma unroll
-        for (int r = 0; r < RPL; ++r) xs[r] = 0.0;
-#pragma unroll
-        for (int c = 0; c < KC; ++c)
-          if (c == cj) {
-#pragma unroll
-            for (int r = 0; r < RPL; ++r) {
-              xs[r] = x[c][r];
-              x[c][r] = 0.0;
-            }
-          }
-        double sig = 0.0;
-#pragma unroll
-        for (int r = 0; r < RPL; ++r) sig = fma(xs[r], xs[r], sig);
-        sig = warp_sum(sig);
+        // everyone waits at the barrier below for this chain, so it is kept short: the slot is
+        // picked with a warp-uniform switch (no select chains), alpha is loaded first, and
+        // tau = (beta - alpha) / beta = 1 + |alpha| / ||x|| comes from one reciprocal square root
         const double alpha = R[pk(j, j)];
+        double xs[RPL];
+        switch (cj) {
+#define AZ_TSQR_TAKE(C)                                   \
+  case C:                                                 \
+    if constexpr (C < KC) {                               \
+      _Pragma("unroll") for (int r = 0; r < RPL; ++r) {   \
+        xs[r] = x[C][r];                                  \
+        x[C][r] = 0.0;                                    \
+      }                                                   \
+    }                                                     \
+    break;
+          AZ_TSQR_TAKE(0)
+          AZ_TSQR_TAKE(1)
+          AZ_TSQR_TAKE(2)
+          AZ_TSQR_TAKE(3)
+          AZ_TSQR_TAKE(4)
+          AZ_TSQR_TAKE(5)
+          AZ_TSQR_TAKE(6)
+          AZ_TSQR_TAKE(7)
+#undef AZ_TSQR_TAKE
+          default:
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) xs[r] = 0.0;
+        }
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int r = 0; r < RPL; r += 2) {
+          s0 = fma(xs[r], xs[r], s0);
+          if (r + 1 < RPL) s1 = fma(xs[r + 1], xs[r + 1], s1);
+        }
+        const double sig = warp_sum(s0 + s1);
         double tau = 0.0, scale = 0.0, beta = alpha;
         if (sig > 0.0) {
-          const double nrm = sqrt(fma(alpha, alpha, sig));
+          const double s2 = fma(alpha, alpha, sig);
+          const double rinv = rsqrt(s2);
+          const double nrm = s2 * rinv;
           beta = alpha >= 0.0 ? -nrm : nrm;
-          tau = (beta - alpha) / beta;
+          tau = fma(fabs(alpha), rinv, 1.0);
           scale = 1.0 / (alpha - beta);
         }
 #pragma unroll
