@@ -196,3 +196,26 @@ def test_solve_host_pipelined_matches_solve():
     api.plan_sync(plan)
     for c, xx in zip(cs, xs):
         assert np.array_equal(xx.numpy(), c * x_ref)
+
+
+@pytest.mark.parametrize("name,cfg,max_blocks", [("interval_n8192_4step", I.make_config("interval", 8192, nrhs=3, R=48), 1),
+                                                 ("c1", I.get_config("c1"), 4),
+                                                 ("disk_n16", I.make_config("disk", 16), 8)])
+def test_solve_zero_and_single_rhs(name, cfg, max_blocks):
+    """Degenerate right-hand sides: b = 0 gives x = 0 exactly (every reflector and rotation of the
+    sketch is still applied, the right-hand-side columns stay zero), and a single right-hand side
+    (an odd vector count: the complex packing's second half is absent) matches the same column
+    solved among several."""
+    from paper_2308_14490_b200.api import Plan
+    plan = Plan.from_config(cfg)
+    theta = max(cfg.tol * 1e-2, 1e-12)
+    z = np.zeros((plan.rows, 2))
+    x0, _ = plan.solve(_dev(z), theta, cfg.R, max_blocks)
+    assert np.array_equal(_host(x0), np.zeros((cfg.N, 2)))
+    b = I.rhs(cfg)
+    xs, _ = plan.solve(_dev(b), theta, cfg.R, max_blocks)
+    x1, _ = plan.solve(_dev(b[:, :1]), theta, cfg.R, max_blocks)
+    grid = I.test_grid(cfg)
+    f = OA.evaluate(cfg, _host(x1), grid)
+    fs = OA.evaluate(cfg, _host(xs)[:, :1], grid)
+    assert np.max(np.abs(f - fs)) <= 1e-9 * np.max(np.abs(fs))
