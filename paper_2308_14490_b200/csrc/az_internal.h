@@ -99,8 +99,9 @@ az_status_t az2_apply(az_plan_s* p, int op, int src, const double* in, int64_t l
 az_status_t az_fft_batch(const cplx* tw, cplx* data, int64_t len, int64_t count, int dir, cudaStream_t st);
 
 // --- QR / SVD / solve
+// a_scratch: A may be overwritten (the solve's sketch buffer), which enables the split TSQR leaf
 az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R, int64_t ldr,
-                         void* ws, size_t ws_bytes, cudaStream_t st, int64_t k1 = 0);
+                         void* ws, size_t ws_bytes, cudaStream_t st, int64_t k1 = 0, bool a_scratch = false);
 size_t az_qr_ws_bytes(int64_t m, int64_t k);
 az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta,
                          double* y, int64_t ldy, double* sigma_out, int64_t* rank_out,

@@ -37,7 +37,13 @@ struct QRIn {
   int64_t rb;       // rows per block of the stacked input (row r at (r / rb) * bstride + (r % rb))
   int64_t bstride;
   int64_t rows_per_cta;
-  double* Rout;     // per CTA k x k column-major (ld = k)
+  double* Rout;     // per CTA k1 x k column-major (ld = k1), CTA stride ostride
+  int64_t ostride;
+  // optional (split leaf): the chunk parts y_j of the reflectors and their tau, per chunk
+  double* Y;        // y_j of chunk rows written to Y[row + j ldY] (the triangularised columns' storage)
+  int64_t ldY;
+  double* taus;     // taus[(cta cmax + chunk) k1 + j]
+  int cmax;         // chunks per CTA (ceil(rows_per_cta / MC))
 };
 
 template <int KC, int RPL>
@@ -119,6 +125,14 @@ __global__ void __launch_bounds__(512, 1) k_tsqr(QRIn q) {
         }
 #pragma unroll
         for (int r = 0; r < RPL; ++r) vj[lane + 32 * r] = xs[r] * scale;
+        if (q.Y) {   // split leaf: keep the reflector for the right-hand-side pass (k_tsqr_rhs)
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) {
+            const int64_t row = base + lane + 32 * r;
+            if (row < r1) q.Y[row + (int64_t)j * q.ldY] = xs[r] * scale;
+          }
+          if (lane == 0) q.taus[((int64_t)blockIdx.x * q.cmax + (base - r0) / MC) * q.k1 + j] = tau;
+        }
         __syncwarp();
         if (lane == 0) {
           R[pk(j, j)] = beta;
@@ -177,13 +191,129 @@ __global__ void __launch_bounds__(512, 1) k_tsqr(QRIn q) {
   __syncthreads();
   // top k1 rows of R (k1 x k, ld k1)
   const int k1 = q.k1;
-  double* Ro = q.Rout + (int64_t)blockIdx.x * k1 * k;
+  double* Ro = q.Rout + (int64_t)blockIdx.x * q.ostride;
   for (int e = threadIdx.x; e < k1 * k; e += blockDim.x) {
     const int i = e % k1, l = e / k1;
     Ro[e] = i <= l ? R[pk(i, l)] : 0.0;
   }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Split leaf, pass B: the right-hand-side columns X = b' of a CTA's row range
+// are carried through the same chunk sequence as pass A's [R; chunk] QR of the probe columns, but
+// each chunk's 64 reflectors are applied at once in compact-WY form.  With V = [I; Y] (the unit
+// R-part over the chunk part Y, MC x k1) and T from the dlarft recurrence,
+//   H_{k1-1} ... H_0 [R_b; X] :  R_b <- R_b - T^T (R_b + Y^T X)
+// (the chunk part of X is not needed afterwards: only R's rows survive a TSQR leaf).  Y^T Y (for T)
+// and Y^T X are DMMA Gram products over the chunk rows.  Same values as applying the reflectors one
+// by one, up to rounding.
+// ------------------------------------------------------------------------------------------
+struct QRr {
+  const double* Y;      // m x k1 (ld ldY): pass A's reflectors
+  int64_t ldY;
+  const double* X;      // m x nb (ld ldX): the right-hand-side columns
+  int64_t ldX;
+  int64_t m, rows_per_cta;
+  int k1, nb, MC, cmax;
+  const double* taus;
+  double* Rout;         // per CTA k1 x (k1 + nb), ld k1, CTA stride ostride: writes columns k1..
+  int64_t ostride;
+};
+
+constexpr int RR_S = 36;   // operand tile stride (== 4 mod 16)
+
+__global__ void __launch_bounds__(512, 1) k_tsqr_rhs(QRr q) {
+  extern __shared__ double sm[];
+  double* Ys = sm;                       // IMAJ [col][row], 64 x RR_S (32-row sub-block)
+  double* Xs = Ys + 64 * RR_S;           // IMAJ [col][row]
+  double* G = Xs + 64 * RR_S;            // 64 x 64 (ld 65): Y^T Y, then TG[j][m] = tau_m G[j][m]
+  double* P = G + 64 * 65;               // 64 x 64 (ld 65): Y^T X, then W = R_b + P, then d
+  double* Rb = P + 64 * 65;              // 64 x 64 (ld 65)
+  double* tau_s = Rb + 64 * 65;          // 64
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int k1 = q.k1, nb = q.nb;
+  for (int e = tid; e < 64 * 65; e += 512) Rb[e] = 0.0;
+  const int64_t r0 = (int64_t)blockIdx.x * q.rows_per_cta;
+  const int64_t r1 = min(q.m, r0 + q.rows_per_cta);
+  // warps 0-7: G tiles rows (w & 1) 32.., cols (w >> 1) 16..;  warps 8-15: the same tiles of P
+  const int ww = w & 7, wm = ww & 1, wn = ww >> 1;
+  const bool isG = w < 8;
+  double ry[4], rx[4];   // the next 32-row sub-block, in flight during the current MMAs
+  auto load = [&](int64_t rr, int64_t cend) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int e = tid + 512 * t, cidx = e >> 5, rl = e & 31;
+      const int64_t row = rr + rl;
+      const bool in = row < cend;
+      ry[t] = (in && cidx < k1) ? q.Y[row + (int64_t)cidx * q.ldY] : 0.0;
+      rx[t] = (in && cidx < nb) ? q.X[row + (int64_t)cidx * q.ldX] : 0.0;
+    }
+  };
+  int chunk = 0;
+  for (int64_t base = r0; base < r1; base += q.MC, ++chunk) {
+    const int64_t cend = min(r1, base + (int64_t)q.MC);
+    double acc[4][2][2];
+    acc_zero(acc);
+    load(base, cend);
+    if (tid < 64) tau_s[tid] = tid < k1 ? q.taus[((int64_t)blockIdx.x * q.cmax + chunk) * k1 + tid] : 0.0;
+    for (int64_t rr = base; rr < cend; rr += 32) {
+      __syncthreads();
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int e = tid + 512 * t, cidx = e >> 5, rl = e & 31;
+        Ys[cidx * RR_S + rl] = ry[t];
+        Xs[cidx * RR_S + rl] = rx[t];
+      }
+      __syncthreads();
+      if (rr + 32 < cend) load(rr + 32, cend);
+      warp_mma<4, 2, IMAJ, IMAJ>(acc, Ys, RR_S, isG ? Ys : Xs, RR_S, wm * 32, wn * 16, 0, 32, lane);
+    }
+    double* D = isG ? G : P;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          D[acc_row(wm * 32, i, lane) * 65 + acc_col(wn * 16, jj, e, lane)] = acc[i][jj][e];
+    __syncthreads();
+    // TG[j][m] = tau_m (y_j . y_m) for m < j;  W = R_b + Y^T X
+    for (int e = tid; e < 64 * 64; e += 512) {
+      const int j = e >> 6, m = e & 63;
+      G[j * 65 + m] = m < j ? tau_s[m] * G[j * 65 + m] : 0.0;
+      P[j * 65 + m] += Rb[j * 65 + m];
+    }
+    __syncthreads();
+    // Reflectors in order, per right-hand-side column c (independent): with d_m = v_m^T [R_b; X^(m)]
+    // (X^(m): X after reflectors < m; R row j is only touched by reflector j),
+    //   d_j = W[j][c] - sum_{m<j} tau_m (y_j . y_m) d_m,   R_b[j][c] -= tau_j d_j
+    if (tid < nb) {
+      const int c = tid;
+      for (int j = 0; j < k1; ++j) {
+        double s0 = P[j * 65 + c], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        const double* tg = G + j * 65;
+        int m = 0;
+        for (; m + 3 < j; m += 4) {
+          s0 = fma(-tg[m], P[m * 65 + c], s0);
+          s1 = fma(-tg[m + 1], P[(m + 1) * 65 + c], s1);
+          s2 = fma(-tg[m + 2], P[(m + 2) * 65 + c], s2);
+          s3 = fma(-tg[m + 3], P[(m + 3) * 65 + c], s3);
+        }
+        for (; m < j; ++m) s0 = fma(-tg[m], P[m * 65 + c], s0);
+        const double d = (s0 + s1) + (s2 + s3);
+        P[j * 65 + c] = d;
+        Rb[j * 65 + c] -= tau_s[j] * d;
+      }
+    }
+    __syncthreads();
+  }
+  double* Ro = q.Rout + (int64_t)blockIdx.x * q.ostride;
+  for (int e = tid; e < k1 * nb; e += 512) {
+    const int i = e % k1, c = e / k1;
+    Ro[(int64_t)(k1 + c) * k1 + i] = Rb[i * 65 + c];
+  }
+}
 
 // ------------------------------------------------------------------------------------------
 // Blocked TSQR leaf (k <= 128 columns, the first k1 triangularised).  The CTA keeps R (k1 x k)
@@ -478,7 +608,8 @@ size_t az_qr_ws_bytes(int64_t m, int64_t k) {
     return a256q((size_t)np * QBw * QBw * sizeof(double)) + az_qrw_ws_bytes(m, k);
   }
   const int64_t P = std::max<int64_t>(1, std::min<int64_t>(num_sms(), (m + 127) / 128));
-  return (size_t)(2 * P * k * k) * sizeof(double) + 256;
+  // leaf / merge factors (two buffers) + the split leaf's reflector taus (per 256-row chunk)
+  return (size_t)(2 * P * k * k + ((m + 255) / 256 + 2 * P) * k) * sizeof(double) + 256;
 }
 
 static az_status_t qr_r_wide(double* A, int64_t m, int64_t k, int64_t lda, double* R, int64_t ldr, void* ws,
@@ -500,8 +631,17 @@ __global__ void k_copy_R(const double* Rin, int k1, int k, double* R, int64_t ld
 
 // k1 < k: only the leading k1 columns are triangularised and only the top k1 rows of R are
 // returned (R[:k1, k1:] = (Q^T A[:, k1:])[:k1], e.g. Q^T b' for the right-hand sides riding along).
+static bool tsqr_split() {   // AZ_TSQR_SPLIT=0 keeps the single-pass leaf for [S | b']
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AZ_TSQR_SPLIT");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R, int64_t ldr,
-                         void* ws, size_t ws_bytes, cudaStream_t st, int64_t k1) {
+                         void* ws, size_t ws_bytes, cudaStream_t st, int64_t k1, bool a_scratch) {
   if (k1 <= 0 || k1 > k) k1 = k;
   if (ws_bytes < az_qr_ws_bytes(m, k)) {
     az_set_error("az_qr_r: workspace too small");
@@ -526,7 +666,48 @@ az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R
   q.bstride = 0;
   q.rows_per_cta = (m + P - 1) / P;
   q.Rout = buf[0];
-  AZ_TRY(tsqr_pass(q, (int)P, st));
+  q.ostride = k1 * k;
+  q.Y = nullptr;
+  q.ldY = 0;
+  q.taus = nullptr;
+  q.cmax = 0;
+  const int64_t nb = k - k1;
+  if (a_scratch && k1 < k && k1 <= 64 && nb <= 64 && tsqr_split()) {
+    // split leaf: pass A triangularises the k1 probe columns alone in 256-row chunks (KC = 4,
+    // RPL = 8: half the column steps per row of the 128-column pass) and keeps each chunk's
+    // reflectors in place of those columns; pass B applies them to the right-hand sides in
+    // compact-WY form (DMMA Gram products)
+    constexpr int MC = 256;
+    q.k = (int)k1;
+    q.Y = A;
+    q.ldY = lda;
+    q.cmax = (int)((q.rows_per_cta + MC - 1) / MC);
+    q.taus = (double*)ws + 2 * P * k * k;
+    AZ_TRY((tsqr_launch<4, 8>(q, (int)P, st)));
+    QRr r;
+    r.Y = A;
+    r.ldY = lda;
+    r.X = A + k1 * lda;
+    r.ldX = lda;
+    r.m = m;
+    r.rows_per_cta = q.rows_per_cta;
+    r.k1 = (int)k1;
+    r.nb = (int)nb;
+    r.MC = MC;
+    r.cmax = q.cmax;
+    r.taus = q.taus;
+    r.Rout = buf[0];
+    r.ostride = k1 * k;
+    const size_t rsm = (size_t)(2 * 64 * RR_S + 3 * 64 * 65 + 64) * sizeof(double);
+    AZ_CUDA_CHECK(az_smem_attr(k_tsqr_rhs, rsm));
+    {
+      AzTrace tr("tsqr_rhs", st, m);
+      k_tsqr_rhs<<<(unsigned)P, 512, rsm, st>>>(r);
+      AZ_LAUNCH_CHECK();
+    }
+  } else {
+    AZ_TRY(tsqr_pass(q, (int)P, st));
+  }
   int64_t cur = P;
   int which = 0;
   // fixed-shape reduction tree: groups of 4 R factors
@@ -543,6 +724,11 @@ az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R
     t.bstride = k1 * k;
     t.rows_per_cta = G * k1;
     t.Rout = buf[which ^ 1];
+    t.ostride = k1 * k;
+    t.Y = nullptr;
+    t.ldY = 0;
+    t.taus = nullptr;
+    t.cmax = 0;
     AZ_TRY(tsqr_pass(t, (int)next, st));
     which ^= 1;
     cur = next;

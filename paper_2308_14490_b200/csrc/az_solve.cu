@@ -311,7 +311,8 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
     cudaEventRecord(e1, st);
     if (dbg_host) fprintf(stderr, "az_solve host: sketch issued +%.2f ms\n", hnow() - th0);
     if (!w.wide) {
-      AZ_TRY(az_qr_r_impl(w.S, rows, kt, rows, w.Rf, kt, w.qrws, w.qrbytes, st, kp));
+      // a single probe block: the sketch columns are not needed after this QR (split leaf allowed)
+      AZ_TRY(az_qr_r_impl(w.S, rows, kt, rows, w.Rf, kt, w.qrws, w.qrbytes, st, kp, max_blocks == 1));
     } else {
       if (kp > rows) {
         az_set_error("az_solve: %lld probe columns exceed the %lld rows", (long long)kp, (long long)rows);
