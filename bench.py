@@ -45,7 +45,7 @@ def measured_peaks():
 # algorithmic bytes / flops per unit (per complex vector PAIR for the pass kernels), DESIGN.md
 # "Algorithmic bytes per kernel".  n = coefficient length, L = fine length, M = rows.
 # ------------------------------------------------------------------------------------------
-def kernel_model(name, cfg, M, k_cols, k1=None, kept=False):
+def kernel_model(name, cfg, M, k_cols, k1=None, kept=False, split=False):
     n = cfg.N
     L = cfg.N * cfg.s ** cfg.dim
     C = 16  # bytes per complex128
@@ -72,9 +72,15 @@ def kernel_model(name, cfg, M, k_cols, k1=None, kept=False):
         return "hbm", hbm[name]
     if name == "tsqr_leaf":
         # Householder on [S | b'] triangularising the k1 probe columns: per row and reflector j a
-        # dot product and an axpy over the k - j - 1 trailing columns (4 flops each) plus the norm
+        # dot product and an axpy over the k - j - 1 trailing columns (4 flops each) plus the norm.
+        # Split leaf (single probe block, az_qr.cu): this pass holds the k1 probe columns only.
         k1 = k_cols if k1 is None else k1
-        return "alu", float(sum(4 * (k_cols - j - 1) + 2 for j in range(k1)))   # flops per row
+        kk = k1 if split else k_cols
+        return "alu", float(sum(4 * (kk - j - 1) + 2 for j in range(k1)))   # flops per row
+    if name == "tsqr_rhs":
+        # split leaf, pass B: Y^T Y and Y^T b' per row (the chunk reflectors' Gram products)
+        k1 = k_cols if k1 is None else k1
+        return "alu", float(2 * k1 * k1 + 2 * k1 * (k_cols - k1))
     if name == "omega_apply":
         return "alu", 2.0                       # flops per (row x column x rhs) unit
     return None, None
@@ -372,7 +378,9 @@ def run_ours(args, cfg):
     # the four-step narrow solve keeps Omega and A Omega from the sketch (az_solve.cu keep_aomega)
     kept = (cfg.dim == 1 and cfg.N * cfg.s > 2048 and kcols <= 128
             and os.environ.get("AZ_KEEP_AOMEGA", "1") != "0")
-    bound, per_unit = kernel_model(name, cfg, plan.M, kcols, reps[-1]["probes"], kept)
+    split = (kcols <= 128 and reps[-1]["probes"] <= 64 and cfg.nrhs <= 64 and max_blocks == 1
+             and not args.sharded and os.environ.get("AZ_TSQR_SPLIT", "1") != "0")
+    bound, per_unit = kernel_model(name, cfg, plan.M, kcols, reps[-1]["probes"], kept, split)
     roof = {"kernel": name, "launches": cnt, "ms_total": tot_ms, "share_of_step": tot_ms / sum(ms)}
     if bound == "hbm":
         achieved = per_unit * units / (tot_ms * 1e-3) / 1e9

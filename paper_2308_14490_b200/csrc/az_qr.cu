@@ -221,13 +221,13 @@ struct QRr {
   int64_t ostride;
 };
 
-constexpr int RR_S = 36;   // operand tile stride (== 4 mod 16)
+constexpr int RR_S2 = 68;  // operand tile stride (== 4 mod 16), 64-row sub-blocks
 
 __global__ void __launch_bounds__(512, 1) k_tsqr_rhs(QRr q) {
   extern __shared__ double sm[];
-  double* Ys = sm;                       // IMAJ [col][row], 64 x RR_S (32-row sub-block)
-  double* Xs = Ys + 64 * RR_S;           // IMAJ [col][row]
-  double* G = Xs + 64 * RR_S;            // 64 x 64 (ld 65): Y^T Y, then TG[j][m] = tau_m G[j][m]
+  double* Ys = sm;                       // IMAJ [col][row], 64 x RR_S2 (64-row sub-block)
+  double* Xs = Ys + 64 * RR_S2;          // IMAJ [col][row]
+  double* G = Xs + 64 * RR_S2;           // 64 x 64 (ld 65): Y^T Y, then TG[j][m] = tau_m G[j][m]
   double* P = G + 64 * 65;               // 64 x 64 (ld 65): Y^T X, then W = R_b + P, then d
   double* Rb = P + 64 * 65;              // 64 x 64 (ld 65)
   double* tau_s = Rb + 64 * 65;          // 64
@@ -239,11 +239,11 @@ __global__ void __launch_bounds__(512, 1) k_tsqr_rhs(QRr q) {
   // warps 0-7: G tiles rows (w & 1) 32.., cols (w >> 1) 16..;  warps 8-15: the same tiles of P
   const int ww = w & 7, wm = ww & 1, wn = ww >> 1;
   const bool isG = w < 8;
-  double ry[4], rx[4];   // the next 32-row sub-block, in flight during the current MMAs
+  double ry[8], rx[8];   // the next 64-row sub-block, in flight during the current MMAs
   auto load = [&](int64_t rr, int64_t cend) {
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int e = tid + 512 * t, cidx = e >> 5, rl = e & 31;
+    for (int t = 0; t < 8; ++t) {
+      const int e = tid + 512 * t, cidx = e >> 6, rl = e & 63;
       const int64_t row = rr + rl;
       const bool in = row < cend;
       ry[t] = (in && cidx < k1) ? q.Y[row + (int64_t)cidx * q.ldY] : 0.0;
@@ -257,17 +257,17 @@ __global__ void __launch_bounds__(512, 1) k_tsqr_rhs(QRr q) {
     acc_zero(acc);
     load(base, cend);
     if (tid < 64) tau_s[tid] = tid < k1 ? q.taus[((int64_t)blockIdx.x * q.cmax + chunk) * k1 + tid] : 0.0;
-    for (int64_t rr = base; rr < cend; rr += 32) {
+    for (int64_t rr = base; rr < cend; rr += 64) {
       __syncthreads();
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int e = tid + 512 * t, cidx = e >> 5, rl = e & 31;
-        Ys[cidx * RR_S + rl] = ry[t];
-        Xs[cidx * RR_S + rl] = rx[t];
+      for (int t = 0; t < 8; ++t) {
+        const int e = tid + 512 * t, cidx = e >> 6, rl = e & 63;
+        Ys[cidx * RR_S2 + rl] = ry[t];
+        Xs[cidx * RR_S2 + rl] = rx[t];
       }
       __syncthreads();
-      if (rr + 32 < cend) load(rr + 32, cend);
-      warp_mma<4, 2, IMAJ, IMAJ>(acc, Ys, RR_S, isG ? Ys : Xs, RR_S, wm * 32, wn * 16, 0, 32, lane);
+      if (rr + 64 < cend) load(rr + 64, cend);
+      warp_mma<4, 2, IMAJ, IMAJ>(acc, Ys, RR_S2, isG ? Ys : Xs, RR_S2, wm * 32, wn * 16, 0, 64, lane);
     }
     double* D = isG ? G : P;
 #pragma unroll
@@ -288,25 +288,47 @@ __global__ void __launch_bounds__(512, 1) k_tsqr_rhs(QRr q) {
     // Reflectors in order, per right-hand-side column c (independent): with d_m = v_m^T [R_b; X^(m)]
     // (X^(m): X after reflectors < m; R row j is only touched by reflector j),
     //   d_j = W[j][c] - sum_{m<j} tau_m (y_j . y_m) d_m,   R_b[j][c] -= tau_j d_j
-    if (tid < nb) {
-      const int c = tid;
-      for (int j = 0; j < k1; ++j) {
-        double s0 = P[j * 65 + c], s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        const double* tg = G + j * 65;
-        int m = 0;
-        for (; m + 3 < j; m += 4) {
-          s0 = fma(-tg[m], P[m * 65 + c], s0);
-          s1 = fma(-tg[m + 1], P[(m + 1) * 65 + c], s1);
-          s2 = fma(-tg[m + 2], P[(m + 2) * 65 + c], s2);
-          s3 = fma(-tg[m + 3], P[(m + 3) * 65 + c], s3);
+    // in blocks of 8 j: the part over earlier blocks by all threads (one (j, c) each), the
+    // triangle inside the block by one thread per column.
+    double* S8 = Ys;   // 8 x 64 partial sums (the operand tiles are free now)
+    for (int jb = 0; jb < k1; jb += 8) {
+      {
+        const int r = tid >> 6, c = tid & 63, j = jb + r;
+        if (j < k1 && c < nb) {
+          double s0 = P[j * 65 + c], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+          const double* tg = G + j * 65;
+          for (int m = 0; m < jb; m += 4) {   // jb is a multiple of 8
+            s0 = fma(-tg[m], P[m * 65 + c], s0);
+            s1 = fma(-tg[m + 1], P[(m + 1) * 65 + c], s1);
+            s2 = fma(-tg[m + 2], P[(m + 2) * 65 + c], s2);
+            s3 = fma(-tg[m + 3], P[(m + 3) * 65 + c], s3);
+          }
+          S8[r * 64 + c] = (s0 + s1) + (s2 + s3);
         }
-        for (; m < j; ++m) s0 = fma(-tg[m], P[m * 65 + c], s0);
-        const double d = (s0 + s1) + (s2 + s3);
-        P[j * 65 + c] = d;
-        Rb[j * 65 + c] -= tau_s[j] * d;
       }
+      __syncthreads();
+      if (tid < nb) {   // the block's triangle, its d values in registers (k1 is a multiple of 8 or
+        const int c = tid;   // the rows past k1 have zero sums and are not stored)
+        double d[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int j = jb + r;
+          double v = (j < k1) ? S8[r * 64 + c] : 0.0;
+#pragma unroll
+          for (int rr = 0; rr < r; ++rr) v = fma(-G[j * 65 + jb + rr], d[rr], v);
+          d[r] = v;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int j = jb + r;
+          if (j < k1) {
+            P[j * 65 + c] = d[r];
+            Rb[j * 65 + c] -= tau_s[j] * d[r];
+          }
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
   double* Ro = q.Rout + (int64_t)blockIdx.x * q.ostride;
   for (int e = tid; e < k1 * nb; e += 512) {
@@ -698,7 +720,7 @@ az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R
     r.taus = q.taus;
     r.Rout = buf[0];
     r.ostride = k1 * k;
-    const size_t rsm = (size_t)(2 * 64 * RR_S + 3 * 64 * 65 + 64) * sizeof(double);
+    const size_t rsm = (size_t)(2 * 64 * RR_S2 + 3 * 64 * 65 + 64) * sizeof(double);
     AZ_CUDA_CHECK(az_smem_attr(k_tsqr_rhs, rsm));
     {
       AzTrace tr("tsqr_rhs", st, m);
