@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(512, 1) k_tsqr(QRIn q) {
 // by one, up to rounding.
 // ------------------------------------------------------------------------------------------
 struct QRr {
+  int64_t rb, bstride;  // stacked rows (merges): row r at (r / rb) bstride + r % rb; 0 = plain
   const double* Y;      // m x k1 (ld ldY): pass A's reflectors
   int64_t ldY;
   const double* X;      // m x nb (ld ldX): the right-hand-side columns
@@ -246,8 +247,9 @@ __global__ void __launch_bounds__(512, 1) k_tsqr_rhs(QRr q) {
       const int e = tid + 512 * t, cidx = e >> 6, rl = e & 63;
       const int64_t row = rr + rl;
       const bool in = row < cend;
-      ry[t] = (in && cidx < k1) ? q.Y[row + (int64_t)cidx * q.ldY] : 0.0;
-      rx[t] = (in && cidx < nb) ? q.X[row + (int64_t)cidx * q.ldX] : 0.0;
+      const int64_t off = q.bstride ? (row / q.rb) * q.bstride + (row % q.rb) : row;
+      ry[t] = (in && cidx < k1) ? q.Y[off + (int64_t)cidx * q.ldY] : 0.0;
+      rx[t] = (in && cidx < nb) ? q.X[off + (int64_t)cidx * q.ldX] : 0.0;
     }
   };
   int chunk = 0;
@@ -707,6 +709,8 @@ az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R
     q.taus = (double*)ws + 2 * P * k * k;
     AZ_TRY((tsqr_launch<4, 8>(q, (int)P, st)));
     QRr r;
+    r.rb = 0;
+    r.bstride = 0;
     r.Y = A;
     r.ldY = lda;
     r.X = A + k1 * lda;
@@ -752,6 +756,7 @@ az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R
     t.taus = nullptr;
     t.cmax = 0;
     AZ_TRY(tsqr_pass(t, (int)next, st));
+
     which ^= 1;
     cur = next;
   }
