@@ -51,15 +51,17 @@ def kernel_model(name, cfg, M, k_cols, k1=None, kept=False, split=False):
     C = 16  # bytes per complex128
     # 1-D intervals: the mask is one run of the grid, so no row-map / mask bytes are read
     pos_b, mask_b = (0, 0) if cfg.dim == 1 else (4, 1)
-    # kept: the four-step narrow solve stores Omega (probe pass) and A Omega (mask pass) for step 2
-    kw_om, kw_aom = (2 * 8 * n, 2 * 8 * M) if kept else (0, 0)
+    # kept: the four-step narrow solve stores Omega (probe pass) for step 2 and takes the Z* parts of
+    # the b' and sketch chains to the coefficient side (row passes write them, two column passes finish)
+    kw_om, kw_z = (2 * 8 * n, C * n) if kept else (0, 0)
+    kw_aom = 0
     hbm = {
         "1f_cols_in_coef": C * n + kw_om,              # probes generated on chip; write spectrum (+ Omega)
         "1f_rows_expand_keep": 2 * C * n + C * L,
         "1f_rows_expand": C * n + C * L,
         "1f_cols_fine_mask": 2 * C * L + mask_b * L + kw_aom,   # fine grid in/out, mask (1 B) (+ A Omega rows)
-        "1f_rows_step1": 2 * C * L + C * n + 8 * n,    # fine grid in/out, v^ and zinv in
-        "1f_rows_resid": 2 * C * L + 8 * n,
+        "1f_rows_step1": 2 * C * L + C * n + 8 * n + kw_z,    # fine grid in/out, v^ and zinv in (+ Z* part)
+        "1f_rows_resid": 2 * C * L + 8 * n + kw_z,
         "1f_rows_zstar": C * L + C * n + 8 * n,
         "1f_cols_out_gather": C * L + pos_b * L + 2 * 8 * M,   # fine grid + row map in, 2 columns out
         "1f_cols_out_resid": C * L + pos_b * L + 4 * 8 * M,
@@ -67,6 +69,8 @@ def kernel_model(name, cfg, M, k_cols, k1=None, kept=False, split=False):
         "1f_cols_out_coef": C * n + 2 * 8 * n,
         "1f_cols_out_coef_add": C * n + 4 * 8 * n,             # spectrum + x2 in, x out
         "1f_cols_resid_mid": 2 * C * L + 2 * 8 * M,            # fine grid in/out, b rows in
+        "1f_cols_out_z": C * n + 2 * 8 * n,                    # Z* b: spectrum in, 2 columns out
+        "1f_cols_out_omz": C * n + 2 * 2 * 8 * n,              # M = Omega - Z* A Omega: spectrum + Omega in, M out
     }
     if name in hbm:
         return "hbm", hbm[name]

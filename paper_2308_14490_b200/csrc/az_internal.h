@@ -60,6 +60,7 @@ struct az_plan_s {
   // scratch for the pass kernels
   int64_t Bmax = 0;             // max vector PAIRS per batch
   cplx* d_C1 = nullptr;         // Bmax * N complex
+  cplx* d_Z2 = nullptr;         // four-step: Bmax * N complex (Z* outputs of the b' / sketch chains)
   cplx* d_G = nullptr;          // Bmax * G complex
   // host-side info
   double sigma_max2 = 0, sigma_min_kept2 = 0;
@@ -90,6 +91,12 @@ az_status_t az1f_sketch_keep(az_plan_s* p, int64_t col0, int64_t ncols, double* 
                              int64_t ldA, double* Om, int64_t ldOm, cudaStream_t st);
 az_status_t az1f_zstar_add(az_plan_s* p, const double* r, int64_t ldr, const double* x2, int64_t ldx2, double* x,
                            int64_t ldx, int64_t nvec, cudaStream_t st);
+// b' = (I - A Z*) b that also returns Z* b (N x nvec); the sketch that also returns
+// M = Omega - Z* A Omega (N x ncols, written over the kept Omega)
+az_status_t az1f_resid_z(az_plan_s* p, const double* b, int64_t ldb, double* bp, int64_t ldbp, double* Zb, int64_t ldz,
+                         int64_t nvec, cudaStream_t st);
+az_status_t az1f_sketch_m(az_plan_s* p, int64_t col0, int64_t ncols, double* S, int64_t ldS, double* Om, int64_t ldOm,
+                          cudaStream_t st);
 
 // --- 2-D layout (az_ops2d.cu)
 az_status_t az2_apply(az_plan_s* p, int op, int src, const double* in, int64_t ldin, double* out,

@@ -51,6 +51,9 @@ struct P1f {
   int64_t ldaux;
   double* aux2;          // FC_IN_COEF with probes: optional copy of the probe columns (the sketch keeps Omega)
   int64_t ldaux2;
+  cplx* Z2;              // FR_STEP1 / FR_RESID: optional Z*-part output (coefficient spectrum after IFFT_N2)
+  double* out2;          // FC_OUT_Z / FC_OUT_OMZ output (N x nvec)
+  int64_t ldout2;
   int64_t nvec, col0, pair0;
 };
 
@@ -87,7 +90,9 @@ AZ_D Cols1 pcols(const P1f& a, int b) {
 // 32 / TC rows per access.
 // ------------------------------------------------------------------------------------------
 enum { FC_IN_COEF = 0, FC_FINE_MASK = 1, FC_OUT_GATHER = 2, FC_OUT_RESID = 3, FC_IN_ROWS = 4, FC_OUT_COEF = 5,
-       FC_FWD_G = 6, FC_RESID_MID = 7, FC_OUT_COEF_ADD = 8 };
+       FC_FWD_G = 6, FC_RESID_MID = 7, FC_OUT_COEF_ADD = 8, FC_OUT_Z = 9, FC_OUT_OMZ = 10 };
+// FC_OUT_Z:   IFFT_N1 of the Z2 buffer -> out2 = (.) / n          (Z* b from the b' chain)
+// FC_OUT_OMZ: IFFT_N1 of the Z2 buffer -> out2 = out2 - (.) / n   (M = Omega - Z* A Omega in place)
 // FC_RESID_MID: IFFT_N1 -> r = b - (A x) on Omega, 0 outside -> FFT_N1 -> twiddle  (the A -> b - A x ->
 //               Z* junction of step 2 in one pass, no row vector written or read)
 // FC_OUT_COEF_ADD: IFFT_N1 -> x = x2 + (.) / n  (the closing addition of step 2)
@@ -103,9 +108,10 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
   const int c0 = blockIdx.x * TC;
   const int col = c0 + c;
   const Cols1 cc = pcols(a, b);
-  const bool coef = (KIND == FC_IN_COEF || KIND == FC_OUT_COEF || KIND == FC_OUT_COEF_ADD);
+  const bool coef = (KIND == FC_IN_COEF || KIND == FC_OUT_COEF || KIND == FC_OUT_COEF_ADD || KIND == FC_OUT_Z ||
+                     KIND == FC_OUT_OMZ);
   const int W = coef ? a.N2 : a.L2;                    // row length of the matrix
-  cplx* C1b = a.C1 + (int64_t)b * a.n;
+  cplx* C1b = (KIND == FC_OUT_Z || KIND == FC_OUT_OMZ) ? a.Z2 + (int64_t)b * a.n : a.C1 + (int64_t)b * a.n;
   cplx* Gb = a.G + (int64_t)b * a.L;
   const int64_t tmul = coef ? a.s : 1;                 // e^{-2 pi i n2 k1 / n} = e^{-2 pi i (s n2 k1) / L}
   cplx* buf = sm + c * fftr::padded_len(NC);
@@ -227,6 +233,20 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
       a.out[i + cc.cre * a.ldout] = fma(v[e].x, cout, a.in[i + cc.cre * a.ldin]);
       if (cc.has_im) a.out[i + cc.cim * a.ldout] = fma(v[e].y, cout, a.in[i + cc.cim * a.ldin]);
     }
+  } else if constexpr (KIND == FC_OUT_Z) {
+#pragma unroll
+    for (int e = 0; e < EC; ++e) {
+      const int64_t i = (int64_t)(j + e * T) * W + col;
+      a.out2[i + cc.cre * a.ldout2] = v[e].x * cout;
+      if (cc.has_im) a.out2[i + cc.cim * a.ldout2] = v[e].y * cout;
+    }
+  } else if constexpr (KIND == FC_OUT_OMZ) {
+#pragma unroll
+    for (int e = 0; e < EC; ++e) {
+      const int64_t i = (int64_t)(j + e * T) * W + col;
+      a.out2[i + cc.cre * a.ldout2] = fma(-v[e].x, cout, a.out2[i + cc.cre * a.ldout2]);
+      if (cc.has_im) a.out2[i + cc.cim * a.ldout2] = fma(-v[e].y, cout, a.out2[i + cc.cim * a.ldout2]);
+    }
   } else {   // FC_OUT_COEF
 #pragma unroll
     for (int e = 0; e < EC; ++e) {
@@ -304,8 +324,29 @@ __global__ void __launch_bounds__(RPC * (LR2 / EL), MINB) k1f_rows(P1f a, int nr
       const int k2 = j + e * T;
       cplx acc = cadd(cscale(vl[e], Ws[k2]), cscale(vl[e + EN], Ws[k2 + NR2]));
       if constexpr (KIND != FR_AT) acc = cscale(acc, Zs[k2]);
-      if constexpr (KIND == FR_STEP1) acc = csub(Cs[k2], acc);
       vn[e] = acc;
+    }
+    if constexpr (KIND == FR_STEP1 || KIND == FR_RESID) {
+      if (a.Z2) {   // the Z* part itself (Z* A v, Z* b) on to the coefficient side: IFFT_N2 + twiddle
+        cplx wz[EN];
+#pragma unroll
+        for (int e = 0; e < EN; ++e) wz[e] = vn[e];
+        fftr::fft<NR2, EN, 1>(wz, j, buf, a.tw, TWN);
+        if (live) {
+          cplx* Zb = a.Z2 + (int64_t)b * a.n;
+          cplx w = tw4<1>(a, ((int64_t)j * k1 * 2) & (a.L - 1));
+          const cplx ws = tw4<1>(a, ((int64_t)T * k1 * 2) & (a.L - 1));
+#pragma unroll
+          for (int e = 0; e < EN; ++e) {
+            Zb[rowC + j + e * T] = cmul(wz[e], w);
+            w = cmul(w, ws);
+          }
+        }
+      }
+    }
+    if constexpr (KIND == FR_STEP1) {
+#pragma unroll
+      for (int e = 0; e < EN; ++e) vn[e] = csub(Cs[j + e * T], vn[e]);
     }
   }
   if constexpr (KIND == FR_ZSTAR || KIND == FR_AT) {
@@ -370,7 +411,7 @@ static az_status_t fcols_e(const P1f& a, int ncols, int nb, double cout, cudaStr
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   static const char* names[] = {"1f_cols_in_coef", "1f_cols_fine_mask", "1f_cols_out_gather", "1f_cols_out_resid",
                                 "1f_cols_in_rows", "1f_cols_out_coef", "1f_cols_fwd", "1f_cols_resid_mid",
-                                "1f_cols_out_coef_add"};
+                                "1f_cols_out_coef_add", "1f_cols_out_z", "1f_cols_out_omz"};
   AzTrace tr(names[KIND], st, nb);
   kern<<<dim3(az_div_up(ncols, TC), nb), TC * T, sm, st>>>(a, cout);
   AZ_LAUNCH_CHECK();
@@ -429,11 +470,13 @@ static az_status_t run1f(const P1f& a0, int op, int src, int64_t npairs, int64_t
         AZ_TRY(fcols<NC, FC_FINE_MASK, SRC_VEC>(a, L2, nb, 1.0, st));
         AZ_TRY(frows<NR2, FR_STEP1>(a, nb, st));
         AZ_TRY(fcols<NC, FC_OUT_GATHER, SRC_VEC>(a, L2, nb, 1.0, st));
+        if (a.Z2) AZ_TRY(fcols<NC, FC_OUT_OMZ, SRC_VEC>(a, N2, nb, 1.0 / (double)a.n, st));
         break;
       case OP_RESID:
         AZ_TRY(fcols<NC, FC_IN_ROWS, SRC_VEC>(a, L2, nb, 1.0, st));
         AZ_TRY(frows<NR2, FR_RESID>(a, nb, st));
         AZ_TRY(fcols<NC, FC_OUT_RESID, SRC_VEC>(a, L2, nb, 1.0, st));
+        if (a.Z2) AZ_TRY(fcols<NC, FC_OUT_Z, SRC_VEC>(a, N2, nb, 1.0 / (double)a.n, st));
         break;
       case OP_ZSTAR:
         AZ_TRY(fcols<NC, FC_IN_ROWS, SRC_VEC>(a, L2, nb, 1.0, st));
@@ -499,6 +542,9 @@ static P1f make_p1f(az_plan_s* p) {
   a.ldaux = 0;
   a.aux2 = nullptr;
   a.ldaux2 = 0;
+  a.Z2 = nullptr;
+  a.out2 = nullptr;
+  a.ldout2 = 0;
   a.ldin = a.ldout = 0;
   a.nvec = a.col0 = a.pair0 = 0;
   return a;
@@ -611,4 +657,41 @@ az_status_t az1f_zstar_add(az_plan_s* p, const double* r, int64_t ldr, const dou
   a.col0 = 0;
   const int64_t npairs = (nvec + 1) / 2;
   AZ_1F_DISPATCH(run1f, a, OP_ZSTAR_ADD, SRC_VEC, npairs, p->Bmax, st)
+}
+
+// b' = (I - A Z*) b (out = bp) and Z* b (out2 = Zb, N x nvec) in one chain: the row pass also takes
+// its Z* b spectrum to the coefficient side, one extra column pass finishes it.
+az_status_t az1f_resid_z(az_plan_s* p, const double* b, int64_t ldb, double* bp, int64_t ldbp, double* Zb, int64_t ldz,
+                         int64_t nvec, cudaStream_t st) {
+  P1f a = make_p1f(p);
+  a.in = b;
+  a.ldin = ldb;
+  a.out = bp;
+  a.ldout = ldbp;
+  a.Z2 = p->d_Z2;
+  a.out2 = Zb;
+  a.ldout2 = ldz;
+  a.nvec = nvec;
+  a.col0 = 0;
+  const int64_t npairs = (nvec + 1) / 2;
+  AZ_1F_DISPATCH(run1f, a, OP_RESID, SRC_VEC, npairs, p->Bmax, st)
+}
+
+// S = (A - A Z* A) Omega[:, col0 ..) and, over the probes kept in Om by the probe pass,
+// M = Omega - Z* A Omega (step 2 of the solve is then x = Z* b + M y: no FFT pass, PAPER.md:229-230
+// by linearity of Z*)
+az_status_t az1f_sketch_m(az_plan_s* p, int64_t col0, int64_t ncols, double* S, int64_t ldS, double* Om, int64_t ldOm,
+                          cudaStream_t st) {
+  P1f a = make_p1f(p);
+  a.out = S;
+  a.ldout = ldS;
+  a.aux2 = Om;
+  a.ldaux2 = ldOm;
+  a.Z2 = p->d_Z2;
+  a.out2 = Om;
+  a.ldout2 = ldOm;
+  a.nvec = ncols;
+  a.col0 = col0;
+  const int64_t npairs = (ncols + 1) / 2;
+  AZ_1F_DISPATCH(run1f, a, OP_STEP1, SRC_PROBE, npairs, p->Bmax, st)
 }

@@ -372,7 +372,7 @@ static void plan_free(az_plan_s* p) {
   if (p->d_W0y == p->d_W0) p->d_W0y = nullptr;   // aliases of the x tables (square boxes)
   if (p->d_W2y == p->d_W2) p->d_W2y = nullptr;
   void* ptrs[] = {p->d_mask, p->d_pos, p->d_W0, p->d_W2, p->d_W0y, p->d_W2y, p->d_Wr, p->d_zinv, p->d_tw,
-                  p->d_tw4hi, p->d_tw4lo, p->d_bxy, p->d_bw, p->d_bj, p->d_C1, p->d_G, p->d_solve_ws};
+                  p->d_tw4hi, p->d_tw4lo, p->d_bxy, p->d_bw, p->d_bj, p->d_C1, p->d_Z2, p->d_G, p->d_solve_ws};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->h_stage) cudaFreeHost(p->h_stage);
@@ -479,6 +479,7 @@ static az_status_t plan_build(az_plan_s* p, const az_plan_desc_t* d, cudaStream_
     B = std::max<int64_t>(1, std::min<int64_t>(B, 32));
     p->Bmax = B;
     AZ_TRY(dalloc(&p->d_C1, B * p->N));
+    if (p->layout == AZ_LAYOUT_1D_FOURSTEP) AZ_TRY(dalloc(&p->d_Z2, B * p->N));
     AZ_TRY(dalloc(&p->d_G, B * p->G));
   }
   // ---- symbol tables: fine-grid kernel samples and their DFT (Lemma 3), per axis ----

@@ -137,8 +137,8 @@ struct SolveWS {
   double* sig;   // Rmax
   double* tmp;   // rows x nrhs
   double* x2;    // N x nrhs
-  double* AOm;   // rows x Rmax: A Omega kept by the sketch (four-step narrow path), else null
-  double* Om;    // N x Rmax: Omega kept by the sketch (same condition)
+  double* Zb;    // N x nrhs: Z* b from the b' chain (four-step narrow path), else null
+  double* Om;    // N x Rmax: M = Omega - Z* A Omega from the sketch (same condition)
   void* qrws;
   size_t qrbytes;
   void* svdws;
@@ -153,9 +153,9 @@ static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 // Y = A B (or C - A B), DMMA tiles; defined with the factored-solve kernels below
 __global__ void k_gemm_mn(const double* A, int64_t lda, const double* Bm, int64_t ldb, double* Y, int64_t ldy, int64_t m,
-                          int64_t k, int64_t n, const double* C = nullptr, int64_t ldc = 0);
+                          int64_t k, int64_t n, const double* C = nullptr, int64_t ldc = 0, double sgn = -1.0);
 __global__ void k_gemm_mn_small(const double* A, int64_t lda, const double* Bm, int64_t ldb, double* Y, int64_t ldy,
-                                int64_t m, int k, int n, const double* C, int64_t ldc);
+                                int64_t m, int k, int n, const double* C, int64_t ldc, double sgn = -1.0);
 
 // four-step narrow solves keep A Omega from the sketch for step 2 (AZ_KEEP_AOMEGA=0 disables)
 static bool keep_aomega() {
@@ -187,7 +187,7 @@ static SolveWS layout(az_plan_s* p, int64_t nrhs, int64_t R, int32_t max_blocks,
   w.x2 = (double*)take(sizeof(double) * p->N * nrhs);
   w.wide = kt > AZ_NARROW_MAX;
   const bool keep = !w.wide && p->layout == AZ_LAYOUT_1D_FOURSTEP && keep_aomega();
-  w.AOm = keep ? (double*)take(sizeof(double) * rows * Rmax) : nullptr;
+  w.Zb = keep ? (double*)take(sizeof(double) * p->N * nrhs) : nullptr;
   w.Om = keep ? (double*)take(sizeof(double) * p->N * Rmax) : nullptr;
   if (w.wide) {
     const int64_t QBw = az_qrw_panel_width();
@@ -281,7 +281,10 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   cudaEventRecord(ev.e[0], st);
   // ---- right-hand side b' = (I - A Z*) b (narrow single-block solve: straight into S) ----
   const bool bp_in_S = !w.wide && max_blocks == 1;
-  AZ_TRY(az_apply_op(p, OP_RESID, b, ldb, bp_in_S ? w.S + R * rows : w.bp, rows, nrhs, st));
+  if (w.Zb)   // b' and, for step 2, Z* b (one extra column pass)
+    AZ_TRY(az1f_resid_z(p, b, ldb, bp_in_S ? w.S + R * rows : w.bp, rows, w.Zb, p->N, nrhs, st));
+  else
+    AZ_TRY(az_apply_op(p, OP_RESID, b, ldb, bp_in_S ? w.S + R * rows : w.bp, rows, nrhs, st));
   cudaEventRecord(ev.e[1], st);
   if (dbg_host) fprintf(stderr, "az_solve host: resid issued +%.2f ms\n", hnow() - th0);
   double ms_sketch = 0, ms_qr = 0, ms_svd = 0;
@@ -298,9 +301,8 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
     const int64_t kt = kp + nrhs;
     cudaEvent_t e0 = ev.e[2], e1 = ev.e[3], e2 = ev.e[4], e3 = ev.e[5];
     cudaEventRecord(e0, st);
-    if (w.AOm)
-      AZ_TRY(az1f_sketch_keep(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, w.AOm + (nb - 1) * R * rows, rows,
-                              w.Om + (nb - 1) * R * p->N, p->N, st));
+    if (w.Om)   // the sketch and M = Omega - Z* A Omega for step 2
+      AZ_TRY(az1f_sketch_m(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, w.Om + (nb - 1) * R * p->N, p->N, st));
     else
       AZ_TRY(az_sketch(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, st));
     if (!w.wide && !bp_in_S) {
@@ -375,37 +377,24 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   if (dbg_host) fprintf(stderr, "az_solve host: svd issued +%.2f ms\n", hnow() - th0);
   cudaEventRecord(ev.e[6], st);
   // ---- x2 = Omega y ; x = x2 + Z* (b - A x2) ----
-  if (w.Om && kp <= 64) {
-    AzTrace tr("omega_apply", st, p->N * kp * nrhs);   // x2 = Omega y from the kept probes
-    const size_t gs = 2 * 64 * 68 * sizeof(double);
-    AZ_CUDA_CHECK(az_smem_attr(k_gemm_mn_small, gs));
-    for (int64_t c0 = 0; c0 < nrhs; c0 += 64)
-      k_gemm_mn_small<<<(unsigned)std::min<int64_t>(az_div_up(p->N, 64), 3 * 148), 256, gs, st>>>(
-          w.Om, p->N, w.y + c0 * kp, kp, w.x2 + c0 * p->N, p->N, p->N, (int)kp, (int)std::min<int64_t>(64, nrhs - c0),
-          nullptr, 0);
+  if (w.Om) {
+    // by linearity of Z* (PAPER.md:229-230): x = Omega y + Z* b - (Z* A Omega) y = Z* b + M y, with
+    // Z* b and M = Omega - Z* A Omega produced by the b' and sketch chains: one DMMA pass, no FFT
+    AzTrace tr("step2_gemm", st, 2 * p->N * kp * nrhs);
+    if (kp <= 64) {
+      const size_t gs = 2 * 64 * 68 * sizeof(double);
+      AZ_CUDA_CHECK(az_smem_attr(k_gemm_mn_small, gs));
+      for (int64_t c0 = 0; c0 < nrhs; c0 += 64)
+        k_gemm_mn_small<<<(unsigned)std::min<int64_t>(az_div_up(p->N, 64), 3 * 148), 256, gs, st>>>(
+            w.Om, p->N, w.y + c0 * kp, kp, x + c0 * ldx, ldx, p->N, (int)kp, (int)std::min<int64_t>(64, nrhs - c0),
+            w.Zb + c0 * p->N, p->N, 1.0);
+    } else {
+      k_gemm_mn<<<dim3(az_div_up(p->N, 64), az_div_up(nrhs, 64)), 256, 0, st>>>(w.Om, p->N, w.y, kp, x, ldx, p->N, kp,
+                                                                                nrhs, w.Zb, p->N, 1.0);
+    }
     AZ_LAUNCH_CHECK();
   } else {
     AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, p->N, 0, st));
-  }
-  if (w.AOm) {
-    // r = b - A x2 = b - (A Omega) y (one DMMA GEMM), then x = x2 + Z* r (three passes)
-    {
-      AzTrace tr("resid_aomega", st, 2 * rows * kp * nrhs);
-      if (kp <= 64) {
-        const size_t gs = 2 * 64 * 68 * sizeof(double);
-        AZ_CUDA_CHECK(az_smem_attr(k_gemm_mn_small, gs));
-        for (int64_t c0 = 0; c0 < nrhs; c0 += 64)
-          k_gemm_mn_small<<<(unsigned)std::min<int64_t>(az_div_up(rows, 64), 3 * 148), 256, gs, st>>>(
-              w.AOm, rows, w.y + c0 * kp, kp, w.tmp + c0 * rows, rows, rows, (int)kp,
-              (int)std::min<int64_t>(64, nrhs - c0), b + c0 * ldb, ldb);
-      } else {
-        k_gemm_mn<<<dim3(az_div_up(rows, 64), az_div_up(nrhs, 64)), 256, 0, st>>>(w.AOm, rows, w.y, kp, w.tmp, rows,
-                                                                                 rows, kp, nrhs, b, ldb);
-      }
-      AZ_LAUNCH_CHECK();
-    }
-    AZ_TRY(az1f_zstar_add(p, w.tmp, rows, w.x2, p->N, x, ldx, nrhs, st));
-  } else {
     AZ_TRY(step2(p, w.x2, b, ldb, x, ldx, w.tmp, nrhs, st));
   }
   cudaEventRecord(ev.e[7], st);
@@ -518,7 +507,7 @@ __global__ void k_omega_fill(int64_t N, int64_t col0, int64_t ncols, double* Om,
 constexpr int GS = 36;   // operand tile stride (== 4 mod 16: conflict-free fragments)
 __global__ void __launch_bounds__(256) k_gemm_mn(const double* A, int64_t lda, const double* Bm, int64_t ldb, double* Y,
                                                  int64_t ldy, int64_t m, int64_t k, int64_t n, const double* C,
-                                                 int64_t ldc) {   // C non-null: Y = C - A B
+                                                 int64_t ldc, double sgn) {   // C non-null: Y = C + sgn A B
   __shared__ double As[32 * 68];   // KMAJ [k][row], stride 68 (== 4 mod 16)
   __shared__ double Bs[32 * 68];   // KMAJ [k][col]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -544,7 +533,7 @@ __global__ void __launch_bounds__(256) k_gemm_mn(const double* A, int64_t lda, c
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int64_t r = r0 + acc_row(wm * 32, i, lane), cc = c0 + acc_col(wn * 16, j, e, lane);
-        if (r < m && cc < n) Y[cc * ldy + r] = C ? C[cc * ldc + r] - acc[i][j][e] : acc[i][j][e];
+        if (r < m && cc < n) Y[cc * ldy + r] = C ? fma(sgn, acc[i][j][e], C[cc * ldc + r]) : acc[i][j][e];
       }
 }
 
@@ -553,7 +542,7 @@ __global__ void __launch_bounds__(256) k_gemm_mn(const double* A, int64_t lda, c
 // row tiles of 64 (grid-stride), so the small operand is not re-read per tile.
 __global__ void __launch_bounds__(256) k_gemm_mn_small(const double* A, int64_t lda, const double* Bm, int64_t ldb,
                                                        double* Y, int64_t ldy, int64_t m, int k, int n, const double* C,
-                                                       int64_t ldc) {
+                                                       int64_t ldc, double sgn) {
   extern __shared__ double gsm[];
   double* As = gsm;                // KMAJ [k][row], 64 x 68
   double* Bs = gsm + 64 * 68;      // KMAJ [k][col]
@@ -608,7 +597,7 @@ __global__ void __launch_bounds__(256) k_gemm_mn_small(const double* A, int64_t 
         for (int e = 0; e < 2; ++e) {
           const int64_t r = r0 + acc_row(wm * 32, i, lane);
           const int cc = acc_col(wn * 16, j, e, lane);
-          if (r < m && cc < n) Y[(int64_t)cc * ldy + r] = C ? cf[i][j][e] - acc[i][j][e] : acc[i][j][e];
+          if (r < m && cc < n) Y[(int64_t)cc * ldy + r] = C ? fma(sgn, acc[i][j][e], cf[i][j][e]) : acc[i][j][e];
         }
   }
 }
