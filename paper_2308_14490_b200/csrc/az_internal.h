@@ -14,7 +14,7 @@ enum az_layout_t {
 };
 
 // Operation selectors shared by the pass kernels.
-enum az_op_t { OP_A = 0, OP_AT = 1, OP_ZSTAR = 2, OP_STEP1 = 3, OP_RESID = 4, OP_STEP2 = 5, OP_ZSTAR_ADD = 6 };
+enum az_op_t { OP_A = 0, OP_AT = 1, OP_ZSTAR = 2, OP_STEP1 = 3, OP_RESID = 4, OP_STEP2 = 5 };
 
 // Input sources for coefficient-space entry.
 enum az_src_t { SRC_VEC = 0, SRC_PROBE = 1 };
@@ -87,10 +87,6 @@ az_status_t az1f_apply(az_plan_s* p, int op, int src, const double* in, int64_t 
 az_status_t az1f_fft_fine_forward(az_plan_s* p, cplx* data, cudaStream_t st);
 az_status_t az1f_step2(az_plan_s* p, const double* x2, int64_t ldx2, const double* b, int64_t ldb, double* x,
                        int64_t ldx, int64_t nvec, cudaStream_t st);
-az_status_t az1f_sketch_keep(az_plan_s* p, int64_t col0, int64_t ncols, double* S, int64_t ldS, double* AOm,
-                             int64_t ldA, double* Om, int64_t ldOm, cudaStream_t st);
-az_status_t az1f_zstar_add(az_plan_s* p, const double* r, int64_t ldr, const double* x2, int64_t ldx2, double* x,
-                           int64_t ldx, int64_t nvec, cudaStream_t st);
 // b' = (I - A Z*) b that also returns Z* b (N x nvec); the sketch that also returns
 // M = Omega - Z* A Omega (N x ncols, written over the kept Omega)
 az_status_t az1f_resid_z(az_plan_s* p, const double* b, int64_t ldb, double* bp, int64_t ldbp, double* Zb, int64_t ldz,

@@ -47,8 +47,6 @@ struct P1f {
   int64_t ldin2;
   double* out;
   int64_t ldout;
-  double* aux;           // FC_FINE_MASK: optional copy of (A v) on the rows (the sketch keeps A Omega)
-  int64_t ldaux;
   double* aux2;          // FC_IN_COEF with probes: optional copy of the probe columns (the sketch keeps Omega)
   int64_t ldaux2;
   cplx* Z2;              // FR_STEP1 / FR_RESID: optional Z*-part output (coefficient spectrum after IFFT_N2)
@@ -182,15 +180,6 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
     fftr::fft<NC, EC, -1>(v, j, buf, a.tw, TWN);
   } else if constexpr (KIND == FC_FINE_MASK) {
     fftr::fft<NC, EC, 1>(v, j, buf, a.tw, TWN);
-    if (a.aux) {   // (A v) on the rows = the masked fine-grid values (the FC_OUT_GATHER output)
-#pragma unroll
-      for (int e = 0; e < EC; ++e)
-        if ((mbits >> e) & 1u) {
-          const int r = row_of(a, (int64_t)(j + e * T) * W + col);
-          a.aux[r + cc.cre * a.ldaux] = v[e].x;
-          if (cc.has_im) a.aux[r + cc.cim * a.ldaux] = v[e].y;
-        }
-    }
 #pragma unroll
     for (int e = 0; e < EC; ++e)
       if (!((mbits >> e) & 1u)) v[e] = czero();
@@ -490,15 +479,6 @@ static az_status_t run1f(const P1f& a0, int op, int src, int64_t npairs, int64_t
         AZ_TRY(frows<NR2, FR_ZSTAR>(a, nb, st));
         AZ_TRY(fcols<NC, FC_OUT_COEF_ADD, SRC_VEC>(a, N2, nb, 1.0 / (double)a.n, st));
         break;
-      case OP_ZSTAR_ADD: {   // x = x2 + Z* r: in = x2, in2 = r, out = x
-        P1f ar = a;
-        ar.in = a.in2;
-        ar.ldin = a.ldin2;
-        AZ_TRY(fcols<NC, FC_IN_ROWS, SRC_VEC>(ar, L2, nb, 1.0, st));
-        AZ_TRY(frows<NR2, FR_ZSTAR>(a, nb, st));
-        AZ_TRY(fcols<NC, FC_OUT_COEF_ADD, SRC_VEC>(a, N2, nb, 1.0 / (double)a.n, st));
-        break;
-      }
       case OP_AT:
         AZ_TRY(fcols<NC, FC_IN_ROWS, SRC_VEC>(a, L2, nb, 1.0, st));
         AZ_TRY(frows<NR2, FR_AT>(a, nb, st));
@@ -538,8 +518,6 @@ static P1f make_p1f(az_plan_s* p) {
   a.in2 = nullptr;
   a.ldin2 = 0;
   a.out = nullptr;
-  a.aux = nullptr;
-  a.ldaux = 0;
   a.aux2 = nullptr;
   a.ldaux2 = 0;
   a.Z2 = nullptr;
@@ -622,41 +600,6 @@ az_status_t az1f_step2(az_plan_s* p, const double* x2, int64_t ldx2, const doubl
   a.col0 = 0;
   const int64_t npairs = (nvec + 1) / 2;
   AZ_1F_DISPATCH(run1f, a, OP_STEP2, SRC_VEC, npairs, p->Bmax, st)
-}
-
-// The sketch S = (A - A Z* A) Omega[:, col0 .. col0 + ncols) that also keeps A Omega on the rows
-// (AOm, rows x ncols) and Omega itself (Om, N x ncols, optional): step 2 then forms x2 = Omega y and
-// b - A x2 = b - (A Omega) y with two small GEMMs instead of regenerating the probes and running
-// three FFT passes over x2.
-az_status_t az1f_sketch_keep(az_plan_s* p, int64_t col0, int64_t ncols, double* S, int64_t ldS, double* AOm,
-                             int64_t ldA, double* Om, int64_t ldOm, cudaStream_t st) {
-  P1f a = make_p1f(p);
-  a.out = S;
-  a.ldout = ldS;
-  a.aux = AOm;
-  a.ldaux = ldA;
-  a.aux2 = Om;
-  a.ldaux2 = ldOm;
-  a.nvec = ncols;
-  a.col0 = col0;
-  const int64_t npairs = (ncols + 1) / 2;
-  AZ_1F_DISPATCH(run1f, a, OP_STEP1, SRC_PROBE, npairs, p->Bmax, st)
-}
-
-// x = x2 + Z* r in three passes (r on the rows)
-az_status_t az1f_zstar_add(az_plan_s* p, const double* r, int64_t ldr, const double* x2, int64_t ldx2, double* x,
-                           int64_t ldx, int64_t nvec, cudaStream_t st) {
-  P1f a = make_p1f(p);
-  a.in = x2;
-  a.ldin = ldx2;
-  a.in2 = r;
-  a.ldin2 = ldr;
-  a.out = x;
-  a.ldout = ldx;
-  a.nvec = nvec;
-  a.col0 = 0;
-  const int64_t npairs = (nvec + 1) / 2;
-  AZ_1F_DISPATCH(run1f, a, OP_ZSTAR_ADD, SRC_VEC, npairs, p->Bmax, st)
 }
 
 // b' = (I - A Z*) b (out = bp) and Z* b (out2 = Zb, N x nvec) in one chain: the row pass also takes

@@ -474,7 +474,8 @@ struct az_factor_s {
   az_vbuf_s* Svb = nullptr;   // S's virtual range (physical HBM mapped per probe block), else cudaMalloc
   double* Q1 = nullptr;    // explicit leading kp columns of Q (rows x kp): S's own columns, in place
   double* Om = nullptr;    // explicit probes Omega (N x kp), the same Philox values as on the fly
-  double* AOm = nullptr;   // four-step layout, narrow probe counts: A Omega on the rows (rows x kpmax)
+  double* Mm = nullptr;    // four-step layout, <= 64 probes: M = Omega - Z* A Omega (N x kpmax), so a
+                           // factored solve is x = Z* b + M y (no x2 = Omega y, no step-2 passes)
   std::vector<int64_t> pj0;
   std::vector<int> pnb;
   int64_t np = 0;
@@ -866,9 +867,9 @@ extern "C" az_status_t az_factorize(az_plan_t p, double theta, int64_t R, int32_
   // four-step layout with at most 64 probes: keep A Omega (step 2 of a factored solve is then one
   // small GEMM and three FFT passes)
   if (p->layout == AZ_LAYOUT_1D_FOURSTEP && kpmax <= 64 && keep_aomega() &&
-      cudaMalloc(&f->AOm, sizeof(double) * rows * kpmax) != cudaSuccess) {
+      cudaMalloc(&f->Mm, sizeof(double) * p->N * kpmax) != cudaSuccess) {
     cudaGetLastError();
-    f->AOm = nullptr;
+    f->Mm = nullptr;
   }
   const int pfix = 10;
   double s1lo = 0.0;
@@ -883,9 +884,8 @@ extern "C" az_status_t az_factorize(az_plan_t p, double theta, int64_t R, int32_
       az_set_error("az_factorize: out of device memory (probe block %lld)", (long long)nb);
       return fail(AZ_ERR_OUT_OF_MEMORY);
     }
-    az_status_t s = f->AOm ? az1f_sketch_keep(p, (nb - 1) * R, R, Snew, rows, f->AOm + (nb - 1) * R * rows, rows,
-                                              nullptr, 0, st)
-                           : az_sketch(p, (nb - 1) * R, R, Snew, rows, st);
+    az_status_t s = f->Mm ? az1f_sketch_m(p, (nb - 1) * R, R, Snew, rows, f->Mm + (nb - 1) * R * p->N, p->N, st)
+                          : az_sketch(p, (nb - 1) * R, R, Snew, rows, st);
     if (s != AZ_OK) return fail(s);
     cudaEventRecord(ev.e[3], st);
     if ((s = az_qrw_apply(f->S, rows, rows, f->pj0.data(), f->pnb.data(), f->Tb, 0, f->np, Snew, rows, R, qrws, qrbytes, st)) != AZ_OK ||
@@ -956,7 +956,7 @@ extern "C" az_status_t az_factorize(az_plan_t p, double theta, int64_t R, int32_
       f->Q1 = f->S;
       cudaFree(f->Tb);
       f->Tb = nullptr;
-      if (cudaMalloc(&f->Om, sizeof(double) * p->N * kp) == cudaSuccess) {
+      if (!f->Mm && cudaMalloc(&f->Om, sizeof(double) * p->N * kp) == cudaSuccess) {
         AzTrace tr("omega_fill", st);
         k_omega_fill<<<az_div_up(((p->N + 1) / 2) * kp, 256), 256, 0, st>>>(p->N, 0, kp, f->Om, p->seed);
         if (cudaGetLastError() != cudaSuccess) return fail(AZ_ERR_CUDA);
@@ -993,7 +993,7 @@ extern "C" az_status_t az_factor_destroy(az_factor_t f) {
   cudaFree(f->Tb);
   cudaFree(f->P);
   cudaFree(f->Om);
-  cudaFree(f->AOm);
+  cudaFree(f->Mm);
   delete f;
   return AZ_OK;
 }
@@ -1118,7 +1118,11 @@ extern "C" az_status_t az_solve_factored(az_factor_t f, const double* b, int64_t
   const int64_t rows = f->rows, kp = f->kp;
   Ev ev;
   cudaEventRecord(ev.e[0], st);
-  AZ_TRY(az_apply_op(p, OP_RESID, b, ldb, w.bp, rows, nrhs, st));            // b' = (I - A Z*) b
+  const bool use_m = f->Mm && kp <= 64;
+  if (use_m)   // b' = (I - A Z*) b and Z* b (into the x2 slot)
+    AZ_TRY(az1f_resid_z(p, b, ldb, w.bp, rows, w.x2, p->N, nrhs, st));
+  else
+    AZ_TRY(az_apply_op(p, OP_RESID, b, ldb, w.bp, rows, nrhs, st));          // b' = (I - A Z*) b
   cudaEventRecord(ev.e[1], st);
   if (!f->Q1) {
     // compact form: Q^T b' through the Householder panels, y = P (Q^T b')[:kp], x2 = Omega y regenerated
@@ -1129,7 +1133,7 @@ extern "C" az_status_t az_solve_factored(az_factor_t f, const double* b, int64_t
       AZ_TRY(nn_product(f->P, f->kpmax, kp, kp, w.bp, rows, w.y, kp, nrhs, w.part, st));   // y = P (Q^T b')[:kp]
     }
     cudaEventRecord(ev.e[2], st);
-    AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, p->N, 0, st));
+    if (!use_m) AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, p->N, 0, st));
   } else {
     // c = Q1^T b' (split-K over the rows, ordered reduction), y = P c, x2 = Omega y
     {
@@ -1172,24 +1176,24 @@ extern "C" az_status_t az_solve_factored(az_factor_t f, const double* b, int64_t
     }
     cudaEventRecord(ev.e[2], st);
     const int64_t N = p->N;
-    AzTrace tr2("fac_omega_y", st, sizeof(double) * N * kp);
-    if (!f->Om)
-      AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, N, 0, st));   // Omega did not fit: regenerated
-    else
-      AZ_TRY(nn_product(f->Om, N, N, kp, w.y, kp, w.x2, N, nrhs, w.part, st));
-  }
-  if (f->AOm && kp <= 64) {
-    {
-      AzTrace tr("resid_aomega", st, 2 * rows * kp * nrhs);
-      const size_t gs = 2 * 64 * 68 * sizeof(double);
-      AZ_CUDA_CHECK(az_smem_attr(k_gemm_mn_small, gs));
-      for (int64_t c0 = 0; c0 < nrhs; c0 += 64)
-        k_gemm_mn_small<<<(unsigned)std::min<int64_t>(az_div_up(rows, 64), 3 * 148), 256, gs, st>>>(
-            f->AOm, rows, w.y + c0 * kp, kp, w.tmp + c0 * rows, rows, rows, (int)kp,
-            (int)std::min<int64_t>(64, nrhs - c0), b + c0 * ldb, ldb);
-      AZ_LAUNCH_CHECK();
+    if (!use_m) {
+      AzTrace tr2("fac_omega_y", st, sizeof(double) * N * kp);
+      if (!f->Om)
+        AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, N, 0, st));   // Omega did not fit: regenerated
+      else
+        AZ_TRY(nn_product(f->Om, N, N, kp, w.y, kp, w.x2, N, nrhs, w.part, st));
     }
-    AZ_TRY(az1f_zstar_add(p, w.tmp, rows, w.x2, p->N, x, ldx, nrhs, st));
+  }
+  if (use_m) {
+    // x = Z* b + M y  (M = Omega - Z* A Omega kept at factorisation, Z* b from the b' chain)
+    AzTrace tr("step2_gemm", st, 2 * p->N * kp * nrhs);
+    const size_t gs = 2 * 64 * 68 * sizeof(double);
+    AZ_CUDA_CHECK(az_smem_attr(k_gemm_mn_small, gs));
+    for (int64_t c0 = 0; c0 < nrhs; c0 += 64)
+      k_gemm_mn_small<<<(unsigned)std::min<int64_t>(az_div_up(p->N, 64), 3 * 148), 256, gs, st>>>(
+          f->Mm, p->N, w.y + c0 * kp, kp, x + c0 * ldx, ldx, p->N, (int)kp, (int)std::min<int64_t>(64, nrhs - c0),
+          w.x2 + c0 * p->N, p->N, 1.0);
+    AZ_LAUNCH_CHECK();
   } else {
     AZ_TRY(step2(p, w.x2, b, ldb, x, ldx, w.tmp, nrhs, st));
   }

@@ -215,6 +215,25 @@ def test_factored_explicit_matches_compact(nrhs, monkeypatch):
     assert np.all(np.abs(re - rc) <= 1e-8 * np.linalg.norm(b, axis=0)), (re, rc)
 
 
+def test_factored_four_step_m_path_compact_and_explicit(monkeypatch):
+    """Four-step factors with one probe block keep M = Omega - Z* A Omega and solve x = Z* b + M y;
+    with the compact Householder form (AZ_FACTOR_EXPLICIT=0) and the explicit Q1 the approximants
+    agree with a full az_solve."""
+    from paper_2308_14490_b200.api import Factor, Plan
+    cfg = I.make_config("interval", 8192, nrhs=6, R=48)
+    plan = Plan.from_config(cfg)
+    theta = max(cfg.tol * 1e-2, 1e-12)
+    b = I.rhs(cfg)
+    xs, _ = plan.solve(_dev(b), theta, cfg.R, 1)
+    grid = I.test_grid(cfg)
+    for mode in ("1", "0"):
+        monkeypatch.setenv("AZ_FACTOR_EXPLICIT", mode)
+        fac = Factor(plan, theta, cfg.R, 1)
+        xf, _ = fac.solve(_dev(b))
+        err = _approx_err(cfg, _host(xf), _host(xs), grid)
+        assert np.all(err <= 1e-9), (mode, err)
+
+
 PAPER_EPS_CASES = [("interval_paper_n256", I.make_config("interval_paper", 256), 4),
                    ("interval_paper_n1024", I.make_config("interval_paper", 1024), 8),
                    ("disk_paper_n32", I.make_config("disk_paper", 32), 12),
