@@ -53,7 +53,7 @@ def kernel_model(name, cfg, M, k_cols, k1=None, kept=False, split=False):
     pos_b, mask_b = (0, 0) if cfg.dim == 1 else (4, 1)
     # kept: the four-step narrow solve stores Omega (probe pass) for step 2 and takes the Z* parts of
     # the b' and sketch chains to the coefficient side (row passes write them, two column passes finish)
-    kw_om, kw_z = (2 * 8 * n, C * n) if kept else (0, 0)
+    kw_om, kw_z = (0, C * n) if kept else (0, 0)
     kw_aom = 0
     hbm = {
         "1f_cols_in_coef": C * n + kw_om,              # probes generated on chip; write spectrum (+ Omega)
@@ -70,7 +70,6 @@ def kernel_model(name, cfg, M, k_cols, k1=None, kept=False, split=False):
         "1f_cols_out_coef_add": C * n + 4 * 8 * n,             # spectrum + x2 in, x out
         "1f_cols_resid_mid": 2 * C * L + 2 * 8 * M,            # fine grid in/out, b rows in
         "1f_cols_out_z": C * n + 2 * 8 * n,                    # Z* b: spectrum in, 2 columns out
-        "1f_cols_out_omz": C * n + 2 * 2 * 8 * n,              # M = Omega - Z* A Omega: spectrum + Omega in, M out
     }
     if name in hbm:
         return "hbm", hbm[name]

@@ -47,10 +47,8 @@ struct P1f {
   int64_t ldin2;
   double* out;
   int64_t ldout;
-  double* aux2;          // FC_IN_COEF with probes: optional copy of the probe columns (the sketch keeps Omega)
-  int64_t ldaux2;
   cplx* Z2;              // FR_STEP1 / FR_RESID: optional Z*-part output (coefficient spectrum after IFFT_N2)
-  double* out2;          // FC_OUT_Z / FC_OUT_OMZ output (N x nvec)
+  double* out2;          // FC_OUT_Z output (N x nvec)
   int64_t ldout2;
   int64_t nvec, col0, pair0;
 };
@@ -88,9 +86,9 @@ AZ_D Cols1 pcols(const P1f& a, int b) {
 // 32 / TC rows per access.
 // ------------------------------------------------------------------------------------------
 enum { FC_IN_COEF = 0, FC_FINE_MASK = 1, FC_OUT_GATHER = 2, FC_OUT_RESID = 3, FC_IN_ROWS = 4, FC_OUT_COEF = 5,
-       FC_FWD_G = 6, FC_RESID_MID = 7, FC_OUT_COEF_ADD = 8, FC_OUT_Z = 9, FC_OUT_OMZ = 10 };
-// FC_OUT_Z:   IFFT_N1 of the Z2 buffer -> out2 = (.) / n          (Z* b from the b' chain)
-// FC_OUT_OMZ: IFFT_N1 of the Z2 buffer -> out2 = out2 - (.) / n   (M = Omega - Z* A Omega in place)
+       FC_FWD_G = 6, FC_RESID_MID = 7, FC_OUT_COEF_ADD = 8, FC_OUT_Z = 9 };
+// FC_OUT_Z: IFFT_N1 of the Z2 buffer -> out2 = (.) / n  (Z* b from the b' chain; M = Omega - Z* A Omega
+//           from the sketch, whose row pass wrote the spectrum r^ = v^ - w^)
 // FC_RESID_MID: IFFT_N1 -> r = b - (A x) on Omega, 0 outside -> FFT_N1 -> twiddle  (the A -> b - A x ->
 //               Z* junction of step 2 in one pass, no row vector written or read)
 // FC_OUT_COEF_ADD: IFFT_N1 -> x = x2 + (.) / n  (the closing addition of step 2)
@@ -106,10 +104,9 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
   const int c0 = blockIdx.x * TC;
   const int col = c0 + c;
   const Cols1 cc = pcols(a, b);
-  const bool coef = (KIND == FC_IN_COEF || KIND == FC_OUT_COEF || KIND == FC_OUT_COEF_ADD || KIND == FC_OUT_Z ||
-                     KIND == FC_OUT_OMZ);
+  const bool coef = (KIND == FC_IN_COEF || KIND == FC_OUT_COEF || KIND == FC_OUT_COEF_ADD || KIND == FC_OUT_Z);
   const int W = coef ? a.N2 : a.L2;                    // row length of the matrix
-  cplx* C1b = (KIND == FC_OUT_Z || KIND == FC_OUT_OMZ) ? a.Z2 + (int64_t)b * a.n : a.C1 + (int64_t)b * a.n;
+  cplx* C1b = (KIND == FC_OUT_Z) ? a.Z2 + (int64_t)b * a.n : a.C1 + (int64_t)b * a.n;
   cplx* Gb = a.G + (int64_t)b * a.L;
   const int64_t tmul = coef ? a.s : 1;                 // e^{-2 pi i n2 k1 / n} = e^{-2 pi i (s n2 k1) / L}
   cplx* buf = sm + c * fftr::padded_len(NC);
@@ -128,14 +125,6 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
       const double send = odd ? z.x : z.y;
       const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
       v[e] = odd ? make_double2(recv, z.y) : make_double2(z.x, recv);
-    }
-    if (a.aux2) {   // Omega itself, natural row order (x2 = Omega y later reads it instead of regenerating)
-#pragma unroll
-      for (int e = 0; e < EC; ++e) {
-        const int64_t i = (int64_t)(j + e * T) * W + col;
-        a.aux2[i + cc.cre * a.ldaux2] = v[e].x;
-        if (cc.has_im) a.aux2[i + cc.cim * a.ldaux2] = v[e].y;
-      }
     }
   } else if constexpr (KIND == FC_IN_COEF) {
 #pragma unroll
@@ -229,13 +218,6 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
       a.out2[i + cc.cre * a.ldout2] = v[e].x * cout;
       if (cc.has_im) a.out2[i + cc.cim * a.ldout2] = v[e].y * cout;
     }
-  } else if constexpr (KIND == FC_OUT_OMZ) {
-#pragma unroll
-    for (int e = 0; e < EC; ++e) {
-      const int64_t i = (int64_t)(j + e * T) * W + col;
-      a.out2[i + cc.cre * a.ldout2] = fma(-v[e].x, cout, a.out2[i + cc.cre * a.ldout2]);
-      if (cc.has_im) a.out2[i + cc.cim * a.ldout2] = fma(-v[e].y, cout, a.out2[i + cc.cim * a.ldout2]);
-    }
   } else {   // FC_OUT_COEF
 #pragma unroll
     for (int e = 0; e < EC; ++e) {
@@ -315,8 +297,12 @@ __global__ void __launch_bounds__(RPC * (LR2 / EL), MINB) k1f_rows(P1f a, int nr
       if constexpr (KIND != FR_AT) acc = cscale(acc, Zs[k2]);
       vn[e] = acc;
     }
+    if constexpr (KIND == FR_STEP1) {   // r^ = v^ - w^  (the spectrum of M = v - Z* A v)
+#pragma unroll
+      for (int e = 0; e < EN; ++e) vn[e] = csub(Cs[j + e * T], vn[e]);
+    }
     if constexpr (KIND == FR_STEP1 || KIND == FR_RESID) {
-      if (a.Z2) {   // the Z* part itself (Z* A v, Z* b) on to the coefficient side: IFFT_N2 + twiddle
+      if (a.Z2) {   // r^ (STEP1: M = v - Z* A v) or w^ (RESID: Z* b) on to the coefficient side: IFFT_N2 + twiddle
         cplx wz[EN];
 #pragma unroll
         for (int e = 0; e < EN; ++e) wz[e] = vn[e];
@@ -332,10 +318,6 @@ __global__ void __launch_bounds__(RPC * (LR2 / EL), MINB) k1f_rows(P1f a, int nr
           }
         }
       }
-    }
-    if constexpr (KIND == FR_STEP1) {
-#pragma unroll
-      for (int e = 0; e < EN; ++e) vn[e] = csub(Cs[j + e * T], vn[e]);
     }
   }
   if constexpr (KIND == FR_ZSTAR || KIND == FR_AT) {
@@ -400,7 +382,7 @@ static az_status_t fcols_e(const P1f& a, int ncols, int nb, double cout, cudaStr
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   static const char* names[] = {"1f_cols_in_coef", "1f_cols_fine_mask", "1f_cols_out_gather", "1f_cols_out_resid",
                                 "1f_cols_in_rows", "1f_cols_out_coef", "1f_cols_fwd", "1f_cols_resid_mid",
-                                "1f_cols_out_coef_add", "1f_cols_out_z", "1f_cols_out_omz"};
+                                "1f_cols_out_coef_add", "1f_cols_out_z"};
   AzTrace tr(names[KIND], st, nb);
   kern<<<dim3(az_div_up(ncols, TC), nb), TC * T, sm, st>>>(a, cout);
   AZ_LAUNCH_CHECK();
@@ -459,7 +441,7 @@ static az_status_t run1f(const P1f& a0, int op, int src, int64_t npairs, int64_t
         AZ_TRY(fcols<NC, FC_FINE_MASK, SRC_VEC>(a, L2, nb, 1.0, st));
         AZ_TRY(frows<NR2, FR_STEP1>(a, nb, st));
         AZ_TRY(fcols<NC, FC_OUT_GATHER, SRC_VEC>(a, L2, nb, 1.0, st));
-        if (a.Z2) AZ_TRY(fcols<NC, FC_OUT_OMZ, SRC_VEC>(a, N2, nb, 1.0 / (double)a.n, st));
+        if (a.Z2) AZ_TRY(fcols<NC, FC_OUT_Z, SRC_VEC>(a, N2, nb, 1.0 / (double)a.n, st));   // M
         break;
       case OP_RESID:
         AZ_TRY(fcols<NC, FC_IN_ROWS, SRC_VEC>(a, L2, nb, 1.0, st));
@@ -518,8 +500,6 @@ static P1f make_p1f(az_plan_s* p) {
   a.in2 = nullptr;
   a.ldin2 = 0;
   a.out = nullptr;
-  a.aux2 = nullptr;
-  a.ldaux2 = 0;
   a.Z2 = nullptr;
   a.out2 = nullptr;
   a.ldout2 = 0;
@@ -620,16 +600,14 @@ az_status_t az1f_resid_z(az_plan_s* p, const double* b, int64_t ldb, double* bp,
   AZ_1F_DISPATCH(run1f, a, OP_RESID, SRC_VEC, npairs, p->Bmax, st)
 }
 
-// S = (A - A Z* A) Omega[:, col0 ..) and, over the probes kept in Om by the probe pass,
-// M = Omega - Z* A Omega (step 2 of the solve is then x = Z* b + M y: no FFT pass, PAPER.md:229-230
-// by linearity of Z*)
+// S = (A - A Z* A) Omega[:, col0 ..) and M = Omega - Z* A Omega (Om, N x ncols): the step-1 row
+// pass already forms M's spectrum r^ = v^ - w^ and takes it to the coefficient side; one column pass
+// finishes it.  Step 2 of the solve is then x = Z* b + M y (PAPER.md:229-230 by linearity of Z*).
 az_status_t az1f_sketch_m(az_plan_s* p, int64_t col0, int64_t ncols, double* S, int64_t ldS, double* Om, int64_t ldOm,
                           cudaStream_t st) {
   P1f a = make_p1f(p);
   a.out = S;
   a.ldout = ldS;
-  a.aux2 = Om;
-  a.ldaux2 = ldOm;
   a.Z2 = p->d_Z2;
   a.out2 = Om;
   a.ldout2 = ldOm;
