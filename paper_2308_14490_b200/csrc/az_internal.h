@@ -71,6 +71,9 @@ struct az_plan_s {
   void* d_solve_ws = nullptr;
   size_t d_solve_ws_bytes = 0;
   az_pipe_s* pipe = nullptr;
+  // side stream of az_solve: the Z* b / M column passes run beside the TSQR merges and the SVD
+  cudaStream_t side = nullptr;
+  cudaEvent_t side_ev[3] = {nullptr, nullptr, nullptr};
 };
 
 constexpr int TWN = 2048;
@@ -89,10 +92,13 @@ az_status_t az1f_step2(az_plan_s* p, const double* x2, int64_t ldx2, const doubl
                        int64_t ldx, int64_t nvec, cudaStream_t st);
 // b' = (I - A Z*) b that also returns Z* b (N x nvec); the sketch that also returns
 // M = Omega - Z* A Omega (N x ncols, written over the kept Omega)
+// Zspec: the spectrum buffer (B x N complex; null = the plan's d_Z2); defer: leave the closing column
+// pass to az1f_out_z (single batch only), so it can run on another stream
 az_status_t az1f_resid_z(az_plan_s* p, const double* b, int64_t ldb, double* bp, int64_t ldbp, double* Zb, int64_t ldz,
-                         int64_t nvec, cudaStream_t st);
+                         int64_t nvec, cudaStream_t st, cplx* Zspec = nullptr, bool defer = false);
 az_status_t az1f_sketch_m(az_plan_s* p, int64_t col0, int64_t ncols, double* S, int64_t ldS, double* Om, int64_t ldOm,
-                          cudaStream_t st);
+                          cudaStream_t st, cplx* Zspec = nullptr, bool defer = false);
+az_status_t az1f_out_z(az_plan_s* p, const cplx* Zspec, double* out, int64_t ldout, int64_t nvec, cudaStream_t st);
 
 // --- 2-D layout (az_ops2d.cu)
 az_status_t az2_apply(az_plan_s* p, int op, int src, const double* in, int64_t ldin, double* out,
@@ -103,8 +109,10 @@ az_status_t az_fft_batch(const cplx* tw, cplx* data, int64_t len, int64_t count,
 
 // --- QR / SVD / solve
 // a_scratch: A may be overwritten (the solve's sketch buffer), which enables the split TSQR leaf
+// after_leaf (optional): recorded once the leaf passes are enqueued (before the merge tree)
 az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R, int64_t ldr,
-                         void* ws, size_t ws_bytes, cudaStream_t st, int64_t k1 = 0, bool a_scratch = false);
+                         void* ws, size_t ws_bytes, cudaStream_t st, int64_t k1 = 0, bool a_scratch = false,
+                         cudaEvent_t after_leaf = nullptr);
 size_t az_qr_ws_bytes(int64_t m, int64_t k);
 az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta,
                          double* y, int64_t ldy, double* sigma_out, int64_t* rank_out,

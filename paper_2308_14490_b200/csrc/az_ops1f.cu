@@ -50,6 +50,7 @@ struct P1f {
   cplx* Z2;              // FR_STEP1 / FR_RESID: optional Z*-part output (coefficient spectrum after IFFT_N2)
   double* out2;          // FC_OUT_Z output (N x nvec)
   int64_t ldout2;
+  bool defer_z;          // skip the closing FC_OUT_Z pass (az1f_out_z runs it later)
   int64_t nvec, col0, pair0;
 };
 
@@ -441,13 +442,13 @@ static az_status_t run1f(const P1f& a0, int op, int src, int64_t npairs, int64_t
         AZ_TRY(fcols<NC, FC_FINE_MASK, SRC_VEC>(a, L2, nb, 1.0, st));
         AZ_TRY(frows<NR2, FR_STEP1>(a, nb, st));
         AZ_TRY(fcols<NC, FC_OUT_GATHER, SRC_VEC>(a, L2, nb, 1.0, st));
-        if (a.Z2) AZ_TRY(fcols<NC, FC_OUT_Z, SRC_VEC>(a, N2, nb, 1.0 / (double)a.n, st));   // M
+        if (a.Z2 && !a.defer_z) AZ_TRY(fcols<NC, FC_OUT_Z, SRC_VEC>(a, N2, nb, 1.0 / (double)a.n, st));   // M
         break;
       case OP_RESID:
         AZ_TRY(fcols<NC, FC_IN_ROWS, SRC_VEC>(a, L2, nb, 1.0, st));
         AZ_TRY(frows<NR2, FR_RESID>(a, nb, st));
         AZ_TRY(fcols<NC, FC_OUT_RESID, SRC_VEC>(a, L2, nb, 1.0, st));
-        if (a.Z2) AZ_TRY(fcols<NC, FC_OUT_Z, SRC_VEC>(a, N2, nb, 1.0 / (double)a.n, st));
+        if (a.Z2 && !a.defer_z) AZ_TRY(fcols<NC, FC_OUT_Z, SRC_VEC>(a, N2, nb, 1.0 / (double)a.n, st));
         break;
       case OP_ZSTAR:
         AZ_TRY(fcols<NC, FC_IN_ROWS, SRC_VEC>(a, L2, nb, 1.0, st));
@@ -503,6 +504,7 @@ static P1f make_p1f(az_plan_s* p) {
   a.Z2 = nullptr;
   a.out2 = nullptr;
   a.ldout2 = 0;
+  a.defer_z = false;
   a.ldin = a.ldout = 0;
   a.nvec = a.col0 = a.pair0 = 0;
   return a;
@@ -585,13 +587,14 @@ az_status_t az1f_step2(az_plan_s* p, const double* x2, int64_t ldx2, const doubl
 // b' = (I - A Z*) b (out = bp) and Z* b (out2 = Zb, N x nvec) in one chain: the row pass also takes
 // its Z* b spectrum to the coefficient side, one extra column pass finishes it.
 az_status_t az1f_resid_z(az_plan_s* p, const double* b, int64_t ldb, double* bp, int64_t ldbp, double* Zb, int64_t ldz,
-                         int64_t nvec, cudaStream_t st) {
+                         int64_t nvec, cudaStream_t st, cplx* Zspec, bool defer) {
   P1f a = make_p1f(p);
   a.in = b;
   a.ldin = ldb;
   a.out = bp;
   a.ldout = ldbp;
-  a.Z2 = p->d_Z2;
+  a.Z2 = Zspec ? Zspec : p->d_Z2;
+  a.defer_z = defer && (nvec + 1) / 2 <= p->Bmax;
   a.out2 = Zb;
   a.ldout2 = ldz;
   a.nvec = nvec;
@@ -604,15 +607,39 @@ az_status_t az1f_resid_z(az_plan_s* p, const double* b, int64_t ldb, double* bp,
 // pass already forms M's spectrum r^ = v^ - w^ and takes it to the coefficient side; one column pass
 // finishes it.  Step 2 of the solve is then x = Z* b + M y (PAPER.md:229-230 by linearity of Z*).
 az_status_t az1f_sketch_m(az_plan_s* p, int64_t col0, int64_t ncols, double* S, int64_t ldS, double* Om, int64_t ldOm,
-                          cudaStream_t st) {
+                          cudaStream_t st, cplx* Zspec, bool defer) {
   P1f a = make_p1f(p);
   a.out = S;
   a.ldout = ldS;
-  a.Z2 = p->d_Z2;
+  a.Z2 = Zspec ? Zspec : p->d_Z2;
+  a.defer_z = defer && (ncols + 1) / 2 <= p->Bmax;
   a.out2 = Om;
   a.ldout2 = ldOm;
   a.nvec = ncols;
   a.col0 = col0;
   const int64_t npairs = (ncols + 1) / 2;
   AZ_1F_DISPATCH(run1f, a, OP_STEP1, SRC_PROBE, npairs, p->Bmax, st)
+}
+
+// The closing column pass of az1f_resid_z / az1f_sketch_m (deferred, single batch): IFFT_N1 of the
+// spectra in Zspec -> out (N x nvec)
+template <int NC, int NR2>
+static az_status_t out_z_run(const P1f& a, int64_t npairs, cudaStream_t st) {
+  return fcols<NC, FC_OUT_Z, SRC_VEC>(a, NR2, (int)npairs, 1.0 / (double)a.n, st);
+}
+
+az_status_t az1f_out_z(az_plan_s* p, const cplx* Zspec, double* out, int64_t ldout, int64_t nvec, cudaStream_t st) {
+  P1f a = make_p1f(p);
+  a.Z2 = const_cast<cplx*>(Zspec);
+  a.out2 = out;
+  a.ldout2 = ldout;
+  a.nvec = nvec;
+  a.col0 = 0;
+  a.pair0 = 0;
+  const int64_t npairs = (nvec + 1) / 2;
+  if (npairs > p->Bmax) {
+    az_set_error("az1f_out_z: more than one batch");
+    return AZ_ERR_NOT_SUPPORTED;
+  }
+  AZ_1F_DISPATCH(out_z_run, a, npairs, st)
 }

@@ -369,6 +369,12 @@ static int ilog2(int64_t v) { int k = 0; while ((int64_t(1) << k) < v) ++k; retu
 static void plan_free(az_plan_s* p) {
   if (p) az_pipe_destroy(p);
   if (!p) return;
+  if (p->side) {
+    cudaStreamSynchronize(p->side);
+    cudaStreamDestroy(p->side);
+    for (auto& e : p->side_ev)
+      if (e) cudaEventDestroy(e);
+  }
   if (p->d_W0y == p->d_W0) p->d_W0y = nullptr;   // aliases of the x tables (square boxes)
   if (p->d_W2y == p->d_W2) p->d_W2y = nullptr;
   void* ptrs[] = {p->d_mask, p->d_pos, p->d_W0, p->d_W2, p->d_W0y, p->d_W2y, p->d_Wr, p->d_zinv, p->d_tw,

@@ -665,7 +665,8 @@ static bool tsqr_split() {   // AZ_TSQR_SPLIT=0 keeps the single-pass leaf for [
 }
 
 az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R, int64_t ldr,
-                         void* ws, size_t ws_bytes, cudaStream_t st, int64_t k1, bool a_scratch) {
+                         void* ws, size_t ws_bytes, cudaStream_t st, int64_t k1, bool a_scratch,
+                         cudaEvent_t after_leaf) {
   if (k1 <= 0 || k1 > k) k1 = k;
   if (ws_bytes < az_qr_ws_bytes(m, k)) {
     az_set_error("az_qr_r: workspace too small");
@@ -734,6 +735,7 @@ az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R
   } else {
     AZ_TRY(tsqr_pass(q, (int)P, st));
   }
+  if (after_leaf) AZ_CUDA_CHECK(cudaEventRecord(after_leaf, st));
   int64_t cur = P;
   int which = 0;
   // fixed-shape reduction tree: groups of 4 R factors

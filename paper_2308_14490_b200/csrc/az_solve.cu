@@ -138,6 +138,7 @@ struct SolveWS {
   double* tmp;   // rows x nrhs
   double* x2;    // N x nrhs
   double* Zb;    // N x nrhs: Z* b from the b' chain (four-step narrow path), else null
+  cplx* Zs;      // the b' chain's Z* b spectra (N x ceil(nrhs / 2) complex), same condition
   double* Om;    // N x Rmax: M = Omega - Z* A Omega from the sketch (same condition)
   void* qrws;
   size_t qrbytes;
@@ -188,6 +189,7 @@ static SolveWS layout(az_plan_s* p, int64_t nrhs, int64_t R, int32_t max_blocks,
   w.wide = kt > AZ_NARROW_MAX;
   const bool keep = !w.wide && p->layout == AZ_LAYOUT_1D_FOURSTEP && keep_aomega();
   w.Zb = keep ? (double*)take(sizeof(double) * p->N * nrhs) : nullptr;
+  w.Zs = keep ? (cplx*)take(sizeof(cplx) * p->N * ((nrhs + 1) / 2)) : nullptr;
   w.Om = keep ? (double*)take(sizeof(double) * p->N * Rmax) : nullptr;
   if (w.wide) {
     const int64_t QBw = az_qrw_panel_width();
@@ -281,10 +283,18 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   cudaEventRecord(ev.e[0], st);
   // ---- right-hand side b' = (I - A Z*) b (narrow single-block solve: straight into S) ----
   const bool bp_in_S = !w.wide && max_blocks == 1;
-  if (w.Zb)   // b' and, for step 2, Z* b (one extra column pass)
-    AZ_TRY(az1f_resid_z(p, b, ldb, bp_in_S ? w.S + R * rows : w.bp, rows, w.Zb, p->N, nrhs, st));
-  else
+  // the Z* b and M column passes are only needed by step 2: with one probe block and one batch per
+  // chain they run on a side stream beside the TSQR merges and the SVD (which leave most SMs idle)
+  const bool side = w.Zb && max_blocks == 1 && (nrhs + 1) / 2 <= p->Bmax && (R + 1) / 2 <= p->Bmax;
+  if (side && !p->side) {
+    AZ_CUDA_CHECK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+    for (auto& e : p->side_ev) AZ_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  if (w.Zb) {   // b' and, for step 2, Z* b (one extra column pass)
+    AZ_TRY(az1f_resid_z(p, b, ldb, bp_in_S ? w.S + R * rows : w.bp, rows, w.Zb, p->N, nrhs, st, w.Zs, side));
+  } else {
     AZ_TRY(az_apply_op(p, OP_RESID, b, ldb, bp_in_S ? w.S + R * rows : w.bp, rows, nrhs, st));
+  }
   cudaEventRecord(ev.e[1], st);
   if (dbg_host) fprintf(stderr, "az_solve host: resid issued +%.2f ms\n", hnow() - th0);
   double ms_sketch = 0, ms_qr = 0, ms_svd = 0;
@@ -301,8 +311,11 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
     const int64_t kt = kp + nrhs;
     cudaEvent_t e0 = ev.e[2], e1 = ev.e[3], e2 = ev.e[4], e3 = ev.e[5];
     cudaEventRecord(e0, st);
-    if (w.Om)   // the sketch and M = Omega - Z* A Omega for step 2
-      AZ_TRY(az1f_sketch_m(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, w.Om + (nb - 1) * R * p->N, p->N, st));
+    if (w.Om) {   // the sketch and M = Omega - Z* A Omega for step 2
+      AZ_TRY(az1f_sketch_m(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, w.Om + (nb - 1) * R * p->N, p->N, st,
+                           nullptr, side));
+
+    }
     else
       AZ_TRY(az_sketch(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, st));
     if (!w.wide && !bp_in_S) {
@@ -314,7 +327,14 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
     if (dbg_host) fprintf(stderr, "az_solve host: sketch issued +%.2f ms\n", hnow() - th0);
     if (!w.wide) {
       // a single probe block: the sketch columns are not needed after this QR (split leaf allowed)
-      AZ_TRY(az_qr_r_impl(w.S, rows, kt, rows, w.Rf, kt, w.qrws, w.qrbytes, st, kp, max_blocks == 1));
+      AZ_TRY(az_qr_r_impl(w.S, rows, kt, rows, w.Rf, kt, w.qrws, w.qrbytes, st, kp, max_blocks == 1,
+                          side ? p->side_ev[0] : nullptr));
+      if (side) {   // the deferred Z* b and M passes beside the merges and the SVD
+        AZ_CUDA_CHECK(cudaStreamWaitEvent(p->side, p->side_ev[0], 0));
+        AZ_TRY(az1f_out_z(p, w.Zs, w.Zb, p->N, nrhs, p->side));
+        AZ_TRY(az1f_out_z(p, p->d_Z2, w.Om, p->N, R, p->side));
+        AZ_CUDA_CHECK(cudaEventRecord(p->side_ev[2], p->side));
+      }
     } else {
       if (kp > rows) {
         az_set_error("az_solve: %lld probe columns exceed the %lld rows", (long long)kp, (long long)rows);
@@ -380,6 +400,7 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   if (w.Om) {
     // by linearity of Z* (PAPER.md:229-230): x = Omega y + Z* b - (Z* A Omega) y = Z* b + M y, with
     // Z* b and M = Omega - Z* A Omega produced by the b' and sketch chains: one DMMA pass, no FFT
+    if (side) AZ_CUDA_CHECK(cudaStreamWaitEvent(st, p->side_ev[2], 0));   // Z* b and M are ready
     AzTrace tr("step2_gemm", st, 2 * p->N * kp * nrhs);
     if (kp <= 64) {
       const size_t gs = 2 * 64 * 68 * sizeof(double);
