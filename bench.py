@@ -378,9 +378,9 @@ def run_ours(args, cfg):
     kcols = reps[-1]["probes"] + cfg.nrhs
     dom = max(trace.items(), key=lambda kv: kv[1][1])
     name, (cnt, tot_ms, units) = dom
-    # the four-step narrow solve keeps Omega and A Omega from the sketch (az_solve.cu keep_aomega)
+    # the four-step narrow solve takes Z* b and M = Omega - Z* A Omega from its chains (az_solve.cu step2_linear)
     kept = (cfg.dim == 1 and cfg.N * cfg.s > 2048 and kcols <= 128
-            and os.environ.get("AZ_KEEP_AOMEGA", "1") != "0")
+            and os.environ.get("AZ_STEP2_LINEAR", "1") != "0")
     split = (kcols <= 128 and reps[-1]["probes"] <= 64 and cfg.nrhs <= 64 and max_blocks == 1
              and not args.sharded and os.environ.get("AZ_TSQR_SPLIT", "1") != "0")
     bound, per_unit = kernel_model(name, cfg, plan.M, kcols, reps[-1]["probes"], kept, split)

@@ -158,11 +158,12 @@ __global__ void k_gemm_mn(const double* A, int64_t lda, const double* Bm, int64_
 __global__ void k_gemm_mn_small(const double* A, int64_t lda, const double* Bm, int64_t ldb, double* Y, int64_t ldy,
                                 int64_t m, int k, int n, const double* C, int64_t ldc, double sgn = -1.0);
 
-// four-step narrow solves keep A Omega from the sketch for step 2 (AZ_KEEP_AOMEGA=0 disables)
-static bool keep_aomega() {
+// four-step narrow solves: step 2 as x = Z* b + M y from the b' and sketch chains (reading R30;
+// AZ_STEP2_LINEAR=0 disables)
+static bool step2_linear() {
   static int k = -1;
   if (k < 0) {
-    const char* e = getenv("AZ_KEEP_AOMEGA");
+    const char* e = getenv("AZ_STEP2_LINEAR");
     k = e ? atoi(e) : 1;
   }
   return k != 0;
@@ -187,7 +188,7 @@ static SolveWS layout(az_plan_s* p, int64_t nrhs, int64_t R, int32_t max_blocks,
   w.tmp = (double*)take(sizeof(double) * rows * nrhs);
   w.x2 = (double*)take(sizeof(double) * p->N * nrhs);
   w.wide = kt > AZ_NARROW_MAX;
-  const bool keep = !w.wide && p->layout == AZ_LAYOUT_1D_FOURSTEP && keep_aomega();
+  const bool keep = !w.wide && p->layout == AZ_LAYOUT_1D_FOURSTEP && step2_linear();
   w.Zb = keep ? (double*)take(sizeof(double) * p->N * nrhs) : nullptr;
   w.Zs = keep ? (cplx*)take(sizeof(cplx) * p->N * ((nrhs + 1) / 2)) : nullptr;
   w.Om = keep ? (double*)take(sizeof(double) * p->N * Rmax) : nullptr;
@@ -887,7 +888,7 @@ extern "C" az_status_t az_factorize(az_plan_t p, double theta, int64_t R, int32_
   }
   // four-step layout with at most 64 probes: keep A Omega (step 2 of a factored solve is then one
   // small GEMM and three FFT passes)
-  if (p->layout == AZ_LAYOUT_1D_FOURSTEP && kpmax <= 64 && keep_aomega() &&
+  if (p->layout == AZ_LAYOUT_1D_FOURSTEP && kpmax <= 64 && step2_linear() &&
       cudaMalloc(&f->Mm, sizeof(double) * p->N * kpmax) != cudaSuccess) {
     cudaGetLastError();
     f->Mm = nullptr;
