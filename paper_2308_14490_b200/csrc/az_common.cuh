@@ -27,6 +27,29 @@ AZ_HD cplx czero() { return make_double2(0.0, 0.0); }
 AZ_HD constexpr int spad(int i) { return i + (i >> 3); }
 AZ_HD constexpr int spad_len(int L) { return L + (L >> 3) + 1; }   // +1 staggers consecutive FFT buffers
 
+// 1 / d to within an ulp or so: the MUFU reciprocal seed refined by two Newton steps, for
+// latency- or issue-bound chains (the Householder reflector chain of the TSQR, the Jacobi rotation):
+// no IEEE division slow-path check.  d must be a nonzero normal number (callers guarantee it)
+AZ_D double fast_rcp(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
+// 1 / sqrt(x) likewise: MUFU seed, two Newton steps y (3 - x y^2) / 2 (x a positive normal number)
+AZ_D double fast_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  double t = fma(-hx * y, y, 0.5);
+  y = fma(y, t, y);
+  t = fma(-hx * y, y, 0.5);
+  return fma(y, t, y);
+}
+
 // --------------------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al. SC'11) and the probe generator.
 // Independent of oracle/philox.py by construction (task rules); same specification.

@@ -74,6 +74,9 @@ struct az_plan_s {
   // side stream of az_solve: the Z* b / M column passes run beside the TSQR merges and the SVD
   cudaStream_t side = nullptr;
   cudaEvent_t side_ev[3] = {nullptr, nullptr, nullptr};
+  // high-priority stream for the TSQR and the SVD while the side stream runs: the block scheduler
+  // then hands freed SMs to the merge tree (the critical path) before the side stream's passes
+  cudaStream_t hi = nullptr;
 };
 
 constexpr int TWN = 2048;

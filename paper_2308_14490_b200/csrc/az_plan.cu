@@ -375,6 +375,10 @@ static void plan_free(az_plan_s* p) {
     for (auto& e : p->side_ev)
       if (e) cudaEventDestroy(e);
   }
+  if (p->hi) {
+    cudaStreamSynchronize(p->hi);
+    cudaStreamDestroy(p->hi);
+  }
   if (p->d_W0y == p->d_W0) p->d_W0y = nullptr;   // aliases of the x tables (square boxes)
   if (p->d_W2y == p->d_W2) p->d_W2y = nullptr;
   void* ptrs[] = {p->d_mask, p->d_pos, p->d_W0, p->d_W2, p->d_W0y, p->d_W2y, p->d_Wr, p->d_zinv, p->d_tw,

@@ -117,11 +117,11 @@ __global__ void __launch_bounds__(512, 1) k_tsqr(QRIn q) {
         double tau = 0.0, scale = 0.0, beta = alpha;
         if (sig > 0.0) {
           const double s2 = fma(alpha, alpha, sig);
-          const double rinv = rsqrt(s2);
+          const double rinv = fast_rsqrt(s2);
           const double nrm = s2 * rinv;
           beta = alpha >= 0.0 ? -nrm : nrm;
           tau = fma(fabs(alpha), rinv, 1.0);
-          scale = 1.0 / (alpha - beta);
+          scale = fast_rcp(alpha - beta);
         }
 #pragma unroll
         for (int r = 0; r < RPL; ++r) vj[lane + 32 * r] = xs[r] * scale;
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(512, 1) k_tsqr_blk(QRb q) {
             const double nrm = sqrt(fma(alpha, alpha, sg));
             beta = alpha >= 0.0 ? -nrm : nrm;
             tau = (beta - alpha) / beta;
-            scale = 1.0 / (alpha - beta);
+            scale = fast_rcp(alpha - beta);
           }
           if (lane == 0) taus[c] = tau;
 #pragma unroll

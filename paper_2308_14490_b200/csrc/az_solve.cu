@@ -169,6 +169,16 @@ static bool step2_linear() {
   return k != 0;
 }
 
+// AZ_SOLVE_HI=0: the QR and the SVD stay on the caller's stream while the side stream runs
+static bool no_hi() {
+  static int k = -1;
+  if (k < 0) {
+    const char* e = getenv("AZ_SOLVE_HI");
+    k = e ? atoi(e) : 1;
+  }
+  return k == 0;
+}
+
 static SolveWS layout(az_plan_s* p, int64_t nrhs, int64_t R, int32_t max_blocks, char* base) {
   SolveWS w;
   const int64_t rows = p->M + p->Mb;
@@ -290,7 +300,12 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   if (side && !p->side) {
     AZ_CUDA_CHECK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
     for (auto& e : p->side_ev) AZ_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    int lo = 0, top = 0;
+    AZ_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &top));
+    AZ_CUDA_CHECK(cudaStreamCreateWithPriority(&p->hi, cudaStreamNonBlocking, top));
   }
+  // the QR and the SVD: on the high-priority stream beside the side stream (joined back below)
+  cudaStream_t qs = side && !no_hi() ? p->hi : st;
   if (w.Zb) {   // b' and, for step 2, Z* b (one extra column pass)
     AZ_TRY(az1f_resid_z(p, b, ldb, bp_in_S ? w.S + R * rows : w.bp, rows, w.Zb, p->N, nrhs, st, w.Zs, side));
   } else {
@@ -325,10 +340,11 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
       AZ_LAUNCH_CHECK();
     }
     cudaEventRecord(e1, st);
+    if (qs != st) AZ_CUDA_CHECK(cudaStreamWaitEvent(qs, e1, 0));
     if (dbg_host) fprintf(stderr, "az_solve host: sketch issued +%.2f ms\n", hnow() - th0);
     if (!w.wide) {
       // a single probe block: the sketch columns are not needed after this QR (split leaf allowed)
-      AZ_TRY(az_qr_r_impl(w.S, rows, kt, rows, w.Rf, kt, w.qrws, w.qrbytes, st, kp, max_blocks == 1,
+      AZ_TRY(az_qr_r_impl(w.S, rows, kt, rows, w.Rf, kt, w.qrws, w.qrbytes, qs, kp, max_blocks == 1,
                           side ? p->side_ev[0] : nullptr));
       if (side) {   // the deferred Z* b and M passes beside the merges and the SVD
         AZ_CUDA_CHECK(cudaStreamWaitEvent(p->side, p->side_ev[0], 0));
@@ -351,7 +367,7 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
       k_copy_cols<<<az_div_up(kp * nrhs, 256), 256, 0, st>>>(w.bp, rows, w.Rf + kp * kt, kt, kp, nrhs);
       AZ_LAUNCH_CHECK();
     }
-    cudaEventRecord(e2, st);
+    cudaEventRecord(e2, qs);
     if (dbg_host) fprintf(stderr, "az_solve host: qr issued +%.2f ms\n", hnow() - th0);
     bool full_svd = true;
     if (w.wide && nb >= 2 && nb < max_blocks) {
@@ -375,7 +391,7 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
     }
     if (full_svd) {
       AZ_TRY(az_tsvd_impl(w.Rf, kt, kp, nrhs, theta, w.y, kp, w.sig, async_mode ? nullptr : &rank, w.svdws,
-                          w.svdbytes, st));
+                          w.svdbytes, qs));
       if (w.wide && nb < max_blocks) {   // sigma_1 lower bound for the next block's pre-test
         double s1 = 0.0;
         AZ_CUDA_CHECK(cudaMemcpyAsync(&s1, w.sig, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -383,7 +399,8 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
         s1lo = std::max(s1lo, s1);
       }
     }
-    cudaEventRecord(e3, st);
+    cudaEventRecord(e3, qs);
+    if (qs != st) AZ_CUDA_CHECK(cudaStreamWaitEvent(st, e3, 0));
     if (!async_mode) {
       cudaEventSynchronize(e3);
       ms_sketch += ms_between(e0, e1);

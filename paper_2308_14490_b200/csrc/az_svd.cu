@@ -12,6 +12,8 @@
 // per round, one warp per pair.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "az_internal.h"
 
 AZ_D double wsum(double v) {
@@ -113,13 +115,16 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
         g = hsum(g);
         if (!pair_ok || fmin(a, b) < negl || g == 0.0) continue;
         const double g2 = g * g, ab = a * b;
-        off_me = fmax(off_me, g2 / ab);
+        if (g2 > off_me * ab) off_me = g2 / ab;   // running max of g^2 / ab, divides only on a new max
         if (!(g2 > tol * tol * ab)) continue;
         // tan of the rotation angle, t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (b - a) / 2g,
         // written without the intermediate division: t = 2 g sign(b - a) / (|b - a| + sqrt((b - a)^2 + 4 g^2))
         const double d = b - a;
-        const double tt = (d >= 0.0 ? 2.0 * g : -2.0 * g) / (fabs(d) + sqrt(fma(d, d, 4.0 * g2)));
-        const double cs = rsqrt(fma(tt, tt, 1.0)), sn = cs * tt;
+        // (MUFU-seeded reciprocal / rsqrt with Newton steps: the IEEE division and square root are
+        // several times the instructions, and the round is issue-bound)
+        const double h = fma(d, d, 4.0 * g2);
+        const double tt = (d >= 0.0 ? 2.0 * g : -2.0 * g) * fast_rcp(fabs(d) + h * fast_rsqrt(h));
+        const double cs = fast_rsqrt(fma(tt, tt, 1.0)), sn = cs * tt;
 #pragma unroll
         for (int e = 0; e < EPL; ++e) {
           const int t = hl + 16 * e;
@@ -208,7 +213,11 @@ az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs,
                          cudaStream_t st) {
   if (!small_fits(r, nrhs))
     return az_tsvdw_impl(Rf, ldr, r, nrhs, theta, y, ldy, sigma_out, rank_out, ws, ws_bytes, st, 40, nullptr);
-  const size_t sm = (size_t)(r * r + r * nrhs + r) * sizeof(double);
+  size_t sm = (size_t)(r * r + r * nrhs + r) * sizeof(double);
+  // the CTA takes an SM to itself (shared memory no other kernel's CTA fits beside): the round is
+  // issue-bound, and in az_solve the side stream's column passes run meanwhile
+  static const int excl = getenv("AZ_JAC_EXCL") ? atoi(getenv("AZ_JAC_EXCL")) : 1;
+  if (excl) sm = std::max<size_t>(sm, 160 * 1024);
   if (ws_bytes < az_tsvd_ws_bytes(r, nrhs)) {
     az_set_error("az_tsvd_solve: workspace too small");
     return AZ_ERR_WORKSPACE;
