@@ -179,6 +179,25 @@ static bool no_hi() {
   return k == 0;
 }
 
+// k_gemm_mn_small walks its 64-row tiles grid-stride: one wave of exactly the resident CTAs (126
+// registers per thread allow two per SM, not the three its shared memory would), or the CTAs past
+// the first wave run alone at the end
+static unsigned gemm_small_grid(int64_t m) {
+  static int per_sm = 0, sms = 0;
+  if (!per_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm_mn_small, 256, 2 * 64 * 68 * sizeof(double)) !=
+            cudaSuccess ||
+        per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+  }
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(az_div_up(m, 64), (int64_t)per_sm * sms));
+}
+
 static SolveWS layout(az_plan_s* p, int64_t nrhs, int64_t R, int32_t max_blocks, char* base) {
   SolveWS w;
   const int64_t rows = p->M + p->Mb;
@@ -424,7 +443,7 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
       const size_t gs = 2 * 64 * 68 * sizeof(double);
       AZ_CUDA_CHECK(az_smem_attr(k_gemm_mn_small, gs));
       for (int64_t c0 = 0; c0 < nrhs; c0 += 64)
-        k_gemm_mn_small<<<(unsigned)std::min<int64_t>(az_div_up(p->N, 64), 3 * 148), 256, gs, st>>>(
+        k_gemm_mn_small<<<gemm_small_grid(p->N), 256, gs, st>>>(
             w.Om, p->N, w.y + c0 * kp, kp, x + c0 * ldx, ldx, p->N, (int)kp, (int)std::min<int64_t>(64, nrhs - c0),
             w.Zb + c0 * p->N, p->N, 1.0);
     } else {
@@ -1229,7 +1248,7 @@ extern "C" az_status_t az_solve_factored(az_factor_t f, const double* b, int64_t
     const size_t gs = 2 * 64 * 68 * sizeof(double);
     AZ_CUDA_CHECK(az_smem_attr(k_gemm_mn_small, gs));
     for (int64_t c0 = 0; c0 < nrhs; c0 += 64)
-      k_gemm_mn_small<<<(unsigned)std::min<int64_t>(az_div_up(p->N, 64), 3 * 148), 256, gs, st>>>(
+      k_gemm_mn_small<<<gemm_small_grid(p->N), 256, gs, st>>>(
           f->Mm, p->N, w.y + c0 * kp, kp, x + c0 * ldx, ldx, p->N, (int)kp, (int)std::min<int64_t>(64, nrhs - c0),
           w.x2 + c0 * p->N, p->N, 1.0);
     AZ_LAUNCH_CHECK();
