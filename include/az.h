@@ -22,6 +22,11 @@
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *     All calls are asynchronous on `stream` unless stated; the library never
  *     synchronises the device except where a host result is returned.
+ *   - A plan owns scratch that its calls share: calls on one plan must be ordered by the
+ *     caller (one stream, or explicit stream dependencies); different plans are independent.
+ *     az_solve may run parts of a solve on internal streams of the plan (a side stream and a
+ *     high-priority stream); their work is joined back into `stream` by events before the
+ *     solve's last kernel, so stream order on `stream` still holds.
  *   - Errors are status codes; no C++ exception crosses the ABI.  Arguments are
  *     validated before any launch and outputs are untouched on argument errors.
  *     az_last_error() returns a thread-local detail string for the last failure.
