@@ -117,6 +117,13 @@ az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R
                          void* ws, size_t ws_bytes, cudaStream_t st, int64_t k1 = 0, bool a_scratch = false,
                          cudaEvent_t after_leaf = nullptr);
 size_t az_qr_ws_bytes(int64_t m, int64_t k);
+// R_S of the k1 probe columns on st (ev_leaf / ev_merged recorded there), then (Q^T b')[:k1] of the
+// k - k1 right-hand-side columns on rhs_st (k1, k - k1 <= 64; A is scratch) (az_qr.cu)
+az_status_t az_qr_r_deferred(double* A, int64_t m, int64_t k, int64_t k1, int64_t lda, double* Rs, int64_t ldrs,
+                             void* ws, size_t ws_bytes, cudaStream_t st, cudaEvent_t ev_leaf, cudaEvent_t ev_merged);
+az_status_t az_qr_rhs_deferred(double* A, int64_t m, int64_t k, int64_t k1, int64_t lda, double* C, int64_t ldc,
+                               void* ws, size_t ws_bytes, cudaStream_t rhs_st, cudaEvent_t ev_leaf,
+                               cudaEvent_t ev_merged);
 az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta,
                          double* y, int64_t ldy, double* sigma_out, int64_t* rank_out,
                          void* ws, size_t ws_bytes, cudaStream_t st);

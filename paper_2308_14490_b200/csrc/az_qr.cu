@@ -40,13 +40,14 @@ struct QRIn {
   double* Rout;     // per CTA k1 x k column-major (ld = k1), CTA stride ostride
   int64_t ostride;
   // optional (split leaf): the chunk parts y_j of the reflectors and their tau, per chunk
-  double* Y;        // y_j of chunk rows written to Y[row + j ldY] (the triangularised columns' storage)
+  double* Y;        // y_j of chunk rows written to Y[row + j ldY] (the triangularised columns' storage);
+                    // merges: Y[(row / rb) bstride + row % rb + j ldY], the input's block layout
   int64_t ldY;
   double* taus;     // taus[(cta cmax + chunk) k1 + j]
   int cmax;         // chunks per CTA (ceil(rows_per_cta / MC))
 };
 
-template <int KC, int RPL>
+template <int KC, int RPL, bool YSTACK = false>
 __global__ void __launch_bounds__(512, 1) k_tsqr(QRIn q) {
   constexpr int MC = 32 * RPL;
   extern __shared__ double sm[];
@@ -125,11 +126,19 @@ __global__ void __launch_bounds__(512, 1) k_tsqr(QRIn q) {
         }
 #pragma unroll
         for (int r = 0; r < RPL; ++r) vj[lane + 32 * r] = xs[r] * scale;
-        if (q.Y) {   // split leaf: keep the reflector for the right-hand-side pass (k_tsqr_rhs)
+        if (q.Y) {   // split leaf / merge: keep the reflector for the right-hand-side pass (k_tsqr_rhs)
+          if constexpr (YSTACK) {   // merges: Y in the stacked block layout of the input
 #pragma unroll
-          for (int r = 0; r < RPL; ++r) {
-            const int64_t row = base + lane + 32 * r;
-            if (row < r1) q.Y[row + (int64_t)j * q.ldY] = xs[r] * scale;
+            for (int r = 0; r < RPL; ++r) {
+              const int64_t row = base + lane + 32 * r;
+              if (row < r1) q.Y[(row / q.rb) * q.bstride + (row % q.rb) + (int64_t)j * q.ldY] = xs[r] * scale;
+            }
+          } else {
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) {
+              const int64_t row = base + lane + 32 * r;
+              if (row < r1) q.Y[row + (int64_t)j * q.ldY] = xs[r] * scale;
+            }
           }
           if (lane == 0) q.taus[((int64_t)blockIdx.x * q.cmax + (base - r0) / MC) * q.k1 + j] = tau;
         }
@@ -585,7 +594,9 @@ template <int KC, int RPL>
 static az_status_t tsqr_launch(const QRIn& q, int nblocks, cudaStream_t st) {
   constexpr int MC = 32 * RPL;
   const size_t sm = ((size_t)q.k * (q.k + 1) / 2 + 2 * MC + 2) * sizeof(double);
-  auto kern = k_tsqr<KC, RPL>;
+  // (a separate instantiation for the merges' stacked reflector store keeps the leaf's owner
+  // chain free of it)
+  auto kern = (q.Y && q.bstride) ? k_tsqr<KC, RPL, true> : k_tsqr<KC, RPL, false>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   AzTrace tr(q.bstride ? "tsqr_merge" : "tsqr_leaf", st, q.m);
   kern<<<nblocks, 512, sm, st>>>(q);
@@ -633,7 +644,13 @@ size_t az_qr_ws_bytes(int64_t m, int64_t k) {
   }
   const int64_t P = std::max<int64_t>(1, std::min<int64_t>(num_sms(), (m + 127) / 128));
   // leaf / merge factors (two buffers) + the split leaf's reflector taus (per 256-row chunk)
-  return (size_t)(2 * P * k * k + ((m + 255) / 256 + 2 * P) * k) * sizeof(double) + 256;
+  // + the deferred-rhs merge reflectors of every tree level (az_qr_r_deferred)
+  int64_t ylev = 0, tlev = 0;
+  for (int64_t cur = P; cur > 1; cur = (cur + 3) / 4) {
+    ylev += cur * k * k;
+    tlev += (cur + 3) / 4 * k;
+  }
+  return (size_t)(2 * P * k * k + ((m + 255) / 256 + 2 * P) * k + ylev + tlev) * sizeof(double) + 256;
 }
 
 static az_status_t qr_r_wide(double* A, int64_t m, int64_t k, int64_t lda, double* R, int64_t ldr, void* ws,
@@ -763,6 +780,166 @@ az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R
     cur = next;
   }
   k_copy_R<<<az_div_up(k1 * k, 256), 256, 0, st>>>(buf[which], (int)k1, (int)k, R, ldr);
+  AZ_LAUNCH_CHECK();
+  return AZ_OK;
+}
+
+// The split leaf with Q^T b' taken off the R factor's critical path (single probe block, k1 <= 64
+// probe columns, nb = k - k1 <= 64 right-hand sides; A is scratch), in two enqueue calls:
+//   az_qr_r_deferred (st):  pass A (probe columns, reflectors kept in place) -> ev_leaf -> merge
+//           tree of the probe columns alone, each level's reflectors kept (in the input's block
+//           layout) -> R_S into Rs (k1 x k1, ld ldrs) -> ev_merged
+//   az_qr_rhs_deferred (rhs_st, after ev_leaf): pass B, b' through the leaf chunks' reflectors ->
+//           (after ev_merged) the same compact-WY pass over each merge level's stacked blocks ->
+//           C = (Q^T b')[:k1] (k1 x nb, ld ldc)
+// Same R_S and Q^T b' as az_qr_r_impl up to rounding (the same reflectors, applied in the same
+// order per column).  The caller may enqueue other work on rhs_st between the two calls.
+namespace {
+constexpr int DEF_MC = 256;
+struct DefLev {
+  double* Y;
+  double* taus;
+  int64_t cur, next;
+  int which;
+};
+struct DefLayout {
+  int64_t P, rows_per_cta;
+  int cmax;
+  double* buf[2];
+  double* taus0;
+  std::vector<DefLev> lev;
+  int final_which;
+};
+DefLayout def_layout(int64_t m, int64_t k, void* ws) {
+  DefLayout d;
+  // one leaf block fewer than SMs: pass B (one 170 KB CTA per SM and leaf block) then runs in a
+  // single wave beside the one-CTA Jacobi, which holds an SM of its own
+  d.P = std::max<int64_t>(1, std::min<int64_t>(num_sms() - 1, (m + 127) / 128));
+  d.rows_per_cta = (m + d.P - 1) / d.P;
+  d.cmax = (int)((d.rows_per_cta + DEF_MC - 1) / DEF_MC);
+  d.buf[0] = (double*)ws;
+  d.buf[1] = (double*)ws + d.P * k * k;
+  d.taus0 = (double*)ws + 2 * d.P * k * k;
+  double* yp = d.taus0 + ((m + 255) / 256 + 2 * d.P) * k;
+  int which = 0;
+  for (int64_t cur = d.P; cur > 1;) {
+    const int64_t next = (cur + 3) / 4;
+    d.lev.push_back(DefLev{yp, yp + cur * k * k, cur, next, which});
+    yp += cur * k * k + next * k;
+    which ^= 1;
+    cur = next;
+  }
+  d.final_which = which;
+  return d;
+}
+bool def_ok(int64_t k, int64_t k1) { return k1 >= 1 && k1 <= 64 && k - k1 >= 1 && k - k1 <= 64; }
+size_t def_rhs_smem() { return (size_t)(2 * 64 * RR_S2 + 3 * 64 * 65 + 64) * sizeof(double); }
+}  // namespace
+
+az_status_t az_qr_r_deferred(double* A, int64_t m, int64_t k, int64_t k1, int64_t lda, double* Rs, int64_t ldrs,
+                             void* ws, size_t ws_bytes, cudaStream_t st, cudaEvent_t ev_leaf, cudaEvent_t ev_merged) {
+  if (!def_ok(k, k1) || ws_bytes < az_qr_ws_bytes(m, k)) {
+    az_set_error("az_qr_r_deferred: needs 1 <= k1 <= 64, 1 <= k - k1 <= 64 and the az_qr workspace");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  const DefLayout d = def_layout(m, k, ws);
+  QRIn q;
+  q.A = A;
+  q.m = m;
+  q.k = (int)k1;
+  q.k1 = (int)k1;
+  q.ld = lda;
+  q.rb = m;
+  q.bstride = 0;
+  q.rows_per_cta = d.rows_per_cta;
+  q.Rout = d.buf[0];
+  q.ostride = k1 * k;
+  q.Y = A;
+  q.ldY = lda;
+  q.cmax = d.cmax;
+  q.taus = d.taus0;
+  AZ_TRY((tsqr_launch<4, 8>(q, (int)d.P, st)));
+  AZ_CUDA_CHECK(cudaEventRecord(ev_leaf, st));
+  for (const DefLev& L : d.lev) {   // merge tree of the probe columns, reflectors kept per level
+    QRIn t;
+    t.A = d.buf[L.which];
+    t.m = L.cur * k1;
+    t.k = (int)k1;
+    t.k1 = (int)k1;
+    t.ld = k1;
+    t.rb = k1;
+    t.bstride = k1 * k;
+    t.rows_per_cta = 4 * k1;
+    t.Rout = d.buf[L.which ^ 1];
+    t.ostride = k1 * k;
+    t.Y = L.Y;
+    t.ldY = k1;
+    t.taus = L.taus;
+    t.cmax = 1;
+    AZ_TRY((tsqr_launch<4, 8>(t, (int)L.next, st)));
+  }
+  k_copy_R<<<az_div_up(k1 * k1, 256), 256, 0, st>>>(d.buf[d.final_which], (int)k1, (int)k1, Rs, ldrs);
+  AZ_LAUNCH_CHECK();
+  AZ_CUDA_CHECK(cudaEventRecord(ev_merged, st));
+  return AZ_OK;
+}
+
+az_status_t az_qr_rhs_deferred(double* A, int64_t m, int64_t k, int64_t k1, int64_t lda, double* C, int64_t ldc,
+                               void* ws, size_t ws_bytes, cudaStream_t rhs_st, cudaEvent_t ev_leaf,
+                               cudaEvent_t ev_merged) {
+  if (!def_ok(k, k1) || ws_bytes < az_qr_ws_bytes(m, k)) {
+    az_set_error("az_qr_rhs_deferred: needs 1 <= k1 <= 64, 1 <= k - k1 <= 64 and the az_qr workspace");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  const int64_t nb = k - k1;
+  const DefLayout d = def_layout(m, k, ws);
+  const size_t rsm = def_rhs_smem();
+  AZ_CUDA_CHECK(az_smem_attr(k_tsqr_rhs, rsm));
+  AZ_CUDA_CHECK(cudaStreamWaitEvent(rhs_st, ev_leaf, 0));
+  QRr r;   // pass B: the leaf blocks' Q^T b' rows into columns k1.. of buf[0]
+  r.rb = 0;
+  r.bstride = 0;
+  r.Y = A;
+  r.ldY = lda;
+  r.X = A + k1 * lda;
+  r.ldX = lda;
+  r.m = m;
+  r.rows_per_cta = d.rows_per_cta;
+  r.k1 = (int)k1;
+  r.nb = (int)nb;
+  r.MC = DEF_MC;
+  r.cmax = d.cmax;
+  r.taus = d.taus0;
+  r.Rout = d.buf[0];
+  r.ostride = k1 * k;
+  {
+    AzTrace tr("tsqr_rhs", rhs_st, m);
+    k_tsqr_rhs<<<(unsigned)d.P, 512, rsm, rhs_st>>>(r);
+    AZ_LAUNCH_CHECK();
+  }
+  AZ_CUDA_CHECK(cudaStreamWaitEvent(rhs_st, ev_merged, 0));
+  for (const DefLev& L : d.lev) {   // the stacked blocks' right-hand-side columns, level by level
+    QRr c;
+    c.rb = k1;
+    c.bstride = k1 * k;
+    c.Y = L.Y;
+    c.ldY = k1;
+    c.X = d.buf[L.which] + k1 * k1;
+    c.ldX = k1;
+    c.m = L.cur * k1;
+    c.rows_per_cta = 4 * k1;
+    c.k1 = (int)k1;
+    c.nb = (int)nb;
+    c.MC = DEF_MC;
+    c.cmax = 1;
+    c.taus = L.taus;
+    c.Rout = d.buf[L.which ^ 1];
+    c.ostride = k1 * k;
+    AzTrace tr("tsqr_rhs_merge", rhs_st, c.m);
+    k_tsqr_rhs<<<(unsigned)L.next, 512, rsm, rhs_st>>>(c);
+    AZ_LAUNCH_CHECK();
+  }
+  k_copy_R<<<az_div_up(k1 * nb, 256), 256, 0, rhs_st>>>(d.buf[d.final_which] + k1 * k1, (int)k1, (int)nb, C, ldc);
   AZ_LAUNCH_CHECK();
   return AZ_OK;
 }

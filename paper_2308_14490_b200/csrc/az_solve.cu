@@ -140,6 +140,9 @@ struct SolveWS {
   double* Zb;    // N x nrhs: Z* b from the b' chain (four-step narrow path), else null
   cplx* Zs;      // the b' chain's Z* b spectra (N x ceil(nrhs / 2) complex), same condition
   double* Om;    // N x Rmax: M = Omega - Z* A Omega from the sketch (same condition)
+  double* Rp;    // Rmax x 2 Rmax: [R_S | I] for P = pinv_theta(R_S) (deferred Q^T b', same condition)
+  double* Pm;    // Rmax x Rmax: P
+  double* cq;    // Rmax x nrhs: Q^T b' from the right-hand-side stream
   void* qrws;
   size_t qrbytes;
   void* svdws;
@@ -157,6 +160,7 @@ __global__ void k_gemm_mn(const double* A, int64_t lda, const double* Bm, int64_
                           int64_t k, int64_t n, const double* C = nullptr, int64_t ldc = 0, double sgn = -1.0);
 __global__ void k_gemm_mn_small(const double* A, int64_t lda, const double* Bm, int64_t ldb, double* Y, int64_t ldy,
                                 int64_t m, int k, int n, const double* C, int64_t ldc, double sgn = -1.0);
+__global__ void k_identity_cols(double* Rf, int64_t ld, int64_t k, int64_t col0);
 
 // four-step narrow solves: step 2 as x = Z* b + M y from the b' and sketch chains (reading R30;
 // AZ_STEP2_LINEAR=0 disables)
@@ -164,6 +168,17 @@ static bool step2_linear() {
   static int k = -1;
   if (k < 0) {
     const char* e = getenv("AZ_STEP2_LINEAR");
+    k = e ? atoi(e) : 1;
+  }
+  return k != 0;
+}
+
+// AZ_QR_DEFER=0: Q^T b' rides along in the TSQR merges (on the R factor's critical path) instead of
+// following on the side stream while the SVD computes P = pinv_theta(R_S)
+static bool qr_defer() {
+  static int k = -1;
+  if (k < 0) {
+    const char* e = getenv("AZ_QR_DEFER");
     k = e ? atoi(e) : 1;
   }
   return k != 0;
@@ -221,6 +236,9 @@ static SolveWS layout(az_plan_s* p, int64_t nrhs, int64_t R, int32_t max_blocks,
   w.Zb = keep ? (double*)take(sizeof(double) * p->N * nrhs) : nullptr;
   w.Zs = keep ? (cplx*)take(sizeof(cplx) * p->N * ((nrhs + 1) / 2)) : nullptr;
   w.Om = keep ? (double*)take(sizeof(double) * p->N * Rmax) : nullptr;
+  w.Rp = keep ? (double*)take(sizeof(double) * Rmax * 2 * Rmax) : nullptr;
+  w.Pm = keep ? (double*)take(sizeof(double) * Rmax * Rmax) : nullptr;
+  w.cq = keep ? (double*)take(sizeof(double) * Rmax * nrhs) : nullptr;
   if (w.wide) {
     const int64_t QBw = az_qrw_panel_width();
     w.maxpanels = max_blocks * ((R + QBw - 1) / QBw);
@@ -325,6 +343,9 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   }
   // the QR and the SVD: on the high-priority stream beside the side stream (joined back below)
   cudaStream_t qs = side && !no_hi() ? p->hi : st;
+  // Q^T b' off the R factor's critical path: R_S alone through the merge tree, P = pinv_theta(R_S) by
+  // the SVD of [R_S | I], while b' follows the kept reflectors on the side stream; y = P (Q^T b')
+  const bool defer = side && qr_defer() && R <= 64 && nrhs <= 64 && w.Rp;
   if (w.Zb) {   // b' and, for step 2, Z* b (one extra column pass)
     AZ_TRY(az1f_resid_z(p, b, ldb, bp_in_S ? w.S + R * rows : w.bp, rows, w.Zb, p->N, nrhs, st, w.Zs, side));
   } else {
@@ -363,12 +384,22 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
     if (dbg_host) fprintf(stderr, "az_solve host: sketch issued +%.2f ms\n", hnow() - th0);
     if (!w.wide) {
       // a single probe block: the sketch columns are not needed after this QR (split leaf allowed)
-      AZ_TRY(az_qr_r_impl(w.S, rows, kt, rows, w.Rf, kt, w.qrws, w.qrbytes, qs, kp, max_blocks == 1,
-                          side ? p->side_ev[0] : nullptr));
-      if (side) {   // the deferred Z* b and M passes beside the merges and the SVD
+      if (defer) {
+        AZ_TRY(az_qr_r_deferred(w.S, rows, kt, kp, rows, w.Rp, kp, w.qrws, w.qrbytes, qs, p->side_ev[0],
+                                p->side_ev[1]));
+      } else {
+        AZ_TRY(az_qr_r_impl(w.S, rows, kt, rows, w.Rf, kt, w.qrws, w.qrbytes, qs, kp, max_blocks == 1,
+                            side ? p->side_ev[0] : nullptr));
+      }
+      if (side) {
+        // side stream: the deferred Z* b and M passes beside the merges (whose CTAs take freed SMs
+        // first), then -- deferred -- Q^T b' through the kept reflectors beside the SVD
         AZ_CUDA_CHECK(cudaStreamWaitEvent(p->side, p->side_ev[0], 0));
         AZ_TRY(az1f_out_z(p, w.Zs, w.Zb, p->N, nrhs, p->side));
         AZ_TRY(az1f_out_z(p, p->d_Z2, w.Om, p->N, R, p->side));
+        if (defer)
+          AZ_TRY(az_qr_rhs_deferred(w.S, rows, kt, kp, rows, w.cq, kp, w.qrws, w.qrbytes, p->side, p->side_ev[0],
+                                    p->side_ev[1]));
         AZ_CUDA_CHECK(cudaEventRecord(p->side_ev[2], p->side));
       }
     } else {
@@ -408,7 +439,13 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
       full_svd = k22 <= R - pfix;
       rank = kp;   // not computed: treated as saturated unless the full SVD runs
     }
-    if (full_svd) {
+    if (full_svd && defer) {
+      // [R_S | I]: the truncated SVD solve of the identity is P = V_k Sigma_k^-1 U_k^T
+      k_identity_cols<<<az_div_up(kp * kp, 256), 256, 0, qs>>>(w.Rp, kp, kp, kp);
+      AZ_LAUNCH_CHECK();
+      AZ_TRY(az_tsvd_impl(w.Rp, kp, kp, kp, theta, w.Pm, kp, w.sig, async_mode ? nullptr : &rank, w.svdws,
+                          w.svdbytes, qs));
+    } else if (full_svd) {
       AZ_TRY(az_tsvd_impl(w.Rf, kt, kp, nrhs, theta, w.y, kp, w.sig, async_mode ? nullptr : &rank, w.svdws,
                           w.svdbytes, qs));
       if (w.wide && nb < max_blocks) {   // sigma_1 lower bound for the next block's pre-test
@@ -438,6 +475,12 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
     // by linearity of Z* (PAPER.md:229-230): x = Omega y + Z* b - (Z* A Omega) y = Z* b + M y, with
     // Z* b and M = Omega - Z* A Omega produced by the b' and sketch chains: one DMMA pass, no FFT
     if (side) AZ_CUDA_CHECK(cudaStreamWaitEvent(st, p->side_ev[2], 0));   // Z* b and M are ready
+    if (defer) {   // y = P (Q^T b')
+      AzTrace tr("y_pc", st);
+      k_gemm_mn<<<dim3(az_div_up(kp, 64), az_div_up(nrhs, 64)), 256, 0, st>>>(w.Pm, kp, w.cq, kp, w.y, kp, kp, kp,
+                                                                             nrhs);
+      AZ_LAUNCH_CHECK();
+    }
     AzTrace tr("step2_gemm", st, 2 * p->N * kp * nrhs);
     if (kp <= 64) {
       const size_t gs = 2 * 64 * 68 * sizeof(double);
