@@ -249,6 +249,9 @@ __global__ void __launch_bounds__(512, 1) k_tsqr_rhs(QRr q) {
   // warps 0-7: G tiles rows (w & 1) 32.., cols (w >> 1) 16..;  warps 8-15: the same tiles of P
   const int ww = w & 7, wm = ww & 1, wn = ww >> 1;
   const bool isG = w < 8;
+  // tiles that hold no needed entry skip their MMAs (the DP tensor pipe is the shared limit): G is
+  // only read below its diagonal (m < j), and only rows < k1 and columns < k1 (G) / nb (P) exist
+  const bool mma_on = 32 * wm < k1 && (isG ? (16 * wn < k1 && 16 * wn < 32 * wm + 31) : 16 * wn < nb);
   double ry[8], rx[8];   // the next 64-row sub-block, in flight during the current MMAs
   auto load = [&](int64_t rr, int64_t cend) {
 #pragma unroll
@@ -278,7 +281,7 @@ __global__ void __launch_bounds__(512, 1) k_tsqr_rhs(QRr q) {
       }
       __syncthreads();
       if (rr + 64 < cend) load(rr + 64, cend);
-      warp_mma<4, 2, IMAJ, IMAJ>(acc, Ys, RR_S2, isG ? Ys : Xs, RR_S2, wm * 32, wn * 16, 0, 64, lane);
+      if (mma_on) warp_mma<4, 2, IMAJ, IMAJ>(acc, Ys, RR_S2, isG ? Ys : Xs, RR_S2, wm * 32, wn * 16, 0, 64, lane);
     }
     double* D = isG ? G : P;
 #pragma unroll
