@@ -8,6 +8,10 @@
 //   x   = x2 + Z* (b - A x2)                              (step 2 + step 3)
 // Probe blocks are added while the sketch is saturated, rank > probes - p (p = 10),
 // up to max_blocks (reading R5).
+// Four-step narrow solves with one probe block (c2) reorganise the same algebra:
+//   x = Z* b + M y, M = Omega - Z* A Omega (reading R30), both from the b' / sketch chains;
+//   y = P (Q^T b'), P = pinv_theta(R_S) from the SVD of [R_S | I], with Q^T b' carried through the
+//   kept TSQR reflectors on a side stream while the merge tree and the SVD run at high priority.
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -474,7 +478,7 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   if (w.Om) {
     // by linearity of Z* (PAPER.md:229-230): x = Omega y + Z* b - (Z* A Omega) y = Z* b + M y, with
     // Z* b and M = Omega - Z* A Omega produced by the b' and sketch chains: one DMMA pass, no FFT
-    if (side) AZ_CUDA_CHECK(cudaStreamWaitEvent(st, p->side_ev[2], 0));   // Z* b and M are ready
+    if (side) AZ_CUDA_CHECK(cudaStreamWaitEvent(st, p->side_ev[2], 0));   // Z* b, M (and Q^T b') are ready
     if (defer) {   // y = P (Q^T b')
       AzTrace tr("y_pc", st);
       k_gemm_mn<<<dim3(az_div_up(kp, 64), az_div_up(nrhs, 64)), 256, 0, st>>>(w.Pm, kp, w.cq, kp, w.y, kp, kp, kp,
