@@ -125,9 +125,11 @@ az_status_t az_qr_r_deferred(double* A, int64_t m, int64_t k, int64_t k1, int64_
 az_status_t az_qr_rhs_deferred(double* A, int64_t m, int64_t k, int64_t k1, int64_t lda, double* C, int64_t ldc,
                                void* ws, size_t ws_bytes, cudaStream_t rhs_st, cudaEvent_t ev_leaf,
                                cudaEvent_t ev_merged);
+// rank_out: HOST, filled synchronously (may be null); rank_dev (optional): receives the DEVICE
+// address where the rank lands on `st` (valid while ws is)
 az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta,
                          double* y, int64_t ldy, double* sigma_out, int64_t* rank_out,
-                         void* ws, size_t ws_bytes, cudaStream_t st);
+                         void* ws, size_t ws_bytes, cudaStream_t st, const int64_t** rank_dev = nullptr);
 size_t az_tsvd_ws_bytes(int64_t r, int64_t nrhs);
 
 // --- wide (2-D) dense path: blocked Householder QR (az_qrw.cu), block Jacobi SVD (az_svdw.cu)
@@ -159,7 +161,7 @@ void az_vbuf_free(az_vbuf_s* v);
 size_t az_tsvdw_ws_bytes(int64_t r, int64_t nrhs);
 az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta, double* y,
                           int64_t ldy, double* sigma_out, int64_t* rank_out, void* ws, size_t ws_bytes,
-                          cudaStream_t st, int max_sweeps, int* sweeps_out);
+                          cudaStream_t st, int max_sweeps, int* sweeps_out, const int64_t** rank_dev = nullptr);
 
 
 // Optional per-launch CUDA-event tracing (az_trace_enable): records an event pair around each

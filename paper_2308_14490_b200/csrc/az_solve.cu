@@ -328,6 +328,10 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   // no report and a single probe block: nothing needs to come back to the host, so the whole solve
   // is enqueued without a host synchronisation (az_solve_host_pipelined relies on this)
   const bool async_mode = report == nullptr && max_blocks == 1;
+  // the rank is needed on the host mid-solve only to decide on another probe block; with one block
+  // it is read after the last kernel, so step 2 is enqueued without waiting for the SVD
+  const bool host_rank = max_blocks > 1;
+  const int64_t* rank_dev = nullptr;
   static const bool dbg_host = getenv("AZ_DEBUG_HOST") != nullptr;
   auto hnow = []() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   const double th0 = dbg_host ? hnow() : 0.0;
@@ -447,11 +451,11 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
       // [R_S | I]: the truncated SVD solve of the identity is P = V_k Sigma_k^-1 U_k^T
       k_identity_cols<<<az_div_up(kp * kp, 256), 256, 0, qs>>>(w.Rp, kp, kp, kp);
       AZ_LAUNCH_CHECK();
-      AZ_TRY(az_tsvd_impl(w.Rp, kp, kp, kp, theta, w.Pm, kp, w.sig, async_mode ? nullptr : &rank, w.svdws,
-                          w.svdbytes, qs));
+      AZ_TRY(az_tsvd_impl(w.Rp, kp, kp, kp, theta, w.Pm, kp, w.sig, host_rank ? &rank : nullptr, w.svdws,
+                          w.svdbytes, qs, &rank_dev));
     } else if (full_svd) {
-      AZ_TRY(az_tsvd_impl(w.Rf, kt, kp, nrhs, theta, w.y, kp, w.sig, async_mode ? nullptr : &rank, w.svdws,
-                          w.svdbytes, qs));
+      AZ_TRY(az_tsvd_impl(w.Rf, kt, kp, nrhs, theta, w.y, kp, w.sig, host_rank ? &rank : nullptr, w.svdws,
+                          w.svdbytes, qs, &rank_dev));
       if (w.wide && nb < max_blocks) {   // sigma_1 lower bound for the next block's pre-test
         double s1 = 0.0;
         AZ_CUDA_CHECK(cudaMemcpyAsync(&s1, w.sig, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -461,13 +465,13 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
     }
     cudaEventRecord(e3, qs);
     if (qs != st) AZ_CUDA_CHECK(cudaStreamWaitEvent(st, e3, 0));
-    if (!async_mode) {
+    if (host_rank) {
       cudaEventSynchronize(e3);
       ms_sketch += ms_between(e0, e1);
       ms_qr += ms_between(e1, e2);
       ms_svd += ms_between(e2, e3);
     }
-    saturated = !async_mode && rank > kp - pfix;
+    saturated = host_rank && rank > kp - pfix;
     if (!saturated || nb == max_blocks) break;
   }
   if (nb > max_blocks) nb = max_blocks;
@@ -506,6 +510,13 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   if (dbg_host) fprintf(stderr, "az_solve host: all issued +%.2f ms\n", hnow() - th0);
   if (async_mode) return AZ_OK;
   AZ_CUDA_CHECK(cudaEventSynchronize(ev.e[7]));
+  if (!host_rank) {
+    if (rank_dev) AZ_CUDA_CHECK(cudaMemcpy(&rank, rank_dev, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    ms_sketch = ms_between(ev.e[2], ev.e[3]);
+    ms_qr = ms_between(ev.e[3], ev.e[4]);
+    ms_svd = ms_between(ev.e[4], ev.e[5]);
+    saturated = rank > kp - pfix;
+  }
   if (report) {
     double sg[1] = {0};
     report->rank_used = rank;

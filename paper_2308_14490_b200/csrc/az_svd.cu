@@ -210,9 +210,10 @@ size_t az_tsvd_ws_bytes(int64_t r, int64_t nrhs) {
 
 az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta, double* y,
                          int64_t ldy, double* sigma_out, int64_t* rank_out, void* ws, size_t ws_bytes,
-                         cudaStream_t st) {
+                         cudaStream_t st, const int64_t** rank_dev) {
   if (!small_fits(r, nrhs))
-    return az_tsvdw_impl(Rf, ldr, r, nrhs, theta, y, ldy, sigma_out, rank_out, ws, ws_bytes, st, 40, nullptr);
+    return az_tsvdw_impl(Rf, ldr, r, nrhs, theta, y, ldy, sigma_out, rank_out, ws, ws_bytes, st, 40, nullptr,
+                         rank_dev);
   size_t sm = (size_t)(r * r + r * nrhs + r) * sizeof(double);
   // the CTA takes an SM to itself (shared memory no other kernel's CTA fits beside): the round is
   // issue-bound, and in az_solve the side stream's column passes run meanwhile
@@ -223,6 +224,7 @@ az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs,
     return AZ_ERR_WORKSPACE;
   }
   int64_t* d_rank = (int64_t*)ws;
+  if (rank_dev) *rank_dev = d_rank;
   // one half warp per pair: n / 2 pairs -> 16 (n / 2) threads, whole warps, at most 1024
   const int nth = (int)std::min<int64_t>(1024, std::max<int64_t>(64, 32 * ((r + 3) / 4)));
   AzTrace tr("jacobi_svd", st);

@@ -477,7 +477,7 @@ __global__ void k_copy_block(const double* src, int64_t lds, double* dst, int64_
 
 az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta, double* y,
                           int64_t ldy, double* sigma_out, int64_t* rank_out, void* ws, size_t ws_bytes,
-                          cudaStream_t st, int max_sweeps, int* sweeps_out) {
+                          cudaStream_t st, int max_sweeps, int* sweeps_out, const int64_t** rank_dev) {
   if (ws_bytes < az_tsvdw_ws_bytes(r, nrhs)) {
     az_set_error("az_tsvd_solve (block Jacobi): workspace too small");
     return AZ_ERR_WORKSPACE;
@@ -492,6 +492,7 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
   double* smax2 = (double*)p;
   unsigned long long* off = (unsigned long long*)(p + 64);
   int64_t* d_rank = (int64_t*)(p + 128);
+  if (rank_dev) *rank_dev = d_rank;
   // ---- optional QR preconditioning ----
   const bool pre = bjac_precond();
   double *M2 = nullptr, *M3 = nullptr, *T2 = nullptr, *T3 = nullptr, *Z = nullptr;
