@@ -10,6 +10,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 timeout 300 python tools/prof_c2.py solve > gpurun_out/plain2.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:'k_tsqr|k1f_rows|k1f_cols|k_jacobi_small|k_omega_apply' -c 12 -o gpurun_out/prof_c2 \
+  -k regex:'k_tsqr|k1f_rows|k1f_cols|k_jacobi_small|k_gemm_mn_small' -c 24 -o gpurun_out/prof_c2 \
   python tools/prof_c2.py solve > gpurun_out/ncu_full.log 2>&1
 ls -la gpurun_out
