@@ -13,3 +13,9 @@ timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:'k_tsqr|k1f_rows|k1f_cols|k_jacobi_small|k_gemm_mn_small' -c 24 -o gpurun_out/prof_c2 \
   python tools/prof_c2.py solve > gpurun_out/ncu_full.log 2>&1
 ls -la gpurun_out
+# summaries on the box; the full report only travels back when small (gpurun_out/ is capped at 64 MiB)
+python tools/summarize_ncu.py launches gpurun_out/launches.csv > gpurun_out/launches_summary.txt 2>&1
+python tools/summarize_ncu.py full gpurun_out/prof_c2.ncu-rep > gpurun_out/ncu_full_summary.txt 2>&1
+[ "$(stat -c %s gpurun_out/prof_c2.ncu-rep 2>/dev/null || echo 0)" -gt 40000000 ] && rm -f gpurun_out/prof_c2.ncu-rep
+rm -f gpurun_out/launches.csv.big
+ls -la gpurun_out
