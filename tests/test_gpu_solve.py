@@ -225,15 +225,17 @@ _ALT_SCRIPT = """
 import sys, numpy as np, torch
 sys.path.insert(0, {root!r})
 from paper_2308_14490_b200 import api, inputs as I
-cfg = I.make_config("interval", 8192, nrhs=5, R=48, seed=4)
+cfg = I.make_config("interval", 8192, nrhs={nrhs}, R={R}, seed=4)
 plan = api.Plan.from_config(cfg)
 x, rep = plan.solve(torch.from_numpy(np.asfortranarray(I.rhs(cfg))).cuda(), 1e-12, cfg.R, 1)
 np.save({out!r}, x.cpu().numpy())
 """
 
 
-@pytest.mark.parametrize("env", [{"AZ_QR_DEFER": "0"}, {"AZ_SOLVE_HI": "0", "AZ_JAC_EXCL": "0"}])
-def test_four_step_solve_schedule_variants_agree(env, tmp_path):
+@pytest.mark.parametrize("env,R,nrhs", [({"AZ_QR_DEFER": "0"}, 48, 5), ({"AZ_QR_DEFER": "0"}, 32, 1),
+                                        ({"AZ_QR_DEFER": "0"}, 64, 64),
+                                        ({"AZ_SOLVE_HI": "0", "AZ_JAC_EXCL": "0"}, 48, 5)])
+def test_four_step_solve_schedule_variants_agree(env, R, nrhs, tmp_path):
     """The four-step single-block solve's schedules give the same x up to rounding: Q^T b' deferred
     to the side stream with y = pinv(R_S) Q^T b' (default) against Q^T b' riding along in the
     merges (AZ_QR_DEFER=0), and the stream-priority / exclusive-SM choices switched off.  The
@@ -243,9 +245,9 @@ def test_four_step_solve_schedule_variants_agree(env, tmp_path):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = str(tmp_path / "x_alt.npy")
-    subprocess.run([sys.executable, "-c", _ALT_SCRIPT.format(root=root, out=out)], check=True,
+    subprocess.run([sys.executable, "-c", _ALT_SCRIPT.format(root=root, out=out, R=R, nrhs=nrhs)], check=True,
                    env={**os.environ, **env}, timeout=600)
-    cfg = I.make_config("interval", 8192, nrhs=5, R=48, seed=4)
+    cfg = I.make_config("interval", 8192, nrhs=nrhs, R=R, seed=4)
     from paper_2308_14490_b200.api import Plan
     plan = Plan.from_config(cfg)
     x, _ = plan.solve(_dev(I.rhs(cfg)), 1e-12, cfg.R, 1)
