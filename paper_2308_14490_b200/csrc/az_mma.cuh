@@ -29,12 +29,12 @@ AZ_D double frag_ld(const double* s, int S, int i, int k) {
 
 // acc[mi][ni] (8x8 tiles) += A[m0 + 8 mi .., k0..k0+KD) * B[k0.., n0 + 8 ni ..)
 // A element (m, k) and B element (k, n) are read with frag_ld<LA>(As, SA, m, k) and
-// frag_ld<LB>(Bs, SB, n, k).
-template <int MI, int NI, int LA, int LB>
+// frag_ld<LB>(Bs, SB, n, k).  KU: k-steps unrolled together (fragment loads hoisted over them).
+template <int MI, int NI, int LA, int LB, int KU = 2>
 AZ_D void warp_mma(double (&acc)[MI][NI][2], const double* As, int SA, const double* Bs, int SB, int m0, int n0,
                    int k0, int KD, int lane) {
   const int r = lane >> 2, q = lane & 3;
-#pragma unroll 2
+#pragma unroll KU
   for (int kk = k0; kk < k0 + KD; kk += 4) {
     double a[MI], b[NI];
 #pragma unroll

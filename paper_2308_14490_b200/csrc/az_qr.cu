@@ -232,6 +232,9 @@ struct QRr {
 };
 
 constexpr int RR_S2 = 68;  // operand tile stride (== 4 mod 16), 64-row sub-blocks
+#ifndef PB_KU
+#define PB_KU 16           // pass B: k-steps per unrolled group of the DMMA loop
+#endif
 
 __global__ void __launch_bounds__(512, 1) k_tsqr_rhs(QRr q) {
   extern __shared__ double sm[];
@@ -281,7 +284,7 @@ __global__ void __launch_bounds__(512, 1) k_tsqr_rhs(QRr q) {
       }
       __syncthreads();
       if (rr + 64 < cend) load(rr + 64, cend);
-      if (mma_on) warp_mma<4, 2, IMAJ, IMAJ>(acc, Ys, RR_S2, isG ? Ys : Xs, RR_S2, wm * 32, wn * 16, 0, 64, lane);
+      if (mma_on) warp_mma<4, 2, IMAJ, IMAJ, PB_KU>(acc, Ys, RR_S2, isG ? Ys : Xs, RR_S2, wm * 32, wn * 16, 0, 64, lane);
     }
     double* D = isG ? G : P;
 #pragma unroll
