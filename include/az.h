@@ -170,6 +170,11 @@ typedef struct {
   int32_t saturated;        /* 1 if k > probes_used - p after max_blocks blocks */
   double sigma_first, sigma_last_kept;
   double ms_rhs, ms_sketch, ms_qr, ms_svd, ms_step2, ms_total;   /* CUDA-event stage times */
+  const double* sigma;      /* az_solve: DEVICE pointer INTO the caller's workspace to the n_sigma
+                               singular values of the sketch's R factor, descending (the spectrum the
+                               truncation at theta sigma_1 is taken on); valid until the
+                               workspace is reused or freed.  NULL from the factored entry points. */
+  int64_t n_sigma;          /* = probes_used */
 } az_solve_report_t;
 
 /* Bytes of DEVICE workspace az_solve needs for nrhs right-hand sides, probe block R and at
@@ -180,8 +185,12 @@ az_status_t az_solve_workspace_size(az_plan_t plan, int64_t nrhs, int64_t R, int
  * theta: sketch truncation threshold relative to sigma_1 of the sketch (R4).
  * R: probe block size; blocks are added until rank <= probes - p (p = 10) or
  * max_blocks is reached (R5; max_blocks = 1 is the literal single-block sketch).
- * report: HOST, may be NULL.  Synchronises the stream (block-adaptive decisions and the
- * report need host values).  Returns AZ_WARN_SKETCH_SATURATED if the last block saturated.  */
+ * The dense stage follows the probes actually drawn: while probes + nrhs <= 128 the single-pass
+ * TSQR and one-CTA Jacobi take the sketch; an adaptive solve whose first block fits runs it that
+ * way and moves to the blocked path (drawing its blocks afresh) only if that block saturated.
+ * report: HOST, may be NULL.  ALWAYS synchronises the stream before returning (whether or not a
+ * report is requested), so x, the workspace and the status are final on return.  Returns
+ * AZ_WARN_SKETCH_SATURATED (x still written) if the last block saturated.                     */
 az_status_t az_solve(az_plan_t plan, const double* b, int64_t ldb, double* x, int64_t ldx,
                      int64_t nrhs, double theta, int64_t R, int32_t max_blocks,
                      void* workspace, size_t ws_bytes, az_solve_report_t* report, void* stream);
@@ -199,13 +208,18 @@ const char* az_last_error(void);
 int64_t az_launch_count(int reset);
 
 /* Pipelined host-buffer solves (the e2e path): enqueue H2D of b_host (an internal upload stream),
- * az_solve on `stream` (no report, no host synchronisation when max_blocks == 1) and D2H into
- * x_host (an internal download stream), then return.  Two internal device slots let a call's
- * upload and the previous call's download overlap the current solve.  x_host is valid after
- * az_plan_sync.  Host buffers should be pinned (cudaHostAlloc / torch pin_memory); b_host must not
- * be modified until az_plan_sync.  Same shapes as az_solve_host.                             */
+ * the solve on `stream` and D2H into x_host (an internal download stream), then return.  With
+ * max_blocks == 1 nothing is synchronised (the solve's saturation test runs on the device and sets
+ * a plan flag); max_blocks > 1 needs the rank on the host and synchronises like az_solve.  Two
+ * internal device slots let a call's upload and the previous call's download overlap the current
+ * solve.  x_host is valid after az_plan_sync.  Host buffers should be pinned (cudaHostAlloc / torch
+ * pin_memory); b_host must not be modified until az_plan_sync.  Same shapes as az_solve_host.
+ * Returns errors of the enqueue only.                                                         */
 az_status_t az_solve_host_pipelined(az_plan_t plan, const double* b_host, double* x_host, int64_t nrhs,
                                     double theta, int64_t R, int32_t max_blocks, void* stream);
+/* Waits for every pipelined solve of the plan (and the device).  Returns AZ_WARN_SKETCH_SATURATED
+ * if any single-block pipelined solve since the last az_plan_sync saturated (rank > probes - p), and
+ * clears that flag.                                                                            */
 az_status_t az_plan_sync(az_plan_t plan);
 
 /* ---- factorisation reuse --------------------------------------------
@@ -233,6 +247,11 @@ az_status_t az_solve_factored(az_factor_t f, const double* b, int64_t ldb, doubl
  * Tracing adds two event records per launch; it is off by default. */
 int az_trace_enable(int on);
 int az_trace_report(char* buf, int len);
+
+/* Diagnostics (tests and tools): Jacobi sweeps of the last truncated SVD.  which = 0: the one-CTA
+ * one-sided Jacobi (r <= 128; reads a device counter, synchronising); which = 1: the block Jacobi
+ * (r > 128; outer sweeps, host counter).  PAPER.md:269 (the SVD of the sketch).               */
+int az_svd_sweeps_last(int which);
 
 #ifdef __cplusplus
 }

@@ -38,6 +38,18 @@ def tsvd_lsq(A: np.ndarray, b: np.ndarray, tol: float):
     return Vt[:k].T @ coef, k, s
 
 
+def tsvd_lsq_multi(A: np.ndarray, b: np.ndarray, tols):
+    """`tsvd_lsq` at several truncation levels from one SVD of A (the oracle's determinacy
+    delta_det compares the solutions at tol and tol/100).
+    Returns [(x, k) per tol], s."""
+    U, s, Vt = np.linalg.svd(A, full_matrices=False)
+    out = []
+    for tol in tols:
+        k = int((s > tol * s[0]).sum()) if s.size and s[0] > 0 else 0
+        out.append((Vt[:k].T @ ((U[:, :k].T @ b) / s[:k, None]), k))
+    return out, s
+
+
 # --------------------------------------------------------------------------------------
 # the problem: A and Z* as operators
 # --------------------------------------------------------------------------------------

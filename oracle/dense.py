@@ -99,8 +99,9 @@ def A_row_entries(cfg: I.Config, i_grid, half_width: int = 40):
     """Nonzero window of interior row for grid index i_grid (1-D int, 2-D (qx, qy)).
 
     Returns (column indices, values) for the columns within +-half_width centers per
-    axis; outside that window phi^per < 1e-300 for eps h = 0.5 (exp(-(0.5*40)^2) ~ 1e-174,
-    and the row is summed exactly by the caller).  Used for sampled full-size parity.
+    axis; outside that window phi^per < 1e-170 for eps h = 0.5 (exp(-(0.5*40)^2) ~ 1e-174),
+    far below binary64 resolution of the row sum.  Used for sampled full-size parity.
+    Pinned against the entrywise dense row (tests/test_oracle_pins.py).
     """
     n, s = cfg.n, cfg.s
     g = I.grid_axis(cfg)

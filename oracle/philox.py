@@ -1,7 +1,7 @@
 """Philox4x32-10 counter-based generator + Box-Muller, the probe matrix Omega.
 
 Test infrastructure only (see oracle/__init__.py).  This is an independent
-implementation of the same generator the CUDA path uses (csrc/az_philox.cuh);
+implementation of the same generator the CUDA path uses (csrc/az_common.cuh (probe_pair));
 the two share no code (task rules: "each side implements the same
 counter-based generator").
 

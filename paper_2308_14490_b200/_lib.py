@@ -36,7 +36,8 @@ class SolveReport(C.Structure):
     _fields_ = [("rank_used", C.c_int64), ("probes_used", C.c_int64), ("saturated", C.c_int32),
                 ("sigma_first", C.c_double), ("sigma_last_kept", C.c_double),
                 ("ms_rhs", C.c_double), ("ms_sketch", C.c_double), ("ms_qr", C.c_double),
-                ("ms_svd", C.c_double), ("ms_step2", C.c_double), ("ms_total", C.c_double)]
+                ("ms_svd", C.c_double), ("ms_step2", C.c_double), ("ms_total", C.c_double),
+                ("sigma", C.c_void_p), ("n_sigma", C.c_int64)]
 
 
 class AZError(RuntimeError):
@@ -95,6 +96,8 @@ def lib():
     L.az_trace_enable.restype = C.c_int
     L.az_trace_report.argtypes = [C.c_char_p, C.c_int]
     L.az_trace_report.restype = C.c_int
+    L.az_svd_sweeps_last.argtypes = [C.c_int]
+    L.az_svd_sweeps_last.restype = C.c_int
     L.az_launch_count.argtypes = [C.c_int]
     L.az_launch_count.restype = C.c_int64
     _lib = L
@@ -107,7 +110,7 @@ EXPORTED = ["az_plan_create", "az_plan_destroy", "az_plan_query", "az_apply_A", 
             "az_solve_workspace_size", "az_solve", "az_solve_host", "az_status_string",
             "az_last_error", "az_launch_count", "az_trace_enable", "az_trace_report",
             "az_factorize", "az_factor_destroy", "az_factor_query", "az_factor_workspace_size",
-            "az_solve_factored", "az_solve_host_pipelined", "az_plan_sync"]
+            "az_solve_factored", "az_solve_host_pipelined", "az_plan_sync", "az_svd_sweeps_last"]
 
 
 def check(fn: str, status: int, allow=(AZ_OK,)):

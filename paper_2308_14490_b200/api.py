@@ -46,6 +46,16 @@ def _stream(stream=None):
     return C.c_void_p(s.cuda_stream)
 
 
+def _keep(stream, *tensors):
+    """Tensors allocated on the current stream but used by libaz work enqueued on another `stream`:
+    tell the caching allocator, so their memory is not reused before that work completes."""
+    if stream is None or stream == torch.cuda.current_stream():
+        return
+    for t in tensors:
+        if t is not None and t.is_cuda:
+            t.record_stream(stream)
+
+
 class Plan:
     """An AZ plan (az_plan_create): geometry, symbols of B and B^dag, scratch."""
 
@@ -112,6 +122,7 @@ class Plan:
             out = empty_colmajor(rows_out, k, x.device) if x.dim() == 2 else torch.empty(rows_out, dtype=torch.float64, device=x.device)
         py, ldy, _ = _mat(out)
         check(name, getattr(lib(), name)(self._h, C.c_void_p(px), ldx, C.c_void_p(py), ldy, k, _stream(stream)))
+        _keep(stream, x, out)
         return out
 
     def apply_A(self, x, out=None, stream=None):
@@ -134,6 +145,7 @@ class Plan:
             out = empty_colmajor(self.rows, ncols)
         p, ld, _ = _mat(out)
         check("az_sketch", lib().az_sketch(self._h, col0, ncols, C.c_void_p(p), ld, _stream(stream)))
+        _keep(stream, out)
         return out
 
     def omega_apply(self, col0: int, y, out=None, accumulate=False, stream=None):
@@ -144,6 +156,7 @@ class Plan:
         px, ldx, _ = _mat(out)
         check("az_omega_apply", lib().az_omega_apply(self._h, col0, ncols, C.c_void_p(py), ldy, nrhs,
                                                      C.c_void_p(px), ldx, int(accumulate), _stream(stream)))
+        _keep(stream, y, out)
         return out
 
     # ---------------------------------------------------------------- solve
@@ -165,7 +178,8 @@ class Plan:
                                               max_blocks, C.c_void_p(workspace.data_ptr()), workspace.numel(),
                                               C.byref(rep), _stream(stream)),
                    allow=(_lib.AZ_OK, _lib.AZ_WARN_SKETCH_SATURATED))
-        return x, _report(rep, st)
+        # az_solve synchronises its stream before returning: the workspace is free to go
+        return x, _report(rep, st, workspace)
 
     def solve_host(self, b, theta: float, R: int, max_blocks: int = 1, x=None, stream=None):
         """End-to-end solve on HOST buffers (host->device copy of b, solve, device->host copy of x
@@ -260,11 +274,17 @@ def plan_sync(plan: "Plan"):
     check("az_plan_sync", lib().az_plan_sync(plan._h))
 
 
-def _report(rep, status):
-    return {"rank": rep.rank_used, "probes": rep.probes_used, "saturated": bool(rep.saturated),
-            "sigma_first": rep.sigma_first, "sigma_last_kept": rep.sigma_last_kept,
-            "ms_rhs": rep.ms_rhs, "ms_sketch": rep.ms_sketch, "ms_qr": rep.ms_qr, "ms_svd": rep.ms_svd,
-            "ms_step2": rep.ms_step2, "ms_total": rep.ms_total, "status": _lib.STATUS.get(status, status)}
+def _report(rep, status, workspace=None):
+    out = {"rank": rep.rank_used, "probes": rep.probes_used, "saturated": bool(rep.saturated),
+           "sigma_first": rep.sigma_first, "sigma_last_kept": rep.sigma_last_kept,
+           "ms_rhs": rep.ms_rhs, "ms_sketch": rep.ms_sketch, "ms_qr": rep.ms_qr, "ms_svd": rep.ms_svd,
+           "ms_step2": rep.ms_step2, "ms_total": rep.ms_total, "status": _lib.STATUS.get(status, status)}
+    if workspace is not None and rep.sigma and rep.n_sigma > 0:
+        # the sketch's singular values live in the caller's workspace: copy them out
+        off = rep.sigma - workspace.data_ptr()
+        if 0 <= off and off + 8 * rep.n_sigma <= workspace.numel():
+            out["sigma"] = workspace[off:off + 8 * rep.n_sigma].view(torch.float64).clone()
+    return out
 
 
 def qr_r(A: torch.Tensor, stream=None) -> torch.Tensor:
@@ -278,6 +298,7 @@ def qr_r(A: torch.Tensor, stream=None) -> torch.Tensor:
     pr, ldr, _ = _mat(R)
     check("az_qr_r", lib().az_qr_r(None, C.c_void_p(pa), m, k, lda, C.c_void_p(pr), ldr,
                                    C.c_void_p(w.data_ptr()), w.numel(), _stream(stream)))
+    _keep(stream, A, w, R)
     return R
 
 
@@ -293,6 +314,7 @@ def qr_r_partial(A: torch.Tensor, k1: int, stream=None) -> torch.Tensor:
     pr, ldr, _ = _mat(R)
     check("az_qr_r_partial", lib().az_qr_r_partial(None, C.c_void_p(pa), m, k, k1, lda, C.c_void_p(pr), ldr,
                                                    C.c_void_p(w.data_ptr()), w.numel(), _stream(stream)))
+    _keep(stream, A, w, R)
     return R
 
 
@@ -309,6 +331,7 @@ def tsvd_solve(Rf: torch.Tensor, r: int, nrhs: int, theta: float, stream=None):
     check("az_tsvd_solve", lib().az_tsvd_solve(C.c_void_p(pr), ldr, r, nrhs, theta, C.c_void_p(py), ldy,
                                                C.c_void_p(sig.data_ptr()), C.byref(k),
                                                C.c_void_p(w.data_ptr()), w.numel(), _stream(stream)))
+    _keep(stream, Rf, w, y, sig)
     return y, sig, k.value
 
 

@@ -71,6 +71,7 @@ struct az_plan_s {
   void* d_solve_ws = nullptr;
   size_t d_solve_ws_bytes = 0;
   az_pipe_s* pipe = nullptr;
+  int* d_satflag = nullptr;     // set by pipelined solves whose sketch saturated; read by az_plan_sync
   // side stream of az_solve: the Z* b / M column passes (and, deferred, Q^T b') run beside the TSQR
   // merges and the SVD; side_ev: [0] TSQR leaf done, [1] R_S merged, [2] the side stream's work done
   cudaStream_t side = nullptr;

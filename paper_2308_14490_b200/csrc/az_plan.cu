@@ -100,6 +100,11 @@ extern "C" int az_trace_report(char* buf, int len) {
   }
   return (int)out.size();
 }
+int az_small_sweeps_last();
+int az_bjac_sweeps_last();
+extern "C" int az_svd_sweeps_last(int which) {
+  return which == 0 ? az_small_sweeps_last() : az_bjac_sweeps_last();
+}
 extern "C" int64_t az_launch_count(int reset) {
   return reset ? g_launches.exchange(0) : g_launches.load();
 }
@@ -382,7 +387,7 @@ static void plan_free(az_plan_s* p) {
   if (p->d_W0y == p->d_W0) p->d_W0y = nullptr;   // aliases of the x tables (square boxes)
   if (p->d_W2y == p->d_W2) p->d_W2y = nullptr;
   void* ptrs[] = {p->d_mask, p->d_pos, p->d_W0, p->d_W2, p->d_W0y, p->d_W2y, p->d_Wr, p->d_zinv, p->d_tw,
-                  p->d_tw4hi, p->d_tw4lo, p->d_bxy, p->d_bw, p->d_bj, p->d_C1, p->d_Z2, p->d_G, p->d_solve_ws};
+                  p->d_tw4hi, p->d_tw4lo, p->d_bxy, p->d_bw, p->d_bj, p->d_C1, p->d_Z2, p->d_G, p->d_solve_ws, p->d_satflag};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->h_stage) cudaFreeHost(p->h_stage);

@@ -981,6 +981,3 @@ extern "C" az_status_t az_qr_r_partial(az_plan_t, double* A, int64_t m, int64_t 
   return az_qr_r_impl(A, m, k, lda, R, ldr, ws, ws_bytes, (cudaStream_t)stream, k1);
 }
 
-extern "C" void az_debug_tsqr(long long* out3) {
-  cudaMemcpyFromSymbol(out3, g_tsqr_dbg, 3 * sizeof(long long));
-}

@@ -217,6 +217,14 @@ static unsigned gemm_small_grid(int64_t m) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(az_div_up(m, 64), (int64_t)per_sm * sms));
 }
 
+// The single-pass TSQR / one-CTA Jacobi (narrow) path takes the sketch while probes + nrhs <= 128;
+// the blocked Householder / block-Jacobi (wide) path beyond.  The choice follows the probes a solve
+// actually draws: an adaptive solve whose first block fits the narrow path runs it first and moves to
+// the wide path (drawing its blocks afresh) only if that block saturated (reading R5).
+static bool narrow_first(int64_t nrhs, int64_t R, int32_t max_blocks) {
+  return max_blocks > 1 && R + nrhs <= AZ_NARROW_MAX && R * max_blocks + nrhs > AZ_NARROW_MAX;
+}
+
 static SolveWS layout(az_plan_s* p, int64_t nrhs, int64_t R, int32_t max_blocks, char* base) {
   SolveWS w;
   const int64_t rows = p->M + p->Mb;
@@ -266,6 +274,7 @@ extern "C" az_status_t az_solve_workspace_size(az_plan_t p, int64_t nrhs, int64_
     return AZ_ERR_INVALID_ARGUMENT;
   }
   *bytes = layout(p, nrhs, R, max_blocks, nullptr).total;
+  if (narrow_first(nrhs, R, max_blocks)) *bytes = std::max(*bytes, layout(p, nrhs, R, 1, nullptr).total);
   return AZ_OK;
 }
 
@@ -309,25 +318,19 @@ static az_status_t step2(az_plan_s* p, const double* x2, const double* b, int64_
   return AZ_OK;
 }
 
-extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, double* x, int64_t ldx, int64_t nrhs,
-                                double theta, int64_t R, int32_t max_blocks, void* workspace, size_t ws_bytes,
-                                az_solve_report_t* report, void* stream) {
-  if (!p || !b || !x || nrhs < 1 || R < 1 || max_blocks < 1 || !(theta >= 0.0) || ldb < p->M + p->Mb || ldx < p->N) {
-    az_set_error("az_solve: bad arguments");
-    return AZ_ERR_INVALID_ARGUMENT;
-  }
-  SolveWS w = layout(p, nrhs, R, max_blocks, nullptr);
-  if (!workspace || ws_bytes < w.total) {
-    az_set_error("az_solve: workspace too small (%zu < %zu)", ws_bytes, w.total);
-    return AZ_ERR_WORKSPACE;
-  }
-  w = layout(p, nrhs, R, max_blocks, (char*)workspace);
-  cudaStream_t st = (cudaStream_t)stream;
+__global__ void k_flag_saturated(const int64_t* rank, int64_t limit, int* flag) {
+  if (*rank > limit) atomicOr(flag, 1);
+}
+
+// One solve on a workspace laid out for (nrhs, R, max_blocks).  async (max_blocks == 1 only): the
+// solve is enqueued without any host synchronisation and no report; if sat_flag (DEVICE) is given,
+// a saturated sketch sets it (az_solve_host_pipelined / az_plan_sync).
+static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double* x, int64_t ldx, int64_t nrhs,
+                              double theta, int64_t R, int32_t max_blocks, void* workspace,
+                              az_solve_report_t* report, cudaStream_t st, bool async_mode, int* sat_flag) {
+  SolveWS w = layout(p, nrhs, R, max_blocks, (char*)workspace);
   const int64_t rows = p->M + p->Mb;
   const int pfix = 10;
-  // no report and a single probe block: nothing needs to come back to the host, so the whole solve
-  // is enqueued without a host synchronisation (az_solve_host_pipelined relies on this)
-  const bool async_mode = report == nullptr && max_blocks == 1;
   // the rank is needed on the host mid-solve only to decide on another probe block; with one block
   // it is read after the last kernel, so step 2 is enqueued without waiting for the SVD
   const bool host_rank = max_blocks > 1;
@@ -508,7 +511,13 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   }
   cudaEventRecord(ev.e[7], st);
   if (dbg_host) fprintf(stderr, "az_solve host: all issued +%.2f ms\n", hnow() - th0);
-  if (async_mode) return AZ_OK;
+  if (async_mode) {
+    if (sat_flag && rank_dev) {
+      k_flag_saturated<<<1, 1, 0, st>>>(rank_dev, kp - pfix, sat_flag);
+      AZ_LAUNCH_CHECK();
+    }
+    return AZ_OK;
+  }
   AZ_CUDA_CHECK(cudaEventSynchronize(ev.e[7]));
   if (!host_rank) {
     if (rank_dev) AZ_CUDA_CHECK(cudaMemcpy(&rank, rank_dev, sizeof(int64_t), cudaMemcpyDeviceToHost));
@@ -532,8 +541,44 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
     report->ms_svd = ms_svd;
     report->ms_step2 = ms_between(ev.e[6], ev.e[7]);
     report->ms_total = ms_between(ev.e[0], ev.e[7]);
+    report->sigma = w.sig;
+    report->n_sigma = kp;
   }
   return saturated ? AZ_WARN_SKETCH_SATURATED : AZ_OK;
+}
+
+extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, double* x, int64_t ldx, int64_t nrhs,
+                                double theta, int64_t R, int32_t max_blocks, void* workspace, size_t ws_bytes,
+                                az_solve_report_t* report, void* stream) {
+  if (!p || !b || !x || nrhs < 1 || R < 1 || max_blocks < 1 || !(theta >= 0.0) || ldb < p->M + p->Mb || ldx < p->N) {
+    az_set_error("az_solve: bad arguments");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  size_t need = 0;
+  AZ_TRY(az_solve_workspace_size(p, nrhs, R, max_blocks, &need));
+  if (!workspace || ws_bytes < need) {
+    az_set_error("az_solve: workspace too small (%zu < %zu)", ws_bytes, need);
+    return AZ_ERR_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  az_solve_report_t rep;
+  memset(&rep, 0, sizeof(rep));
+  double ms_first = 0.0;
+  if (narrow_first(nrhs, R, max_blocks)) {
+    // the first probe block on the narrow path; kept unless it saturated
+    const az_status_t s = solve_impl(p, b, ldb, x, ldx, nrhs, theta, R, 1, workspace, &rep, st, false, nullptr);
+    if (s != AZ_WARN_SKETCH_SATURATED) {
+      if (report) *report = rep;
+      return s;
+    }
+    ms_first = rep.ms_total;
+    memset(&rep, 0, sizeof(rep));
+  }
+  const az_status_t s = solve_impl(p, b, ldb, x, ldx, nrhs, theta, R, max_blocks, workspace, &rep, st, false, nullptr);
+  if (s != AZ_OK && s != AZ_WARN_SKETCH_SATURATED) return s;
+  rep.ms_total += ms_first;
+  if (report) *report = rep;
+  return s;
 }
 
 // Host-buffer convenience (end-to-end timing: host->device copy of b, solve, device->host x).
@@ -1411,8 +1456,17 @@ extern "C" az_status_t az_solve_host_pipelined(az_plan_t p, const double* b_host
   // solve once the upload is in and the slot's previous result has been downloaded
   AZ_CUDA_CHECK(cudaStreamWaitEvent(st, q->ev_up[sl], 0));
   AZ_CUDA_CHECK(cudaStreamWaitEvent(st, q->ev_down[sl], 0));
-  az_status_t s = az_solve(p, q->bdev[sl], rows, q->xdev[sl], p->N, nrhs, theta, R, max_blocks, q->ws, q->ws_bytes,
-                           nullptr, stream);
+  if (!p->d_satflag) {
+    AZ_CUDA_CHECK(cudaMalloc(&p->d_satflag, sizeof(int)));
+    AZ_CUDA_CHECK(cudaMemsetAsync(p->d_satflag, 0, sizeof(int), st));
+  }
+  // one probe block: enqueued without a host synchronisation (saturation lands in the plan's device
+  // flag, read by az_plan_sync); adaptive solves need the rank on the host and synchronise
+  az_status_t s = max_blocks == 1
+                      ? solve_impl(p, q->bdev[sl], rows, q->xdev[sl], p->N, nrhs, theta, R, 1, q->ws, nullptr, st,
+                                   true, p->d_satflag)
+                      : az_solve(p, q->bdev[sl], rows, q->xdev[sl], p->N, nrhs, theta, R, max_blocks, q->ws,
+                                 q->ws_bytes, nullptr, stream);
   if (s != AZ_OK && s != AZ_WARN_SKETCH_SATURATED) return s;
   AZ_CUDA_CHECK(cudaEventRecord(q->ev_solved[sl], st));
   AZ_CUDA_CHECK(cudaStreamWaitEvent(q->down, q->ev_solved[sl], 0));
@@ -1428,5 +1482,11 @@ extern "C" az_status_t az_plan_sync(az_plan_t p) {
     AZ_CUDA_CHECK(cudaStreamSynchronize(p->pipe->down));
   }
   AZ_CUDA_CHECK(cudaDeviceSynchronize());
+  if (p->d_satflag) {
+    int f = 0;
+    AZ_CUDA_CHECK(cudaMemcpy(&f, p->d_satflag, sizeof(int), cudaMemcpyDeviceToHost));
+    AZ_CUDA_CHECK(cudaMemset(p->d_satflag, 0, sizeof(int)));
+    if (f) return AZ_WARN_SKETCH_SATURATED;
+  }
   return AZ_OK;
 }

@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
   }
 }
 
-extern "C" int az_debug_small_sweeps() {
+int az_small_sweeps_last() {
   int v = -1;
   cudaMemcpyFromSymbol(&v, g_small_sweeps, sizeof(int));
   return v;

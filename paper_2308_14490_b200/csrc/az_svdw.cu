@@ -429,11 +429,8 @@ __global__ void k_bjac_load(const double* Rf, int64_t ldr, int64_t r, int nrhs, 
 static size_t a256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 static int g_last_sweeps = 0;
-static int g_inner_sweeps = 1;
-extern "C" int az_debug_jacobi(int inner_sweeps) {   // returns the outer sweeps of the last block-Jacobi SVD
-  if (inner_sweeps > 0) g_inner_sweeps = inner_sweeps;
-  return g_last_sweeps;
-}
+static const int g_inner_sweeps = 1;
+int az_bjac_sweeps_last() { return g_last_sweeps; }   // outer sweeps of the last block-Jacobi SVD
 
 // QR preconditioning (Drmac & Veselic): R_S^T = Q2 R2, R2^T = Q3 R3, so R_S = Q3 R3 Q2^T and
 // pinv(R_S) c = Q2 pinv(R3) (Q3^T c).  One-sided Jacobi on R3^T needs markedly fewer sweeps than on

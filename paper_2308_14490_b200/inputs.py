@@ -15,7 +15,7 @@ both sides consume as inputs:
 
 The probe matrix Omega is NOT generated here: each side implements the same
 counter-based Philox4x32-10 generator itself (oracle/philox.py and
-csrc/az_philox.cuh), per the task rules.
+csrc/az_common.cuh (probe_pair)), per the task rules.
 
 Grid conventions (PAPER.md:76-83 Eqs. set_centers / set_Xtilde with T=1):
   centers  c_j = -1 + j*h,          h = 2/n,      j = 0..n-1

@@ -52,3 +52,15 @@ def test_status_strings_without_gpu(libpath):
     L.az_status_string.argtypes = [ctypes.c_int]
     assert L.az_status_string(0)
     assert L.az_status_string(100)
+
+
+def test_library_exports_nothing_undeclared(libpath):
+    """Every exported az_* symbol of libaz.so is declared in include/az.h (no hidden entry points)."""
+    import shutil
+    import subprocess
+    if not shutil.which("nm"):
+        pytest.skip("nm not available")
+    out = subprocess.run(["nm", "-D", "--defined-only", libpath], capture_output=True, text=True, check=True).stdout
+    exported = {ln.split()[-1] for ln in out.splitlines() if ln.split() and ln.split()[-1].startswith("az_")}
+    extra = exported - set(_declared())
+    assert not extra, sorted(extra)

@@ -7,6 +7,14 @@ Tolerances:
   I - A Z*:        ||y - y_ref|| <= 1e-12 ||A||_2 ||Z*||_2 ||b||
 Each bound is the forward-error scale of the composite in binary64 (the reference itself is
 computed with 64-bit-mantissa DFTs).
+
+On top of those scale-derived bounds every operator test also holds the ACHIEVED error, normwise
+relative to the reference (||y - y_ref|| / ||y_ref||), to 10x the error a binary64 FFT
+implementation reaches (measured with numpy's FFT against the same references):
+A, A^T 2e-14 (measured <= 1.8e-15); Z* 2e-10 (<= 1.8e-11); A - A Z* A and I - A Z* 1e-10 in 1-D
+(<= 1.2e-11) and 1e-9 in 2-D (~1e-10).  The paper-regime family (eps from Eq. 4, ||Z*|| ~ 1e8,
+PAPER.md:437) is outside those measurements: its achieved errors are recorded, not held to them.
+Achieved errors go to the parity log (tests/conftest.py PARITY_LOG).
 """
 import numpy as np
 import pytest
@@ -70,6 +78,21 @@ def _rel(y, ref):
     return np.linalg.norm(y - ref) / np.linalg.norm(ref)
 
 
+TIGHT = {"A": 2e-14, "Zstar": 2e-10, "K1": 1e-10, "K2": 1e-9}
+
+
+def _achieved(record, cfg, kind, y, ref):
+    """Normwise relative error per column; recorded, and held to the TIGHT bar of its kind."""
+    y, ref = y.reshape(y.shape[0], -1), ref.reshape(ref.shape[0], -1)
+    err = max(_rel(y[:, c], ref[:, c]) for c in range(y.shape[1]))
+    key = kind if kind in ("A", "Zstar") else f"K{cfg.dim}"
+    bar = TIGHT[key]
+    record(case=cfg.name, op=kind, achieved=float(err), bar=bar)
+    if cfg.eps_h == 0.5:
+        assert err <= bar, (kind, err, bar)
+    return err
+
+
 def test_plan_info(setup):
     cfg, plan, prob, A = setup
     assert plan.M == int(I.mask(cfg).sum()) and plan.N == cfg.N and plan.Mb == cfg.n_boundary
@@ -86,18 +109,20 @@ def prob_sigma2(cfg):
 
 
 @pytest.mark.parametrize("nvec", [1, 2, 5])
-def test_apply_A_and_At(setup, nvec):
+def test_apply_A_and_At(setup, nvec, parity_record):
     cfg, plan, prob, A = setup
     x = I.gaussian_matrix(cfg.N, nvec, 10 + nvec)
     y = _host(plan.apply_A(_dev(x)))
     ref = A @ x
     for c in range(nvec):
         assert _rel(y[:, c], ref[:, c]) <= 1e-12
+    _achieved(parity_record, cfg, "A", y, ref)
     yy = I.gaussian_matrix(A.shape[0], nvec, 20 + nvec)
     xt = _host(plan.apply_At(_dev(yy)))
     reft = A.T @ yy
     for c in range(nvec):
         assert _rel(xt[:, c], reft[:, c]) <= 1e-12
+    _achieved(parity_record, cfg, "A", xt, reft)
 
 
 def test_adjoint_identity(setup):
@@ -111,17 +136,18 @@ def test_adjoint_identity(setup):
 
 
 @pytest.mark.parametrize("nvec", [1, 3])
-def test_apply_Zstar(setup, nvec):
+def test_apply_Zstar(setup, nvec, parity_record):
     cfg, plan, prob, A = setup
     y = I.gaussian_matrix(A.shape[0], nvec, 30 + nvec)
     x = _host(plan.apply_Zstar(_dev(y)))
     ref = prob.apply_Zstar(y)
     for c in range(nvec):
         assert np.linalg.norm(x[:, c] - ref[:, c]) <= 1e-12 * plan.zstar_norm * np.linalg.norm(y[:, c])
+    _achieved(parity_record, cfg, "Zstar", x, ref)
 
 
 @pytest.mark.parametrize("nvec", [2, 3])
-def test_apply_step1_and_resid(setup, nvec):
+def test_apply_step1_and_resid(setup, nvec, parity_record):
     cfg, plan, prob, A = setup
     nA = plan.sigma_max
     v = I.gaussian_matrix(cfg.N, nvec, 40 + nvec)
@@ -129,18 +155,20 @@ def test_apply_step1_and_resid(setup, nvec):
     ref = OA.step1_apply(prob, v)
     for c in range(nvec):
         assert np.linalg.norm(y[:, c] - ref[:, c]) <= 1e-12 * nA * nA * plan.zstar_norm * np.linalg.norm(v[:, c])
+    _achieved(parity_record, cfg, "step1", y, ref)
     b = I.gaussian_matrix(A.shape[0], nvec, 50 + nvec)
     r = _host(plan.apply_resid(_dev(b)))
     refr = OA.resid_apply(prob, b)
     for c in range(nvec):
         assert np.linalg.norm(r[:, c] - refr[:, c]) <= 1e-12 * nA * plan.zstar_norm * np.linalg.norm(b[:, c])
+    _achieved(parity_record, cfg, "resid", r, refr)
     # on the interior block I - A Z* is a projector complement: ||b'_i|| <= ||b_i|| (Lemma 5
     # proof); boundary rows are outside that statement
     M = plan.M
     assert np.all(np.linalg.norm(r[:M], axis=0) <= np.linalg.norm(b[:M], axis=0) * (1 + 1e-12))
 
 
-def test_sketch_matches_oracle_probes(setup):
+def test_sketch_matches_oracle_probes(setup, parity_record):
     cfg, plan, prob, A = setup
     col0, ncols = 5, 7      # ragged: odd count, non-zero global offset
     S = _host(plan.sketch(col0, ncols))
@@ -149,6 +177,7 @@ def test_sketch_matches_oracle_probes(setup):
     nA = plan.sigma_max
     for c in range(ncols):
         assert np.linalg.norm(S[:, c] - ref[:, c]) <= 1e-12 * nA * nA * plan.zstar_norm * np.linalg.norm(Om[:, c])
+    _achieved(parity_record, cfg, "sketch", S, ref)
 
 
 def test_leading_dimension_and_empty(setup):
@@ -180,7 +209,7 @@ FULL_CASES = [(n, I.get_config(n)) for n in ("c2", "c3", "c4", "c5")] + [
 
 
 @pytest.mark.parametrize("name,cfg", FULL_CASES, ids=[c[0] for c in FULL_CASES])
-def test_full_size_sampled_and_normwise(name, cfg):
+def test_full_size_sampled_and_normwise(name, cfg, parity_record):
     """BASELINE full sizes (c2: n = 2^20, fine grid 2^21; c3/c4/c5: 256^2 / 128^2 / 512^2 centres)
     in the bench's launch configuration: sampled rows of A x against the windowed exact row sums
     (interior and, for c4, boundary rows), and the composite operators against the FFT oracle
@@ -206,17 +235,27 @@ def test_full_size_sampled_and_normwise(name, cfg):
             assert np.all(np.abs(y[plan.M + i] - ref) <= 1e-12 * np.abs(rowv) @ np.abs(x))
     ref = prob.apply_A(x)
     assert _rel(y, ref) <= 1e-12
+    _achieved(parity_record, cfg, "A", y, ref)
     nA = plan.sigma_max
     S = _host(plan.sketch(0, 4))
     Om = OP.probes(cfg.N, [0, 1, 2, 3], cfg.seed)
     refS = OA.step1_apply(prob, Om)
     for c in range(4):
         assert np.linalg.norm(S[:, c] - refS[:, c]) <= 1e-12 * nA * nA * plan.zstar_norm * np.linalg.norm(Om[:, c])
+    # the full-size references are the binary64 FFT oracle (numpy.fft), not the extended-precision
+    # closed form: the achieved error is the sum of both implementations' rounding (recorded; held
+    # to 10x the reduced-size bars)
+    errS = max(_rel(S[:, c], refS[:, c]) for c in range(4))
+    parity_record(case=name, op="sketch_full", achieved=float(errS), bar=10 * TIGHT[f"K{cfg.dim}"])
+    assert errS <= 10 * TIGHT[f"K{cfg.dim}"]
     b = I.rhs(cfg)[:, :3]
     z = _host(plan.apply_Zstar(_dev(b)))
     refz = prob.apply_Zstar(b)
     for c in range(b.shape[1]):
         assert np.linalg.norm(z[:, c] - refz[:, c]) <= 1e-12 * plan.zstar_norm * np.linalg.norm(b[:, c])
+    errZ = max(_rel(z[:, c], refz[:, c]) for c in range(b.shape[1]))
+    parity_record(case=name, op="Zstar_full", achieved=float(errZ), bar=10 * TIGHT["Zstar"])
+    assert errZ <= 10 * TIGHT["Zstar"]
 
 
 def _plan_kwargs(cfg, **over):

@@ -127,25 +127,6 @@ def test_solve_literal_single_block_reports_saturation_flag():
     assert not rep["saturated"] and rep["probes"] == 32
 
 
-def test_solve_c2_full_size():
-    """BASELINE config 2 at full size (n = 2^20, 64 RHS, 64 probes): manufactured-solution error,
-    residual, rank (Theorem 7 bound), and the approximant of the FFT oracle (O2) on 4 RHS."""
-    from paper_2308_14490_b200.api import Plan
-    cfg = I.get_config("c2")
-    plan = Plan.from_config(cfg)
-    b = I.rhs(cfg)
-    x, rep = plan.solve(_dev(b), 1e-12, cfg.R, 1)
-    x = _host(x)
-    assert not rep["saturated"] and 12 <= rep["rank"] <= 40
-    grid = I.test_grid(cfg)
-    f = OA.evaluate(cfg, x, grid)
-    err = np.max(np.abs(f - grid.exact), axis=0)
-    assert np.all(err <= 1e-9), err.max()
-    prob = OA.make_problem(cfg, "fft")
-    res = OA.relative_residual(prob, x[:, :4], b[:, :4])
-    assert np.all(res <= 1e-8)
-
-
 @pytest.mark.parametrize("name,cfg,max_blocks", [("c1", I.get_config("c1"), 4),
                                                  ("interval_n4096_4step", I.make_config("interval", 4096, nrhs=6, R=40), 4),
                                                  ("star_n32", I.make_config("star", 32), 8)])

@@ -1,0 +1,79 @@
+"""Pins of the oracle functions the verdict of round 1 found unpinned: ||Z*||_2 (which scales every
+Z* / composite parity bar), the windowed branch of `evaluate` (n > 4096, used for every c2 check)
+and the 1-D branch of `A_row_entries` (sampled full-size parity).  Each is checked against an
+independent computation: LAPACK on the entrywise-assembled matrix, or the plain dense sum."""
+import numpy as np
+import pytest
+
+from paper_2308_14490_b200 import inputs as I
+from oracle import az as OA
+from oracle import circulant as C
+from oracle import dense as D
+from oracle.kernel import periodized
+
+
+@pytest.mark.parametrize("family,n", [("box1d", 32), ("interval", 256), ("ode", 64), ("box2d", 8),
+                                      ("disk", 16), ("star", 8), ("star", 16), ("helm", 8)])
+def test_zstar_norm_is_the_norm_of_the_thresholded_pinv(family, n):
+    """||Z*||_2 = ||pinv_rcond(A^c)||_2 (Z* = F B^dag P E is the thresholded pseudo-inverse of the
+    periodic A^c on the full grid): against LAPACK's SVD of the
+    entrywise-assembled A^c (numpy pinv drops sigma <= rcond sigma_1, the same rule as reading R3),
+    and the number of dropped modes against LAPACK's count."""
+    cfg = I.make_config(family, n)
+    sym = C.Symbol(cfg.dim, cfg.n, cfg.s, cfg.eps, cfg.T, cfg.row_op, alpha=cfg.row_scale, k0sq=cfg.k0sq,
+                   n_y=cfg.ny if cfg.dim == 2 else 0, T_y=cfg.Ty if cfg.dim == 2 else 0.0)
+    ops = C.PeriodicOperators(sym, cfg.tol)
+    Ac = D.assemble_Ac(cfg)
+    s = np.linalg.svd(Ac, compute_uv=False)
+    keep = s > cfg.tol * s[0]
+    assert ops.n_dropped == int((~keep).sum())
+    ref = np.linalg.norm(np.linalg.pinv(Ac, rcond=cfg.tol), 2)
+    # LAPACK resolves sigma_min to absolute O(u sigma_1): relative u kappa (kappa <= 1e7 here)
+    assert abs(ops.zstar_norm() - ref) <= 1e-8 * ref
+    assert abs(ops.zstar_norm() - 1.0 / s[keep].min()) <= 1e-8 * ref
+
+
+def test_evaluate_windowed_branch_equals_the_dense_sum():
+    """`evaluate` for n > 4096 sums over +-40 centres of each point; against the plain sum over all
+    n centres on the same test grid and random coefficients."""
+    cfg = I.make_config("interval", 8192, nrhs=3)
+    grid = I.test_grid(cfg, points_1d=3001)
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((cfg.N, 3))
+    got = OA.evaluate(cfg, x, grid)
+    c = I.center_axis(cfg)
+    t = grid.axes[0]
+    ref = np.zeros((t.size, 3))
+    for j0 in range(0, cfg.n, 1024):          # the full sum, in column blocks to bound memory
+        Phi = periodized(t[:, None] - c[None, j0:j0 + 1024], cfg.eps, cfg.T, 0)
+        ref += Phi @ x[j0:j0 + 1024]
+    assert np.max(np.abs(got - ref[grid.inside])) <= 1e-14 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("family,n", [("interval", 256), ("ode", 128), ("interval", 64)])
+def test_A_row_entries_1d_equals_the_dense_row(family, n):
+    """The windowed 1-D row of A (value rows, and the alpha (phi'' + k^2 phi) rows of the ODE)
+    against the entrywise dense row of `dense.assemble_A`: the window agrees with it exactly and the
+    entries it omits are below 1e-170 of the row's largest (exp(-(eps h 40)^2) = e^-400), far below
+    binary64 resolution of any row sum."""
+    cfg = I.make_config(family, n)
+    A = D.assemble_A(cfg)
+    m = I.mask(cfg).astype(bool)
+    rows = np.flatnonzero(m)
+    for r in (0, len(rows) // 3, len(rows) - 1):
+        cols, vals = D.A_row_entries(cfg, rows[r])
+        dense = A[r]
+        np.testing.assert_array_equal(vals, dense[cols])
+        rest = np.delete(dense, cols)
+        assert rest.size == 0 or np.max(np.abs(rest)) <= 1e-170 * np.max(np.abs(dense))
+
+
+def test_A_row_entries_2d_equals_the_dense_row():
+    cfg = I.make_config("star", 16)
+    A = D.assemble_A(cfg)
+    m = I.mask(cfg).astype(bool)
+    qs = np.argwhere(m)
+    for r in (0, len(qs) // 2, len(qs) - 1):
+        cols, vals = D.A_row_entries(cfg, tuple(qs[r]))
+        order = np.argsort(cols)
+        np.testing.assert_allclose(vals[order], A[r][cols[order]], rtol=1e-15, atol=1e-300)

@@ -37,4 +37,4 @@ else:
     y, s, kk = api.tsvd_solve(Rf, r, nrhs, 1e-12)
     torch.cuda.synchronize()
     dt = time.time() - t
-    print(f"svd r={r}: {dt*1e3:.1f} ms, rank {kk}, sweeps {lib().az_debug_jacobi(0)}, {13*8*r**3/dt/1e12:.2f} 'TFLOP/s' at 8r^3 x 13 sweeps")
+    print(f"svd r={r}: {dt*1e3:.1f} ms, rank {kk}, sweeps {lib().az_svd_sweeps_last(1)}, {13*8*r**3/dt/1e12:.2f} 'TFLOP/s' at 8r^3 x 13 sweeps")
