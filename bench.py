@@ -133,35 +133,76 @@ class Clocks:
 # CPU oracle sample (cpu_baseline and --impl reference)
 # ------------------------------------------------------------------------------------------
 def oracle_sample(cfg, R):
-    """Time the oracle (oracle/az.py, paper's algorithm with numpy FFTs, fp64) on a bounded sample
-    of the workload and scale to one full solve: 2 probes of the sketch, 2 RHS of b' and step 2,
-    2 probe columns of Omega y, and the dense SVD of an (M x R) matrix at full size."""
+    """One bounded sample of the oracle's own AZ (O2: oracle/az.py, the paper's Alg. 1 with numpy FFT
+    operators, fp64) on this workload, and the full-solve time it implies.
+
+    Timed, every call: the Philox generation and the step-1 operator (A - A Z* A) of 2 of the R probe
+    columns; b' = (I - A Z*) b and the step-2 correction Z*(b - A x2) for 2 of the nrhs right-hand
+    sides; 2 columns of x2 = Omega y; and the dense SVD of a full-size rows x R sketch.  The solve time
+    is ESTIMATED by scaling the per-column parts linearly to R probes / nrhs right-hand sides (every
+    column costs the same FFTs) and adding the full-size SVD once.  Returns (estimate_s, sample_s, desc)."""
     from oracle import az as OA
     from oracle import philox as OP
-    t0 = time.perf_counter()
     prob = OA.make_problem(cfg, "fft")
-    t_setup = time.perf_counter() - t0
     b = I.rhs(cfg)
     nr = cfg.nrhs
+    kc, kr = min(2, R), min(2, nr)
+    t_all = time.perf_counter()
     t = time.perf_counter()
-    Om = OP.probes(cfg.N, [0, 1], cfg.seed)
-    t_gen2 = time.perf_counter() - t
+    Om = OP.probes(cfg.N, list(range(kc)), cfg.seed)
+    t_gen = time.perf_counter() - t
     t = time.perf_counter()
     S2 = OA.step1_apply(prob, Om)
-    t_probe2 = time.perf_counter() - t
+    t_probe = time.perf_counter() - t
     t = time.perf_counter()
-    bp = OA.resid_apply(prob, b[:, :2])
-    x1 = prob.apply_Zstar(b[:, :2] - prob.apply_A(np.zeros((cfg.N, 2))))
-    t_rhs2 = time.perf_counter() - t
+    OA.resid_apply(prob, b[:, :kr])
+    x2 = Om[:, :1] @ np.ones((1, kr))
+    prob.apply_Zstar(b[:, :kr] - prob.apply_A(x2))
+    t_rhs = time.perf_counter() - t
     rng = np.random.default_rng(0)
     Sfull = rng.standard_normal((S2.shape[0], R))
     t = time.perf_counter()
     np.linalg.svd(Sfull, full_matrices=False)
     t_svd = time.perf_counter() - t
-    est = (R / 2) * (t_gen2 + t_probe2) + (nr / 2) * t_rhs2 + t_svd + (R / 2) * t_gen2
-    sample = (f"oracle (numpy FFT AZ, fp64) on {cfg.name}: 2 probes + 2 RHS + 2 Omega columns + dense SVD "
-              f"{S2.shape[0]}x{R}, scaled to {R} probes and {nr} RHS; measured {t_gen2 + t_probe2 + t_rhs2 + t_svd:.1f} s")
-    return est, sample, t_setup
+    sample_s = time.perf_counter() - t_all
+    est = (R / kc) * (t_gen + t_probe) + (nr / kr) * t_rhs + t_svd + (R / kc) * t_gen
+    desc = (f"O2 (oracle/az.py Alg. 1, numpy FFT operators, fp64 -- a CPU AZ) on {cfg.name}: timed {kc} of {R} "
+            f"probe columns (Philox + (A - A Z* A)), {kr} of {nr} RHS (b' and step 2), {kc} Omega columns and "
+            f"the full-size SVD of a {S2.shape[0]} x {R} sketch ({sample_s:.1f} s); the solve time is ESTIMATED "
+            f"by scaling the per-column parts to {R} probes / {nr} RHS")
+    return est, sample_s, desc
+
+
+def o1_timings(max_seconds=25.0):
+    """The dense O1 oracle (entrywise A + LAPACK SVD-truncated least squares,
+    oracle/az.py tsvd_lsq, multithreaded LAPACK) timed as a whole solve, on c1 and on the largest
+    member of the c2 family that fits the time budget; c4's committed golden run is quoted from its
+    record (tests/golden/c4_o1.npz, made by tests/golden/make_o1_golden.py)."""
+    from oracle import az as OA
+    from oracle import dense as OD
+    out = {}
+    spent = 0.0
+    for cfg in (I.get_config("c1"), I.make_config("interval", 1024, nrhs=64, R=64, seed=1),
+                I.make_config("interval", 2048, nrhs=64, R=64, seed=1),
+                I.make_config("interval", 4096, nrhs=64, R=64, seed=1)):
+        t = time.perf_counter()
+        A = OD.assemble_A(cfg)
+        b = I.rhs(cfg)
+        OA.tsvd_lsq(A, b, cfg.tol)
+        dt = time.perf_counter() - t
+        spent += dt
+        out[cfg.name] = {"s_per_solve": dt, "solves_per_s": 1.0 / dt, "rows": int(A.shape[0]), "cols": int(A.shape[1]),
+                         "nrhs": cfg.nrhs, "measured": True}
+        if spent + 8 * dt > max_seconds:      # the next size costs ~8x (SVD ~ m n^2)
+            break
+    g = os.path.join(ROOT, "tests", "golden", "c4_o1.npz")
+    if os.path.exists(g):
+        d = np.load(g)
+        out["c4"] = {"s_per_solve": float(d["assemble_s"] + d["svd_s"]), "rows": 19632, "cols": 16384,
+                     "measured": "on the build container (tests/golden/c4_o1.npz), not in this run",
+                     "threads": int(d["threads"])}
+    out["c2"] = {"measured": False, "why": "dense A would be 2^20 x 2^20 (8.8 TB), SURVEY.md §8(c) F5"}
+    return out
 
 
 def run_reference(args, cfg):
@@ -169,20 +210,93 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     cores = os.cpu_count()
-    ests = []
-    sample = ""
+    if args.warmup > 0:
+        oracle_sample(cfg, cfg.R)
+    ests, samples = [], []
+    desc = ""
     for _ in range(args.steps):
-        est, sample, _ = oracle_sample(cfg, cfg.R)
+        est, sample_s, desc = oracle_sample(cfg, cfg.R)
         ests.append(est)
+        samples.append(sample_s)
     sec = statistics.mean(ests)
     value = 1.0 / sec
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "steps": args.steps, "warmup": min(args.warmup, 1),
+            "ms_per_step": statistics.mean(samples) * 1e3,
+            "ms_per_step_note": "wall time of one bounded oracle sample (what each step actually ran)",
+            "estimated_ms_per_solve": sec * 1e3, "extrapolated": True,
+            "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "n": cfg.n, "L": cfg.s, "nrhs": cfg.nrhs, "R": cfg.R, "tol": cfg.tol},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                             "extrapolated": True},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# the other BASELINE configs (c1, c3, c4, c5): fewer timed steps, stated per config
+# ------------------------------------------------------------------------------------------
+EXTRA_STEPS = {"c1": (3, 50), "c3": (1, 2), "c4": (1, 3), "c5": (1, 1)}   # (warmup, timed steps)
+
+
+def qr_flops(rows, kp, nrhs):
+    """Householder QR of the rows x kp sketch with nrhs columns carried: 2 rows kp^2 - 2/3 kp^3
+    (the factorisation) + 4 rows kp nrhs (applying the reflectors to b')."""
+    return 2.0 * rows * kp * kp - 2.0 / 3.0 * kp ** 3 + 4.0 * rows * kp * nrhs
+
+
+def measure_config(name, dev, flush):
+    import torch
+    from paper_2308_14490_b200 import api
+    cfg = I.get_config(name)
+    warm, steps = EXTRA_STEPS[name]
+    theta = max(cfg.tol * 1e-2, 1e-12)
+    max_blocks = 4 if cfg.dim == 1 else (16 if cfg.n < 512 else 6)
+    t0 = time.perf_counter()
+    plan = api.Plan.from_config(cfg)
+    plan_s = time.perf_counter() - t0
+    b = api.colmajor(torch.from_numpy(I.rhs(cfg)).to(dev))
+    x = api.empty_colmajor(plan.N, cfg.nrhs, dev)
+    ws = torch.empty(plan.solve_workspace_bytes(cfg.nrhs, cfg.R, max_blocks), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(warm):
+        plan.solve(b, theta, cfg.R, max_blocks, x=x, workspace=ws)
+    torch.cuda.synchronize()
+    clocks = Clocks(dev.index or 0)
+    api.trace_enable(True)
+    ms, reps = [], []
+    for i in range(steps):
+        flush.fill_(i & 0xFF)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, rep = plan.solve(b, theta, cfg.R, max_blocks, x=x, workspace=ws)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        reps.append(rep)
+    trace = api.trace_report()
+    api.trace_enable(False)
+    clk = clocks.stop()
+    rep = reps[-1]
+    mean = sum(ms) / len(ms)
+    qr_ms = sum(v[1] for k, v in trace.items() if k.startswith("qrw_") or k.startswith("tsqr")) / steps
+    svd_ms = sum(v[1] for k, v in trace.items() if k.startswith("bjac") or k == "jacobi_svd") / steps
+    fl = qr_flops(plan.rows, rep["probes"], cfg.nrhs)
+    out = {"solves_per_s": 1000.0 / mean, "ms_per_solve": mean, "steps": steps, "warmup": warm,
+           "max_blocks": max_blocks, "plan_s": plan_s, "probes": rep["probes"], "rank": rep["rank"],
+           "saturated": rep["saturated"], "probe_applies_per_s": rep["probes"] / (rep["ms_sketch"] * 1e-3)
+           if rep["ms_sketch"] else None,
+           "stages_ms": {k: rep[k] for k in ("ms_rhs", "ms_sketch", "ms_qr", "ms_svd", "ms_step2")},
+           "qr": {"ms": qr_ms, "flops": fl, "tflops": fl / (qr_ms * 1e-3) / 1e12 if qr_ms else None,
+                  "frac_fp64": fl / (qr_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS if qr_ms else None},
+           "svd_ms": svd_ms,
+           "top_kernels_ms": {k: round(v[1] / steps, 3) for k, v in sorted(trace.items(), key=lambda kv: -kv[1][1])[:8]},
+           "clocks": clk}
+    del ws, x, b
+    plan.close()
+    torch.cuda.empty_cache()
+    return out
 
 
 # ------------------------------------------------------------------------------------------
@@ -443,8 +557,9 @@ def run_ours(args, cfg):
     value = (1 if args.sharded else world) * 1000.0 / ms_step
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        est, sample, _ = oracle_sample(cfg, cfg.R)
-        cpu = {"value": 1.0 / est, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": sample}
+        est, sample_s, desc = oracle_sample(cfg, cfg.R)
+        cpu = {"value": 1.0 / est, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": desc,
+               "extrapolated": True, "sample_s": sample_s, "o1_dense": o1_timings()}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if args.sharded else "weak",
@@ -472,6 +587,16 @@ def run_ours(args, cfg):
         "gpu_launches": int(launches),
         "clocks": clk,
     }
+    if world == 1 and args.extra_configs:
+        extra = {}
+        del ws
+        torch.cuda.empty_cache()
+        for nm in [c for c in args.extra_configs.split(",") if c]:
+            try:
+                extra[nm] = measure_config(nm, dev, flush)
+            except Exception as exc:      # report, never hide: a failed config is a visible gap
+                extra[nm] = {"error": repr(exc)}
+        line["other_configs"] = extra
     print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
@@ -486,6 +611,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--extra-configs", default="c1,c3,c4,c5",
+                    help="other BASELINE configs timed after the headline (fewer steps, stated); '' = none")
     ap.add_argument("--sharded", action="store_true",
                     help="one solve sharded over the ranks (probe/RHS columns + all-to-all re-block, strong "
                          "scaling) instead of independent replicas (weak scaling)")

@@ -77,3 +77,21 @@ def test_A_row_entries_2d_equals_the_dense_row():
         cols, vals = D.A_row_entries(cfg, tuple(qs[r]))
         order = np.argsort(cols)
         np.testing.assert_allclose(vals[order], A[r][cols[order]], rtol=1e-15, atol=1e-300)
+
+
+def test_c4_o1_golden_is_consistent_with_the_oracle():
+    """The committed dense-O1 golden of c4 (tests/golden/make_o1_golden.py: LAPACK SVD of the
+    entrywise A) against the oracle's independent FFT operator: its stored residual is reproduced,
+    it solves the manufactured problem (u = sin3x cos2y) to the survey's O1 level (3.4e-9,
+    SURVEY.md §8(c) F4), and its truncation rank is the survey's k = 6792 at tol 1e-10."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "c4_o1.npz"))
+    cfg = I.get_config("c4")
+    prob = OA.make_problem(cfg, "fft")
+    b = I.rhs(cfg)
+    res = OA.relative_residual(prob, g["x_tol"], b)
+    assert np.allclose(res, g["res_tol"], rtol=1e-2)
+    assert int(g["k_tol"]) == 6792
+    grid = I.test_grid(cfg)
+    f = OA.evaluate(cfg, g["x_tol"], grid)
+    assert np.max(np.abs(f - grid.exact)) <= 1e-8 * np.max(np.abs(grid.exact))
