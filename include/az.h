@@ -139,6 +139,15 @@ az_status_t az_sketch(az_plan_t plan, int64_t col0, int64_t ncols, double* S, in
 az_status_t az_omega_apply(az_plan_t plan, int64_t col0, int64_t ncols, const double* y, int64_t ldy,
                            int64_t nrhs, double* x, int64_t ldx, int accumulate, void* stream);
 
+/* Steps 2 and 3 of Alg. 1 for a given step-1 solution: x = x2 + Z* (b - A x2).
+ * x2: N x nrhs (ld ldx2), b: (M+Mb) x nrhs (ld ldb), x: N x nrhs (ld ldx), all DEVICE; x must not
+ * alias x2 or b.  Used by multi-GPU drivers for their right-hand-side shard (az_solve does the same
+ * internally).  workspace: az_step2_workspace_size bytes of DEVICE scratch (0 for the 1-D four-step
+ * layout, which runs the correction as one fused five-pass chain).  Asynchronous on stream.       */
+az_status_t az_step2_workspace_size(az_plan_t plan, int64_t nrhs, size_t* bytes);
+az_status_t az_step2(az_plan_t plan, const double* x2, int64_t ldx2, const double* b, int64_t ldb, double* x,
+                     int64_t ldx, int64_t nrhs, void* workspace, size_t ws_bytes, void* stream);
+
 /* R factor of a tall matrix by Householder TSQR (no Q is formed; "SVD of an
  * (r+p)-by-M matrix" done as QR + small SVD).  A: m x k DEVICE column-major (ld lda), k <= 128
  * for the single-pass TSQR; larger k uses blocked Householder (A is overwritten, needs m >= k).

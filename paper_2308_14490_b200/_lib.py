@@ -85,6 +85,8 @@ def lib():
         "az_solve_workspace_size": [P, I64, I64, C.c_int32, C.POINTER(C.c_size_t)],
         "az_solve": [P, P, I64, P, I64, I64, D, I64, C.c_int32, P, C.c_size_t, C.POINTER(SolveReport), P],
         "az_solve_host": [P, P, P, I64, D, I64, C.c_int32, C.POINTER(SolveReport), P],
+        "az_step2_workspace_size": [P, I64, C.POINTER(C.c_size_t)],
+        "az_step2": [P, P, I64, P, I64, P, I64, I64, P, C.c_size_t, P],
     }
     for name, argt in sig.items():
         fn = getattr(L, name)
@@ -110,7 +112,8 @@ EXPORTED = ["az_plan_create", "az_plan_destroy", "az_plan_query", "az_apply_A", 
             "az_solve_workspace_size", "az_solve", "az_solve_host", "az_status_string",
             "az_last_error", "az_launch_count", "az_trace_enable", "az_trace_report",
             "az_factorize", "az_factor_destroy", "az_factor_query", "az_factor_workspace_size",
-            "az_solve_factored", "az_solve_host_pipelined", "az_plan_sync", "az_svd_sweeps_last"]
+            "az_solve_factored", "az_solve_host_pipelined", "az_plan_sync", "az_svd_sweeps_last",
+            "az_step2_workspace_size", "az_step2"]
 
 
 def check(fn: str, status: int, allow=(AZ_OK,)):

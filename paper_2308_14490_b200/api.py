@@ -159,6 +159,24 @@ class Plan:
         _keep(stream, y, out)
         return out
 
+    def step2(self, x2, b, out=None, stream=None):
+        """x = x2 + Z* (b - A x2) (az_step2: steps 2-3 of Alg. 1 for a given step-1 solution)."""
+        p2, ld2, nrhs = _mat(x2)
+        pb, ldb, nb = _mat(b)
+        if nb != nrhs or x2.shape[0] != self.N or b.shape[0] != self.rows:
+            raise ValueError("az_step2: shapes")
+        if out is None:
+            out = empty_colmajor(self.N, nrhs, x2.device) if x2.dim() == 2 else torch.empty(self.N, dtype=torch.float64,
+                                                                                           device=x2.device)
+        px, ldx, _ = _mat(out)
+        need = C.c_size_t()
+        check("az_step2_workspace_size", lib().az_step2_workspace_size(self._h, nrhs, C.byref(need)))
+        ws = torch.empty(max(need.value, 1), dtype=torch.uint8, device=x2.device)
+        check("az_step2", lib().az_step2(self._h, C.c_void_p(p2), ld2, C.c_void_p(pb), ldb, C.c_void_p(px), ldx, nrhs,
+                                         C.c_void_p(ws.data_ptr()), ws.numel(), _stream(stream)))
+        _keep(stream, x2, b, out, ws)
+        return out
+
     # ---------------------------------------------------------------- solve
     def solve_workspace_bytes(self, nrhs: int, R: int, max_blocks: int) -> int:
         b = C.c_size_t()

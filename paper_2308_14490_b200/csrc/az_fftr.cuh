@@ -116,10 +116,16 @@ AZ_D void dftR(cplx (&u)[R]) {
   else dft2<DIR>(u);
 }
 
-// shared-memory padding: one complex slot per 16 keeps the stride-16 writes of a first stage
-// conflict-free (17 lanes apart -> distinct 16-byte bank groups)
-AZ_HD constexpr int pad(int i) { return i + (i >> 4); }
-AZ_HD constexpr int padded_len(int L) { return L + (L >> 4) + 1; }
+// shared-memory padding: one complex slot per E keeps the stride-E writes of a first stage
+// conflict-free.  A 128-bit shared access is served per quarter warp (8 lanes x 16 B = one 128-byte
+// wavefront), so 8 consecutive butterflies must land in 8 distinct 16-byte bank groups: with E
+// values per thread the stride-E write index E j + r becomes (E + 1) j + r -> bank group j + r.
+// (A stride-8 transform padded every 16 would put lanes j, j + 1 in the same group: 2-way.)
+template <int E>
+AZ_HD constexpr int padE(int i) { return i + (i >> (E >= 16 ? 4 : 3)); }
+template <int E>
+AZ_HD constexpr int padded_lenE(int L) { return L + (L >> (E >= 16 ? 4 : 3)) + 1; }
+AZ_HD constexpr int padded_len(int L) { return padded_lenE<16>(L); }
 
 // radix of the stage whose span is NS
 template <int L, int E, int NS>
@@ -178,20 +184,20 @@ AZ_D void stages(cplx (&v)[E], int j, cplx* buf, const cplx* __restrict__ tw, in
       const int k = jj & (NS - 1);
       const int o = (jj / NS) * NS * R + k;
 #pragma unroll
-      for (int r = 0; r < R; ++r) buf[pad(o + r * NS)] = v[b + r * NB];
+      for (int r = 0; r < R; ++r) buf[padE<E>(o + r * NS)] = v[b + r * NB];
     }
     __syncthreads();
 #pragma unroll
     for (int b = 0; b < NB2; ++b) {
       const int jj = j + b * T;
 #pragma unroll
-      for (int r = 0; r < R2; ++r) v[b + r * NB2] = buf[pad(jj + r * (L / R2))];
+      for (int r = 0; r < R2; ++r) v[b + r * NB2] = buf[padE<E>(jj + r * (L / R2))];
     }
     stages<L, E, DIR, NS * R>(v, j, buf, tw, twn);
   }
 }
 
-// All threads of the CTA must call this (it contains __syncthreads).  buf: padded_len(L) complex
+// All threads of the CTA must call this (it contains __syncthreads).  buf: padded_lenE<E>(L) complex
 // values private to this FFT.  tw[t] = e^{-2 pi i t / twn}, twn >= L a power of two.
 template <int L, int E, int DIR>
 AZ_D void fft(cplx (&v)[E], int j, cplx* buf, const cplx* __restrict__ tw, int twn) {

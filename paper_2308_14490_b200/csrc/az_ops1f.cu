@@ -94,6 +94,17 @@ enum { FC_IN_COEF = 0, FC_FINE_MASK = 1, FC_OUT_GATHER = 2, FC_OUT_RESID = 3, FC
 //               Z* junction of step 2 in one pass, no row vector written or read)
 // FC_OUT_COEF_ADD: IFFT_N1 -> x = x2 + (.) / n  (the closing addition of step 2)
 
+// Per-column exchange buffers (complex slots apart): a quarter warp (8 lanes, one 128-byte wavefront
+// of a 128-bit shared access) holds TC adjacent columns x 8 / TC consecutive rows j; consecutive j
+// already fall in consecutive 16-byte bank groups (az_fftr.cuh padE), so the column buffers are
+// offset by 8 / TC groups (an odd number of groups for TC >= 8): all 8 lanes in distinct groups.
+template <int NC, int TC, int EC>
+AZ_HD constexpr int col_stride() {
+  constexpr int base = fftr::padded_lenE<EC>(NC) - 1;
+  constexpr int want = TC >= 8 ? 1 : 8 / TC;
+  return base + ((want - base % 8) % 8 + 8) % 8;
+}
+
 // EC = values per thread in the column FFTs (16: fewer exchanges; 8: half the registers, more
 // resident warps); MINB = CTAs per SM the register budget is sized for.
 template <int NC, int TC, int KIND, int SRC, int EC, int MINB>
@@ -110,7 +121,7 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
   cplx* C1b = (KIND == FC_OUT_Z) ? a.Z2 + (int64_t)b * a.n : a.C1 + (int64_t)b * a.n;
   cplx* Gb = a.G + (int64_t)b * a.L;
   const int64_t tmul = coef ? a.s : 1;                 // e^{-2 pi i n2 k1 / n} = e^{-2 pi i (s n2 k1) / L}
-  cplx* buf = sm + c * fftr::padded_len(NC);
+  cplx* buf = sm + c * col_stride<NC, TC, EC>();
   cplx v[EC];
 
   // ---- load (element e: row j + e T) ----
@@ -235,6 +246,12 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
 // spectrum (k2 = j + e T) and its alias k2 + NR2 (element e + 8 of the fine spectrum) are in the
 // same thread: fold, expand, the symbol multiply and the v^ - w^ update are all thread-local.
 // ------------------------------------------------------------------------------------------
+template <int NR2, int LR2, int EL>
+AZ_HD constexpr int row_buf() {
+  return fftr::padded_lenE<EL>(LR2) > fftr::padded_lenE<EL / 2>(NR2) ? fftr::padded_lenE<EL>(LR2)
+                                                                      : fftr::padded_lenE<EL / 2>(NR2);
+}
+
 enum { FR_EXPAND = 0, FR_EXPAND_KEEP = 1, FR_STEP1 = 2, FR_RESID = 3, FR_ZSTAR = 4, FR_AT = 5 };
 
 template <int NR2, int LR2, int RPC, int KIND, int EL, int MINB>
@@ -247,7 +264,9 @@ __global__ void __launch_bounds__(RPC * (LR2 / EL), MINB) k1f_rows(P1f a, int nr
   const int k1 = blockIdx.x * RPC + f;
   const bool live = k1 < nrows;
   const int b = blockIdx.y;
-  cplx* buf = sm + f * fftr::padded_len(LR2);
+  // one buffer serves the length-LR2 (EL values per thread) and length-NR2 (EN) transforms
+  constexpr int PB = row_buf<NR2, LR2, EL>();
+  cplx* buf = sm + f * PB;
   cplx* C1b = a.C1 + (int64_t)b * a.n;
   cplx* Gb = a.G + (int64_t)b * a.L;
   const double invL = 1.0 / (double)a.L;
@@ -259,7 +278,7 @@ __global__ void __launch_bounds__(RPC * (LR2 / EL), MINB) k1f_rows(P1f a, int nr
   // start, so their DRAM latency overlaps the first transform instead of stalling the fold
   constexpr bool NEED_Z = (KIND == FR_STEP1 || KIND == FR_RESID || KIND == FR_ZSTAR);
   constexpr bool NEED_C = (KIND == FR_STEP1);
-  double* pre = reinterpret_cast<double*>(sm + RPC * fftr::padded_len(LR2)) + f * (LR2 + 3 * NR2);
+  double* pre = reinterpret_cast<double*>(sm + RPC * PB) + f * (LR2 + 3 * NR2);
   double* Ws = pre;                 // LR2 real symbol values of the row
   double* Zs = pre + LR2;           // NR2 values of 1/sigma^2
   cplx* Cs = reinterpret_cast<cplx*>(pre + LR2 + NR2);   // NR2 values of v^
@@ -378,7 +397,7 @@ static az_status_t fcols_e(const P1f& a, int ncols, int nb, double cout, cudaStr
   constexpr int T = NC / EC;
   constexpr int TC0 = (MINB == 1 ? 512 : 256) / T;
   constexpr int TC = TC0 < 2 ? 2 : (TC0 > 16 ? 16 : TC0);
-  const size_t sm = (size_t)TC * fftr::padded_len(NC) * sizeof(cplx);
+  const size_t sm = (size_t)TC * col_stride<NC, TC, EC>() * sizeof(cplx);
   auto kern = k1f_cols<NC, TC, KIND, SRC, EC, MINB>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   static const char* names[] = {"1f_cols_in_coef", "1f_cols_fine_mask", "1f_cols_out_gather", "1f_cols_out_resid",
@@ -403,7 +422,7 @@ static az_status_t frows_e(const P1f& a, int nb, cudaStream_t st) {
   constexpr int T = LR2 / EL;
   constexpr int RPC0 = 128 / T;
   constexpr int RPC = RPC0 < 1 ? 1 : (RPC0 > 64 ? 64 : RPC0);
-  const size_t sm = (size_t)RPC * (fftr::padded_len(LR2) * sizeof(cplx) + (LR2 + 3 * NR2) * sizeof(double));
+  const size_t sm = (size_t)RPC * (row_buf<NR2, LR2, EL>() * sizeof(cplx) + (LR2 + 3 * NR2) * sizeof(double));
   auto kern = k1f_rows<NR2, LR2, RPC, KIND, EL, MINB>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   static const char* names[] = {"1f_rows_expand", "1f_rows_expand_keep", "1f_rows_step1", "1f_rows_resid",

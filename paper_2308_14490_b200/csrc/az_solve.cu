@@ -300,10 +300,11 @@ az_status_t az_apply_op(az_plan_s* p, int op, const double* in, int64_t ldin, do
 // Step 2 + 3 of Alg. 1: x = x2 + Z* (b - A x2).  Four-step layout: one fused
 // five-pass chain (az1f_step2); otherwise A, b - A x2, Z*, + x2.  tmp: (M + Mb) x nrhs scratch.
 static az_status_t step2(az_plan_s* p, const double* x2, const double* b, int64_t ldb, double* x, int64_t ldx,
-                         double* tmp, int64_t nrhs, cudaStream_t st) {
-  if (p->layout == AZ_LAYOUT_1D_FOURSTEP) return az1f_step2(p, x2, p->N, b, ldb, x, ldx, nrhs, st);
+                         double* tmp, int64_t nrhs, cudaStream_t st, int64_t ldx2 = 0) {
+  if (!ldx2) ldx2 = p->N;
+  if (p->layout == AZ_LAYOUT_1D_FOURSTEP) return az1f_step2(p, x2, ldx2, b, ldb, x, ldx, nrhs, st);
   const int64_t rows = p->M + p->Mb;
-  AZ_TRY(az_apply_op(p, OP_A, x2, p->N, tmp, rows, nrhs, st));
+  AZ_TRY(az_apply_op(p, OP_A, x2, ldx2, tmp, rows, nrhs, st));
   {
     AzTrace tr("elementwise", st);
     k_sub_cols<<<az_div_up(rows * nrhs, 256), 256, 0, st>>>(b, ldb, tmp, rows, rows, nrhs);
@@ -312,10 +313,35 @@ static az_status_t step2(az_plan_s* p, const double* x2, const double* b, int64_
   AZ_TRY(az_apply_op(p, OP_ZSTAR, tmp, rows, x, ldx, nrhs, st));
   {
     AzTrace tr("elementwise", st);
-    k_add_cols<<<az_div_up(p->N * nrhs, 256), 256, 0, st>>>(x2, p->N, x, ldx, p->N, nrhs);
+    k_add_cols<<<az_div_up(p->N * nrhs, 256), 256, 0, st>>>(x2, ldx2, x, ldx, p->N, nrhs);
   }
   AZ_LAUNCH_CHECK();
   return AZ_OK;
+}
+
+extern "C" az_status_t az_step2_workspace_size(az_plan_t p, int64_t nrhs, size_t* bytes) {
+  if (!p || !bytes || nrhs < 0) {
+    az_set_error("az_step2_workspace_size: bad arguments");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  *bytes = p->layout == AZ_LAYOUT_1D_FOURSTEP ? 0 : sizeof(double) * (size_t)(p->M + p->Mb) * (size_t)nrhs;
+  return AZ_OK;
+}
+
+extern "C" az_status_t az_step2(az_plan_t p, const double* x2, int64_t ldx2, const double* b, int64_t ldb, double* x,
+                                int64_t ldx, int64_t nrhs, void* workspace, size_t ws_bytes, void* stream) {
+  size_t need = 0;
+  if (!p || nrhs < 0 || (nrhs > 0 && (!x2 || !b || !x)) || ldx2 < p->N || ldb < p->M + p->Mb || ldx < p->N ||
+      az_step2_workspace_size(p, nrhs, &need) != AZ_OK) {
+    az_set_error("az_step2: bad arguments");
+    return AZ_ERR_INVALID_ARGUMENT;
+  }
+  if (nrhs == 0) return AZ_OK;
+  if (ws_bytes < need || (need && !workspace)) {
+    az_set_error("az_step2: workspace too small (%zu < %zu)", ws_bytes, need);
+    return AZ_ERR_WORKSPACE;
+  }
+  return step2(p, x2, b, ldb, x, ldx, (double*)workspace, nrhs, (cudaStream_t)stream, ldx2);
 }
 
 __global__ void k_flag_saturated(const int64_t* rank, int64_t limit, int* flag) {

@@ -1,33 +1,52 @@
 """Multi-GPU AZ solve: probe columns and right-hand sides sharded over ranks.
 
-One process per GPU; torch.distributed (NCCL on GPUs) is the plumbing, every arithmetic step runs
+One process per GPU; torch.distributed (NCCL on GPUs) moves the data, every arithmetic step runs
 in libaz through the `Ops` adapter (GpuOps).  Steps (Alg. 1):
 
   1. rank g computes b' = (I - A Z*) b for its share of the right-hand-side columns and the sketch
-     S = (A - A Z* A) Omega for its share of the probe columns (Philox keyed by the GLOBAL column, so
-     the probes are the single-GPU ones): no communication (a1-a6 of SURVEY.md §8(a));
-  2. all-to-all re-block: the column-sharded [S | b'] becomes G row blocks (the exchange step);
-  3. local TSQR of each row block -> [R_g | c_g] (k1 x k, az_qr_r_partial), all-gather of these
-     small factors, and a second TSQR of the stacked factors on every rank -> [R_S | Q^T b'];
+     S = (A - A Z* A) Omega for its share of each new probe block (Philox keyed by the GLOBAL
+     column, so the probes are the single-GPU ones): no communication (a1-a6 of SURVEY.md §8(a));
+  2. all-to-all re-block of the NEW columns only: the column-sharded block becomes row blocks
+     appended to the rank's rows of the earlier blocks (the exchange step);
+  3. TSQR over a FIXED tree: the rows are cut into NLEAF leaves whatever the world size (rank g owns
+     NLEAF/G consecutive leaves), each leaf gives [R_l | c_l] (k1 x k, az_qr_r_partial), the NLEAF
+     factors are all-gathered and stacked in leaf order, and one more az_qr_r_partial merges them
+     into [R_S | Q^T b'] on every rank;
   4. truncated SVD solve y = V_k Sigma_k^-1 U_k^T (Q^T b') on every rank (identical inputs, so
      identical results; no broadcast needed);
-  5. x2 = Omega y and the step-2 correction x = x2 + Z*(b - A x2) for the rank's right-hand-side
-     columns, then all-gather of x (b and x are replicated on every rank).
+  5. x2 = Omega y and the step-2 correction x = x2 + Z*(b - A x2) (az_omega_apply, az_step2) for the
+     rank's right-hand-side columns, then all-gather of x (b and x are replicated).
+
+Shards of probe and right-hand-side columns are aligned to column PAIRS: libaz packs two real
+columns into one complex FFT vector, so a column's rounding depends on its partner; pair-aligned
+shards give every column the same partner at every world size.  With the fixed leaf tree, every
+operation then sees the same operands at G = 1, 2, 4, 8 and x is bitwise identical across G
+(SURVEY.md §4 "bitwise-identical across G"; H6).
 
 The orchestration is backend-agnostic (duck-typed `ops`), so the host logic (shard ranges, the
-re-blocking, the factor merge) is tested on CPU with the gloo backend at world size 2.
+re-blocking, the fixed tree, the determinism across G) is tested on CPU with the gloo backend at
+world sizes 1, 2 and 4 (tests/test_dist.py).
 """
 from __future__ import annotations
 
-from typing import List, Optional, Tuple
+from typing import List, Tuple
 
 import torch
 import torch.distributed as dist
+
+NLEAF = 8     # leaves of the TSQR tree, independent of the world size (G must divide it)
 
 
 def split(n: int, parts: int) -> List[int]:
     """Balanced contiguous partition of range(n): boundaries b[0] = 0 <= ... <= b[parts] = n."""
     return [(n * g) // parts for g in range(parts + 1)]
+
+
+def split_pairs(n: int, parts: int) -> List[int]:
+    """Partition of range(n) into `parts` contiguous runs whose boundaries fall on even columns
+    (a column and its complex-packing partner 2p, 2p + 1 stay on one rank)."""
+    npairs = (n + 1) // 2
+    return [min(n, 2 * b) for b in split(npairs, parts)]
 
 
 def colmajor_empty(rows: int, cols: int, like: torch.Tensor) -> torch.Tensor:
@@ -39,10 +58,9 @@ def reblock(local: torch.Tensor, col_owner: List[Tuple[int, int, int]], k: int, 
     """Column-sharded -> row-blocked.
 
     local: (rows x c_me) column-major, this rank's columns in the order listed for it in col_owner.
-    col_owner: for every rank g, a list of (global column, ...) is given as runs (g, c0, c1): rank g's
-               local columns j = 0.. map to global columns c0..c1-1 of its runs, runs concatenated
-               in list order.
-    Returns this rank's row block (rows_me x k) column-major, columns in global order.
+    col_owner: runs (g, c0, c1): rank g's local columns j = 0.. map to columns c0..c1-1 of the
+               result (0 <= c < k), runs concatenated in list order.
+    Returns this rank's row block (rows_me x k) column-major.
     """
     G = dist.get_world_size(group)
     me = dist.get_rank(group)
@@ -75,72 +93,72 @@ def reblock(local: torch.Tensor, col_owner: List[Tuple[int, int, int]], k: int, 
 
 
 def solve_sharded(ops, b: torch.Tensor, theta: float, R: int, max_blocks: int = 1, p_over: int = 10,
-                  group=None) -> Tuple[torch.Tensor, dict]:
+                  group=None, nleaf: int = NLEAF) -> Tuple[torch.Tensor, dict]:
     """Distributed AZ solve; b: rows x nrhs column-major, replicated on every rank.  Returns x
     (N x nrhs, replicated) and a report {rank, probes, saturated}.  Collective over `group`."""
     G = dist.get_world_size(group)
     me = dist.get_rank(group)
+    if nleaf % G:
+        raise ValueError(f"world size {G} must divide the {nleaf} leaves of the TSQR tree")
     rows, N = ops.rows, ops.N
     nrhs = b.shape[1]
-    qs = split(nrhs, G)
+    qs = split_pairs(nrhs, G)
     q0, q1 = qs[me], qs[me + 1]
-    bp = ops.resid(b[:, q0:q1]) if q1 > q0 else None       # my b' columns
-    row_splits = split(rows, G)
+    bp = ops.resid(b[:, q0:q1]) if q1 > q0 else colmajor_empty(rows, 0, b)   # my b' columns
+    leaves = split(rows, nleaf)
+    lpr = nleaf // G                                          # leaves per rank
+    row_splits = [leaves[g * lpr] for g in range(G + 1)]
+    r_lo = row_splits[me]
+    # right-hand sides re-blocked once: my rows of b'
+    owner_b = [(g, qs[g], qs[g + 1]) for g in range(G) if qs[g + 1] > qs[g]]
+    Bme = reblock(bp, owner_b, nrhs, row_splits, group)      # rows_me x nrhs
+    Sme = colmajor_empty(row_splits[me + 1] - r_lo, 0, b)    # my rows of the probe columns so far
     rank_k, kp, y = 0, 0, None
     saturated = False
     for nb in range(1, max_blocks + 1):
+        c0 = (nb - 1) * R                                    # the new block's global probe columns
         kp = nb * R
         k = kp + nrhs
-        ps = split(kp, G)
+        ps = split_pairs(R, G)
         p0, p1 = ps[me], ps[me + 1]
-        parts = []
-        if p1 > p0:
-            parts.append(ops.sketch(p0, p1 - p0))
-        if bp is not None:
-            parts.append(bp)
-        if parts:
-            local = parts[0] if len(parts) == 1 else torch.cat([t.t() for t in parts]).t()
-        else:
-            local = colmajor_empty(rows, 0, b)
-        owner = []
-        for g in range(G):
-            if ps[g + 1] > ps[g]:
-                owner.append((g, ps[g], ps[g + 1]))
-            if qs[g + 1] > qs[g]:
-                owner.append((g, kp + qs[g], kp + qs[g + 1]))
-        A = reblock(local, owner, k, row_splits, group)
-        Rg = ops.qr_partial(A, kp)                               # kp x k
-        Rg = Rg.t().contiguous()                                 # k x kp row-major == Rg column-major, packed
-        gathered = [torch.empty_like(Rg) for _ in range(G)]
-        dist.all_gather(gathered, Rg, group=group)
-        # stack the G factors by rows: (G kp) x k column-major
-        stacked = colmajor_empty(G * kp, k, b)
-        for g in range(G):
-            stacked[g * kp:(g + 1) * kp, :] = gathered[g].t()
-        Rf = ops.qr_partial(stacked, kp)                        # [R_S | Q^T b'] (kp x k)
+        new = ops.sketch(c0 + p0, p1 - p0) if p1 > p0 else colmajor_empty(rows, 0, b)
+        owner = [(g, ps[g], ps[g + 1]) for g in range(G) if ps[g + 1] > ps[g]]
+        Snew = reblock(new, owner, R, row_splits, group)     # rows_me x R
+        # my rows of [S | b'] (rows_me x k): earlier blocks, the new block, b'
+        Sme = torch.cat([Sme.t(), Snew.t()]).t() if Sme.shape[1] else Snew
+        Ame = torch.cat([Sme.t(), Bme.t()]).t()
+        mine = []
+        for leaf in range(me * lpr, (me + 1) * lpr):
+            a0, a1 = leaves[leaf] - r_lo, leaves[leaf + 1] - r_lo
+            mine.append(ops.qr_partial(Ame[a0:a1].clone(), kp))   # kp x k; az_qr_r_partial overwrites its input
+        packed = torch.cat([f.t().contiguous().reshape(-1) for f in mine])   # lpr factors, each k x kp row-major
+        gathered = torch.empty(G * packed.numel(), dtype=packed.dtype, device=packed.device)
+        dist.all_gather_into_tensor(gathered, packed, group=group)
+        # stack the nleaf factors by rows, in leaf order: (nleaf kp) x k column-major
+        stacked = colmajor_empty(nleaf * kp, k, b)
+        fac = gathered.view(nleaf, k, kp)
+        for leaf in range(nleaf):
+            stacked[leaf * kp:(leaf + 1) * kp, :] = fac[leaf].t()
+        Rf = ops.qr_partial(stacked, kp)                     # [R_S | Q^T b'] (kp x k)
         y, _, rank_k = ops.tsvd(Rf, kp, nrhs, theta)
         saturated = rank_k > kp - p_over
         if not saturated:
             break
-    # x2 = Omega y and step 2 for my right-hand sides
-    xs = None
-    if q1 > q0:
-        x2 = ops.omega_apply(0, y[:, q0:q1])
-        r = ops.apply_A(x2)
-        r = b[:, q0:q1] - r
-        xs = x2 + ops.apply_Zstar(ops.contig(r))
-    # all-gather the x columns (pad to the largest share)
+    # x2 = Omega y and steps 2-3 (az_step2) for my right-hand sides, all in libaz
     qmax = max(qs[g + 1] - qs[g] for g in range(G))
     buf = torch.zeros((qmax, N), dtype=torch.float64, device=b.device)
-    if xs is not None:
+    if q1 > q0:
+        x2 = ops.omega_apply(0, y[:, q0:q1])
+        xs = ops.step2(x2, b[:, q0:q1])
         buf[:q1 - q0] = xs.t()
-    allx = [torch.empty_like(buf) for _ in range(G)]
-    dist.all_gather(allx, buf, group=group)
+    # all-gather the x columns (padded to the largest share)
+    allx = torch.empty((G * qmax, N), dtype=torch.float64, device=b.device)
+    dist.all_gather_into_tensor(allx, buf, group=group)
     x = colmajor_empty(N, nrhs, b)
     for g in range(G):
         c = qs[g + 1] - qs[g]
         if c:
-            x[:, qs[g]:qs[g + 1]] = allx[g][:c].t()
+            x[:, qs[g]:qs[g + 1]] = allx[g * qmax:g * qmax + c].t()
     return x, {"rank": int(rank_k), "probes": int(kp), "saturated": bool(saturated)}
 
 
@@ -165,13 +183,13 @@ class GpuOps:
     def qr_partial(self, A, k1):
         from .api import qr_r, qr_r_partial
         A = self.contig(A)
-        if A.shape[1] <= 128:
-            return qr_r_partial(A, k1)
-        if A.shape[0] < A.shape[1]:     # the blocked path needs m >= k: zero rows leave R unchanged
+        if A.shape[0] < A.shape[1]:     # fewer rows than columns (a small leaf): zero rows leave R unchanged
             Z = colmajor_empty(A.shape[1], A.shape[1], A)
             Z.zero_()
             Z[:A.shape[0]] = A
             A = Z
+        if A.shape[1] <= 128:
+            return qr_r_partial(A, k1)
         return qr_r(A)[:k1]
 
     def tsvd(self, Rf, r, nrhs, theta):
@@ -181,8 +199,5 @@ class GpuOps:
     def omega_apply(self, col0, y):
         return self.plan.omega_apply(col0, self.contig(y))
 
-    def apply_A(self, x):
-        return self.plan.apply_A(self.contig(x))
-
-    def apply_Zstar(self, y):
-        return self.plan.apply_Zstar(self.contig(y))
+    def step2(self, x2, b):
+        return self.plan.step2(self.contig(x2), self.contig(b))

@@ -88,7 +88,10 @@ def _achieved(record, cfg, kind, y, ref):
     key = kind if kind in ("A", "Zstar") else f"K{cfg.dim}"
     bar = TIGHT[key]
     record(case=cfg.name, op=kind, achieved=float(err), bar=bar)
-    if cfg.eps_h == 0.5:
+    # the whole periodic box makes A - A Z* A and I - A Z* vanish (their output is rounding noise, a
+    # relative error is meaningless there: test_box_step1_operator_vanishes holds those cases)
+    degenerate = cfg.domain == "box" and kind not in ("A", "Zstar")
+    if cfg.eps_h == 0.5 and not degenerate:
         assert err <= bar, (kind, err, bar)
     return err
 
