@@ -153,3 +153,40 @@ inline cudaError_t az_smem_attr(K kernel, size_t bytes) {
     az_status_t _s = (__VA_ARGS__);                                            \
     if (_s != AZ_OK) return _s;                                                \
   } while (0)
+
+// --------------------------------------------------------------------------------------
+// Bulk asynchronous copies (the TMA engine's 1-D form, cp.async.bulk -> SASS UBLKCP) into shared
+// memory, completion tracked by an mbarrier's transaction count.  Addresses and sizes must be
+// multiples of 16 bytes.
+// --------------------------------------------------------------------------------------
+namespace bulk {
+AZ_D uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+AZ_D void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count));
+}
+// make the initialised barriers visible to the async proxy (the copy engine)
+AZ_D void fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::); }
+// order this thread's earlier generic-proxy shared-memory accesses before later async-proxy writes
+AZ_D void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::); }
+AZ_D void arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+AZ_D void copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+AZ_D void wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+}  // namespace bulk

@@ -370,6 +370,162 @@ __global__ void __launch_bounds__(RPC * (LR2 / EL), MINB) k1f_rows(P1f a, int nr
 }
 
 // ------------------------------------------------------------------------------------------
+// Persistent row passes (default; AZ_ROWS_PERSIST=0 selects k1f_rows): a CTA owns one row k1 and
+// walks a contiguous range of the batch's vector pairs (grid.y splits the pairs).  The row's symbol
+// and 1/sigma^2 tables come in once per CTA instead of once per pair, and the NEXT pair's input row
+// is in flight -- a bulk asynchronous copy (cp.async.bulk, the TMA engine's 1-D form) into a
+// shared-memory stage tracked by an mbarrier -- while the current pair is transformed, so the HBM
+// latency that stalled the one-pair CTAs (ncu: 35-39 % of their warp samples on long-scoreboard
+// waits) overlaps the FFTs.  The step-1 pass's v^ row has its own stage, requested at the start of
+// the pair and waited for only at the fold.  Same arithmetic, in the same order, as k1f_rows.
+// ------------------------------------------------------------------------------------------
+template <int NR2, int LR2, int KIND>
+struct RowsP {
+  static constexpr int EL = 16, EN = 8, T = LR2 / EL;
+  static constexpr bool IN_FINE = !(KIND == FR_EXPAND || KIND == FR_EXPAND_KEEP);
+  static constexpr int INLEN = IN_FINE ? LR2 : NR2;     // complex values of the input row
+  static constexpr bool NEED_Z = (KIND == FR_STEP1 || KIND == FR_RESID || KIND == FR_ZSTAR);
+  static constexpr bool NEED_C = (KIND == FR_STEP1);
+  static constexpr int PB = row_buf<NR2, LR2, EL>();
+  // [3 mbarriers, 64 B][W row: LR2 doubles][1/sigma^2 row: NR2 doubles][v^ row: NR2 complex if NEED_C]
+  // [input stage: INLEN complex][exchange buffer: PB complex]
+  static constexpr size_t smem = 64 + sizeof(double) * (LR2 + NR2) + sizeof(cplx) * ((NEED_C ? NR2 : 0) + INLEN + PB);
+};
+
+template <int NR2, int LR2, int KIND>
+__global__ void __launch_bounds__(LR2 / 16, 2) k1f_rows_p(P1f a, int npairs, int pgroups) {
+  using C = RowsP<NR2, LR2, KIND>;
+  constexpr int EL = C::EL, EN = C::EN, T = C::T, INLEN = C::INLEN;
+  static_assert(LR2 == 2 * NR2, "four-step rows: L = 2 only");
+  extern __shared__ __align__(128) unsigned char smraw[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smraw);   // 0: tables, 1: input stage, 2: v^ row
+  double* Ws = reinterpret_cast<double*>(smraw + 64);
+  double* Zs = Ws + LR2;
+  cplx* Cs = reinterpret_cast<cplx*>(Zs + NR2);
+  cplx* stage = Cs + (C::NEED_C ? NR2 : 0);
+  cplx* buf = stage + INLEN;
+  const int j = threadIdx.x;
+  const int k1 = blockIdx.x;
+  const int b0 = (int)(((int64_t)npairs * blockIdx.y) / pgroups);
+  const int b1 = (int)(((int64_t)npairs * (blockIdx.y + 1)) / pgroups);
+  const int64_t rowW = (int64_t)k1 * LR2, rowC = (int64_t)k1 * NR2;
+  const double invL = 1.0 / (double)a.L;
+  auto in_row = [&](int b) -> const cplx* {
+    return C::IN_FINE ? a.G + (int64_t)b * a.L + rowW : a.C1 + (int64_t)b * a.n + rowC;
+  };
+  if (j == 0) {
+    bulk::mbar_init(&bars[0], 1);
+    bulk::mbar_init(&bars[1], 1);
+    bulk::mbar_init(&bars[2], 1);
+    bulk::fence_init();
+  }
+  __syncthreads();
+  if (j == 0 && b0 < b1) {
+    bulk::arrive_expect_tx(&bars[0], (uint32_t)(sizeof(double) * (LR2 + (C::NEED_Z ? NR2 : 0))));
+    bulk::copy_g2s(Ws, a.Wr + rowW, sizeof(double) * LR2, &bars[0]);
+    if constexpr (C::NEED_Z) bulk::copy_g2s(Zs, a.zinv + rowC, sizeof(double) * NR2, &bars[0]);
+    bulk::arrive_expect_tx(&bars[1], sizeof(cplx) * INLEN);
+    bulk::copy_g2s(stage, in_row(b0), sizeof(cplx) * INLEN, &bars[1]);
+  }
+  uint32_t ph_in = 0, ph_c = 0;
+  bool tables = false;
+  for (int b = b0; b < b1; ++b) {
+    cplx* C1b = a.C1 + (int64_t)b * a.n;
+    cplx* Gb = a.G + (int64_t)b * a.L;
+    cplx vn[EN];
+    cplx vl[EL];
+    bulk::wait(&bars[1], ph_in);
+    ph_in ^= 1;
+    if constexpr (C::IN_FINE) {
+#pragma unroll
+      for (int e = 0; e < EL; ++e) vl[e] = stage[j + e * T];
+    } else {
+#pragma unroll
+      for (int e = 0; e < EN; ++e) vn[e] = stage[j + e * T];
+    }
+    __syncthreads();   // every thread holds its input: the stage (and the v^ row) may be refilled
+    if (j == 0) {
+      bulk::fence_proxy_async();
+      if (b + 1 < b1) {
+        bulk::arrive_expect_tx(&bars[1], sizeof(cplx) * INLEN);
+        bulk::copy_g2s(stage, in_row(b + 1), sizeof(cplx) * INLEN, &bars[1]);
+      }
+      if constexpr (C::NEED_C) {
+        bulk::arrive_expect_tx(&bars[2], sizeof(cplx) * NR2);
+        bulk::copy_g2s(Cs, C1b + rowC, sizeof(cplx) * NR2, &bars[2]);
+      }
+    }
+    if constexpr (KIND == FR_EXPAND || KIND == FR_EXPAND_KEEP) {
+      fftr::fft<NR2, EN, -1>(vn, j, buf, a.tw, TWN);
+      if constexpr (KIND == FR_EXPAND_KEEP) {
+#pragma unroll
+        for (int e = 0; e < EN; ++e) C1b[rowC + j + e * T] = vn[e];
+      }
+      if (!tables) {
+        bulk::wait(&bars[0], 0);
+        tables = true;
+      }
+    } else {
+      fftr::fft<LR2, EL, -1>(vl, j, buf, a.tw, TWN);
+      if (!tables) {
+        bulk::wait(&bars[0], 0);
+        tables = true;
+      }
+#pragma unroll
+      for (int e = 0; e < EN; ++e) {
+        const int k2 = j + e * T;
+        cplx acc = cadd(cscale(vl[e], Ws[k2]), cscale(vl[e + EN], Ws[k2 + NR2]));
+        if constexpr (KIND != FR_AT) acc = cscale(acc, Zs[k2]);
+        vn[e] = acc;
+      }
+      if constexpr (KIND == FR_STEP1) {   // r^ = v^ - w^  (the spectrum of M = v - Z* A v)
+        bulk::wait(&bars[2], ph_c);
+        ph_c ^= 1;
+#pragma unroll
+        for (int e = 0; e < EN; ++e) vn[e] = csub(Cs[j + e * T], vn[e]);
+      }
+      if constexpr (KIND == FR_STEP1 || KIND == FR_RESID) {
+        if (a.Z2) {   // r^ (STEP1) or w^ (RESID) on to the coefficient side: IFFT_N2 + twiddle
+          cplx wz[EN];
+#pragma unroll
+          for (int e = 0; e < EN; ++e) wz[e] = vn[e];
+          fftr::fft<NR2, EN, 1>(wz, j, buf, a.tw, TWN);
+          cplx* Zb = a.Z2 + (int64_t)b * a.n;
+          cplx w = tw4<1>(a, ((int64_t)j * k1 * 2) & (a.L - 1));
+          const cplx ws = tw4<1>(a, ((int64_t)T * k1 * 2) & (a.L - 1));
+#pragma unroll
+          for (int e = 0; e < EN; ++e) {
+            Zb[rowC + j + e * T] = cmul(wz[e], w);
+            w = cmul(w, ws);
+          }
+        }
+      }
+    }
+    if constexpr (KIND == FR_ZSTAR || KIND == FR_AT) {
+      fftr::fft<NR2, EN, 1>(vn, j, buf, a.tw, TWN);
+      cplx w = tw4<1>(a, ((int64_t)j * k1 * 2) & (a.L - 1));
+      const cplx ws = tw4<1>(a, ((int64_t)T * k1 * 2) & (a.L - 1));
+#pragma unroll
+      for (int e = 0; e < EN; ++e) {
+        C1b[rowC + j + e * T] = cmul(vn[e], w);
+        w = cmul(w, ws);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < EL; ++e) vl[e] = cscale(vn[e & (EN - 1)], Ws[j + e * T] * invL);
+      fftr::fft<LR2, EL, 1>(vl, j, buf, a.tw, TWN);
+      cplx w = tw4<1>(a, ((int64_t)j * k1) & (a.L - 1));
+      const cplx ws = tw4<1>(a, ((int64_t)T * k1) & (a.L - 1));
+#pragma unroll
+      for (int e = 0; e < EL; ++e) {
+        Gb[rowW + j + e * T] = cmul(vl[e], w);
+        w = cmul(w, ws);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // host orchestration
 // ------------------------------------------------------------------------------------------
 static int fft_e() {   // tuning knob: AZ_FFT_E=8 (8 values per thread), 17 (16 values, 8 columns per CTA)
@@ -433,9 +589,47 @@ static az_status_t frows_e(const P1f& a, int nb, cudaStream_t st) {
   return AZ_OK;
 }
 
+static bool rows_persist() {   // AZ_ROWS_PERSIST=0: one CTA per (row, pair), no prefetch (k1f_rows)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AZ_ROWS_PERSIST");
+    v = (e && *e == '0') ? 0 : 1;
+  }
+  return v != 0;
+}
+
+template <int NR2, int KIND>
+static az_status_t frows_p(const P1f& a, int nb, cudaStream_t st) {
+  constexpr int LR2 = 2 * NR2;
+  using C = RowsP<NR2, LR2, KIND>;
+  auto kern = k1f_rows_p<NR2, LR2, KIND>;
+  AZ_CUDA_CHECK(az_smem_attr(kern, C::smem));
+  static int resident = 0;   // CTAs the GPU holds at once (2 per SM by the launch bound / shared memory)
+  if (!resident) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, C::T, C::smem) != cudaSuccess || per < 1) {
+      cudaGetLastError();
+      per = 1;
+    }
+    resident = per * sms;
+  }
+  // split the pairs so that the grid is >= 4 waves (tails) while each CTA still walks several pairs
+  const int pg = std::max(1, std::min(nb, (4 * resident + a.N1 - 1) / a.N1));
+  static const char* names[] = {"1f_rows_expand", "1f_rows_expand_keep", "1f_rows_step1", "1f_rows_resid",
+                                "1f_rows_zstar", "1f_rows_at"};
+  AzTrace tr(names[KIND], st, nb);
+  kern<<<dim3(a.N1, pg), C::T, C::smem, st>>>(a, nb, pg);
+  AZ_LAUNCH_CHECK();
+  return AZ_OK;
+}
+
 template <int NR2, int KIND>
 static az_status_t frows(const P1f& a, int nb, cudaStream_t st) {
   if (fft_er() == 8) return frows_e<NR2, KIND, 8, 3>(a, nb, st);
+  // the persistent form needs 16-byte aligned rows of at least 16 values (NR2 >= 64 here)
+  if (rows_persist() && NR2 >= 64) return frows_p<NR2, KIND>(a, nb, st);
   return frows_e<NR2, KIND, 16, 3>(a, nb, st);
 }
 
