@@ -141,11 +141,21 @@ void az_set_error(const char* fmt, ...);
     }                                                                          \
   } while (0)
 
-// Opt a kernel into > 48 KB of dynamic shared memory (idempotent, cheap).
+// Opt a kernel into > 48 KB of dynamic shared memory (idempotent).  The attribute call is made once
+// per (kernel, size): it is a driver round trip, and the small solves (c1) are host-latency bound.
 template <class K>
 inline cudaError_t az_smem_attr(K kernel, size_t bytes) {
   if (bytes <= 48 * 1024) return cudaSuccess;
-  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  static thread_local const void* last_k[64];
+  static thread_local size_t last_b[64];
+  const size_t h = (((size_t)(const void*)kernel) >> 4) & 63;
+  if (last_k[h] == (const void*)kernel && last_b[h] >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) {
+    last_k[h] = (const void*)kernel;
+    last_b[h] = bytes;
+  }
+  return e;
 }
 
 #define AZ_TRY(...)                                                            \

@@ -278,15 +278,24 @@ extern "C" az_status_t az_solve_workspace_size(az_plan_t p, int64_t nrhs, int64_
   return AZ_OK;
 }
 
+// Stage-timing events, drawn from a per-thread pool (created once: event creation is a driver
+// round trip, and the small solves are host-latency bound).  Nested users take the next set.
 struct Ev {
-  cudaEvent_t e[8];
+  cudaEvent_t* e;
+  static constexpr int kDepth = 4;
+  static thread_local cudaEvent_t pool[kDepth][8];
+  static thread_local int depth;
   Ev() {
-    for (auto& x : e) cudaEventCreate(&x);
+    const int d = depth < kDepth ? depth : kDepth - 1;
+    ++depth;
+    e = pool[d];
+    if (!e[0])
+      for (int i = 0; i < 8; ++i) cudaEventCreate(&e[i]);
   }
-  ~Ev() {
-    for (auto& x : e) cudaEventDestroy(x);
-  }
+  ~Ev() { --depth; }
 };
+thread_local cudaEvent_t Ev::pool[Ev::kDepth][8] = {};
+thread_local int Ev::depth = 0;
 
 static double ms_between(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
@@ -553,14 +562,21 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
     saturated = rank > kp - pfix;
   }
   if (report) {
-    double sg[1] = {0};
     report->rank_used = rank;
     report->probes_used = kp;
     report->saturated = saturated ? 1 : 0;
-    AZ_CUDA_CHECK(cudaMemcpy(sg, w.sig, sizeof(double), cudaMemcpyDeviceToHost));
-    report->sigma_first = sg[0];
+    report->sigma_first = 0;
     report->sigma_last_kept = 0;
-    if (rank > 0) AZ_CUDA_CHECK(cudaMemcpy(&report->sigma_last_kept, w.sig + rank - 1, sizeof(double), cudaMemcpyDeviceToHost));
+    if (kp <= 256) {   // one copy of the (short) spectrum: both values from it
+      double sg[256];
+      AZ_CUDA_CHECK(cudaMemcpy(sg, w.sig, sizeof(double) * kp, cudaMemcpyDeviceToHost));
+      report->sigma_first = sg[0];
+      if (rank > 0) report->sigma_last_kept = sg[rank - 1];
+    } else {
+      AZ_CUDA_CHECK(cudaMemcpy(&report->sigma_first, w.sig, sizeof(double), cudaMemcpyDeviceToHost));
+      if (rank > 0)
+        AZ_CUDA_CHECK(cudaMemcpy(&report->sigma_last_kept, w.sig + rank - 1, sizeof(double), cudaMemcpyDeviceToHost));
+    }
     report->ms_rhs = ms_between(ev.e[0], ev.e[1]);
     report->ms_sketch = ms_sketch;
     report->ms_qr = ms_qr;
