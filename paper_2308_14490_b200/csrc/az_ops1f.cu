@@ -19,6 +19,9 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "az_fftr.cuh"
 #include "az_internal.h"
 
@@ -107,54 +110,17 @@ AZ_HD constexpr int col_stride() {
 
 // EC = values per thread in the column FFTs (16: fewer exchanges; 8: half the registers, more
 // resident warps); MINB = CTAs per SM the register budget is sized for.
-template <int NC, int TC, int KIND, int SRC, int EC, int MINB>
-__global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double cout) {
-  extern __shared__ cplx sm[];
+// The transform and store of a column pass on the values v (element e: row j + e T of column col,
+// vector pair b), shared by the one-tile kernel (k1f_cols) and the persistent TMA-fed one (k1f_cols_p).
+template <int NC, int TC, int KIND, int EC>
+AZ_D void cols_body(const P1f& a, cplx (&v)[EC], int j, int col, int b, cplx* buf, double cout) {
   constexpr int T = NC / EC;
-  const int tid = threadIdx.x, c = tid % TC, j = tid / TC;
-  const int b = blockIdx.y;
-  const int c0 = blockIdx.x * TC;
-  const int col = c0 + c;
   const Cols1 cc = pcols(a, b);
   const bool coef = (KIND == FC_IN_COEF || KIND == FC_OUT_COEF || KIND == FC_OUT_COEF_ADD || KIND == FC_OUT_Z);
   const int W = coef ? a.N2 : a.L2;                    // row length of the matrix
   cplx* C1b = (KIND == FC_OUT_Z) ? a.Z2 + (int64_t)b * a.n : a.C1 + (int64_t)b * a.n;
   cplx* Gb = a.G + (int64_t)b * a.L;
   const int64_t tmul = coef ? a.s : 1;                 // e^{-2 pi i n2 k1 / n} = e^{-2 pi i (s n2 k1) / L}
-  cplx* buf = sm + c * col_stride<NC, TC, EC>();
-  cplx v[EC];
-
-  // ---- load (element e: row j + e T) ----
-  if constexpr (KIND == FC_IN_COEF && SRC == SRC_PROBE) {
-    // lanes (2m, 2m+1) hold columns (col, col + 1), col even: the even lane draws the real-part
-    // probe pair of the two columns, the odd lane the imaginary-part pair, and they swap halves.
-    const bool odd = c & 1;
-#pragma unroll
-    for (int e = 0; e < EC; ++e) {
-      const int64_t i = (int64_t)(j + e * T) * W + (col & ~1);
-      double2 z = make_double2(0.0, 0.0);
-      if (!odd || cc.has_im) z = probe_pair((uint64_t)(i >> 1), (uint64_t)(a.col0 + (odd ? cc.cim : cc.cre)), a.seed);
-      const double send = odd ? z.x : z.y;
-      const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
-      v[e] = odd ? make_double2(recv, z.y) : make_double2(z.x, recv);
-    }
-  } else if constexpr (KIND == FC_IN_COEF) {
-#pragma unroll
-    for (int e = 0; e < EC; ++e) {
-      const int64_t i = (int64_t)(j + e * T) * W + col;
-      v[e] = make_double2(a.in[i + cc.cre * a.ldin], cc.has_im ? a.in[i + cc.cim * a.ldin] : 0.0);
-    }
-  } else if constexpr (KIND == FC_IN_ROWS) {
-#pragma unroll
-    for (int e = 0; e < EC; ++e) {
-      const int r = row_of(a, (int64_t)(j + e * T) * W + col);
-      v[e] = r >= 0 ? make_double2(a.in[r + cc.cre * a.ldin], cc.has_im ? a.in[r + cc.cim * a.ldin] : 0.0) : czero();
-    }
-  } else {
-    const cplx* src = coef ? C1b : Gb;
-#pragma unroll
-    for (int e = 0; e < EC; ++e) v[e] = src[(int64_t)(j + e * T) * W + col];
-  }
   uint32_t mbits = 0;   // FC_FINE_MASK: the 16 mask bytes of this thread, packed
   if constexpr (KIND == FC_FINE_MASK) {
 #pragma unroll
@@ -237,6 +203,121 @@ __global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double c
       a.out[i + cc.cre * a.ldout] = v[e].x * cout;
       if (cc.has_im) a.out[i + cc.cim * a.ldout] = v[e].y * cout;
     }
+  }
+}
+
+template <int NC, int TC, int KIND, int SRC, int EC, int MINB>
+__global__ void __launch_bounds__(TC * (NC / EC), MINB) k1f_cols(P1f a, double cout) {
+  extern __shared__ cplx sm[];
+  constexpr int T = NC / EC;
+  const int tid = threadIdx.x, c = tid % TC, j = tid / TC;
+  const int b = blockIdx.y;
+  const int c0 = blockIdx.x * TC;
+  const int col = c0 + c;
+  const Cols1 cc = pcols(a, b);
+  const bool coef = (KIND == FC_IN_COEF || KIND == FC_OUT_COEF || KIND == FC_OUT_COEF_ADD || KIND == FC_OUT_Z);
+  const int W = coef ? a.N2 : a.L2;                    // row length of the matrix
+  cplx* C1b = (KIND == FC_OUT_Z) ? a.Z2 + (int64_t)b * a.n : a.C1 + (int64_t)b * a.n;
+  cplx* Gb = a.G + (int64_t)b * a.L;
+  cplx* buf = sm + c * col_stride<NC, TC, EC>();
+  cplx v[EC];
+
+  // ---- load (element e: row j + e T) ----
+  if constexpr (KIND == FC_IN_COEF && SRC == SRC_PROBE) {
+    // lanes (2m, 2m+1) hold columns (col, col + 1), col even: the even lane draws the real-part
+    // probe pair of the two columns, the odd lane the imaginary-part pair, and they swap halves.
+    const bool odd = c & 1;
+#pragma unroll
+    for (int e = 0; e < EC; ++e) {
+      const int64_t i = (int64_t)(j + e * T) * W + (col & ~1);
+      double2 z = make_double2(0.0, 0.0);
+      if (!odd || cc.has_im) z = probe_pair((uint64_t)(i >> 1), (uint64_t)(a.col0 + (odd ? cc.cim : cc.cre)), a.seed);
+      const double send = odd ? z.x : z.y;
+      const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
+      v[e] = odd ? make_double2(recv, z.y) : make_double2(z.x, recv);
+    }
+  } else if constexpr (KIND == FC_IN_COEF) {
+#pragma unroll
+    for (int e = 0; e < EC; ++e) {
+      const int64_t i = (int64_t)(j + e * T) * W + col;
+      v[e] = make_double2(a.in[i + cc.cre * a.ldin], cc.has_im ? a.in[i + cc.cim * a.ldin] : 0.0);
+    }
+  } else if constexpr (KIND == FC_IN_ROWS) {
+#pragma unroll
+    for (int e = 0; e < EC; ++e) {
+      const int r = row_of(a, (int64_t)(j + e * T) * W + col);
+      v[e] = r >= 0 ? make_double2(a.in[r + cc.cre * a.ldin], cc.has_im ? a.in[r + cc.cim * a.ldin] : 0.0) : czero();
+    }
+  } else {
+    const cplx* src = coef ? C1b : Gb;
+#pragma unroll
+    for (int e = 0; e < EC; ++e) v[e] = src[(int64_t)(j + e * T) * W + col];
+  }
+  cols_body<NC, TC, KIND, EC>(a, v, j, col, b, buf, cout);
+}
+
+// ------------------------------------------------------------------------------------------
+// Persistent column passes over plan-owned tiles (default; AZ_COLS_PERSIST=0 selects k1f_cols): a CTA
+// owns TC adjacent columns and walks a range of the batch's vector pairs; the next pair's TC x NC
+// tile is brought in by the TMA engine (cp.async.bulk.tensor.3d, SASS UTMALDG, boxes of TC complex x
+// 256 rows of the [pair][row][column] tensor) into a shared-memory stage tracked by an mbarrier while
+// the current pair is transformed.  Same arithmetic as k1f_cols (cols_body).
+// ------------------------------------------------------------------------------------------
+template <int NC, int TC, int EC>
+struct ColsP {
+  static constexpr int T = NC / EC;
+  static constexpr int NT = TC * T;
+  static constexpr int BOXR = NC < 256 ? NC : 256;     // rows per TMA box
+  static constexpr size_t stage_bytes = sizeof(cplx) * TC * NC;
+  static constexpr size_t smem = 1024 + stage_bytes + sizeof(cplx) * TC * col_stride<NC, TC, EC>();
+};
+
+template <int NC, int TC, int KIND, int EC, int MINB>
+__global__ void __launch_bounds__(TC * (NC / EC), MINB)
+    k1f_cols_p(P1f a, double cout, const __grid_constant__ CUtensorMap tmap, int npairs, int pgroups) {
+  using C = ColsP<NC, TC, EC>;
+  constexpr int T = C::T;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw);
+  cplx* stage = reinterpret_cast<cplx*>(smraw + 1024);   // [row][TC] complex, as the box lands
+  cplx* xbuf = stage + TC * NC;
+  const int tid = threadIdx.x, c = tid % TC, j = tid / TC;
+  const int c0 = blockIdx.x * TC;
+  const int col = c0 + c;
+  const int b0 = (int)(((int64_t)npairs * blockIdx.y) / pgroups);
+  const int b1 = (int)(((int64_t)npairs * (blockIdx.y + 1)) / pgroups);
+  cplx* buf = xbuf + c * col_stride<NC, TC, EC>();
+  auto issue = [&](int b) {
+    bulk::arrive_expect_tx(bar, (uint32_t)C::stage_bytes);
+#pragma unroll
+    for (int r0 = 0; r0 < NC; r0 += C::BOXR) {
+      const uint32_t dst = bulk::smem_addr(stage + r0 * TC);
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+              dst),
+          "l"(&tmap), "r"(2 * c0), "r"(r0), "r"(b), "r"(bulk::smem_addr(bar))
+          : "memory");
+    }
+  };
+  if (tid == 0) {
+    bulk::mbar_init(bar, 1);
+    bulk::fence_init();
+  }
+  __syncthreads();
+  if (tid == 0 && b0 < b1) issue(b0);
+  uint32_t ph = 0;
+  for (int b = b0; b < b1; ++b) {
+    cplx v[EC];
+    bulk::wait(bar, ph);
+    ph ^= 1;
+#pragma unroll
+    for (int e = 0; e < EC; ++e) v[e] = stage[(j + e * T) * TC + c];
+    __syncthreads();   // the stage is free: the next pair's tile may land
+    if (tid == 0 && b + 1 < b1) {
+      bulk::fence_proxy_async();
+      issue(b + 1);
+    }
+    cols_body<NC, TC, KIND, EC>(a, v, j, col, b, buf, cout);
   }
 }
 
@@ -565,8 +646,94 @@ static az_status_t fcols_e(const P1f& a, int ncols, int nb, double cout, cudaStr
   return AZ_OK;
 }
 
+static bool cols_persist() {   // AZ_COLS_PERSIST=0: one CTA per (column tile, pair), no prefetch
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AZ_COLS_PERSIST");
+    v = (e && *e == '0') ? 0 : 1;
+  }
+  return v != 0;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency)
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+// the [pair][row][column] complex tensor of a column pass's input: rows N1, row length W complex,
+// pair stride pstride complex; boxes of TC complex x BOXR rows x 1 pair
+static bool make_cols_tmap(CUtensorMap* m, const cplx* base, int N1, int W, int64_t pstride, int nb, int TC, int BOXR) {
+  auto enc = tmap_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)(2 * W), (cuuint64_t)N1, (cuuint64_t)nb};
+  const cuuint64_t strides[2] = {(cuuint64_t)W * sizeof(cplx), (cuuint64_t)pstride * sizeof(cplx)};
+  const cuuint32_t box[3] = {(cuuint32_t)(2 * TC), (cuuint32_t)BOXR, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<cplx*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int NC, int KIND>
+static az_status_t fcols_p(const P1f& a, int ncols, int nb, double cout, cudaStream_t st, bool* done) {
+  constexpr int EC = 16, TC = 4, MINB = 1;
+  using C = ColsP<NC, TC, EC>;
+  *done = false;
+  const bool coef = (KIND == FC_OUT_COEF || KIND == FC_OUT_COEF_ADD || KIND == FC_OUT_Z);
+  const cplx* base = KIND == FC_OUT_Z ? a.Z2 : (coef ? a.C1 : a.G);
+  const int W = coef ? a.N2 : a.L2;
+  const int64_t pstride = coef ? a.n : a.L;
+  if (ncols % TC || ((uintptr_t)base & 15)) return AZ_OK;
+  CUtensorMap m;
+  if (!make_cols_tmap(&m, base + (int64_t)a.pair0 * 0, a.N1, W, pstride, nb, TC, C::BOXR)) return AZ_OK;
+  auto kern = k1f_cols_p<NC, TC, KIND, EC, MINB>;
+  AZ_CUDA_CHECK(az_smem_attr(kern, C::smem));
+  static int resident = 0;
+  if (!resident) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, C::NT, C::smem) != cudaSuccess || per < 1) {
+      cudaGetLastError();
+      per = 1;
+    }
+    resident = per * sms;
+  }
+  const int tiles = ncols / TC;
+  const int pg = std::max(1, std::min(nb, (4 * resident + tiles - 1) / tiles));
+  static const char* names[] = {"1f_cols_in_coef", "1f_cols_fine_mask", "1f_cols_out_gather", "1f_cols_out_resid",
+                                "1f_cols_in_rows", "1f_cols_out_coef", "1f_cols_fwd", "1f_cols_resid_mid",
+                                "1f_cols_out_coef_add", "1f_cols_out_z"};
+  AzTrace tr(names[KIND], st, nb);
+  kern<<<dim3(tiles, pg), C::NT, C::smem, st>>>(a, cout, m, nb, pg);
+  AZ_LAUNCH_CHECK();
+  *done = true;
+  return AZ_OK;
+}
+
 template <int NC, int KIND, int SRC>
 static az_status_t fcols(const P1f& a, int ncols, int nb, double cout, cudaStream_t st) {
+  constexpr bool tile_in = KIND == FC_FINE_MASK || KIND == FC_OUT_GATHER || KIND == FC_OUT_RESID ||
+                           KIND == FC_RESID_MID || KIND == FC_OUT_COEF || KIND == FC_OUT_COEF_ADD || KIND == FC_OUT_Z;
+  if constexpr (tile_in && NC >= 256) {
+    if (cols_persist() && fft_e() == 16) {
+      bool done = false;
+      AZ_TRY((fcols_p<NC, KIND>(a, ncols, nb, cout, st, &done)));
+      if (done) return AZ_OK;
+    }
+  }
   if (fft_e() == 8) return fcols_e<NC, KIND, SRC, 8, 3>(a, ncols, nb, cout, st);
   if (fft_e() == 17) return fcols_e<NC, KIND, SRC, 16, 1>(a, ncols, nb, cout, st);
   return fcols_e<NC, KIND, SRC, 16, 2>(a, ncols, nb, cout, st);

@@ -95,3 +95,31 @@ def test_c4_o1_golden_is_consistent_with_the_oracle():
     grid = I.test_grid(cfg)
     f = OA.evaluate(cfg, g["x_tol"], grid)
     assert np.max(np.abs(f - grid.exact)) <= 1e-8 * np.max(np.abs(grid.exact))
+
+
+def test_evaluate_1d_dense_branch_unit_coefficients():
+    """`evaluate` for n <= 4096 (the dense branch) on unit coefficient vectors: the approximant of
+    e_j is the periodised Gaussian centred at c_j, sampled on the test grid."""
+    cfg = I.make_config("interval", 64)
+    grid = I.test_grid(cfg, points_1d=101)
+    c = I.center_axis(cfg)
+    for j in (0, 17, 63):
+        x = np.zeros(cfg.N)
+        x[j] = 1.0
+        f = OA.evaluate(cfg, x, grid)[:, 0]
+        ref = periodized(grid.axes[0] - c[j], cfg.eps, cfg.T, 0)
+        np.testing.assert_allclose(f, ref[grid.inside], rtol=1e-14, atol=1e-300)
+
+
+def test_tsvd_lsq_multi_equals_tsvd_lsq():
+    """The several-tolerance O1 solve (one SVD) gives tsvd_lsq's solution and rank at each tolerance."""
+    rng = np.random.default_rng(3)
+    U, _ = np.linalg.qr(rng.standard_normal((60, 40)))
+    V, _ = np.linalg.qr(rng.standard_normal((40, 40)))
+    A = (U * np.logspace(0, -14, 40)) @ V.T
+    b = rng.standard_normal((60, 2))
+    sols, s = OA.tsvd_lsq_multi(A, b, (1e-6, 1e-10))
+    for (x, k), tol in zip(sols, (1e-6, 1e-10)):
+        x1, k1, _ = OA.tsvd_lsq(A, b, tol)
+        assert k == k1
+        np.testing.assert_allclose(x, x1, rtol=1e-12, atol=1e-12 * np.abs(x1).max())
