@@ -725,9 +725,11 @@ static az_status_t fcols_p(const P1f& a, int ncols, int nb, double cout, cudaStr
 
 template <int NC, int KIND, int SRC>
 static az_status_t fcols(const P1f& a, int ncols, int nb, double cout, cudaStream_t st) {
-  constexpr bool tile_in = KIND == FC_FINE_MASK || KIND == FC_OUT_GATHER || KIND == FC_OUT_RESID ||
-                           KIND == FC_RESID_MID || KIND == FC_OUT_COEF || KIND == FC_OUT_COEF_ADD || KIND == FC_OUT_Z;
-  if constexpr (tile_in && NC >= 256) {
+  // measured on c2 (ms per step, one-tile -> persistent): out_z 0.644 -> 0.612, out_gather 0.460 ->
+  // 0.441, fine_mask 0.762 -> 0.779, out_resid 0.893 -> 1.407 (its gather of b stalls the one 8-warp
+  // CTA per SM): the persistent form is used where the tile is the pass's only input
+  constexpr bool tile_in = KIND == FC_OUT_GATHER || KIND == FC_OUT_COEF || KIND == FC_OUT_Z;
+  if constexpr (tile_in && NC >= 256 && ColsP<NC, 4, 16>::smem <= 227 * 1024) {
     if (cols_persist() && fft_e() == 16) {
       bool done = false;
       AZ_TRY((fcols_p<NC, KIND>(a, ncols, nb, cout, st, &done)));
