@@ -336,13 +336,12 @@ def run_ours(args, cfg):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # > L2 (126 MB)
 
     if args.sharded:
-        from paper_2308_14490_b200 import dist as D
-        ops = D.GpuOps(plan)
+        # az_solve_sharded: the multi-GPU solve inside libaz (NCCL all-to-all + all-gathers over
+        # NVLink, fixed 8-leaf TSQR tree); torch.distributed only bootstraps the communicator
+        comm = api.Comm.from_process_group()
 
         def step(bb=None):
-            xs, r = D.solve_sharded(ops, b if bb is None else bb, theta, cfg.R, max_blocks)
-            return xs, dict(r, ms_rhs=0.0, ms_sketch=0.0, ms_qr=0.0, ms_svd=0.0, ms_step2=0.0, ms_total=0.0,
-                            sigma_first=0.0, sigma_last_kept=0.0)
+            return api.solve_sharded(plan, comm, b if bb is None else bb, theta, cfg.R, max_blocks, x=x)
     else:
         def step():
             return plan.solve(b, theta, cfg.R, max_blocks, x=x, workspace=ws)
@@ -567,7 +566,7 @@ def run_ours(args, cfg):
         "data": "synthetic",
         "config": {"workload": cfg.name, "n": cfg.n, "L": cfg.s, "dim": cfg.dim, "nrhs": cfg.nrhs, "R": cfg.R,
                    "tol": cfg.tol, "theta": theta, "max_blocks": max_blocks,
-                   "parallelism": (f"probe+rhs sharded over {world} (all-to-all re-block)" if args.sharded
+                   "parallelism": (f"az_solve_sharded over {world} (NCCL all-to-all re-block, 8-leaf TSQR tree)" if args.sharded
                                    else f"replicas{world}"),
                    "l2": "flushed between timed steps (256 MB write); S alone is 1.07 GB"},
         "probe_applies_per_s": world * rep["probes"] / (rep["ms_sketch"] * 1e-3) if rep["ms_sketch"] else None,

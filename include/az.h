@@ -231,6 +231,29 @@ az_status_t az_solve_host_pipelined(az_plan_t plan, const double* b_host, double
  * clears that flag.                                                                            */
 az_status_t az_plan_sync(az_plan_t plan);
 
+/* ---- multi-GPU: NCCL over NVLink / NVSwitch, one process per GPU ----------------
+ * NCCL is loaded at run time (the libnccl.so.2 already in the process, else the system one); without
+ * it these entry points return AZ_ERR_NOT_SUPPORTED.  Bootstrap: rank 0 calls az_comm_unique_id, the
+ * caller broadcasts the 128 bytes (e.g. over torch.distributed), every rank calls az_comm_create
+ * (collective, blocking).  world must divide 8 (the leaves of the fixed TSQR tree).               */
+typedef struct az_comm_s* az_comm_t;
+az_status_t az_comm_unique_id(void* id128);          /* HOST, 128 bytes out (an ncclUniqueId) */
+az_status_t az_comm_create(int32_t world, int32_t rank, const void* id128, az_comm_t* out);
+az_status_t az_comm_destroy(az_comm_t comm);
+/* The sharded AZ solve, collective over comm (every rank calls it with the same plan descriptor,
+ * b, theta, R, max_blocks; b and x are replicated DEVICE arrays, shapes as az_solve).  Rank g
+ * computes b' for its pair-aligned share of the right-hand sides and the sketch of its share of
+ * every probe block (Philox keyed by the global column); an all-to-all (grouped ncclSend/ncclRecv)
+ * re-blocks each new block by rows; the rows are cut into 8 fixed leaves, each leaf is reduced by
+ * the single-pass TSQR to [R_l | c_l], the 8 factors are all-gathered and merged on every rank;
+ * every rank runs the truncated SVD; x2 = Omega y and step 2 run per right-hand-side shard and x is
+ * all-gathered (Alg. 1, :222-232).  x is bitwise identical at world
+ * sizes 1, 2, 4 and 8.  Scratch is stream-ordered device memory (cudaMallocAsync) of the call.
+ * Synchronises the stream; the report (HOST, may be NULL) has rank, probes, saturation and sigma.  */
+az_status_t az_solve_sharded(az_plan_t plan, az_comm_t comm, const double* b, int64_t ldb, double* x, int64_t ldx,
+                             int64_t nrhs, double theta, int64_t R, int32_t max_blocks,
+                             az_solve_report_t* report, void* stream);
+
 /* ---- factorisation reuse --------------------------------------------
  * The step-1 matrix (A - A Z* A) Omega does not depend on b (Alg. 1, :228, :283): factor
  * it once, then solve for any number of right-hand sides at the cost of b' = (I - A Z*) b, Q^T b'

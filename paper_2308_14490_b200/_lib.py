@@ -87,6 +87,10 @@ def lib():
         "az_solve_host": [P, P, P, I64, D, I64, C.c_int32, C.POINTER(SolveReport), P],
         "az_step2_workspace_size": [P, I64, C.POINTER(C.c_size_t)],
         "az_step2": [P, P, I64, P, I64, P, I64, I64, P, C.c_size_t, P],
+        "az_comm_unique_id": [P],
+        "az_comm_create": [C.c_int32, C.c_int32, P, C.POINTER(P)],
+        "az_comm_destroy": [P],
+        "az_solve_sharded": [P, P, P, I64, P, I64, I64, D, I64, C.c_int32, C.POINTER(SolveReport), P],
     }
     for name, argt in sig.items():
         fn = getattr(L, name)
@@ -113,7 +117,8 @@ EXPORTED = ["az_plan_create", "az_plan_destroy", "az_plan_query", "az_apply_A", 
             "az_last_error", "az_launch_count", "az_trace_enable", "az_trace_report",
             "az_factorize", "az_factor_destroy", "az_factor_query", "az_factor_workspace_size",
             "az_solve_factored", "az_solve_host_pipelined", "az_plan_sync", "az_svd_sweeps_last",
-            "az_step2_workspace_size", "az_step2"]
+            "az_step2_workspace_size", "az_step2", "az_comm_unique_id", "az_comm_create", "az_comm_destroy",
+            "az_solve_sharded"]
 
 
 def check(fn: str, status: int, allow=(AZ_OK,)):

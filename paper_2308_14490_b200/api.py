@@ -224,6 +224,63 @@ class Plan:
         return x, _report(rep, st)
 
 
+class Comm:
+    """An NCCL communicator inside libaz (az_comm_create) for az_solve_sharded.  Collective: every
+    rank of a torch.distributed process group builds it with `Comm.from_process_group()` (rank 0's
+    unique id is broadcast over the group: torch.distributed is the bootstrap plumbing only)."""
+
+    def __init__(self, world: int, rank: int, uid: bytes):
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(uid), 128)
+        check("az_comm_create", lib().az_comm_create(world, rank, buf, C.byref(h)))
+        self._h = h
+        self.world, self.rank = world, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check("az_comm_unique_id", lib().az_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_process_group(cls, group=None) -> "Comm":
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        t = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            t = torch.frombuffer(bytearray(cls.unique_id()), dtype=torch.uint8).clone()
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda()
+        dist.broadcast(t, 0, group=group)
+        return cls(world, rank, bytes(t.cpu().numpy().tobytes()))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().az_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def solve_sharded(plan: "Plan", comm: Comm, b, theta: float, R: int, max_blocks: int = 1, x=None, stream=None):
+    """az_solve_sharded: the multi-GPU AZ solve inside libaz (NCCL), collective over `comm`;
+    b replicated on every rank, x returned replicated."""
+    pb, ldb, nrhs = _mat(b)
+    if x is None:
+        x = empty_colmajor(plan.N, nrhs, b.device) if b.dim() == 2 else torch.empty(plan.N, dtype=torch.float64,
+                                                                                   device=b.device)
+    px, ldx, _ = _mat(x)
+    rep = _lib.SolveReport()
+    st = check("az_solve_sharded", lib().az_solve_sharded(plan._h, comm._h, C.c_void_p(pb), ldb, C.c_void_p(px), ldx,
+                                                          nrhs, theta, R, max_blocks, C.byref(rep), _stream(stream)),
+               allow=(_lib.AZ_OK, _lib.AZ_WARN_SKETCH_SATURATED))
+    return x, _report(rep, st)
+
+
 class Factor:
     """A factored step-1 sketch (az_factorize): solve for new right-hand sides without redrawing,
     re-factoring or re-decomposing the sketch."""

@@ -158,6 +158,44 @@ def test_solve_sharded_nccl_world1_matches_az_solve(name, cfg, max_blocks):
         dist.destroy_process_group()
 
 
+SHARDED_CASES = [("c1", I.get_config("c1"), 4),
+                 ("interval_n8192_4step", I.make_config("interval", 8192, nrhs=6, R=40), 4),
+                 ("interval_n256_adaptive", I.make_config("interval", 256, R=16, nrhs=3), 8),
+                 ("star_n32", I.make_config("star", 32), 8)]
+
+
+@pytest.mark.parametrize("name,cfg,max_blocks", SHARDED_CASES, ids=[c[0] for c in SHARDED_CASES])
+def test_libaz_sharded_solve_nccl_world1(name, cfg, max_blocks):
+    """az_solve_sharded (the multi-GPU solve inside libaz: NCCL all-to-all / all-gathers, fixed
+    8-leaf TSQR tree, step 2 per right-hand-side shard) at world size 1 on the GPU: BITWISE equal to
+    the torch.distributed orchestration of dist.py over the same libaz kernels (the same operations
+    on the same operands), and the approximant of az_solve to the parity bar."""
+    import socket
+    import torch.distributed as dist
+    from paper_2308_14490_b200 import api
+    from paper_2308_14490_b200 import dist as D
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        plan = api.Plan.from_config(cfg)
+        b = _dev(I.rhs(cfg))
+        comm = api.Comm.from_process_group()
+        xs, reps = api.solve_sharded(plan, comm, b, 1e-12, cfg.R, max_blocks)
+        xd, repd = D.solve_sharded(D.GpuOps(plan), api.colmajor(b), 1e-12, cfg.R, max_blocks)
+        assert reps["probes"] == repd["probes"] and reps["rank"] == repd["rank"]
+        assert torch.equal(xs, xd)
+        x1, rep1 = plan.solve(b, 1e-12, cfg.R, max_blocks)
+        grid = I.test_grid(cfg)
+        bar = 1e-10 if cfg.dim == 1 else 1e-8
+        assert np.all(_approx_err(cfg, _host(xs), _host(x1), grid) <= bar)
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
 def test_solve_host_pipelined_matches_solve():
     """az_solve_host_pipelined (the e2e path): several enqueued host-buffer solves with different
     right-hand sides, results after az_plan_sync equal to az_solve's (AZ is linear in b for a fixed
