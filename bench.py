@@ -6,9 +6,10 @@ probes, tol 1e-12) on B200, with the roofline of the dominant kernel and the CPU
 
 One "step" = one az_solve (Alg. 1: b' = (I - A Z*) b, the 64-probe sketch
 (A - A Z* A) Omega, TSQR + truncated SVD, x2 = Omega y, step 2 x = x2 + Z*(b - A x2)) over the
-config's whole RHS batch, inputs resident in HBM.  Multi-GPU (torchrun): every rank solves its own
-independent c2 problem (weak scaling, no data-path collective); the time is
-the max over ranks.  The reference arm (--impl reference) times the CPU oracle (oracle/, the
+config's whole RHS batch, inputs resident in HBM.  Multi-GPU (torchrun): ONE solve sharded over the
+ranks by az_solve_sharded (probe / RHS column shards, NCCL all-to-all re-block, fixed 8-leaf TSQR
+tree; strong scaling); --replicas times independent per-rank solves (weak
+scaling) instead; the time is the max over ranks.  The reference arm (--impl reference) times the CPU oracle (oracle/, the
 paper's algorithm with numpy FFTs) on a bounded sample of the same workload, scaled to one solve.
 """
 from __future__ import annotations
@@ -311,6 +312,11 @@ def run_ours(args, cfg):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
+    if world > 1 and not args.replicas:
+        # several GPUs: ONE solve sharded over the ranks (az_solve_sharded: the probe / RHS column shards,
+        # the NCCL all-to-all re-block and the factor all-gathers; strong scaling).  --replicas times
+        # independent single-GPU solves instead (weak scaling, no data-path collective).
+        args.sharded = True
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", init_method="env://")
@@ -613,8 +619,10 @@ def main():
     ap.add_argument("--extra-configs", default="c1,c3,c4,c5",
                     help="other BASELINE configs timed after the headline (fewer steps, stated); '' = none")
     ap.add_argument("--sharded", action="store_true",
-                    help="one solve sharded over the ranks (probe/RHS columns + all-to-all re-block, strong "
-                         "scaling) instead of independent replicas (weak scaling)")
+                    help="one solve sharded over the ranks (az_solve_sharded: probe/RHS columns + NCCL all-to-all "
+                         "re-block, strong scaling); the default whenever WORLD_SIZE > 1")
+    ap.add_argument("--replicas", action="store_true",
+                    help="with WORLD_SIZE > 1: independent single-GPU solves per rank (weak scaling) instead")
     args = ap.parse_args()
     cfg = I.get_config(args.config)
     if args.impl == "reference":
