@@ -6,10 +6,11 @@
 //      sketch S = (A - A Z* A) Omega for its share of each new probe block (Philox keyed by the
 //      GLOBAL column: the probes are the single-GPU ones);
 //   2. an all-to-all (grouped ncclSend / ncclRecv) re-blocks the NEW columns into row blocks;
-//   3. TSQR over a FIXED tree of NLEAF = 8 row leaves (rank g owns 8 / G consecutive leaves), the
-//      leaf factors [R_l | c_l] are all-gathered (ncclAllGather) and merged by one more QR on every
-//      rank -> [R_S | Q^T b'];
-//   4. the truncated SVD solve y on every rank (identical inputs, identical results);
+//   3. TSQR over a FIXED tree of NLEAF = 8 row leaves (rank g owns 8 / G consecutive leaves): each
+//      leaf gives [R_l | c_l]; a binary tree of pairwise merges (left over right, by the owner of the
+//      left child; ncclSend/ncclRecv where the children live on different ranks -- one factor per
+//      rank and level) ends in [R_S | Q^T b'] on rank 0;
+//   4. the truncated SVD solve on rank 0; y and the rank are broadcast (ncclBroadcast);
 //   5. x2 = Omega y and x = x2 + Z* (b - A x2) for the rank's right-hand sides, then an all-gather of
 //      x (b and x replicated on every rank).
 // Pair-aligned shards and the fixed tree make every operation see the same operands at G = 1, 2, 4
@@ -35,6 +36,7 @@ struct Nccl {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
@@ -56,12 +58,14 @@ Nccl& nccl() {
     sym(n.CommInitRank, "ncclCommInitRank");
     sym(n.CommDestroy, "ncclCommDestroy");
     sym(n.AllGather, "ncclAllGather");
+    sym(n.Broadcast, "ncclBroadcast");
     sym(n.Send, "ncclSend");
     sym(n.Recv, "ncclRecv");
     sym(n.GroupStart, "ncclGroupStart");
     sym(n.GroupEnd, "ncclGroupEnd");
     sym(n.GetErrorString, "ncclGetErrorString");
-    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.AllGather && n.Send && n.Recv && n.GroupStart &&
+    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.AllGather && n.Broadcast && n.Send && n.Recv &&
+           n.GroupStart &&
            n.GroupEnd && n.GetErrorString;
   });
   return n;
@@ -221,7 +225,7 @@ extern "C" az_status_t az_solve_sharded(az_plan_t p, az_comm_t c, const double* 
       wsv(st);
   const int64_t pme_max = std::max<int64_t>(qme, ps[me + 1] - ps[me]);
   const int64_t leafrows = std::max(leafmax, kmax);
-  const int64_t stkrows = std::max<int64_t>(NLEAF * kpmax, kmax);
+  const int64_t stkrows = std::max<int64_t>(2 * kpmax, kmax);
   size_t qrw = 0, svw = 0;
   for (int64_t b2 = 1; b2 <= max_blocks; ++b2) {   // the QR / SVD workspaces of every block's shapes
     const int64_t k2 = b2 * R + nrhs;
@@ -232,7 +236,7 @@ extern "C" az_status_t az_solve_sharded(az_plan_t p, az_comm_t c, const double* 
   AZ_TRY(az_step2_workspace_size(p, std::max<int64_t>(qme, 1), &s2bytes));
   if (loc.alloc(rows * std::max<int64_t>(pme_max, 1)) || snd.alloc(rows * std::max<int64_t>(pme_max, 1)) ||
       Ame.alloc(rme * kmax) || leaf.alloc(leafrows * kmax) || fac.alloc((size_t)NLEAF * kpmax * kmax) ||
-      stk.alloc(stkrows * kmax) || Rm.alloc(kmax * kmax) || yb.alloc(kpmax * nrhs) || sg.alloc(kpmax) ||
+      stk.alloc(stkrows * kmax) || Rm.alloc(kmax * kmax) || yb.alloc(kpmax * nrhs) || sg.alloc(kpmax + 1) ||
       xs.alloc(N * qmax * G) || x2.alloc(N * std::max<int64_t>(qme, 1)) || wq.alloc(qrw / sizeof(double) + 1) ||
       ws2.alloc(s2bytes / sizeof(double) + 1) || wsv.alloc(svw / sizeof(double) + 1)) {
     az_set_error("az_solve_sharded: out of device memory");
@@ -272,24 +276,54 @@ extern "C" az_status_t az_solve_sharded(az_plan_t p, az_comm_t c, const double* 
                                         cudaMemcpyDeviceToDevice, st));
       }
     }
-    // all-gather the leaf factors (rank g's lpr factors are leaves g lpr ..: leaf order)
-    const size_t fsz = (size_t)lpr * kp * k;
-    AZ_NCCL(nccl().AllGather(fac.p + (size_t)me * fsz, fac.p, fsz, ncclFloat64, c->comm, st));
-    // stack by rows in leaf order: (NLEAF kp) x k, ld srows
-    const int64_t srows = std::max<int64_t>(NLEAF * kp, k);
-    if (srows > NLEAF * kp) AZ_CUDA_CHECK(cudaMemsetAsync(stk.p, 0, sizeof(double) * srows * k, st));
-    for (int l = 0; l < NLEAF; ++l)
-      AZ_CUDA_CHECK(cudaMemcpy2DAsync(stk.p + l * kp, srows * sizeof(double), fac.p + (size_t)l * kp * k,
-                                      kp * sizeof(double), kp * sizeof(double), k, cudaMemcpyDeviceToDevice, st));
-    int64_t ldrf = kp;
-    if (k <= AZ_NARROW_MAX) {
-      AZ_TRY(az_qr_r_impl(stk.p, srows, k, srows, Rm.p, kp, wq.p, qrw, st, kp));
-    } else {
-      AZ_TRY(az_qr_r_impl(stk.p, srows, k, srows, Rm.p, k, wq.p, qrw, st));
-      ldrf = k;
+    // binary tree of pairwise merges over the 8 leaves (fixed shape: bitwise identical across G)
+    const size_t fsz = (size_t)kp * k;
+    const int64_t mrows = std::max<int64_t>(2 * kp, k);   // stacked pair (zero rows pad m < k)
+    for (int width = 1; width < NLEAF; width *= 2) {
+      AZ_NCCL(nccl().GroupStart());
+      for (int i = 0; i < NLEAF / width; i += 2) {
+        const int ol = (i * width) / lpr, orr = ((i + 1) * width) / lpr;
+        double* rf = fac.p + (size_t)(i + 1) * width * fsz;   // node (i + 1)'s factor, at its first leaf's slot
+        if (ol != orr && me == orr) AZ_NCCL(nccl().Send(rf, fsz, ncclFloat64, ol, c->comm, st));
+        if (ol != orr && me == ol) AZ_NCCL(nccl().Recv(rf, fsz, ncclFloat64, orr, c->comm, st));
+      }
+      AZ_NCCL(nccl().GroupEnd());
+      for (int i = 0; i < NLEAF / width; i += 2) {
+        if ((i * width) / lpr != me) continue;
+        double* lf = fac.p + (size_t)i * width * fsz;
+        double* rf = fac.p + (size_t)(i + 1) * width * fsz;
+        if (mrows > 2 * kp) AZ_CUDA_CHECK(cudaMemsetAsync(stk.p, 0, sizeof(double) * mrows * k, st));
+        AZ_CUDA_CHECK(cudaMemcpy2DAsync(stk.p, mrows * sizeof(double), lf, kp * sizeof(double), kp * sizeof(double), k,
+                                        cudaMemcpyDeviceToDevice, st));
+        AZ_CUDA_CHECK(cudaMemcpy2DAsync(stk.p + kp, mrows * sizeof(double), rf, kp * sizeof(double),
+                                        kp * sizeof(double), k, cudaMemcpyDeviceToDevice, st));
+        // the parent's factor replaces the left child's (kp x k, ld kp)
+        if (k <= AZ_NARROW_MAX) {
+          AZ_TRY(az_qr_r_impl(stk.p, mrows, k, mrows, lf, kp, wq.p, qrw, st, kp));
+        } else {
+          AZ_TRY(az_qr_r_impl(stk.p, mrows, k, mrows, Rm.p, k, wq.p, qrw, st));
+          AZ_CUDA_CHECK(cudaMemcpy2DAsync(lf, kp * sizeof(double), Rm.p, k * sizeof(double), kp * sizeof(double), k,
+                                          cudaMemcpyDeviceToDevice, st));
+        }
+      }
     }
-    // 4. truncated SVD solve of [R_S | Q^T b'] (host rank: the block decision)
-    AZ_TRY(az_tsvd_impl(Rm.p, ldrf, kp, nrhs, theta, yb.p, kp, sg.p, &rank, wsv.p, svw, st));
+    // 4. truncated SVD solve on rank 0 (the root factor, kp x k at fac), y and the rank broadcast
+    double* info = sg.p + kpmax;   // one double beside sigma: the rank, as a value
+    if (me == 0) {
+      AZ_TRY(az_tsvd_impl(fac.p, kp, kp, nrhs, theta, yb.p, kp, sg.p, &rank, wsv.p, svw, st));
+      const double rv = (double)rank;
+      AZ_CUDA_CHECK(cudaMemcpyAsync(info, &rv, sizeof(double), cudaMemcpyHostToDevice, st));
+    }
+    AZ_NCCL(nccl().GroupStart());
+    AZ_NCCL(nccl().Broadcast(yb.p, yb.p, (size_t)kp * nrhs, ncclFloat64, 0, c->comm, st));
+    AZ_NCCL(nccl().Broadcast(sg.p, sg.p, (size_t)kpmax + 1, ncclFloat64, 0, c->comm, st));
+    AZ_NCCL(nccl().GroupEnd());
+    if (me != 0) {
+      double rv = 0.0;
+      AZ_CUDA_CHECK(cudaMemcpyAsync(&rv, info, sizeof(double), cudaMemcpyDeviceToHost, st));
+      AZ_CUDA_CHECK(cudaStreamSynchronize(st));
+      rank = (int64_t)rv;
+    }
     saturated = rank > kp - pfix;
     if (!saturated || nb == max_blocks) break;
   }

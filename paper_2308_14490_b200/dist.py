@@ -9,11 +9,12 @@ in libaz through the `Ops` adapter (GpuOps).  Steps (Alg. 1, lines 227-
   2. all-to-all re-block of the NEW columns only: the column-sharded block becomes row blocks
      appended to the rank's rows of the earlier blocks (the exchange step);
   3. TSQR over a FIXED tree: the rows are cut into NLEAF leaves whatever the world size (rank g owns
-     NLEAF/G consecutive leaves), each leaf gives [R_l | c_l] (k1 x k, az_qr_r_partial), the NLEAF
-     factors are all-gathered and stacked in leaf order, and one more az_qr_r_partial merges them
-     into [R_S | Q^T b'] on every rank;
-  4. truncated SVD solve y = V_k Sigma_k^-1 U_k^T (Q^T b') on every rank (identical inputs, so
-     identical results; no broadcast needed);
+     NLEAF/G consecutive leaves), each leaf gives [R_l | c_l] (k1 x k, az_qr_r_partial), and a binary
+     tree of pairwise merges (left over right, by the owner of the left child; a factor crosses to
+     another rank only where the two children live on different ranks, one factor per rank and
+     level) ends in [R_S | Q^T b'] on rank 0;
+  4. truncated SVD solve y = V_k Sigma_k^-1 U_k^T (Q^T b') on rank 0; y (probes x nrhs) and the rank
+     are broadcast;
   5. x2 = Omega y and the step-2 correction x = x2 + Z*(b - A x2) (az_omega_apply, az_step2) for the
      rank's right-hand-side columns, then all-gather of x (b and x are replicated).
 
@@ -92,6 +93,46 @@ def reblock(local: torch.Tensor, col_owner: List[Tuple[int, int, int]], k: int, 
     return out
 
 
+def tree_merge(ops, facs: dict, nleaf: int, lpr: int, k1: int, k: int, like: torch.Tensor, group=None):
+    """Binary reduction of the nleaf leaf factors [R_l | c_l] (k1 x k each) over a FIXED tree: node i of
+    level l (covering leaves i 2^l .. (i + 1) 2^l - 1) is the TSQR of its two children stacked (left
+    over right), computed by the owner of its first leaf; a child on another rank is sent there.  The
+    same merges in the same order at every world size; the root ends on rank 0 (returned there,
+    None elsewhere).  Each rank sends at most one factor per level (log2 nleaf levels)."""
+    me = dist.get_rank(group)
+    cur = dict(facs)                 # node index -> factor, for the nodes this rank holds
+    width = 1                        # leaves per node at the current level
+    while width < nleaf:
+        nxt = {}
+        ops_ = []
+        for i in range(0, nleaf // width, 2):
+            left, right = i * width, (i + 1) * width          # first leaves of the two children
+            ol, orr = left // lpr, right // lpr                # their owners
+            if orr != ol:
+                if me == orr:
+                    ops_.append(dist.P2POp(dist.isend, cur.pop(i + 1).t().contiguous(), ol, group=group))
+                elif me == ol:
+                    buf = torch.empty((k, k1), dtype=torch.float64, device=like.device)
+                    ops_.append(dist.P2POp(dist.irecv, buf, orr, group=group))
+                    cur[("in", i + 1)] = buf
+        if ops_:
+            for req in dist.batch_isend_irecv(ops_):
+                req.wait()
+        for i in range(0, nleaf // width, 2):
+            left = i * width
+            if left // lpr != me:
+                continue
+            rt = cur.pop(i + 1) if (i + 1) in cur else cur.pop(("in", i + 1)).t()
+            lt = cur.pop(i)
+            st = colmajor_empty(2 * k1, k, like)
+            st[:k1] = lt
+            st[k1:] = rt
+            nxt[i // 2] = ops.qr_partial(st, k1)
+        cur = nxt
+        width *= 2
+    return cur.get(0)
+
+
 def solve_sharded(ops, b: torch.Tensor, theta: float, R: int, max_blocks: int = 1, p_over: int = 10,
                   group=None, nleaf: int = NLEAF) -> Tuple[torch.Tensor, dict]:
     """Distributed AZ solve; b: rows x nrhs column-major, replicated on every rank.  Returns x
@@ -127,20 +168,24 @@ def solve_sharded(ops, b: torch.Tensor, theta: float, R: int, max_blocks: int = 
         # my rows of [S | b'] (rows_me x k): earlier blocks, the new block, b'
         Sme = torch.cat([Sme.t(), Snew.t()]).t() if Sme.shape[1] else Snew
         Ame = torch.cat([Sme.t(), Bme.t()]).t()
-        mine = []
+        facs = {}
         for leaf in range(me * lpr, (me + 1) * lpr):
             a0, a1 = leaves[leaf] - r_lo, leaves[leaf + 1] - r_lo
-            mine.append(ops.qr_partial(Ame[a0:a1].clone(), kp))   # kp x k; az_qr_r_partial overwrites its input
-        packed = torch.cat([f.t().contiguous().reshape(-1) for f in mine])   # lpr factors, each k x kp row-major
-        gathered = torch.empty(G * packed.numel(), dtype=packed.dtype, device=packed.device)
-        dist.all_gather_into_tensor(gathered, packed, group=group)
-        # stack the nleaf factors by rows, in leaf order: (nleaf kp) x k column-major
-        stacked = colmajor_empty(nleaf * kp, k, b)
-        fac = gathered.view(nleaf, k, kp)
-        for leaf in range(nleaf):
-            stacked[leaf * kp:(leaf + 1) * kp, :] = fac[leaf].t()
-        Rf = ops.qr_partial(stacked, kp)                     # [R_S | Q^T b'] (kp x k)
-        y, _, rank_k = ops.tsvd(Rf, kp, nrhs, theta)
+            facs[leaf] = ops.qr_partial(Ame[a0:a1].clone(), kp)   # kp x k; az_qr_r_partial overwrites its input
+        Rf = tree_merge(ops, facs, nleaf, lpr, kp, k, b, group)    # [R_S | Q^T b'] on rank 0, None elsewhere
+        # the truncated SVD on rank 0; y (kp x nrhs) and the rank are broadcast
+        info = torch.zeros(1, dtype=torch.float64, device=b.device)
+        if me == 0:
+            y, _, rank_k = ops.tsvd(Rf, kp, nrhs, theta)
+            y = ops.contig(y)
+            info[0] = rank_k
+        else:
+            y = colmajor_empty(kp, nrhs, b)
+        ybuf = y.t().contiguous()                             # nrhs x kp row-major == y column-major
+        dist.broadcast(ybuf, 0, group=group)
+        dist.broadcast(info, 0, group=group)
+        y = ybuf.t()
+        rank_k = int(info[0].item())
         saturated = rank_k > kp - p_over
         if not saturated:
             break
