@@ -154,13 +154,18 @@ __global__ void __launch_bounds__(32 * NW, NW >= 16 ? 1 : 2) k_tsqr(QRIn q) {
         double v[RPL];
 #pragma unroll
         for (int r = 0; r < RPL; ++r) v[r] = vj[lane + 32 * r];
-        // all owned columns at once: KC independent dot products, interleaved warp reductions
+        // all owned live columns at once: KC independent dot products, interleaved warp reductions.
+        // A column at or left of j is already triangularised (its registers hold zeros): its dot is
+        // skipped (warp-uniform), which removes half of the step's dot-product FMAs on average -- the
+        // apply phase is FP64-pipe bound (ncu: math-throttle / not-selected stalls on these DFMAs)
         double p[KC];
 #pragma unroll
         for (int c = 0; c < KC; ++c) {
           p[c] = 0.0;
+          if (w + NW * c > j) {
 #pragma unroll
-          for (int r = 0; r < RPL; ++r) p[c] = fma(v[r], x[c][r], p[c]);
+            for (int r = 0; r < RPL; ++r) p[c] = fma(v[r], x[c][r], p[c]);
+          }
         }
         // transpose-reduce: KC - 1 + (5 - log2 KC) shuffles instead of 5 KC; afterwards lane L holds
         // the full dot of column slot L / (32 / KC)
@@ -207,239 +212,6 @@ __global__ void __launch_bounds__(32 * NW, NW >= 16 ? 1 : 2) k_tsqr(QRIn q) {
   }
 }
 
-
-// ------------------------------------------------------------------------------------------
-// Panel-blocked TSQR pass for k = k1 <= 64 columns (the split leaf's pass A and the merge levels of
-// the deferred path).  Same reflectors as k_tsqr (H_j = I - tau_j v_j v_j^T, v_j = [e_j; y_j],
-// dlarfg convention), applied in the same order, but grouped in panels of 4 columns:
-//   * warp w owns the 4 consecutive columns 4w .. 4w+3 (panel w); the owner factors its panel
-//     alone -- 4 Householder steps with in-warp reductions, no block barrier -- and also forms the
-//     panel's couplings g_im = y_i . y_m (m < i);
-//   * one block barrier publishes the panel; every warp owning later columns applies its 4
-//     reflectors at once (16 independent dot products in one warp reduction):
-//        s_i = R[c_i][l] + y_i . x_l,   d_i = s_i - sum_{m<i} tau_m g_im d_m,
-//        R[c_i][l] -= tau_i d_i,        x_l -= sum_i tau_i d_i y_i;
-//   * the next panel's owner applies the current panel to its own columns first and factors its
-//     panel while the other warps apply: the critical path per panel is one apply + one panel
-//     factorisation, and a chunk takes 16 block barriers instead of 64 (k_tsqr: one per column,
-//     with every warp idle while the owner builds the reflector -- 37 % of its warp samples wait at
-//     that barrier, ncu).
-// ------------------------------------------------------------------------------------------
-template <int RPL, bool YSTACK>
-__global__ void __launch_bounds__(512, 1) k_tsqr_p(QRIn q) {
-  constexpr int MC = 32 * RPL, KC = 4;
-  extern __shared__ double sm[];
-  const int k = q.k;                             // == q.k1 <= 64
-  double* R = sm;                                // k (k+1) / 2, packed upper triangle
-  double* vb = R + (k * (k + 1)) / 2;            // 2 panels (parity) x KC x MC: the panel's y
-  double* pb = vb + 2 * KC * MC;                 // 2 panels x 32: tau[4], g[4][4] at 4 + 4 i + m
-  double* db = pb + 64;                          // 16 warps x 16: the applied d values tau_i d_i
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int np = (k + KC - 1) / KC;
-  for (int i = threadIdx.x; i < (k * (k + 1)) / 2; i += blockDim.x) R[i] = 0.0;
-  const int64_t r0 = (int64_t)blockIdx.x * q.rows_per_cta;
-  const int64_t r1 = (q.m < r0 + q.rows_per_cta) ? q.m : r0 + q.rows_per_cta;
-  double x[KC][RPL];
-
-  auto row_off = [&](int64_t row) -> int64_t { return q.bstride ? (row / q.rb) * q.bstride + (row % q.rb) : row; };
-
-  // ---- the owner warp factors panel p of the current chunk (x holds its 4 columns) ----
-  auto factor_panel = [&](int p, int64_t base, int chunk) {
-    const int j0 = KC * p;
-    double* vp = vb + (p & 1) * KC * MC;
-    double* pp = pb + (p & 1) * 32;
-#pragma unroll
-    for (int i = 0; i < KC; ++i) {
-      const int c = j0 + i;
-      if (c >= k) {
-        if (lane == 0) pp[i] = 0.0;
-        continue;
-      }
-      const double alpha = R[pk(c, c)];
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int r = 0; r < RPL; r += 2) {
-        s0 = fma(x[i][r], x[i][r], s0);
-        if (r + 1 < RPL) s1 = fma(x[i][r + 1], x[i][r + 1], s1);
-      }
-      const double sig = warp_sum(s0 + s1);
-      double tau = 0.0, scale = 0.0, beta = alpha;
-      if (sig > 0.0) {
-        const double s2 = fma(alpha, alpha, sig);
-        const double rinv = fast_rsqrt(s2);
-        const double nrm = s2 * rinv;
-        beta = alpha >= 0.0 ? -nrm : nrm;
-        tau = fma(fabs(alpha), rinv, 1.0);
-        scale = fast_rcp(alpha - beta);
-      }
-      double y[RPL];
-#pragma unroll
-      for (int r = 0; r < RPL; ++r) {
-        y[r] = x[i][r] * scale;
-        vp[i * MC + lane + 32 * r] = y[r];
-      }
-      if (q.Y) {
-#pragma unroll
-        for (int r = 0; r < RPL; ++r) {
-          const int64_t row = base + lane + 32 * r;
-          if (row < r1) {
-            if constexpr (YSTACK)
-              q.Y[(row / q.rb) * q.bstride + (row % q.rb) + (int64_t)c * q.ldY] = y[r];
-            else
-              q.Y[row + (int64_t)c * q.ldY] = y[r];
-          }
-        }
-        if (lane == 0) q.taus[((int64_t)blockIdx.x * q.cmax + chunk) * q.k1 + c] = tau;
-      }
-      // couplings with the panel's earlier reflectors and dots with its later columns, in one
-      // multi-value reduction: t[m] = y . y_m (m < i), t[i'] = y . x_i' (i' > i)
-      double t[KC];
-#pragma unroll
-      for (int m = 0; m < KC; ++m) {
-        t[m] = 0.0;
-        if (m == i) continue;
-#pragma unroll
-        for (int r = 0; r < RPL; ++r) t[m] = fma(y[r], m < i ? vp[m * MC + lane + 32 * r] : x[m][r], t[m]);
-      }
-#pragma unroll
-      for (int m = 0; m < KC; ++m)
-        if (m != i) t[m] = warp_sum(t[m]);
-      if (lane == 0) {
-        pp[i] = tau;
-        R[pk(c, c)] = beta;
-#pragma unroll
-        for (int m = 0; m < KC; ++m)
-          if (m < i) pp[4 + 4 * i + m] = t[m];
-      }
-#pragma unroll
-      for (int m = 0; m < KC; ++m) {
-        if (m <= i || j0 + m >= k) continue;
-        const double rv = R[pk(c, j0 + m)];
-        const double tw = tau * (rv + t[m]);
-#pragma unroll
-        for (int r = 0; r < RPL; ++r) x[m][r] = fma(-tw, y[r], x[m][r]);
-        __syncwarp();
-        if (lane == 0) R[pk(c, j0 + m)] = rv - tw;
-      }
-#pragma unroll
-      for (int r = 0; r < RPL; ++r) x[i][r] = 0.0;
-      __syncwarp();
-    }
-  };
-
-  // ---- warp w (> p) applies panel p to its 4 columns ----
-  auto apply_panel = [&](int p) {
-    const int j0 = KC * p;
-    const double* vp = vb + (p & 1) * KC * MC;
-    const double* pp = pb + (p & 1) * 32;
-    // 16 partial dots s[c][i] = y_i . x_c over this lane's rows
-    double s[KC * KC];
-#pragma unroll
-    for (int e = 0; e < KC * KC; ++e) s[e] = 0.0;
-#pragma unroll
-    for (int i = 0; i < KC; ++i) {
-#pragma unroll
-      for (int r = 0; r < RPL; ++r) {
-        const double yv = vp[i * MC + lane + 32 * r];
-#pragma unroll
-        for (int c = 0; c < KC; ++c) s[c * KC + i] = fma(yv, x[c][r], s[c * KC + i]);
-      }
-    }
-    // transpose-reduce the 16 values: afterwards lanes 2 e, 2 e + 1 hold the full dot of slot e
-#pragma unroll
-    for (int o = 16, n = KC * KC; n > 1; o >>= 1, n >>= 1) {
-      const bool hi = lane & o;
-#pragma unroll
-      for (int e = 0; e < n / 2; ++e) {
-        const double send = hi ? s[e] : s[e + n / 2];
-        const double keep = hi ? s[e + n / 2] : s[e];
-        s[e] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-      }
-    }
-    double dsum = s[0] + __shfl_xor_sync(0xffffffffu, s[0], 1);
-    // lanes 8 c .. 8 c + 7 hold column c's four dots (slot 4 c + i at lanes 8 c + 2 i, + 1)
-    const int cg = lane >> 3;
-    const int l = KC * w + cg;
-    double sv[KC];
-#pragma unroll
-    for (int i = 0; i < KC; ++i) sv[i] = __shfl_sync(0xffffffffu, dsum, 8 * cg + 2 * i);
-    const bool lok = l < k;
-    double d[KC];
-#pragma unroll
-    for (int i = 0; i < KC; ++i) {
-      const int c = j0 + i;
-      double v = 0.0;
-      if (c < k && lok) {
-        v = R[pk(c, l)] + sv[i];
-#pragma unroll
-        for (int m = 0; m < i; ++m) v = fma(-pp[m] * pp[4 + 4 * i + m], d[m], v);
-      }
-      d[i] = v;
-    }
-    double* dw = db + 16 * w;
-    if ((lane & 7) == 0 && lok) {
-#pragma unroll
-      for (int i = 0; i < KC; ++i) {
-        const int c = j0 + i;
-        if (c < k) {
-          const double td = pp[i] * d[i];
-          R[pk(c, l)] -= td;
-          dw[cg * KC + i] = td;
-        } else {
-          dw[cg * KC + i] = 0.0;
-        }
-      }
-    } else if ((lane & 7) == 0) {
-#pragma unroll
-      for (int i = 0; i < KC; ++i) dw[cg * KC + i] = 0.0;
-    }
-    __syncwarp();
-    double td[KC * KC];
-#pragma unroll
-    for (int e = 0; e < KC * KC; ++e) td[e] = dw[e];
-#pragma unroll
-    for (int i = 0; i < KC; ++i) {
-#pragma unroll
-      for (int r = 0; r < RPL; ++r) {
-        const double yv = vp[i * MC + lane + 32 * r];
-#pragma unroll
-        for (int c = 0; c < KC; ++c) x[c][r] = fma(-td[c * KC + i], yv, x[c][r]);
-      }
-    }
-    __syncwarp();
-  };
-
-  int chunk = 0;
-  for (int64_t base = r0; base < r1; base += MC, ++chunk) {
-    __syncthreads();   // the previous chunk's last panel is applied everywhere
-    if (w < np) {
-#pragma unroll
-      for (int c = 0; c < KC; ++c) {
-        const int l = KC * w + c;
-#pragma unroll
-        for (int r = 0; r < RPL; ++r) {
-          const int64_t row = base + lane + 32 * r;
-          x[c][r] = (row < r1 && l < k) ? q.A[row_off(row) + (int64_t)l * q.ld] : 0.0;
-        }
-      }
-    }
-    if (w == 0) factor_panel(0, base, chunk);
-    for (int p = 0; p < np; ++p) {
-      __syncthreads();   // panel p (y, tau, g) published
-      if (w > p && w < np) {
-        apply_panel(p);
-        if (w == p + 1) factor_panel(p + 1, base, chunk);
-      }
-    }
-  }
-  __syncthreads();
-  const int k1 = q.k1;
-  double* Ro = q.Rout + (int64_t)blockIdx.x * q.ostride;
-  for (int e = threadIdx.x; e < k1 * k; e += blockDim.x) {
-    const int i = e % k1, l = e / k1;
-    Ro[e] = i <= l ? R[pk(i, l)] : 0.0;
-  }
-}
 
 // ------------------------------------------------------------------------------------------
 // Split leaf, pass B: the right-hand-side columns X = b' of a CTA's row range
@@ -844,32 +616,6 @@ static az_status_t tsqr_launch(const QRIn& q, int nblocks, cudaStream_t st) {
   return AZ_OK;
 }
 
-// AZ_TSQR_PANEL=1: the deferred split leaf and its merges use the panel-blocked k_tsqr_p.  Measured
-// slower on c2 (pass A 2.34 vs 1.82 ms, merges 0.79 vs 0.59 ms): with the per-column barrier gone
-// the other warps wait on the owner's in-warp panel chain instead (ncu: 77 % of warp samples at the
-// panel barrier, issue slots 17 % busy) -- the chain of dependent reductions, not the barrier count,
-// sets the step time.  Kept opt-in as the measured alternative.
-static bool tsqr_panel() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("AZ_TSQR_PANEL");
-    v = (e && *e == '1') ? 1 : 0;
-  }
-  return v != 0;
-}
-
-// k_tsqr_p for k = k1 <= 64 (256-row chunks)
-static az_status_t tsqr_panel_launch(const QRIn& q, int nblocks, cudaStream_t st) {
-  constexpr int RPL = 8, MC = 32 * RPL;
-  const size_t sm = ((size_t)q.k * (q.k + 1) / 2 + 2 * 4 * MC + 64 + 16 * 16) * sizeof(double);
-  auto kern = (q.Y && q.bstride) ? k_tsqr_p<RPL, true> : k_tsqr_p<RPL, false>;
-  AZ_CUDA_CHECK(az_smem_attr(kern, sm));
-  AzTrace tr(q.bstride ? "tsqr_merge" : "tsqr_leaf", st, q.m);
-  kern<<<nblocks, 512, sm, st>>>(q);
-  AZ_LAUNCH_CHECK();
-  return AZ_OK;
-}
-
 static az_status_t tsqr_pass(const QRIn& q, int nblocks, cudaStream_t st) {
   // The blocked leaf (k_tsqr_blk) is opt-in (AZ_TSQR_BLK=1): its warp-0 panel factorisation is
   // latency-bound and it measured slower than the per-column kernel on c2 (5.9 vs 3.9 ms).
@@ -1140,8 +886,6 @@ az_status_t az_qr_r_deferred(double* A, int64_t m, int64_t k, int64_t k1, int64_
   q.taus = d.taus0;
   if (def_nw() == 8)
     AZ_TRY((tsqr_launch<8, 4, 8>(q, (int)d.P, st)));
-  else if (tsqr_panel())
-    AZ_TRY(tsqr_panel_launch(q, (int)d.P, st));
   else
     AZ_TRY((tsqr_launch<4, 8>(q, (int)d.P, st)));
   AZ_CUDA_CHECK(cudaEventRecord(ev_leaf, st));
@@ -1161,10 +905,7 @@ az_status_t az_qr_r_deferred(double* A, int64_t m, int64_t k, int64_t k1, int64_
     t.ldY = k1;
     t.taus = L.taus;
     t.cmax = 1;
-    if (tsqr_panel())
-      AZ_TRY(tsqr_panel_launch(t, (int)L.next, st));
-    else
-      AZ_TRY((tsqr_launch<4, 8>(t, (int)L.next, st)));
+    AZ_TRY((tsqr_launch<4, 8>(t, (int)L.next, st)));
   }
   k_copy_R<<<az_div_up(k1 * k1, 256), 256, 0, st>>>(d.buf[d.final_which], (int)k1, (int)k1, Rs, ldrs);
   AZ_LAUNCH_CHECK();
