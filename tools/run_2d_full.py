@@ -34,6 +34,7 @@ t2 = time.time()
 tr = api.trace_report()
 api.trace_enable(False)
 x = x.cpu().numpy() if x is not None else None
+rep = {k: v for k, v in rep.items() if k != "sigma"}
 out = {"config": name, "plan_s": t1 - t0, "solve_s": t2 - t1, "report": rep,
        "kernels_ms": {k: round(v[1], 3) for k, v in sorted(tr.items(), key=lambda kv: -kv[1][1])[:14]}}
 if "--factored" in sys.argv:
