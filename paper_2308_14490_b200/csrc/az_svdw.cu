@@ -551,6 +551,9 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     while (CS < 8 && (int64_t)(n / 2) * CS * 2 <= sms && r / (2 * CS) >= 256) CS *= 2;
+    // more pairs than SMs: a round takes two waves at CS = 1 whose second is partly empty; pairs of
+    // CTAs split each pair's rows instead (c5, 240 pairs: rounds 16.2 -> 14.8 s, CS = 4 16.6 s)
+    if (CS == 1 && (int64_t)(n / 2) > sms && r / 4 >= 256) CS = 2;
     if (const char* e = getenv("AZ_BJAC_CS"))
       if (*e) CS = std::max(1, std::min(8, atoi(e)));
   }
