@@ -306,3 +306,26 @@ def test_box_step1_operator_vanishes():
         b = Av + 0.0
         r = _host(plan.apply_resid(_dev(b)))
         assert np.linalg.norm(r) <= 1e-11 * plan.zstar_norm * plan.sigma_max * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("name,cfg", [("c1", I.get_config("c1")), ("interval_n8192_4step", I.make_config("interval", 8192)),
+                                      ("star_n16", I.make_config("star", 16)), ("disk_n32", I.make_config("disk", 32))],
+                         ids=["c1", "interval_n8192_4step", "star_n16", "disk_n32"])
+def test_step2_entry_matches_oracle(name, cfg, parity_record):
+    """az_step2 (steps 2-3 of Alg. 1 for a given step-1 solution): x = x2 + Z*(b - A x2)
+    against the oracle's operators on random x2 and b, for an odd column count (the complex packing's
+    unpaired last column) and a padded leading dimension."""
+    from paper_2308_14490_b200.api import Plan
+    plan = Plan.from_config(cfg)
+    prob = OA.make_problem(cfg, "dense" if cfg.N <= 2048 else "fft")
+    x2 = I.gaussian_matrix(cfg.N, 3, 71)
+    b = I.gaussian_matrix(plan.rows, 3, 72)
+    big = torch.zeros((3, cfg.N + 3), dtype=torch.float64, device="cuda").t()[: cfg.N]   # ld = N + 3
+    big.copy_(_dev(x2))
+    x = _host(plan.step2(big, _dev(b)))
+    ref = x2 + prob.apply_Zstar(b - prob.apply_A(x2))
+    # forward error of x2 + Z*(b - A x2) in binary64: ||Z*|| (||b|| + ||A|| ||x2||) u-scale
+    for c in range(3):
+        scale = plan.zstar_norm * (np.linalg.norm(b[:, c]) + plan.sigma_max * np.linalg.norm(x2[:, c]))
+        assert np.linalg.norm(x[:, c] - ref[:, c]) <= 1e-12 * scale
+    parity_record(case=cfg.name, op="step2", achieved=float(max(_rel(x[:, c], ref[:, c]) for c in range(3))))
