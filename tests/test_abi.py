@@ -64,3 +64,31 @@ def test_library_exports_nothing_undeclared(libpath):
     exported = {ln.split()[-1] for ln in out.splitlines() if ln.split() and ln.split()[-1].startswith("az_")}
     extra = exported - set(_declared())
     assert not extra, sorted(extra)
+
+
+def test_only_tests_bench_and_smoke_import_the_oracle():
+    """The oracle is test infrastructure: outside tests/ and oracle/ itself, only bench.py (its CPU
+    baseline legs) and __graft_entry__.py (smoke) may import it; the product package never does."""
+    import ast
+    allowed = {"bench.py", "__graft_entry__.py"}
+    offenders = []
+    for dirpath, _, files in os.walk(ROOT):
+        rel = os.path.relpath(dirpath, ROOT)
+        if rel.split(os.sep)[0] in ("tests", "oracle", ".git", "build", "baseline", "gpurun_out"):
+            continue
+        for f in files:
+            if not f.endswith(".py"):
+                continue
+            path = os.path.join(dirpath, f)
+            if os.path.relpath(path, ROOT) in allowed:
+                continue
+            tree = ast.parse(open(path).read())
+            for node in ast.walk(tree):
+                mods = []
+                if isinstance(node, ast.Import):
+                    mods = [a.name for a in node.names]
+                elif isinstance(node, ast.ImportFrom) and node.module:
+                    mods = [node.module]
+                if any(m == "oracle" or m.startswith("oracle.") for m in mods):
+                    offenders.append(os.path.relpath(path, ROOT))
+    assert not offenders, offenders

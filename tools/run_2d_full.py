@@ -1,5 +1,5 @@
-"""Full-size 2-D solves (BASELINE configs c3, c4, c5): time, probes, rank, residual (oracle FFT
-operator), manufactured-solution error on the test grid.
+"""Full-size 2-D solves (BASELINE configs c3, c4, c5): time, probes, rank, per-kernel times, the
+factorisation-reuse path (--factored).
 
     python tools/run_2d_full.py c4 [max_blocks]
 """
@@ -70,13 +70,8 @@ if "--factored" in sys.argv:
     out["factored"] = {"factorize_s": t4 - t3, "nrhs_sweep": sweep, "first_solve_s": t5 - t4, "solve_s": t6 - t5, "report": fac.report,
                        "solve_report": frep,
                        "kernels_ms": {k: round(v[1], 3) for k, v in sorted(ftr.items(), key=lambda kv: -kv[1][1])[:12]}}
-if "--check" in sys.argv:
-    from oracle import az as OA
-    grid = I.test_grid(cfg, 201)
-    f = OA.evaluate(cfg, x, grid)
-    if grid.exact.shape[1]:
-        out["max_err_vs_exact"] = float(np.max(np.abs(f - grid.exact)) / np.max(np.abs(grid.exact)))
-    out["coef_norm_over_sqrtN"] = float(np.linalg.norm(x) / np.sqrt(cfg.N))
-    prob = OA.make_problem(cfg, "fft")
-    out["rel_residual"] = OA.relative_residual(prob, x, b).tolist()
+# (accuracy against the manufactured solution and the oracle is checked by the test suite,
+# tests/test_gpu_wide.py::test_solve_2d_full_size -- only tests/, smoke() and bench.py's CPU
+# baseline run the oracle)
+out["coef_norm_over_sqrtN"] = float(np.linalg.norm(x) / np.sqrt(cfg.N)) if x is not None else None
 print(json.dumps(out))
