@@ -274,3 +274,32 @@ def test_four_step_solve_schedule_variants_agree(env, R, nrhs, tmp_path):
     grid = I.test_grid(cfg)
     f, fa = OA.evaluate(cfg, _host(x), grid), OA.evaluate(cfg, xa, grid)
     assert np.max(np.abs(f - fa)) <= 1e-10 * np.max(np.abs(f))
+
+
+def test_solve_argument_and_size_errors():
+    """Degenerate requests come back as status codes before (or instead of) any wrong result: no right-
+    hand side, no probes, a non-positive threshold, more probe columns than rows, a short workspace."""
+    from paper_2308_14490_b200 import _lib
+    from paper_2308_14490_b200.api import Plan
+    import ctypes as C
+    cfg = I.make_config("star", 16)                # 364 rows
+    plan = Plan.from_config(cfg)
+    b = _dev(I.rhs(cfg))
+    with pytest.raises(_lib.AZError) as e:
+        plan.solve(b, 1e-12, 128, 3)                # 384 probe columns > 364 rows
+    assert e.value.status == 6                      # AZ_ERR_NOT_SUPPORTED
+    x = torch.empty((1, plan.N), dtype=torch.float64, device="cuda").t()
+    ws = torch.empty(16, dtype=torch.uint8, device="cuda")
+    rep = _lib.SolveReport()
+    L = _lib.lib()
+    st = L.az_solve(plan._h, C.c_void_p(b.data_ptr()), plan.rows, C.c_void_p(x.data_ptr()), plan.N, 0, 1e-12, 16, 1,
+                    C.c_void_p(ws.data_ptr()), ws.numel(), C.byref(rep), None)
+    assert st == 1                                  # nrhs = 0: AZ_ERR_INVALID_ARGUMENT
+    st = L.az_solve(plan._h, C.c_void_p(b.data_ptr()), plan.rows, C.c_void_p(x.data_ptr()), plan.N, 1, -1.0, 16, 1,
+                    C.c_void_p(ws.data_ptr()), ws.numel(), C.byref(rep), None)
+    assert st == 1                                  # theta < 0
+    st = L.az_solve(plan._h, C.c_void_p(b.data_ptr()), plan.rows, C.c_void_p(x.data_ptr()), plan.N, 1, 1e-12, 16, 1,
+                    C.c_void_p(ws.data_ptr()), ws.numel(), C.byref(rep), None)
+    assert st == 7                                  # AZ_ERR_WORKSPACE
+    empty = plan.sketch(0, 0)                       # no probe columns: nothing launched, nothing written
+    assert empty.shape == (plan.rows, 0)
