@@ -345,8 +345,11 @@ def solve_host_pipelined(plan: "Plan", b, x, theta: float, R: int, max_blocks: i
     return x
 
 
-def plan_sync(plan: "Plan"):
-    check("az_plan_sync", lib().az_plan_sync(plan._h))
+def plan_sync(plan: "Plan") -> str:
+    """az_plan_sync: wait for the plan's pipelined solves; returns "AZ_OK" or "AZ_WARN_SKETCH_SATURATED"
+    (some single-block pipelined solve since the last sync saturated its sketch)."""
+    st = check("az_plan_sync", lib().az_plan_sync(plan._h), allow=(_lib.AZ_OK, _lib.AZ_WARN_SKETCH_SATURATED))
+    return _lib.STATUS.get(st, st)
 
 
 def _report(rep, status, workspace=None):

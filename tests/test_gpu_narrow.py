@@ -183,9 +183,8 @@ def test_pipelined_saturation_is_reported_by_plan_sync():
     b = torch.from_numpy(np.asfortranarray(I.rhs(cfg))).t().contiguous().pin_memory().t()
     xh = torch.empty((1, cfg.N), dtype=torch.float64).pin_memory().t()
     api.solve_host_pipelined(plan, b, xh, 1e-12, 16, 1)
-    st = _lib.lib().az_plan_sync(plan._h)
-    assert st == _lib.AZ_WARN_SKETCH_SATURATED
-    assert _lib.lib().az_plan_sync(plan._h) == _lib.AZ_OK
+    assert api.plan_sync(plan) == "AZ_WARN_SKETCH_SATURATED"
+    assert api.plan_sync(plan) == "AZ_OK"
     cfg2 = I.make_config("interval", 256, R=40)
     plan2 = api.Plan.from_config(cfg2)
     api.solve_host_pipelined(plan2, b, xh, 1e-12, 40, 1)
