@@ -53,6 +53,7 @@ typedef enum {
   AZ_ERR_CUDA = 5,
   AZ_ERR_NOT_SUPPORTED = 6,     /* size/oversampling outside the supported FFT lengths              */
   AZ_ERR_WORKSPACE = 7,         /* workspace too small                                              */
+  AZ_ERR_NCCL = 8,              /* a collective of the multi-GPU solve failed (NCCL error or async error) */
   AZ_WARN_SKETCH_SATURATED = 100 /* rank == probes - p after max_blocks probe blocks (x still written) */
 } az_status_t;
 

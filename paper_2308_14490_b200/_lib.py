@@ -15,6 +15,7 @@ AZ_OK = 0
 AZ_WARN_SKETCH_SATURATED = 100
 STATUS = {0: "AZ_OK", 1: "AZ_ERR_INVALID_ARGUMENT", 2: "AZ_ERR_OVERSAMPLING", 3: "AZ_ERR_SINGULAR_SYMBOL",
           4: "AZ_ERR_OUT_OF_MEMORY", 5: "AZ_ERR_CUDA", 6: "AZ_ERR_NOT_SUPPORTED", 7: "AZ_ERR_WORKSPACE",
+          8: "AZ_ERR_NCCL",
           100: "AZ_WARN_SKETCH_SATURATED"}
 
 

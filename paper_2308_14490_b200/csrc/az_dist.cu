@@ -39,6 +39,7 @@ struct Nccl {
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -61,6 +62,7 @@ Nccl& nccl() {
     sym(n.Broadcast, "ncclBroadcast");
     sym(n.Send, "ncclSend");
     sym(n.Recv, "ncclRecv");
+    sym(n.CommGetAsyncError, "ncclCommGetAsyncError");
     sym(n.GroupStart, "ncclGroupStart");
     sym(n.GroupEnd, "ncclGroupEnd");
     sym(n.GetErrorString, "ncclGetErrorString");
@@ -76,7 +78,7 @@ Nccl& nccl() {
     ncclResult_t _r = (call);                                                            \
     if (_r != ncclSuccess) {                                                             \
       az_set_error("%s:%d %s: %s", __FILE__, __LINE__, #call, nccl().GetErrorString(_r)); \
-      return AZ_ERR_CUDA;                                                                \
+      return AZ_ERR_NCCL;                                                                \
     }                                                                                    \
   } while (0)
 
@@ -150,7 +152,7 @@ extern "C" az_status_t az_comm_create(int32_t world, int32_t rank, const void* i
   if (r != ncclSuccess) {
     az_set_error("az_comm_create: ncclCommInitRank: %s", nccl().GetErrorString(r));
     delete c;
-    return AZ_ERR_CUDA;
+    return AZ_ERR_NCCL;
   }
   *out = c;
   return AZ_OK;
@@ -342,6 +344,13 @@ extern "C" az_status_t az_solve_sharded(az_plan_t p, az_comm_t c, const double* 
                                       N * sizeof(double), N * sizeof(double), cg, cudaMemcpyDeviceToDevice, st));
   }
   AZ_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (nccl().CommGetAsyncError) {   // a peer failing mid-collective surfaces here, not as a hang later
+    ncclResult_t ae = ncclSuccess;
+    if (nccl().CommGetAsyncError(c->comm, &ae) == ncclSuccess && ae != ncclSuccess) {
+      az_set_error("az_solve_sharded: NCCL async error: %s", nccl().GetErrorString(ae));
+      return AZ_ERR_NCCL;
+    }
+  }
   if (report) {
     memset(report, 0, sizeof(*report));
     report->rank_used = rank;

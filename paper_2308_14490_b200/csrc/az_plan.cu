@@ -118,6 +118,7 @@ extern "C" const char* az_status_string(az_status_t s) {
     case AZ_ERR_CUDA: return "AZ_ERR_CUDA";
     case AZ_ERR_NOT_SUPPORTED: return "AZ_ERR_NOT_SUPPORTED";
     case AZ_ERR_WORKSPACE: return "AZ_ERR_WORKSPACE";
+    case AZ_ERR_NCCL: return "AZ_ERR_NCCL";
     case AZ_WARN_SKETCH_SATURATED: return "AZ_WARN_SKETCH_SATURATED";
   }
   return "AZ_UNKNOWN";
