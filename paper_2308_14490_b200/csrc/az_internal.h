@@ -85,8 +85,10 @@ constexpr int TWN = 2048;
 constexpr int TW4B = 11;
 
 // --- 1-D small layout (az_ops1d.cu)
+// zout (OP_STEP1 / OP_RESID only): also write M = Omega - Z* A Omega / Z* b (N x nvec, ld ldz)
 az_status_t az1s_apply(az_plan_s* p, int op, int src, const double* in, int64_t ldin, double* out,
-                       int64_t ldout, int64_t nvec, int64_t col0, cudaStream_t st);
+                       int64_t ldout, int64_t nvec, int64_t col0, cudaStream_t st, double* zout = nullptr,
+                       int64_t ldz = 0);
 az_status_t az1s_fft_table(az_plan_s* p, cplx* data, int64_t len, cudaStream_t st);
 
 // --- 1-D four-step layout (az_ops1f.cu)

@@ -38,6 +38,10 @@ struct P1s {
   int win;
   const double* bw;
   const int32_t* bj;
+  // optional (OP_STEP1 / OP_RESID, step 2 by linearity, reading R30): the coefficient vector whose
+  // spectrum the chain forms anyway -- M = Omega - Z* A Omega (step 1) or Z* b (resid) -- to zout
+  double* zout;
+  int64_t ldz;
 };
 
 // beta sum_t bw[b][t] coef[(j0_b + t) mod n] for boundary point b, by one thread (win <= 64 terms;
@@ -53,8 +57,19 @@ AZ_D cplx boundary_dot(const P1s& a, int b, F coef) {
   return cscale(acc, a.beta);
 }
 
-AZ_D cplx sym1(const P1s& a, int kf) {
-  return a.lap ? cscale(cadd(a.W2[kf], cscale(a.W0[kf], a.k0sq)), a.alpha) : a.W0[kf];
+AZ_D void cpa16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
+// shared memory of one chain CTA: the transform buffer, the n-point spectrum, and the plan tables
+// (symbol W, and W'' for the Laplacian rows; 1/sigma^2; the row map), staged once per CTA by one
+// batch of cp.async -- a CTA of L/8 threads has no other warps to hide a table load's latency,
+// and the loops that read them would otherwise wait on one round trip per iteration
+template <int L>
+AZ_HD size_t chain1s_smem(int n, int lap) {
+  return (size_t)(spad_len(L) + n + L * (lap ? 2 : 1)) * sizeof(cplx) + (size_t)n * sizeof(double) +
+         (size_t)L * sizeof(int32_t);
 }
 
 template <int L, int OP, int SRC>
@@ -65,6 +80,20 @@ __global__ void __launch_bounds__(L / 8) k_chain1s(P1s a) {
   constexpr int NT = L / 8;
   const int tid = threadIdx.x;
   const int n = a.n, s = a.s;
+  cplx* W0s = aux + n;                  // L
+  cplx* W2s = W0s + L;                  // L (Laplacian rows only)
+  double* zs = (double*)(W0s + L * (a.lap ? 2 : 1));   // n
+  int32_t* ps = (int32_t*)(zs + n);     // L
+  for (int i = tid; i < L; i += NT) {
+    cpa16(W0s + i, a.W0 + i);
+    if (a.lap) cpa16(W2s + i, a.W2 + i);
+  }
+  for (int i = tid; 2 * i < n; i += NT) cpa16(zs + 2 * i, a.zinv + 2 * i);
+  for (int i = tid; 4 * i < L; i += NT) cpa16(ps + 4 * i, a.pos + 4 * i);
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  auto sym = [&](int kf) { return a.lap ? cscale(cadd(W2s[kf], cscale(W0s[kf], a.k0sq)), a.alpha) : W0s[kf]; };
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
   const int64_t cre = 2 * (int64_t)blockIdx.x, cim = cre + 1;
   const bool has_im = cim < a.nvec;
   const double invL = 1.0 / (double)L;
@@ -102,13 +131,13 @@ __global__ void __launch_bounds__(L / 8) k_chain1s(P1s a) {
     if constexpr (OP == OP_STEP1) {
       for (int k = tid; k < n; k += NT) aux[k] = buf[spad(k)];   // v^ kept for r^ = v^ - w^
     }
-    for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = cscale(cmul(buf[spad(kf)], sym1(a, kf)), invL);
+    for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = cscale(cmul(buf[spad(kf)], sym(kf)), invL);
     __syncthreads();
     fft_smem<L, 1>(buf, tid, a.tw, TWN);           // A^c a on the full grid
     if constexpr (OP == OP_STEP1) {
       // E R: keep the collocation points only
       for (int q = tid; q < L; q += NT)
-        if (a.pos[q] < 0) buf[spad(q)] = czero();
+        if (ps[q] < 0) buf[spad(q)] = czero();
       __syncthreads();
       fft_smem<L, -1>(buf, tid, a.tw, TWN);
       // B^dag P fold + spectral division, then r^ = v^ - w^
@@ -116,17 +145,23 @@ __global__ void __launch_bounds__(L / 8) k_chain1s(P1s a) {
         cplx acc = czero();
         for (int m = 0; m < s; ++m) {
           const int kf = k + m * n;
-          acc = cadd(acc, cmulc(buf[spad(kf)], sym1(a, kf)));
+          acc = cadd(acc, cmulc(buf[spad(kf)], sym(kf)));
         }
-        aux[k] = csub(aux[k], cscale(acc, a.zinv[k]));
+        aux[k] = csub(aux[k], cscale(acc, zs[k]));
       }
       __syncthreads();
-      if (a.Mb > 0) {
-        // boundary rows of (A - A Z* A) v = A^b r, r = v - Z* A v: r from its spectrum r^ (aux),
-        // IFFT_L(extend r^)[s j] / L = r_j
+      if (a.Mb > 0 || a.zout) {
+        // r = v - Z* A v from its spectrum r^ (aux), IFFT_L(extend r^)[s j] / L = r_j: the boundary
+        // rows of (A - A Z* A) v = A^b r, and M's column pair
         for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = aux[kf & (n - 1)];
         __syncthreads();
         fft_smem<L, 1>(buf, tid, a.tw, TWN);
+        if (a.zout)
+          for (int j = tid; j < n; j += NT) {
+            const cplx v = cscale(buf[spad(j * s)], invL);
+            a.zout[j + cre * a.ldz] = v.x;
+            if (has_im) a.zout[j + cim * a.ldz] = v.y;
+          }
         for (int bp = tid; bp < a.Mb; bp += NT) {
           const cplx yb = boundary_dot(a, bp, [&](int j) { return cscale(buf[spad(j * s)], invL); });
           a.out[a.M + bp + cre * a.ldout] = yb.x;
@@ -134,13 +169,13 @@ __global__ void __launch_bounds__(L / 8) k_chain1s(P1s a) {
         }
         __syncthreads();
       }
-      for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = cscale(cmul(aux[kf & (n - 1)], sym1(a, kf)), invL);
+      for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = cscale(cmul(aux[kf & (n - 1)], sym(kf)), invL);
       __syncthreads();
       fft_smem<L, 1>(buf, tid, a.tw, TWN);
     }
     // ---- R: gather the collocation rows ----
     for (int q = tid; q < L; q += NT) {
-      const int r = a.pos[q];
+      const int r = ps[q];
       if (r >= 0) {
         const cplx v = buf[spad(q)];
         a.out[r + cre * a.ldout] = v.x;
@@ -150,7 +185,7 @@ __global__ void __launch_bounds__(L / 8) k_chain1s(P1s a) {
   } else {
     // ---- row input, E: zero padding onto the fine grid ----
     for (int q = tid; q < L; q += NT) {
-      const int r = a.pos[q];
+      const int r = ps[q];
       cplx v = czero();
       if (r >= 0) v = make_double2(a.in[r + cre * a.ldin], has_im ? a.in[r + cim * a.ldin] : 0.0);
       buf[spad(q)] = v;
@@ -161,17 +196,23 @@ __global__ void __launch_bounds__(L / 8) k_chain1s(P1s a) {
       cplx acc = czero();
       for (int m = 0; m < s; ++m) {
         const int kf = k + m * n;
-        acc = cadd(acc, cmulc(buf[spad(kf)], sym1(a, kf)));
+        acc = cadd(acc, cmulc(buf[spad(kf)], sym(kf)));
       }
-      aux[k] = (OP == OP_AT) ? acc : cscale(acc, a.zinv[k]);
+      aux[k] = (OP == OP_AT) ? acc : cscale(acc, zs[k]);
     }
     __syncthreads();
     if constexpr (OP == OP_RESID) {
-      if (a.Mb > 0) {
-        // boundary rows of (I - A Z*) b: b_b - A^b w, w = Z* b from its spectrum (aux)
+      if (a.Mb > 0 || a.zout) {
+        // w = Z* b from its spectrum (aux): the boundary rows of (I - A Z*) b, b_b - A^b w, and Z* b
         for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = aux[kf & (n - 1)];
         __syncthreads();
         fft_smem<L, 1>(buf, tid, a.tw, TWN);
+        if (a.zout)
+          for (int j = tid; j < n; j += NT) {
+            const cplx v = cscale(buf[spad(j * s)], invL);
+            a.zout[j + cre * a.ldz] = v.x;
+            if (has_im) a.zout[j + cim * a.ldz] = v.y;
+          }
         for (int bp = tid; bp < a.Mb; bp += NT) {
           const cplx yb = boundary_dot(a, bp, [&](int j) { return cscale(buf[spad(j * s)], invL); });
           const int64_t r = a.M + bp;
@@ -180,7 +221,7 @@ __global__ void __launch_bounds__(L / 8) k_chain1s(P1s a) {
         }
         __syncthreads();
       }
-      for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = cscale(cmul(aux[kf & (n - 1)], sym1(a, kf)), invL);
+      for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = cscale(cmul(aux[kf & (n - 1)], sym(kf)), invL);
     } else {
       for (int kf = tid; kf < L; kf += NT) buf[spad(kf)] = aux[kf & (n - 1)];
     }
@@ -188,7 +229,7 @@ __global__ void __launch_bounds__(L / 8) k_chain1s(P1s a) {
     fft_smem<L, 1>(buf, tid, a.tw, TWN);
     if constexpr (OP == OP_RESID) {
       for (int q = tid; q < L; q += NT) {
-        const int r = a.pos[q];
+        const int r = ps[q];
         if (r >= 0) {
           const cplx v = buf[spad(q)];
           a.out[r + cre * a.ldout] = a.in[r + cre * a.ldin] - v.x;
@@ -217,7 +258,7 @@ __global__ void __launch_bounds__(L / 8) k_chain1s(P1s a) {
 
 template <int L>
 static az_status_t launch1s(const P1s& a, int op, int src, int64_t npairs, cudaStream_t st) {
-  const size_t sm = (size_t)(spad_len(L) + a.n) * sizeof(cplx);
+  const size_t sm = chain1s_smem<L>(a.n, a.lap);
   const dim3 grid((unsigned)npairs), block(L / 8);
   AzTrace tr("1d_chain", st, npairs);
 #define AZ_L1S(OPV, SRCV) (az_smem_attr(k_chain1s<L, OPV, SRCV>, sm), k_chain1s<L, OPV, SRCV><<<grid, block, sm, st>>>(a))
@@ -233,8 +274,10 @@ static az_status_t launch1s(const P1s& a, int op, int src, int64_t npairs, cudaS
 }
 
 az_status_t az1s_apply(az_plan_s* p, int op, int src, const double* in, int64_t ldin, double* out,
-                       int64_t ldout, int64_t nvec, int64_t col0, cudaStream_t st) {
+                       int64_t ldout, int64_t nvec, int64_t col0, cudaStream_t st, double* zout, int64_t ldz) {
   P1s a;
+  a.zout = (op == OP_STEP1 || op == OP_RESID) ? zout : nullptr;
+  a.ldz = ldz;
   a.W0 = p->d_W0;
   a.W2 = p->d_W2;
   a.zinv = p->d_zinv;

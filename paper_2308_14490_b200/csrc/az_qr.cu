@@ -608,7 +608,9 @@ static az_status_t tsqr_launch(const QRIn& q, int nblocks, cudaStream_t st) {
   const size_t sm = ((size_t)q.k * (q.k + 1) / 2 + 2 * MC + 2) * sizeof(double);
   // (a separate instantiation for the merges' stacked reflector store keeps the leaf's owner
   // chain free of it)
-  auto kern = (q.Y && q.bstride) ? k_tsqr<KC, RPL, true, NW> : k_tsqr<KC, RPL, false, NW>;
+  auto kern = k_tsqr<KC, RPL, false, NW>;
+  if constexpr (RPL == 8 || RPL == 4)   // (merges run the 256- / 128-row shapes only)
+    if (q.Y && q.bstride) kern = k_tsqr<KC, RPL, true, NW>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   AzTrace tr(q.bstride ? "tsqr_merge" : "tsqr_leaf", st, q.m);
   kern<<<nblocks, 32 * NW, sm, st>>>(q);
@@ -708,7 +710,10 @@ az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R
     }
     return qr_r_wide(A, m, k, lda, R, ldr, ws, ws_bytes, st);
   }
-  const int64_t P = std::max<int64_t>(1, std::min<int64_t>(num_sms(), (m + 127) / 128));
+  // a sketch of at most 288 rows (c1: 257) is one chunk of one CTA: k1 column steps in all, no
+  // merge, the right-hand sides riding along (instead of 3 leaf CTAs, pass B and a merge level)
+  const bool one = m <= 288 && k <= 64;
+  const int64_t P = one ? 1 : std::max<int64_t>(1, std::min<int64_t>(num_sms(), (m + 127) / 128));
   double* buf[2] = {(double*)ws, (double*)ws + P * k * k};
   QRIn q;
   q.A = A;
@@ -726,7 +731,12 @@ az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R
   q.taus = nullptr;
   q.cmax = 0;
   const int64_t nb = k - k1;
-  if (a_scratch && k1 < k && k1 <= 64 && nb <= 64 && tsqr_split()) {
+  if (one) {
+    if (k <= 32)
+      AZ_TRY((tsqr_launch<2, 9>(q, 1, st)));
+    else
+      AZ_TRY((tsqr_launch<4, 9>(q, 1, st)));
+  } else if (a_scratch && k1 < k && k1 <= 64 && nb <= 64 && tsqr_split()) {
     // split leaf: pass A triangularises the k1 probe columns alone in 256-row chunks (KC = 4,
     // RPL = 8: half the column steps per row of the 128-column pass) and keeps each chunk's
     // reflectors in place of those columns; pass B applies them to the right-hand sides in

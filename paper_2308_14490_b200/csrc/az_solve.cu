@@ -166,15 +166,20 @@ __global__ void k_gemm_mn_small(const double* A, int64_t lda, const double* Bm, 
                                 int64_t m, int k, int n, const double* C, int64_t ldc, double sgn = -1.0);
 __global__ void k_identity_cols(double* Rf, int64_t ld, int64_t k, int64_t col0);
 
-// four-step narrow solves: step 2 as x = Z* b + M y from the b' and sketch chains (reading R30;
-// AZ_STEP2_LINEAR=0 disables)
-static bool step2_linear() {
+// 1-D narrow solves (four-step and one-CTA layouts): step 2 as x = Z* b + M y from the b' and sketch
+// chains (reading R30; AZ_STEP2_LINEAR=0 disables).  Its rounding error is of the order
+// u ||Z*|| ||b|| (Z* b and (Z* A Omega) y cancel), against u ||Z*|| ||b - A x2|| for the residual form
+// x2 + Z* (b - A x2): it is used only while ||Z*|| <= 1e5 (c1 / c2: 2.7e3; the paper's own eps regime
+// reaches 1e9, where the residual form is kept)
+static bool step2_linear(const az_plan_s* p) {
   static int k = -1;
   if (k < 0) {
     const char* e = getenv("AZ_STEP2_LINEAR");
     k = e ? atoi(e) : 1;
   }
-  return k != 0;
+  const double sd = p->dim == 1 ? (double)p->s : (double)(p->s * p->s);
+  const double zstar_norm = p->sigma_min_kept2 > 0 ? 1.0 / std::sqrt(p->sigma_min_kept2 / sd) : 1e300;
+  return k != 0 && zstar_norm <= 1e5;
 }
 
 // AZ_QR_DEFER=0: Q^T b' rides along in the TSQR merges (on the R factor's critical path) instead of
@@ -244,13 +249,14 @@ static SolveWS layout(az_plan_s* p, int64_t nrhs, int64_t R, int32_t max_blocks,
   w.tmp = (double*)take(sizeof(double) * rows * nrhs);
   w.x2 = (double*)take(sizeof(double) * p->N * nrhs);
   w.wide = kt > AZ_NARROW_MAX;
-  const bool keep = !w.wide && p->layout == AZ_LAYOUT_1D_FOURSTEP && step2_linear();
+  const bool four = p->layout == AZ_LAYOUT_1D_FOURSTEP;
+  const bool keep = !w.wide && (four || p->layout == AZ_LAYOUT_1D_SMALL) && step2_linear(p);
   w.Zb = keep ? (double*)take(sizeof(double) * p->N * nrhs) : nullptr;
-  w.Zs = keep ? (cplx*)take(sizeof(cplx) * p->N * ((nrhs + 1) / 2)) : nullptr;
+  w.Zs = keep && four ? (cplx*)take(sizeof(cplx) * p->N * ((nrhs + 1) / 2)) : nullptr;
   w.Om = keep ? (double*)take(sizeof(double) * p->N * Rmax) : nullptr;
-  w.Rp = keep ? (double*)take(sizeof(double) * Rmax * 2 * Rmax) : nullptr;
-  w.Pm = keep ? (double*)take(sizeof(double) * Rmax * Rmax) : nullptr;
-  w.cq = keep ? (double*)take(sizeof(double) * Rmax * nrhs) : nullptr;
+  w.Rp = keep && four ? (double*)take(sizeof(double) * Rmax * 2 * Rmax) : nullptr;
+  w.Pm = keep && four ? (double*)take(sizeof(double) * Rmax * Rmax) : nullptr;
+  w.cq = keep && four ? (double*)take(sizeof(double) * Rmax * nrhs) : nullptr;
   if (w.wide) {
     const int64_t QBw = az_qrw_panel_width();
     w.maxpanels = max_blocks * ((R + QBw - 1) / QBw);
@@ -392,8 +398,10 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
   // Q^T b' off the R factor's critical path: R_S alone through the merge tree, P = pinv_theta(R_S) by
   // the SVD of [R_S | I], while b' follows the kept reflectors on the side stream; y = P (Q^T b')
   const bool defer = side && qr_defer() && R <= 64 && nrhs <= 64 && w.Rp;
-  if (w.Zb) {   // b' and, for step 2, Z* b (one extra column pass)
+  if (w.Zb && w.Zs) {   // b' and, for step 2, Z* b (one extra column pass)
     AZ_TRY(az1f_resid_z(p, b, ldb, bp_in_S ? w.S + R * rows : w.bp, rows, w.Zb, p->N, nrhs, st, w.Zs, side));
+  } else if (w.Zb) {    // one-CTA layout: Z* b from the chain's spectrum of it (one more transform)
+    AZ_TRY(az1s_apply(p, OP_RESID, SRC_VEC, b, ldb, bp_in_S ? w.S + R * rows : w.bp, rows, nrhs, 0, st, w.Zb, p->N));
   } else {
     AZ_TRY(az_apply_op(p, OP_RESID, b, ldb, bp_in_S ? w.S + R * rows : w.bp, rows, nrhs, st));
   }
@@ -413,12 +421,13 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
     const int64_t kt = kp + nrhs;
     cudaEvent_t e0 = ev.e[2], e1 = ev.e[3], e2 = ev.e[4], e3 = ev.e[5];
     cudaEventRecord(e0, st);
-    if (w.Om) {   // the sketch and M = Omega - Z* A Omega for step 2
+    if (w.Om && w.Zs) {   // the sketch and M = Omega - Z* A Omega for step 2
       AZ_TRY(az1f_sketch_m(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, w.Om + (nb - 1) * R * p->N, p->N, st,
                            nullptr, side));
-
-    }
-    else
+    } else if (w.Om) {
+      AZ_TRY(az1s_apply(p, OP_STEP1, SRC_PROBE, nullptr, 0, w.S + (nb - 1) * R * rows, rows, R, (nb - 1) * R, st,
+                        w.Om + (nb - 1) * R * p->N, p->N));
+    } else
       AZ_TRY(az_sketch(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, st));
     if (!w.wide && !bp_in_S) {
       AzTrace tr("elementwise", st);
@@ -1069,7 +1078,7 @@ extern "C" az_status_t az_factorize(az_plan_t p, double theta, int64_t R, int32_
   }
   // four-step layout with at most 64 probes: keep A Omega (step 2 of a factored solve is then one
   // small GEMM and three FFT passes)
-  if (p->layout == AZ_LAYOUT_1D_FOURSTEP && kpmax <= 64 && step2_linear() &&
+  if (p->layout == AZ_LAYOUT_1D_FOURSTEP && kpmax <= 64 && step2_linear(p) &&
       cudaMalloc(&f->Mm, sizeof(double) * p->N * kpmax) != cudaSuccess) {
     cudaGetLastError();
     f->Mm = nullptr;

@@ -24,10 +24,18 @@ AZ_D double wsum(double v) {
 
 __device__ int g_small_sweeps;
 
-AZ_D double hsum(double v) {   // sum over the 16 lanes of a half warp
+// three sums over the 16 lanes of a half warp, the levels interleaved (written out: left to the
+// compiler the three reductions ran one after another, a chain of 12 dependent shuffles)
+AZ_D void hsum3(double& a, double& b, double& g) {
 #pragma unroll
-  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+  for (int o = 8; o > 0; o >>= 1) {
+    const double ta = __shfl_xor_sync(0xffffffffu, a, o);
+    const double tb = __shfl_xor_sync(0xffffffffu, b, o);
+    const double tg = __shfl_xor_sync(0xffffffffu, g, o);
+    a += ta;
+    b += tb;
+    g += tg;
+  }
 }
 
 // One CTA, r <= 16 EPL.  A pair (p, q) of columns of B = R_S^T is handled by a HALF warp, each lane
@@ -35,7 +43,7 @@ AZ_D double hsum(double v) {   // sum over the 16 lanes of a half warp
 // one SM, so the instruction count per pair is what matters (no modulo arithmetic, unrolled
 // element loops, 4-level reductions, no shared atomics).
 template <int EPL>
-__global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int64_t ldr, int r, int nrhs,
+__global__ void __launch_bounds__(EPL <= 4 ? 512 : 1024, 1) k_jacobi_small(const double* Rf, int64_t ldr, int r, int nrhs,
                                                           double theta, double* y, int64_t ldy, double* sig_out,
                                                           int64_t* rank_dev, int max_sweeps) {
   extern __shared__ double sm[];
@@ -44,8 +52,9 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
   double* nrm2 = Cm + r * nrhs;        // r
   // per-half-warp sweep statistics, reduced once per sweep
   __shared__ int rot_h[64];
-  __shared__ double off_h[64];
+  __shared__ int big_h[64];
   __shared__ double smax2_sweep;
+  __shared__ unsigned char quiet[AZ_NARROW_MAX];   // column in the sweep's negligible set S
   const double tol = 1.1102230246251565e-16 * sqrt((double)r);   // rotation threshold
   const int tid = threadIdx.x, nth = blockDim.x;
   const int w = tid >> 5, lane = tid & 31, nw = nth >> 5;
@@ -70,14 +79,27 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
       if (lane == 0) nrm2[i] = a;
     }
     __syncthreads();
-    if (tid == 0) {
+    // S = the columns with norm^2 below nu = theta^2 smax^2 / 4.  When their total is below nu as
+    // well, every singular value of S's span is below theta sigma_1 / 2 (||X_S||_2 <= ||X_S||_F), so
+    // pairs inside S are neither rotated nor counted for convergence this sweep: the rotations against
+    // the other columns still make those orthogonal to S, and by Weyl the kept singular values and
+    // vectors are those of the other columns alone (reading R34).  The columns of S are not
+    // diagonalised among themselves (their reported values are column norms below theta sigma_1 / 2).
+    if (w == 0) {
       double m = 0.0;
-      for (int i = 0; i < r; ++i) m = fmax(m, nrm2[i]);
-      smax2_sweep = m;
+      for (int i = lane; i < r; i += 32) m = fmax(m, nrm2[i]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      const double nu = 0.25 * theta * theta * m;
+      double tail = 0.0;
+      for (int i = lane; i < r; i += 32) tail += nrm2[i] < nu ? nrm2[i] : 0.0;
+      tail = wsum(tail);
+      for (int i = lane; i < r; i += 32) quiet[i] = tail < nu && nrm2[i] < nu;
+      if (lane == 0) smax2_sweep = m;
     }
     __syncthreads();
     const double negl = (1e-3 * theta) * (1e-3 * theta) * smax2_sweep;
-    double off_me = 0.0;
+    int big_me = 0;   // pairs whose cosine exceeds the convergence level 8 tol
     int rot_me = 0;
     for (int round = 0; round < n - 1; ++round) {
       // both halves of a warp run the same trip count (the shuffles span the whole warp)
@@ -110,12 +132,11 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
           b = fma(xq[e], xq[e], b);
           g = fma(xp[e], xq[e], g);
         }
-        a = hsum(a);
-        b = hsum(b);
-        g = hsum(g);
-        if (!pair_ok || fmin(a, b) < negl || g == 0.0) continue;
+        const bool qq = pair_ok && (quiet[p] & quiet[q]);
+        hsum3(a, b, g);
+        if (!pair_ok || fmin(a, b) < negl || g == 0.0 || qq) continue;
         const double g2 = g * g, ab = a * b;
-        if (g2 > off_me * ab) off_me = g2 / ab;   // running max of g^2 / ab, divides only on a new max
+        big_me += g2 > (64.0 * tol * tol) * ab;
         if (!(g2 > tol * tol * ab)) continue;
         // tan of the rotation angle, t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (b - a) / 2g,
         // written without the intermediate division: t = 2 g sign(b - a) / (|b - a| + sqrt((b - a)^2 + 4 g^2))
@@ -144,18 +165,17 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi_small(const double* Rf, int6
     }
     if (hl == 0) {
       rot_h[hw] = rot_me;
-      off_h[hw] = off_me;
+      big_h[hw] = big_me;
     }
     __syncthreads();
-    int rots = 0;
-    double offm = 0.0;
+    int rots = 0, bigs = 0;
     for (int i = 0; i < nh; ++i) {
       rots += rot_h[i];
-      offm = fmax(offm, off_h[i]);
+      bigs += big_h[i];
     }
-    // converged: no rotation, or every measured off-diagonal at the rounding level of the dots
+    // converged: no rotation, or every measured off-diagonal cosine at the rounding level of the dots
     if (tid == 0) g_small_sweeps = sweep + 1;
-    if (rots == 0 || sqrt(offm) <= 8.0 * tol) break;
+    if (rots == 0 || bigs == 0) break;
     __syncthreads();
   }
   // singular values = column norms of B W
