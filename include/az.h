@@ -200,10 +200,19 @@ az_status_t az_solve_workspace_size(az_plan_t plan, int64_t nrhs, int64_t R, int
  * way and moves to the blocked path (drawing its blocks afresh) only if that block saturated.
  * report: HOST, may be NULL.  ALWAYS synchronises the stream before returning (whether or not a
  * report is requested), so x, the workspace and the status are final on return.  Returns
- * AZ_WARN_SKETCH_SATURATED (x still written) if the last block saturated.                     */
+ * AZ_WARN_SKETCH_SATURATED (x still written) if the last block saturated.
+ * CUDA graphs: a single-block narrow solve (max_blocks = 1, or the first block of an adaptive solve;
+ * one-CTA 1-D and 2-D layouts) whose arguments (b, ldb, x, ldx, nrhs, theta, R, workspace) repeat
+ * those of the plan's previous such call is captured into a graph owned by the plan (at most 4 per
+ * plan) and replayed on later calls with the same arguments: same kernels, same results; b and the
+ * workspace are read at replay, so their contents may change between calls, but b, x and the
+ * workspace must stay allocated at those addresses while the plan lives (az_plan_destroy frees the
+ * graphs).  Disabled by AZ_SOLVE_GRAPH=0 and while tracing is on.                             */
 az_status_t az_solve(az_plan_t plan, const double* b, int64_t ldb, double* x, int64_t ldx,
                      int64_t nrhs, double theta, int64_t R, int32_t max_blocks,
                      void* workspace, size_t ws_bytes, az_solve_report_t* report, void* stream);
+/* Number of solve graphs the plan holds (diagnostics / tests). */
+int32_t az_solve_graph_count(az_plan_t plan);
 
 /* Host-buffer convenience: b (HOST, (M+Mb) x nrhs) -> x (HOST, N x nrhs), including the
  * host<->device copies (pinned staging owned by the plan).  Used for end-to-end timing.      */

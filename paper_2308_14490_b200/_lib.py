@@ -105,6 +105,8 @@ def lib():
     L.az_trace_report.restype = C.c_int
     L.az_svd_sweeps_last.argtypes = [C.c_int]
     L.az_svd_sweeps_last.restype = C.c_int
+    L.az_solve_graph_count.argtypes = [C.c_void_p]
+    L.az_solve_graph_count.restype = C.c_int32
     L.az_launch_count.argtypes = [C.c_int]
     L.az_launch_count.restype = C.c_int64
     _lib = L
@@ -117,7 +119,7 @@ EXPORTED = ["az_plan_create", "az_plan_destroy", "az_plan_query", "az_apply_A", 
             "az_solve_workspace_size", "az_solve", "az_solve_host", "az_status_string",
             "az_last_error", "az_launch_count", "az_trace_enable", "az_trace_report",
             "az_factorize", "az_factor_destroy", "az_factor_query", "az_factor_workspace_size",
-            "az_solve_factored", "az_solve_host_pipelined", "az_plan_sync", "az_svd_sweeps_last",
+            "az_solve_factored", "az_solve_host_pipelined", "az_plan_sync", "az_svd_sweeps_last", "az_solve_graph_count",
             "az_step2_workspace_size", "az_step2", "az_comm_unique_id", "az_comm_create", "az_comm_destroy",
             "az_solve_sharded"]
 

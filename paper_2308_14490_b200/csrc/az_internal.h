@@ -79,7 +79,11 @@ struct az_plan_s {
   // high-priority stream for the TSQR and the SVD while the side stream runs: the block scheduler
   // then hands freed SMs to the merge tree (the critical path) before the side stream's passes
   cudaStream_t hi = nullptr;
+  // CUDA graphs of repeated single-block narrow solves (az_solve.cu)
+  struct az_graphs_s* graphs = nullptr;
 };
+void az_graphs_free(az_plan_s* p);
+bool az_trace_active();
 
 constexpr int TWN = 2048;
 constexpr int TW4B = 11;

@@ -45,6 +45,8 @@ std::vector<TraceRec> g_tr;
 size_t g_tr_used = 0;
 }  // namespace
 
+bool az_trace_active() { return g_tr_on; }
+
 AzTrace::AzTrace(const char* name, cudaStream_t s, int64_t units) : slot(-1), st(s) {
   if (!g_tr_on) return;
   std::lock_guard<std::mutex> lk(g_tr_mu);
@@ -375,6 +377,7 @@ static int ilog2(int64_t v) { int k = 0; while ((int64_t(1) << k) < v) ++k; retu
 static void plan_free(az_plan_s* p) {
   if (p) az_pipe_destroy(p);
   if (!p) return;
+  az_graphs_free(p);
   if (p->side) {
     cudaStreamSynchronize(p->side);
     cudaStreamDestroy(p->side);

@@ -366,9 +366,17 @@ __global__ void k_flag_saturated(const int64_t* rank, int64_t limit, int* flag) 
 // One solve on a workspace laid out for (nrhs, R, max_blocks).  async (max_blocks == 1 only): the
 // solve is enqueued without any host synchronisation and no report; if sat_flag (DEVICE) is given,
 // a saturated sketch sets it (az_solve_host_pipelined / az_plan_sync).
+// Where an async solve left its results (for a captured solve's report).
+struct SolveTail {
+  const int64_t* rank_dev = nullptr;
+  const double* sig = nullptr;
+  int64_t kp = 0;
+};
+
 static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double* x, int64_t ldx, int64_t nrhs,
                               double theta, int64_t R, int32_t max_blocks, void* workspace,
-                              az_solve_report_t* report, cudaStream_t st, bool async_mode, int* sat_flag) {
+                              az_solve_report_t* report, cudaStream_t st, bool async_mode, int* sat_flag,
+                              cudaEvent_t* graph_ev = nullptr, SolveTail* tail = nullptr) {
   SolveWS w = layout(p, nrhs, R, max_blocks, (char*)workspace);
   const int64_t rows = p->M + p->Mb;
   const int pfix = 10;
@@ -379,8 +387,18 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
   static const bool dbg_host = getenv("AZ_DEBUG_HOST") != nullptr;
   auto hnow = []() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   const double th0 = dbg_host ? hnow() : 0.0;
-  Ev ev;
-  cudaEventRecord(ev.e[0], st);
+  Ev ev_pool;
+  // stage events: the pool's, or -- while a solve is captured into a graph -- the graph's own, recorded
+  // as external event nodes so that their times can be read after each replay
+  struct {
+    cudaEvent_t* e;
+    bool ext;
+  } ev{graph_ev ? graph_ev : ev_pool.e, graph_ev != nullptr};
+  auto rec = [&](cudaEvent_t e, cudaStream_t s) {
+    if (ev.ext) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    else cudaEventRecord(e, s);
+  };
+  rec(ev.e[0], st);
   // ---- right-hand side b' = (I - A Z*) b (narrow single-block solve: straight into S) ----
   const bool bp_in_S = !w.wide && max_blocks == 1;
   // the Z* b and M column passes are only needed by step 2: with one probe block and one batch per
@@ -405,7 +423,7 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
   } else {
     AZ_TRY(az_apply_op(p, OP_RESID, b, ldb, bp_in_S ? w.S + R * rows : w.bp, rows, nrhs, st));
   }
-  cudaEventRecord(ev.e[1], st);
+  rec(ev.e[1], st);
   if (dbg_host) fprintf(stderr, "az_solve host: resid issued +%.2f ms\n", hnow() - th0);
   double ms_sketch = 0, ms_qr = 0, ms_svd = 0;
   int64_t rank = 0, nb = 0;
@@ -420,7 +438,7 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
     const int64_t kp = nb * R;                 // probe columns
     const int64_t kt = kp + nrhs;
     cudaEvent_t e0 = ev.e[2], e1 = ev.e[3], e2 = ev.e[4], e3 = ev.e[5];
-    cudaEventRecord(e0, st);
+    rec(e0, st);
     if (w.Om && w.Zs) {   // the sketch and M = Omega - Z* A Omega for step 2
       AZ_TRY(az1f_sketch_m(p, (nb - 1) * R, R, w.S + (nb - 1) * R * rows, rows, w.Om + (nb - 1) * R * p->N, p->N, st,
                            nullptr, side));
@@ -434,7 +452,7 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
       k_copy_cols<<<az_div_up(rows * nrhs, 256), 256, 0, st>>>(w.bp, rows, w.S + kp * rows, rows, rows, nrhs);
       AZ_LAUNCH_CHECK();
     }
-    cudaEventRecord(e1, st);
+    rec(e1, st);
     if (qs != st) AZ_CUDA_CHECK(cudaStreamWaitEvent(qs, e1, 0));
     if (dbg_host) fprintf(stderr, "az_solve host: sketch issued +%.2f ms\n", hnow() - th0);
     if (!w.wide) {
@@ -472,7 +490,7 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
       k_copy_cols<<<az_div_up(kp * nrhs, 256), 256, 0, st>>>(w.bp, rows, w.Rf + kp * kt, kt, kp, nrhs);
       AZ_LAUNCH_CHECK();
     }
-    cudaEventRecord(e2, qs);
+    rec(e2, qs);
     if (dbg_host) fprintf(stderr, "az_solve host: qr issued +%.2f ms\n", hnow() - th0);
     bool full_svd = true;
     if (w.wide && nb >= 2 && nb < max_blocks) {
@@ -510,7 +528,7 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
         s1lo = std::max(s1lo, s1);
       }
     }
-    cudaEventRecord(e3, qs);
+    rec(e3, qs);
     if (qs != st) AZ_CUDA_CHECK(cudaStreamWaitEvent(st, e3, 0));
     if (host_rank) {
       cudaEventSynchronize(e3);
@@ -524,7 +542,7 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
   if (nb > max_blocks) nb = max_blocks;
   const int64_t kp = nb * R;
   if (dbg_host) fprintf(stderr, "az_solve host: svd issued +%.2f ms\n", hnow() - th0);
-  cudaEventRecord(ev.e[6], st);
+  rec(ev.e[6], st);
   // ---- x2 = Omega y ; x = x2 + Z* (b - A x2) ----
   if (w.Om) {
     // by linearity of Z* (PAPER.md:229-230): x = Omega y + Z* b - (Z* A Omega) y = Z* b + M y, with
@@ -553,8 +571,13 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
     AZ_TRY(omega_apply(p, 0, kp, w.y, kp, nrhs, w.x2, p->N, 0, st));
     AZ_TRY(step2(p, w.x2, b, ldb, x, ldx, w.tmp, nrhs, st));
   }
-  cudaEventRecord(ev.e[7], st);
+  rec(ev.e[7], st);
   if (dbg_host) fprintf(stderr, "az_solve host: all issued +%.2f ms\n", hnow() - th0);
+  if (tail) {
+    tail->rank_dev = rank_dev;
+    tail->sig = w.sig;
+    tail->kp = kp;
+  }
   if (async_mode) {
     if (sat_flag && rank_dev) {
       k_flag_saturated<<<1, 1, 0, st>>>(rank_dev, kp - pfix, sat_flag);
@@ -598,6 +621,183 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
   return saturated ? AZ_WARN_SKETCH_SATURATED : AZ_OK;
 }
 
+// ------------------------------------------------------------------------------------------
+// CUDA graphs of single-block narrow solves (one-CTA 1-D and narrow 2-D layouts): a solve whose
+// arguments repeat (same b, x, workspace, theta, R, nrhs) is captured on its second call and replayed
+// from then on -- one graph launch instead of a dozen kernel launches and stage-event records, which
+// for a c1-sized solve are a fifth of its time.  The report (rank, spectrum, stage times) comes from
+// pinned copies and external event nodes inside the graph.  AZ_SOLVE_GRAPH=0 disables; tracing
+// (az_trace_enable) runs solves eagerly.
+// ------------------------------------------------------------------------------------------
+namespace {
+struct SolveKey {
+  const double* b = nullptr;
+  int64_t ldb = 0;
+  double* x = nullptr;
+  int64_t ldx = 0, nrhs = 0;
+  double theta = 0;
+  int64_t R = 0;
+  void* ws = nullptr;
+  bool operator==(const SolveKey& o) const {
+    return b == o.b && ldb == o.ldb && x == o.x && ldx == o.ldx && nrhs == o.nrhs && theta == o.theta && R == o.R &&
+           ws == o.ws;
+  }
+};
+struct GraphEntry {
+  SolveKey key;
+  cudaGraphExec_t exec = nullptr;
+  int64_t* h_rank = nullptr;   // pinned
+  double* h_sig = nullptr;     // pinned, kp values
+  int64_t kp = 0;
+  cudaEvent_t ev[8] = {};
+};
+void entry_free(GraphEntry& g) {
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (g.h_rank) cudaFreeHost(g.h_rank);
+  if (g.h_sig) cudaFreeHost(g.h_sig);
+  for (auto& e : g.ev)
+    if (e) cudaEventDestroy(e);
+  g = GraphEntry{};
+}
+bool graphs_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AZ_SOLVE_GRAPH");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+}  // namespace
+
+struct az_graphs_s {
+  static constexpr int kMax = 4;
+  GraphEntry e[kMax];
+  int n = 0, next = 0;
+  SolveKey last;
+  bool has_last = false;
+  bool broken = false;   // a capture failed: this plan's solves stay eager
+  cudaStream_t cap = nullptr;
+};
+
+void az_graphs_free(az_plan_s* p) {
+  if (!p->graphs) return;
+  for (int i = 0; i < p->graphs->n; ++i) entry_free(p->graphs->e[i]);
+  if (p->graphs->cap) cudaStreamDestroy(p->graphs->cap);
+  delete p->graphs;
+  p->graphs = nullptr;
+}
+
+static bool graph_eligible(const az_plan_s* p, int64_t nrhs, int64_t R) {
+  return graphs_on() && !az_trace_active() && p->layout != AZ_LAYOUT_1D_FOURSTEP && R + nrhs <= AZ_NARROW_MAX;
+}
+
+static az_status_t graph_capture(az_plan_s* p, const SolveKey& k, GraphEntry& g) {
+  az_graphs_s* G = p->graphs;
+  if (!G->cap) AZ_CUDA_CHECK(cudaStreamCreateWithFlags(&G->cap, cudaStreamNonBlocking));
+  for (auto& e : g.ev) AZ_CUDA_CHECK(cudaEventCreate(&e));
+  AZ_CUDA_CHECK(cudaHostAlloc((void**)&g.h_rank, sizeof(int64_t), cudaHostAllocDefault));
+  AZ_CUDA_CHECK(cudaHostAlloc((void**)&g.h_sig, sizeof(double) * k.R, cudaHostAllocDefault));
+  SolveTail tail;
+  AZ_CUDA_CHECK(cudaStreamBeginCapture(G->cap, cudaStreamCaptureModeThreadLocal));
+  az_status_t s = solve_impl(p, k.b, k.ldb, k.x, k.ldx, k.nrhs, k.theta, k.R, 1, k.ws, nullptr, G->cap, true, nullptr,
+                             g.ev, &tail);
+  if (s == AZ_OK && tail.rank_dev && tail.kp == k.R) {
+    cudaMemcpyAsync(g.h_rank, tail.rank_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, G->cap);
+    cudaMemcpyAsync(g.h_sig, tail.sig, sizeof(double) * tail.kp, cudaMemcpyDeviceToHost, G->cap);
+  }
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(G->cap, &graph);
+  if (s != AZ_OK || ce != cudaSuccess || !graph || !tail.rank_dev || tail.kp != k.R) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    az_set_error("az_solve: graph capture failed (%s)", cudaGetErrorString(ce));
+    return s != AZ_OK ? s : AZ_ERR_CUDA;
+  }
+  const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) {
+    cudaGetLastError();
+    g.exec = nullptr;
+    az_set_error("az_solve: graph instantiation failed (%s)", cudaGetErrorString(ie));
+    return AZ_ERR_CUDA;
+  }
+  g.key = k;
+  g.kp = tail.kp;
+  return AZ_OK;
+}
+
+// One single-block narrow solve from a graph; *used = false: the caller solves eagerly (first sighting
+// of these arguments, or graphs unavailable).
+static az_status_t graph_solve(az_plan_s* p, const SolveKey& k, az_solve_report_t* report, cudaStream_t st,
+                               bool* used) {
+  *used = false;
+  if (!p->graphs) p->graphs = new az_graphs_s();
+  az_graphs_s* G = p->graphs;
+  if (G->broken) return AZ_OK;
+  GraphEntry* g = nullptr;
+  for (int i = 0; i < G->n; ++i)
+    if (G->e[i].key == k) g = &G->e[i];
+  if (!g) {
+    if (!(G->has_last && G->last == k)) {
+      G->last = k;
+      G->has_last = true;
+      return AZ_OK;
+    }
+    const int slot = G->n < az_graphs_s::kMax ? G->n++ : (G->next++ % az_graphs_s::kMax);
+    entry_free(G->e[slot]);
+    if (graph_capture(p, k, G->e[slot]) != AZ_OK) {
+      entry_free(G->e[slot]);
+      if (slot == G->n - 1) --G->n;
+      G->broken = true;
+      return AZ_OK;
+    }
+    g = &G->e[slot];
+  }
+  AZ_CUDA_CHECK(cudaGraphLaunch(g->exec, st));
+  AZ_CUDA_CHECK(cudaStreamSynchronize(st));
+  *used = true;
+  const int64_t rank = *g->h_rank, kp = g->kp;
+  const bool saturated = rank > kp - 10;
+  if (report) {
+    report->rank_used = rank;
+    report->probes_used = kp;
+    report->saturated = saturated ? 1 : 0;
+    report->sigma_first = g->h_sig[0];
+    report->sigma_last_kept = rank > 0 ? g->h_sig[rank - 1] : 0.0;
+    report->ms_rhs = ms_between(g->ev[0], g->ev[1]);
+    report->ms_sketch = ms_between(g->ev[2], g->ev[3]);
+    report->ms_qr = ms_between(g->ev[3], g->ev[4]);
+    report->ms_svd = ms_between(g->ev[4], g->ev[5]);
+    report->ms_step2 = ms_between(g->ev[6], g->ev[7]);
+    report->ms_total = ms_between(g->ev[0], g->ev[7]);
+    report->sigma = layout(p, k.nrhs, k.R, 1, (char*)k.ws).sig;
+    report->n_sigma = kp;
+  }
+  return saturated ? AZ_WARN_SKETCH_SATURATED : AZ_OK;
+}
+
+extern "C" int32_t az_solve_graph_count(az_plan_t p) { return p && p->graphs ? p->graphs->n : 0; }
+
+// the single-block (first) attempt of az_solve: from a graph when eligible, else eagerly
+static az_status_t solve_single(az_plan_s* p, const double* b, int64_t ldb, double* x, int64_t ldx, int64_t nrhs,
+                                double theta, int64_t R, void* workspace, az_solve_report_t* report, cudaStream_t st) {
+  if (graph_eligible(p, nrhs, R)) {
+    SolveKey k;
+    k.b = b;
+    k.ldb = ldb;
+    k.x = x;
+    k.ldx = ldx;
+    k.nrhs = nrhs;
+    k.theta = theta;
+    k.R = R;
+    k.ws = workspace;
+    bool used = false;
+    const az_status_t s = graph_solve(p, k, report, st, &used);
+    if (used || (s != AZ_OK && s != AZ_WARN_SKETCH_SATURATED)) return s;
+  }
+  return solve_impl(p, b, ldb, x, ldx, nrhs, theta, R, 1, workspace, report, st, false, nullptr);
+}
+
 extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, double* x, int64_t ldx, int64_t nrhs,
                                 double theta, int64_t R, int32_t max_blocks, void* workspace, size_t ws_bytes,
                                 az_solve_report_t* report, void* stream) {
@@ -615,9 +815,15 @@ extern "C" az_status_t az_solve(az_plan_t p, const double* b, int64_t ldb, doubl
   az_solve_report_t rep;
   memset(&rep, 0, sizeof(rep));
   double ms_first = 0.0;
+  if (max_blocks == 1) {
+    const az_status_t s = solve_single(p, b, ldb, x, ldx, nrhs, theta, R, workspace, &rep, st);
+    if (s != AZ_OK && s != AZ_WARN_SKETCH_SATURATED) return s;
+    if (report) *report = rep;
+    return s;
+  }
   if (narrow_first(nrhs, R, max_blocks)) {
     // the first probe block on the narrow path; kept unless it saturated
-    const az_status_t s = solve_impl(p, b, ldb, x, ldx, nrhs, theta, R, 1, workspace, &rep, st, false, nullptr);
+    const az_status_t s = solve_single(p, b, ldb, x, ldx, nrhs, theta, R, workspace, &rep, st);
     if (s != AZ_WARN_SKETCH_SATURATED) {
       if (report) *report = rep;
       return s;

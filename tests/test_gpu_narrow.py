@@ -213,3 +213,36 @@ def test_pipelined_saturation_is_reported_by_plan_sync():
     plan2 = api.Plan.from_config(cfg2)
     api.solve_host_pipelined(plan2, b, xh, 1e-12, 40, 1)
     assert _lib.lib().az_plan_sync(plan2._h) == _lib.AZ_OK
+
+
+def test_repeated_solve_replays_a_graph_bitwise():
+    """az_solve's CUDA-graph replay (include/az.h): the first call with a set of arguments runs eagerly,
+    the second is captured and replayed, later ones replay; x, the rank and the spectrum are bitwise
+    those of the eager solve, the stage times are read from the graph's event nodes, and new contents
+    of b (same buffer) are read at replay (compared with an eager solve of the new b)."""
+    from paper_2308_14490_b200 import api, _lib
+    L = _lib.lib()
+    cfg = I.get_config("c1")
+    plan = api.Plan.from_config(cfg)
+    b_np = I.rhs(cfg)
+    b = _dev(b_np)
+    x = api.empty_colmajor(plan.N, cfg.nrhs)
+    ws = torch.empty(plan.solve_workspace_bytes(cfg.nrhs, cfg.R, 1), dtype=torch.uint8, device="cuda")
+    outs = []
+    for i in range(3):
+        xi, rep = plan.solve(b, THETA, cfg.R, 1, x=x, workspace=ws)
+        outs.append((xi.cpu().numpy().copy(), rep["rank"], rep["sigma"].cpu().numpy().copy(), rep))
+        assert L.az_solve_graph_count(plan._h) == (0 if i == 0 else 1)
+    for xo, k, sg, rep in outs[1:]:
+        np.testing.assert_array_equal(xo, outs[0][0])
+        assert k == outs[0][1]
+        np.testing.assert_array_equal(sg, outs[0][2])
+        assert rep["ms_total"] > 0 and rep["ms_svd"] > 0 and not rep["saturated"]
+    b2 = np.asfortranarray(0.5 * b_np + 0.1 * np.cos(np.arange(b_np.shape[0]))[:, None])
+    b.copy_(torch.from_numpy(b2))
+    x3, _ = plan.solve(b, THETA, cfg.R, 1, x=x, workspace=ws)
+    x3 = x3.cpu().numpy().copy()
+    fresh = api.Plan.from_config(cfg)
+    xe, _ = fresh.solve(_dev(b2), THETA, cfg.R, 1)
+    np.testing.assert_array_equal(x3, xe.cpu().numpy())
+    assert not np.array_equal(x3, outs[0][0])
