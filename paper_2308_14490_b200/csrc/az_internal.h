@@ -125,6 +125,11 @@ az_status_t az_qr_r_impl(double* A, int64_t m, int64_t k, int64_t lda, double* R
                          void* ws, size_t ws_bytes, cudaStream_t st, int64_t k1 = 0, bool a_scratch = false,
                          cudaEvent_t after_leaf = nullptr);
 size_t az_qr_ws_bytes(int64_t m, int64_t k);
+// pass A of the split leaf as a blocked QR with look-ahead (az_qr_la.cu): 256-row chunks, P CTAs of
+// rows_per_cta rows; Y (in place of A's k1 columns), taus and the per-CTA R factors as k_tsqr's pass A
+bool az_tsqr_la_enabled();
+az_status_t az_tsqr_la_leaf(const double* A, int64_t m, int k1, int64_t ld, int64_t rows_per_cta, int P, double* Rout,
+                            int64_t ostride, double* Y, int64_t ldY, double* taus, int cmax, cudaStream_t st);
 // R_S of the k1 probe columns on st (ev_leaf / ev_merged recorded there), then (Q^T b')[:k1] of the
 // k - k1 right-hand-side columns on rhs_st (k1, k - k1 <= 64; A is scratch) (az_qr.cu)
 az_status_t az_qr_r_deferred(double* A, int64_t m, int64_t k, int64_t k1, int64_t lda, double* Rs, int64_t ldrs,

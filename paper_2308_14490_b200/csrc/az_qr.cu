@@ -359,237 +359,6 @@ __global__ void __launch_bounds__(512, 1) k_tsqr_rhs(QRr q) {
   }
 }
 
-// ------------------------------------------------------------------------------------------
-// Blocked TSQR leaf (k <= 128 columns, the first k1 triangularised).  The CTA keeps R (k1 x k)
-// and a chunk of MB = 128 rows of A in shared memory.  Per chunk, the k1 columns are processed in
-// panels of 8:
-//   * warp 0 factors the panel's 8 columns of [R; chunk] column by column in registers
-//     (structured reflectors v = [e_j; y_j], dlarfg convention), warp-synchronous: no block
-//     barrier inside the panel; it also forms the panel's T (8 x 8, dlarft) from y_m . y_i;
-//   * all warps then apply the block reflector I - V T V^T, V = [E; Y], to the remaining columns
-//     with DMMA:  W = R[panel rows, rest] + Y^T X_rest,  W <- T^T W,  R[panel rows, rest] -= W,
-//     X_rest -= Y W  (8-column tiles distributed over the warps).
-// Only two block barriers per panel, against one per column in k_tsqr.
-// ------------------------------------------------------------------------------------------
-constexpr int TB_MB = 128;            // chunk rows
-constexpr int TB_LDX = TB_MB + 4;     // X column stride (== 4 mod 16: conflict-free DMMA fragments)
-constexpr int TB_LDR = 65;            // R column stride (k1 <= 64 rows)
-constexpr int TB_PW = 8;              // panel width
-
-struct QRb {
-  const double* A;
-  int64_t m, ld, rb, bstride, rows_per_cta;
-  int k, k1;
-  double* Rout;   // per CTA k1 x k (ld k1)
-};
-
-__device__ long long g_tsqr_dbg[8];
-__global__ void __launch_bounds__(512, 1) k_tsqr_blk(QRb q) {
-  extern __shared__ double sm[];
-  const bool dbg = blockIdx.x == 0 && threadIdx.x == 0;
-  long long t_load = 0, t_panel = 0, t_upd = 0, tc0 = 0;
-  const int k = q.k, k1 = q.k1;
-  double* X = sm;                                 // k columns x TB_LDX
-  double* R = X + 128 * TB_LDX;                   // k columns x TB_LDR (rows < k1)
-  double* Y = R + 128 * TB_LDR;                   // TB_PW x TB_LDX  (Y[i][row])
-  double* Tm = Y + TB_PW * TB_LDX;                // 8 x 8 (T[m][i] at m * 8 + i)
-  double* Wsc = Tm + 64;                          // 16 warps x 64 scratch
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (int e = tid; e < 128 * TB_LDR; e += 512) R[e] = 0.0;
-  const int64_t r0 = (int64_t)blockIdx.x * q.rows_per_cta;
-  const int64_t r1 = min(q.m, r0 + q.rows_per_cta);
-  for (int64_t base = r0; base < r1; base += TB_MB) {
-    __syncthreads();
-    if (dbg) tc0 = clock64();
-    // ---- load the chunk (columns contiguous in rows: coalesced) ----
-    {
-      // 512 threads = 4 x 128: each thread keeps one row of the chunk (offset computed once)
-      const int ri = tid & (TB_MB - 1);
-      const int64_t row = base + ri;
-      const int64_t off = q.bstride ? (row / q.rb) * q.bstride + (row % q.rb) : row;
-      const bool ok = row < r1;
-      for (int c = tid >> 7; c < k; c += 4) X[c * TB_LDX + ri] = ok ? q.A[off + (int64_t)c * q.ld] : 0.0;
-    }
-    __syncthreads();
-    if (dbg) { const long long t = clock64(); t_load += t - tc0; tc0 = t; }
-    for (int j0 = 0; j0 < k1; j0 += TB_PW) {
-      const int pw = min(TB_PW, k1 - j0);
-      if (w == 0) {
-        // ---- panel factorisation, warp-synchronous; lane owns rows lane + 32 i ----
-        double x[TB_PW][4];
-#pragma unroll
-        for (int c = 0; c < TB_PW; ++c)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) x[c][i] = c < pw ? X[(j0 + c) * TB_LDX + lane + 32 * i] : 0.0;
-        double* yy = Wsc;          // warp 0's scratch: y_m . y_c at m * 8 + c (m < c)
-        double* taus = Wsc + 64 * 15;   // tau of the panel columns (warp 15's scratch, idle now)
-        if (lane < TB_PW) taus[lane] = 0.0;
-#pragma unroll
-        for (int c = 0; c < TB_PW; ++c) {
-          if (c >= pw) break;
-          const int jc = j0 + c;
-          double sg = 0.0;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) sg = fma(x[c][i], x[c][i], sg);
-          sg = warp_sum(sg);
-          const double alpha = R[jc * TB_LDR + jc];
-          double beta = alpha, tau = 0.0, scale = 0.0;
-          if (sg > 0.0) {
-            const double nrm = sqrt(fma(alpha, alpha, sg));
-            beta = alpha >= 0.0 ? -nrm : nrm;
-            tau = (beta - alpha) / beta;
-            scale = fast_rcp(alpha - beta);
-          }
-          if (lane == 0) taus[c] = tau;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) x[c][i] *= scale;       // y_c
-          __syncwarp();
-          if (lane == 0) R[jc * TB_LDR + jc] = beta;
-          // dots of y_c with the later panel columns (update) and the earlier y (T)
-          double d[TB_PW];
-#pragma unroll
-          for (int l = 0; l < TB_PW; ++l) {
-            d[l] = 0.0;
-            if (l != c)
-#pragma unroll
-              for (int i = 0; i < 4; ++i) d[l] = fma(x[c][i], x[l][i], d[l]);
-          }
-          {
-            // transpose-reduce the 8 dots (7 + 2 shuffles), then broadcast (8 shuffles)
-#pragma unroll
-            for (int o = 16, n = TB_PW; n > 1; o >>= 1, n >>= 1) {
-              const bool hi = lane & o;
-#pragma unroll
-              for (int i2 = 0; i2 < n / 2; ++i2) {
-                const double send = hi ? d[i2] : d[i2 + n / 2];
-                const double keep = hi ? d[i2 + n / 2] : d[i2];
-                d[i2] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-              }
-            }
-            double ds = d[0];
-            ds += __shfl_xor_sync(0xffffffffu, ds, 2);
-            ds += __shfl_xor_sync(0xffffffffu, ds, 1);
-#pragma unroll
-            for (int l = 0; l < TB_PW; ++l) d[l] = __shfl_sync(0xffffffffu, ds, 4 * l);
-          }
-          if (lane == 0)
-#pragma unroll
-            for (int m = 0; m < TB_PW; ++m)
-              if (m < c) yy[m * 8 + c] = d[m];
-          if (tau != 0.0) {
-#pragma unroll
-            for (int l = 0; l < TB_PW; ++l) {
-              if (l > c && l < pw) {
-                const double rl = R[(j0 + l) * TB_LDR + jc];
-                const double wl = tau * (rl + d[l]);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) x[l][i] = fma(-wl, x[c][i], x[l][i]);
-                __syncwarp();
-                if (lane == 0) R[(j0 + l) * TB_LDR + jc] = rl - wl;
-              }
-            }
-          }
-        }
-        // Y to shared memory (zero columns past pw), T by the dlarft recurrence (lane 0)
-#pragma unroll
-        for (int c = 0; c < TB_PW; ++c)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) Y[c * TB_LDX + lane + 32 * i] = c < pw ? x[c][i] : 0.0;
-        __syncwarp();
-        // T by the dlarft recurrence: column c from columns < c; lane a computes T[a][c]
-        if (lane < TB_PW * TB_PW) Tm[lane] = 0.0;
-        if (lane + 32 < TB_PW * TB_PW) Tm[lane + 32] = 0.0;
-        __syncwarp();
-        for (int c = 0; c < pw; ++c) {
-          if (lane < c) {
-            double t = 0.0;
-            for (int m = lane; m < c; ++m) t = fma(Tm[lane * 8 + m], yy[m * 8 + c], t);
-            Tm[lane * 8 + c] = -taus[c] * t;
-          }
-          if (lane == 0) Tm[c * 8 + c] = taus[c];
-          __syncwarp();
-        }
-      }
-      __syncthreads();
-      if (dbg) { const long long t = clock64(); t_panel += t - tc0; tc0 = t; }
-      // ---- block update of the columns right of the panel: 8-column tiles over the warps ----
-      const int c_first = j0 + pw;
-      const int ntiles = (k - c_first + 7) / 8;
-      for (int t = w; t < ntiles; t += 16) {
-        const int c0 = c_first + 8 * t;
-        const int r = lane >> 2, q2 = (lane & 3) * 2;
-        // W = R[j0 + 0..7, c0..c0+7] + Y^T X[:, c0..]   (A = Y^T: m = panel col, k = row)
-        double acc[2];
-        acc[0] = (r < pw && c0 + q2 < k) ? R[(c0 + q2) * TB_LDR + j0 + r] : 0.0;
-        acc[1] = (r < pw && c0 + q2 + 1 < k) ? R[(c0 + q2 + 1) * TB_LDR + j0 + r] : 0.0;
-#pragma unroll 8
-        for (int kk = 0; kk < TB_MB; kk += 4) {
-          const double av = Y[r * TB_LDX + kk + (lane & 3)];
-          const double bv = (c0 + r < k) ? X[(c0 + r) * TB_LDX + kk + (lane & 3)] : 0.0;
-          dmma(acc, av, bv);
-        }
-        // W' = T^T W (8 x 8) through the warp's scratch
-        double* ws = Wsc + w * 64;
-        ws[r * 8 + q2] = acc[0];
-        ws[r * 8 + q2 + 1] = acc[1];
-        __syncwarp();
-        double wp[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          double t2 = 0.0;
-#pragma unroll
-          for (int m = 0; m < TB_PW; ++m)
-            if (m <= r) t2 = fma(Tm[m * 8 + r], ws[m * 8 + q2 + e], t2);
-          wp[e] = t2;
-        }
-        __syncwarp();
-        // R rows of the panel -= W'
-        if (r < pw) {
-          if (c0 + q2 < k) R[(c0 + q2) * TB_LDR + j0 + r] -= wp[0];
-          if (c0 + q2 + 1 < k) R[(c0 + q2 + 1) * TB_LDR + j0 + r] -= wp[1];
-        }
-        ws[r * 8 + q2] = wp[0];
-        ws[r * 8 + q2 + 1] = wp[1];
-        __syncwarp();
-        // X[:, c0..] -= Y W'   (m = row: 16 tiles of 8; k = panel col: 2 k-steps; n = 8 columns)
-#pragma unroll 4
-        for (int mt = 0; mt < TB_MB / 8; ++mt) {
-          double xa[2];
-          const int row = mt * 8 + r;
-          xa[0] = (c0 + q2 < k) ? X[(c0 + q2) * TB_LDX + row] : 0.0;
-          xa[1] = (c0 + q2 + 1 < k) ? X[(c0 + q2 + 1) * TB_LDX + row] : 0.0;
-#pragma unroll
-          for (int kk = 0; kk < TB_PW; kk += 4) {
-            const double av = -Y[(kk + (lane & 3)) * TB_LDX + mt * 8 + r];   // A(m = row, k = panel col)
-            const double bv = ws[(kk + (lane & 3)) * 8 + r];                 // B(k, n = col)
-            dmma(xa, av, bv);
-          }
-          if (c0 + q2 < k) X[(c0 + q2) * TB_LDX + row] = xa[0];
-          if (c0 + q2 + 1 < k) X[(c0 + q2 + 1) * TB_LDX + row] = xa[1];
-        }
-        __syncwarp();
-      }
-      __syncthreads();
-      if (dbg) { const long long t = clock64(); t_upd += t - tc0; tc0 = t; }
-    }
-  }
-  if (dbg && q.bstride == 0) {
-    g_tsqr_dbg[0] = t_load;
-    g_tsqr_dbg[1] = t_panel;
-    g_tsqr_dbg[2] = t_upd;
-  }
-  __syncthreads();
-  double* Ro = q.Rout + (int64_t)blockIdx.x * k1 * k;
-  for (int e = tid; e < k1 * k; e += 512) {
-    const int i = e % k1, l = e / k1;
-    Ro[e] = i <= l ? R[l * TB_LDR + i] : 0.0;
-  }
-}
-
-static size_t tsqr_blk_smem() {
-  return (size_t)(128 * TB_LDX + 128 * TB_LDR + TB_PW * TB_LDX + 64 + 16 * 64) * sizeof(double);
-}
-
 static int g_sms = 0;
 static int num_sms() {
   if (!g_sms) {
@@ -619,28 +388,6 @@ static az_status_t tsqr_launch(const QRIn& q, int nblocks, cudaStream_t st) {
 }
 
 static az_status_t tsqr_pass(const QRIn& q, int nblocks, cudaStream_t st) {
-  // The blocked leaf (k_tsqr_blk) is opt-in (AZ_TSQR_BLK=1): its warp-0 panel factorisation is
-  // latency-bound and it measured slower than the per-column kernel on c2 (5.9 vs 3.9 ms).
-  static int blk = -1;
-  if (blk < 0) blk = getenv("AZ_TSQR_BLK") != nullptr;
-  if (blk && q.k1 <= 64 && q.k <= 128) {
-    QRb b;
-    b.A = q.A;
-    b.m = q.m;
-    b.ld = q.ld;
-    b.rb = q.rb;
-    b.bstride = q.bstride;
-    b.rows_per_cta = q.rows_per_cta;
-    b.k = q.k;
-    b.k1 = q.k1;
-    b.Rout = q.Rout;
-    const size_t sm = tsqr_blk_smem();
-    AZ_CUDA_CHECK(az_smem_attr(k_tsqr_blk, sm));
-    AzTrace tr(q.bstride ? "tsqr_merge" : "tsqr_leaf", st, q.m);
-    k_tsqr_blk<<<nblocks, 512, sm, st>>>(b);
-    AZ_LAUNCH_CHECK();
-    return AZ_OK;
-  }
   if (q.k <= 32) return tsqr_launch<2, 8>(q, nblocks, st);
   if (q.k <= 64) return tsqr_launch<4, 8>(q, nblocks, st);
   if (q.k <= 128) return tsqr_launch<8, 4>(q, nblocks, st);
@@ -896,6 +643,8 @@ az_status_t az_qr_r_deferred(double* A, int64_t m, int64_t k, int64_t k1, int64_
   q.taus = d.taus0;
   if (def_nw() == 8)
     AZ_TRY((tsqr_launch<8, 4, 8>(q, (int)d.P, st)));
+  else if (az_tsqr_la_enabled())
+    AZ_TRY(az_tsqr_la_leaf(A, m, (int)k1, lda, d.rows_per_cta, (int)d.P, d.buf[0], k1 * k, A, lda, d.taus0, d.cmax, st));
   else
     AZ_TRY((tsqr_launch<4, 8>(q, (int)d.P, st)));
   AZ_CUDA_CHECK(cudaEventRecord(ev_leaf, st));

@@ -1,0 +1,389 @@
+// Split TSQR leaf, pass A, as a blocked Householder QR with look-ahead (the QR that
+// reduces the M x (r + p) sketch to its R factor).
+//
+// Same arithmetic as k_tsqr's pass A (az_qr.cu): each CTA streams its row range in 256-row chunks
+// through the structured QR of [R; chunk] (R: the k1 x k1 triangle so far), reflector j being
+// H_j = I - tau_j v_j v_j^T with v_j = [e_j ; y_j] (LAPACK dlarfg convention: beta = -sign(alpha)
+// ||(alpha, x)||, tau = (beta - alpha) / beta, y = x / (alpha - beta)), and leaves y_j in place of
+// column j and tau_j in taus for pass B (k_tsqr_rhs).  Only the ORDER of the work differs: the
+// columns are taken in panels of 8, and per panel
+//   * warps 0..3 (one per SM sub-partition, 64 rows each, the panel in registers) factorise it column
+//     by column -- two 128-thread named barriers per column for the norm and the dot products -- and
+//     form its T (dlarft: H_0 .. H_7 = I - V T V^T);
+//   * all eight warps then apply it to the NEXT panel's columns (the look-ahead tile) in compact-WY
+//     form on the FP64 tensor cores (DMMA m8n8k4):
+//         W = R[J, tile] + Y_J^T X[:, tile],  W <- T^T W,  R[J, tile] -= W,  X[:, tile] -= Y_J W;
+//   * and while warps 0..3 factorise that next panel, warps 4..7 apply the panel to the remaining
+//     columns the same way, write its y columns back and refill their shared-memory slots with the
+//     same columns of the next chunk (cp.async), so the chunk loads overlap the QR.
+// The per-column step of k_tsqr (every warp applies every reflector to its own columns, one 512-thread
+// barrier per column) becomes a 4-warp chain per column plus DMMA block updates off the chain: the
+// same reflectors up to rounding (the columns right of a panel receive its reflectors as one block).
+#include <cstdlib>
+
+#include "az_internal.h"
+#include "az_mma.cuh"
+
+namespace {
+constexpr int LA_MC = 256;            // chunk rows
+constexpr int LA_LDX = LA_MC + 4;     // X column stride (== 4 mod 16: conflict-free DMMA fragments)
+constexpr int LA_LDR = 65;            // R column stride
+constexpr int LA_PW = 8;              // panel width
+constexpr int LA_NW = 8;              // warps: 0..3 factorise panels, 4..7 update
+constexpr int LA_NP = 4;              // panel warps
+constexpr int LA_NU = LA_NW - LA_NP;  // update warps
+constexpr int LA_RPW = LA_MC / LA_NP / 32;   // rows per lane in a panel warp (2)
+
+struct LAIn {
+  const double* A;     // m x k1 (ld), the probe columns
+  double* Y;           // y_j written back (== A for the split leaf)
+  int64_t m, ld, ldY, rows_per_cta;
+  int k1, cmax;
+  double* Rout;        // per CTA k1 x k1 (ld k1), CTA stride ostride
+  int64_t ostride;
+  double* taus;        // taus[(cta cmax + chunk) k1 + j]
+};
+
+AZ_D double la_wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+AZ_D void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+enum { BAR_P = 1, BAR_U = 2 };   // panel warps / update warps (128 threads each)
+
+AZ_D void cpa8(double* dst, const double* src, bool in) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(in ? 8 : 0)
+               : "memory");
+}
+
+// shared-memory layout (doubles)
+struct LASmem {
+  static constexpr int X = 0;                  // 64 columns x LA_LDX
+  static constexpr int R = X + 64 * LA_LDX;    // 64 columns x LA_LDR
+  static constexpr int T = R + 64 * LA_LDR;    // 2 x 64: T[a][m] at a * 8 + m (double-buffered by panel parity)
+  static constexpr int RED1 = T + 128;         // 4: the panel warps' partial norms
+  static constexpr int RED2 = RED1 + 4;        // 8 x 4: partial dots, d[l] of warp i at l * 4 + i
+  static constexpr int WP = RED2 + 32;         // 8 x 64: the look-ahead tile's partial W (one per warp)
+  static constexpr int WSUM = WP + 8 * 64;     // 64: W
+  static constexpr int WL = WSUM + 64;         // 64: W' = T^T W
+  static constexpr int WS = WL + 64;           // 4 x 64: the update warps' W / W' of a remaining tile
+  static constexpr int END = WS + LA_NU * 64;
+};
+
+// W'[m][n] = sum_{i <= m} T[i][m] W[i][n]   (W at W[i * 8 + n])
+AZ_D double tt_w(const double* T, const double* W, int m, int n) {
+  double t = 0.0;
+#pragma unroll
+  for (int i = 0; i < LA_PW; ++i)
+    if (i <= m) t = fma(T[i * 8 + m], W[i * 8 + n], t);
+  return t;
+}
+
+// X[:, c0 .. c0+8) -= Y_J W' over row tiles mt = mt0, mt0 + mstep, .. (W' at Wp[m * 8 + n])
+AZ_D void tile_rank_update(double* X, const double* Wp, int j0, int c0, int k1, int mt0, int mstep, int lane) {
+  const int r = lane >> 2, q = lane & 3;
+  const int ca = c0 + 2 * q, cb = ca + 1;
+  const double b0 = Wp[q * 8 + r], b1 = Wp[(q + 4) * 8 + r];   // B(k = panel col, n = tile col)
+  for (int mt = mt0; mt < LA_MC / 8; mt += mstep) {
+    const int row = 8 * mt + r;
+    double c[2];
+    c[0] = ca < k1 ? X[ca * LA_LDX + row] : 0.0;
+    c[1] = cb < k1 ? X[cb * LA_LDX + row] : 0.0;
+    dmma(c, -X[(j0 + q) * LA_LDX + row], b0);       // A(m = row, k = panel col)
+    dmma(c, -X[(j0 + q + 4) * LA_LDX + row], b1);
+    if (ca < k1) X[ca * LA_LDX + row] = c[0];
+    if (cb < k1) X[cb * LA_LDX + row] = c[1];
+  }
+}
+
+// W (8 x 8 C fragment) += Y_J^T X[:, c0..c0+8) over rows [k0, k1r), two accumulators
+AZ_D void tile_w(double (&acc)[2], const double* X, int j0, int c0, int k1, int k0, int k1r, int lane) {
+  const int r = lane >> 2, qd = lane & 3;
+  const int cb = c0 + r;
+  double a2[2] = {0.0, 0.0};
+#pragma unroll 4
+  for (int kk = k0; kk < k1r; kk += 8) {
+    const double a0 = X[(j0 + r) * LA_LDX + kk + qd];
+    const double b0 = cb < k1 ? X[cb * LA_LDX + kk + qd] : 0.0;
+    const double a1 = X[(j0 + r) * LA_LDX + kk + 4 + qd];
+    const double b1 = cb < k1 ? X[cb * LA_LDX + kk + 4 + qd] : 0.0;
+    dmma(acc, a0, b0);
+    dmma(a2, a1, b1);
+  }
+  acc[0] += a2[0];
+  acc[1] += a2[1];
+}
+
+__global__ void __launch_bounds__(32 * LA_NW, 1) k_tsqr_la(LAIn q) {
+  extern __shared__ double sm[];
+  double* X = sm + LASmem::X;
+  double* R = sm + LASmem::R;
+  const int k1 = q.k1;
+  const int np = (k1 + LA_PW - 1) / LA_PW;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int r8 = lane >> 2, qd = lane & 3;
+  for (int e = tid; e < 64 * LA_LDR; e += 32 * LA_NW) R[e] = 0.0;
+  // column slots past k1 are read as (zero) columns of a last, narrower panel or tile
+  for (int e = tid; e < (64 - k1) * LA_LDX; e += 32 * LA_NW) X[k1 * LA_LDX + e] = 0.0;
+  const int64_t r0 = (int64_t)blockIdx.x * q.rows_per_cta;
+  const int64_t r1 = min(q.m, r0 + q.rows_per_cta);
+  // first chunk: columns of 256 contiguous rows; rows past r1 zero-filled
+  for (int e = tid; e < k1 * LA_MC; e += 32 * LA_NW) {
+    const int c = e / LA_MC, i = e % LA_MC;
+    const int64_t row = r0 + i;
+    cpa8(X + c * LA_LDX + i, q.A + (row < r1 ? row : 0) + (int64_t)c * q.ld, row < r1);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+
+  // update warps: write panel pp's y columns back, then refill their slots from the next chunk
+  auto writeback = [&](int pp, int64_t base, int64_t nbase) {
+    const int j0 = pp * LA_PW, pw = min(LA_PW, k1 - j0);
+    const int ut = tid - 32 * LA_NP;
+    bar_sync(BAR_U, 32 * LA_NU);   // every update of panel pp is done
+    for (int e = ut; e < pw * LA_MC; e += 32 * LA_NU) {
+      const int c = e / LA_MC, i = e % LA_MC;
+      const int64_t row = base + i;
+      if (row < r1) q.Y[row + (int64_t)(j0 + c) * q.ldY] = X[(j0 + c) * LA_LDX + i];
+    }
+    if (nbase < r1) {
+      bar_sync(BAR_U, 32 * LA_NU);   // the slot is read before it is overwritten
+      for (int e = ut; e < pw * LA_MC; e += 32 * LA_NU) {
+        const int c = e / LA_MC, i = e % LA_MC;
+        const int64_t row = nbase + i;
+        cpa8(X + (j0 + c) * LA_LDX + i, q.A + (row < r1 ? row : 0) + (int64_t)(j0 + c) * q.ld, row < r1);
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+  };
+
+  int chunk = 0;
+  for (int64_t base = r0; base < r1; base += LA_MC, ++chunk) {
+    const int64_t nbase = base + LA_MC;
+    for (int p = 0; p < np; ++p) {
+      const int j0 = p * LA_PW, pw = min(LA_PW, k1 - j0);
+      double* Tm = sm + LASmem::T + (p & 1) * 64;
+      if (w < LA_NP) {
+        // ================= panel p, warps 0..3: rows 64 w .. 64 w + 63 =================
+        double* red1 = sm + LASmem::RED1;
+        double* red2 = sm + LASmem::RED2;
+        double x[LA_PW][LA_RPW];   // column j0 + c, row 64 w + lane + 32 i
+#pragma unroll
+        for (int c = 0; c < LA_PW; ++c)
+#pragma unroll
+          for (int i = 0; i < LA_RPW; ++i) x[c][i] = c < pw ? X[(j0 + c) * LA_LDX + 64 * w + lane + 32 * i] : 0.0;
+        double trow[LA_PW];   // warp 0, lane a < 8: row a of T
+#pragma unroll
+        for (int m = 0; m < LA_PW; ++m) trow[m] = 0.0;
+#pragma unroll
+        for (int c = 0; c < LA_PW; ++c) {
+          if (c >= pw) break;
+          const int jc = j0 + c;
+          const double alpha = R[jc * LA_LDR + jc];
+          double rl[LA_PW];   // R[jc][j0 + l], read before any warp writes the row (after the second barrier)
+#pragma unroll
+          for (int l = 0; l < LA_PW; ++l) rl[l] = (l > c && l < pw) ? R[(j0 + l) * LA_LDR + jc] : 0.0;
+          double s = 0.0;
+#pragma unroll
+          for (int i = 0; i < LA_RPW; ++i) s = fma(x[c][i], x[c][i], s);
+          s = la_wsum(s);
+          if (lane == 0) red1[w] = s;
+          bar_sync(BAR_P, 32 * LA_NP);
+          const double sig = (red1[0] + red1[1]) + (red1[2] + red1[3]);   // same order in every warp
+          double tau = 0.0, scale = 0.0, beta = alpha;
+          if (sig > 0.0) {   // (the formulas of k_tsqr)
+            const double s2 = fma(alpha, alpha, sig);
+            const double rinv = fast_rsqrt(s2);
+            const double nrm = s2 * rinv;
+            beta = alpha >= 0.0 ? -nrm : nrm;
+            tau = fma(fabs(alpha), rinv, 1.0);
+            scale = fast_rcp(alpha - beta);
+          }
+#pragma unroll
+          for (int i = 0; i < LA_RPW; ++i) x[c][i] *= scale;   // y_c
+          // dots of y_c with the panel's other columns: later ones (update), earlier y's (T)
+          double d[LA_PW];
+#pragma unroll
+          for (int l = 0; l < LA_PW; ++l) {
+            d[l] = 0.0;
+            if (l != c && l < pw)
+#pragma unroll
+              for (int i = 0; i < LA_RPW; ++i) d[l] = fma(x[c][i], x[l][i], d[l]);
+          }
+          // transpose-reduce: 3 halving levels leave lane L a partial of slot L / 4, 2 more complete it
+#pragma unroll
+          for (int o = 16, n = LA_PW; n > 1; o >>= 1, n >>= 1) {
+            const bool hi = lane & o;
+#pragma unroll
+            for (int i2 = 0; i2 < n / 2; ++i2) {
+              const double send = hi ? d[i2] : d[i2 + n / 2];
+              const double keep = hi ? d[i2 + n / 2] : d[i2];
+              d[i2] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+          }
+          double ds = d[0];
+          ds += __shfl_xor_sync(0xffffffffu, ds, 2);
+          ds += __shfl_xor_sync(0xffffffffu, ds, 1);
+          if ((lane & 3) == 0) red2[(lane >> 2) * 4 + w] = ds;
+          bar_sync(BAR_P, 32 * LA_NP);
+#pragma unroll
+          for (int l = 0; l < LA_PW; ++l) {
+            const double2 u = *reinterpret_cast<const double2*>(red2 + l * 4);
+            const double2 v = *reinterpret_cast<const double2*>(red2 + l * 4 + 2);
+            d[l] = (u.x + u.y) + (v.x + v.y);
+          }
+          if (w == 0) {
+            if (lane == 0) {
+              R[jc * LA_LDR + jc] = beta;
+              q.taus[((int64_t)blockIdx.x * q.cmax + chunk) * k1 + jc] = tau;
+            }
+            // T[a][c] = -tau_c sum_{a <= m < c} T[a][m] (y_m . y_c), T[c][c] = tau_c (lane a owns row a)
+            double t = 0.0;
+#pragma unroll
+            for (int m = 0; m < LA_PW; ++m)
+              if (m < c && m >= lane) t = fma(trow[m], d[m], t);
+            trow[c] = lane < c ? -tau * t : (lane == c ? tau : 0.0);
+          }
+          if (tau != 0.0) {
+#pragma unroll
+            for (int l = 0; l < LA_PW; ++l) {
+              if (l > c && l < pw) {
+                const double wl = tau * (rl[l] + d[l]);
+#pragma unroll
+                for (int i = 0; i < LA_RPW; ++i) x[l][i] = fma(-wl, x[c][i], x[l][i]);
+                if (w == 0 && lane == 0) R[(j0 + l) * LA_LDR + jc] = rl[l] - wl;
+              }
+            }
+          }
+        }
+        // y's in place of the panel columns; T
+#pragma unroll
+        for (int c = 0; c < LA_PW; ++c)
+#pragma unroll
+          for (int i = 0; i < LA_RPW; ++i)
+            if (c < pw) X[(j0 + c) * LA_LDX + 64 * w + lane + 32 * i] = x[c][i];
+        if (w == 0 && lane < LA_PW)
+#pragma unroll
+          for (int m = 0; m < LA_PW; ++m) Tm[lane * 8 + m] = trow[m];
+      } else if (p > 0) {
+        // ========= warps 4..7: panel p - 1 on the columns right of panel p (tiles p + 1 ..) =========
+        const int uw = w - LA_NP, pj0 = j0 - LA_PW;
+        const double* Tp = sm + LASmem::T + ((p - 1) & 1) * 64;
+        double* WS = sm + LASmem::WS + uw * 64;
+        for (int t = p + 1 + uw; t * LA_PW < k1; t += LA_NU) {
+          const int ct = t * LA_PW;
+          double acc[2] = {0.0, 0.0};
+          tile_w(acc, X, pj0, ct, k1, 0, LA_MC, lane);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int n = 2 * qd + e;
+            WS[r8 * 8 + n] = acc[e] + ((ct + n < k1) ? R[(ct + n) * LA_LDR + pj0 + r8] : 0.0);
+          }
+          __syncwarp();
+          double wv[2];
+#pragma unroll
+          for (int e2 = 0; e2 < 2; ++e2) {
+            const int e = lane + 32 * e2;
+            wv[e2] = tt_w(Tp, WS, e >> 3, e & 7);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int e2 = 0; e2 < 2; ++e2) {
+            const int e = lane + 32 * e2, m = e >> 3, n = e & 7;
+            WS[e] = wv[e2];
+            if (ct + n < k1) R[(ct + n) * LA_LDR + pj0 + m] -= wv[e2];
+          }
+          __syncwarp();
+          tile_rank_update(X, WS, pj0, ct, k1, 0, 1, lane);
+          __syncwarp();
+        }
+        writeback(p - 1, base, nbase);
+      }
+      __syncthreads();   // panel p factorised; panel p - 1 applied everywhere
+      if (p + 1 < np) {
+        // ====== look-ahead: panel p on the next panel's columns, all warps (K split 8 ways) ======
+        const int c0 = j0 + LA_PW;
+        double* Wp = sm + LASmem::WP;
+        double* Ws = sm + LASmem::WSUM;
+        double* WL = sm + LASmem::WL;
+        double acc[2] = {0.0, 0.0};
+        tile_w(acc, X, j0, c0, k1, 32 * w, 32 * w + 32, lane);
+        Wp[w * 64 + r8 * 8 + 2 * qd] = acc[0];
+        Wp[w * 64 + r8 * 8 + 2 * qd + 1] = acc[1];
+        __syncthreads();
+        if (tid < 64) {
+          const int m = tid >> 3, n = tid & 7;
+          double s = (c0 + n < k1) ? R[(c0 + n) * LA_LDR + j0 + m] : 0.0;
+#pragma unroll
+          for (int t = 0; t < LA_NW; ++t) s += Wp[t * 64 + tid];
+          Ws[tid] = s;
+        }
+        __syncthreads();
+        if (tid < 64) {
+          const int m = tid >> 3, n = tid & 7;
+          const double wv = tt_w(Tm, Ws, m, n);
+          WL[tid] = wv;
+          if (c0 + n < k1) R[(c0 + n) * LA_LDR + j0 + m] -= wv;
+        }
+        __syncthreads();
+        tile_rank_update(X, WL, j0, c0, k1, w, LA_NW, lane);
+        __syncthreads();
+      }
+    }
+    if (w >= LA_NP) {
+      writeback(np - 1, base, nbase);   // (the last panel has no columns right of the look-ahead)
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+    }
+    __syncthreads();   // the next chunk is in place; R holds this chunk's triangle
+  }
+  // R (k1 x k1, ld k1)
+  double* Ro = q.Rout + (int64_t)blockIdx.x * q.ostride;
+  for (int e = tid; e < k1 * k1; e += 32 * LA_NW) {
+    const int i = e % k1, l = e / k1;
+    Ro[e] = i <= l ? R[l * LA_LDR + i] : 0.0;
+  }
+}
+}  // namespace
+
+size_t az_tsqr_la_smem() { return (size_t)LASmem::END * sizeof(double); }
+
+// AZ_TSQR_LA=0: pass A of the split leaf by the per-column kernel k_tsqr instead
+bool az_tsqr_la_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AZ_TSQR_LA");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
+az_status_t az_tsqr_la_leaf(const double* A, int64_t m, int k1, int64_t ld, int64_t rows_per_cta, int P, double* Rout,
+                            int64_t ostride, double* Y, int64_t ldY, double* taus, int cmax, cudaStream_t st) {
+  if (k1 < 1 || k1 > 64) {
+    az_set_error("tsqr_la: k1 = %d not in [1, 64]", k1);
+    return AZ_ERR_NOT_SUPPORTED;
+  }
+  LAIn q;
+  q.A = A;
+  q.Y = Y;
+  q.m = m;
+  q.ld = ld;
+  q.ldY = ldY;
+  q.rows_per_cta = rows_per_cta;
+  q.k1 = k1;
+  q.cmax = cmax;
+  q.Rout = Rout;
+  q.ostride = ostride;
+  q.taus = taus;
+  const size_t sm = az_tsqr_la_smem();
+  AZ_CUDA_CHECK(az_smem_attr(k_tsqr_la, sm));
+  AzTrace tr("tsqr_leaf", st, m);
+  k_tsqr_la<<<P, 32 * LA_NW, sm, st>>>(q);
+  AZ_LAUNCH_CHECK();
+  return AZ_OK;
+}
+

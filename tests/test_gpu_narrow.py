@@ -74,7 +74,9 @@ def _assert_narrow(tr):
 
 
 FOURSTEP = [("interval_n8192_R64_rhs8", 1 << 13, 64, 8), ("interval_n65536_R64_rhs64", 1 << 16, 64, 64),
-            ("interval_n65536_R64_rhs8", 1 << 16, 64, 8), ("interval_n8192_R40_rhs1", 1 << 13, 40, 1)]
+            ("interval_n65536_R64_rhs8", 1 << 16, 64, 8), ("interval_n8192_R40_rhs1", 1 << 13, 40, 1),
+            # panels of 8 with a narrower last one (the look-ahead leaf, az_qr_la.cu): 36 = 4 x 8 + 4, 61 = 7 x 8 + 5
+            ("interval_n8192_R36_rhs3", 1 << 13, 36, 3), ("interval_n65536_R61_rhs5", 1 << 16, 61, 5)]
 
 
 @pytest.mark.parametrize("name,n,R,nrhs", FOURSTEP, ids=[c[0] for c in FOURSTEP])
