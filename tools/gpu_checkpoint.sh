@@ -15,4 +15,5 @@ timeout 900 ncu -f --set full --clock-control none --import-source on \
 python tools/summarize_ncu.py launches gpurun_out/launches.csv > gpurun_out/launches_summary.txt 2>&1
 python tools/summarize_ncu.py full /tmp/prof_c2.ncu-rep > gpurun_out/ncu_full_summary.txt 2>&1
 rm -f gpurun_out/launches.csv
+bash tools/prof_c1.sh
 ls -la gpurun_out
