@@ -8,8 +8,9 @@
 // column j and tau_j in taus for pass B (k_tsqr_rhs).  Only the ORDER of the work differs: the
 // columns are taken in panels of 8, and per panel
 //   * warps 0..3 (one per SM sub-partition, 64 rows each, the panel in registers) factorise it column
-//     by column -- two 128-thread named barriers per column for the norm and the dot products -- and
-//     form its T (dlarft: H_0 .. H_7 = I - V T V^T);
+//     by column -- one 128-thread named barrier per column: the column's norm and its dot products with
+//     the panel's other columns are reduced together, the dots taken with the unscaled column and scaled
+//     by 1 / (alpha - beta) afterwards -- and form its T (dlarft: H_0 .. H_7 = I - V T V^T);
 //   * all eight warps then apply it to the NEXT panel's columns (the look-ahead tile) in compact-WY
 //     form on the FP64 tensor cores (DMMA m8n8k4):
 //         W = R[J, tile] + Y_J^T X[:, tile],  W <- T^T W,  R[J, tile] -= W,  X[:, tile] -= Y_J W;
@@ -44,12 +45,6 @@ struct LAIn {
   double* taus;        // taus[(cta cmax + chunk) k1 + j]
 };
 
-AZ_D double la_wsum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
 AZ_D void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 enum { BAR_P = 1, BAR_U = 2 };   // panel warps / update warps (128 threads each)
 
@@ -64,9 +59,8 @@ struct LASmem {
   static constexpr int X = 0;                  // 64 columns x LA_LDX
   static constexpr int R = X + 64 * LA_LDX;    // 64 columns x LA_LDR
   static constexpr int T = R + 64 * LA_LDR;    // 2 x 64: T[a][m] at a * 8 + m (double-buffered by panel parity)
-  static constexpr int RED1 = T + 128;         // 4: the panel warps' partial norms
-  static constexpr int RED2 = RED1 + 4;        // 8 x 4: partial dots, d[l] of warp i at l * 4 + i
-  static constexpr int WP = RED2 + 32;         // 8 x 64: the look-ahead tile's partial W (one per warp)
+  static constexpr int RED2 = T + 128;         // 2 x 8 x 4: partial dots, d[l] of warp i at l * 4 + i
+  static constexpr int WP = RED2 + 64;         // 8 x 64: the look-ahead tile's partial W (one per warp)
   static constexpr int WSUM = WP + 8 * 64;     // 64: W
   static constexpr int WL = WSUM + 64;         // 64: W' = T^T W
   static constexpr int WS = WL + 64;           // 4 x 64: the update warps' W / W' of a remaining tile
@@ -115,6 +109,112 @@ AZ_D void tile_w(double (&acc)[2], const double* X, int j0, int c0, int k1, int 
   }
   acc[0] += a2[0];
   acc[1] += a2[1];
+}
+
+// Panel factorisation by warps 0..3 (rows 64 w .. 64 w + 63 of the chunk, lane rows 64 w + lane + 32 i).
+// FULLW = 8: a full panel (every column test resolved at compile time); 0: a last, narrower panel.
+// Warp 0 writes R's panel rows, warp 1 forms T (lane a owns row a), warp 2 stores the taus, so that
+// no warp carries all the side work between the two barriers of a column.
+template <int FULLW>
+AZ_D void la_panel(double* X, double* R, double* sm, double* Tm, const LAIn& q, int chunk, int j0, int k1, int w,
+                   int lane) {
+  const int PWN = FULLW ? FULLW : min(LA_PW, k1 - j0);
+  double* red2 = sm + LASmem::RED2;
+  double x[LA_PW][LA_RPW];   // column j0 + c, row 64 w + lane + 32 i
+#pragma unroll
+  for (int c = 0; c < LA_PW; ++c)
+#pragma unroll
+    for (int i = 0; i < LA_RPW; ++i) x[c][i] = c < PWN ? X[(j0 + c) * LA_LDX + 64 * w + lane + 32 * i] : 0.0;
+  double trow[LA_PW];   // warp 1, lane a < 8: row a of T
+#pragma unroll
+  for (int m = 0; m < LA_PW; ++m) trow[m] = 0.0;
+#pragma unroll
+  for (int c = 0; c < LA_PW; ++c) {
+    if (c >= PWN) break;
+    const int jc = j0 + c;
+    const double alpha = R[jc * LA_LDR + jc];
+    double rl[LA_PW];   // R[jc][j0 + l], read before any warp writes the row (after the barrier)
+#pragma unroll
+    for (int l = 0; l < LA_PW; ++l) rl[l] = (l > c && l < PWN) ? R[(j0 + l) * LA_LDR + jc] : 0.0;
+    // ONE reduction per column: slot c = ||x_c||^2 (the chunk part), slot l != c = x_c . x_l -- the
+    // dots are taken with the unscaled column and scaled by the reflector's 1 / (alpha - beta) after,
+    // so they need not wait for the reflector (y_c . x_l = scale (x_c . x_l))
+    double d[LA_PW];
+#pragma unroll
+    for (int l = 0; l < LA_PW; ++l) {
+      d[l] = 0.0;
+      if (l < PWN)
+#pragma unroll
+        for (int i = 0; i < LA_RPW; ++i) d[l] = fma(x[c][i], x[l][i], d[l]);
+    }
+    // transpose-reduce: 3 halving levels leave lane L a partial of slot L / 4, 2 more complete it
+#pragma unroll
+    for (int o = 16, n = LA_PW; n > 1; o >>= 1, n >>= 1) {
+      const bool hi = lane & o;
+#pragma unroll
+      for (int i2 = 0; i2 < n / 2; ++i2) {
+        const double send = hi ? d[i2] : d[i2 + n / 2];
+        const double keep = hi ? d[i2 + n / 2] : d[i2];
+        d[i2] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    double ds = d[0];
+    ds += __shfl_xor_sync(0xffffffffu, ds, 2);
+    ds += __shfl_xor_sync(0xffffffffu, ds, 1);
+    double* rb = red2 + (c & 1) * 32;   // (double-buffered: one barrier per column)
+    if ((lane & 3) == 0) rb[(lane >> 2) * 4 + w] = ds;
+    bar_sync(BAR_P, 32 * LA_NP);
+#pragma unroll
+    for (int l = 0; l < LA_PW; ++l) {
+      const double2 u = *reinterpret_cast<const double2*>(rb + l * 4);
+      const double2 v = *reinterpret_cast<const double2*>(rb + l * 4 + 2);
+      d[l] = (u.x + u.y) + (v.x + v.y);
+    }
+    const double sig = d[c];
+    double tau = 0.0, scale = 0.0, beta = alpha;
+    if (sig > 0.0) {   // (the formulas of k_tsqr)
+      const double s2 = fma(alpha, alpha, sig);
+      const double rinv = fast_rsqrt(s2);
+      const double nrm = s2 * rinv;
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = fma(fabs(alpha), rinv, 1.0);
+      scale = fast_rcp(alpha - beta);
+    }
+#pragma unroll
+    for (int i = 0; i < LA_RPW; ++i) x[c][i] *= scale;   // y_c
+#pragma unroll
+    for (int l = 0; l < LA_PW; ++l) d[l] *= scale;       // y_c . x_l (l > c), y_c . y_l (l < c)
+    if (w == 0 && lane == 0) R[jc * LA_LDR + jc] = beta;
+    if (w == 2 && lane == 0) q.taus[((int64_t)blockIdx.x * q.cmax + chunk) * k1 + jc] = tau;
+    if (w == 1) {
+      // T[a][c] = -tau_c sum_{a <= m < c} T[a][m] (y_m . y_c), T[c][c] = tau_c (lane a owns row a)
+      double t = 0.0;
+#pragma unroll
+      for (int m = 0; m < LA_PW; ++m)
+        if (m < c && m >= lane) t = fma(trow[m], d[m], t);
+      trow[c] = lane < c ? -tau * t : (lane == c ? tau : 0.0);
+    }
+    if (tau != 0.0) {
+#pragma unroll
+      for (int l = 0; l < LA_PW; ++l) {
+        if (l > c && l < PWN) {
+          const double wl = tau * (rl[l] + d[l]);
+#pragma unroll
+          for (int i = 0; i < LA_RPW; ++i) x[l][i] = fma(-wl, x[c][i], x[l][i]);
+          if (w == 0 && lane == 0) R[(j0 + l) * LA_LDR + jc] = rl[l] - wl;
+        }
+      }
+    }
+  }
+  // y's in place of the panel columns; T
+#pragma unroll
+  for (int c = 0; c < LA_PW; ++c)
+#pragma unroll
+    for (int i = 0; i < LA_RPW; ++i)
+      if (c < PWN) X[(j0 + c) * LA_LDX + 64 * w + lane + 32 * i] = x[c][i];
+  if (w == 1 && lane < LA_PW)
+#pragma unroll
+    for (int m = 0; m < LA_PW; ++m) Tm[lane * 8 + m] = trow[m];
 }
 
 __global__ void __launch_bounds__(32 * LA_NW, 1) k_tsqr_la(LAIn q) {
@@ -169,106 +269,10 @@ __global__ void __launch_bounds__(32 * LA_NW, 1) k_tsqr_la(LAIn q) {
       double* Tm = sm + LASmem::T + (p & 1) * 64;
       if (w < LA_NP) {
         // ================= panel p, warps 0..3: rows 64 w .. 64 w + 63 =================
-        double* red1 = sm + LASmem::RED1;
-        double* red2 = sm + LASmem::RED2;
-        double x[LA_PW][LA_RPW];   // column j0 + c, row 64 w + lane + 32 i
-#pragma unroll
-        for (int c = 0; c < LA_PW; ++c)
-#pragma unroll
-          for (int i = 0; i < LA_RPW; ++i) x[c][i] = c < pw ? X[(j0 + c) * LA_LDX + 64 * w + lane + 32 * i] : 0.0;
-        double trow[LA_PW];   // warp 0, lane a < 8: row a of T
-#pragma unroll
-        for (int m = 0; m < LA_PW; ++m) trow[m] = 0.0;
-#pragma unroll
-        for (int c = 0; c < LA_PW; ++c) {
-          if (c >= pw) break;
-          const int jc = j0 + c;
-          const double alpha = R[jc * LA_LDR + jc];
-          double rl[LA_PW];   // R[jc][j0 + l], read before any warp writes the row (after the second barrier)
-#pragma unroll
-          for (int l = 0; l < LA_PW; ++l) rl[l] = (l > c && l < pw) ? R[(j0 + l) * LA_LDR + jc] : 0.0;
-          double s = 0.0;
-#pragma unroll
-          for (int i = 0; i < LA_RPW; ++i) s = fma(x[c][i], x[c][i], s);
-          s = la_wsum(s);
-          if (lane == 0) red1[w] = s;
-          bar_sync(BAR_P, 32 * LA_NP);
-          const double sig = (red1[0] + red1[1]) + (red1[2] + red1[3]);   // same order in every warp
-          double tau = 0.0, scale = 0.0, beta = alpha;
-          if (sig > 0.0) {   // (the formulas of k_tsqr)
-            const double s2 = fma(alpha, alpha, sig);
-            const double rinv = fast_rsqrt(s2);
-            const double nrm = s2 * rinv;
-            beta = alpha >= 0.0 ? -nrm : nrm;
-            tau = fma(fabs(alpha), rinv, 1.0);
-            scale = fast_rcp(alpha - beta);
-          }
-#pragma unroll
-          for (int i = 0; i < LA_RPW; ++i) x[c][i] *= scale;   // y_c
-          // dots of y_c with the panel's other columns: later ones (update), earlier y's (T)
-          double d[LA_PW];
-#pragma unroll
-          for (int l = 0; l < LA_PW; ++l) {
-            d[l] = 0.0;
-            if (l != c && l < pw)
-#pragma unroll
-              for (int i = 0; i < LA_RPW; ++i) d[l] = fma(x[c][i], x[l][i], d[l]);
-          }
-          // transpose-reduce: 3 halving levels leave lane L a partial of slot L / 4, 2 more complete it
-#pragma unroll
-          for (int o = 16, n = LA_PW; n > 1; o >>= 1, n >>= 1) {
-            const bool hi = lane & o;
-#pragma unroll
-            for (int i2 = 0; i2 < n / 2; ++i2) {
-              const double send = hi ? d[i2] : d[i2 + n / 2];
-              const double keep = hi ? d[i2 + n / 2] : d[i2];
-              d[i2] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-            }
-          }
-          double ds = d[0];
-          ds += __shfl_xor_sync(0xffffffffu, ds, 2);
-          ds += __shfl_xor_sync(0xffffffffu, ds, 1);
-          if ((lane & 3) == 0) red2[(lane >> 2) * 4 + w] = ds;
-          bar_sync(BAR_P, 32 * LA_NP);
-#pragma unroll
-          for (int l = 0; l < LA_PW; ++l) {
-            const double2 u = *reinterpret_cast<const double2*>(red2 + l * 4);
-            const double2 v = *reinterpret_cast<const double2*>(red2 + l * 4 + 2);
-            d[l] = (u.x + u.y) + (v.x + v.y);
-          }
-          if (w == 0) {
-            if (lane == 0) {
-              R[jc * LA_LDR + jc] = beta;
-              q.taus[((int64_t)blockIdx.x * q.cmax + chunk) * k1 + jc] = tau;
-            }
-            // T[a][c] = -tau_c sum_{a <= m < c} T[a][m] (y_m . y_c), T[c][c] = tau_c (lane a owns row a)
-            double t = 0.0;
-#pragma unroll
-            for (int m = 0; m < LA_PW; ++m)
-              if (m < c && m >= lane) t = fma(trow[m], d[m], t);
-            trow[c] = lane < c ? -tau * t : (lane == c ? tau : 0.0);
-          }
-          if (tau != 0.0) {
-#pragma unroll
-            for (int l = 0; l < LA_PW; ++l) {
-              if (l > c && l < pw) {
-                const double wl = tau * (rl[l] + d[l]);
-#pragma unroll
-                for (int i = 0; i < LA_RPW; ++i) x[l][i] = fma(-wl, x[c][i], x[l][i]);
-                if (w == 0 && lane == 0) R[(j0 + l) * LA_LDR + jc] = rl[l] - wl;
-              }
-            }
-          }
-        }
-        // y's in place of the panel columns; T
-#pragma unroll
-        for (int c = 0; c < LA_PW; ++c)
-#pragma unroll
-          for (int i = 0; i < LA_RPW; ++i)
-            if (c < pw) X[(j0 + c) * LA_LDX + 64 * w + lane + 32 * i] = x[c][i];
-        if (w == 0 && lane < LA_PW)
-#pragma unroll
-          for (int m = 0; m < LA_PW; ++m) Tm[lane * 8 + m] = trow[m];
+        if (pw == LA_PW)
+          la_panel<LA_PW>(X, R, sm, Tm, q, chunk, j0, k1, w, lane);
+        else
+          la_panel<0>(X, R, sm, Tm, q, chunk, j0, k1, w, lane);
       } else if (p > 0) {
         // ========= warps 4..7: panel p - 1 on the columns right of panel p (tiles p + 1 ..) =========
         const int uw = w - LA_NP, pj0 = j0 - LA_PW;
