@@ -76,12 +76,12 @@ AZ_D double tt_w(const double* T, const double* W, int m, int n) {
   return t;
 }
 
-// X[:, c0 .. c0+8) -= Y_J W' over row tiles mt = mt0, mt0 + mstep, .. (W' at Wp[m * 8 + n])
-AZ_D void tile_rank_update(double* X, const double* Wp, int j0, int c0, int k1, int mt0, int mstep, int lane) {
+// X[:, c0 .. c0+8) -= Y_J W' over the row tiles mt0 .. mt1 - 1 (8 rows each; W' at Wp[m * 8 + n])
+AZ_D void tile_rank_update(double* X, const double* Wp, int j0, int c0, int k1, int mt0, int mt1, int lane) {
   const int r = lane >> 2, q = lane & 3;
   const int ca = c0 + 2 * q, cb = ca + 1;
   const double b0 = Wp[q * 8 + r], b1 = Wp[(q + 4) * 8 + r];   // B(k = panel col, n = tile col)
-  for (int mt = mt0; mt < LA_MC / 8; mt += mstep) {
+  for (int mt = mt0; mt < mt1; ++mt) {
     const int row = 8 * mt + r;
     double c[2];
     c[0] = ca < k1 ? X[ca * LA_LDX + row] : 0.0;
@@ -302,14 +302,15 @@ __global__ void __launch_bounds__(32 * LA_NW, 1) k_tsqr_la(LAIn q) {
             if (ct + n < k1) R[(ct + n) * LA_LDR + pj0 + m] -= wv[e2];
           }
           __syncwarp();
-          tile_rank_update(X, WS, pj0, ct, k1, 0, 1, lane);
+          tile_rank_update(X, WS, pj0, ct, k1, 0, LA_MC / 8, lane);
           __syncwarp();
         }
-        writeback(p - 1, base, nbase);
       }
       __syncthreads();   // panel p factorised; panel p - 1 applied everywhere
       if (p + 1 < np) {
-        // ====== look-ahead: panel p on the next panel's columns, all warps (K split 8 ways) ======
+        // ====== look-ahead: panel p on the next panel's columns; W split 8 ways over all warps, then
+        // W' = T^T W by warp 0 and each panel warp updates its own 64 rows (so it can go straight on to
+        // factorising the next panel); the update warps meanwhile write back panel p - 1 ======
         const int c0 = j0 + LA_PW;
         double* Wp = sm + LASmem::WP;
         double* Ws = sm + LASmem::WSUM;
@@ -319,23 +320,32 @@ __global__ void __launch_bounds__(32 * LA_NW, 1) k_tsqr_la(LAIn q) {
         Wp[w * 64 + r8 * 8 + 2 * qd] = acc[0];
         Wp[w * 64 + r8 * 8 + 2 * qd + 1] = acc[1];
         __syncthreads();
-        if (tid < 64) {
-          const int m = tid >> 3, n = tid & 7;
-          double s = (c0 + n < k1) ? R[(c0 + n) * LA_LDR + j0 + m] : 0.0;
+        if (w == 0) {
 #pragma unroll
-          for (int t = 0; t < LA_NW; ++t) s += Wp[t * 64 + tid];
-          Ws[tid] = s;
+          for (int e2 = 0; e2 < 2; ++e2) {
+            const int e = lane + 32 * e2, m = e >> 3, n = e & 7;
+            double sum = (c0 + n < k1) ? R[(c0 + n) * LA_LDR + j0 + m] : 0.0;
+#pragma unroll
+            for (int t = 0; t < LA_NW; ++t) sum += Wp[t * 64 + e];
+            Ws[e] = sum;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int e2 = 0; e2 < 2; ++e2) {
+            const int e = lane + 32 * e2, m = e >> 3, n = e & 7;
+            const double wv = tt_w(Tm, Ws, m, n);
+            WL[e] = wv;
+            if (c0 + n < k1) R[(c0 + n) * LA_LDR + j0 + m] -= wv;
+          }
         }
-        __syncthreads();
-        if (tid < 64) {
-          const int m = tid >> 3, n = tid & 7;
-          const double wv = tt_w(Tm, Ws, m, n);
-          WL[tid] = wv;
-          if (c0 + n < k1) R[(c0 + n) * LA_LDR + j0 + m] -= wv;
+        if (w < LA_NP) {
+          bar_sync(BAR_P, 32 * LA_NP);
+          tile_rank_update(X, WL, j0, c0, k1, 8 * w, 8 * w + 8, lane);
+        } else if (p > 0) {
+          writeback(p - 1, base, nbase);
         }
-        __syncthreads();
-        tile_rank_update(X, WL, j0, c0, k1, w, LA_NW, lane);
-        __syncthreads();
+      } else if (w >= LA_NP && p > 0) {
+        writeback(p - 1, base, nbase);
       }
     }
     if (w >= LA_NP) {
