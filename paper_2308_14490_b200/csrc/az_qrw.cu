@@ -269,7 +269,11 @@ __global__ void __launch_bounds__(256) k_qr_wred(UpdArgs a, int KC) {
 // (DMMA computes D = A B + C with A = -V), and the next tile's C fragments and W' tile are
 // fetched into registers while the current tile's MMAs run.
 constexpr int UP_SA = 132, UP_SB = 68;
-__global__ void __launch_bounds__(256, 2) k_qr_upd(UpdArgs a) {
+// PF = 1: the next tile's C fragments are prefetched into registers during the current tile's MMAs
+// (with the current tile and W' that is ~80 doubles per thread: 1 CTA per SM without spills);
+// PF = 0: C is loaded at the tile's start and only W' is prefetched (2 CTAs per SM)
+template <int PF>
+__global__ void __launch_bounds__(256, PF ? 1 : 2) k_qr_upd(UpdArgs a) {
   extern __shared__ double sm[];
   double* As = sm;                    // KMAJ [k = panel col][m = row], stride 132 (holds -V)
   double* Bs = sm + QB * UP_SA;       // IMAJ [n = target col][k], stride 68
@@ -283,7 +287,7 @@ __global__ void __launch_bounds__(256, 2) k_qr_upd(UpdArgs a) {
   }
   double acc[4][4][2];
   double wv[16];
-  auto load_tile = [&](int64_t n0) {
+  auto load_c = [&](int64_t n0) {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -294,13 +298,16 @@ __global__ void __launch_bounds__(256, 2) k_qr_upd(UpdArgs a) {
           const int64_t n = n0 + acc_col(wn * 32, j, e, lane);
           acc[i][j][e] = (r < a.m && n < a.nt) ? a.C[n * a.ldc + r] : 0.0;
         }
+  };
+  auto load_w = [&](int64_t n0) {
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
       const int e = tid + 256 * t, n = e >> 6, l = e & 63;
       wv[t] = (n0 + n < a.nt) ? a.Wfin[(n0 + n) * QB + l] : 0.0;
     }
   };
-  load_tile(0);
+  if (PF) load_c(0);
+  load_w(0);
   for (int64_t n0 = 0; n0 < a.nt; n0 += 64) {
     __syncthreads();                  // previous tile's MMAs are done with Bs
 #pragma unroll
@@ -309,29 +316,48 @@ __global__ void __launch_bounds__(256, 2) k_qr_upd(UpdArgs a) {
       Bs[n * UP_SB + l] = wv[t];
     }
     __syncthreads();
-    double cur[4][4][2];
+    auto mma_store = [&](double (&cc)[4][4][2]) {
+      warp_mma<4, 4, KMAJ, IMAJ>(cc, As, UP_SA, Bs, UP_SB, wm * 32, wn * 32, 0, QB, lane);
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        cur[i][j][0] = acc[i][j][0];
-        cur[i][j][1] = acc[i][j][1];
-      }
-    if (n0 + 64 < a.nt) load_tile(n0 + 64);   // next C fragments and W' tile in flight
-    warp_mma<4, 4, KMAJ, IMAJ>(cur, As, UP_SA, Bs, UP_SB, wm * 32, wn * 32, 0, QB, lane);
+        for (int j = 0; j < 4; ++j)
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+          for (int e = 0; e < 2; ++e) {
+            const int64_t r = rbase + acc_row(wm * 32, i, lane);
+            const int64_t n = n0 + acc_col(wn * 32, j, e, lane);
+            if (r < a.m && n < a.nt) a.C[n * a.ldc + r] = cc[i][j][e];
+          }
+    };
+    if constexpr (PF != 0) {
+      double cur[4][4][2];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t r = rbase + acc_row(wm * 32, i, lane);
-          const int64_t n = n0 + acc_col(wn * 32, j, e, lane);
-          if (r < a.m && n < a.nt) a.C[n * a.ldc + r] = cur[i][j][e];
+        for (int j = 0; j < 4; ++j) {
+          cur[i][j][0] = acc[i][j][0];
+          cur[i][j][1] = acc[i][j][1];
         }
+      if (n0 + 64 < a.nt) load_c(n0 + 64);   // next C fragments in flight
+      if (n0 + 64 < a.nt) load_w(n0 + 64);   // next W' tile in flight
+      mma_store(cur);
+    } else {
+      load_c(n0);
+      if (n0 + 64 < a.nt) load_w(n0 + 64);
+      mma_store(acc);
+    }
   }
 }
 
+// AZ_QR_UPD_PF: 1 (register prefetch of the next C tile, one CTA per SM) or 0 (two CTAs per SM)
+static int upd_pf() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AZ_QR_UPD_PF");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
 
 // ------------------------------------------------------------------------------------------
 // T of a QB-wide panel from its Gram matrix: Gv = V^T V (split-K DMMA partials over row chunks,
@@ -470,7 +496,8 @@ static az_status_t qrw_apply_dir(const double* V, int64_t ldv, int64_t m, const 
     return AZ_ERR_WORKSPACE;
   }
   const size_t ups = (size_t)(QB * UP_SA + 64 * UP_SB) * sizeof(double);
-  AZ_CUDA_CHECK(az_smem_attr(k_qr_upd, ups));
+  AZ_CUDA_CHECK(az_smem_attr(k_qr_upd<1>, ups));
+  AZ_CUDA_CHECK(az_smem_attr(k_qr_upd<0>, ups));
   for (int64_t pi = 0; pi < p1 - p0; ++pi) {
     const int64_t p = applyQ ? p1 - 1 - pi : p0 + pi;
     UpdArgs u;
@@ -502,7 +529,10 @@ static az_status_t qrw_apply_dir(const double* V, int64_t ldv, int64_t m, const 
     }
     {
       AzTrace tr("qrw_upd", st, 2 * rows * u.nb * nt);
-      k_qr_upd<<<az_div_up(rows, 128), 256, ups, st>>>(u);
+      if (upd_pf())
+        k_qr_upd<1><<<az_div_up(rows, 128), 256, ups, st>>>(u);
+      else
+        k_qr_upd<0><<<az_div_up(rows, 128), 256, ups, st>>>(u);
       AZ_LAUNCH_CHECK();
     }
   }
