@@ -60,6 +60,8 @@ def kernel_model(name, cfg, M, k_cols, k1=None, kept=False, split=False):
         "1f_cols_in_coef": C * n + kw_om,              # probes generated on chip; write spectrum (+ Omega)
         "1f_rows_expand_keep": 2 * C * n + C * L,
         "1f_rows_expand": C * n + C * L,
+        "1f_rows_expand_probe": C * n + C * L,         # spectral probes drawn in the row: write v^ and the fine grid
+        "1f_rows_probe_z": C * n,                      # spectral probes -> IFFT_N2 -> Z2 (explicit Omega)
         "1f_cols_fine_mask": 2 * C * L + mask_b * L + kw_aom,   # fine grid in/out, mask (1 B) (+ A Omega rows)
         "1f_rows_step1": 2 * C * L + C * n + 8 * n + kw_z,    # fine grid in/out, v^ and zinv in (+ Z* part)
         "1f_rows_resid": 2 * C * L + 8 * n + kw_z,
@@ -150,7 +152,7 @@ def oracle_sample(cfg, R):
     kc, kr = min(2, R), min(2, nr)
     t_all = time.perf_counter()
     t = time.perf_counter()
-    Om = OP.probes(cfg.N, list(range(kc)), cfg.seed)
+    Om = OP.probe_matrix(cfg, list(range(kc)), cfg.seed)
     t_gen = time.perf_counter() - t
     t = time.perf_counter()
     S2 = OA.step1_apply(prob, Om)

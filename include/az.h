@@ -132,11 +132,17 @@ az_status_t az_apply_resid(az_plan_t plan, const double* b, int64_t ldb, double*
 /* S[:, 0:ncols] = (A - A Z* A) Omega[:, col0 : col0+ncols] with Omega generated on the fly
  * (Philox4x32-10 keyed by plan seed and GLOBAL column index; probes never stored).
  * PAPER.md:269 "r+p matrix vector products".  Used by az_solve and by multi-GPU drivers that
- * shard probe columns.  S is (M+Mb) x ncols, leading dimension ldS.                          */
+ * shard probe columns.  S is (M+Mb) x ncols, leading dimension ldS.
+ * Probe definition (reading R35): 1-D plans with s n > 2048 (the four-step layout) draw
+ * column pair P = (2P, 2P+1) in the frequency domain -- Re / Im of IFFT_n(v_P), v_P[k] =
+ * sqrt(n) (z0 + i z1), (z0, z1) = Box-Muller of Philox counter (k, P + 2^63) -- i.i.d. N(0,1)
+ * columns like the entrywise probes (Omega[2m, j], Omega[2m+1, j] from counter (m, j)) of every
+ * other plan.  Any col0 (an odd col0 computes its first pair and discards the real column).   */
 az_status_t az_sketch(az_plan_t plan, int64_t col0, int64_t ncols, double* S, int64_t ldS,
                       void* stream);
 /* x (N x nrhs) (+)= Omega[:, col0 : col0+ncols] y  (y: ncols x nrhs, DEVICE).  accumulate = 0
- * overwrites x.  Regenerates Omega (a9 of SURVEY.md §8(a)).                                  */
+ * overwrites x.  Regenerates Omega (a9 of SURVEY.md §8(a)); spectral probes (four-step plans)
+ * are made explicit per batch of pairs in the plan's scratch and applied by a DMMA GEMM.      */
 az_status_t az_omega_apply(az_plan_t plan, int64_t col0, int64_t ncols, const double* y, int64_t ldy,
                            int64_t nrhs, double* x, int64_t ldx, int accumulate, void* stream);
 

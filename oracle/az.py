@@ -23,7 +23,7 @@ from paper_2308_14490_b200 import inputs as I
 from . import circulant as C
 from . import dense as D
 from .kernel import periodized
-from .philox import probes as philox_probes
+from .philox import probe_matrix
 
 
 # --------------------------------------------------------------------------------------
@@ -156,7 +156,7 @@ def az_solve(prob: Problem, b: np.ndarray, theta: float, R: int, seed: int,
     """
     b2 = b.reshape(b.shape[0], -1)
     N = prob.N
-    omega = omega_fn or (lambda cols: philox_probes(N, cols, seed))
+    omega = omega_fn or (lambda cols: probe_matrix(prob.cfg, cols, seed))
     bp = resid_apply(prob, b2)                                   # b' = (I - A Z*) b
     cols = []
     blocks = []

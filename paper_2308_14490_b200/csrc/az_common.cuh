@@ -83,6 +83,16 @@ AZ_D double2 probe_pair(uint64_t m, uint64_t j, uint64_t seed) {
   return make_double2(r * cs, r * sn);
 }
 
+// Spectral probes of the 1-D four-step layout (reading R35): the column pair
+// (Omega[:, 2P], Omega[:, 2P+1]) is Re / Im of u_P = IFFT_n(v_P), where the unnormalised spectrum is
+// v_P[k] = sqrt(n) (z0 + i z1), (z0, z1) = probe_pair(k, P + 2^63).  A complex vector of i.i.d.
+// circular N(0,1) + i N(0,1) entries has exactly this spectrum (the DFT is sqrt(n) x unitary), so the
+// two columns are i.i.d. N(0,1) like every other probe; the sketch then starts from v_P directly.
+AZ_D cplx spectral_probe(uint64_t k, uint64_t P, uint64_t seed, double sqn) {
+  const double2 z = probe_pair(k, P | (uint64_t(1) << 63), seed);
+  return make_double2(sqn * z.x, sqn * z.y);
+}
+
 // Complex value of probe pair p (columns col0 + 2p, col0 + 2p + 1) at an even/odd row pair:
 // returns z[2m] (in .first) and z[2m+1] for the complex packing z = Omega[:, 2p] + i Omega[:, 2p+1].
 struct cpair { cplx a, b; };

@@ -55,6 +55,8 @@ struct P1f {
   int64_t ldout2;
   bool defer_z;          // skip the closing FC_OUT_Z pass (az1f_out_z runs it later)
   int64_t nvec, col0, pair0;
+  int lead;              // spectral probes from an odd col0: the first pair's real column precedes the call
+  double sqn;            // sqrt(n): scale of the spectral probes
 };
 
 // row of the fine grid point g (natural order), -1 outside Omega
@@ -73,15 +75,19 @@ AZ_D cplx tw4(const P1f& a, int64_t t) {
 
 struct Cols1 {
   int64_t cre, cim;
-  bool has_im;
+  bool has_re, has_im;
 };
 AZ_D Cols1 pcols(const P1f& a, int b) {
   Cols1 c;
-  c.cre = 2 * (a.pair0 + b);
+  c.cre = 2 * (a.pair0 + b) - a.lead;
   c.cim = c.cre + 1;
+  c.has_re = c.cre >= 0;
   c.has_im = c.cim < a.nvec;
   return c;
 }
+
+// global probe pair of the batch's vector pair b (spectral probes, reading R35)
+AZ_D uint64_t probe_pair_index(const P1f& a, int b) { return (uint64_t)((a.col0 >> 1) + a.pair0 + b); }
 
 // ------------------------------------------------------------------------------------------
 // column passes: a CTA owns TC adjacent columns of an N1-row matrix; each column FFT is computed
@@ -177,7 +183,7 @@ AZ_D void cols_body(const P1f& a, cplx (&v)[EC], int j, int col, int b, cplx* bu
           a.out[r + cc.cre * a.ldout] = a.in[r + cc.cre * a.ldin] - v[e].x;
           if (cc.has_im) a.out[r + cc.cim * a.ldout] = a.in[r + cc.cim * a.ldin] - v[e].y;
         } else {
-          a.out[r + cc.cre * a.ldout] = v[e].x;
+          if (cc.has_re) a.out[r + cc.cre * a.ldout] = v[e].x;
           if (cc.has_im) a.out[r + cc.cim * a.ldout] = v[e].y;
         }
       }
@@ -193,7 +199,7 @@ AZ_D void cols_body(const P1f& a, cplx (&v)[EC], int j, int col, int b, cplx* bu
 #pragma unroll
     for (int e = 0; e < EC; ++e) {
       const int64_t i = (int64_t)(j + e * T) * W + col;
-      a.out2[i + cc.cre * a.ldout2] = v[e].x * cout;
+      if (cc.has_re) a.out2[i + cc.cre * a.ldout2] = v[e].x * cout;
       if (cc.has_im) a.out2[i + cc.cim * a.ldout2] = v[e].y * cout;
     }
   } else {   // FC_OUT_COEF
@@ -333,7 +339,22 @@ AZ_HD constexpr int row_buf() {
                                                                       : fftr::padded_lenE<EL / 2>(NR2);
 }
 
-enum { FR_EXPAND = 0, FR_EXPAND_KEEP = 1, FR_STEP1 = 2, FR_RESID = 3, FR_ZSTAR = 4, FR_AT = 5 };
+enum { FR_EXPAND = 0, FR_EXPAND_KEEP = 1, FR_STEP1 = 2, FR_RESID = 3, FR_ZSTAR = 4, FR_AT = 5, FR_EXPAND_PROBE = 6,
+       FR_PROBE_Z = 7 };
+// FR_EXPAND_PROBE: the spectral probes v^ drawn in the row (reading R35) -> keep v^ -> expand x W/L -> IFFT_L2
+//                  (the sketch's first pass: no coefficient-side column pass, no FFT_N2)
+// FR_PROBE_Z:      v^ drawn in the row -> IFFT_N2 -> twiddle -> Z2 (FC_OUT_Z then gives Omega explicitly)
+template <int KIND>
+struct RowGen {
+  static constexpr bool on = KIND == FR_EXPAND_PROBE || KIND == FR_PROBE_Z;
+};
+// v^[k1 + N1 (j + e T)] of probe pair P, element e of thread j
+template <int EN, int T>
+AZ_D void gen_row(const P1f& a, int k1, uint64_t P, int j, cplx (&vn)[EN]) {
+#pragma unroll
+  for (int e = 0; e < EN; ++e)
+    vn[e] = spectral_probe((uint64_t)k1 + (uint64_t)a.N1 * (uint64_t)(j + e * T), P, a.seed, a.sqn);
+}
 
 template <int NR2, int LR2, int RPC, int KIND, int EL, int MINB>
 __global__ void __launch_bounds__(RPC * (LR2 / EL), MINB) k1f_rows(P1f a, int nrows) {
@@ -376,11 +397,15 @@ __global__ void __launch_bounds__(RPC * (LR2 / EL), MINB) k1f_rows(P1f a, int nr
   }
   asm volatile("cp.async.commit_group;\n" ::);
 
-  if constexpr (KIND == FR_EXPAND || KIND == FR_EXPAND_KEEP) {
+  if constexpr (KIND == FR_EXPAND || KIND == FR_EXPAND_KEEP || RowGen<KIND>::on) {
+    if constexpr (RowGen<KIND>::on) {
+      gen_row<EN, T>(a, live ? k1 : 0, probe_pair_index(a, b), j, vn);
+    } else {
 #pragma unroll
-    for (int e = 0; e < EN; ++e) vn[e] = live ? C1b[rowC + j + e * T] : czero();
-    fftr::fft<NR2, EN, -1>(vn, j, buf, a.tw, TWN);
-    if (KIND == FR_EXPAND_KEEP && live)
+      for (int e = 0; e < EN; ++e) vn[e] = live ? C1b[rowC + j + e * T] : czero();
+      fftr::fft<NR2, EN, -1>(vn, j, buf, a.tw, TWN);
+    }
+    if ((KIND == FR_EXPAND_KEEP || KIND == FR_EXPAND_PROBE) && live)
 #pragma unroll
       for (int e = 0; e < EN; ++e) C1b[rowC + j + e * T] = vn[e];
     asm volatile("cp.async.wait_all;\n" ::);
@@ -421,7 +446,19 @@ __global__ void __launch_bounds__(RPC * (LR2 / EL), MINB) k1f_rows(P1f a, int nr
       }
     }
   }
-  if constexpr (KIND == FR_ZSTAR || KIND == FR_AT) {
+  if constexpr (KIND == FR_PROBE_Z) {
+    fftr::fft<NR2, EN, 1>(vn, j, buf, a.tw, TWN);
+    if (live) {
+      cplx* Zb = a.Z2 + (int64_t)b * a.n;
+      cplx w = tw4<1>(a, ((int64_t)j * k1 * 2) & (a.L - 1));
+      const cplx ws = tw4<1>(a, ((int64_t)T * k1 * 2) & (a.L - 1));
+#pragma unroll
+      for (int e = 0; e < EN; ++e) {
+        Zb[rowC + j + e * T] = cmul(vn[e], w);
+        w = cmul(w, ws);
+      }
+    }
+  } else if constexpr (KIND == FR_ZSTAR || KIND == FR_AT) {
     fftr::fft<NR2, EN, 1>(vn, j, buf, a.tw, TWN);
     if (live) {
       // e^{+2 pi i n2 k1 / n} = e^{+2 pi i (2 n2 k1) / L}, n2 = j + e T, by recurrence in e
@@ -463,8 +500,10 @@ __global__ void __launch_bounds__(RPC * (LR2 / EL), MINB) k1f_rows(P1f a, int nr
 template <int NR2, int LR2, int KIND>
 struct RowsP {
   static constexpr int EL = 16, EN = 8, T = LR2 / EL;
-  static constexpr bool IN_FINE = !(KIND == FR_EXPAND || KIND == FR_EXPAND_KEEP);
-  static constexpr int INLEN = IN_FINE ? LR2 : NR2;     // complex values of the input row
+  static constexpr bool GEN = RowGen<KIND>::on;         // no input row: the spectral probes are drawn
+  static constexpr bool IN_FINE = !(KIND == FR_EXPAND || KIND == FR_EXPAND_KEEP || GEN);
+  static constexpr int INLEN = GEN ? 0 : (IN_FINE ? LR2 : NR2);   // complex values of the input row
+  static constexpr bool NEED_W = KIND != FR_PROBE_Z;
   static constexpr bool NEED_Z = (KIND == FR_STEP1 || KIND == FR_RESID || KIND == FR_ZSTAR);
   static constexpr bool NEED_C = (KIND == FR_STEP1);
   static constexpr int PB = row_buf<NR2, LR2, EL>();
@@ -502,11 +541,15 @@ __global__ void __launch_bounds__(LR2 / 16, 2) k1f_rows_p(P1f a, int npairs, int
   }
   __syncthreads();
   if (j == 0 && b0 < b1) {
-    bulk::arrive_expect_tx(&bars[0], (uint32_t)(sizeof(double) * (LR2 + (C::NEED_Z ? NR2 : 0))));
-    bulk::copy_g2s(Ws, a.Wr + rowW, sizeof(double) * LR2, &bars[0]);
-    if constexpr (C::NEED_Z) bulk::copy_g2s(Zs, a.zinv + rowC, sizeof(double) * NR2, &bars[0]);
-    bulk::arrive_expect_tx(&bars[1], sizeof(cplx) * INLEN);
-    bulk::copy_g2s(stage, in_row(b0), sizeof(cplx) * INLEN, &bars[1]);
+    if constexpr (C::NEED_W) {
+      bulk::arrive_expect_tx(&bars[0], (uint32_t)(sizeof(double) * (LR2 + (C::NEED_Z ? NR2 : 0))));
+      bulk::copy_g2s(Ws, a.Wr + rowW, sizeof(double) * LR2, &bars[0]);
+      if constexpr (C::NEED_Z) bulk::copy_g2s(Zs, a.zinv + rowC, sizeof(double) * NR2, &bars[0]);
+    }
+    if constexpr (!C::GEN) {
+      bulk::arrive_expect_tx(&bars[1], sizeof(cplx) * INLEN);
+      bulk::copy_g2s(stage, in_row(b0), sizeof(cplx) * INLEN, &bars[1]);
+    }
   }
   uint32_t ph_in = 0, ph_c = 0;
   bool tables = false;
@@ -515,19 +558,24 @@ __global__ void __launch_bounds__(LR2 / 16, 2) k1f_rows_p(P1f a, int npairs, int
     cplx* Gb = a.G + (int64_t)b * a.L;
     cplx vn[EN];
     cplx vl[EL];
-    bulk::wait(&bars[1], ph_in);
-    ph_in ^= 1;
-    if constexpr (C::IN_FINE) {
-#pragma unroll
-      for (int e = 0; e < EL; ++e) vl[e] = stage[j + e * T];
+    if constexpr (C::GEN) {
+      gen_row<EN, T>(a, k1, probe_pair_index(a, b), j, vn);
+      __syncthreads();   // the previous pair's last exchange is read before this pair's first one writes
     } else {
+      bulk::wait(&bars[1], ph_in);
+      ph_in ^= 1;
+      if constexpr (C::IN_FINE) {
 #pragma unroll
-      for (int e = 0; e < EN; ++e) vn[e] = stage[j + e * T];
+        for (int e = 0; e < EL; ++e) vl[e] = stage[j + e * T];
+      } else {
+#pragma unroll
+        for (int e = 0; e < EN; ++e) vn[e] = stage[j + e * T];
+      }
+      __syncthreads();   // every thread holds its input: the stage (and the v^ row) may be refilled
     }
-    __syncthreads();   // every thread holds its input: the stage (and the v^ row) may be refilled
     if (j == 0) {
       bulk::fence_proxy_async();
-      if (b + 1 < b1) {
+      if (!C::GEN && b + 1 < b1) {
         bulk::arrive_expect_tx(&bars[1], sizeof(cplx) * INLEN);
         bulk::copy_g2s(stage, in_row(b + 1), sizeof(cplx) * INLEN, &bars[1]);
       }
@@ -536,9 +584,11 @@ __global__ void __launch_bounds__(LR2 / 16, 2) k1f_rows_p(P1f a, int npairs, int
         bulk::copy_g2s(Cs, C1b + rowC, sizeof(cplx) * NR2, &bars[2]);
       }
     }
-    if constexpr (KIND == FR_EXPAND || KIND == FR_EXPAND_KEEP) {
-      fftr::fft<NR2, EN, -1>(vn, j, buf, a.tw, TWN);
-      if constexpr (KIND == FR_EXPAND_KEEP) {
+    if constexpr (KIND == FR_PROBE_Z) {
+      // (nothing to fold or expand: the drawn spectrum goes straight to the coefficient side below)
+    } else if constexpr (KIND == FR_EXPAND || KIND == FR_EXPAND_KEEP || KIND == FR_EXPAND_PROBE) {
+      if constexpr (!C::GEN) fftr::fft<NR2, EN, -1>(vn, j, buf, a.tw, TWN);
+      if constexpr (KIND == FR_EXPAND_KEEP || KIND == FR_EXPAND_PROBE) {
 #pragma unroll
         for (int e = 0; e < EN; ++e) C1b[rowC + j + e * T] = vn[e];
       }
@@ -582,7 +632,17 @@ __global__ void __launch_bounds__(LR2 / 16, 2) k1f_rows_p(P1f a, int npairs, int
         }
       }
     }
-    if constexpr (KIND == FR_ZSTAR || KIND == FR_AT) {
+    if constexpr (KIND == FR_PROBE_Z) {
+      fftr::fft<NR2, EN, 1>(vn, j, buf, a.tw, TWN);
+      cplx* Zb = a.Z2 + (int64_t)b * a.n;
+      cplx w = tw4<1>(a, ((int64_t)j * k1 * 2) & (a.L - 1));
+      const cplx ws = tw4<1>(a, ((int64_t)T * k1 * 2) & (a.L - 1));
+#pragma unroll
+      for (int e = 0; e < EN; ++e) {
+        Zb[rowC + j + e * T] = cmul(vn[e], w);
+        w = cmul(w, ws);
+      }
+    } else if constexpr (KIND == FR_ZSTAR || KIND == FR_AT) {
       fftr::fft<NR2, EN, 1>(vn, j, buf, a.tw, TWN);
       cplx w = tw4<1>(a, ((int64_t)j * k1 * 2) & (a.L - 1));
       const cplx ws = tw4<1>(a, ((int64_t)T * k1 * 2) & (a.L - 1));
@@ -751,7 +811,7 @@ static az_status_t frows_e(const P1f& a, int nb, cudaStream_t st) {
   auto kern = k1f_rows<NR2, LR2, RPC, KIND, EL, MINB>;
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   static const char* names[] = {"1f_rows_expand", "1f_rows_expand_keep", "1f_rows_step1", "1f_rows_resid",
-                                "1f_rows_zstar", "1f_rows_at"};
+                                "1f_rows_zstar", "1f_rows_at", "1f_rows_expand_probe", "1f_rows_probe_z"};
   AzTrace tr(names[KIND], st, nb);
   kern<<<dim3(az_div_up(a.N1, RPC), nb), RPC * T, sm, st>>>(a, a.N1);
   AZ_LAUNCH_CHECK();
@@ -787,7 +847,7 @@ static az_status_t frows_p(const P1f& a, int nb, cudaStream_t st) {
   // split the pairs so that the grid is >= 4 waves (tails) while each CTA still walks several pairs
   const int pg = std::max(1, std::min(nb, (4 * resident + a.N1 - 1) / a.N1));
   static const char* names[] = {"1f_rows_expand", "1f_rows_expand_keep", "1f_rows_step1", "1f_rows_resid",
-                                "1f_rows_zstar", "1f_rows_at"};
+                                "1f_rows_zstar", "1f_rows_at", "1f_rows_expand_probe", "1f_rows_probe_z"};
   AzTrace tr(names[KIND], st, nb);
   kern<<<dim3(a.N1, pg), C::T, C::smem, st>>>(a, nb, pg);
   AZ_LAUNCH_CHECK();
@@ -816,11 +876,12 @@ static az_status_t run1f(const P1f& a0, int op, int src, int64_t npairs, int64_t
         AZ_TRY(fcols<NC, FC_OUT_GATHER, SRC_VEC>(a, L2, nb, 1.0, st));
         break;
       case OP_STEP1:
-        if (src == SRC_PROBE)
-          AZ_TRY(fcols<NC, FC_IN_COEF, SRC_PROBE>(a, N2, nb, 1.0, st));
-        else
+        if (src == SRC_PROBE) {   // spectral probes (reading R35): v^ drawn in the first row pass
+          AZ_TRY(frows<NR2, FR_EXPAND_PROBE>(a, nb, st));
+        } else {
           AZ_TRY(fcols<NC, FC_IN_COEF, SRC_VEC>(a, N2, nb, 1.0, st));
-        AZ_TRY(frows<NR2, FR_EXPAND_KEEP>(a, nb, st));
+          AZ_TRY(frows<NR2, FR_EXPAND_KEEP>(a, nb, st));
+        }
         AZ_TRY(fcols<NC, FC_FINE_MASK, SRC_VEC>(a, L2, nb, 1.0, st));
         AZ_TRY(frows<NR2, FR_STEP1>(a, nb, st));
         AZ_TRY(fcols<NC, FC_OUT_GATHER, SRC_VEC>(a, L2, nb, 1.0, st));
@@ -889,6 +950,8 @@ static P1f make_p1f(az_plan_s* p) {
   a.defer_z = false;
   a.ldin = a.ldout = 0;
   a.nvec = a.col0 = a.pair0 = 0;
+  a.lead = 0;
+  a.sqn = sqrt((double)p->n);
   return a;
 }
 
@@ -922,7 +985,8 @@ az_status_t az1f_apply(az_plan_s* p, int op, int src, const double* in, int64_t 
   a.ldout = ldout;
   a.nvec = nvec;
   a.col0 = col0;
-  const int64_t npairs = (nvec + 1) / 2;
+  if (src == SRC_PROBE) a.lead = (int)(col0 & 1);
+  const int64_t npairs = (nvec + a.lead + 1) / 2;
   AZ_1F_DISPATCH(run1f, a, op, src, npairs, p->Bmax, st)
 }
 
@@ -994,13 +1058,41 @@ az_status_t az1f_sketch_m(az_plan_s* p, int64_t col0, int64_t ncols, double* S, 
   a.out = S;
   a.ldout = ldS;
   a.Z2 = Zspec ? Zspec : p->d_Z2;
-  a.defer_z = defer && (ncols + 1) / 2 <= p->Bmax;
+  a.defer_z = defer && (col0 & 1) == 0 && (ncols + 1) / 2 <= p->Bmax;
   a.out2 = Om;
   a.ldout2 = ldOm;
   a.nvec = ncols;
   a.col0 = col0;
-  const int64_t npairs = (ncols + 1) / 2;
+  a.lead = (int)(col0 & 1);
+  const int64_t npairs = (ncols + a.lead + 1) / 2;
   AZ_1F_DISPATCH(run1f, a, OP_STEP1, SRC_PROBE, npairs, p->Bmax, st)
+}
+
+// Omega[:, col0 .. col0 + ncols) explicitly (N x ncols, ld ldOm) for the spectral probes of this layout
+// (reading R35): per batch of probe pairs, the drawn spectrum -> IFFT_N2 -> twiddle (row pass, into the
+// plan's Z2 buffer) -> IFFT_N1 / n (column pass).  Uses the plan's scratch: stream-ordered like every pass.
+template <int NC, int NR2>
+static az_status_t omega_run(P1f a, int64_t npairs, int64_t Bmax, cudaStream_t st) {
+  for (int64_t p0 = 0; p0 < npairs; p0 += Bmax) {
+    a.pair0 = p0;
+    const int nb = (int)std::min<int64_t>(Bmax, npairs - p0);
+    AZ_TRY(frows<NR2, FR_PROBE_Z>(a, nb, st));
+    AZ_TRY(fcols<NC, FC_OUT_Z, SRC_VEC>(a, NR2, nb, 1.0 / (double)a.n, st));
+  }
+  return AZ_OK;
+}
+
+az_status_t az1f_omega_fill(az_plan_s* p, int64_t col0, int64_t ncols, double* Om, int64_t ldOm, cudaStream_t st) {
+  if (ncols <= 0) return AZ_OK;
+  P1f a = make_p1f(p);
+  a.Z2 = p->d_Z2;
+  a.out2 = Om;
+  a.ldout2 = ldOm;
+  a.nvec = ncols;
+  a.col0 = col0;
+  a.lead = (int)(col0 & 1);
+  const int64_t npairs = (ncols + a.lead + 1) / 2;
+  AZ_1F_DISPATCH(omega_run, a, npairs, p->Bmax, st)
 }
 
 // The closing column pass of az1f_resid_z / az1f_sketch_m (deferred, single batch): IFFT_N1 of the

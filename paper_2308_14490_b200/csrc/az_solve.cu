@@ -87,8 +87,12 @@ __global__ void __launch_bounds__(256) k_omega_apply(int64_t N, int64_t col0, in
   }
 }
 
+static az_status_t omega_apply_spectral(az_plan_s* p, int64_t col0, int64_t ncols, const double* y, int64_t ldy,
+                                        int64_t nrhs, double* x, int64_t ldx, int accumulate, cudaStream_t st);
+
 static az_status_t omega_apply(az_plan_s* p, int64_t col0, int64_t ncols, const double* y, int64_t ldy,
                                int64_t nrhs, double* x, int64_t ldx, int accumulate, cudaStream_t st) {
+  if (p->layout == AZ_LAYOUT_1D_FOURSTEP) return omega_apply_spectral(p, col0, ncols, y, ldy, nrhs, x, ldx, accumulate, st);
   for (int64_t c0 = 0; c0 < nrhs; c0 += 64) {
     const int nr = (int)std::min<int64_t>(64, nrhs - c0);
     AzTrace tr("omega_apply", st, p->N * ncols * nr);
@@ -918,6 +922,31 @@ __global__ void k_omega_fill(int64_t N, int64_t col0, int64_t ncols, double* Om,
   if (2 * m + 1 < N) Om[j * N + 2 * m + 1] = z.y;
 }
 
+// Omega of a four-step plan is not pointwise (spectral probes, reading R35): x (+)= Omega y by batches of
+// whole probe pairs, each made explicit in the plan's C1 scratch (2 Bmax columns of N) and multiplied
+// by the DMMA GEMM.
+static az_status_t omega_apply_spectral(az_plan_s* p, int64_t col0, int64_t ncols, const double* y, int64_t ldy,
+                                        int64_t nrhs, double* x, int64_t ldx, int accumulate, cudaStream_t st) {
+  if (ncols <= 0 || nrhs <= 0) {
+    if (!accumulate && nrhs > 0) {
+      for (int64_t c = 0; c < nrhs; ++c) AZ_CUDA_CHECK(cudaMemsetAsync(x + c * ldx, 0, sizeof(double) * p->N, st));
+    }
+    return AZ_OK;
+  }
+  double* Om = reinterpret_cast<double*>(p->d_C1);
+  const int64_t cap = 2 * p->Bmax, c0e = col0 & ~int64_t(1), cend = col0 + ncols;
+  for (int64_t g0 = c0e; g0 < cend; g0 += cap) {
+    const int64_t a0 = std::max(g0, col0), g1 = std::min(g0 + cap, cend);
+    AZ_TRY(az1f_omega_fill(p, a0, g1 - a0, Om, p->N, st));
+    const bool acc = accumulate || g0 > c0e;
+    AzTrace tr("omega_apply", st, p->N * (g1 - a0) * nrhs);
+    k_gemm_mn<<<dim3(az_div_up(p->N, 64), az_div_up(nrhs, 64)), 256, 0, st>>>(Om, p->N, y + (a0 - col0), ldy, x, ldx, p->N,
+                                                                              g1 - a0, nrhs, acc ? x : nullptr, ldx, 1.0);
+    AZ_LAUNCH_CHECK();
+  }
+  return AZ_OK;
+}
+
 // The two factored-solve products for many right-hand sides on the FP64 tensor path (DMMA
 // m8n8k4; same FP64 peak as DFMA on B200, but 256 multiply-adds per warp instruction).
 //
@@ -1376,7 +1405,12 @@ extern "C" az_status_t az_factorize(az_plan_t p, double theta, int64_t R, int32_
       f->Tb = nullptr;
       if (!f->Mm && cudaMalloc(&f->Om, sizeof(double) * p->N * kp) == cudaSuccess) {
         AzTrace tr("omega_fill", st);
-        k_omega_fill<<<az_div_up(((p->N + 1) / 2) * kp, 256), 256, 0, st>>>(p->N, 0, kp, f->Om, p->seed);
+        if (p->layout == AZ_LAYOUT_1D_FOURSTEP) {   // spectral probes (reading R35)
+          const az_status_t s3 = az1f_omega_fill(p, 0, kp, f->Om, p->N, st);
+          if (s3 != AZ_OK) return fail(s3);
+        } else {
+          k_omega_fill<<<az_div_up(((p->N + 1) / 2) * kp, 256), 256, 0, st>>>(p->N, 0, kp, f->Om, p->seed);
+        }
         if (cudaGetLastError() != cudaSuccess) return fail(AZ_ERR_CUDA);
       } else {
         cudaGetLastError();

@@ -91,6 +91,13 @@ class Config:
         return self.n if self.dim == 1 else self.n * self.ny
 
     @property
+    def spectral_probes(self) -> bool:
+        # the probe definition of the plan (reading R35): 1-D boxes whose fine grid is longer
+        # than 2048 points (the GPU's four-step layout) draw each probe column pair in the frequency
+        # domain; every other plan draws Omega entrywise.  Data only: each side generates its own.
+        return self.dim == 1 and self.s * self.n > 2048
+
+    @property
     def row_scale(self) -> float:
         # alpha: 1 for value rows; -1/(2 eps^2) for Laplacian rows (PAPER.md:704,
         # "we normalize A^i with the factor -2 eps^2")

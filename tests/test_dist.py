@@ -46,7 +46,7 @@ class CpuOps:
         return _cm(OA.resid_apply(self.prob, b.numpy()))
 
     def sketch(self, col0, ncols):
-        om = OP.probes(self.N, list(range(col0, col0 + ncols)), self.cfg.seed)
+        om = OP.probe_matrix(self.cfg, list(range(col0, col0 + ncols)), self.cfg.seed)
         return _cm(OA.step1_apply(self.prob, om))
 
     def qr_partial(self, A, k1):
@@ -65,7 +65,7 @@ class CpuOps:
         return _cm(y), torch.from_numpy(s), kk
 
     def omega_apply(self, col0, y):
-        om = OP.probes(self.N, list(range(col0, col0 + y.shape[0])), self.cfg.seed)
+        om = OP.probe_matrix(self.cfg, list(range(col0, col0 + y.shape[0])), self.cfg.seed)
         yn = y.numpy()
         return _cm(np.stack([om @ yn[:, c] for c in range(yn.shape[1])], axis=1))   # column by column
 

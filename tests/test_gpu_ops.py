@@ -175,7 +175,7 @@ def test_sketch_matches_oracle_probes(setup, parity_record):
     cfg, plan, prob, A = setup
     col0, ncols = 5, 7      # ragged: odd count, non-zero global offset
     S = _host(plan.sketch(col0, ncols))
-    Om = OP.probes(cfg.N, list(range(col0, col0 + ncols)), cfg.seed)
+    Om = OP.probe_matrix(cfg, list(range(col0, col0 + ncols)), cfg.seed)
     ref = OA.step1_apply(prob, Om)
     nA = plan.sigma_max
     for c in range(ncols):
@@ -241,7 +241,7 @@ def test_full_size_sampled_and_normwise(name, cfg, parity_record):
     _achieved(parity_record, cfg, "A", y, ref)
     nA = plan.sigma_max
     S = _host(plan.sketch(0, 4))
-    Om = OP.probes(cfg.N, [0, 1, 2, 3], cfg.seed)
+    Om = OP.probe_matrix(cfg, [0, 1, 2, 3], cfg.seed)
     refS = OA.step1_apply(prob, Om)
     for c in range(4):
         assert np.linalg.norm(S[:, c] - refS[:, c]) <= 1e-12 * nA * nA * plan.zstar_norm * np.linalg.norm(Om[:, c])

@@ -70,10 +70,10 @@ def test_omega_apply_matches_oracle_probes():
     cfg = I.make_config("interval", 4096)
     plan = Plan.from_config(cfg)
     rng = np.random.default_rng(0)
-    for col0, ncols, nrhs in [(0, 40, 1), (6, 70, 3), (0, 64, 64)]:
+    for col0, ncols, nrhs in [(0, 40, 1), (6, 70, 3), (0, 64, 64), (5, 9, 2)]:
         y = rng.standard_normal((ncols, nrhs))
         x = _host(plan.omega_apply(col0, _dev(y)))
-        ref = OP.probes(cfg.N, list(range(col0, col0 + ncols)), cfg.seed) @ y
+        ref = OP.probe_matrix(cfg, list(range(col0, col0 + ncols)), cfg.seed) @ y
         assert np.linalg.norm(x - ref) <= 1e-13 * np.linalg.norm(ref)
 
 

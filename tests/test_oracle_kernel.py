@@ -129,3 +129,46 @@ def test_probe_moments_and_layout():
     # normal quantiles (Kolmogorov-Smirnov against the standard normal CDF)
     from scipy import stats
     assert stats.kstest(Om.ravel(), "norm").pvalue > 1e-3
+
+
+def test_spectral_probes_definition_by_brute_force_dft():
+    """Reading R35: column pair P is Re / Im of u_P[j] = (1/n) sum_k v_P[k] e^{+2 pi i j k / n},
+    v_P[k] = sqrt(n) (z0 + i z1) from Philox counter (k, P + 2^63) -- checked against an O(n^2)
+    explicit inverse DFT (catches a sign, scale or index error of the numpy route)."""
+    n, seed = 64, 3
+    for P_ in (0, 5):
+        Om = P.spectral_probes(n, [2 * P_, 2 * P_ + 1], seed)
+        z0, z1 = P.normal_pairs(np.arange(n, dtype=np.uint64), np.uint64(P_ | (1 << 63)), seed)
+        v = np.sqrt(n) * (z0 + 1j * z1)
+        jj, kk = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+        u = (np.exp(2j * np.pi * jj * kk / n) @ v) / n
+        assert np.max(np.abs(Om[:, 0] - u.real)) <= 1e-13
+        assert np.max(np.abs(Om[:, 1] - u.imag)) <= 1e-13
+    # a column does not depend on which others are requested (odd column alone, out of order)
+    Om = P.spectral_probes(n, [7, 4, 5], seed)
+    assert np.array_equal(Om[:, 2], P.spectral_probes(n, [4, 5], seed)[:, 1])
+    assert np.array_equal(Om[:, 0], P.spectral_probes(n, [6, 7], seed)[:, 1])
+
+
+def test_spectral_probes_are_iid_standard_normal():
+    """The distribution claim of reading R35: entries N(0,1), columns (also the two of a pair and
+    the entries of one column) uncorrelated, and a different stream from the entrywise probes."""
+    n = 1 << 14
+    Om = P.spectral_probes(n, list(range(8)), seed=1)
+    assert Om.shape == (n, 8) and Om.flags.f_contiguous
+    assert abs(Om.mean()) < 0.02
+    assert abs(Om.var() - 1.0) < 0.03
+    c = np.corrcoef(Om.T)
+    assert np.max(np.abs(c - np.eye(8))) < 0.05
+    assert abs(np.corrcoef(Om[:-1, 0], Om[1:, 0])[0, 1]) < 0.05     # neighbouring entries
+    from scipy import stats
+    assert stats.kstest(Om.ravel(), "norm").pvalue > 1e-3
+    E = P.probes(n, list(range(8)), seed=1)
+    assert np.max(np.abs(np.corrcoef(np.hstack([Om, E]).T)[:8, 8:])) < 0.05
+    # the plan rule: 1-D boxes with more than 2048 fine-grid points (the four-step layout)
+    from paper_2308_14490_b200 import inputs as I
+    assert I.make_config("interval", 2048).spectral_probes and not I.make_config("interval", 1024).spectral_probes
+    assert not I.get_config("c1").spectral_probes and I.get_config("c2").spectral_probes
+    assert not I.get_config("c3").spectral_probes
+    cfg = I.make_config("interval", 2048)
+    assert np.array_equal(P.probe_matrix(cfg, [3], cfg.seed), P.spectral_probes(cfg.N, [3], cfg.seed))
