@@ -76,6 +76,10 @@ struct az_plan_s {
   // merges and the SVD; side_ev: [0] TSQR leaf done, [1] R_S merged, [2] the side stream's work done
   cudaStream_t side = nullptr;
   cudaEvent_t side_ev[3] = {nullptr, nullptr, nullptr};
+  // second side stream: the Z* b column pass beside the right-hand-side merge passes, once pass B is
+  // done (side2_ev: [0] pass B done, [1] Z* b done)
+  cudaStream_t side2 = nullptr;
+  cudaEvent_t side2_ev[2] = {nullptr, nullptr};
   // high-priority stream for the TSQR and the SVD while the side stream runs: the block scheduler
   // then hands freed SMs to the merge tree (the critical path) before the side stream's passes
   cudaStream_t hi = nullptr;
@@ -130,6 +134,7 @@ size_t az_qr_ws_bytes(int64_t m, int64_t k);
 // pass A of the split leaf as a blocked QR with look-ahead (az_qr_la.cu): 256-row chunks, P CTAs of
 // rows_per_cta rows; Y (in place of A's k1 columns), taus and the per-CTA R factors as k_tsqr's pass A
 bool az_tsqr_la_enabled();
+int az_tsqr_la_mc();   // chunk rows of the look-ahead leaf (AZ_TSQR_LA_MC: 256 or 128)
 az_status_t az_tsqr_la_leaf(const double* A, int64_t m, int k1, int64_t ld, int64_t rows_per_cta, int P, double* Rout,
                             int64_t ostride, double* Y, int64_t ldY, double* taus, int cmax, cudaStream_t st);
 // R_S of the k1 probe columns on st (ev_leaf / ev_merged recorded there), then (Q^T b')[:k1] of the
@@ -138,7 +143,7 @@ az_status_t az_qr_r_deferred(double* A, int64_t m, int64_t k, int64_t k1, int64_
                              void* ws, size_t ws_bytes, cudaStream_t st, cudaEvent_t ev_leaf, cudaEvent_t ev_merged);
 az_status_t az_qr_rhs_deferred(double* A, int64_t m, int64_t k, int64_t k1, int64_t lda, double* C, int64_t ldc,
                                void* ws, size_t ws_bytes, cudaStream_t rhs_st, cudaEvent_t ev_leaf,
-                               cudaEvent_t ev_merged);
+                               cudaEvent_t ev_merged, cudaEvent_t ev_passb = nullptr);
 // rank_out: HOST, filled synchronously (may be null); rank_dev (optional): receives the DEVICE
 // address where the rank lands on `st` (valid while ws is)
 az_status_t az_tsvd_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs, double theta,

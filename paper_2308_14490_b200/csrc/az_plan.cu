@@ -384,6 +384,12 @@ static void plan_free(az_plan_s* p) {
     for (auto& e : p->side_ev)
       if (e) cudaEventDestroy(e);
   }
+  if (p->side2) {
+    cudaStreamSynchronize(p->side2);
+    cudaStreamDestroy(p->side2);
+    for (auto& e : p->side2_ev)
+      if (e) cudaEventDestroy(e);
+  }
   if (p->hi) {
     cudaStreamSynchronize(p->hi);
     cudaStreamDestroy(p->hi);

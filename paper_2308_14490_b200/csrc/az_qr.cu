@@ -577,7 +577,10 @@ static int def_nw() {
   }
   return v;
 }
-static int def_leaf_mc() { return def_nw() == 16 ? 256 : 128; }
+static int def_leaf_mc() {
+  if (def_nw() == 8) return 128;
+  return az_tsqr_la_enabled() ? az_tsqr_la_mc() : 256;
+}
 struct DefLev {
   double* Y;
   double* taus;
@@ -596,7 +599,7 @@ DefLayout def_layout(int64_t m, int64_t k, void* ws) {
   DefLayout d;
   // one leaf block fewer than SMs: pass B (one 170 KB CTA per SM and leaf block) then runs in a
   // single wave beside the one-CTA Jacobi, which holds an SM of its own
-  const int64_t per_sm = def_nw() == 16 ? 1 : 2;
+  const int64_t per_sm = def_leaf_mc() == 128 ? 2 : 1;
   d.P = std::max<int64_t>(1, std::min<int64_t>(per_sm * (num_sms() - 1), (m + 127) / 128));
   d.rows_per_cta = (m + d.P - 1) / d.P;
   d.cmax = (int)((d.rows_per_cta + def_leaf_mc() - 1) / def_leaf_mc());
@@ -674,7 +677,7 @@ az_status_t az_qr_r_deferred(double* A, int64_t m, int64_t k, int64_t k1, int64_
 
 az_status_t az_qr_rhs_deferred(double* A, int64_t m, int64_t k, int64_t k1, int64_t lda, double* C, int64_t ldc,
                                void* ws, size_t ws_bytes, cudaStream_t rhs_st, cudaEvent_t ev_leaf,
-                               cudaEvent_t ev_merged) {
+                               cudaEvent_t ev_merged, cudaEvent_t ev_passb) {
   if (!def_ok(k, k1) || ws_bytes < az_qr_ws_bytes(m, k)) {
     az_set_error("az_qr_rhs_deferred: needs 1 <= k1 <= 64, 1 <= k - k1 <= 64 and the az_qr workspace");
     return AZ_ERR_INVALID_ARGUMENT;
@@ -705,6 +708,7 @@ az_status_t az_qr_rhs_deferred(double* A, int64_t m, int64_t k, int64_t k1, int6
     k_tsqr_rhs<<<(unsigned)d.P, 512, rsm, rhs_st>>>(r);
     AZ_LAUNCH_CHECK();
   }
+  if (ev_passb) AZ_CUDA_CHECK(cudaEventRecord(ev_passb, rhs_st));
   AZ_CUDA_CHECK(cudaStreamWaitEvent(rhs_st, ev_merged, 0));
   for (const DefLev& L : d.lev) {   // the stacked blocks' right-hand-side columns, level by level
     QRr c;

@@ -27,14 +27,20 @@
 #include "az_mma.cuh"
 
 namespace {
-constexpr int LA_MC = 256;            // chunk rows
-constexpr int LA_LDX = LA_MC + 4;     // X column stride (== 4 mod 16: conflict-free DMMA fragments)
 constexpr int LA_LDR = 65;            // R column stride
 constexpr int LA_PW = 8;              // panel width
 constexpr int LA_NW = 8;              // warps: 0..3 factorise panels, 4..7 update
 constexpr int LA_NP = 4;              // panel warps
 constexpr int LA_NU = LA_NW - LA_NP;  // update warps
-constexpr int LA_RPW = LA_MC / LA_NP / 32;   // rows per lane in a panel warp (2)
+// Chunk shape: MC rows per chunk (256: one 175 KB CTA per SM; 128: two 110 KB CTAs per SM, whose
+// panel chains interleave), X column stride MC + 4 (== 4 mod 16: conflict-free DMMA fragments)
+template <int MC>
+struct LAShape {
+  static constexpr int LDX = MC + 4;
+  static constexpr int PR = MC / 4;          // rows of a panel warp
+  static constexpr int RPW = PR / 32;        // rows per lane in a panel warp
+  static constexpr int MINB = MC == 256 ? 1 : 2;
+};
 
 struct LAIn {
   const double* A;     // m x k1 (ld), the probe columns
@@ -56,9 +62,10 @@ AZ_D void cpa8(double* dst, const double* src, bool in) {
 }
 
 // shared-memory layout (doubles)
+template <int MC>
 struct LASmem {
-  static constexpr int X = 0;                  // 64 columns x LA_LDX
-  static constexpr int R = X + 64 * LA_LDX;    // 64 columns x LA_LDR
+  static constexpr int X = 0;                          // 64 columns x LDX
+  static constexpr int R = X + 64 * LAShape<MC>::LDX;  // 64 columns x LA_LDR
   static constexpr int T = R + 64 * LA_LDR;    // 2 x 64: T[a][m] at a * 8 + m (double-buffered by panel parity)
   static constexpr int RED2 = T + 128;         // 2 x 8 x 4: partial dots, d[l] of warp i at l * 4 + i
   static constexpr int WP = RED2 + 64;         // 8 x 64: the look-ahead tile's partial W (one per warp)
@@ -78,6 +85,7 @@ AZ_D double tt_w(const double* T, const double* W, int m, int n) {
 }
 
 // X[:, c0 .. c0+8) -= Y_J W' over the row tiles mt0 .. mt1 - 1 (8 rows each; W' at Wp[m * 8 + n])
+template <int LDX>
 AZ_D void tile_rank_update(double* X, const double* Wp, int j0, int c0, int k1, int mt0, int mt1, int lane) {
   const int r = lane >> 2, q = lane & 3;
   const int ca = c0 + 2 * q, cb = ca + 1;
@@ -85,26 +93,27 @@ AZ_D void tile_rank_update(double* X, const double* Wp, int j0, int c0, int k1, 
   for (int mt = mt0; mt < mt1; ++mt) {
     const int row = 8 * mt + r;
     double c[2];
-    c[0] = ca < k1 ? X[ca * LA_LDX + row] : 0.0;
-    c[1] = cb < k1 ? X[cb * LA_LDX + row] : 0.0;
-    dmma(c, -X[(j0 + q) * LA_LDX + row], b0);       // A(m = row, k = panel col)
-    dmma(c, -X[(j0 + q + 4) * LA_LDX + row], b1);
-    if (ca < k1) X[ca * LA_LDX + row] = c[0];
-    if (cb < k1) X[cb * LA_LDX + row] = c[1];
+    c[0] = ca < k1 ? X[ca * LDX + row] : 0.0;
+    c[1] = cb < k1 ? X[cb * LDX + row] : 0.0;
+    dmma(c, -X[(j0 + q) * LDX + row], b0);       // A(m = row, k = panel col)
+    dmma(c, -X[(j0 + q + 4) * LDX + row], b1);
+    if (ca < k1) X[ca * LDX + row] = c[0];
+    if (cb < k1) X[cb * LDX + row] = c[1];
   }
 }
 
 // W (8 x 8 C fragment) += Y_J^T X[:, c0..c0+8) over rows [k0, k1r), two accumulators
+template <int LDX>
 AZ_D void tile_w(double (&acc)[2], const double* X, int j0, int c0, int k1, int k0, int k1r, int lane) {
   const int r = lane >> 2, qd = lane & 3;
   const int cb = c0 + r;
   double a2[2] = {0.0, 0.0};
 #pragma unroll 4
   for (int kk = k0; kk < k1r; kk += 8) {
-    const double a0 = X[(j0 + r) * LA_LDX + kk + qd];
-    const double b0 = cb < k1 ? X[cb * LA_LDX + kk + qd] : 0.0;
-    const double a1 = X[(j0 + r) * LA_LDX + kk + 4 + qd];
-    const double b1 = cb < k1 ? X[cb * LA_LDX + kk + 4 + qd] : 0.0;
+    const double a0 = X[(j0 + r) * LDX + kk + qd];
+    const double b0 = cb < k1 ? X[cb * LDX + kk + qd] : 0.0;
+    const double a1 = X[(j0 + r) * LDX + kk + 4 + qd];
+    const double b1 = cb < k1 ? X[cb * LDX + kk + 4 + qd] : 0.0;
     dmma(acc, a0, b0);
     dmma(a2, a1, b1);
   }
@@ -117,16 +126,17 @@ AZ_D void tile_w(double (&acc)[2], const double* X, int j0, int c0, int k1, int 
 // FULLW = 8: a full panel (every column test resolved at compile time); 0: a last, narrower panel.
 // Warp 0 writes R's panel rows, warp 1 forms T (lane a owns row a), warp 2 stores the taus, so that
 // no warp carries all the side work between the two barriers of a column.
-template <int FULLW>
+template <int MC, int FULLW>
 AZ_D void la_panel(double* X, double* R, double* sm, double* Tm, const LAIn& q, int chunk, int j0, int k1, int w,
                    int lane) {
+  constexpr int LDX = LAShape<MC>::LDX, RPW = LAShape<MC>::RPW, PR = LAShape<MC>::PR;
   const int PWN = FULLW ? FULLW : min(LA_PW, k1 - j0);
-  double* red2 = sm + LASmem::RED2;
-  double x[LA_PW][LA_RPW];   // column j0 + c, row 64 w + lane + 32 i
+  double* red2 = sm + LASmem<MC>::RED2;
+  double x[LA_PW][RPW];   // column j0 + c, row PR w + lane + 32 i
 #pragma unroll
   for (int c = 0; c < LA_PW; ++c)
 #pragma unroll
-    for (int i = 0; i < LA_RPW; ++i) x[c][i] = c < PWN ? X[(j0 + c) * LA_LDX + 64 * w + lane + 32 * i] : 0.0;
+    for (int i = 0; i < RPW; ++i) x[c][i] = c < PWN ? X[(j0 + c) * LDX + PR * w + lane + 32 * i] : 0.0;
   double trow[LA_PW];   // warp 1, lane a < 8: row a of T
 #pragma unroll
   for (int m = 0; m < LA_PW; ++m) trow[m] = 0.0;
@@ -147,7 +157,7 @@ AZ_D void la_panel(double* X, double* R, double* sm, double* Tm, const LAIn& q, 
       d[l] = 0.0;
       if (l < PWN)
 #pragma unroll
-        for (int i = 0; i < LA_RPW; ++i) d[l] = fma(x[c][i], x[l][i], d[l]);
+        for (int i = 0; i < RPW; ++i) d[l] = fma(x[c][i], x[l][i], d[l]);
     }
     // transpose-reduce: 3 halving levels leave lane L a partial of slot L / 4, 2 more complete it
 #pragma unroll
@@ -183,7 +193,7 @@ AZ_D void la_panel(double* X, double* R, double* sm, double* Tm, const LAIn& q, 
       scale = fast_rcp(alpha - beta);
     }
 #pragma unroll
-    for (int i = 0; i < LA_RPW; ++i) x[c][i] *= scale;   // y_c
+    for (int i = 0; i < RPW; ++i) x[c][i] *= scale;   // y_c
 #pragma unroll
     for (int l = 0; l < LA_PW; ++l) d[l] *= scale;       // y_c . x_l (l > c), y_c . y_l (l < c)
     if (w == 0 && lane == 0) R[jc * LA_LDR + jc] = beta;
@@ -202,7 +212,7 @@ AZ_D void la_panel(double* X, double* R, double* sm, double* Tm, const LAIn& q, 
         if (l > c && l < PWN) {
           const double wl = tau * (rl[l] + d[l]);
 #pragma unroll
-          for (int i = 0; i < LA_RPW; ++i) x[l][i] = fma(-wl, x[c][i], x[l][i]);
+          for (int i = 0; i < RPW; ++i) x[l][i] = fma(-wl, x[c][i], x[l][i]);
           if (w == 0 && lane == 0) R[(j0 + l) * LA_LDR + jc] = rl[l] - wl;
         }
       }
@@ -212,17 +222,20 @@ AZ_D void la_panel(double* X, double* R, double* sm, double* Tm, const LAIn& q, 
 #pragma unroll
   for (int c = 0; c < LA_PW; ++c)
 #pragma unroll
-    for (int i = 0; i < LA_RPW; ++i)
-      if (c < PWN) X[(j0 + c) * LA_LDX + 64 * w + lane + 32 * i] = x[c][i];
+    for (int i = 0; i < RPW; ++i)
+      if (c < PWN) X[(j0 + c) * LDX + PR * w + lane + 32 * i] = x[c][i];
   if (w == 1 && lane < LA_PW)
 #pragma unroll
     for (int m = 0; m < LA_PW; ++m) Tm[lane * 8 + m] = trow[m];
 }
 
-__global__ void __launch_bounds__(32 * LA_NW, 1) k_tsqr_la(LAIn q) {
+template <int MC>
+__global__ void __launch_bounds__(32 * LA_NW, LAShape<MC>::MINB) k_tsqr_la(LAIn q) {
+  constexpr int LDX = LAShape<MC>::LDX;
+  using SM = LASmem<MC>;
   extern __shared__ double sm[];
-  double* X = sm + LASmem::X;
-  double* R = sm + LASmem::R;
+  double* X = sm + SM::X;
+  double* R = sm + SM::R;
   const int k1 = q.k1;
   const int np = (k1 + LA_PW - 1) / LA_PW;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -235,14 +248,14 @@ __global__ void __launch_bounds__(32 * LA_NW, 1) k_tsqr_la(LAIn q) {
   const int gi = (w & 1) | ((w >> 2) << 1);   // index within the warp's group (0..3)
   for (int e = tid; e < 64 * LA_LDR; e += 32 * LA_NW) R[e] = 0.0;
   // column slots past k1 are read as (zero) columns of a last, narrower panel or tile
-  for (int e = tid; e < (64 - k1) * LA_LDX; e += 32 * LA_NW) X[k1 * LA_LDX + e] = 0.0;
+  for (int e = tid; e < (64 - k1) * LDX; e += 32 * LA_NW) X[k1 * LDX + e] = 0.0;
   const int64_t r0 = (int64_t)blockIdx.x * q.rows_per_cta;
   const int64_t r1 = min(q.m, r0 + q.rows_per_cta);
   // first chunk: columns of 256 contiguous rows; rows past r1 zero-filled
-  for (int e = tid; e < k1 * LA_MC; e += 32 * LA_NW) {
-    const int c = e / LA_MC, i = e % LA_MC;
+  for (int e = tid; e < k1 * MC; e += 32 * LA_NW) {
+    const int c = e / MC, i = e % MC;
     const int64_t row = r0 + i;
-    cpa8(X + c * LA_LDX + i, q.A + (row < r1 ? row : 0) + (int64_t)c * q.ld, row < r1);
+    cpa8(X + c * LDX + i, q.A + (row < r1 ? row : 0) + (int64_t)c * q.ld, row < r1);
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
   asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -253,43 +266,43 @@ __global__ void __launch_bounds__(32 * LA_NW, 1) k_tsqr_la(LAIn q) {
     const int j0 = pp * LA_PW, pw = min(LA_PW, k1 - j0);
     const int ut = 32 * gi + lane;
     bar_sync(BAR_U, 32 * LA_NU);   // every update of panel pp is done
-    for (int e = ut; e < pw * LA_MC; e += 32 * LA_NU) {
-      const int c = e / LA_MC, i = e % LA_MC;
+    for (int e = ut; e < pw * MC; e += 32 * LA_NU) {
+      const int c = e / MC, i = e % MC;
       const int64_t row = base + i;
-      if (row < r1) q.Y[row + (int64_t)(j0 + c) * q.ldY] = X[(j0 + c) * LA_LDX + i];
+      if (row < r1) q.Y[row + (int64_t)(j0 + c) * q.ldY] = X[(j0 + c) * LDX + i];
     }
     if (nbase < r1) {
       bar_sync(BAR_U, 32 * LA_NU);   // the slot is read before it is overwritten
-      for (int e = ut; e < pw * LA_MC; e += 32 * LA_NU) {
-        const int c = e / LA_MC, i = e % LA_MC;
+      for (int e = ut; e < pw * MC; e += 32 * LA_NU) {
+        const int c = e / MC, i = e % MC;
         const int64_t row = nbase + i;
-        cpa8(X + (j0 + c) * LA_LDX + i, q.A + (row < r1 ? row : 0) + (int64_t)(j0 + c) * q.ld, row < r1);
+        cpa8(X + (j0 + c) * LDX + i, q.A + (row < r1 ? row : 0) + (int64_t)(j0 + c) * q.ld, row < r1);
       }
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
   };
 
   int chunk = 0;
-  for (int64_t base = r0; base < r1; base += LA_MC, ++chunk) {
-    const int64_t nbase = base + LA_MC;
+  for (int64_t base = r0; base < r1; base += MC, ++chunk) {
+    const int64_t nbase = base + MC;
     for (int p = 0; p < np; ++p) {
       const int j0 = p * LA_PW, pw = min(LA_PW, k1 - j0);
-      double* Tm = sm + LASmem::T + (p & 1) * 64;
+      double* Tm = sm + SM::T + (p & 1) * 64;
       if (panel_w) {
         // ================= panel p, panel warp gi: rows 64 gi .. 64 gi + 63 =================
         if (pw == LA_PW)
-          la_panel<LA_PW>(X, R, sm, Tm, q, chunk, j0, k1, gi, lane);
+          la_panel<MC, LA_PW>(X, R, sm, Tm, q, chunk, j0, k1, gi, lane);
         else
-          la_panel<0>(X, R, sm, Tm, q, chunk, j0, k1, gi, lane);
+          la_panel<MC, 0>(X, R, sm, Tm, q, chunk, j0, k1, gi, lane);
       } else if (p > 0) {
         // ========= update warps: panel p - 1 on the columns right of panel p (tiles p + 1 ..) =========
         const int uw = gi, pj0 = j0 - LA_PW;
-        const double* Tp = sm + LASmem::T + ((p - 1) & 1) * 64;
-        double* WS = sm + LASmem::WS + uw * 64;
+        const double* Tp = sm + SM::T + ((p - 1) & 1) * 64;
+        double* WS = sm + SM::WS + uw * 64;
         for (int t = p + 1 + uw; t * LA_PW < k1; t += LA_NU) {
           const int ct = t * LA_PW;
           double acc[2] = {0.0, 0.0};
-          tile_w(acc, X, pj0, ct, k1, 0, LA_MC, lane);
+          tile_w<LDX>(acc, X, pj0, ct, k1, 0, MC, lane);
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int n = 2 * qd + e;
@@ -310,7 +323,7 @@ __global__ void __launch_bounds__(32 * LA_NW, 1) k_tsqr_la(LAIn q) {
             if (ct + n < k1) R[(ct + n) * LA_LDR + pj0 + m] -= wv[e2];
           }
           __syncwarp();
-          tile_rank_update(X, WS, pj0, ct, k1, 0, LA_MC / 8, lane);
+          tile_rank_update<LDX>(X, WS, pj0, ct, k1, 0, MC / 8, lane);
           __syncwarp();
         }
       }
@@ -320,11 +333,11 @@ __global__ void __launch_bounds__(32 * LA_NW, 1) k_tsqr_la(LAIn q) {
         // W' = T^T W by warp 0 and each panel warp updates its own 64 rows (so it can go straight on to
         // factorising the next panel); the update warps meanwhile write back panel p - 1 ======
         const int c0 = j0 + LA_PW;
-        double* Wp = sm + LASmem::WP;
-        double* Ws = sm + LASmem::WSUM;
-        double* WL = sm + LASmem::WL;
+        double* Wp = sm + SM::WP;
+        double* Ws = sm + SM::WSUM;
+        double* WL = sm + SM::WL;
         double acc[2] = {0.0, 0.0};
-        tile_w(acc, X, j0, c0, k1, 32 * w, 32 * w + 32, lane);
+        tile_w<LDX>(acc, X, j0, c0, k1, (MC / 8) * w, (MC / 8) * (w + 1), lane);
         Wp[w * 64 + r8 * 8 + 2 * qd] = acc[0];
         Wp[w * 64 + r8 * 8 + 2 * qd + 1] = acc[1];
         __syncthreads();
@@ -348,7 +361,7 @@ __global__ void __launch_bounds__(32 * LA_NW, 1) k_tsqr_la(LAIn q) {
         }
         if (panel_w) {
           bar_sync(BAR_P, 32 * LA_NP);
-          tile_rank_update(X, WL, j0, c0, k1, 8 * gi, 8 * gi + 8, lane);
+          tile_rank_update<LDX>(X, WL, j0, c0, k1, (MC / 32) * gi, (MC / 32) * (gi + 1), lane);
         } else if (p > 0) {
           writeback(p - 1, base, nbase);
         }
@@ -371,7 +384,19 @@ __global__ void __launch_bounds__(32 * LA_NW, 1) k_tsqr_la(LAIn q) {
 }
 }  // namespace
 
-size_t az_tsqr_la_smem() { return (size_t)LASmem::END * sizeof(double); }
+// AZ_TSQR_LA_MC=128: 128-row chunks, two CTAs per SM (default 256: one CTA per SM)
+int az_tsqr_la_mc() {
+  static int v = 0;
+  if (!v) {
+    const char* e = getenv("AZ_TSQR_LA_MC");
+    v = (e && atoi(e) == 128) ? 128 : 256;
+  }
+  return v;
+}
+
+size_t az_tsqr_la_smem() {
+  return (size_t)(az_tsqr_la_mc() == 128 ? LASmem<128>::END : LASmem<256>::END) * sizeof(double);
+}
 
 // AZ_TSQR_LA=0: pass A of the split leaf by the per-column kernel k_tsqr instead
 bool az_tsqr_la_enabled() {
@@ -402,9 +427,10 @@ az_status_t az_tsqr_la_leaf(const double* A, int64_t m, int k1, int64_t ld, int6
   q.ostride = ostride;
   q.taus = taus;
   const size_t sm = az_tsqr_la_smem();
-  AZ_CUDA_CHECK(az_smem_attr(k_tsqr_la, sm));
+  auto kern = az_tsqr_la_mc() == 128 ? k_tsqr_la<128> : k_tsqr_la<256>;
+  AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   AzTrace tr("tsqr_leaf", st, m);
-  k_tsqr_la<<<P, 32 * LA_NW, sm, st>>>(q);
+  kern<<<P, 32 * LA_NW, sm, st>>>(q);
   AZ_LAUNCH_CHECK();
   return AZ_OK;
 }

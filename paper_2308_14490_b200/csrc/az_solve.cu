@@ -198,6 +198,20 @@ static bool qr_defer() {
 }
 
 // AZ_SOLVE_HI=0: the QR and the SVD stay on the caller's stream while the side stream runs
+// AZ_SIDE2: 2 (default) the Z* b column pass on a second side stream right after the TSQR leaf, beside
+// the M pass and the merges; 1: on that stream after pass B; 0: on the side stream before the M pass
+// (the former order).  Measured c2 ms per step (two 20-step runs each): 2: 9.21 / 9.22, 1: 9.30 / 9.30,
+// 0: 9.28 / 9.33.
+static int side2_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AZ_SIDE2");
+    v = e ? atoi(e) : 2;
+    if (v < 0 || v > 2) v = 2;
+  }
+  return v;
+}
+
 static bool no_hi() {
   static int k = -1;
   if (k < 0) {
@@ -414,12 +428,16 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
     int lo = 0, top = 0;
     AZ_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &top));
     AZ_CUDA_CHECK(cudaStreamCreateWithPriority(&p->hi, cudaStreamNonBlocking, top));
+    AZ_CUDA_CHECK(cudaStreamCreateWithFlags(&p->side2, cudaStreamNonBlocking));
+    for (auto& e : p->side2_ev) AZ_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   // the QR and the SVD: on the high-priority stream beside the side stream (joined back below)
   cudaStream_t qs = side && !no_hi() ? p->hi : st;
   // Q^T b' off the R factor's critical path: R_S alone through the merge tree, P = pinv_theta(R_S) by
   // the SVD of [R_S | I], while b' follows the kept reflectors on the side stream; y = P (Q^T b')
   const bool defer = side && qr_defer() && R <= 64 && nrhs <= 64 && w.Rp;
+  const int s2mode = side2_mode();
+  const bool use_side2 = side && defer && s2mode != 0;
   if (w.Zb && w.Zs) {   // b' and, for step 2, Z* b (one extra column pass)
     AZ_TRY(az1f_resid_z(p, b, ldb, bp_in_S ? w.S + R * rows : w.bp, rows, w.Zb, p->N, nrhs, st, w.Zs, side));
   } else if (w.Zb) {    // one-CTA layout: Z* b from the chain's spectrum of it (one more transform)
@@ -472,11 +490,24 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
         // side stream: the deferred Z* b and M passes beside the merges (whose CTAs take freed SMs
         // first), then -- deferred -- Q^T b' through the kept reflectors beside the SVD
         AZ_CUDA_CHECK(cudaStreamWaitEvent(p->side, p->side_ev[0], 0));
-        AZ_TRY(az1f_out_z(p, w.Zs, w.Zb, p->N, nrhs, p->side));
+        if (!use_side2) AZ_TRY(az1f_out_z(p, w.Zs, w.Zb, p->N, nrhs, p->side));
         AZ_TRY(az1f_out_z(p, p->d_Z2, w.Om, p->N, R, p->side));
+        // Z* b on a second side stream: after pass B (mode 1; it then runs beside the right-hand-side
+        // merge passes and the SVD, which leave most SMs idle) or right after the leaf (mode 2)
+        if (use_side2 && s2mode == 2) {
+          AZ_CUDA_CHECK(cudaStreamWaitEvent(p->side2, p->side_ev[0], 0));
+          AZ_TRY(az1f_out_z(p, w.Zs, w.Zb, p->N, nrhs, p->side2));
+        }
         if (defer)
           AZ_TRY(az_qr_rhs_deferred(w.S, rows, kt, kp, rows, w.cq, kp, w.qrws, w.qrbytes, p->side, p->side_ev[0],
-                                    p->side_ev[1]));
+                                    p->side_ev[1], use_side2 && s2mode == 1 ? p->side2_ev[0] : nullptr));
+        if (use_side2) {
+          if (s2mode == 1) {
+            AZ_CUDA_CHECK(cudaStreamWaitEvent(p->side2, p->side2_ev[0], 0));
+            AZ_TRY(az1f_out_z(p, w.Zs, w.Zb, p->N, nrhs, p->side2));
+          }
+          AZ_CUDA_CHECK(cudaEventRecord(p->side2_ev[1], p->side2));
+        }
         AZ_CUDA_CHECK(cudaEventRecord(p->side_ev[2], p->side));
       }
     } else {
@@ -552,6 +583,7 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
     // by linearity of Z* (PAPER.md:229-230): x = Omega y + Z* b - (Z* A Omega) y = Z* b + M y, with
     // Z* b and M = Omega - Z* A Omega produced by the b' and sketch chains: one DMMA pass, no FFT
     if (side) AZ_CUDA_CHECK(cudaStreamWaitEvent(st, p->side_ev[2], 0));   // Z* b, M (and Q^T b') are ready
+    if (use_side2) AZ_CUDA_CHECK(cudaStreamWaitEvent(st, p->side2_ev[1], 0));
     if (defer) {   // y = P (Q^T b')
       AzTrace tr("y_pc", st);
       k_gemm_mn<<<dim3(az_div_up(kp, 64), az_div_up(nrhs, 64)), 256, 0, st>>>(w.Pm, kp, w.cq, kp, w.y, kp, kp, kp,
