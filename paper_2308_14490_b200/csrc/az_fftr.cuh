@@ -133,30 +133,64 @@ struct StageRadix {
   static constexpr int value = (L / NS) >= E ? E : (L / NS);
 };
 
+// twiddle operands of the stage whose span is NS: per butterfly b, w^(2^q) (q < NQ) with
+// w = e^{DIR 2 pi i k / (NS R)}, k = (j + b T) mod NS, read from the table (conjugated for DIR > 0)
+template <int L, int E, int NS>
+struct StageTw {
+  static constexpr int R = StageRadix<L, E, NS>::value;
+  static constexpr int NB = E / R;
+  static constexpr int NQ = R >= 16 ? 4 : (R >= 8 ? 3 : (R >= 4 ? 2 : 1));
+};
+
 template <int L, int E, int DIR, int NS>
-AZ_D void stages(cplx (&v)[E], int j, cplx* buf, const cplx* __restrict__ tw, int twn) {
+AZ_D void load_tw(cplx (&wp)[StageTw<L, E, NS>::NB][4], int j, const cplx* __restrict__ tw, int twn) {
+  using S = StageTw<L, E, NS>;
+  constexpr int T = L / E;
+#pragma unroll
+  for (int b = 0; b < S::NB; ++b) {
+    const int k = (j + b * T) & (NS - 1);
+    const int tstep = k * (twn / (NS * S::R));
+#pragma unroll
+    for (int q = 0; q < S::NQ; ++q) {
+      wp[b][q] = tw[tstep << q];
+      if (DIR > 0) wp[b][q].y = -wp[b][q].y;
+    }
+  }
+}
+
+// One stage and, recursively, the rest.  PRE: this stage's twiddle operands wpre were loaded by the
+// previous stage, so the table reads overlap its butterflies and exchange instead of stalling this
+// stage's multiplies; a stage prefetches the next one's when they are at most PF complex values per
+// thread (the register budget: PF = 8 for the 2048-point row transforms, 4 for the column passes).
+template <int L, int E, int DIR, int NS, int PF, bool PRE>
+AZ_D void stages(cplx (&v)[E], int j, cplx* buf, const cplx* __restrict__ tw, int twn,
+                 const cplx (&wpre)[StageTw<L, E, NS>::NB][4]) {
   constexpr int R = StageRadix<L, E, NS>::value;
   constexpr int T = L / E;
   constexpr int NB = E / R;            // butterflies per thread
   constexpr bool last = NS * R == L;
+  constexpr int NSN = last ? NS : NS * R;   // next stage's span
+  constexpr bool pre_next = !last && StageTw<L, E, NSN>::NB * StageTw<L, E, NSN>::NQ <= PF;
+  cplx wn[StageTw<L, E, NSN>::NB][4];
+  if constexpr (pre_next) load_tw<L, E, DIR, NSN>(wn, j, tw, twn);
+  cplx wp[NB][4];
+  if constexpr (NS > 1) {
+    if constexpr (PRE) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) wp[b][q] = wpre[b][q];
+    } else {
+      load_tw<L, E, DIR, NS>(wp, j, tw, twn);
+    }
+  }
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
-    const int jj = j + b * T;
-    const int k = jj & (NS - 1);
     cplx u[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) u[r] = v[b + r * NB];
     if constexpr (NS > 1) {
-      // w^r from the table entries w, w^2, w^4, w^8 (at most 3 extra products per power: a few
-      // ulps), so a stage holds 4 loaded twiddles instead of R - 1
-      const int tstep = k * (twn / (NS * R));
-      cplx wp[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if ((1 << q) < R) {
-          wp[q] = tw[tstep << q];
-          if (DIR > 0) wp[q].y = -wp[q].y;
-        }
+      // w^r from w, w^2, w^4, w^8 (at most 3 extra products per power: a few ulps)
 #pragma unroll
       for (int r = 1; r < R; ++r) {
         cplx w = make_double2(1.0, 0.0);
@@ -164,7 +198,7 @@ AZ_D void stages(cplx (&v)[E], int j, cplx* buf, const cplx* __restrict__ tw, in
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           if (r & (1 << q)) {
-            w = first ? wp[q] : cmul(w, wp[q]);
+            w = first ? wp[b][q] : cmul(w, wp[b][q]);
             first = false;
           }
         u[r] = cmul(u[r], w);
@@ -193,17 +227,18 @@ AZ_D void stages(cplx (&v)[E], int j, cplx* buf, const cplx* __restrict__ tw, in
 #pragma unroll
       for (int r = 0; r < R2; ++r) v[b + r * NB2] = buf[padE<E>(jj + r * (L / R2))];
     }
-    stages<L, E, DIR, NS * R>(v, j, buf, tw, twn);
+    stages<L, E, DIR, NS * R, PF, pre_next>(v, j, buf, tw, twn, wn);
   }
 }
 
 // All threads of the CTA must call this (it contains __syncthreads).  buf: padded_lenE<E>(L) complex
 // values private to this FFT.  tw[t] = e^{-2 pi i t / twn}, twn >= L a power of two.
-template <int L, int E, int DIR>
+template <int L, int E, int DIR, int PF = 8>
 AZ_D void fft(cplx (&v)[E], int j, cplx* buf, const cplx* __restrict__ tw, int twn) {
   static_assert((L & (L - 1)) == 0 && (E & (E - 1)) == 0 && E <= 16 && E >= 2, "power-of-two sizes");
   static_assert(L % E == 0, "E must divide L");
-  stages<L, E, DIR, 1>(v, j, buf, tw, twn);
+  const cplx none[StageTw<L, E, 1>::NB][4] = {};   // the first stage has no twiddles
+  stages<L, E, DIR, 1, PF, false>(v, j, buf, tw, twn, none);
 }
 
 }  // namespace fftr

@@ -136,7 +136,9 @@ size_t az_qr_ws_bytes(int64_t m, int64_t k);
 bool az_tsqr_la_enabled();
 int az_tsqr_la_mc();   // chunk rows of the look-ahead leaf (AZ_TSQR_LA_MC: 256 or 128)
 az_status_t az_tsqr_la_leaf(const double* A, int64_t m, int k1, int64_t ld, int64_t rows_per_cta, int P, double* Rout,
-                            int64_t ostride, double* Y, int64_t ldY, double* taus, int cmax, cudaStream_t st);
+                            int64_t ostride, double* Y, int64_t ldY, double* taus, int cmax, cudaStream_t st,
+                            int64_t rb = 0, int64_t bstride = 0);
+bool az_tsqr_la_merge_enabled();   // AZ_TSQR_LA_MERGE (default 1): merge levels by the look-ahead kernel
 // R_S of the k1 probe columns on st (ev_leaf / ev_merged recorded there), then (Q^T b')[:k1] of the
 // k - k1 right-hand-side columns on rhs_st (k1, k - k1 <= 64; A is scratch) (az_qr.cu)
 az_status_t az_qr_r_deferred(double* A, int64_t m, int64_t k, int64_t k1, int64_t lda, double* Rs, int64_t ldrs,

@@ -140,9 +140,9 @@ AZ_D void cols_body(const P1f& a, cplx (&v)[EC], int j, int col, int b, cplx* bu
 
   // ---- transforms ----
   if constexpr (KIND == FC_IN_COEF || KIND == FC_IN_ROWS || KIND == FC_FWD_G) {
-    fftr::fft<NC, EC, -1>(v, j, buf, a.tw, TWN);
+    fftr::fft<NC, EC, -1, 4>(v, j, buf, a.tw, TWN);
   } else if constexpr (KIND == FC_RESID_MID) {
-    fftr::fft<NC, EC, 1>(v, j, buf, a.tw, TWN);
+    fftr::fft<NC, EC, 1, 4>(v, j, buf, a.tw, TWN);
 #pragma unroll
     for (int e = 0; e < EC; ++e) {
       const int r = row_of(a, (int64_t)(j + e * T) * W + col);
@@ -150,15 +150,15 @@ AZ_D void cols_body(const P1f& a, cplx (&v)[EC], int j, int col, int b, cplx* bu
                                    cc.has_im ? a.in2[r + cc.cim * a.ldin2] - v[e].y : 0.0)
                     : czero();
     }
-    fftr::fft<NC, EC, -1>(v, j, buf, a.tw, TWN);
+    fftr::fft<NC, EC, -1, 4>(v, j, buf, a.tw, TWN);
   } else if constexpr (KIND == FC_FINE_MASK) {
-    fftr::fft<NC, EC, 1>(v, j, buf, a.tw, TWN);
+    fftr::fft<NC, EC, 1, 4>(v, j, buf, a.tw, TWN);
 #pragma unroll
     for (int e = 0; e < EC; ++e)
       if (!((mbits >> e) & 1u)) v[e] = czero();
-    fftr::fft<NC, EC, -1>(v, j, buf, a.tw, TWN);
+    fftr::fft<NC, EC, -1, 4>(v, j, buf, a.tw, TWN);
   } else {
-    fftr::fft<NC, EC, 1>(v, j, buf, a.tw, TWN);
+    fftr::fft<NC, EC, 1, 4>(v, j, buf, a.tw, TWN);
   }
 
   // ---- store ----

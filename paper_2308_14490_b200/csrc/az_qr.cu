@@ -667,7 +667,11 @@ az_status_t az_qr_r_deferred(double* A, int64_t m, int64_t k, int64_t k1, int64_
     t.ldY = k1;
     t.taus = L.taus;
     t.cmax = 1;
-    AZ_TRY((tsqr_launch<4, 8>(t, (int)L.next, st)));
+    if (az_tsqr_la_merge_enabled())   // 4 stacked k1 x k1 factors = one chunk of <= 256 rows per CTA
+      AZ_TRY(az_tsqr_la_leaf(t.A, t.m, (int)k1, t.ld, t.rows_per_cta, (int)L.next, t.Rout, t.ostride, t.Y, t.ldY,
+                             t.taus, 1, st, t.rb, t.bstride));
+    else
+      AZ_TRY((tsqr_launch<4, 8>(t, (int)L.next, st)));
   }
   k_copy_R<<<az_div_up(k1 * k1, 256), 256, 0, st>>>(d.buf[d.final_which], (int)k1, (int)k1, Rs, ldrs);
   AZ_LAUNCH_CHECK();

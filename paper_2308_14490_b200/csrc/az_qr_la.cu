@@ -46,6 +46,7 @@ struct LAIn {
   const double* A;     // m x k1 (ld), the probe columns
   double* Y;           // y_j written back (== A for the split leaf)
   int64_t m, ld, ldY, rows_per_cta;
+  int64_t rb, bstride;   // merges: stacked row r of A and Y at (r / rb) bstride + r % rb (0 = plain rows)
   int k1, cmax;
   double* Rout;        // per CTA k1 x k1 (ld k1), CTA stride ostride
   int64_t ostride;
@@ -229,7 +230,7 @@ AZ_D void la_panel(double* X, double* R, double* sm, double* Tm, const LAIn& q, 
     for (int m = 0; m < LA_PW; ++m) Tm[lane * 8 + m] = trow[m];
 }
 
-template <int MC>
+template <int MC, bool STACK>
 __global__ void __launch_bounds__(32 * LA_NW, LAShape<MC>::MINB) k_tsqr_la(LAIn q) {
   constexpr int LDX = LAShape<MC>::LDX;
   using SM = LASmem<MC>;
@@ -251,11 +252,15 @@ __global__ void __launch_bounds__(32 * LA_NW, LAShape<MC>::MINB) k_tsqr_la(LAIn 
   for (int e = tid; e < (64 - k1) * LDX; e += 32 * LA_NW) X[k1 * LDX + e] = 0.0;
   const int64_t r0 = (int64_t)blockIdx.x * q.rows_per_cta;
   const int64_t r1 = min(q.m, r0 + q.rows_per_cta);
+  auto roff = [&](int64_t row) -> int64_t {
+    if constexpr (STACK) return (row / q.rb) * q.bstride + row % q.rb;
+    return row;
+  };
   // first chunk: columns of 256 contiguous rows; rows past r1 zero-filled
   for (int e = tid; e < k1 * MC; e += 32 * LA_NW) {
     const int c = e / MC, i = e % MC;
     const int64_t row = r0 + i;
-    cpa8(X + c * LDX + i, q.A + (row < r1 ? row : 0) + (int64_t)c * q.ld, row < r1);
+    cpa8(X + c * LDX + i, q.A + roff(row < r1 ? row : r0) + (int64_t)c * q.ld, row < r1);
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
   asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -269,14 +274,14 @@ __global__ void __launch_bounds__(32 * LA_NW, LAShape<MC>::MINB) k_tsqr_la(LAIn 
     for (int e = ut; e < pw * MC; e += 32 * LA_NU) {
       const int c = e / MC, i = e % MC;
       const int64_t row = base + i;
-      if (row < r1) q.Y[row + (int64_t)(j0 + c) * q.ldY] = X[(j0 + c) * LDX + i];
+      if (row < r1) q.Y[roff(row) + (int64_t)(j0 + c) * q.ldY] = X[(j0 + c) * LDX + i];
     }
     if (nbase < r1) {
       bar_sync(BAR_U, 32 * LA_NU);   // the slot is read before it is overwritten
       for (int e = ut; e < pw * MC; e += 32 * LA_NU) {
         const int c = e / MC, i = e % MC;
         const int64_t row = nbase + i;
-        cpa8(X + (j0 + c) * LDX + i, q.A + (row < r1 ? row : 0) + (int64_t)(j0 + c) * q.ld, row < r1);
+        cpa8(X + (j0 + c) * LDX + i, q.A + roff(row < r1 ? row : r0) + (int64_t)(j0 + c) * q.ld, row < r1);
       }
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
@@ -394,6 +399,16 @@ int az_tsqr_la_mc() {
   return v;
 }
 
+// AZ_TSQR_LA_MERGE=0: the deferred merge levels by the per-column kernel k_tsqr instead
+bool az_tsqr_la_merge_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AZ_TSQR_LA_MERGE");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0 && az_tsqr_la_enabled() && az_tsqr_la_mc() == 256;
+}
+
 size_t az_tsqr_la_smem() {
   return (size_t)(az_tsqr_la_mc() == 128 ? LASmem<128>::END : LASmem<256>::END) * sizeof(double);
 }
@@ -409,7 +424,8 @@ bool az_tsqr_la_enabled() {
 }
 
 az_status_t az_tsqr_la_leaf(const double* A, int64_t m, int k1, int64_t ld, int64_t rows_per_cta, int P, double* Rout,
-                            int64_t ostride, double* Y, int64_t ldY, double* taus, int cmax, cudaStream_t st) {
+                            int64_t ostride, double* Y, int64_t ldY, double* taus, int cmax, cudaStream_t st,
+                            int64_t rb, int64_t bstride) {
   if (k1 < 1 || k1 > 64) {
     az_set_error("tsqr_la: k1 = %d not in [1, 64]", k1);
     return AZ_ERR_NOT_SUPPORTED;
@@ -426,10 +442,12 @@ az_status_t az_tsqr_la_leaf(const double* A, int64_t m, int k1, int64_t ld, int6
   q.Rout = Rout;
   q.ostride = ostride;
   q.taus = taus;
-  const size_t sm = az_tsqr_la_smem();
-  auto kern = az_tsqr_la_mc() == 128 ? k_tsqr_la<128> : k_tsqr_la<256>;
+  q.rb = rb;
+  q.bstride = bstride;
+  const size_t sm = bstride ? (size_t)LASmem<256>::END * sizeof(double) : az_tsqr_la_smem();
+  auto kern = bstride ? k_tsqr_la<256, true> : (az_tsqr_la_mc() == 128 ? k_tsqr_la<128, false> : k_tsqr_la<256, false>);
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
-  AzTrace tr("tsqr_leaf", st, m);
+  AzTrace tr(bstride ? "tsqr_merge" : "tsqr_leaf", st, m);
   kern<<<P, 32 * LA_NW, sm, st>>>(q);
   AZ_LAUNCH_CHECK();
   return AZ_OK;
