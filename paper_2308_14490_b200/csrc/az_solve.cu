@@ -199,15 +199,16 @@ static bool qr_defer() {
 
 // AZ_SOLVE_HI=0: the QR and the SVD stay on the caller's stream while the side stream runs
 // AZ_SIDE2: 2 (default) the Z* b column pass on a second side stream right after the TSQR leaf, beside
-// the M pass and the merges; 1: on that stream after pass B; 0: on the side stream before the M pass
-// (the former order).  Measured c2 ms per step (two 20-step runs each): 2: 9.21 / 9.22, 1: 9.30 / 9.30,
-// 0: 9.28 / 9.33.
+// the M pass and the merges; 1: on that stream after pass B; 3: the M pass on it too (the side stream
+// then starts pass B at once); 0: on the side stream before the M pass (the former order).  Measured
+// c2 ms per step (two 20-step runs each): 2: 9.21 / 9.22, 1: 9.30 / 9.30, 0: 9.28 / 9.33; later, with
+// the look-ahead merges: 2: 9.02 / 8.96, 3: 9.04 / 9.01.
 static int side2_mode() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("AZ_SIDE2");
     v = e ? atoi(e) : 2;
-    if (v < 0 || v > 2) v = 2;
+    if (v < 0 || v > 3) v = 2;
   }
   return v;
 }
@@ -491,12 +492,14 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
         // first), then -- deferred -- Q^T b' through the kept reflectors beside the SVD
         AZ_CUDA_CHECK(cudaStreamWaitEvent(p->side, p->side_ev[0], 0));
         if (!use_side2) AZ_TRY(az1f_out_z(p, w.Zs, w.Zb, p->N, nrhs, p->side));
-        AZ_TRY(az1f_out_z(p, p->d_Z2, w.Om, p->N, R, p->side));
+        if (!(use_side2 && s2mode == 3)) AZ_TRY(az1f_out_z(p, p->d_Z2, w.Om, p->N, R, p->side));
         // Z* b on a second side stream: after pass B (mode 1; it then runs beside the right-hand-side
         // merge passes and the SVD, which leave most SMs idle) or right after the leaf (mode 2)
-        if (use_side2 && s2mode == 2) {
+        if (use_side2 && s2mode >= 2) {
           AZ_CUDA_CHECK(cudaStreamWaitEvent(p->side2, p->side_ev[0], 0));
           AZ_TRY(az1f_out_z(p, w.Zs, w.Zb, p->N, nrhs, p->side2));
+          // mode 3: the M pass too, so the side stream starts pass B right after the leaf
+          if (s2mode == 3) AZ_TRY(az1f_out_z(p, p->d_Z2, w.Om, p->N, R, p->side2));
         }
         if (defer)
           AZ_TRY(az_qr_rhs_deferred(w.S, rows, kt, kp, rows, w.cq, kp, w.qrws, w.qrbytes, p->side, p->side_ev[0],
