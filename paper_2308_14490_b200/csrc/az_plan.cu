@@ -79,10 +79,17 @@ extern "C" int az_trace_report(char* buf, int len) {
     double ms = 0.0;
   };
   std::map<std::string, Agg> agg;
+  // diagnostics: per-launch start / end (printed by the filling call only, not by the size query)
+  const bool timeline = buf && getenv("AZ_TRACE_TIMELINE") != nullptr;
   for (size_t i = 0; i < g_tr_used; ++i) {
     cudaEventSynchronize(g_tr[i].e1);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, g_tr[i].e0, g_tr[i].e1);
+    if (timeline) {
+      float t0 = 0.f;
+      cudaEventElapsedTime(&t0, g_tr[0].e0, g_tr[i].e0);
+      fprintf(stderr, "timeline %-24s %9.3f %9.3f\n", g_tr[i].name.c_str(), t0, t0 + ms);
+    }
     auto& a = agg[g_tr[i].name];
     a.count += 1;
     a.ms += ms;
