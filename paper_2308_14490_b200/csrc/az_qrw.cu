@@ -27,6 +27,7 @@ namespace cg = cooperative_groups;
 
 constexpr int QB = 64;            // panel width
 constexpr int QB0 = 8;            // base panel width of the recursive panel factorisation
+static_assert(QB0 <= 16 && QB >= 64, "k_qr_panel packs 2 x 16 partial slots per column parity into QB");
 constexpr int PANEL_THREADS = 512;
 
 AZ_D double qr_warp_sum(double v) {
@@ -63,25 +64,35 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) k_qr_panel(PanelArgs a) {
     double* col = a.A + jc * a.lda;
     const int64_t rlo = max(rb, jc + 1);
     const bool owner = jc >= rb && jc < re;
-    // ---- phase A: ||x(jc+1:m)||^2 partial ----
-    double s = 0.0;
-    for (int64_t r = rlo + tid; r < re; r += PANEL_THREADS) s = fma(col[r], col[r], s);
-    s = qr_warp_sum(s);
-    if (lane == 0) red[w] = s;
-    __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-      for (int i = 0; i < NW; ++i) t += red[i];
-      R1[c] = t;
+    // ---- phase A: ONE reduction per column (one grid barrier instead of two): slot l of the
+    // partials is the dot of the UNSCALED column j with column l over rows > jc (slot j: ||x||^2),
+    // slot 16 + l is row jc of column l (only its owner contributes, so the sum is exact).  Then
+    // d_l = v_j^T A[:, l] (v_j[jc] = 1) = A[jc, l] + scale * dot_l.  The partials are double-buffered
+    // by column parity: a CTA one column step ahead writes the other buffer ----
+    double* P2 = R2 + (j & 1) * 32;
+    for (int l = w; l < a.nb; l += NW) {
+      const double* cl = a.A + (a.j0 + l) * a.lda;
+      double d = 0.0;
+      for (int64_t r = rlo + lane; r < re; r += 32) d = fma(col[r], cl[r], d);
+      d = qr_warp_sum(d);
+      if (lane == 0) {
+        P2[(int64_t)c * QB + l] = d;
+        P2[(int64_t)c * QB + 16 + l] = owner ? cl[jc] : 0.0;
+      }
     }
     grid.sync();
-    // ---- phase B: reflector (every CTA computes the same numbers in the same order) ----
-    if (w == 0) {
-      // fixed-order cross-CTA sum: lane-strided partials, then a fixed shuffle tree
-      double sig = 0.0;
-      for (int i = lane; i < G; i += 32) sig += R1[i];
-      sig = qr_warp_sum(sig);
-      const double alpha = col[jc];
+    // ---- phase B: fixed-order cross-CTA sums (every CTA the same numbers in the same order) ----
+    for (int l = w; l < 2 * a.nb; l += NW) {   // one warp per slot, lanes over the CTAs' partials
+      const int sl = l < a.nb ? l : 16 + (l - a.nb);
+      double t = 0.0;
+      for (int i = lane; i < G; i += 32) t += P2[(int64_t)i * QB + sl];
+      t = qr_warp_sum(t);
+      if (lane == 0) dsum[sl] = t;   // (dsum has QB slots)
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const double sig = dsum[j];
+      const double alpha = dsum[16 + j];
       double beta = alpha, tau = 0.0, scale = 0.0;
       if (sig > 0.0) {
         const double nrm = sqrt(fma(alpha, alpha, sig));
@@ -89,36 +100,16 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) k_qr_panel(PanelArgs a) {
         tau = (beta - alpha) / beta;
         scale = 1.0 / (alpha - beta);
       }
-      if (lane == 0) {
-        sc[0] = beta;
-        sc[1] = tau;
-        sc[2] = scale;
-      }
+      sc[0] = beta;
+      sc[1] = tau;
+      sc[2] = scale;
     }
     __syncthreads();
-    const double scale = sc[2];
+    const double scale = sc[2], tau = sc[1];
+    if (tid < a.nb && tid != j) dsum[tid] = fma(scale, dsum[tid], dsum[16 + tid]);   // d_l
+    __syncthreads();
     for (int64_t r = rlo + tid; r < re; r += PANEL_THREADS) col[r] *= scale;
-    __syncthreads();
-    // ---- phase C: d_l = v_j^T A[:, l] over rows >= jc (v_j[jc] = 1), every panel column l != j ----
-    for (int l = w; l < a.nb; l += NW) {
-      if (l == j) continue;
-      const double* cl = a.A + (a.j0 + l) * a.lda;
-      double d = 0.0;
-      for (int64_t r = rlo + lane; r < re; r += 32) d = fma(col[r], cl[r], d);
-      d = qr_warp_sum(d);
-      if (lane == 0) R2[(int64_t)c * QB + l] = d + (owner ? cl[jc] : 0.0);
-    }
-    grid.sync();
     // ---- phase D: apply H_j to the remaining panel columns; extend T ----
-    const double tau = sc[1];
-    for (int l = w; l < a.nb; l += NW) {   // one warp per column, lanes over the CTAs' partials
-      double t = 0.0;
-      if (l != j)
-        for (int i = lane; i < G; i += 32) t += R2[(int64_t)i * QB + l];
-      t = qr_warp_sum(t);
-      if (lane == 0) dsum[l] = t;
-    }
-    __syncthreads();
     if (tau != 0.0) {
       const int64_t nr = re - rlo;
       const int ncl = a.nb - j - 1;

@@ -186,7 +186,6 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
         if (tid == 0) rot_any = 0;
         __syncthreads();
         for (int rd = 0; rd < PW - 1; ++rd) {
-          if (dbg && rd == 5 && sw == 0) a.dbg[0] = clock64();
           int p, q;
           pair_of(rd, pk, PW, p, q);
           const double gp = G[p * GS + p], gq = G[q * GS + q], g = G[p * GS + q];
@@ -195,9 +194,12 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
           const bool rot_pq = g != 0.0 && g2 > tol2 * gp * gq && fmin(gp, gq) >= negl;
           if (rot_pq) {
             // t = tan = 2 g sign(d) / (|d| + sqrt(d^2 + 4 g^2)), d = G_qq - G_pp
+            // (MUFU-seeded reciprocal / rsqrt with Newton steps, as in az_svd.cu: the IEEE division and
+            // square root dominated this latency-bound chain -- one inner sweep cost ~0.2 ms per round)
             const double d = gq - gp;
-            const double t = (d >= 0.0 ? 2.0 * g : -2.0 * g) / (fabs(d) + sqrt(fma(d, d, 4.0 * g2)));
-            c = rsqrt(fma(t, t, 1.0));
+            const double h = fma(d, d, 4.0 * g2);
+            const double t = (d >= 0.0 ? 2.0 * g : -2.0 * g) * fast_rcp(fabs(d) + h * fast_rsqrt(h));
+            c = fast_rsqrt(fma(t, t, 1.0));
             sn = c * t;
             if (sub == 0) rot_any = 1;
           }
@@ -429,7 +431,16 @@ __global__ void k_bjac_load(const double* Rf, int64_t ldr, int64_t r, int nrhs, 
 static size_t a256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 static int g_last_sweeps = 0;
-static const int g_inner_sweeps = 1;
+// inner cyclic sweeps of the pair's 64 x 64 Gram eigensolver per round (AZ_BJAC_INNER, default 1)
+static int inner_sweeps() {
+  static int v = 0;
+  if (!v) {
+    const char* e = getenv("AZ_BJAC_INNER");
+    v = e ? atoi(e) : 1;
+    if (v < 1 || v > 16) v = 1;
+  }
+  return v;
+}
 int az_bjac_sweeps_last() { return g_last_sweeps; }   // outer sweeps of the last block-Jacobi SVD
 
 // QR preconditioning (Drmac & Veselic): R_S^T = Q2 R2, R2^T = Q3 R3, so R_S = Q3 R3 Q2^T and
@@ -567,7 +578,7 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
   a.theta = theta;
   a.off = off;
   a.tol = 4.0 * 1.1102230246251565e-16 * std::sqrt((double)r);
-  a.inner_sweeps = g_inner_sweeps;
+  a.inner_sweeps = inner_sweeps();
   a.dbg = nullptr;
   static long long* d_dbg = nullptr;
   const bool want_dbg = getenv("AZ_DEBUG_JACOBI") != nullptr;
@@ -609,8 +620,10 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
     if (want_dbg) {
       long long h[8];
       cudaMemcpy(h, d_dbg, sizeof(h), cudaMemcpyDeviceToHost);
-      fprintf(stderr, "bjac r=%lld CS=%d sweep %d off %.3e tol %.3e | last round clocks: eig %lld wait2 %lld | inner round: param %lld sync1 %lld\n",
-              (long long)r, CS, sw, offd, a.tol, h[3] - h[2], h[4] - h[3], h[6] - h[0], h[7] - h[6]);
+      fprintf(stderr, "bjac r=%lld CS=%d sweep %d off %.3e tol %.3e | last round clocks (cluster 0 leader): gram %lld "
+              "csync %lld eig %lld vsync %lld update %lld | inner round sync1 %lld\n",
+              (long long)r, CS, sw, offd, a.tol, h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4],
+              h[7] - h[6]);
     }
     if (offd <= 4.0 * a.tol) {   // rounding level of the measured off-diagonals
       ++sw;
