@@ -455,6 +455,15 @@ static bool bjac_precond() {
   return v == 1;
 }
 
+static int64_t precond_min() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("AZ_BJAC_PRECOND_MIN");
+    v = e ? atoll(e) : 2500;   // measured: c4 876 -> 829 ms, c3 4.03 -> 3.97 s against 0 (always)
+  }
+  return v;
+}
+
 static size_t tsvdw_pre_bytes(int64_t r, int64_t nrhs) {
   if (!bjac_precond()) return 0;
   const int64_t QBw = az_qrw_panel_width();
@@ -502,7 +511,9 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
   int64_t* d_rank = (int64_t*)(p + 128);
   if (rank_dev) *rank_dev = d_rank;
   // ---- optional QR preconditioning ----
-  const bool pre = bjac_precond();
+  // (small sketches -- the R22 pre-tests of the probe blocks -- converge in a few more cheap sweeps
+  // than the two preconditioning QRs cost: AZ_BJAC_PRECOND_MIN, the smallest r preconditioned)
+  const bool pre = bjac_precond() && r >= precond_min();
   double *M2 = nullptr, *M3 = nullptr, *T2 = nullptr, *T3 = nullptr, *Z = nullptr;
   void* qws = nullptr;
   size_t qbytes = 0;
