@@ -7,8 +7,8 @@
 // ||(alpha, x)||, tau = (beta - alpha) / beta, y = x / (alpha - beta)), and leaves y_j in place of
 // column j and tau_j in taus for pass B (k_tsqr_rhs).  Only the ORDER of the work differs: the
 // columns are taken in panels of 8, and per panel
-//   * four panel warps (on two SM sub-partitions, 64 rows each, the panel in registers) factorise it column
-//     by column -- one 128-thread named barrier per column: the column's norm and its dot products with
+//   * two panel warps (on SM sub-partitions 0 and 1, 128 rows each, the panel in registers; AZ_TSQR_LA_NP=4:
+//     four, 64 rows each) factorise it column by column -- one 128-thread named barrier per column: the column's norm and its dot products with
 //     the panel's other columns are reduced together, the dots taken with the unscaled column and scaled
 //     by 1 / (alpha - beta) afterwards -- and form its T (dlarft: H_0 .. H_7 = I - V T V^T);
 //   * all eight warps then apply it to the NEXT panel's columns (the look-ahead tile) in compact-WY
@@ -29,15 +29,16 @@
 namespace {
 constexpr int LA_LDR = 65;            // R column stride
 constexpr int LA_PW = 8;              // panel width
-constexpr int LA_NW = 8;              // warps: 0..3 factorise panels, 4..7 update
-constexpr int LA_NP = 4;              // panel warps
-constexpr int LA_NU = LA_NW - LA_NP;  // update warps
+constexpr int LA_NW = 8;              // warps
+constexpr int LA_NU = 4;              // update warps (2, 3, 6, 7: sub-partitions 2 and 3)
 // Chunk shape: MC rows per chunk (256: one 175 KB CTA per SM; 128: two 110 KB CTAs per SM, whose
 // panel chains interleave), X column stride MC + 4 (== 4 mod 16: conflict-free DMMA fragments)
-template <int MC>
+// NP panel warps: 4 (0, 1, 4, 5: two per sub-partition 0 and 1) or 2 (0 and 1: one per sub-partition,
+// twice the rows each; warps 4 and 5 then only join the look-ahead W and the CTA barriers)
+template <int MC, int NP = 4>
 struct LAShape {
   static constexpr int LDX = MC + 4;
-  static constexpr int PR = MC / 4;          // rows of a panel warp
+  static constexpr int PR = MC / NP;         // rows of a panel warp
   static constexpr int RPW = PR / 32;        // rows per lane in a panel warp
   static constexpr int MINB = MC == 256 ? 1 : 2;
 };
@@ -127,10 +128,11 @@ AZ_D void tile_w(double (&acc)[2], const double* X, int j0, int c0, int k1, int 
 // FULLW = 8: a full panel (every column test resolved at compile time); 0: a last, narrower panel.
 // Warp 0 writes R's panel rows, warp 1 forms T (lane a owns row a), warp 2 stores the taus, so that
 // no warp carries all the side work between the two barriers of a column.
-template <int MC, int FULLW>
+template <int MC, int NP, int FULLW>
 AZ_D void la_panel(double* X, double* R, double* sm, double* Tm, const LAIn& q, int chunk, int j0, int k1, int w,
                    int lane) {
-  constexpr int LDX = LAShape<MC>::LDX, RPW = LAShape<MC>::RPW, PR = LAShape<MC>::PR;
+  constexpr int LDX = LAShape<MC, NP>::LDX, RPW = LAShape<MC, NP>::RPW, PR = LAShape<MC, NP>::PR;
+  constexpr int TAU_W = NP > 2 ? 2 : 0, TAU_L = NP > 2 ? 0 : 1;   // who stores the taus
   const int PWN = FULLW ? FULLW : min(LA_PW, k1 - j0);
   double* red2 = sm + LASmem<MC>::RED2;
   double x[LA_PW][RPW];   // column j0 + c, row PR w + lane + 32 i
@@ -175,13 +177,17 @@ AZ_D void la_panel(double* X, double* R, double* sm, double* Tm, const LAIn& q, 
     ds += __shfl_xor_sync(0xffffffffu, ds, 2);
     ds += __shfl_xor_sync(0xffffffffu, ds, 1);
     double* rb = red2 + (c & 1) * 32;   // (double-buffered: one barrier per column)
-    if ((lane & 3) == 0) rb[(lane >> 2) * 4 + w] = ds;
-    bar_sync(BAR_P, 32 * LA_NP);
+    if ((lane & 3) == 0) rb[(lane >> 2) * NP + w] = ds;
+    bar_sync(BAR_P, 32 * NP);
 #pragma unroll
     for (int l = 0; l < LA_PW; ++l) {
-      const double2 u = *reinterpret_cast<const double2*>(rb + l * 4);
-      const double2 v = *reinterpret_cast<const double2*>(rb + l * 4 + 2);
-      d[l] = (u.x + u.y) + (v.x + v.y);
+      const double2 u = *reinterpret_cast<const double2*>(rb + l * NP);
+      if constexpr (NP == 4) {
+        const double2 v = *reinterpret_cast<const double2*>(rb + l * 4 + 2);
+        d[l] = (u.x + u.y) + (v.x + v.y);
+      } else {
+        d[l] = u.x + u.y;
+      }
     }
     const double sig = d[c];
     double tau = 0.0, scale = 0.0, beta = alpha;
@@ -198,7 +204,7 @@ AZ_D void la_panel(double* X, double* R, double* sm, double* Tm, const LAIn& q, 
 #pragma unroll
     for (int l = 0; l < LA_PW; ++l) d[l] *= scale;       // y_c . x_l (l > c), y_c . y_l (l < c)
     if (w == 0 && lane == 0) R[jc * LA_LDR + jc] = beta;
-    if (w == 2 && lane == 0) q.taus[((int64_t)blockIdx.x * q.cmax + chunk) * k1 + jc] = tau;
+    if (w == TAU_W && lane == TAU_L) q.taus[((int64_t)blockIdx.x * q.cmax + chunk) * k1 + jc] = tau;
     if (w == 1) {
       // T[a][c] = -tau_c sum_{a <= m < c} T[a][m] (y_m . y_c), T[c][c] = tau_c (lane a owns row a)
       double t = 0.0;
@@ -230,9 +236,9 @@ AZ_D void la_panel(double* X, double* R, double* sm, double* Tm, const LAIn& q, 
     for (int m = 0; m < LA_PW; ++m) Tm[lane * 8 + m] = trow[m];
 }
 
-template <int MC, bool STACK>
-__global__ void __launch_bounds__(32 * LA_NW, LAShape<MC>::MINB) k_tsqr_la(LAIn q) {
-  constexpr int LDX = LAShape<MC>::LDX;
+template <int MC, bool STACK, int NP = 4>
+__global__ void __launch_bounds__(32 * LA_NW, LAShape<MC, NP>::MINB) k_tsqr_la(LAIn q) {
+  constexpr int LDX = LAShape<MC, NP>::LDX;
   using SM = LASmem<MC>;
   extern __shared__ double sm[];
   double* X = sm + SM::X;
@@ -245,7 +251,8 @@ __global__ void __launch_bounds__(32 * LA_NW, LAShape<MC>::MINB) k_tsqr_la(LAIn 
   // the update warps 2, 3, 6, 7, so the panel chain never queues behind the updates' DMMA on its FP64
   // pipe (measured: with the panel and update warps paired on every sub-partition the leaf took 19 %
   // longer than the chain alone)
-  const bool panel_w = (w & 2) == 0;
+  const bool panel_w = NP == 4 ? (w & 2) == 0 : w < 2;
+  const bool upd_w = (w & 2) != 0;
   const int gi = (w & 1) | ((w >> 2) << 1);   // index within the warp's group (0..3)
   for (int e = tid; e < 64 * LA_LDR; e += 32 * LA_NW) R[e] = 0.0;
   // column slots past k1 are read as (zero) columns of a last, narrower panel or tile
@@ -296,10 +303,10 @@ __global__ void __launch_bounds__(32 * LA_NW, LAShape<MC>::MINB) k_tsqr_la(LAIn 
       if (panel_w) {
         // ================= panel p, panel warp gi: rows 64 gi .. 64 gi + 63 =================
         if (pw == LA_PW)
-          la_panel<MC, LA_PW>(X, R, sm, Tm, q, chunk, j0, k1, gi, lane);
+          la_panel<MC, NP, LA_PW>(X, R, sm, Tm, q, chunk, j0, k1, gi, lane);
         else
-          la_panel<MC, 0>(X, R, sm, Tm, q, chunk, j0, k1, gi, lane);
-      } else if (p > 0) {
+          la_panel<MC, NP, 0>(X, R, sm, Tm, q, chunk, j0, k1, gi, lane);
+      } else if (upd_w && p > 0) {
         // ========= update warps: panel p - 1 on the columns right of panel p (tiles p + 1 ..) =========
         const int uw = gi, pj0 = j0 - LA_PW;
         const double* Tp = sm + SM::T + ((p - 1) & 1) * 64;
@@ -365,16 +372,16 @@ __global__ void __launch_bounds__(32 * LA_NW, LAShape<MC>::MINB) k_tsqr_la(LAIn 
           }
         }
         if (panel_w) {
-          bar_sync(BAR_P, 32 * LA_NP);
-          tile_rank_update<LDX>(X, WL, j0, c0, k1, (MC / 32) * gi, (MC / 32) * (gi + 1), lane);
-        } else if (p > 0) {
+          bar_sync(BAR_P, 32 * NP);
+          tile_rank_update<LDX>(X, WL, j0, c0, k1, (MC / NP / 8) * gi, (MC / NP / 8) * (gi + 1), lane);
+        } else if (upd_w && p > 0) {
           writeback(p - 1, base, nbase);
         }
-      } else if (!panel_w && p > 0) {
+      } else if (upd_w && p > 0) {
         writeback(p - 1, base, nbase);
       }
     }
-    if (!panel_w) {
+    if (upd_w) {
       writeback(np - 1, base, nbase);   // (the last panel has no columns right of the look-ahead)
       asm volatile("cp.async.wait_all;\n" ::: "memory");
     }
@@ -388,6 +395,18 @@ __global__ void __launch_bounds__(32 * LA_NW, LAShape<MC>::MINB) k_tsqr_la(LAIn 
   }
 }
 }  // namespace
+
+// AZ_TSQR_LA_NP: 2 (default) panel warps, one per sub-partition 0 and 1 with 128 rows each, or 4 (two
+// per sub-partition, 64 rows each).  The chain is partly issue-bound on its sub-partitions: measured
+// pass A 1.431 ms (4) against 1.364 ms (2) on c2.
+static int la_np() {
+  static int v = 0;
+  if (!v) {
+    const char* e = getenv("AZ_TSQR_LA_NP");
+    v = (e && atoi(e) == 4) ? 4 : 2;
+  }
+  return v;
+}
 
 // AZ_TSQR_LA_MC=128: 128-row chunks, two CTAs per SM (default 256: one CTA per SM)
 int az_tsqr_la_mc() {
@@ -445,7 +464,9 @@ az_status_t az_tsqr_la_leaf(const double* A, int64_t m, int k1, int64_t ld, int6
   q.rb = rb;
   q.bstride = bstride;
   const size_t sm = bstride ? (size_t)LASmem<256>::END * sizeof(double) : az_tsqr_la_smem();
-  auto kern = bstride ? k_tsqr_la<256, true> : (az_tsqr_la_mc() == 128 ? k_tsqr_la<128, false> : k_tsqr_la<256, false>);
+  auto kern = bstride ? k_tsqr_la<256, true>
+                      : (az_tsqr_la_mc() == 128 ? k_tsqr_la<128, false>
+                                                : (la_np() == 2 ? k_tsqr_la<256, false, 2> : k_tsqr_la<256, false>));
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   AzTrace tr(bstride ? "tsqr_merge" : "tsqr_leaf", st, m);
   kern<<<P, 32 * LA_NW, sm, st>>>(q);
