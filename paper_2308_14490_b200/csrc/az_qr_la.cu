@@ -133,6 +133,7 @@ AZ_D void la_panel(double* X, double* R, double* sm, double* Tm, const LAIn& q, 
                    int lane) {
   constexpr int LDX = LAShape<MC, NP>::LDX, RPW = LAShape<MC, NP>::RPW, PR = LAShape<MC, NP>::PR;
   constexpr int TAU_W = NP > 2 ? 2 : 0, TAU_L = NP > 2 ? 0 : 1;   // who stores the taus
+  constexpr int T_W = NP > 1 ? 1 : 0;                              // who forms T
   const int PWN = FULLW ? FULLW : min(LA_PW, k1 - j0);
   double* red2 = sm + LASmem<MC>::RED2;
   double x[LA_PW][RPW];   // column j0 + c, row PR w + lane + 32 i
@@ -176,17 +177,22 @@ AZ_D void la_panel(double* X, double* R, double* sm, double* Tm, const LAIn& q, 
     double ds = d[0];
     ds += __shfl_xor_sync(0xffffffffu, ds, 2);
     ds += __shfl_xor_sync(0xffffffffu, ds, 1);
-    double* rb = red2 + (c & 1) * 32;   // (double-buffered: one barrier per column)
-    if ((lane & 3) == 0) rb[(lane >> 2) * NP + w] = ds;
-    bar_sync(BAR_P, 32 * NP);
+    if constexpr (NP == 1) {   // one panel warp: the slot sums are broadcast, no barrier
 #pragma unroll
-    for (int l = 0; l < LA_PW; ++l) {
-      const double2 u = *reinterpret_cast<const double2*>(rb + l * NP);
-      if constexpr (NP == 4) {
-        const double2 v = *reinterpret_cast<const double2*>(rb + l * 4 + 2);
-        d[l] = (u.x + u.y) + (v.x + v.y);
-      } else {
-        d[l] = u.x + u.y;
+      for (int l = 0; l < LA_PW; ++l) d[l] = __shfl_sync(0xffffffffu, ds, 4 * l);
+    } else {
+      double* rb = red2 + (c & 1) * 32;   // (double-buffered: one barrier per column)
+      if ((lane & 3) == 0) rb[(lane >> 2) * NP + w] = ds;
+      bar_sync(BAR_P, 32 * NP);
+#pragma unroll
+      for (int l = 0; l < LA_PW; ++l) {
+        const double2 u = *reinterpret_cast<const double2*>(rb + l * NP);
+        if constexpr (NP == 4) {
+          const double2 v = *reinterpret_cast<const double2*>(rb + l * 4 + 2);
+          d[l] = (u.x + u.y) + (v.x + v.y);
+        } else {
+          d[l] = u.x + u.y;
+        }
       }
     }
     const double sig = d[c];
@@ -205,7 +211,7 @@ AZ_D void la_panel(double* X, double* R, double* sm, double* Tm, const LAIn& q, 
     for (int l = 0; l < LA_PW; ++l) d[l] *= scale;       // y_c . x_l (l > c), y_c . y_l (l < c)
     if (w == 0 && lane == 0) R[jc * LA_LDR + jc] = beta;
     if (w == TAU_W && lane == TAU_L) q.taus[((int64_t)blockIdx.x * q.cmax + chunk) * k1 + jc] = tau;
-    if (w == 1) {
+    if (w == T_W) {
       // T[a][c] = -tau_c sum_{a <= m < c} T[a][m] (y_m . y_c), T[c][c] = tau_c (lane a owns row a)
       double t = 0.0;
 #pragma unroll
@@ -231,7 +237,7 @@ AZ_D void la_panel(double* X, double* R, double* sm, double* Tm, const LAIn& q, 
 #pragma unroll
     for (int i = 0; i < RPW; ++i)
       if (c < PWN) X[(j0 + c) * LDX + PR * w + lane + 32 * i] = x[c][i];
-  if (w == 1 && lane < LA_PW)
+  if (w == T_W && lane < LA_PW)
 #pragma unroll
     for (int m = 0; m < LA_PW; ++m) Tm[lane * 8 + m] = trow[m];
 }
@@ -251,7 +257,7 @@ __global__ void __launch_bounds__(32 * LA_NW, LAShape<MC, NP>::MINB) k_tsqr_la(L
   // the update warps 2, 3, 6, 7, so the panel chain never queues behind the updates' DMMA on its FP64
   // pipe (measured: with the panel and update warps paired on every sub-partition the leaf took 19 %
   // longer than the chain alone)
-  const bool panel_w = NP == 4 ? (w & 2) == 0 : w < 2;
+  const bool panel_w = NP == 4 ? (w & 2) == 0 : w < NP;
   const bool upd_w = (w & 2) != 0;
   const int gi = (w & 1) | ((w >> 2) << 1);   // index within the warp's group (0..3)
   for (int e = tid; e < 64 * LA_LDR; e += 32 * LA_NW) R[e] = 0.0;
@@ -403,7 +409,8 @@ static int la_np() {
   static int v = 0;
   if (!v) {
     const char* e = getenv("AZ_TSQR_LA_NP");
-    v = (e && atoi(e) == 4) ? 4 : 2;
+    v = e ? atoi(e) : 2;
+    if (v != 1 && v != 4) v = 2;
   }
   return v;
 }
@@ -464,9 +471,11 @@ az_status_t az_tsqr_la_leaf(const double* A, int64_t m, int k1, int64_t ld, int6
   q.rb = rb;
   q.bstride = bstride;
   const size_t sm = bstride ? (size_t)LASmem<256>::END * sizeof(double) : az_tsqr_la_smem();
-  auto kern = bstride ? k_tsqr_la<256, true>
+  auto kern = bstride ? (la_np() == 4 ? k_tsqr_la<256, true> : k_tsqr_la<256, true, 2>)
                       : (az_tsqr_la_mc() == 128 ? k_tsqr_la<128, false>
-                                                : (la_np() == 2 ? k_tsqr_la<256, false, 2> : k_tsqr_la<256, false>));
+                                                : (la_np() == 2   ? k_tsqr_la<256, false, 2>
+                                                   : la_np() == 1 ? k_tsqr_la<256, false, 1>
+                                                                  : k_tsqr_la<256, false>));
   AZ_CUDA_CHECK(az_smem_attr(kern, sm));
   AzTrace tr(bstride ? "tsqr_merge" : "tsqr_leaf", st, m);
   kern<<<P, 32 * LA_NW, sm, st>>>(q);
