@@ -198,6 +198,16 @@ static bool qr_defer() {
 }
 
 // AZ_SOLVE_HI=0: the QR and the SVD stay on the caller's stream while the side stream runs
+// AZ_SIDE_PRIO=0: the side stream at default priority (like the second side stream)
+static bool side_prio_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AZ_SIDE_PRIO");
+    v = (e && *e == '0') ? 0 : 1;
+  }
+  return v != 0;
+}
+
 // AZ_SIDE2: 2 (default) the Z* b column pass on a second side stream right after the TSQR leaf, beside
 // the M pass and the merges; 1: on that stream after pass B; 3: the M pass on it too (the side stream
 // then starts pass B at once); 0: on the side stream before the M pass (the former order).  Measured
@@ -424,10 +434,13 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
   // chain they run on a side stream beside the TSQR merges and the SVD (which leave most SMs idle)
   const bool side = w.Zb && max_blocks == 1 && (nrhs + 1) / 2 <= p->Bmax && (R + 1) / 2 <= p->Bmax;
   if (side && !p->side) {
-    AZ_CUDA_CHECK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
-    for (auto& e : p->side_ev) AZ_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     int lo = 0, top = 0;
     AZ_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &top));
+    // priorities: the QR / SVD stream (hi) first, then the side stream (pass B and the merge-level passes,
+    // whose few CTAs must not queue behind the second side stream's column pass), then side2
+    const int side_prio = (side_prio_on() && top < lo) ? std::min(lo, top + 1) : lo;
+    AZ_CUDA_CHECK(cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, side_prio));
+    for (auto& e : p->side_ev) AZ_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     AZ_CUDA_CHECK(cudaStreamCreateWithPriority(&p->hi, cudaStreamNonBlocking, top));
     AZ_CUDA_CHECK(cudaStreamCreateWithFlags(&p->side2, cudaStreamNonBlocking));
     for (auto& e : p->side2_ev) AZ_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
