@@ -525,7 +525,10 @@ def run_ours(args, cfg):
     # ---- roofline of the dominant kernel (live CUDA-event trace over the timed region) ----
     peaks, peak_src = measured_peaks()
     kcols = reps[-1]["probes"] + cfg.nrhs
-    dom = max(trace.items(), key=lambda kv: kv[1][1])
+    # (a "_bg" pass runs on the lowest-priority stream and yields SMs to the critical branches: its
+    # event-timed duration is not its cost, so it is neither the dominant kernel nor in the pass roofline)
+    fg = {k: v for k, v in trace.items() if not k.endswith("_bg")}
+    dom = max(fg.items(), key=lambda kv: kv[1][1])
     name, (cnt, tot_ms, units) = dom
     # the four-step narrow solve takes Z* b and M = Omega - Z* A Omega from its chains (az_solve.cu step2_linear)
     kept = (cfg.dim == 1 and cfg.N * cfg.s > 2048 and kcols <= 128
@@ -556,7 +559,7 @@ def run_ours(args, cfg):
     roof["traffic"] = traffic
     # aggregate HBM roofline of the FFT operator passes (SURVEY.md §8(d) pass model)
     fb, ft = 0.0, 0.0
-    for k, (c_, t_, u_) in trace.items():
+    for k, (c_, t_, u_) in fg.items():
         bnd, pu = kernel_model(k, cfg, plan.M, kcols, kept=kept)
         if bnd == "hbm":
             fb += pu * u_
@@ -566,7 +569,8 @@ def run_ours(args, cfg):
         ach = fb / (ft * 1e-3) / 1e9
         roof_fft = {"kernels": "all FFT operator passes", "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
                     "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "share_of_step": ft / sum(ms),
-                    "bytes_per_step": fb / args.steps, "peak_source": peak_src}
+                    "bytes_per_step": fb / args.steps, "peak_source": peak_src,
+                    "background_excluded": sorted(k for k in trace if k.endswith("_bg"))}
     # per-kernel table (share of the step)
     kernels = {k: {"launches": v[0], "ms_per_step": v[1] / args.steps, "units": v[2]} for k, v in
                sorted(trace.items(), key=lambda kv: -kv[1][1])}

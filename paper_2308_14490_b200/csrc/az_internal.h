@@ -113,7 +113,8 @@ az_status_t az1f_resid_z(az_plan_s* p, const double* b, int64_t ldb, double* bp,
                          int64_t nvec, cudaStream_t st, cplx* Zspec = nullptr, bool defer = false);
 az_status_t az1f_sketch_m(az_plan_s* p, int64_t col0, int64_t ncols, double* S, int64_t ldS, double* Om, int64_t ldOm,
                           cudaStream_t st, cplx* Zspec = nullptr, bool defer = false);
-az_status_t az1f_out_z(az_plan_s* p, const cplx* Zspec, double* out, int64_t ldout, int64_t nvec, cudaStream_t st);
+az_status_t az1f_out_z(az_plan_s* p, const cplx* Zspec, double* out, int64_t ldout, int64_t nvec, cudaStream_t st,
+                       bool background = false);
 // Omega[:, col0 .. col0 + ncols) of a four-step plan's spectral probes (reading R35), N x ncols, ld ldOm
 az_status_t az1f_omega_fill(az_plan_s* p, int64_t col0, int64_t ncols, double* Om, int64_t ldOm, cudaStream_t st);
 

@@ -57,6 +57,7 @@ struct P1f {
   int64_t nvec, col0, pair0;
   int lead;              // spectral probes from an odd col0: the first pair's real column precedes the call
   double sqn;            // sqrt(n): scale of the spectral probes
+  const char* trace_name;   // trace label override (null: the pass kind's name)
 };
 
 // row of the fine grid point g (natural order), -1 outside Omega
@@ -700,7 +701,7 @@ static az_status_t fcols_e(const P1f& a, int ncols, int nb, double cout, cudaStr
   static const char* names[] = {"1f_cols_in_coef", "1f_cols_fine_mask", "1f_cols_out_gather", "1f_cols_out_resid",
                                 "1f_cols_in_rows", "1f_cols_out_coef", "1f_cols_fwd", "1f_cols_resid_mid",
                                 "1f_cols_out_coef_add", "1f_cols_out_z"};
-  AzTrace tr(names[KIND], st, nb);
+  AzTrace tr(a.trace_name ? a.trace_name : names[KIND], st, nb);
   kern<<<dim3(az_div_up(ncols, TC), nb), TC * T, sm, st>>>(a, cout);
   AZ_LAUNCH_CHECK();
   return AZ_OK;
@@ -776,7 +777,7 @@ static az_status_t fcols_p(const P1f& a, int ncols, int nb, double cout, cudaStr
   static const char* names[] = {"1f_cols_in_coef", "1f_cols_fine_mask", "1f_cols_out_gather", "1f_cols_out_resid",
                                 "1f_cols_in_rows", "1f_cols_out_coef", "1f_cols_fwd", "1f_cols_resid_mid",
                                 "1f_cols_out_coef_add", "1f_cols_out_z"};
-  AzTrace tr(names[KIND], st, nb);
+  AzTrace tr(a.trace_name ? a.trace_name : names[KIND], st, nb);
   kern<<<dim3(tiles, pg), C::NT, C::smem, st>>>(a, cout, m, nb, pg);
   AZ_LAUNCH_CHECK();
   *done = true;
@@ -952,6 +953,7 @@ static P1f make_p1f(az_plan_s* p) {
   a.nvec = a.col0 = a.pair0 = 0;
   a.lead = 0;
   a.sqn = sqrt((double)p->n);
+  a.trace_name = nullptr;
   return a;
 }
 
@@ -1102,8 +1104,12 @@ static az_status_t out_z_run(const P1f& a, int64_t npairs, cudaStream_t st) {
   return fcols<NC, FC_OUT_Z, SRC_VEC>(a, NR2, (int)npairs, 1.0 / (double)a.n, st);
 }
 
-az_status_t az1f_out_z(az_plan_s* p, const cplx* Zspec, double* out, int64_t ldout, int64_t nvec, cudaStream_t st) {
+az_status_t az1f_out_z(az_plan_s* p, const cplx* Zspec, double* out, int64_t ldout, int64_t nvec, cudaStream_t st,
+                       bool background) {
   P1f a = make_p1f(p);
+  // (a background pass on the lowest-priority stream yields SMs to the others: its event-timed
+  // duration is not its cost, so it is traced under its own label)
+  if (background) a.trace_name = "1f_cols_out_z_bg";
   a.Z2 = const_cast<cplx*>(Zspec);
   a.out2 = out;
   a.ldout2 = ldout;

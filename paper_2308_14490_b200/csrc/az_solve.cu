@@ -510,7 +510,7 @@ static az_status_t solve_impl(az_plan_s* p, const double* b, int64_t ldb, double
         // merge passes and the SVD, which leave most SMs idle) or right after the leaf (mode 2)
         if (use_side2 && s2mode >= 2) {
           AZ_CUDA_CHECK(cudaStreamWaitEvent(p->side2, p->side_ev[0], 0));
-          AZ_TRY(az1f_out_z(p, w.Zs, w.Zb, p->N, nrhs, p->side2));
+          AZ_TRY(az1f_out_z(p, w.Zs, w.Zb, p->N, nrhs, p->side2, side_prio_on()));
           // mode 3: the M pass too, so the side stream starts pass B right after the leaf
           if (s2mode == 3) AZ_TRY(az1f_out_z(p, p->d_Z2, w.Om, p->N, R, p->side2));
         }
