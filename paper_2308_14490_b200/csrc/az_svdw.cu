@@ -430,6 +430,34 @@ __global__ void k_bjac_load(const double* Rf, int64_t ldr, int64_t r, int nrhs, 
 
 static size_t a256(size_t v) { return (v + 255) & ~(size_t)255; }
 
+// dst[:, j] = src[:, perm[j]] (r x r, ld r)
+__global__ void k_bjac_permute(const double* src, double* dst, const int* perm, int64_t r) {
+  const int64_t j = blockIdx.x;
+  const int64_t pj = perm[j];
+  for (int64_t t = threadIdx.x; t < r; t += blockDim.x) dst[j * r + t] = src[pj * r + t];
+}
+
+// Cd[j][c] = Cs[perm[j]][c] (r x nrhs, ld r)
+__global__ void k_bjac_permute_rows(const double* Cs, double* Cd, const int* perm, int64_t r, int64_t nrhs) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= r * nrhs) return;
+  const int64_t j = e % r, c = e / r;
+  Cd[c * r + j] = Cs[c * r + perm[j]];
+}
+
+// At the start of every sweep the columns of B (and the rows of C) are permuted into decreasing norm
+// (de Rijk-style ordering at sweep level, a dynamic stand-in for Drmac & Veselic's column pivoting):
+// one outer sweep fewer on c3 / c4 (10 -> 9, 9 -> 8), c5 rounds 14.6 -> 13.2 s.  AZ_BJAC_SORT=0
+// keeps the fixed column order.
+static bool bjac_sort() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AZ_BJAC_SORT");
+    v = (e && *e == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static int g_last_sweeps = 0;
 // inner cyclic sweeps of the pair's 64 x 64 Gram eigensolver per round (AZ_BJAC_INNER, default 1)
 static int inner_sweeps() {
@@ -520,7 +548,7 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
   std::vector<int64_t> pj2, pj3;
   std::vector<int> pn2, pn3;
   int64_t np2 = 0, np3 = 0;
-  if (pre) {
+  if (bjac_precond()) {   // the workspace holds these buffers whenever preconditioning is enabled
     const int64_t QBw = az_qrw_panel_width();
     const int64_t npm = (r + QBw - 1) / QBw;
     char* q = p + 1024;
@@ -540,6 +568,8 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
     pj3.resize(npm);
     pn2.resize(npm);
     pn3.resize(npm);
+  }
+  if (pre) {
     AzTrace tr("bjac_precond", st, 2 * r * r * r);
     k_upper_T<<<az_div_up(r * r, 256), 256, 0, st>>>(Rf, ldr, r, M2);                 // R_S^T
     AZ_LAUNCH_CHECK();
@@ -598,6 +628,36 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
     a.dbg = d_dbg;
   }
   int sw = 0;
+  // sweep-level norm ordering: the permuted copies go to second buffers, the two of each pair swapping
+  // roles each sweep -- B's to M3 (free once B is loaded), C's to Z (unused without preconditioning)
+  // or to the preconditioning QR's workspace (free until the closing Q2 product, which follows the
+  // solve's last read of C); stream-ordered allocations only where the workspace has no such room
+  const bool sort_cols = bjac_sort() && r > PW;
+  const size_t cbytes = sizeof(double) * r * std::max<int64_t>(nrhs, 1);
+  double* Bsp = M3;
+  double* Bmal = nullptr;
+  double* Csp = pre ? (qbytes >= cbytes ? (double*)qws : nullptr) : Z;
+  double* Cmal = nullptr;
+  int* d_perm = (int*)T3;   // T3 (>= r QBw doubles) is read only by the Q3^T c product before the sweeps
+  int* pmal = nullptr;
+  std::vector<double> h_n2;
+  std::vector<int> h_perm;
+  if (sort_cols) {
+    if (!Bsp) {
+      AZ_CUDA_CHECK(cudaMallocAsync((void**)&Bmal, sizeof(double) * r * r, st));
+      Bsp = Bmal;
+    }
+    if (!Csp) {
+      AZ_CUDA_CHECK(cudaMallocAsync((void**)&Cmal, cbytes, st));
+      Csp = Cmal;
+    }
+    if (!d_perm) {
+      AZ_CUDA_CHECK(cudaMallocAsync((void**)&pmal, sizeof(int) * r, st));
+      d_perm = pmal;
+    }
+    h_n2.resize(r);
+    h_perm.resize(r);
+  }
   for (; sw < max_sweeps; ++sw) {
     {
       AzTrace tr("bjac_norms", st);
@@ -605,6 +665,25 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
       AZ_LAUNCH_CHECK();
       k_bjac_max<<<1, 1024, 0, st>>>(nrm2, r, smax2, off);
       AZ_LAUNCH_CHECK();
+    }
+    if (sort_cols) {
+      AzTrace tr("bjac_sort", st);
+      AZ_CUDA_CHECK(cudaMemcpyAsync(h_n2.data(), nrm2, sizeof(double) * r, cudaMemcpyDeviceToHost, st));
+      AZ_CUDA_CHECK(cudaStreamSynchronize(st));
+      for (int64_t i = 0; i < r; ++i) h_perm[i] = (int)i;
+      std::stable_sort(h_perm.begin(), h_perm.end(), [&](int x, int y) { return h_n2[x] > h_n2[y]; });
+      AZ_CUDA_CHECK(cudaMemcpyAsync(d_perm, h_perm.data(), sizeof(int) * r, cudaMemcpyHostToDevice, st));
+      k_bjac_permute<<<(unsigned)r, 256, 0, st>>>(B, Bsp, d_perm, r);
+      AZ_LAUNCH_CHECK();
+      if (nrhs > 0) {
+        k_bjac_permute_rows<<<az_div_up(r * nrhs, 256), 256, 0, st>>>(C, Csp, d_perm, r, nrhs);
+        AZ_LAUNCH_CHECK();
+      }
+      std::swap(B, Bsp);
+      std::swap(C, Csp);
+      a.B = B;
+      a.C = C;
+      AZ_CUDA_CHECK(cudaStreamSynchronize(st));   // h_perm is reused next sweep
     }
     for (int rd = 0; rd < n - 1; ++rd) {
       AzTrace tr("bjac_round", st, 16 * r * BW * BW * (n / 2));
@@ -661,6 +740,11 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
       AZ_LAUNCH_CHECK();
       AZ_TRY(az_qrw_apply_q(M2, r, r, pj2.data(), pn2.data(), T2, 0, np2, y, ldy, nrhs, qws, qbytes, st));
     }
+  }
+  if (sort_cols) {
+    if (Cmal) AZ_CUDA_CHECK(cudaFreeAsync(Cmal, st));
+    if (Bmal) AZ_CUDA_CHECK(cudaFreeAsync(Bmal, st));
+    if (pmal) AZ_CUDA_CHECK(cudaFreeAsync(pmal, st));
   }
   AZ_CUDA_CHECK(cudaMemsetAsync(d_rank, 0, sizeof(int64_t), st));
   k_bjac_sigma<<<az_div_up(r, 256), 256, 0, st>>>(nrm2, smax2, r, theta, sigma_out, d_rank);
