@@ -449,14 +449,17 @@ __global__ void k_bjac_permute_rows(const double* Cs, double* Cd, const int* per
 // (de Rijk-style ordering at sweep level, a dynamic stand-in for Drmac & Veselic's column pivoting):
 // one outer sweep fewer on c3 / c4 (10 -> 9, 9 -> 8), c5 rounds 14.6 -> 13.2 s.  AZ_BJAC_SORT=0
 // keeps the fixed column order.
-static bool bjac_sort() {
+// (experiment modes: 2 = increasing norm, 3 = decreasing norm dealt round-robin over the blocks)
+static int bjac_sort_mode() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("AZ_BJAC_SORT");
-    v = (e && *e == '0') ? 0 : 1;
+    v = e ? atoi(e) : 1;
+    if (v < 0 || v > 3) v = 1;
   }
-  return v == 1;
+  return v;
 }
+static bool bjac_sort() { return bjac_sort_mode() != 0; }
 
 static int g_last_sweeps = 0;
 // inner cyclic sweeps of the pair's 64 x 64 Gram eigensolver per round (AZ_BJAC_INNER, default 1)
@@ -671,7 +674,23 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
       AZ_CUDA_CHECK(cudaMemcpyAsync(h_n2.data(), nrm2, sizeof(double) * r, cudaMemcpyDeviceToHost, st));
       AZ_CUDA_CHECK(cudaStreamSynchronize(st));
       for (int64_t i = 0; i < r; ++i) h_perm[i] = (int)i;
-      std::stable_sort(h_perm.begin(), h_perm.end(), [&](int x, int y) { return h_n2[x] > h_n2[y]; });
+      const int mode = bjac_sort_mode();
+      if (mode == 2)
+        std::stable_sort(h_perm.begin(), h_perm.end(), [&](int x, int y) { return h_n2[x] < h_n2[y]; });
+      else
+        std::stable_sort(h_perm.begin(), h_perm.end(), [&](int x, int y) { return h_n2[x] > h_n2[y]; });
+      if (mode == 3) {   // sorted column t -> block t % nblk, slot t / nblk
+        std::vector<int> dealt(r, -1);
+        int64_t t = 0;
+        for (int64_t slot = 0; slot < BW; ++slot)
+          for (int64_t blk = 0; blk < nblk; ++blk) {
+            const int64_t pos = blk * BW + slot;
+            if (pos < r && t < r) dealt[pos] = h_perm[t++];
+          }
+        for (int64_t i = 0; i < r; ++i)
+          if (dealt[i] < 0) dealt[i] = h_perm[t++];
+        h_perm.swap(dealt);
+      }
       AZ_CUDA_CHECK(cudaMemcpyAsync(d_perm, h_perm.data(), sizeof(int) * r, cudaMemcpyHostToDevice, st));
       k_bjac_permute<<<(unsigned)r, 256, 0, st>>>(B, Bsp, d_perm, r);
       AZ_LAUNCH_CHECK();
