@@ -461,6 +461,45 @@ static int bjac_sort_mode() {
 }
 static bool bjac_sort() { return bjac_sort_mode() != 0; }
 
+// AZ_BJAC_QRCP=1: the first preconditioning QR with panel-level column pivoting (before each 64-column
+// panel the 64 trailing columns of largest remaining norm are moved into it, in decreasing norm):
+// R_S^T P = Q2 R2, so pinv(R_S) c = Q2 pinv(R3) Q3^T (P^T c)  (Drmac & Veselic's pivoted
+// preconditioner, with the pivot search per panel instead of per column)
+static bool bjac_qrcp() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AZ_BJAC_QRCP");
+    v = (e && *e == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// nrm[c - j0] = || A[j0:r, c] ||^2 for the trailing columns c in [j0, r)  (A: r x r, ld r)
+__global__ void __launch_bounds__(256) k_tail_norms(const double* A, int64_t r, int64_t j0, double* nrm) {
+  const int64_t col = j0 + blockIdx.x;
+  double s = 0.0;
+  for (int64_t t = j0 + threadIdx.x; t < r; t += 256) s = fma(A[col * r + t], A[col * r + t], s);
+  __shared__ double red[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < 8; ++i) t += red[i];
+    nrm[blockIdx.x] = t;
+  }
+}
+
+// column moves: scratch[:, i] = A[:, from[i]] (phase 0); A[:, to[i]] = scratch[:, i] (phase 1)
+__global__ void k_move_cols(double* A, double* scratch, const int* from, const int* to, int64_t r, int phase) {
+  const int i = blockIdx.x;
+  if (phase == 0)
+    for (int64_t t = threadIdx.x; t < r; t += blockDim.x) scratch[(int64_t)i * r + t] = A[(int64_t)from[i] * r + t];
+  else
+    for (int64_t t = threadIdx.x; t < r; t += blockDim.x) A[(int64_t)to[i] * r + t] = scratch[(int64_t)i * r + t];
+}
+
 static int g_last_sweeps = 0;
 // inner cyclic sweeps of the pair's 64 x 64 Gram eigensolver per round (AZ_BJAC_INNER, default 1)
 static int inner_sweeps() {
@@ -551,6 +590,7 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
   std::vector<int64_t> pj2, pj3;
   std::vector<int> pn2, pn3;
   int64_t np2 = 0, np3 = 0;
+  std::vector<int> perm;   // AZ_BJAC_QRCP: column j of R_S^T P is column perm[j] of R_S^T
   if (bjac_precond()) {   // the workspace holds these buffers whenever preconditioning is enabled
     const int64_t QBw = az_qrw_panel_width();
     const int64_t npm = (r + QBw - 1) / QBw;
@@ -576,13 +616,82 @@ az_status_t az_tsvdw_impl(const double* Rf, int64_t ldr, int64_t r, int64_t nrhs
     AzTrace tr("bjac_precond", st, 2 * r * r * r);
     k_upper_T<<<az_div_up(r * r, 256), 256, 0, st>>>(Rf, ldr, r, M2);                 // R_S^T
     AZ_LAUNCH_CHECK();
-    AZ_TRY(az_qrw_factor(M2, r, r, 0, r, T2, pj2.data(), pn2.data(), &np2, qws, qbytes, st));   // = Q2 R2
+    if (!bjac_qrcp()) {
+      AZ_TRY(az_qrw_factor(M2, r, r, 0, r, T2, pj2.data(), pn2.data(), &np2, qws, qbytes, st));   // = Q2 R2
+    } else {
+      // R_S^T P = Q2 R2 panel by panel; B (not loaded yet) is the column-move scratch, Z holds the
+      // trailing norms and T3 (not used yet) the move lists
+      const int64_t QBw = az_qrw_panel_width();
+      perm.resize(r);
+      for (int64_t i = 0; i < r; ++i) perm[i] = (int)i;
+      std::vector<double> hn(r);
+      std::vector<int> idx, from, to;
+      int* d_mv = (int*)T3;
+      double* d_nrm = Z;
+      for (int64_t j0 = 0; j0 < r; j0 += QBw) {
+        const int64_t nbp = std::min<int64_t>(QBw, r - j0), nt = r - j0;
+        k_tail_norms<<<(unsigned)nt, 256, 0, st>>>(M2, r, j0, d_nrm);
+        AZ_LAUNCH_CHECK();
+        AZ_CUDA_CHECK(cudaMemcpyAsync(hn.data(), d_nrm, sizeof(double) * nt, cudaMemcpyDeviceToHost, st));
+        AZ_CUDA_CHECK(cudaStreamSynchronize(st));
+        idx.resize(nt);
+        for (int64_t i = 0; i < nt; ++i) idx[i] = (int)i;
+        std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return hn[x] > hn[y]; });
+        // position j0 + i takes the i-th largest column; the panel columns not chosen fill the
+        // vacated positions of the chosen ones from outside the panel
+        std::vector<int> dest(nt, -1);   // dest[old offset] = new offset (affected columns only)
+        std::vector<char> chosen(nt, 0);
+        for (int64_t i = 0; i < nbp; ++i) chosen[idx[i]] = 1;
+        std::vector<int> vac;            // offsets >= nbp vacated by chosen columns
+        for (int64_t i = 0; i < nbp; ++i) {
+          dest[idx[i]] = (int)i;
+          if (idx[i] >= nbp) vac.push_back(idx[i]);
+        }
+        std::sort(vac.begin(), vac.end());
+        size_t v = 0;
+        for (int64_t i = 0; i < nbp; ++i)
+          if (!chosen[i]) dest[i] = vac[v++];
+        from.clear();
+        to.clear();
+        for (int64_t i = 0; i < nt; ++i)
+          if (dest[i] >= 0 && dest[i] != i) {
+            from.push_back((int)(j0 + i));
+            to.push_back((int)(j0 + dest[i]));
+          }
+        if (!from.empty()) {
+          const int nm = (int)from.size();
+          std::vector<int> hv(from);
+          hv.insert(hv.end(), to.begin(), to.end());
+          AZ_CUDA_CHECK(cudaMemcpyAsync(d_mv, hv.data(), sizeof(int) * 2 * nm, cudaMemcpyHostToDevice, st));
+          k_move_cols<<<nm, 256, 0, st>>>(M2, B, d_mv, d_mv + nm, r, 0);
+          AZ_LAUNCH_CHECK();
+          k_move_cols<<<nm, 256, 0, st>>>(M2, B, d_mv, d_mv + nm, r, 1);
+          AZ_LAUNCH_CHECK();
+          std::vector<int> old(perm.begin() + j0, perm.end());
+          for (int i = 0; i < nm; ++i) perm[to[i]] = old[from[i] - j0];
+          AZ_CUDA_CHECK(cudaStreamSynchronize(st));   // hv is reused next panel
+        }
+        AZ_TRY(az_qrw_factor(M2, r, r, j0, j0 + nbp, T2, pj2.data(), pn2.data(), &np2, qws, qbytes, st));
+        if (j0 + nbp < r)
+          AZ_TRY(az_qrw_apply(M2, r, r, pj2.data(), pn2.data(), T2, np2 - 1, np2, M2 + (j0 + nbp) * r, r,
+                              r - j0 - nbp, qws, qbytes, st));
+      }
+    }
     k_upper_T<<<az_div_up(r * r, 256), 256, 0, st>>>(M2, r, r, M3);                    // R2^T
     AZ_LAUNCH_CHECK();
     AZ_TRY(az_qrw_factor(M3, r, r, 0, r, T3, pj3.data(), pn3.data(), &np3, qws, qbytes, st));   // = Q3 R3
     if (nrhs > 0) {
       k_copy_block<<<az_div_up(r * nrhs, 256), 256, 0, st>>>(Rf + r * ldr, ldr, C, r, r, nrhs);
       AZ_LAUNCH_CHECK();
+      if (!perm.empty()) {   // P^T c: row j of the permuted c is row perm[j] of c (nrm2 is free here)
+        int* d_permc = (int*)nrm2;
+        AZ_CUDA_CHECK(cudaMemcpyAsync(d_permc, perm.data(), sizeof(int) * r, cudaMemcpyHostToDevice, st));
+        k_bjac_permute_rows<<<az_div_up(r * nrhs, 256), 256, 0, st>>>(C, Z, d_permc, r, nrhs);
+        AZ_LAUNCH_CHECK();
+        k_copy_block<<<az_div_up(r * nrhs, 256), 256, 0, st>>>(Z, r, C, r, r, nrhs);
+        AZ_LAUNCH_CHECK();
+        AZ_CUDA_CHECK(cudaStreamSynchronize(st));   // perm (host) outlives the copy
+      }
       AZ_TRY(az_qrw_apply(M3, r, r, pj3.data(), pn3.data(), T3, 0, np3, C, r, nrhs, qws, qbytes, st));   // Q3^T c
     }
   }
