@@ -175,77 +175,108 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
     __syncthreads();
     if (any_rot) {
       // ---------------- eigen-decomposition of G by cyclic Jacobi ----------------
-      // 8 threads per rotation pair (32 disjoint pairs per round): each thread recomputes the
-      // pair's (c, s) itself (no broadcast), then rotates 8 of the 64 entries of rows p, q
-      // (phase A) and of columns p, q of G and V (phase B): two barriers per round.
-      for (int e = tid; e < PW * PW; e += 256) V[(e / PW) * VS + (e % PW)] = (e / PW == e % PW) ? 1.0 : 0.0;
+      // A half warp per rotation pair, each thread two pairs (pk0 and pk0 + 16; 32 disjoint pairs per
+      // round): each thread recomputes its pairs' (c, s) itself (no broadcast), then rotates 4 of the
+      // 64 entries of rows p, q (phase A) and of columns p, q of G and V (phase B): two barriers per
+      // round.  Entry t = sub + 16 i: a half warp's 16 accesses fall in 16 distinct bank pairs for
+      // rows (stride 1) and columns (stride GS = 65); V is rotated in the free staging buffer X at the
+      // same stride and copied to its DMMA layout (stride VS) at the end -- the rounds are bound by
+      // shared-memory wavefronts, which the former 8-threads-per-pair layout (two pairs per half warp)
+      // and V's stride 68 multiplied by bank conflicts.  Same operations per entry, same results.
+      double* Ve = X;   // PW x GS
+      for (int e = tid; e < PW * PW; e += 256) Ve[(e / PW) * GS + (e % PW)] = (e / PW == e % PW) ? 1.0 : 0.0;
       __shared__ int rot_any;
-      const int pk = tid >> 3, sub = tid & 7;
+      const int pk0 = tid >> 4, sub = tid & 15;
+      constexpr int NE = PW / 16;
       const double tol2 = a.tol * a.tol;
       for (int sw = 0; sw < a.inner_sweeps; ++sw) {
         if (tid == 0) rot_any = 0;
         __syncthreads();
         for (int rd = 0; rd < PW - 1; ++rd) {
-          int p, q;
-          pair_of(rd, pk, PW, p, q);
-          const double gp = G[p * GS + p], gq = G[q * GS + q], g = G[p * GS + q];
-          double c = 1.0, sn = 0.0;
-          const double g2 = g * g;
-          const bool rot_pq = g != 0.0 && g2 > tol2 * gp * gq && fmin(gp, gq) >= negl;
-          if (rot_pq) {
-            // t = tan = 2 g sign(d) / (|d| + sqrt(d^2 + 4 g^2)), d = G_qq - G_pp
-            // (MUFU-seeded reciprocal / rsqrt with Newton steps, as in az_svd.cu: the IEEE division and
-            // square root dominated this latency-bound chain -- one inner sweep cost ~0.2 ms per round)
-            const double d = gq - gp;
-            const double h = fma(d, d, 4.0 * g2);
-            const double t = (d >= 0.0 ? 2.0 * g : -2.0 * g) * fast_rcp(fabs(d) + h * fast_rsqrt(h));
-            c = fast_rsqrt(fma(t, t, 1.0));
-            sn = c * t;
-            if (sub == 0) rot_any = 1;
+          int pp[2], qq[2];
+          double cc[2], ss[2];
+          bool rr[2];
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            int p, q;
+            pair_of(rd, pk0 + 16 * h2, PW, p, q);
+            pp[h2] = p;
+            qq[h2] = q;
+            const double gp = G[p * GS + p], gq = G[q * GS + q], g = G[p * GS + q];
+            double c = 1.0, sn = 0.0;
+            const double g2 = g * g;
+            const bool rot_pq = g != 0.0 && g2 > tol2 * gp * gq && fmin(gp, gq) >= negl;
+            if (rot_pq) {
+              // t = tan = 2 g sign(d) / (|d| + sqrt(d^2 + 4 g^2)), d = G_qq - G_pp
+              // (MUFU-seeded reciprocal / rsqrt with Newton steps, as in az_svd.cu: the IEEE division and
+              // square root dominated this latency-bound chain -- one inner sweep cost ~0.2 ms per round)
+              const double d = gq - gp;
+              const double h = fma(d, d, 4.0 * g2);
+              const double t = (d >= 0.0 ? 2.0 * g : -2.0 * g) * fast_rcp(fabs(d) + h * fast_rsqrt(h));
+              c = fast_rsqrt(fma(t, t, 1.0));
+              sn = c * t;
+              if (sub == 0) rot_any = 1;
+            }
+            cc[h2] = c;
+            ss[h2] = sn;
+            rr[h2] = rot_pq;
           }
           if (dbg && rd == 5 && sw == 0) a.dbg[6] = clock64();
           __syncthreads();   // every pair has read its 2 x 2 block before any row is rotated
           if (dbg && rd == 5 && sw == 0) a.dbg[7] = clock64();
           // all loads of a phase are issued before its first store (no load waits on a store)
-          if (rot_pq) {
-            double xp[PW / 8], xq[PW / 8];
+          {
+            double xp[2][NE], xq[2][NE];
 #pragma unroll
-            for (int i = 0; i < PW / 8; ++i) {
-              const int t = sub + 8 * i;     // interleaved: 8 consecutive banks per pair
-              xp[i] = G[p * GS + t];
-              xq[i] = G[q * GS + t];
-            }
+            for (int h2 = 0; h2 < 2; ++h2)
+              if (rr[h2])
 #pragma unroll
-            for (int i = 0; i < PW / 8; ++i) {
-              const int t = sub + 8 * i;
-              G[p * GS + t] = c * xp[i] - sn * xq[i];
-              G[q * GS + t] = sn * xp[i] + c * xq[i];
-            }
+                for (int i = 0; i < NE; ++i) {
+                  const int t = sub + 16 * i;
+                  xp[h2][i] = G[pp[h2] * GS + t];
+                  xq[h2][i] = G[qq[h2] * GS + t];
+                }
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2)
+              if (rr[h2])
+#pragma unroll
+                for (int i = 0; i < NE; ++i) {
+                  const int t = sub + 16 * i;
+                  G[pp[h2] * GS + t] = cc[h2] * xp[h2][i] - ss[h2] * xq[h2][i];
+                  G[qq[h2] * GS + t] = ss[h2] * xp[h2][i] + cc[h2] * xq[h2][i];
+                }
           }
           __syncthreads();
-          if (rot_pq) {
-            double xp[PW / 8], xq[PW / 8], vp[PW / 8], vq[PW / 8];
+          {
+            double xp[2][NE], xq[2][NE], vp[2][NE], vq[2][NE];
 #pragma unroll
-            for (int i = 0; i < PW / 8; ++i) {
-              const int t = sub + 8 * i;
-              xp[i] = G[t * GS + p];
-              xq[i] = G[t * GS + q];
-              vp[i] = V[t * VS + p];
-              vq[i] = V[t * VS + q];
-            }
+            for (int h2 = 0; h2 < 2; ++h2)
+              if (rr[h2])
 #pragma unroll
-            for (int i = 0; i < PW / 8; ++i) {
-              const int t = sub + 8 * i;
-              G[t * GS + p] = c * xp[i] - sn * xq[i];
-              G[t * GS + q] = sn * xp[i] + c * xq[i];
-              V[t * VS + p] = c * vp[i] - sn * vq[i];
-              V[t * VS + q] = sn * vp[i] + c * vq[i];
-            }
+                for (int i = 0; i < NE; ++i) {
+                  const int t = sub + 16 * i;
+                  xp[h2][i] = G[t * GS + pp[h2]];
+                  xq[h2][i] = G[t * GS + qq[h2]];
+                  vp[h2][i] = Ve[t * GS + pp[h2]];
+                  vq[h2][i] = Ve[t * GS + qq[h2]];
+                }
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2)
+              if (rr[h2])
+#pragma unroll
+                for (int i = 0; i < NE; ++i) {
+                  const int t = sub + 16 * i;
+                  G[t * GS + pp[h2]] = cc[h2] * xp[h2][i] - ss[h2] * xq[h2][i];
+                  G[t * GS + qq[h2]] = ss[h2] * xp[h2][i] + cc[h2] * xq[h2][i];
+                  Ve[t * GS + pp[h2]] = cc[h2] * vp[h2][i] - ss[h2] * vq[h2][i];
+                  Ve[t * GS + qq[h2]] = ss[h2] * vp[h2][i] + cc[h2] * vq[h2][i];
+                }
           }
           __syncthreads();
         }
         if (!rot_any) break;
       }
+      for (int e = tid; e < PW * PW; e += 256) V[(e / PW) * VS + (e % PW)] = Ve[(e / PW) * GS + (e % PW)];
     }
   }
   if (dbg) a.dbg[3] = clock64();
