@@ -94,7 +94,12 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
   if (dbg) a.dbg[0] = clock64();
   // ---------------- partial Gram G = X^T X over rows [rb, re) ----------------
   {
-    const int wm = w & 1, wn = (w >> 1) & 1, wk = w >> 2;
+    // G is symmetric: only the blocks II, IJ and JJ are formed (JI is mirrored by the leader after the
+    // cluster reduction).  Warps 0-3 take II / IJ over one k half of the staged tile each, warps 4-7
+    // take JJ over one k quarter each: 3 of the 4 block products, the same DMMA count on each SM
+    // sub-partition (warps s and s + 4).
+    const int blk = (w < 4) ? (w & 1) : 2;            // 0: II, 1: IJ, 2: JJ
+    const int gm0 = (blk == 2) ? BW : 0, gn0 = (blk == 0) ? 0 : BW;
     double acc[4][4][2];
     acc_zero(acc);
     const int lk = tid & 31, li = tid >> 5;
@@ -114,26 +119,29 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
       for (int t = 0; t < 8; ++t) X[(li + 8 * t) * GKS + lk] = v[t];
       __syncthreads();
       if (k0 + GK < re) load(k0 + GK);     // next tile in flight during the MMAs
-      warp_mma<4, 4, IMAJ, IMAJ>(acc, X, GKS, X, GKS, wm * 32, wn * 32, wk * 16, 16, lane);
+      if (w < 4)
+        warp_mma<4, 4, IMAJ, IMAJ>(acc, X, GKS, X, GKS, gm0, gn0, (w >> 1) * 16, 16, lane);
+      else
+        warp_mma<4, 4, IMAJ, IMAJ>(acc, X, GKS, X, GKS, gm0, gn0, (w - 4) * 8, 8, lane);
     }
-    // reduce k halves into G
-    if (wk == 1)
+    // fixed-order sums of the k parts into G: step 0 warps 0, 1, 4 store; step 1 warps 2, 3, 5 add;
+    // step 2 warp 6; step 3 warp 7
+    const int step = (w < 4) ? (w >> 1) : (w - 4);
+#pragma unroll 1
+    for (int sidx = 0; sidx < 4; ++sidx) {
+      if (step == sidx) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+          for (int j = 0; j < 4; ++j)
 #pragma unroll
-          for (int e = 0; e < 2; ++e)
-            G[acc_row(wm * 32, i, lane) * GS + acc_col(wn * 32, j, e, lane)] = acc[i][j][e];
-    __syncthreads();
-    if (wk == 0)
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e)
-            G[acc_row(wm * 32, i, lane) * GS + acc_col(wn * 32, j, e, lane)] += acc[i][j][e];
+            for (int e = 0; e < 2; ++e) {
+              double* g = &G[acc_row(gm0, i, lane) * GS + acc_col(gn0, j, e, lane)];
+              *g = sidx == 0 ? acc[i][j][e] : *g + acc[i][j][e];
+            }
+      }
+      if (sidx < 3) __syncthreads();
+    }
   }
   if (dbg) a.dbg[1] = clock64();
   cluster.sync();                     // partial Grams complete
@@ -157,6 +165,12 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
     }
   }
   if (crank == 0) {
+    // the block JI of the symmetric G (not formed above)
+    for (int e = tid; e < BW * BW; e += 256) {
+      const int p = e / BW, q = BW + e % BW;
+      G[q * GS + p] = G[p * GS + q];
+    }
+    __syncthreads();
     // ---------------- convergence measure ----------------
     double mx = 0.0;
     for (int e = tid; e < PW * PW; e += 256) {
