@@ -113,16 +113,21 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
       for (int t = 0; t < 8; ++t) v[t] = (k < re && colp[t] >= 0) ? a.B[colp[t] * r + k] : 0.0;
     };
     load(rb);
-    for (int64_t k0 = rb; k0 < re; k0 += GK) {
-      __syncthreads();
+    // two staging buffers in X and the C tile buffer behind it (free until the c rows at the end), one
+    // barrier per tile: a warp stores tile t + 2 into the buffer of tile t only after the barrier of
+    // tile t + 1, which every warp reaches after its MMAs of tile t
+    static_assert(2 * GKS <= 2 * XS, "Gram double buffer must fit X + Cs");
+    int par = 0;
+    for (int64_t k0 = rb; k0 < re; k0 += GK, par ^= 1) {
+      double* Xt = X + par * (PW * GKS);
 #pragma unroll
-      for (int t = 0; t < 8; ++t) X[(li + 8 * t) * GKS + lk] = v[t];
+      for (int t = 0; t < 8; ++t) Xt[(li + 8 * t) * GKS + lk] = v[t];
       __syncthreads();
       if (k0 + GK < re) load(k0 + GK);     // next tile in flight during the MMAs
       if (w < 4)
-        warp_mma<4, 4, IMAJ, IMAJ>(acc, X, GKS, X, GKS, gm0, gn0, (w >> 1) * 16, 16, lane);
+        warp_mma<4, 4, IMAJ, IMAJ>(acc, Xt, GKS, Xt, GKS, gm0, gn0, (w >> 1) * 16, 16, lane);
       else
-        warp_mma<4, 4, IMAJ, IMAJ>(acc, X, GKS, X, GKS, gm0, gn0, (w - 4) * 8, 8, lane);
+        warp_mma<4, 4, IMAJ, IMAJ>(acc, Xt, GKS, Xt, GKS, gm0, gn0, (w - 4) * 8, 8, lane);
     }
     // fixed-order sums of the k parts into G: step 0 warps 0, 1, 4 store; step 1 warps 2, 3, 5 add;
     // step 2 warp 6; step 3 warp 7
@@ -317,15 +322,19 @@ __global__ void __launch_bounds__(256, 1) k_bjac_round(BJArgs a, int round) {
       for (int t = 0; t < 16; ++t) v[t] = (colp[t] >= 0 && row < re) ? a.B[colp[t] * r + row] : 0.0;
     };
     load(rb);
-    for (int64_t r0 = rb; r0 < re; r0 += 64) {
-      __syncthreads();
+    // two staging buffers (X and the C tile buffer behind it, free until the c rows below), one
+    // barrier per tile (as in the Gram phase)
+    int par = 0;
+    __syncthreads();
+    for (int64_t r0 = rb; r0 < re; r0 += 64, par ^= 1) {
+      double* Xt = X + par * (PW * XS);
 #pragma unroll
-      for (int t = 0; t < 16; ++t) X[(lc + 4 * t) * XS + lr] = v[t];
+      for (int t = 0; t < 16; ++t) Xt[(lc + 4 * t) * XS + lr] = v[t];
       __syncthreads();
       if (r0 + 64 < re) load(r0 + 64);
       double acc[4][2][2];
       acc_zero(acc);
-      warp_mma<4, 2, KMAJ, KMAJ>(acc, X, XS, V, VS, wm * 32, wn * 16, 0, PW, lane);
+      warp_mma<4, 2, KMAJ, KMAJ>(acc, Xt, XS, V, VS, wm * 32, wn * 16, 0, PW, lane);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
