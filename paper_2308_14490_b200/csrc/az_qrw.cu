@@ -187,11 +187,20 @@ __global__ void __launch_bounds__(256) k_qr_vtc(UpdArgs a) {
   double va[8], vb[8];
   auto load = [&](int64_t rr) {
     const int64_t r = rr + lk;
+    if (rr >= a.j0 + QB) {   // (uniform) below the panel's unit triangle: V is the stored column
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int i = li + 8 * t;
-      va[t] = r < r1 ? v_elem(a.V, a.ldv, a.j0, a.nb, r, i) : 0.0;
-      vb[t] = (r < r1 && n0 + i < a.nt) ? a.C[(n0 + i) * a.ldc + r] : 0.0;
+      for (int t = 0; t < 8; ++t) {
+        const int i = li + 8 * t;
+        va[t] = (r < r1 && i < a.nb) ? a.V[(a.j0 + i) * a.ldv + r] : 0.0;
+        vb[t] = (r < r1 && n0 + i < a.nt) ? a.C[(n0 + i) * a.ldc + r] : 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int i = li + 8 * t;
+        va[t] = r < r1 ? v_elem(a.V, a.ldv, a.j0, a.nb, r, i) : 0.0;
+        vb[t] = (r < r1 && n0 + i < a.nt) ? a.C[(n0 + i) * a.ldc + r] : 0.0;
+      }
     }
   };
   load(r0);
