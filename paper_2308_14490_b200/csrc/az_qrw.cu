@@ -244,10 +244,11 @@ __global__ void __launch_bounds__(256) k_qr_vtc(UpdArgs a) {
 
 // Wfin[:, n] = T^T sum_kc Wpart[kc][:, n]   (ordered sum; 4 target columns per CTA, 64 threads each)
 __global__ void __launch_bounds__(256) k_qr_wred(UpdArgs a, int KC) {
-  __shared__ double Ts[QB * QB];
+  constexpr int TS = QB + 1;   // padded: rows (T^T path) and columns (T path) both conflict-free
+  __shared__ double Ts[QB * TS];
   __shared__ double ws[4][QB];
   const int tid = threadIdx.x, l = tid & 63, g = tid >> 6;
-  for (int e = tid; e < QB * QB; e += 256) Ts[e] = a.T[e];
+  for (int e = tid; e < QB * QB; e += 256) Ts[(e / QB) * TS + (e % QB)] = a.T[e];
   const int64_t n = (int64_t)blockIdx.x * 4 + g;
   double s = 0.0;
   if (n < a.nt)
@@ -257,9 +258,9 @@ __global__ void __launch_bounds__(256) k_qr_wred(UpdArgs a, int KC) {
   if (n < a.nt) {
     double t = 0.0;
     if (!a.applyQ)
-      for (int i = 0; i <= l; ++i) t = fma(Ts[l * QB + i], ws[g][i], t);    // (T^T)[l][i] = T[i][l]
+      for (int i = 0; i <= l; ++i) t = fma(Ts[l * TS + i], ws[g][i], t);    // (T^T)[l][i] = T[i][l]
     else
-      for (int i = l; i < QB; ++i) t = fma(Ts[i * QB + l], ws[g][i], t);    // T[l][i], i >= l
+      for (int i = l; i < QB; ++i) t = fma(Ts[i * TS + l], ws[g][i], t);    // T[l][i], i >= l
     a.Wfin[n * QB + l] = t;
   }
 }
